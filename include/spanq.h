@@ -1,0 +1,193 @@
+/* spanq.h — C ABI of the B200-native span-query prefill path (arXiv 2511.02749).
+ *
+ * The calls follow the paper's statement of the problem:
+ *   plan a span-query expression tree      — Def. "Span Query" PAPER.md §4.1,
+ *                                            joins ⊕ / ⋈ Def. P:333-335;
+ *   look up and insert fragment KV         — block hashing with suspended accumulation
+ *                                            §5.4, prefix scan §2;
+ *   run fragment prefill                   — fragments "prepared" independently of context,
+ *                                            §5.1 footnote; span-sparse attention;
+ *   run join prefill                       — the final ⋈ over cached, repositioned blocks
+ *                                            ("ReRoPE", §5.5) + the cross tokens.
+ *
+ * Conventions
+ *  - extern "C", plain pointers and sizes. "device" pointers live on ctx's CUDA device;
+ *    "host" pointers in host memory. Streams are `cudaStream_t` passed as `void*` (NULL = the
+ *    legacy default stream).
+ *  - Every call returns spq_status; no exception crosses the ABI. On failure the message is
+ *    available from spq_last_error() (thread-local, valid until the next failing call on
+ *    the same thread).
+ *  - Layouts are row-major. Activations: q [rows, Hq, d], k/v [rows, Hkv, d], o [rows, Hq, d]
+ *    in the ctx dtype (bf16 = IEEE bfloat16 bit patterns, or fp32), lse [rows, Hq] fp32 natural
+ *    log. KV pools: [num_layers][num_blocks][Hkv][block_size][d] in the ctx dtype; slot
+ *    s = block_id * block_size + offset addresses one token row of one block.
+ *  - A ctx is single-writer (not thread-safe); plans execute in stream order.
+ */
+#ifndef SPANQ_H_
+#define SPANQ_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SPQ_OK = 0,
+  SPQ_EINVAL = 1, /* bad argument, tree shape, op code, arity, empty leaf, negative token   */
+  SPQ_ENOMEM = 2, /* the block pool cannot hold the plan's blocks; the plan is rolled back  */
+  SPQ_ECUDA = 3,  /* CUDA launch/runtime failure, or no usable sm_100 device               */
+  SPQ_ENCCL = 4,  /* reserved for the multi-GPU exchange                                    */
+  SPQ_ESTATE = 5  /* plan used after release, job/query range out of bounds, wrong mode     */
+} spq_status;
+
+typedef enum { SPQ_BF16 = 0, SPQ_FP32 = 1 } spq_dtype;
+
+typedef struct {
+  int32_t num_q_heads;  /* Hq  (multiple of Hkv; GQA q-head h uses kv-head h / (Hq/Hkv))    */
+  int32_t num_kv_heads; /* Hkv                                                               */
+  int32_t head_dim;     /* d: 64 or 128 for SPQ_BF16; any multiple of 32 <= 256 for SPQ_FP32 */
+  int32_t num_layers;   /* L                                                                 */
+  int32_t block_size;   /* bs tokens per KV block: 16/32/64/128 on the GPU; any >=1
+                           for host-only contexts                                            */
+  int64_t num_blocks;   /* pool capacity in blocks on this device                            */
+  int32_t dtype;        /* spq_dtype                                                         */
+  double rope_base;     /* θ_i = rope_base^(-2i/d); rotate-half pairs (R15)     */
+  int32_t max_position; /* RoPE table length (positions 0..max_position-1)                   */
+  uint64_t model_salt;  /* folded into the root digest                                       */
+  void *k_pool;         /* device, CALLER-owned, [L][num_blocks][Hkv][bs][d]; must outlive ctx */
+  void *v_pool;         /* device, CALLER-owned, same layout                                 */
+  int32_t device;       /* CUDA device ordinal; -1 = host-only ctx (planner/store, no kernels) */
+  int32_t rank;         /* reserved (multi-GPU): this rank, 0..world_size-1                  */
+  int32_t world_size;   /* reserved (multi-GPU): must be 1 in this version                   */
+} spq_config;
+
+typedef struct spq_ctx spq_ctx;
+typedef struct spq_plan spq_plan;
+
+/* Create a context: validates cfg, builds the fp64->fp32 RoPE cos/sin table on the device
+ * and the TMA descriptors of both pools. Fails with SPQ_ECUDA if device >= 0 and the device
+ * is not sm_100. */
+spq_status spq_create(const spq_config *cfg, spq_ctx **out);
+void spq_destroy(spq_ctx *ctx); /* synchronizes ctx's device work; NULL is a no-op */
+const char *spq_last_error(void);
+const char *spq_version(void);
+
+/* ------------------------------------------------------------------ span-query trees */
+typedef enum { SPQ_TOKENS = 0, SPQ_PLUS = 1, SPQ_CROSS = 2 } spq_op; /* leaf, ⊕, ⋈ */
+typedef struct {
+  int32_t op;           /* spq_op                                                       */
+  int32_t num_children; /* children follow in pre-order                                 */
+  int64_t tok_begin;    /* TOKENS: first token index into spq_query.tokens              */
+  int64_t tok_len;      /* TOKENS: token count (>= 1)                                   */
+} spq_node;
+/* Accepted tree (v1): root ⋈ with children [TOKENS prefix]? [⊕ ...]? TOKENS cross, where a ⊕
+ * child is a TOKENS fragment, a nested ⊕ (flattened — "plus simplification") or a ⋈ of
+ * TOKENS leaves (concatenated into one fragment). This is the optimized RAG form
+ * G[⋈[S, ⊕[F…], U]] and the judge form ⋈[prefix, ⊕[c…], suffix]. */
+typedef struct {
+  const spq_node *nodes; /* host */
+  int32_t num_nodes;
+  const int32_t *tokens; /* host, token ids >= 0 */
+  int64_t num_tokens;
+} spq_query;
+
+/* ------------------------------------------------------------------ low level */
+/* Digests of one query, 16 bytes each, in the order: prefix blocks, each fragment's blocks (⊕
+ * order), the join fold J, cross blocks. BLAKE2b-128 chains. *n is
+ * set to the count; if cap is smaller, SPQ_EINVAL and nothing is written. */
+spq_status spq_block_hashes(const spq_ctx *ctx, const spq_query *q, uint8_t *digests /*host [cap][16]*/,
+                            int64_t cap, int64_t *n);
+/* Pure lookup: block id of each resident digest, -1 on miss. No stats/LRU side effects. */
+spq_status spq_lookup(const spq_ctx *ctx, const uint8_t *digests, int64_t n, int32_t *block_ids);
+/* Insert digests (ntok tokens each, 1..bs): resident digests return their id, others get the
+ * lowest free block id (evicting LRU unpinned blocks). Blocks are not pinned and their
+ * contents are not written. All-or-nothing: SPQ_ENOMEM rolls back. */
+spq_status spq_insert(spq_ctx *ctx, const uint8_t *digests, const int32_t *ntok, int64_t n,
+                      int32_t *block_ids);
+
+/* ------------------------------------------------------------------ plans */
+/* Plan a batch of queries: validate + flatten trees, assign positions (prefix 0..P-1,
+ * fragment f local 0..L_f-1 stored / global Δ_f = P + Σ_{g<f} L_g, cross P+S+j), hash,
+ * prefix-scan the prefix, all-or-nothing lookup per fragment, dedupe within the plan,
+ * allocate (lowest free id) + insert, evict LRU unpinned, pin everything referenced, build the
+ * kernels' work lists and upload them with one H2D copy on `stream`. Readings R8-R13 in
+ * DESIGN.md. On SPQ_ENOMEM/SPQ_EINVAL the store is unchanged. */
+spq_status spq_plan_create(spq_ctx *ctx, const spq_query *queries, int32_t n_queries, void *stream,
+                           spq_plan **out);
+
+typedef struct {
+  int32_t n_queries, n_segments, n_jobs;
+  int64_t n_blocks_total;
+  /* per segment (query order; within a query: prefix?, fragments in ⊕ order, cross) */
+  const int32_t *seg_query, *seg_kind /*0 prefix 1 fragment 2 cross*/, *seg_frag_idx, *seg_tok_len,
+      *seg_pos0 /*global position of first token*/, *seg_hit /*prefix: #hit blocks; fragment: 0/1*/,
+      *seg_compute_begin /*first recomputed row (tok_len = none)*/, *seg_block_off, *seg_n_blocks;
+  const int32_t *blocks;      /* [n_blocks_total] block ids, segment-major                   */
+  const uint8_t *block_write; /* [n_blocks_total] 1 = written by this plan                   */
+  const uint8_t *digests;     /* [n_blocks_total][16]                                        */
+  const uint8_t *join_digests;/* [n_queries][16]                                             */
+  const int32_t *jobs;        /* [n_jobs] segment index of each prefill job, plan order      */
+  const int64_t *job_row_off; /* [n_jobs+1] packed prefill row offsets                       */
+  int64_t n_prefill_rows;
+  const int32_t *prefill_pos; /* stored position of each packed prefill row                  */
+  const int64_t *prefill_slot;/* pool slot or -1 (resident block: read, not rewritten)       */
+  int64_t n_join_rows;
+  const int64_t *query_join_row_off; /* [n_queries+1]                                        */
+  const int32_t *join_pos;
+  const int64_t *join_slot;
+  int64_t n_pad_slots;
+  const int64_t *pad_slots;   /* slots zero-filled by the first prefill/join call of a plan  */
+  double prefill_flops;       /* algorithmic 4·d·Hq·(visible pairs) of all prefill jobs      */
+  double join_flops;          /* same for all joins                                          */
+  int64_t prefill_kv_bytes;   /* K/V bytes written by rope_kv_write for prefill rows         */
+  int64_t join_kv_bytes;
+} spq_plan_view;
+/* Read-only host arrays, valid until spq_plan_release. */
+spq_status spq_plan_view_get(const spq_plan *plan, spq_plan_view *out);
+
+/* Fragment / prefix prefill for jobs [job_begin, job_end): rope_kv_write of the jobs' rows
+ * with slot >= 0 (RoPE at the stored position, fused with the paged write), then block-diagonal
+ * causal attention (each job attends only within itself).
+ *  q, k, v: device, packed pre-RoPE rows of those jobs, rows [job_row_off[a], job_row_off[b]).
+ *  o: device [rows, Hq, d]; lse: device [rows, Hq] (may be NULL).  ctx must have device >= 0. */
+spq_status spq_prefill_jobs(spq_ctx *ctx, spq_plan *plan, int32_t layer, int32_t job_begin,
+                            int32_t job_end, const void *q, const void *k, const void *v, void *o,
+                            float *lse, void *stream);
+
+/* Join prefill for queries [q_begin, q_end): rope_kv_write of the cross rows, then the cross
+ * rows attend over [prefix | every fragment at its Δ_f | cross causal] from the pool (Q is
+ * counter-rotated by p - Δ_f per fragment: repositioning without touching cached KV), split
+ * over the KV range and merged by `combine`.
+ *  q/k/v: device, cross rows of those queries packed in query order
+ *  (rows [query_join_row_off[a], query_join_row_off[b])). o/lse as above.
+ * All prefill jobs of the plan that precede these queries must have been issued first on the
+ * same stream (their KV is read here). */
+spq_status spq_join(spq_ctx *ctx, spq_plan *plan, int32_t layer, int32_t q_begin, int32_t q_end,
+                    const void *q, const void *k, const void *v, void *o, float *lse, void *stream);
+
+/* Stream-ordered release: unpins the plan's blocks and frees its plan-private blocks; later
+ * kernel calls on any stream wait for `stream` to pass this point before touching them. */
+spq_status spq_plan_release(spq_ctx *ctx, spq_plan *plan, void *stream);
+
+/* ------------------------------------------------------------------ store admin / stats */
+typedef struct {
+  int64_t lookups, hit_blocks, miss_blocks, hit_tokens, input_tokens, evictions, inserted_blocks;
+  int64_t resident_blocks, free_blocks, pinned_blocks, plans;
+} spq_stats;
+spq_status spq_get_stats(const spq_ctx *ctx, spq_stats *out); /* hit rate = hit/input tokens */
+/* Drop every unpinned resident block (cold-cache reset). */
+spq_status spq_evict_all(spq_ctx *ctx);
+
+/* Instrumentation: kernel launches issued by this ctx so far, and the CUDA events bracketing
+ * the most recent attention launch (for roofline timing on the launching stream). */
+spq_status spq_launch_count(const spq_ctx *ctx, int64_t *n);
+spq_status spq_last_attn_ms(spq_ctx *ctx, float *prefill_ms, float *join_ms);
+/* Enable/disable recording of those events (off by default; recording adds 4 event records
+ * per call). */
+spq_status spq_set_timing(spq_ctx *ctx, int32_t enable);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPANQ_H_ */

@@ -104,6 +104,26 @@ class Store:
         """Low-level lookup (SPEC kv_cache.lookup S:301): block id or -1 per digest, no scan."""
         return [self.index.get(d, -1) for d in digests]
 
+    def insert(self, digests: Sequence[bytes], ntok: Sequence[int]) -> List[int]:
+        """Low-level insert (SPEC kv_cache.insert S:310): resident digests keep their block;
+        others get a new unpinned block (lowest free id, else LRU eviction). All-or-nothing."""
+        saved = copy.deepcopy((self.index, self.meta, self.free, self.stats))
+        out = []
+        try:
+            for dig, n in zip(digests, ntok):
+                if dig in self.index:
+                    out.append(self.index[dig])
+                    continue
+                b = self._alloc()
+                self.index[dig] = b
+                self.meta[b] = (dig, int(n), self.plan_no)
+                self.stats["inserted_blocks"] += 1
+                out.append(b)
+        except OracleENOMEM:
+            (self.index, self.meta, self.free, self.stats) = saved
+            raise
+        return out
+
     # -------------------------------------------------------------- planner
     def plan(self, queries: Sequence[Tuple[np.ndarray, List[np.ndarray], np.ndarray]]) -> PlanView:
         saved = copy.deepcopy((self.index, self.meta, self.free, self.pins, self.plan_no,
@@ -207,13 +227,16 @@ class Store:
                                         len(f), [False] * len(s)))
                 else:
                     self.stats["miss_blocks"] += len(s)
+                    # resident blocks are pinned before any allocation of this fragment, so
+                    # an eviction cannot reclaim a block the fragment is about to read
+                    for b in resident:
+                        if b >= 0:
+                            touch(b)
+                            pin(b)
                     blocks, write = [], []
                     for i, dig in enumerate(s):
                         if resident[i] >= 0:
-                            b = resident[i]
-                            touch(b)
-                            pin(b)
-                            blocks.append(b)
+                            blocks.append(resident[i])
                             write.append(False)
                         else:
                             blocks.append(insert_new(dig, min(bs, len(f) - i * bs)))

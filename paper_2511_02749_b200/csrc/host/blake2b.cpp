@@ -1,0 +1,104 @@
+// blake2b.cpp — RFC 7693 BLAKE2b written from the RFC's algorithm description (§2-§3):
+// 12 rounds of the G mixing function over a 16-word state, 128-byte blocks, 128-bit byte
+// counter, final-block flag, parameter block {digest length, key length 0, fanout 1, depth 1}.
+#include "blake2b.h"
+
+#include <cstring>
+
+namespace spq {
+namespace {
+
+constexpr uint64_t kIV[8] = {0x6a09e667f3bcc908ULL, 0xbb67ae8584caa73bULL, 0x3c6ef372fe94f82bULL,
+                             0xa54ff53a5f1d36f1ULL, 0x510e527fade682d1ULL, 0x9b05688c2b3e6c1fULL,
+                             0x1f83d9abfb41bd6bULL, 0x5be0cd19137e2179ULL};
+
+constexpr uint8_t kSigma[12][16] = {
+    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15},
+    {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3},
+    {11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4},
+    {7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8},
+    {9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13},
+    {2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9},
+    {12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11},
+    {13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10},
+    {6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5},
+    {10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0},
+    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15},
+    {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3}};
+
+inline uint64_t rotr(uint64_t x, int n) { return (x >> n) | (x << (64 - n)); }
+
+inline uint64_t load64(const uint8_t* p) {
+  uint64_t v;
+  std::memcpy(&v, p, 8);  // little-endian host (x86_64)
+  return v;
+}
+
+inline void mix(uint64_t* v, int a, int b, int c, int d, uint64_t x, uint64_t y) {
+  v[a] = v[a] + v[b] + x;
+  v[d] = rotr(v[d] ^ v[a], 32);
+  v[c] = v[c] + v[d];
+  v[b] = rotr(v[b] ^ v[c], 24);
+  v[a] = v[a] + v[b] + y;
+  v[d] = rotr(v[d] ^ v[a], 16);
+  v[c] = v[c] + v[d];
+  v[b] = rotr(v[b] ^ v[c], 63);
+}
+
+void compress(uint64_t* h, const uint8_t* block, uint64_t t_lo, uint64_t t_hi, bool last) {
+  uint64_t m[16], v[16];
+  for (int i = 0; i < 16; ++i) m[i] = load64(block + 8 * i);
+  for (int i = 0; i < 8; ++i) {
+    v[i] = h[i];
+    v[i + 8] = kIV[i];
+  }
+  v[12] ^= t_lo;
+  v[13] ^= t_hi;
+  if (last) v[14] = ~v[14];
+  for (int r = 0; r < 12; ++r) {
+    const uint8_t* s = kSigma[r];
+    mix(v, 0, 4, 8, 12, m[s[0]], m[s[1]]);
+    mix(v, 1, 5, 9, 13, m[s[2]], m[s[3]]);
+    mix(v, 2, 6, 10, 14, m[s[4]], m[s[5]]);
+    mix(v, 3, 7, 11, 15, m[s[6]], m[s[7]]);
+    mix(v, 0, 5, 10, 15, m[s[8]], m[s[9]]);
+    mix(v, 1, 6, 11, 12, m[s[10]], m[s[11]]);
+    mix(v, 2, 7, 8, 13, m[s[12]], m[s[13]]);
+    mix(v, 3, 4, 9, 14, m[s[14]], m[s[15]]);
+  }
+  for (int i = 0; i < 8; ++i) h[i] ^= v[i] ^ v[i + 8];
+}
+
+}  // namespace
+
+void blake2b(uint8_t* out, size_t outlen, const void* data, size_t len) {
+  uint64_t h[8];
+  for (int i = 0; i < 8; ++i) h[i] = kIV[i];
+  h[0] ^= 0x01010000ULL ^ static_cast<uint64_t>(outlen);  // fanout 1, depth 1, no key
+  const uint8_t* p = static_cast<const uint8_t*>(data);
+  uint64_t t = 0;
+  // all full blocks except the last one
+  while (len > 128) {
+    t += 128;
+    compress(h, p, t, 0, false);
+    p += 128;
+    len -= 128;
+  }
+  uint8_t last[128] = {0};
+  std::memcpy(last, p, len);
+  t += len;
+  compress(h, last, t, 0, true);
+  uint8_t full[64];
+  std::memcpy(full, h, 64);
+  std::memcpy(out, full, outlen);
+}
+
+bool Digest::operator==(const Digest& o) const { return std::memcmp(b, o.b, 16) == 0; }
+
+size_t DigestHash::operator()(const Digest& d) const {
+  size_t v;
+  std::memcpy(&v, d.b, sizeof(v));
+  return v;
+}
+
+}  // namespace spq

@@ -1,0 +1,514 @@
+// planner.cpp — see planner.h. Semantics are the contract of DESIGN.md (readings R1-R13,
+// hash contract); the CPU oracle (oracle/store.py) implements the same contract separately
+// and tests/test_planner_parity.py checks the two bit-for-bit.
+#include "planner.h"
+
+#include <algorithm>
+#include <cstring>
+
+#include "../../../include/spanq.h"
+
+namespace spq {
+
+// ------------------------------------------------------------------ tree normalization
+namespace {
+
+struct TreeParser {
+  const spq_query& q;
+  std::string* err;
+  bool fail(const char* m) {
+    *err = m;
+    return false;
+  }
+  // index after the subtree rooted at i, or -1
+  int64_t subtree_end(int64_t i) {
+    if (i >= q.num_nodes) return -1;
+    const spq_node& n = q.nodes[i];
+    if (n.op < 0 || n.op > 2 || n.num_children < 0) return -1;
+    int64_t j = i + 1;
+    for (int c = 0; c < n.num_children; ++c) {
+      j = subtree_end(j);
+      if (j < 0) return -1;
+    }
+    return j;
+  }
+  bool leaf(int64_t i, std::vector<int32_t>* out) {
+    const spq_node& n = q.nodes[i];
+    if (n.op != SPQ_TOKENS || n.num_children != 0) return fail("expected TOKENS leaf");
+    if (n.tok_len <= 0) return fail("empty token leaf");
+    if (n.tok_begin < 0 || n.tok_begin + n.tok_len > q.num_tokens) return fail("token range out of bounds");
+    for (int64_t t = 0; t < n.tok_len; ++t) {
+      const int32_t v = q.tokens[n.tok_begin + t];
+      if (v < 0) return fail("negative token id");
+      out->push_back(v);
+    }
+    return true;
+  }
+  // fragments under a PLUS node (nested PLUS flattened); *next = index after it
+  bool plus(int64_t i, std::vector<std::vector<int32_t>>* frags, int64_t* next) {
+    const spq_node& n = q.nodes[i];
+    if (n.op != SPQ_PLUS) return fail("expected PLUS");
+    if (n.num_children < 1) return fail("PLUS needs >= 1 child");
+    int64_t j = i + 1;
+    for (int c = 0; c < n.num_children; ++c) {
+      const spq_node& k = q.nodes[j];
+      if (k.op == SPQ_TOKENS) {
+        frags->emplace_back();
+        if (!leaf(j, &frags->back())) return false;
+        j += 1;
+      } else if (k.op == SPQ_PLUS) {
+        if (!plus(j, frags, &j)) return false;
+      } else {  // CROSS of TOKENS leaves = one fragment
+        if (k.num_children < 1) return fail("CROSS needs >= 1 child");
+        frags->emplace_back();
+        int64_t m = j + 1;
+        for (int cc = 0; cc < k.num_children; ++cc, ++m)
+          if (!leaf(m, &frags->back())) return false;
+        j = m;
+      }
+    }
+    *next = j;
+    return true;
+  }
+};
+
+}  // namespace
+
+bool normalize_tree(const spq_query& q, FlatQuery* out, std::string* err) {
+  TreeParser p{q, err};
+  if (q.num_nodes <= 0 || q.nodes == nullptr) return p.fail("empty tree");
+  if (q.num_tokens > 0 && q.tokens == nullptr) return p.fail("null tokens");
+  if (p.subtree_end(0) != q.num_nodes) return p.fail("malformed tree (op, arity or node count)");
+  const spq_node& root = q.nodes[0];
+  if (root.op != SPQ_CROSS || root.num_children < 1) return p.fail("root must be CROSS with >= 1 child");
+  std::vector<int64_t> kids;
+  int64_t j = 1;
+  for (int c = 0; c < root.num_children; ++c) {
+    kids.push_back(j);
+    j = p.subtree_end(j);
+  }
+  if (q.nodes[kids.back()].op != SPQ_TOKENS) return p.fail("last child must be the cross TOKENS leaf");
+  *out = FlatQuery();
+  if (!p.leaf(kids.back(), &out->cross)) return false;
+  kids.pop_back();
+  std::vector<int32_t> ops;
+  for (int64_t k : kids) ops.push_back(q.nodes[k].op);
+  int64_t dummy;
+  if (ops == std::vector<int32_t>{SPQ_TOKENS, SPQ_PLUS}) {
+    if (!p.leaf(kids[0], &out->prefix)) return false;
+    if (!p.plus(kids[1], &out->frags, &dummy)) return false;
+  } else if (ops == std::vector<int32_t>{SPQ_TOKENS}) {
+    if (!p.leaf(kids[0], &out->prefix)) return false;
+  } else if (ops == std::vector<int32_t>{SPQ_PLUS}) {
+    if (!p.plus(kids[0], &out->frags, &dummy)) return false;
+  } else if (!ops.empty()) {
+    return p.fail("unsupported tree shape");
+  }
+  return true;
+}
+
+// ------------------------------------------------------------------ digests
+namespace {
+inline void put_u32(std::vector<uint8_t>* b, uint32_t v) {
+  for (int i = 0; i < 4; ++i) b->push_back(static_cast<uint8_t>(v >> (8 * i)));
+}
+inline Digest b2(const std::vector<uint8_t>& buf) {
+  Digest d;
+  blake2b(d.b, 16, buf.data(), buf.size());
+  return d;
+}
+}  // namespace
+
+Digest root_digest(int hq, int hkv, int d, int bs, double rope_base, uint64_t salt) {
+  std::vector<uint8_t> buf = {'S', 'P', 'Q', 'v', '1'};
+  put_u32(&buf, hq);
+  put_u32(&buf, hkv);
+  put_u32(&buf, d);
+  put_u32(&buf, bs);
+  uint8_t f[8];
+  std::memcpy(f, &rope_base, 8);
+  buf.insert(buf.end(), f, f + 8);
+  for (int i = 0; i < 8; ++i) buf.push_back(static_cast<uint8_t>(salt >> (8 * i)));
+  return b2(buf);
+}
+
+void chain(char tag, const Digest& seed, const int32_t* tok, int64_t n, int bs,
+           std::vector<Digest>* out) {
+  Digest prev = seed;
+  std::vector<uint8_t> buf;
+  buf.reserve(1 + 16 + 4 + 4 * bs);
+  for (int64_t s = 0; s < n; s += bs) {
+    const int64_t m = std::min<int64_t>(bs, n - s);
+    buf.clear();
+    buf.push_back(static_cast<uint8_t>(tag));
+    buf.insert(buf.end(), prev.b, prev.b + 16);
+    put_u32(&buf, static_cast<uint32_t>(m));
+    for (int64_t t = 0; t < m; ++t) put_u32(&buf, static_cast<uint32_t>(tok[s + t]));
+    prev = b2(buf);
+    out->push_back(prev);
+  }
+}
+
+Digest join_fold(const Digest& h_last, const std::vector<Digest>& frag_lasts) {
+  std::vector<uint8_t> buf = {'J'};
+  buf.insert(buf.end(), h_last.b, h_last.b + 16);
+  put_u32(&buf, static_cast<uint32_t>(frag_lasts.size()));
+  for (const Digest& d : frag_lasts) buf.insert(buf.end(), d.b, d.b + 16);
+  return b2(buf);
+}
+
+// ------------------------------------------------------------------ store
+Store::Store(int64_t num_blocks, int block_size, const Digest& root)
+    : nblocks_(num_blocks), bs_(block_size), root_(root) {
+  meta_.resize(num_blocks);
+  for (auto& m : meta_) m = Meta{Digest{}, 0, 0, false};
+  pins_.assign(num_blocks, 0);
+  pinned_mark_.assign(num_blocks, 0);
+  for (int64_t b = 0; b < num_blocks; ++b) free_.insert(static_cast<int32_t>(b));
+}
+
+int64_t Store::pinned_count() const {
+  int64_t n = 0;
+  for (int32_t p : pins_) n += p > 0;
+  return n;
+}
+
+int32_t Store::lookup(const Digest& d) const {
+  auto it = index_.find(d);
+  return it == index_.end() ? -1 : it->second;
+}
+
+void Store::set_evictable(int32_t b, bool on) {
+  if (on)
+    evictable_.insert({meta_[b].last_use, b});
+  else
+    evictable_.erase({meta_[b].last_use, b});
+}
+
+int32_t Store::alloc(bool* ok) {
+  if (!free_.empty()) {
+    const int32_t b = *free_.begin();
+    free_.erase(free_.begin());
+    if (journaling_) journal_.push_back({kUndoFreePop, b, Meta{}});
+    return b;
+  }
+  if (evictable_.empty()) {
+    *ok = false;
+    return -1;
+  }
+  const int32_t b = evictable_.begin()->second;
+  evictable_.erase(evictable_.begin());
+  if (journaling_) journal_.push_back({kUndoEvict, b, meta_[b]});
+  index_.erase(meta_[b].dig);
+  meta_[b].resident = false;
+  stats_.evictions++;
+  return b;
+}
+
+void Store::pin(int32_t b) {
+  if (pinned_mark_[b]) return;
+  pinned_mark_[b] = 1;
+  cur_pinned_->push_back(b);
+  if (pins_[b] == 0 && meta_[b].resident) set_evictable(b, false);
+  pins_[b]++;
+  journal_.push_back({kUndoPin, b, Meta{}});
+}
+
+void Store::touch(int32_t b) {
+  journal_.push_back({kUndoTouch, b, meta_[b]});
+  meta_[b].last_use = plan_no_;
+}
+
+void Store::rollback() {
+  for (auto it = journal_.rbegin(); it != journal_.rend(); ++it) {
+    const int32_t b = it->block;
+    switch (it->kind) {
+      case kUndoFreePop:
+        free_.insert(b);
+        break;
+      case kUndoEvict:
+        meta_[b] = it->meta;
+        index_[meta_[b].dig] = b;
+        if (pins_[b] == 0) set_evictable(b, true);
+        break;
+      case kUndoInsert:
+        if (pins_[b] == 0) set_evictable(b, false);  // no-op unless the insert was unpinned
+        index_.erase(meta_[b].dig);
+        meta_[b].resident = false;
+        break;
+      case kUndoPin:
+        pins_[b]--;
+        pinned_mark_[b] = 0;
+        if (pins_[b] == 0 && meta_[b].resident) set_evictable(b, true);
+        break;
+      case kUndoTouch:
+        meta_[b].last_use = it->meta.last_use;
+        break;
+    }
+  }
+  journal_.clear();
+}
+
+int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out) {
+  const StoreStats saved_stats = stats_;
+  const int64_t saved_plan = plan_no_;
+  journal_.clear();
+  journaling_ = true;
+  *out = PlanHost();
+  PlanHost& P = *out;
+  P.n_queries = static_cast<int32_t>(qs.size());
+  cur_pinned_ = &P.pinned;
+  plan_no_++;
+  const int bs = bs_;
+  bool ok = true;
+
+  auto insert_new = [&](const Digest& d, int32_t ntok) -> int32_t {
+    const int32_t b = alloc(&ok);
+    if (!ok) return -1;
+    index_[d] = b;
+    meta_[b] = Meta{d, ntok, plan_no_, true};
+    journal_.push_back({kUndoInsert, b, Meta{}});
+    stats_.inserted_blocks++;
+    pin(b);
+    for (int64_t s = static_cast<int64_t>(b) * bs + ntok; s < static_cast<int64_t>(b) * bs + bs; ++s)
+      P.pad_slots.push_back(s);
+    return b;
+  };
+  auto new_private = [&](int32_t ntok) -> int32_t {
+    const int32_t b = alloc(&ok);
+    if (!ok) return -1;
+    P.priv.push_back(b);
+    pin(b);
+    for (int64_t s = static_cast<int64_t>(b) * bs + ntok; s < static_cast<int64_t>(b) * bs + bs; ++s)
+      P.pad_slots.push_back(s);
+    return b;
+  };
+  auto add_seg = [&](int32_t qi, int32_t kind, int32_t fi, int32_t len, int32_t pos0, int32_t hit,
+                     int32_t cb, const std::vector<int32_t>& blocks, const std::vector<uint8_t>& wr,
+                     const std::vector<Digest>& dig) {
+    P.segs.push_back(Segment{qi, kind, fi, len, pos0, hit, cb, static_cast<int32_t>(P.blocks.size()),
+                             static_cast<int32_t>(blocks.size())});
+    P.blocks.insert(P.blocks.end(), blocks.begin(), blocks.end());
+    P.block_write.insert(P.block_write.end(), wr.begin(), wr.end());
+    P.digests.insert(P.digests.end(), dig.begin(), dig.end());
+  };
+
+  std::vector<Digest> dig;
+  std::vector<int32_t> blocks;
+  std::vector<uint8_t> wr;
+  for (int32_t qi = 0; qi < P.n_queries && ok; ++qi) {
+    const FlatQuery& q = qs[qi];
+    int64_t ntot = static_cast<int64_t>(q.prefix.size()) + static_cast<int64_t>(q.cross.size());
+    for (const auto& f : q.frags) ntot += static_cast<int64_t>(f.size());
+    stats_.input_tokens += ntot;
+    // ---- prefix: chained digests + prefix scan; partial tail plan-private (R9)
+    const int32_t plen = static_cast<int32_t>(q.prefix.size());
+    dig.clear();
+    chain('P', root_, q.prefix.data(), plen, bs, &dig);
+    blocks.clear();
+    wr.clear();
+    bool hit_run = true;
+    int32_t n_hit = 0;
+    for (size_t i = 0; i < dig.size() && ok; ++i) {
+      const int32_t ntok = std::min<int32_t>(bs, plen - static_cast<int32_t>(i) * bs);
+      const bool full = ntok == bs;
+      if (full) stats_.lookups++;
+      const int32_t r = full ? lookup(dig[i]) : -1;
+      if (r >= 0) {
+        pin(r);
+        touch(r);
+        blocks.push_back(r);
+        wr.push_back(0);
+        if (hit_run) {
+          n_hit++;
+          stats_.hit_blocks++;
+          stats_.hit_tokens += bs;
+        } else {
+          stats_.miss_blocks++;
+        }
+        continue;
+      }
+      hit_run = false;
+      if (full) {
+        stats_.miss_blocks++;
+        blocks.push_back(insert_new(dig[i], bs));
+      } else {
+        blocks.push_back(new_private(ntok));
+      }
+      wr.push_back(1);
+    }
+    if (!ok) break;
+    if (plen > 0)
+      add_seg(qi, kPrefix, -1, plen, 0, n_hit, std::min(n_hit * bs, plen), blocks, wr, dig);
+    const Digest h_last = dig.empty() ? root_ : dig.back();
+    // ---- fragments: suspended chains, all-or-nothing lookup (R10, R11)
+    int32_t off = plen;
+    std::vector<Digest> lasts;
+    for (size_t fi = 0; fi < q.frags.size() && ok; ++fi) {
+      const auto& f = q.frags[fi];
+      const int32_t flen = static_cast<int32_t>(f.size());
+      dig.clear();
+      chain('F', root_, f.data(), flen, bs, &dig);
+      lasts.push_back(dig.back());
+      stats_.lookups++;
+      std::vector<int32_t> res(dig.size());
+      bool all = true;
+      for (size_t i = 0; i < dig.size(); ++i) {
+        res[i] = lookup(dig[i]);
+        all = all && res[i] >= 0;
+      }
+      for (int32_t b : res)
+        if (b >= 0) {
+          pin(b);
+          touch(b);
+        }
+      blocks.clear();
+      wr.clear();
+      if (all) {
+        stats_.hit_blocks += static_cast<int64_t>(dig.size());
+        stats_.hit_tokens += flen;
+        wr.assign(dig.size(), 0);
+        add_seg(qi, kFrag, static_cast<int32_t>(fi), flen, off, 1, flen, res, wr, dig);
+      } else {
+        stats_.miss_blocks += static_cast<int64_t>(dig.size());
+        for (size_t i = 0; i < dig.size() && ok; ++i) {
+          if (res[i] >= 0) {
+            blocks.push_back(res[i]);
+            wr.push_back(0);
+          } else {
+            blocks.push_back(insert_new(dig[i], std::min<int32_t>(bs, flen - static_cast<int32_t>(i) * bs)));
+            wr.push_back(1);
+          }
+        }
+        if (!ok) break;
+        add_seg(qi, kFrag, static_cast<int32_t>(fi), flen, off, 0, 0, blocks, wr, dig);
+      }
+      off += flen;
+    }
+    if (!ok) break;
+    const Digest J = join_fold(h_last, lasts);
+    P.join_digests.push_back(J);
+    // ---- cross: always computed; full blocks under the X chain (R9)
+    const int32_t clen = static_cast<int32_t>(q.cross.size());
+    dig.clear();
+    chain('X', J, q.cross.data(), clen, bs, &dig);
+    blocks.clear();
+    wr.clear();
+    for (size_t i = 0; i < dig.size() && ok; ++i) {
+      const int32_t ntok = std::min<int32_t>(bs, clen - static_cast<int32_t>(i) * bs);
+      const int32_t r = ntok == bs ? lookup(dig[i]) : -1;
+      if (r >= 0) {
+        pin(r);
+        touch(r);
+        blocks.push_back(r);
+        wr.push_back(0);
+      } else if (ntok == bs) {
+        blocks.push_back(insert_new(dig[i], bs));
+        wr.push_back(1);
+      } else {
+        blocks.push_back(new_private(ntok));
+        wr.push_back(1);
+      }
+    }
+    if (!ok) break;
+    add_seg(qi, kCross, -1, clen, off, 0, 0, blocks, wr, dig);
+  }
+  if (!ok) {
+    rollback();
+    for (int32_t b : P.pinned) pinned_mark_[b] = 0;
+    stats_ = saved_stats;
+    plan_no_ = saved_plan;
+    journaling_ = false;
+    cur_pinned_ = nullptr;
+    *out = PlanHost();
+    return 2;
+  }
+  journal_.clear();
+  journaling_ = false;
+  for (int32_t b : P.pinned) pinned_mark_[b] = 0;
+  cur_pinned_ = nullptr;
+
+  // ---- packed rows (job order for prefill, query order for joins)
+  auto rows = [&](const Segment& s, int32_t begin, std::vector<int32_t>* pos,
+                  std::vector<int64_t>* slot, std::vector<int32_t>* segi, int32_t si) {
+    for (int32_t t = begin; t < s.tok_len; ++t) {
+      const int32_t b = t / bs, o = t % bs;
+      pos->push_back(s.kind == kCross ? s.pos0 + t : t);
+      slot->push_back(P.block_write[s.block_off + b]
+                          ? static_cast<int64_t>(P.blocks[s.block_off + b]) * bs + o
+                          : -1);
+      segi->push_back(si);
+    }
+  };
+  P.job_row_off.push_back(0);
+  for (size_t i = 0; i < P.segs.size(); ++i) {
+    const Segment& s = P.segs[i];
+    if (s.kind != kCross && s.compute_begin < s.tok_len) {
+      P.jobs.push_back(static_cast<int32_t>(i));
+      rows(s, s.compute_begin, &P.prefill_pos, &P.prefill_slot, &P.prefill_seg, static_cast<int32_t>(i));
+      P.job_row_off.push_back(static_cast<int64_t>(P.prefill_pos.size()));
+    }
+  }
+  P.query_join_row_off.push_back(0);
+  for (size_t i = 0; i < P.segs.size(); ++i) {
+    const Segment& s = P.segs[i];
+    if (s.kind == kCross) {
+      rows(s, 0, &P.join_pos, &P.join_slot, &P.join_seg, static_cast<int32_t>(i));
+      P.query_join_row_off.push_back(static_cast<int64_t>(P.join_pos.size()));
+    }
+  }
+  return 0;
+}
+
+void Store::release(const PlanHost& p) {
+  for (int32_t b : p.pinned) {
+    pins_[b]--;
+    if (pins_[b] == 0 && meta_[b].resident) set_evictable(b, true);
+  }
+  for (int32_t b : p.priv) free_.insert(b);
+}
+
+void Store::evict_all() {
+  std::vector<int32_t> victims;
+  for (const auto& kv : index_)
+    if (pins_[kv.second] == 0) victims.push_back(kv.second);
+  for (int32_t b : victims) {
+    set_evictable(b, false);
+    index_.erase(meta_[b].dig);
+    meta_[b].resident = false;
+    free_.insert(b);
+  }
+}
+
+int Store::insert(const Digest* d, const int32_t* ntok, int64_t n, int32_t* ids) {
+  const StoreStats saved = stats_;
+  journal_.clear();
+  journaling_ = true;
+  bool ok = true;
+  for (int64_t i = 0; i < n && ok; ++i) {
+    const int32_t r = lookup(d[i]);
+    if (r >= 0) {
+      ids[i] = r;
+      continue;
+    }
+    const int32_t b = alloc(&ok);
+    if (!ok) break;
+    index_[d[i]] = b;
+    meta_[b] = Meta{d[i], ntok[i], plan_no_, true};
+    journal_.push_back({kUndoInsert, b, Meta{}});
+    set_evictable(b, true);
+    stats_.inserted_blocks++;
+    ids[i] = b;
+  }
+  if (!ok) {
+    rollback();
+    stats_ = saved;
+    journaling_ = false;
+    return 2;
+  }
+  journal_.clear();
+  journaling_ = false;
+  return 0;
+}
+
+}  // namespace spq

@@ -1,0 +1,126 @@
+// planner.h — span-query planner and content-hash block store (host, C++17).
+//
+// Step a1-a3 of SURVEY §8(a): normalize the tree (plus simplification
+// P:439), hash blocks (prefix chain P:97-98, suspended fragment chain P:603, ordered join fold,
+// cross chain), prefix-scan / all-or-nothing lookup, in-plan dedupe, lowest-id allocation, LRU
+// eviction of unpinned blocks, pinning, rollback on ENOMEM. Readings R8-R13.
+#pragma once
+#include <cstdint>
+#include <set>
+#include <string>
+#include <unordered_map>
+#include <utility>
+#include <vector>
+
+#include "blake2b.h"
+
+#include "../../../include/spanq.h"
+
+namespace spq {
+
+enum SegKind : int32_t { kPrefix = 0, kFrag = 1, kCross = 2 };
+
+struct FlatQuery {
+  std::vector<int32_t> prefix;
+  std::vector<std::vector<int32_t>> frags;
+  std::vector<int32_t> cross;
+};
+
+// Validate + flatten an ABI tree. Returns false and sets *err on an invalid tree.
+bool normalize_tree(const spq_query& q, FlatQuery* out, std::string* err);
+
+struct Segment {
+  int32_t query, kind, frag_idx, tok_len, pos0, hit, compute_begin, block_off, n_blocks;
+};
+
+struct StoreStats {
+  int64_t lookups = 0, hit_blocks = 0, miss_blocks = 0, hit_tokens = 0, input_tokens = 0,
+          evictions = 0, inserted_blocks = 0;
+};
+
+struct PlanHost {
+  std::vector<Segment> segs;
+  std::vector<int32_t> blocks;
+  std::vector<uint8_t> block_write;
+  std::vector<Digest> digests;
+  std::vector<Digest> join_digests;
+  std::vector<int32_t> jobs;
+  std::vector<int64_t> job_row_off;
+  std::vector<int32_t> prefill_pos;
+  std::vector<int64_t> prefill_slot;
+  std::vector<int32_t> prefill_seg;
+  std::vector<int32_t> join_pos;
+  std::vector<int64_t> join_slot;
+  std::vector<int32_t> join_seg;
+  std::vector<int64_t> query_join_row_off;
+  std::vector<int64_t> pad_slots;
+  std::vector<int32_t> pinned;
+  std::vector<int32_t> priv;
+  int32_t n_queries = 0;
+};
+
+// Digest chains (hash contract): ROOT, 'P' prefix, 'F' fragment, 'J' fold, 'X' cross.
+Digest root_digest(int hq, int hkv, int d, int bs, double rope_base, uint64_t salt);
+void chain(char tag, const Digest& seed, const int32_t* tok, int64_t n, int bs,
+           std::vector<Digest>* out);
+Digest join_fold(const Digest& h_last, const std::vector<Digest>& frag_lasts);
+
+class Store {
+ public:
+  Store(int64_t num_blocks, int block_size, const Digest& root);
+
+  // Plan a batch. Returns 0 on success, 2 on ENOMEM (state rolled back).
+  int plan(const std::vector<FlatQuery>& qs, PlanHost* out);
+  void release(const PlanHost& p);
+  void evict_all();
+  int32_t lookup(const Digest& d) const;
+  // Low-level insert: returns 0 or 2 (ENOMEM, rolled back).
+  int insert(const Digest* d, const int32_t* ntok, int64_t n, int32_t* ids);
+
+  const StoreStats& stats() const { return stats_; }
+  int64_t resident() const { return static_cast<int64_t>(index_.size()); }
+  int64_t free_count() const { return static_cast<int64_t>(free_.size()); }
+  int64_t pinned_count() const;
+  int64_t plans() const { return plan_no_; }
+  const Digest& root() const { return root_; }
+  int block_size() const { return bs_; }
+
+ private:
+  struct Meta {
+    Digest dig;
+    int32_t ntok;
+    int64_t last_use;
+    bool resident;
+  };
+  enum UndoKind { kUndoFreePop, kUndoEvict, kUndoInsert, kUndoPin, kUndoTouch };
+  struct Undo {
+    UndoKind kind;
+    int32_t block;
+    Meta meta;  // previous meta (evict / touch)
+  };
+
+  int32_t alloc(bool* ok);
+  void pin(int32_t b);
+  void touch(int32_t b);
+  int32_t insert_new(const Digest& d, int32_t ntok);
+  void rollback();
+  void set_evictable(int32_t b, bool on);
+
+  int64_t nblocks_;
+  int bs_;
+  Digest root_;
+  std::unordered_map<Digest, int32_t, DigestHash> index_;
+  std::vector<Meta> meta_;
+  std::vector<int32_t> pins_;
+  std::set<int32_t> free_;
+  std::set<std::pair<int64_t, int32_t>> evictable_;  // (last_use, id), resident & unpinned
+  int64_t plan_no_ = 0;
+  StoreStats stats_;
+  std::vector<Undo> journal_;
+  bool journaling_ = false;
+  // per-plan pin bookkeeping
+  std::vector<uint8_t> pinned_mark_;
+  std::vector<int32_t>* cur_pinned_ = nullptr;
+};
+
+}  // namespace spq

@@ -1,0 +1,78 @@
+// combine.cu — K4: merge split-KV partial attention results.
+//
+//   lse = log Σ_s exp(lse_s),   O = Σ_s exp(lse_s - lse) · O_s
+// over the splits s of one (row, head), in a fixed order (deterministic, no atomics). Partials
+// hold normalized O_s (fp32) and natural-log lse_s (-inf when the split saw no visible key).
+// One warp per (row, head); each lane owns d/32 consecutive columns (float2 loads).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "launch.h"
+
+namespace spq {
+namespace {
+
+template <int D>
+__global__ void __launch_bounds__(256) combine_kernel(const CombineDesc* __restrict__ desc,
+                                                      const float* __restrict__ opart,
+                                                      const float* __restrict__ lsepart,
+                                                      __nv_bfloat16* __restrict__ o,
+                                                      float* __restrict__ lse, int hq) {
+  constexpr int E = D / 32;  // columns per lane
+  const CombineDesc cd = desc[blockIdx.x];
+  const int h = blockIdx.y;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int r = warp; r < cd.n_rows; r += blockDim.x / 32) {
+    float m = -INFINITY;
+    for (int s = 0; s < cd.n_split; ++s)
+      m = fmaxf(m, lsepart[(static_cast<int64_t>(cd.part_base + s) * hq + h) * kTileRows + r]);
+    float acc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = 0.f;
+    float tot = 0.f;
+    for (int s = 0; s < cd.n_split; ++s) {
+      const int64_t pidx = (static_cast<int64_t>(cd.part_base + s) * hq + h) * kTileRows + r;
+      const float ls = lsepart[pidx];
+      const float w = (ls == -INFINITY) ? 0.f : __expf(ls - m);
+      tot += w;
+      const float* src = opart + pidx * D + lane * E;
+#pragma unroll
+      for (int e = 0; e < E; e += 2) {
+        const float2 v = *reinterpret_cast<const float2*>(src + e);
+        acc[e] = fmaf(w, v.x, acc[e]);
+        acc[e + 1] = fmaf(w, v.y, acc[e + 1]);
+      }
+    }
+    const float inv = 1.f / tot;
+    const int64_t row = cd.row0 + r;
+    __nv_bfloat16* dst = o + (row * hq + h) * D + lane * E;
+#pragma unroll
+    for (int e = 0; e < E; e += 2)
+      *reinterpret_cast<__nv_bfloat162*>(dst + e) = __floats2bfloat162_rn(acc[e] * inv, acc[e + 1] * inv);
+    if (lse != nullptr && lane == 0) lse[row * hq + h] = m + logf(tot);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
+  if (a.n_desc == 0) return cudaSuccess;
+  dim3 grid(a.n_desc, a.hq);
+  switch (a.d) {
+    case 64:
+      combine_kernel<64><<<grid, 256, 0, st>>>(a.desc, a.opart, a.lsepart,
+                                                static_cast<__nv_bfloat16*>(a.o), a.lse, a.hq);
+      break;
+    case 128:
+      combine_kernel<128><<<grid, 256, 0, st>>>(a.desc, a.opart, a.lsepart,
+                                                 static_cast<__nv_bfloat16*>(a.o), a.lse, a.hq);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace spq

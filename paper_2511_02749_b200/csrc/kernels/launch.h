@@ -1,0 +1,71 @@
+// launch.h — host-side launchers of the device kernels (called by the C-ABI layer only).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "work.h"
+
+namespace spq {
+
+struct KvWriteArgs {
+  const void* k;  // [rows][hkv][d] pre-RoPE
+  const void* v;
+  const int32_t* pos;
+  const int64_t* slot;
+  int64_t rows;
+  const int64_t* pad_slots;
+  int64_t n_pad;
+  void* k_pool;
+  void* v_pool;
+  int hkv, d, bs;
+  int64_t nblk;
+  int layer;
+  const float2* rope;
+  bool fp32;
+};
+cudaError_t launch_rope_kv_write(const KvWriteArgs& a, cudaStream_t st);
+
+struct AttnArgs {
+  // work list (device)
+  const KvTile* tiles;
+  const int32_t* tile_blocks;
+  const WorkItem* items;
+  int32_t n_items;
+  const int32_t* cta_off;  // persistent schedule (tcgen05 kernel)
+  const int32_t* cta_items;
+  int32_t grid;
+  // rows
+  const int32_t* pos;  // [rows] position of each query row
+  const void* q;       // [rows][hq][d]
+  void* o;             // [rows][hq][d]
+  float* lse;          // [rows][hq] or null
+  float* opart;        // [parts][hq][128][d] fp32
+  float* lsepart;      // [parts][hq][128]
+  // pools
+  const void* k_pool;
+  const void* v_pool;
+  const CUtensorMap* tmap_k;  // host copies (bf16 path)
+  const CUtensorMap* tmap_v;
+  int hq, hkv, d, bs;
+  int64_t nblk;
+  int layer;
+  const float2* rope;
+  int max_pos;
+};
+cudaError_t launch_span_attn_tc(const AttnArgs& a, cudaStream_t st);   // bf16 tcgen05
+cudaError_t launch_span_attn_f32(const AttnArgs& a, cudaStream_t st);  // fp32 SIMT
+
+struct CombineArgs {
+  const CombineDesc* desc;
+  int32_t n_desc;
+  const float* opart;
+  const float* lsepart;
+  void* o;
+  float* lse;
+  int hq, d;
+};
+cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);
+
+}  // namespace spq

@@ -1,0 +1,161 @@
+// rope_kv_write.cu — K1: fused RoPE + paged KV-cache write.
+//
+// For every packed row r with slot[r] >= 0 and every kv head h:
+//   k_pool[layer][slot/bs][h][slot%bs][:] = RoPE(k[r,h,:], pos[r])      (R15 rotate-half)
+//   v_pool[layer][slot/bs][h][slot%bs][:] = v[r,h,:]
+// plus zero-fill of the plan's pad slots (partial blocks, reading R8).
+// RoPE positions: span-local for fragments (reading R2), global for prefix/cross (§5.5
+// P:610). cos/sin come from the fp64-built table [max_pos][d/2] (float2).
+//
+// HBM-bound, no reuse: one thread moves one 16-byte vector of k and of v; the rotate-half
+// partner vector (element i <-> i + d/2) sits d/16 (bf16) or d/8 (fp32) lanes away in the same
+// warp and is fetched with one __shfl_xor. Loads/stores are 128-bit and fully coalesced per row.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "launch.h"
+
+namespace spq {
+namespace {
+
+template <typename T>
+struct Vec;
+template <>
+struct Vec<__nv_bfloat16> {
+  static constexpr int N = 8;
+  __device__ static void unpack(const uint4& u, float (&f)[8]) {
+    const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 t = __bfloat1622float2(p[i]);
+      f[2 * i] = t.x;
+      f[2 * i + 1] = t.y;
+    }
+  }
+  __device__ static uint4 pack(const float (&f)[8]) {
+    uint4 u;
+    __nv_bfloat162* p = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) p[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    return u;
+  }
+};
+template <>
+struct Vec<float> {
+  static constexpr int N = 4;
+  __device__ static void unpack(const uint4& u, float (&f)[4]) {
+    f[0] = __uint_as_float(u.x);
+    f[1] = __uint_as_float(u.y);
+    f[2] = __uint_as_float(u.z);
+    f[3] = __uint_as_float(u.w);
+  }
+  __device__ static uint4 pack(const float (&f)[4]) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
+                      __float_as_uint(f[3]));
+  }
+};
+
+// G = d / N vectors per (row, head); lanes of one (row, head) are G consecutive lanes.
+template <typename T, int D>
+__global__ void __launch_bounds__(256) rope_kv_write_kernel(
+    const T* __restrict__ k, const T* __restrict__ v, const int32_t* __restrict__ pos,
+    const int64_t* __restrict__ slot, int64_t rows, const int64_t* __restrict__ pad_slots,
+    int64_t n_pad, T* __restrict__ k_pool, T* __restrict__ v_pool, int hkv, int bs, int64_t nblk,
+    int layer, const float2* __restrict__ rope) {
+  constexpr int N = Vec<T>::N;
+  constexpr int G = D / N;
+  static_assert(G <= 32 && (G & (G - 1)) == 0, "d/N must be a power of two <= 32");
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t per_row = static_cast<int64_t>(hkv) * G;
+  const int64_t total = rows * per_row;
+  const int64_t layer_off = static_cast<int64_t>(layer) * nblk * hkv * bs * D;
+  // every lane takes part in the partner shuffle (whole warps), then branches
+  const bool main_row = gid < total;
+  int64_t r = 0, src = 0;
+  int h = 0, g = 0;
+  uint4 ku = make_uint4(0, 0, 0, 0);
+  if (main_row) {
+    r = gid / per_row;
+    const int rem = static_cast<int>(gid - r * per_row);
+    h = rem / G;
+    g = rem % G;
+    src = (r * hkv + h) * D + g * N;
+    ku = __ldg(reinterpret_cast<const uint4*>(k + src));
+  }
+  uint4 pu;
+  pu.x = __shfl_xor_sync(0xffffffffu, ku.x, G / 2);
+  pu.y = __shfl_xor_sync(0xffffffffu, ku.y, G / 2);
+  pu.z = __shfl_xor_sync(0xffffffffu, ku.z, G / 2);
+  pu.w = __shfl_xor_sync(0xffffffffu, ku.w, G / 2);
+  if (main_row) {
+    float x[N], y[N];
+    Vec<T>::unpack(ku, x);
+    Vec<T>::unpack(pu, y);
+    const int64_t s = slot[r];
+    if (s >= 0) {
+      const int p = pos[r];
+      const bool first_half = g < G / 2;
+      const int i0 = (first_half ? g : g - G / 2) * N;  // pair index of element 0
+      const float2* cs = rope + static_cast<int64_t>(p) * (D / 2) + i0;
+      float out[N];
+#pragma unroll
+      for (int e = 0; e < N; ++e) {
+        const float2 c = __ldg(cs + e);
+        // first half: x*cos - partner*sin ; second half: x*cos + partner*sin
+        out[e] = first_half ? fmaf(x[e], c.x, -y[e] * c.y) : fmaf(x[e], c.x, y[e] * c.y);
+      }
+      const int64_t blk = s / bs, off = s % bs;
+      const int64_t dst = layer_off + ((blk * hkv + h) * bs + off) * D + g * N;
+      *reinterpret_cast<uint4*>(k_pool + dst) = Vec<T>::pack(out);
+      *reinterpret_cast<uint4*>(v_pool + dst) = __ldg(reinterpret_cast<const uint4*>(v + src));
+    }
+    return;
+  }
+  // pad slots: zero K and V of every head
+  const int64_t pid = gid - total;
+  if (pid >= n_pad * per_row) return;
+  const int64_t pr = pid / per_row;
+  const int prem = static_cast<int>(pid - pr * per_row);
+  const int ph = prem / G, pg = prem % G;
+  const int64_t ps = pad_slots[pr];
+  const int64_t pblk = ps / bs, poff = ps % bs;
+  const int64_t dst = layer_off + ((pblk * hkv + ph) * bs + poff) * D + pg * N;
+  *reinterpret_cast<uint4*>(k_pool + dst) = make_uint4(0, 0, 0, 0);
+  *reinterpret_cast<uint4*>(v_pool + dst) = make_uint4(0, 0, 0, 0);
+}
+
+template <typename T, int D>
+cudaError_t launch_t(const KvWriteArgs& a, cudaStream_t st) {
+  constexpr int G = D / Vec<T>::N;
+  const int64_t threads = (a.rows + a.n_pad) * static_cast<int64_t>(a.hkv) * G;
+  if (threads == 0) return cudaSuccess;
+  const int64_t blocks = (threads + 255) / 256;
+  rope_kv_write_kernel<T, D><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+      static_cast<const T*>(a.k), static_cast<const T*>(a.v), a.pos, a.slot, a.rows, a.pad_slots,
+      a.n_pad, static_cast<T*>(a.k_pool), static_cast<T*>(a.v_pool), a.hkv, a.bs, a.nblk, a.layer,
+      a.rope);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_rope_kv_write(const KvWriteArgs& a, cudaStream_t st) {
+  if (a.fp32) {
+    switch (a.d) {
+      case 32: return launch_t<float, 32>(a, st);
+      case 64: return launch_t<float, 64>(a, st);
+      case 128: return launch_t<float, 128>(a, st);
+    }
+  } else {
+    switch (a.d) {
+      case 64: return launch_t<__nv_bfloat16, 64>(a, st);
+      case 128: return launch_t<__nv_bfloat16, 128>(a, st);
+      case 256: return launch_t<__nv_bfloat16, 256>(a, st);
+    }
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace spq

@@ -1,0 +1,686 @@
+// spanq_api.cpp — implementation of include/spanq.h (the C ABI).
+//
+// Host side of the path: ctx (config, content-hash store, RoPE table, TMA descriptors, staging),
+// plans (planner output + device work lists uploaded with one H2D copy), and the per-call
+// kernel sequence:
+//   spq_prefill_jobs: rope_kv_write (K1) -> span_attn (K2; tcgen05 bf16 or SIMT fp32)
+//   spq_join:         rope_kv_write (K1) -> span_attn (K3, split-KV) -> combine (K4)
+// No CPU fallback: a ctx with device >= 0 requires an sm_100 GPU and fails loudly otherwise.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/spanq.h"
+#include "host/planner.h"
+#include "host/work_builder.h"
+#include "kernels/launch.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+spq_status fail(spq_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(SPQ_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));             \
+  } while (0)
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// One device buffer holding several arrays (one H2D copy).
+struct Packer {
+  std::vector<uint8_t> host;
+  template <typename T>
+  size_t add(const std::vector<T>& v) {
+    const size_t off = align_up(host.size(), 256);
+    host.resize(off + v.size() * sizeof(T));
+    if (!v.empty()) std::memcpy(host.data() + off, v.data(), v.size() * sizeof(T));
+    return off;
+  }
+};
+
+struct DevWork {  // offsets of one attention work list inside a plan buffer
+  size_t tiles, tile_blocks, items, cta_off, cta_items, combine;
+  int32_t n_items = 0, grid = 0, n_combine = 0, n_parts = 0;
+  double flops = 0;
+};
+
+}  // namespace
+
+struct spq_ctx {
+  spq_config cfg;
+  std::unique_ptr<spq::Store> store;
+  int num_sms = 0;
+  float2* rope = nullptr;  // device [max_position][d/2]
+  CUtensorMap tmk, tmv;
+  bool have_tmap = false;
+  std::vector<cudaEvent_t> pending;  // stream-ordered releases
+  int64_t launches = 0;
+  bool timing = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  float last_prefill_ms = 0.f, last_join_ms = 0.f;
+  bool prefill_timed = false, join_timed = false;
+  // pinned upload staging
+  uint8_t* staging = nullptr;
+  size_t staging_size = 0;
+  cudaEvent_t staging_ev = nullptr;
+};
+
+struct spq_plan {
+  spq::PlanHost host;
+  bool released = false;
+  // flat view arrays
+  std::vector<int32_t> seg_query, seg_kind, seg_frag_idx, seg_tok_len, seg_pos0, seg_hit, seg_cb,
+      seg_block_off, seg_n_blocks;
+  std::vector<uint8_t> digests, join_digests;
+  double prefill_flops = 0, join_flops = 0;
+  int64_t prefill_kv_bytes = 0, join_kv_bytes = 0;
+  // device
+  uint8_t* dbuf = nullptr;
+  size_t off_ppos = 0, off_pslot = 0, off_pad = 0, off_jpos = 0, off_jslot = 0;
+  DevWork pw, jw;
+  float* opart = nullptr;
+  float* lsepart = nullptr;
+  std::vector<uint8_t> padded_layers;
+  spq::AttnWorkHost pw_host, jw_host;  // kept for sub-range rebuilds / inspection
+};
+
+namespace {
+
+bool is_gpu(const spq_ctx* c) { return c->cfg.device >= 0; }
+
+int elt_size(const spq_ctx* c) { return c->cfg.dtype == SPQ_FP32 ? 4 : 2; }
+
+spq_status make_tmap(spq_ctx* c, void* pool, CUtensorMap* out) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (fn == nullptr || q != cudaDriverEntryPointSuccess)
+    return fail(SPQ_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const spq_config& g = c->cfg;
+  const uint64_t rows = static_cast<uint64_t>(g.num_layers) * g.num_blocks * g.num_kv_heads * g.block_size;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.head_dim), rows};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.head_dim) * 2};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(g.block_size)};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = reinterpret_cast<EncodeTiledFn>(fn)(
+      out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, pool, dims, strides, box, es,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SPQ_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return SPQ_OK;
+}
+
+spq_status wait_pending(spq_ctx* c, cudaStream_t st) {
+  std::vector<cudaEvent_t> keep;
+  for (cudaEvent_t e : c->pending) {
+    if (cudaEventQuery(e) == cudaSuccess) {
+      cudaEventDestroy(e);
+      continue;
+    }
+    CUDA_TRY(cudaStreamWaitEvent(st, e, 0));
+    keep.push_back(e);
+  }
+  c->pending.swap(keep);
+  return SPQ_OK;
+}
+
+template <typename T>
+T* at(const spq_plan* p, size_t off) {
+  return reinterpret_cast<T*>(p->dbuf + off);
+}
+
+void fill_attn(spq_ctx* c, const spq_plan* p, const DevWork& w, spq::AttnArgs* a) {
+  a->tiles = at<spq::KvTile>(p, w.tiles);
+  a->tile_blocks = at<int32_t>(p, w.tile_blocks);
+  a->items = at<spq::WorkItem>(p, w.items);
+  a->n_items = w.n_items;
+  a->cta_off = at<int32_t>(p, w.cta_off);
+  a->cta_items = at<int32_t>(p, w.cta_items);
+  a->grid = w.grid;
+  a->k_pool = c->cfg.k_pool;
+  a->v_pool = c->cfg.v_pool;
+  a->tmap_k = &c->tmk;
+  a->tmap_v = &c->tmv;
+  a->hq = c->cfg.num_q_heads;
+  a->hkv = c->cfg.num_kv_heads;
+  a->d = c->cfg.head_dim;
+  a->bs = c->cfg.block_size;
+  a->nblk = c->cfg.num_blocks;
+  a->rope = c->rope;
+  a->max_pos = c->cfg.max_position;
+  a->opart = p->opart;
+  a->lsepart = p->lsepart;
+}
+
+spq_status run_attn(spq_ctx* c, const spq::AttnArgs& a, cudaStream_t st) {
+  cudaError_t e = c->cfg.dtype == SPQ_FP32 ? spq::launch_span_attn_f32(a, st) : spq::launch_span_attn_tc(a, st);
+  if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("span_attn launch: ") + cudaGetErrorString(e));
+  if (a.n_items > 0) c->launches++;
+  return SPQ_OK;
+}
+
+spq_status kv_write(spq_ctx* c, spq_plan* p, int32_t layer, const void* k, const void* v,
+                    const int32_t* pos, const int64_t* slot, int64_t rows, cudaStream_t st) {
+  spq::KvWriteArgs w{};
+  w.k = k;
+  w.v = v;
+  w.pos = pos;
+  w.slot = slot;
+  w.rows = rows;
+  const bool pad = !p->padded_layers[layer];
+  w.pad_slots = at<int64_t>(p, p->off_pad);
+  w.n_pad = pad ? static_cast<int64_t>(p->host.pad_slots.size()) : 0;
+  w.k_pool = c->cfg.k_pool;
+  w.v_pool = c->cfg.v_pool;
+  w.hkv = c->cfg.num_kv_heads;
+  w.d = c->cfg.head_dim;
+  w.bs = c->cfg.block_size;
+  w.nblk = c->cfg.num_blocks;
+  w.layer = layer;
+  w.rope = c->rope;
+  w.fp32 = c->cfg.dtype == SPQ_FP32;
+  if (rows + w.n_pad == 0) return SPQ_OK;
+  cudaError_t e = spq::launch_rope_kv_write(w, st);
+  if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("rope_kv_write launch: ") + cudaGetErrorString(e));
+  p->padded_layers[layer] = 1;
+  c->launches++;
+  return SPQ_OK;
+}
+
+spq_status check_call(spq_ctx* c, spq_plan* p, int32_t layer) {
+  if (c == nullptr || p == nullptr) return fail(SPQ_EINVAL, "null ctx/plan");
+  if (!is_gpu(c)) return fail(SPQ_ESTATE, "host-only ctx (device < 0) cannot run kernels");
+  if (p->released) return fail(SPQ_ESTATE, "plan used after release");
+  if (layer < 0 || layer >= c->cfg.num_layers) return fail(SPQ_ESTATE, "layer out of range");
+  return SPQ_OK;
+}
+
+// Upload a sub-range work list (not the precomputed full range) into a temporary buffer.
+struct TempWork {
+  uint8_t* buf = nullptr;
+  DevWork w;
+};
+
+spq_status upload_work(spq_ctx* c, const spq::AttnWorkHost& h, cudaStream_t st, TempWork* tw) {
+  Packer pk;
+  tw->w.tiles = pk.add(h.tiles);
+  tw->w.tile_blocks = pk.add(h.tile_blocks);
+  tw->w.items = pk.add(h.items);
+  tw->w.cta_off = pk.add(h.cta_off);
+  tw->w.cta_items = pk.add(h.cta_items);
+  tw->w.combine = pk.add(h.combine);
+  tw->w.n_items = static_cast<int32_t>(h.items.size());
+  tw->w.grid = h.grid;
+  tw->w.n_combine = static_cast<int32_t>(h.combine.size());
+  tw->w.n_parts = h.n_parts;
+  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&tw->buf), std::max<size_t>(pk.host.size(), 256), st));
+  CUDA_TRY(cudaMemcpyAsync(tw->buf, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaStreamSynchronize(st));  // pageable source: keep it alive until the copy is done
+  return SPQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* spq_last_error(void) { return g_err.c_str(); }
+const char* spq_version(void) { return "spanq-b200 0.1 (sm_100a tcgen05)"; }
+
+spq_status spq_create(const spq_config* cfg, spq_ctx** out) {
+  if (cfg == nullptr || out == nullptr) return fail(SPQ_EINVAL, "null argument");
+  const spq_config& g = *cfg;
+  if (g.num_q_heads <= 0 || g.num_kv_heads <= 0 || g.num_q_heads % g.num_kv_heads != 0)
+    return fail(SPQ_EINVAL, "Hq must be a positive multiple of Hkv");
+  if (g.num_layers <= 0 || g.block_size <= 0 || g.num_blocks <= 0 || g.num_blocks > INT32_MAX)
+    return fail(SPQ_EINVAL, "bad layers/block_size/num_blocks");
+  if (g.dtype != SPQ_BF16 && g.dtype != SPQ_FP32) return fail(SPQ_EINVAL, "bad dtype");
+  if (g.world_size != 1 || g.rank != 0) return fail(SPQ_EINVAL, "world_size must be 1 in this version");
+  if (g.max_position <= 0 || !(g.rope_base > 0)) return fail(SPQ_EINVAL, "bad rope parameters");
+  std::unique_ptr<spq_ctx> c(new spq_ctx());
+  c->cfg = g;
+  c->store.reset(new spq::Store(g.num_blocks, g.block_size,
+                                spq::root_digest(g.num_q_heads, g.num_kv_heads, g.head_dim, g.block_size,
+                                                 g.rope_base, g.model_salt)));
+  if (g.device >= 0) {
+    if (g.head_dim != 64 && g.head_dim != 128) return fail(SPQ_EINVAL, "head_dim must be 64 or 128 on the GPU");
+    if (g.block_size > 128 || (g.block_size & (g.block_size - 1)) != 0)
+      return fail(SPQ_EINVAL, "block_size must be a power of two <= 128 on the GPU");
+    if (g.dtype == SPQ_BF16 && g.block_size < 16) return fail(SPQ_EINVAL, "bf16 path needs block_size >= 16");
+    if (g.k_pool == nullptr || g.v_pool == nullptr) return fail(SPQ_EINVAL, "null KV pool");
+    if ((reinterpret_cast<uintptr_t>(g.k_pool) | reinterpret_cast<uintptr_t>(g.v_pool)) & 127)
+      return fail(SPQ_EINVAL, "KV pools must be 128-byte aligned");
+    CUDA_TRY(cudaSetDevice(g.device));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, g.device));
+    if (prop.major != 10 || prop.minor != 0)
+      return fail(SPQ_ECUDA, "device is sm_" + std::to_string(prop.major) + std::to_string(prop.minor) +
+                                 "; this library is built for sm_100a only");
+    c->num_sms = prop.multiProcessorCount;
+    // RoPE table from fp64: cos/sin(p * base^(-2i/d)) rounded once to fp32
+    const int half = g.head_dim / 2;
+    std::vector<float2> tab(static_cast<size_t>(g.max_position) * half);
+    for (int i = 0; i < half; ++i) {
+      const double th = std::pow(g.rope_base, -2.0 * i / g.head_dim);
+      for (int64_t p = 0; p < g.max_position; ++p) {
+        const double a = static_cast<double>(p) * th;
+        tab[p * half + i] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+      }
+    }
+    CUDA_TRY(cudaMalloc(&c->rope, tab.size() * sizeof(float2)));
+    CUDA_TRY(cudaMemcpy(c->rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    if (g.dtype == SPQ_BF16) {
+      spq_status s = make_tmap(c.get(), g.k_pool, &c->tmk);
+      if (s != SPQ_OK) return s;
+      s = make_tmap(c.get(), g.v_pool, &c->tmv);
+      if (s != SPQ_OK) return s;
+      c->have_tmap = true;
+    }
+    for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->staging_ev, cudaEventDisableTiming));
+  }
+  *out = c.release();
+  return SPQ_OK;
+}
+
+void spq_destroy(spq_ctx* c) {
+  if (c == nullptr) return;
+  if (is_gpu(c)) {
+    cudaSetDevice(c->cfg.device);
+    cudaDeviceSynchronize();
+    for (cudaEvent_t e : c->pending) cudaEventDestroy(e);
+    for (auto& e : c->ev)
+      if (e) cudaEventDestroy(e);
+    if (c->staging_ev) cudaEventDestroy(c->staging_ev);
+    if (c->staging) cudaFreeHost(c->staging);
+    if (c->rope) cudaFree(c->rope);
+  }
+  delete c;
+}
+
+spq_status spq_block_hashes(const spq_ctx* c, const spq_query* q, uint8_t* digests, int64_t cap, int64_t* n) {
+  if (c == nullptr || q == nullptr || n == nullptr) return fail(SPQ_EINVAL, "null argument");
+  spq::FlatQuery fq;
+  std::string err;
+  if (!spq::normalize_tree(*q, &fq, &err)) return fail(SPQ_EINVAL, err);
+  const int bs = c->cfg.block_size;
+  const spq::Digest& root = c->store->root();
+  std::vector<spq::Digest> all, tmp;
+  spq::chain('P', root, fq.prefix.data(), static_cast<int64_t>(fq.prefix.size()), bs, &tmp);
+  all = tmp;
+  const spq::Digest h_last = tmp.empty() ? root : tmp.back();
+  std::vector<spq::Digest> lasts;
+  for (const auto& f : fq.frags) {
+    tmp.clear();
+    spq::chain('F', root, f.data(), static_cast<int64_t>(f.size()), bs, &tmp);
+    lasts.push_back(tmp.back());
+    all.insert(all.end(), tmp.begin(), tmp.end());
+  }
+  const spq::Digest J = spq::join_fold(h_last, lasts);
+  all.push_back(J);
+  tmp.clear();
+  spq::chain('X', J, fq.cross.data(), static_cast<int64_t>(fq.cross.size()), bs, &tmp);
+  all.insert(all.end(), tmp.begin(), tmp.end());
+  *n = static_cast<int64_t>(all.size());
+  if (cap < *n || digests == nullptr) return fail(SPQ_EINVAL, "digest buffer too small");
+  for (size_t i = 0; i < all.size(); ++i) std::memcpy(digests + 16 * i, all[i].b, 16);
+  return SPQ_OK;
+}
+
+spq_status spq_lookup(const spq_ctx* c, const uint8_t* digests, int64_t n, int32_t* ids) {
+  if (c == nullptr || (n > 0 && (digests == nullptr || ids == nullptr))) return fail(SPQ_EINVAL, "null argument");
+  for (int64_t i = 0; i < n; ++i) {
+    spq::Digest d;
+    std::memcpy(d.b, digests + 16 * i, 16);
+    ids[i] = c->store->lookup(d);
+  }
+  return SPQ_OK;
+}
+
+spq_status spq_insert(spq_ctx* c, const uint8_t* digests, const int32_t* ntok, int64_t n, int32_t* ids) {
+  if (c == nullptr || (n > 0 && (digests == nullptr || ntok == nullptr || ids == nullptr)))
+    return fail(SPQ_EINVAL, "null argument");
+  std::vector<spq::Digest> d(n);
+  for (int64_t i = 0; i < n; ++i) {
+    if (ntok[i] < 1 || ntok[i] > c->cfg.block_size) return fail(SPQ_EINVAL, "ntok out of range");
+    std::memcpy(d[i].b, digests + 16 * i, 16);
+  }
+  if (c->store->insert(d.data(), ntok, n, ids) != 0) return fail(SPQ_ENOMEM, "block pool exhausted (insert rolled back)");
+  return SPQ_OK;
+}
+
+spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queries, void* stream, spq_plan** out) {
+  if (c == nullptr || out == nullptr || (n_queries > 0 && queries == nullptr)) return fail(SPQ_EINVAL, "null argument");
+  if (n_queries <= 0) return fail(SPQ_EINVAL, "n_queries must be >= 1");
+  std::vector<spq::FlatQuery> fq(n_queries);
+  for (int32_t i = 0; i < n_queries; ++i) {
+    std::string err;
+    if (!spq::normalize_tree(queries[i], &fq[i], &err))
+      return fail(SPQ_EINVAL, "query " + std::to_string(i) + ": " + err);
+    int64_t n = static_cast<int64_t>(fq[i].prefix.size() + fq[i].cross.size());
+    for (const auto& f : fq[i].frags) n += static_cast<int64_t>(f.size());
+    if (n > c->cfg.max_position)
+      return fail(SPQ_EINVAL, "query " + std::to_string(i) + " exceeds max_position");
+  }
+  std::unique_ptr<spq_plan> p(new spq_plan());
+  if (c->store->plan(fq, &p->host) != 0) return fail(SPQ_ENOMEM, "block pool cannot hold the plan (rolled back)");
+  const spq::PlanHost& H = p->host;
+  for (const spq::Segment& s : H.segs) {
+    p->seg_query.push_back(s.query);
+    p->seg_kind.push_back(s.kind);
+    p->seg_frag_idx.push_back(s.frag_idx);
+    p->seg_tok_len.push_back(s.tok_len);
+    p->seg_pos0.push_back(s.pos0);
+    p->seg_hit.push_back(s.hit);
+    p->seg_cb.push_back(s.compute_begin);
+    p->seg_block_off.push_back(s.block_off);
+    p->seg_n_blocks.push_back(s.n_blocks);
+  }
+  for (const auto& d : H.digests) p->digests.insert(p->digests.end(), d.b, d.b + 16);
+  for (const auto& d : H.join_digests) p->join_digests.insert(p->join_digests.end(), d.b, d.b + 16);
+  p->padded_layers.assign(c->cfg.num_layers, 0);
+  spq::WorkOpts o{c->cfg.num_q_heads, c->cfg.head_dim, c->cfg.block_size, std::max(1, c->num_sms),
+                  c->cfg.dtype == SPQ_BF16, c->cfg.dtype == SPQ_BF16};
+  spq::build_prefill_work(H, o, 0, static_cast<int>(H.jobs.size()), &p->pw_host);
+  spq::build_join_work(H, o, 0, H.n_queries, &p->jw_host);
+  p->prefill_flops = p->pw_host.flops;
+  p->join_flops = p->jw_host.flops;
+  // algorithmic bytes of rope_kv_write: per written row, read k,v and write both pages
+  // (4*Hkv*d*elt), plus 12 B of pos/slot metadata per row
+  const int64_t row_bytes = 4LL * c->cfg.num_kv_heads * c->cfg.head_dim * elt_size(c);
+  for (int64_t s : H.prefill_slot) p->prefill_kv_bytes += 12 + (s >= 0 ? row_bytes : 0);
+  for (int64_t s : H.join_slot) p->join_kv_bytes += 12 + (s >= 0 ? row_bytes : 0);
+  if (is_gpu(c)) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(cudaSetDevice(c->cfg.device));
+    Packer pk;
+    p->off_ppos = pk.add(H.prefill_pos);
+    p->off_pslot = pk.add(H.prefill_slot);
+    p->off_pad = pk.add(H.pad_slots);
+    p->off_jpos = pk.add(H.join_pos);
+    p->off_jslot = pk.add(H.join_slot);
+    auto add_work = [&](const spq::AttnWorkHost& h, DevWork* w) {
+      w->tiles = pk.add(h.tiles);
+      w->tile_blocks = pk.add(h.tile_blocks);
+      w->items = pk.add(h.items);
+      w->cta_off = pk.add(h.cta_off);
+      w->cta_items = pk.add(h.cta_items);
+      w->combine = pk.add(h.combine);
+      w->n_items = static_cast<int32_t>(h.items.size());
+      w->grid = h.grid;
+      w->n_combine = static_cast<int32_t>(h.combine.size());
+      w->n_parts = h.n_parts;
+      w->flops = h.flops;
+    };
+    add_work(p->pw_host, &p->pw);
+    add_work(p->jw_host, &p->jw);
+    const size_t bytes = std::max<size_t>(pk.host.size(), 256);
+    // pinned staging, reused once its previous upload has completed
+    if (c->staging_size < bytes) {
+      CUDA_TRY(cudaEventSynchronize(c->staging_ev));
+      if (c->staging) CUDA_TRY(cudaFreeHost(c->staging));
+      c->staging_size = std::max(bytes, static_cast<size_t>(1) << 20);
+      CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&c->staging), c->staging_size));
+    } else {
+      CUDA_TRY(cudaEventSynchronize(c->staging_ev));
+    }
+    std::memcpy(c->staging, pk.host.data(), pk.host.size());
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->dbuf), bytes, st));
+    CUDA_TRY(cudaMemcpyAsync(p->dbuf, c->staging, pk.host.size(), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaEventRecord(c->staging_ev, st));
+    if (p->jw.n_parts > 0) {
+      const size_t rows = static_cast<size_t>(p->jw.n_parts) * c->cfg.num_q_heads * spq::kTileRows;
+      CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->opart), rows * c->cfg.head_dim * sizeof(float), st));
+      CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->lsepart), rows * sizeof(float), st));
+    }
+  }
+  *out = p.release();
+  return SPQ_OK;
+}
+
+spq_status spq_plan_view_get(const spq_plan* p, spq_plan_view* v) {
+  if (p == nullptr || v == nullptr) return fail(SPQ_EINVAL, "null argument");
+  if (p->released) return fail(SPQ_ESTATE, "plan used after release");
+  const spq::PlanHost& H = p->host;
+  std::memset(v, 0, sizeof(*v));
+  v->n_queries = H.n_queries;
+  v->n_segments = static_cast<int32_t>(H.segs.size());
+  v->n_jobs = static_cast<int32_t>(H.jobs.size());
+  v->n_blocks_total = static_cast<int64_t>(H.blocks.size());
+  v->seg_query = p->seg_query.data();
+  v->seg_kind = p->seg_kind.data();
+  v->seg_frag_idx = p->seg_frag_idx.data();
+  v->seg_tok_len = p->seg_tok_len.data();
+  v->seg_pos0 = p->seg_pos0.data();
+  v->seg_hit = p->seg_hit.data();
+  v->seg_compute_begin = p->seg_cb.data();
+  v->seg_block_off = p->seg_block_off.data();
+  v->seg_n_blocks = p->seg_n_blocks.data();
+  v->blocks = H.blocks.data();
+  v->block_write = H.block_write.data();
+  v->digests = p->digests.data();
+  v->join_digests = p->join_digests.data();
+  v->jobs = H.jobs.data();
+  v->job_row_off = H.job_row_off.data();
+  v->n_prefill_rows = static_cast<int64_t>(H.prefill_pos.size());
+  v->prefill_pos = H.prefill_pos.data();
+  v->prefill_slot = H.prefill_slot.data();
+  v->n_join_rows = static_cast<int64_t>(H.join_pos.size());
+  v->query_join_row_off = H.query_join_row_off.data();
+  v->join_pos = H.join_pos.data();
+  v->join_slot = H.join_slot.data();
+  v->n_pad_slots = static_cast<int64_t>(H.pad_slots.size());
+  v->pad_slots = H.pad_slots.data();
+  v->prefill_flops = p->prefill_flops;
+  v->join_flops = p->join_flops;
+  v->prefill_kv_bytes = p->prefill_kv_bytes;
+  v->join_kv_bytes = p->join_kv_bytes;
+  return SPQ_OK;
+}
+
+spq_status spq_prefill_jobs(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b, const void* q,
+                            const void* k, const void* v, void* o, float* lse, void* stream) {
+  spq_status s = check_call(c, p, layer);
+  if (s != SPQ_OK) return s;
+  const int32_t nj = static_cast<int32_t>(p->host.jobs.size());
+  if (a < 0 || b > nj || a > b) return fail(SPQ_ESTATE, "job range out of bounds");
+  if (a == b) return SPQ_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  s = wait_pending(c, st);
+  if (s != SPQ_OK) return s;
+  const int64_t r0 = p->host.job_row_off[a], r1 = p->host.job_row_off[b];
+  s = kv_write(c, p, layer, k, v, at<int32_t>(p, p->off_ppos) + r0, at<int64_t>(p, p->off_pslot) + r0, r1 - r0, st);
+  if (s != SPQ_OK) return s;
+  spq::AttnArgs args{};
+  TempWork tw;
+  const bool full = (a == 0 && b == nj);
+  if (full) {
+    fill_attn(c, p, p->pw, &args);
+  } else {
+    spq::AttnWorkHost h;
+    spq::WorkOpts o{c->cfg.num_q_heads, c->cfg.head_dim, c->cfg.block_size, std::max(1, c->num_sms), false,
+                    c->cfg.dtype == SPQ_BF16};
+    spq::build_prefill_work(p->host, o, a, b, &h);
+    s = upload_work(c, h, st, &tw);
+    if (s != SPQ_OK) return s;
+    spq_plan tmp_view;  // only dbuf is read by fill_attn through `at`
+    tmp_view.dbuf = tw.buf;
+    tmp_view.opart = nullptr;
+    tmp_view.lsepart = nullptr;
+    fill_attn(c, &tmp_view, tw.w, &args);
+  }
+  args.pos = at<int32_t>(p, p->off_ppos) + r0;
+  args.q = q;
+  args.o = o;
+  args.lse = lse;
+  args.layer = layer;
+  if (c->timing) CUDA_TRY(cudaEventRecord(c->ev[0], st));
+  s = run_attn(c, args, st);
+  if (s != SPQ_OK) return s;
+  if (c->timing) {
+    CUDA_TRY(cudaEventRecord(c->ev[1], st));
+    c->prefill_timed = true;
+  }
+  if (tw.buf) CUDA_TRY(cudaFreeAsync(tw.buf, st));
+  return SPQ_OK;
+}
+
+spq_status spq_join(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b, const void* q, const void* k,
+                    const void* v, void* o, float* lse, void* stream) {
+  spq_status s = check_call(c, p, layer);
+  if (s != SPQ_OK) return s;
+  const int32_t nq = p->host.n_queries;
+  if (a < 0 || b > nq || a > b) return fail(SPQ_ESTATE, "query range out of bounds");
+  if (a == b) return SPQ_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  s = wait_pending(c, st);
+  if (s != SPQ_OK) return s;
+  const int64_t r0 = p->host.query_join_row_off[a], r1 = p->host.query_join_row_off[b];
+  s = kv_write(c, p, layer, k, v, at<int32_t>(p, p->off_jpos) + r0, at<int64_t>(p, p->off_jslot) + r0, r1 - r0, st);
+  if (s != SPQ_OK) return s;
+  spq::AttnArgs args{};
+  TempWork tw;
+  float* opart = p->opart;
+  float* lsepart = p->lsepart;
+  const bool full = (a == 0 && b == nq);
+  DevWork w;
+  if (full) {
+    w = p->jw;
+    fill_attn(c, p, p->jw, &args);
+  } else {
+    spq::AttnWorkHost h;
+    spq::WorkOpts o{c->cfg.num_q_heads, c->cfg.head_dim, c->cfg.block_size, std::max(1, c->num_sms), false,
+                    c->cfg.dtype == SPQ_BF16};
+    spq::build_join_work(p->host, o, a, b, &h);
+    s = upload_work(c, h, st, &tw);
+    if (s != SPQ_OK) return s;
+    spq_plan tmp_view;
+    tmp_view.dbuf = tw.buf;
+    tmp_view.opart = nullptr;
+    tmp_view.lsepart = nullptr;
+    fill_attn(c, &tmp_view, tw.w, &args);
+    w = tw.w;
+  }
+  args.opart = opart;
+  args.lsepart = lsepart;
+  args.pos = at<int32_t>(p, p->off_jpos) + r0;
+  args.q = q;
+  args.o = o;
+  args.lse = lse;
+  args.layer = layer;
+  if (c->timing) CUDA_TRY(cudaEventRecord(c->ev[2], st));
+  s = run_attn(c, args, st);
+  if (s != SPQ_OK) return s;
+  if (c->timing) {
+    CUDA_TRY(cudaEventRecord(c->ev[3], st));
+    c->join_timed = true;
+  }
+  if (w.n_combine > 0) {
+    spq::CombineArgs ca{};
+    ca.desc = reinterpret_cast<const spq::CombineDesc*>((full ? p->dbuf : tw.buf) + w.combine);
+    ca.n_desc = w.n_combine;
+    ca.opart = opart;
+    ca.lsepart = lsepart;
+    ca.o = o;
+    ca.lse = lse;
+    ca.hq = c->cfg.num_q_heads;
+    ca.d = c->cfg.head_dim;
+    cudaError_t e = spq::launch_combine(ca, st);
+    if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("combine launch: ") + cudaGetErrorString(e));
+    c->launches++;
+  }
+  if (tw.buf) CUDA_TRY(cudaFreeAsync(tw.buf, st));
+  return SPQ_OK;
+}
+
+spq_status spq_plan_release(spq_ctx* c, spq_plan* p, void* stream) {
+  if (c == nullptr || p == nullptr) return fail(SPQ_EINVAL, "null argument");
+  if (p->released) return fail(SPQ_ESTATE, "plan released twice");
+  c->store->release(p->host);
+  p->released = true;
+  if (is_gpu(c)) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(cudaSetDevice(c->cfg.device));
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(e, st));
+    c->pending.push_back(e);
+    if (p->dbuf) CUDA_TRY(cudaFreeAsync(p->dbuf, st));
+    if (p->opart) CUDA_TRY(cudaFreeAsync(p->opart, st));
+    if (p->lsepart) CUDA_TRY(cudaFreeAsync(p->lsepart, st));
+  }
+  delete p;
+  return SPQ_OK;
+}
+
+spq_status spq_get_stats(const spq_ctx* c, spq_stats* out) {
+  if (c == nullptr || out == nullptr) return fail(SPQ_EINVAL, "null argument");
+  const spq::StoreStats& s = c->store->stats();
+  out->lookups = s.lookups;
+  out->hit_blocks = s.hit_blocks;
+  out->miss_blocks = s.miss_blocks;
+  out->hit_tokens = s.hit_tokens;
+  out->input_tokens = s.input_tokens;
+  out->evictions = s.evictions;
+  out->inserted_blocks = s.inserted_blocks;
+  out->resident_blocks = c->store->resident();
+  out->free_blocks = c->store->free_count();
+  out->pinned_blocks = c->store->pinned_count();
+  out->plans = c->store->plans();
+  return SPQ_OK;
+}
+
+spq_status spq_evict_all(spq_ctx* c) {
+  if (c == nullptr) return fail(SPQ_EINVAL, "null argument");
+  c->store->evict_all();
+  return SPQ_OK;
+}
+
+spq_status spq_launch_count(const spq_ctx* c, int64_t* n) {
+  if (c == nullptr || n == nullptr) return fail(SPQ_EINVAL, "null argument");
+  *n = c->launches;
+  return SPQ_OK;
+}
+
+spq_status spq_set_timing(spq_ctx* c, int32_t enable) {
+  if (c == nullptr) return fail(SPQ_EINVAL, "null argument");
+  if (!is_gpu(c)) return fail(SPQ_ESTATE, "host-only ctx");
+  c->timing = enable != 0;
+  return SPQ_OK;
+}
+
+spq_status spq_last_attn_ms(spq_ctx* c, float* prefill_ms, float* join_ms) {
+  if (c == nullptr) return fail(SPQ_EINVAL, "null argument");
+  if (!is_gpu(c)) return fail(SPQ_ESTATE, "host-only ctx");
+  if (prefill_ms) {
+    *prefill_ms = 0.f;
+    if (c->prefill_timed) CUDA_TRY(cudaEventElapsedTime(prefill_ms, c->ev[0], c->ev[1]));
+  }
+  if (join_ms) {
+    *join_ms = 0.f;
+    if (c->join_timed) CUDA_TRY(cudaEventElapsedTime(join_ms, c->ev[2], c->ev[3]));
+  }
+  return SPQ_OK;
+}
+
+}  // extern "C"

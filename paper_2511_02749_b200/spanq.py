@@ -1,0 +1,320 @@
+"""Thin Python binding of the C ABI (include/spanq.h) — argument marshalling only.
+
+Every step of the hot path runs inside libspanq.so (C++ planner/store, CUDA kernels). This
+module converts numpy arrays / torch tensors to pointers and back; it never computes any part
+of the method and has no CPU fallback: if the library is missing it raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from . import inputs as _inputs
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libspanq.so")
+_lib = None
+
+OK, EINVAL, ENOMEM, ECUDA, ENCCL, ESTATE = range(6)
+BF16, FP32 = 0, 1
+
+
+class SpanqError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"spanq status {status}: {msg}")
+        self.status = status
+
+
+class spq_config(C.Structure):
+    _fields_ = [
+        ("num_q_heads", C.c_int32), ("num_kv_heads", C.c_int32), ("head_dim", C.c_int32),
+        ("num_layers", C.c_int32), ("block_size", C.c_int32), ("num_blocks", C.c_int64),
+        ("dtype", C.c_int32), ("rope_base", C.c_double), ("max_position", C.c_int32),
+        ("model_salt", C.c_uint64), ("k_pool", C.c_void_p), ("v_pool", C.c_void_p),
+        ("device", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32),
+    ]
+
+
+class spq_node(C.Structure):
+    _fields_ = [("op", C.c_int32), ("num_children", C.c_int32), ("tok_begin", C.c_int64),
+                ("tok_len", C.c_int64)]
+
+
+class spq_query(C.Structure):
+    _fields_ = [("nodes", C.POINTER(spq_node)), ("num_nodes", C.c_int32),
+                ("tokens", C.POINTER(C.c_int32)), ("num_tokens", C.c_int64)]
+
+
+_I32P = C.POINTER(C.c_int32)
+_I64P = C.POINTER(C.c_int64)
+_U8P = C.POINTER(C.c_uint8)
+
+
+class spq_plan_view(C.Structure):
+    _fields_ = [
+        ("n_queries", C.c_int32), ("n_segments", C.c_int32), ("n_jobs", C.c_int32),
+        ("n_blocks_total", C.c_int64),
+        ("seg_query", _I32P), ("seg_kind", _I32P), ("seg_frag_idx", _I32P), ("seg_tok_len", _I32P),
+        ("seg_pos0", _I32P), ("seg_hit", _I32P), ("seg_compute_begin", _I32P),
+        ("seg_block_off", _I32P), ("seg_n_blocks", _I32P),
+        ("blocks", _I32P), ("block_write", _U8P), ("digests", _U8P), ("join_digests", _U8P),
+        ("jobs", _I32P), ("job_row_off", _I64P),
+        ("n_prefill_rows", C.c_int64), ("prefill_pos", _I32P), ("prefill_slot", _I64P),
+        ("n_join_rows", C.c_int64), ("query_join_row_off", _I64P), ("join_pos", _I32P),
+        ("join_slot", _I64P), ("n_pad_slots", C.c_int64), ("pad_slots", _I64P),
+        ("prefill_flops", C.c_double), ("join_flops", C.c_double),
+        ("prefill_kv_bytes", C.c_int64), ("join_kv_bytes", C.c_int64),
+    ]
+
+
+class spq_stats(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in (
+        "lookups", "hit_blocks", "miss_blocks", "hit_tokens", "input_tokens", "evictions",
+        "inserted_blocks", "resident_blocks", "free_blocks", "pinned_blocks", "plans")]
+
+
+# name -> (restype, argtypes) for every entry point of include/spanq.h
+SIGNATURES = {
+    "spq_create": (C.c_int, [C.POINTER(spq_config), C.POINTER(C.c_void_p)]),
+    "spq_destroy": (None, [C.c_void_p]),
+    "spq_last_error": (C.c_char_p, []),
+    "spq_version": (C.c_char_p, []),
+    "spq_block_hashes": (C.c_int, [C.c_void_p, C.POINTER(spq_query), C.c_void_p, C.c_int64, _I64P]),
+    "spq_lookup": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "spq_insert": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "spq_plan_create": (C.c_int, [C.c_void_p, C.POINTER(spq_query), C.c_int32, C.c_void_p,
+                                  C.POINTER(C.c_void_p)]),
+    "spq_plan_view_get": (C.c_int, [C.c_void_p, C.POINTER(spq_plan_view)]),
+    "spq_prefill_jobs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_void_p]),
+    "spq_join": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "spq_plan_release": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "spq_get_stats": (C.c_int, [C.c_void_p, C.POINTER(spq_stats)]),
+    "spq_evict_all": (C.c_int, [C.c_void_p]),
+    "spq_launch_count": (C.c_int, [C.c_void_p, _I64P]),
+    "spq_last_attn_ms": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+    "spq_set_timing": (C.c_int, [C.c_void_p, C.c_int32]),
+}
+
+
+def lib():
+    """Load libspanq.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise FileNotFoundError(
+                f"{_LIB_PATH} not built; run `python -m paper_2511_02749_b200.build` "
+                "(there is no CPU fallback)")
+        L = C.CDLL(_LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != OK:
+        raise SpanqError(status, lib().spq_last_error().decode())
+
+
+def _ptr(x) -> Optional[int]:
+    """torch tensor / numpy array / None -> raw address."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    return x.ctypes.data
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        return None
+    if hasattr(stream, "cuda_stream"):
+        return stream.cuda_stream
+    return int(stream)
+
+
+class _QueryBuf:
+    """Keeps the ctypes arrays of one spq_query alive."""
+
+    def __init__(self, nodes: np.ndarray, tokens: np.ndarray):
+        nodes = np.asarray(nodes, dtype=np.int64).reshape(-1, 4)
+        self.nodes = (spq_node * max(1, len(nodes)))()
+        for i, (op, nc, b, n) in enumerate(nodes):
+            self.nodes[i] = spq_node(int(op), int(nc), int(b), int(n))
+        self.tokens = np.ascontiguousarray(tokens, dtype=np.int32)
+        self.q = spq_query(C.cast(self.nodes, C.POINTER(spq_node)), len(nodes),
+                           self.tokens.ctypes.data_as(_I32P), len(self.tokens))
+
+
+def to_query(q) -> _QueryBuf:
+    if isinstance(q, _inputs.SpanQuery):
+        return _QueryBuf(*_inputs.query_to_tree(q))
+    nodes, toks = q
+    return _QueryBuf(nodes, toks)
+
+
+def _arr(ptr, n, dtype):
+    if n == 0:
+        return np.zeros(0, dtype=dtype)
+    return np.ctypeslib.as_array(ptr, shape=(n,)).astype(dtype, copy=True)
+
+
+class Plan:
+    def __init__(self, ctx: "Context", handle: int):
+        self.ctx = ctx
+        self.handle = handle
+        self.released = False
+
+    def view(self) -> Dict[str, object]:
+        v = spq_plan_view()
+        _check(lib().spq_plan_view_get(self.handle, C.byref(v)))
+        ns, nb, nq = v.n_segments, v.n_blocks_total, v.n_queries
+        out = dict(
+            n_queries=nq, n_segments=ns, n_jobs=v.n_jobs,
+            seg_query=_arr(v.seg_query, ns, np.int32), seg_kind=_arr(v.seg_kind, ns, np.int32),
+            seg_frag_idx=_arr(v.seg_frag_idx, ns, np.int32),
+            seg_tok_len=_arr(v.seg_tok_len, ns, np.int32), seg_pos0=_arr(v.seg_pos0, ns, np.int32),
+            seg_hit=_arr(v.seg_hit, ns, np.int32),
+            seg_compute_begin=_arr(v.seg_compute_begin, ns, np.int32),
+            seg_block_off=_arr(v.seg_block_off, ns, np.int32),
+            seg_n_blocks=_arr(v.seg_n_blocks, ns, np.int32),
+            blocks=_arr(v.blocks, nb, np.int32), block_write=_arr(v.block_write, nb, np.uint8),
+            digests=_arr(v.digests, nb * 16, np.uint8).reshape(nb, 16),
+            join_digests=_arr(v.join_digests, nq * 16, np.uint8).reshape(nq, 16),
+            jobs=_arr(v.jobs, v.n_jobs, np.int32),
+            job_row_off=_arr(v.job_row_off, v.n_jobs + 1, np.int64),
+            prefill_pos=_arr(v.prefill_pos, v.n_prefill_rows, np.int32),
+            prefill_slot=_arr(v.prefill_slot, v.n_prefill_rows, np.int64),
+            query_join_row_off=_arr(v.query_join_row_off, nq + 1, np.int64),
+            join_pos=_arr(v.join_pos, v.n_join_rows, np.int32),
+            join_slot=_arr(v.join_slot, v.n_join_rows, np.int64),
+            pad_slots=_arr(v.pad_slots, v.n_pad_slots, np.int64),
+            prefill_flops=v.prefill_flops, join_flops=v.join_flops,
+            prefill_kv_bytes=v.prefill_kv_bytes, join_kv_bytes=v.join_kv_bytes,
+        )
+        return out
+
+    def prefill(self, layer, q, k, v, o, lse=None, jobs=None, stream=None):
+        a, b = (0, self.view_n_jobs()) if jobs is None else jobs
+        _check(lib().spq_prefill_jobs(self.ctx.handle, self.handle, layer, a, b, _ptr(q), _ptr(k),
+                                      _ptr(v), _ptr(o), _ptr(lse), _stream_ptr(stream)))
+
+    def join(self, layer, q, k, v, o, lse=None, queries=None, stream=None):
+        a, b = (0, self.n_queries) if queries is None else queries
+        _check(lib().spq_join(self.ctx.handle, self.handle, layer, a, b, _ptr(q), _ptr(k), _ptr(v),
+                              _ptr(o), _ptr(lse), _stream_ptr(stream)))
+
+    def view_n_jobs(self) -> int:
+        v = spq_plan_view()
+        _check(lib().spq_plan_view_get(self.handle, C.byref(v)))
+        return v.n_jobs
+
+    @property
+    def n_queries(self) -> int:
+        v = spq_plan_view()
+        _check(lib().spq_plan_view_get(self.handle, C.byref(v)))
+        return v.n_queries
+
+    def release(self, stream=None):
+        if not self.released:
+            _check(lib().spq_plan_release(self.ctx.handle, self.handle, _stream_ptr(stream)))
+            self.released = True
+
+
+class Context:
+    """One ctx per GPU (or host-only with device=-1: planner and store only).
+
+    For a GPU ctx the KV pools are allocated here with torch (caller-owned memory in ABI terms):
+    k_pool/v_pool [L, num_blocks, Hkv, bs, d].
+    """
+
+    def __init__(self, shape: _inputs.Shape, num_blocks: int, device: int = 0,
+                 max_position: int = 1 << 15, pools=None):
+        self.shape = shape
+        self.device = device
+        self.num_blocks = num_blocks
+        self.k_pool = self.v_pool = None
+        if device >= 0:
+            import torch
+
+            dt = torch.bfloat16 if shape.dtype == "bf16" else torch.float32
+            if pools is None:
+                sz = (shape.layers, num_blocks, shape.hkv, shape.block_size, shape.d)
+                self.k_pool = torch.zeros(sz, dtype=dt, device=f"cuda:{device}")
+                self.v_pool = torch.zeros(sz, dtype=dt, device=f"cuda:{device}")
+            else:
+                self.k_pool, self.v_pool = pools
+        cfg = spq_config(shape.hq, shape.hkv, shape.d, shape.layers, shape.block_size, num_blocks,
+                         BF16 if shape.dtype == "bf16" else FP32, float(shape.rope_base),
+                         int(max_position), int(shape.model_salt), _ptr(self.k_pool),
+                         _ptr(self.v_pool), device, 0, 1)
+        h = C.c_void_p()
+        _check(lib().spq_create(C.byref(cfg), C.byref(h)))
+        self.handle = h.value
+
+    def close(self):
+        if self.handle:
+            lib().spq_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def plan(self, queries: Sequence, stream=None) -> Plan:
+        bufs = [to_query(q) for q in queries]
+        arr = (spq_query * len(bufs))(*[b.q for b in bufs])
+        h = C.c_void_p()
+        _check(lib().spq_plan_create(self.handle, arr, len(bufs), _stream_ptr(stream), C.byref(h)))
+        return Plan(self, h.value)
+
+    def block_hashes(self, query) -> np.ndarray:
+        b = to_query(query)
+        n = C.c_int64()
+        cap = 1 << 16
+        out = np.zeros((cap, 16), np.uint8)
+        _check(lib().spq_block_hashes(self.handle, C.byref(b.q), out.ctypes.data, cap, C.byref(n)))
+        return out[: n.value].copy()
+
+    def lookup(self, digests: np.ndarray) -> np.ndarray:
+        d = np.ascontiguousarray(digests, dtype=np.uint8).reshape(-1, 16)
+        ids = np.zeros(len(d), np.int32)
+        _check(lib().spq_lookup(self.handle, d.ctypes.data, len(d), ids.ctypes.data))
+        return ids
+
+    def insert(self, digests: np.ndarray, ntok: Sequence[int]) -> np.ndarray:
+        d = np.ascontiguousarray(digests, dtype=np.uint8).reshape(-1, 16)
+        nt = np.ascontiguousarray(ntok, dtype=np.int32)
+        ids = np.zeros(len(d), np.int32)
+        _check(lib().spq_insert(self.handle, d.ctypes.data, nt.ctypes.data, len(d), ids.ctypes.data))
+        return ids
+
+    def stats(self) -> Dict[str, int]:
+        s = spq_stats()
+        _check(lib().spq_get_stats(self.handle, C.byref(s)))
+        return {n: getattr(s, n) for n, _ in spq_stats._fields_}
+
+    def evict_all(self):
+        _check(lib().spq_evict_all(self.handle))
+
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        _check(lib().spq_launch_count(self.handle, C.byref(n)))
+        return n.value
+
+    def set_timing(self, on: bool):
+        _check(lib().spq_set_timing(self.handle, 1 if on else 0))
+
+    def last_attn_ms(self):
+        a, b = C.c_float(), C.c_float()
+        _check(lib().spq_last_attn_ms(self.handle, C.byref(a), C.byref(b)))
+        return a.value, b.value
