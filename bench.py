@@ -1,0 +1,317 @@
+#!/usr/bin/env python
+"""Benchmark: span-query prefill TTFT and attention TFLOP/s at the 8B GQA shape (BASELINE.json).
+
+One step = one pass of the whole hot path over one RAG span query of configs[1] (C2: 512-token
+prefix + 16 commutative fragments x 1024 + 256-token question, Hq 32 / Hkv 8 / d 128, bf16,
+block 64, COLD cache): spq_plan_create (tree normalisation, BLAKE2b chains, lookup/alloc,
+work lists, one H2D) -> spq_prefill_jobs (rope_kv_write + block-diagonal tcgen05 attention)
+-> spq_join (rope_kv_write + split-KV join attention + combine). The store is emptied before
+every step (cold cache) outside the timed region, and L2 is flushed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Under torchrun each rank runs its own query (weak scaling, no data-path collective: the
+queries are independent units), time = max over ranks, value = all ranks' FLOPs / that time.
+`--impl reference` times the CPU oracle (the reference arm of this tier) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "span-query prefill TTFT (ms) & attention TFLOP/s at 8B GQA shape, 1/2/4/8 B200"
+UNIT = "TFLOP/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["bf16_tflops"], p.get("bf16_tflops_sustained"), p["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v.lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(budget_s: float = 15.0):
+    """The fp64 oracle (as it stands) on a bounded sample of C2: fragment jobs one by one and
+    then join rows in chunks until the time budget is spent; TFLOP/s = algorithmic FLOPs of the
+    sampled work / CPU time."""
+    from oracle import attention as oatt
+    from paper_2511_02749_b200 import inputs
+
+    try:
+        from threadpoolctl import threadpool_info
+
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        threads = os.cpu_count()
+    w = inputs.c2()
+    s = w.shape
+    eq, ek, ev = inputs.layer_tables(s, 0, w.seed)
+    q = w.queries[0]
+    t0 = time.perf_counter()
+    flops = 0.0
+    nfr = 0
+    for f in q.fragments:
+        oatt.segment_causal(f, eq, ek, ev, s.rope_base)
+        L = len(f)
+        flops += 4.0 * s.d * s.hq * L * (L + 1) / 2
+        nfr += 1
+        if time.perf_counter() - t0 > budget_s * 0.6:
+            break
+    rows_done = 0
+    N = q.n_tokens
+    P_S = N - len(q.cross)
+    for r0 in range(0, len(q.cross), 32):
+        rows = np.arange(r0, min(r0 + 32, len(q.cross)))
+        oatt.join_rows(q.prefix, q.fragments, q.cross, eq, ek, ev, s.rope_base, rows)
+        flops += 4.0 * s.d * s.hq * float(np.sum(P_S + rows + 1))
+        rows_done += len(rows)
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": flops / dt / 1e12, "unit": UNIT, "cores": int(threads), "kind": "oracle",
+            "sample": f"C2 fp64 oracle: {nfr}/16 fragment prefills + {rows_done}/256 join rows, all 32 heads, "
+                      f"{dt:.1f} s on {os.cpu_count()} host cpus"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    res = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(budget_s=max(2.0, 60.0 / (args.warmup + args.steps)))
+        if i >= args.warmup:
+            res.append(cb)
+    v = statistics.median(r["value"] for r in res)
+    cb = dict(res[-1])
+    cb["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C2 RAG span query (configs[1]) bounded CPU sample",
+                       "global_batch": 1, "seq_len": 17152, "parallelism": "cpu oracle"},
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="spanq", choices=["spanq", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--out-dtype", default="fp32", choices=["fp32", "bf16"])
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2511_02749_b200 import inputs, runner, spanq
+
+    w = inputs.c2(seed=2 + rank)  # each rank: its own independent query (weak scaling)
+    s = w.shape
+    ctx = spanq.Context(s, 512, device=local, max_position=1 << 15, out_dtype=args.out_dtype)
+    stream = torch.cuda.Stream(dev)
+    tab = runner.device_tables(s, 0, w.seed, dev)
+    # stage this query's packed q/k/v rows once (resident in HBM during the timed region)
+    p0 = ctx.plan(w.queries, stream=stream)
+    view = p0.view()
+    ptok, jtok = runner.prefill_tokens(view, w.queries), runner.join_tokens(view, w.queries)
+    qp, kp, vp = runner.gather(tab, ptok, dev)
+    qj, kj, vj = runner.gather(tab, jtok, dev)
+    odt = torch.float32 if args.out_dtype == "fp32" else torch.bfloat16
+    op = torch.empty((len(ptok), s.hq, s.d), dtype=odt, device=dev)
+    lp = torch.empty((len(ptok), s.hq), dtype=torch.float32, device=dev)
+    oj = torch.empty((len(jtok), s.hq, s.d), dtype=odt, device=dev)
+    lj = torch.empty((len(jtok), s.hq), dtype=torch.float32, device=dev)
+    p0.release(stream=stream)
+    flops = view["prefill_flops"] + view["join_flops"]
+    kv_bytes = view["prefill_kv_bytes"] + view["join_kv_bytes"]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step(timing_events=None):
+        ctx.evict_all()  # cold cache
+        plan = ctx.plan(w.queries, stream=stream)
+        plan.prefill(0, qp, kp, vp, op, lp, stream=stream)
+        plan.join(0, qj, kj, vj, oj, lj, stream=stream)
+        plan.release(stream=stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        # ---- timed region: K steps, events on the launching stream, L2 flushed between steps
+        ctx.set_timing(True)
+        n0 = ctx.launch_count()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        attn_ms = []
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            for i in range(args.steps):
+                flush.zero_()
+                ev[i][0].record(stream)
+                step()
+                ev[i][1].record(stream)
+                stream.synchronize()
+                attn_ms.append(ctx.last_attn_ms())
+        torch.cuda.synchronize()
+        launches = ctx.launch_count() - n0
+        ctx.set_timing(False)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * flops * args.steps / (total_ms / 1e3) / 1e12
+
+    # ---- e2e through the public API with host buffers: H2D of the step's inputs (pinned) and
+    # D2H of the step's result (join O + LSE) inside the timed region
+    hq = [t.cpu().pin_memory() for t in (qp, kp, vp, qj, kj, vj)]
+    h2d = sum(t.numel() * t.element_size() for t in hq)
+    oj_h = torch.empty(oj.shape, dtype=oj.dtype).pin_memory()
+    lj_h = torch.empty(lj.shape, dtype=lj.dtype).pin_memory()
+    d2h = oj_h.numel() * oj_h.element_size() + lj_h.numel() * lj_h.element_size()
+    dq = [torch.empty_like(t, device=dev) for t in hq]
+    e2e_ms = []
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup + args.steps):
+            flush.zero_()
+            stream.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for d_, h_ in zip(dq, hq):
+                d_.copy_(h_, non_blocking=True)
+            ctx.evict_all()
+            plan = ctx.plan(w.queries, stream=stream)
+            plan.prefill(0, dq[0], dq[1], dq[2], op, lp, stream=stream)
+            plan.join(0, dq[3], dq[4], dq[5], oj, lj, stream=stream)
+            oj_h.copy_(oj, non_blocking=True)
+            lj_h.copy_(lj, non_blocking=True)
+            plan.release(stream=stream)
+            b.record(stream)
+            stream.synchronize()
+            if i >= args.warmup:
+                e2e_ms.append(a.elapsed_time(b))
+    e2e_total = float(sum(e2e_ms))
+    if world > 1:
+        t = torch.tensor([e2e_total], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = world * flops * args.steps / (e2e_total / 1e3) / 1e12
+
+    peak_burst, peak_sust, hbm, peak_src = peaks()
+    pre_ms = statistics.median(a for a, _ in attn_ms)
+    join_ms = statistics.median(b for _, b in attn_ms)
+    achieved = view["prefill_flops"] / (pre_ms / 1e3) / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "C2 RAG span query (configs[1]): P512 + 16x1024 plus-fragments + 256 cross, cold cache",
+                   "model": "8B GQA attention shape Hq32/Hkv8/d128, 1 layer, random tables",
+                   "global_batch": world, "seq_len": int(view["prefill_flops"] > 0) and 17152,
+                   "block_size": s.block_size, "out_dtype": args.out_dtype,
+                   "parallelism": f"dp{world} (independent queries per rank)",
+                   "l2": "flushed between steps (256 MB write)"},
+        "ttft_ms": ms_per_step,
+        "step_ms_p50": statistics.median(step_ms), "step_ms_p99": float(np.percentile(step_ms, 99)),
+        "flops_per_step": flops,
+        "roofline": {"kernel": "span_attn_tc (fragment+prefix prefill, K2)", "bound": "tensor",
+                     "achieved": achieved, "peak": peak_burst, "unit": "TFLOP/s",
+                     "frac": achieved / peak_burst, "traffic": None,
+                     "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)" if peak_src == "measured" else "fallback",
+                     "kernel_ms": pre_ms, "algorithmic_flops": view["prefill_flops"]},
+        "join_kernel": {"kernel": "span_attn_tc (join, K3)", "ms": join_ms,
+                        "achieved": view["join_flops"] / (join_ms / 1e3) / 1e12 if join_ms > 0 else None,
+                        "frac": (view["join_flops"] / (join_ms / 1e3) / 1e12) / peak_burst if join_ms > 0 else None},
+        "kv_write_bytes_per_step": kv_bytes,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": e2e_total / args.steps},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -17,8 +17,8 @@
  *  - Every call returns spq_status; no exception crosses the ABI. On failure the message is
  *    available from spq_last_error() (thread-local, valid until the next failing call on
  *    the same thread).
- *  - Layouts are row-major. Activations: q [rows, Hq, d], k/v [rows, Hkv, d], o [rows, Hq, d]
- *    in the ctx dtype (bf16 = IEEE bfloat16 bit patterns, or fp32), lse [rows, Hq] fp32 natural
+ *  - Layouts are row-major. Activations: q [rows, Hq, d], k/v [rows, Hkv, d] in the ctx dtype,
+ *    o [rows, Hq, d] in cfg.out_dtype (bf16 = IEEE bfloat16 bit patterns, or fp32), lse [rows, Hq] fp32 natural
  *    log. KV pools: [num_layers][num_blocks][Hkv][block_size][d] in the ctx dtype; slot
  *    s = block_id * block_size + offset addresses one token row of one block.
  *  - A ctx is single-writer (not thread-safe); plans execute in stream order.
@@ -46,7 +46,7 @@ typedef enum { SPQ_BF16 = 0, SPQ_FP32 = 1 } spq_dtype;
 typedef struct {
   int32_t num_q_heads;  /* Hq  (multiple of Hkv; GQA q-head h uses kv-head h / (Hq/Hkv))    */
   int32_t num_kv_heads; /* Hkv                                                               */
-  int32_t head_dim;     /* d: 64 or 128 for SPQ_BF16; any multiple of 32 <= 256 for SPQ_FP32 */
+  int32_t head_dim;     /* d: 64 or 128 on the GPU (either dtype); any >= 2 for host-only ctx */
   int32_t num_layers;   /* L                                                                 */
   int32_t block_size;   /* bs tokens per KV block: 16/32/64/128 on the GPU; any >=1
                            for host-only contexts                                            */
@@ -60,6 +60,8 @@ typedef struct {
   int32_t device;       /* CUDA device ordinal; -1 = host-only ctx (planner/store, no kernels) */
   int32_t rank;         /* reserved (multi-GPU): this rank, 0..world_size-1                  */
   int32_t world_size;   /* reserved (multi-GPU): must be 1 in this version                   */
+  int32_t out_dtype;    /* spq_dtype of o (attention outputs); SPQ_FP32 is allowed with a bf16
+                           ctx (bf16 MMAs, fp32 outputs: removes the final bf16 rounding of O)  */
 } spq_config;
 
 typedef struct spq_ctx spq_ctx;

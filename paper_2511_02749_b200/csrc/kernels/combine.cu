@@ -14,11 +14,18 @@
 namespace spq {
 namespace {
 
-template <int D>
+__device__ __forceinline__ void store2(__nv_bfloat16* p, float a, float b) {
+  *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(a, b);
+}
+__device__ __forceinline__ void store2(float* p, float a, float b) {
+  *reinterpret_cast<float2*>(p) = make_float2(a, b);
+}
+
+template <int D, typename TO>
 __global__ void __launch_bounds__(256) combine_kernel(const CombineDesc* __restrict__ desc,
                                                       const float* __restrict__ opart,
                                                       const float* __restrict__ lsepart,
-                                                      __nv_bfloat16* __restrict__ o,
+                                                      TO* __restrict__ o,
                                                       float* __restrict__ lse, int hq) {
   constexpr int E = D / 32;  // columns per lane
   const CombineDesc cd = desc[blockIdx.x];
@@ -47,31 +54,29 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineDesc* __restr
     }
     const float inv = 1.f / tot;
     const int64_t row = cd.row0 + r;
-    __nv_bfloat16* dst = o + (row * hq + h) * D + lane * E;
+    TO* dst = o + (row * hq + h) * D + lane * E;
 #pragma unroll
-    for (int e = 0; e < E; e += 2)
-      *reinterpret_cast<__nv_bfloat162*>(dst + e) = __floats2bfloat162_rn(acc[e] * inv, acc[e + 1] * inv);
+    for (int e = 0; e < E; e += 2) store2(dst + e, acc[e] * inv, acc[e + 1] * inv);
     if (lse != nullptr && lane == 0) lse[row * hq + h] = m + logf(tot);
   }
 }
 
 }  // namespace
 
+template <int D, typename TO>
+void launch_dt(const CombineArgs& a, cudaStream_t st) {
+  dim3 grid(a.n_desc, a.hq);
+  combine_kernel<D, TO><<<grid, 256, 0, st>>>(a.desc, a.opart, a.lsepart, static_cast<TO*>(a.o), a.lse, a.hq);
+}
+
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
   if (a.n_desc == 0) return cudaSuccess;
-  dim3 grid(a.n_desc, a.hq);
-  switch (a.d) {
-    case 64:
-      combine_kernel<64><<<grid, 256, 0, st>>>(a.desc, a.opart, a.lsepart,
-                                                static_cast<__nv_bfloat16*>(a.o), a.lse, a.hq);
-      break;
-    case 128:
-      combine_kernel<128><<<grid, 256, 0, st>>>(a.desc, a.opart, a.lsepart,
-                                                 static_cast<__nv_bfloat16*>(a.o), a.lse, a.hq);
-      break;
-    default:
-      return cudaErrorInvalidValue;
-  }
+  if (a.d == 64)
+    a.out_fp32 ? launch_dt<64, float>(a, st) : launch_dt<64, __nv_bfloat16>(a, st);
+  else if (a.d == 128)
+    a.out_fp32 ? launch_dt<128, float>(a, st) : launch_dt<128, __nv_bfloat16>(a, st);
+  else
+    return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 

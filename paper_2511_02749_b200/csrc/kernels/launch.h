@@ -53,6 +53,7 @@ struct AttnArgs {
   int layer;
   const float2* rope;
   int max_pos;
+  bool out_fp32;  // o is fp32 (else ctx dtype)
 };
 cudaError_t launch_span_attn_tc(const AttnArgs& a, cudaStream_t st);   // bf16 tcgen05
 cudaError_t launch_span_attn_f32(const AttnArgs& a, cudaStream_t st);  // fp32 SIMT
@@ -65,6 +66,7 @@ struct CombineArgs {
   void* o;
   float* lse;
   int hq, d;
+  bool out_fp32;
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);
 

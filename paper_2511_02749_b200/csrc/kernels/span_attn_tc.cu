@@ -263,7 +263,13 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
       tmem_ld32(ocol + c * 32, v);
       tmem_wait_ld();
       if (valid) {
-        if (w.part < 0) {
+        if (w.part < 0 && a.out_fp32) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(a.o) + (row * a.hq + h) * D + c * 32);
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            dst[u] = make_float4(__uint_as_float(v[4 * u]) * inv, __uint_as_float(v[4 * u + 1]) * inv,
+                                 __uint_as_float(v[4 * u + 2]) * inv, __uint_as_float(v[4 * u + 3]) * inv);
+        } else if (w.part < 0) {
           uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.o) +
                                                 (row * a.hq + h) * D + c * 32);
 #pragma unroll

@@ -169,6 +169,7 @@ void fill_attn(spq_ctx* c, const spq_plan* p, const DevWork& w, spq::AttnArgs* a
   a->max_pos = c->cfg.max_position;
   a->opart = p->opart;
   a->lsepart = p->lsepart;
+  a->out_fp32 = c->cfg.out_dtype == SPQ_FP32;
 }
 
 spq_status run_attn(spq_ctx* c, const spq::AttnArgs& a, cudaStream_t st) {
@@ -253,6 +254,8 @@ spq_status spq_create(const spq_config* cfg, spq_ctx** out) {
   if (g.num_layers <= 0 || g.block_size <= 0 || g.num_blocks <= 0 || g.num_blocks > INT32_MAX)
     return fail(SPQ_EINVAL, "bad layers/block_size/num_blocks");
   if (g.dtype != SPQ_BF16 && g.dtype != SPQ_FP32) return fail(SPQ_EINVAL, "bad dtype");
+  if (g.out_dtype != SPQ_BF16 && g.out_dtype != SPQ_FP32) return fail(SPQ_EINVAL, "bad out_dtype");
+  if (g.dtype == SPQ_FP32 && g.out_dtype != SPQ_FP32) return fail(SPQ_EINVAL, "fp32 ctx needs fp32 outputs");
   if (g.world_size != 1 || g.rank != 0) return fail(SPQ_EINVAL, "world_size must be 1 in this version");
   if (g.max_position <= 0 || !(g.rope_base > 0)) return fail(SPQ_EINVAL, "bad rope parameters");
   std::unique_ptr<spq_ctx> c(new spq_ctx());
@@ -605,6 +608,7 @@ spq_status spq_join(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b
     ca.lse = lse;
     ca.hq = c->cfg.num_q_heads;
     ca.d = c->cfg.head_dim;
+    ca.out_fp32 = c->cfg.out_dtype == SPQ_FP32;
     cudaError_t e = spq::launch_combine(ca, st);
     if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("combine launch: ") + cudaGetErrorString(e));
     c->launches++;

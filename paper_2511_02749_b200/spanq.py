@@ -34,6 +34,7 @@ class spq_config(C.Structure):
         ("dtype", C.c_int32), ("rope_base", C.c_double), ("max_position", C.c_int32),
         ("model_salt", C.c_uint64), ("k_pool", C.c_void_p), ("v_pool", C.c_void_p),
         ("device", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32),
+        ("out_dtype", C.c_int32),
     ]
 
 
@@ -236,11 +237,12 @@ class Context:
     """
 
     def __init__(self, shape: _inputs.Shape, num_blocks: int, device: int = 0,
-                 max_position: int = 1 << 15, pools=None):
+                 max_position: int = 1 << 15, pools=None, out_dtype: Optional[str] = None):
         self.shape = shape
         self.device = device
         self.num_blocks = num_blocks
         self.k_pool = self.v_pool = None
+        self.out_dtype = out_dtype or shape.dtype
         if device >= 0:
             import torch
 
@@ -254,7 +256,8 @@ class Context:
         cfg = spq_config(shape.hq, shape.hkv, shape.d, shape.layers, shape.block_size, num_blocks,
                          BF16 if shape.dtype == "bf16" else FP32, float(shape.rope_base),
                          int(max_position), int(shape.model_salt), _ptr(self.k_pool),
-                         _ptr(self.v_pool), device, 0, 1)
+                         _ptr(self.v_pool), device, 0, 1,
+                         BF16 if self.out_dtype == "bf16" else FP32)
         h = C.c_void_p()
         _check(lib().spq_create(C.byref(cfg), C.byref(h)))
         self.handle = h.value
