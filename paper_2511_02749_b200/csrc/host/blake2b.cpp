@@ -34,16 +34,28 @@ inline uint64_t load64(const uint8_t* p) {
   return v;
 }
 
-inline void mix(uint64_t* v, int a, int b, int c, int d, uint64_t x, uint64_t y) {
-  v[a] = v[a] + v[b] + x;
-  v[d] = rotr(v[d] ^ v[a], 32);
-  v[c] = v[c] + v[d];
-  v[b] = rotr(v[b] ^ v[c], 24);
-  v[a] = v[a] + v[b] + y;
-  v[d] = rotr(v[d] ^ v[a], 16);
-  v[c] = v[c] + v[d];
-  v[b] = rotr(v[b] ^ v[c], 63);
-}
+#define SPQ_G(r, i, a, b, c, d)                 \
+  do {                                          \
+    v[a] = v[a] + v[b] + m[kSigma[r][2 * i]];     \
+    v[d] = rotr(v[d] ^ v[a], 32);               \
+    v[c] = v[c] + v[d];                         \
+    v[b] = rotr(v[b] ^ v[c], 24);               \
+    v[a] = v[a] + v[b] + m[kSigma[r][2 * i + 1]]; \
+    v[d] = rotr(v[d] ^ v[a], 16);               \
+    v[c] = v[c] + v[d];                         \
+    v[b] = rotr(v[b] ^ v[c], 63);               \
+  } while (0)
+#define SPQ_ROUND(r)                 \
+  do {                               \
+    SPQ_G(r, 0, 0, 4, 8, 12);        \
+    SPQ_G(r, 1, 1, 5, 9, 13);        \
+    SPQ_G(r, 2, 2, 6, 10, 14);       \
+    SPQ_G(r, 3, 3, 7, 11, 15);       \
+    SPQ_G(r, 4, 0, 5, 10, 15);       \
+    SPQ_G(r, 5, 1, 6, 11, 12);       \
+    SPQ_G(r, 6, 2, 7, 8, 13);        \
+    SPQ_G(r, 7, 3, 4, 9, 14);        \
+  } while (0)
 
 void compress(uint64_t* h, const uint8_t* block, uint64_t t_lo, uint64_t t_hi, bool last) {
   uint64_t m[16], v[16];
@@ -55,19 +67,23 @@ void compress(uint64_t* h, const uint8_t* block, uint64_t t_lo, uint64_t t_hi, b
   v[12] ^= t_lo;
   v[13] ^= t_hi;
   if (last) v[14] = ~v[14];
-  for (int r = 0; r < 12; ++r) {
-    const uint8_t* s = kSigma[r];
-    mix(v, 0, 4, 8, 12, m[s[0]], m[s[1]]);
-    mix(v, 1, 5, 9, 13, m[s[2]], m[s[3]]);
-    mix(v, 2, 6, 10, 14, m[s[4]], m[s[5]]);
-    mix(v, 3, 7, 11, 15, m[s[6]], m[s[7]]);
-    mix(v, 0, 5, 10, 15, m[s[8]], m[s[9]]);
-    mix(v, 1, 6, 11, 12, m[s[10]], m[s[11]]);
-    mix(v, 2, 7, 8, 13, m[s[12]], m[s[13]]);
-    mix(v, 3, 4, 9, 14, m[s[14]], m[s[15]]);
-  }
+  // 12 rounds, fully unrolled with compile-time message schedule (RFC 7693 §3.2)
+  SPQ_ROUND(0);
+  SPQ_ROUND(1);
+  SPQ_ROUND(2);
+  SPQ_ROUND(3);
+  SPQ_ROUND(4);
+  SPQ_ROUND(5);
+  SPQ_ROUND(6);
+  SPQ_ROUND(7);
+  SPQ_ROUND(8);
+  SPQ_ROUND(9);
+  SPQ_ROUND(10);
+  SPQ_ROUND(11);
   for (int i = 0; i < 8; ++i) h[i] ^= v[i] ^ v[i + 8];
 }
+#undef SPQ_ROUND
+#undef SPQ_G
 
 }  // namespace
 

@@ -134,17 +134,16 @@ Digest root_digest(int hq, int hkv, int d, int bs, double rope_base, uint64_t sa
 
 void chain(char tag, const Digest& seed, const int32_t* tok, int64_t n, int bs,
            std::vector<Digest>* out) {
+  // message = tag ‖ prev digest ‖ u32 n ‖ n × u32 token (little-endian host)
+  std::vector<uint8_t> buf(1 + 16 + 4 + 4 * static_cast<size_t>(bs));
+  buf[0] = static_cast<uint8_t>(tag);
   Digest prev = seed;
-  std::vector<uint8_t> buf;
-  buf.reserve(1 + 16 + 4 + 4 * bs);
   for (int64_t s = 0; s < n; s += bs) {
-    const int64_t m = std::min<int64_t>(bs, n - s);
-    buf.clear();
-    buf.push_back(static_cast<uint8_t>(tag));
-    buf.insert(buf.end(), prev.b, prev.b + 16);
-    put_u32(&buf, static_cast<uint32_t>(m));
-    for (int64_t t = 0; t < m; ++t) put_u32(&buf, static_cast<uint32_t>(tok[s + t]));
-    prev = b2(buf);
+    const uint32_t m = static_cast<uint32_t>(std::min<int64_t>(bs, n - s));
+    std::memcpy(buf.data() + 1, prev.b, 16);
+    std::memcpy(buf.data() + 17, &m, 4);
+    std::memcpy(buf.data() + 21, tok + s, 4 * static_cast<size_t>(m));
+    blake2b(prev.b, 16, buf.data(), 21 + 4 * static_cast<size_t>(m));
     out->push_back(prev);
   }
 }
@@ -249,7 +248,56 @@ void Store::rollback() {
   journal_.clear();
 }
 
-int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out) {
+namespace {
+struct QueryDigests {
+  std::vector<Digest> prefix, cross;
+  std::vector<std::vector<Digest>> frags;
+  Digest join;
+};
+
+void hash_all(const std::vector<FlatQuery>& qs, int bs, const Digest& root, ThreadPool* pool,
+              std::vector<QueryDigests>* out) {
+  out->assign(qs.size(), QueryDigests());
+  std::vector<std::pair<int32_t, int32_t>> tasks;  // (query, -1 prefix | fragment index)
+  int64_t ntok = 0;
+  for (size_t q = 0; q < qs.size(); ++q) {
+    (*out)[q].frags.resize(qs[q].frags.size());
+    tasks.push_back({static_cast<int32_t>(q), -1});
+    ntok += static_cast<int64_t>(qs[q].prefix.size() + qs[q].cross.size());
+    for (size_t f = 0; f < qs[q].frags.size(); ++f) {
+      tasks.push_back({static_cast<int32_t>(q), static_cast<int32_t>(f)});
+      ntok += static_cast<int64_t>(qs[q].frags[f].size());
+    }
+  }
+  const bool par = pool != nullptr && ntok >= 4096;
+  std::function<void(int64_t)> chains = [&](int64_t i) {
+    const auto [q, f] = tasks[i];
+    if (f < 0)
+      chain('P', root, qs[q].prefix.data(), static_cast<int64_t>(qs[q].prefix.size()), bs, &(*out)[q].prefix);
+    else
+      chain('F', root, qs[q].frags[f].data(), static_cast<int64_t>(qs[q].frags[f].size()), bs,
+            &(*out)[q].frags[f]);
+  };
+  std::function<void(int64_t)> crosses = [&](int64_t q) {
+    QueryDigests& d = (*out)[q];
+    std::vector<Digest> lasts;
+    for (const auto& f : d.frags) lasts.push_back(f.back());
+    d.join = join_fold(d.prefix.empty() ? root : d.prefix.back(), lasts);
+    chain('X', d.join, qs[q].cross.data(), static_cast<int64_t>(qs[q].cross.size()), bs, &d.cross);
+  };
+  if (par) {
+    pool->parallel_for(static_cast<int64_t>(tasks.size()), chains);
+    pool->parallel_for(static_cast<int64_t>(qs.size()), crosses);
+  } else {
+    for (size_t i = 0; i < tasks.size(); ++i) chains(static_cast<int64_t>(i));
+    for (size_t q = 0; q < qs.size(); ++q) crosses(static_cast<int64_t>(q));
+  }
+}
+}  // namespace
+
+int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* pool) {
+  std::vector<QueryDigests> qd;
+  hash_all(qs, bs_, root_, pool, &qd);
   const StoreStats saved_stats = stats_;
   const int64_t saved_plan = plan_no_;
   journal_.clear();
@@ -303,8 +351,7 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out) {
     stats_.input_tokens += ntot;
     // ---- prefix: chained digests + prefix scan; partial tail plan-private (R9)
     const int32_t plen = static_cast<int32_t>(q.prefix.size());
-    dig.clear();
-    chain('P', root_, q.prefix.data(), plen, bs, &dig);
+    dig = qd[qi].prefix;
     blocks.clear();
     wr.clear();
     bool hit_run = true;
@@ -343,13 +390,10 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out) {
     const Digest h_last = dig.empty() ? root_ : dig.back();
     // ---- fragments: suspended chains, all-or-nothing lookup (R10, R11)
     int32_t off = plen;
-    std::vector<Digest> lasts;
     for (size_t fi = 0; fi < q.frags.size() && ok; ++fi) {
       const auto& f = q.frags[fi];
       const int32_t flen = static_cast<int32_t>(f.size());
-      dig.clear();
-      chain('F', root_, f.data(), flen, bs, &dig);
-      lasts.push_back(dig.back());
+      dig = qd[qi].frags[fi];
       stats_.lookups++;
       std::vector<int32_t> res(dig.size());
       bool all = true;
@@ -386,12 +430,12 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out) {
       off += flen;
     }
     if (!ok) break;
-    const Digest J = join_fold(h_last, lasts);
+    (void)h_last;
+    const Digest J = qd[qi].join;
     P.join_digests.push_back(J);
     // ---- cross: always computed; full blocks under the X chain (R9)
     const int32_t clen = static_cast<int32_t>(q.cross.size());
-    dig.clear();
-    chain('X', J, q.cross.data(), clen, bs, &dig);
+    dig = qd[qi].cross;
     blocks.clear();
     wr.clear();
     for (size_t i = 0; i < dig.size() && ok; ++i) {

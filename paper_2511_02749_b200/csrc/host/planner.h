@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "blake2b.h"
+#include "thread_pool.h"
 
 #include "../../../include/spanq.h"
 
@@ -69,8 +70,9 @@ class Store {
  public:
   Store(int64_t num_blocks, int block_size, const Digest& root);
 
-  // Plan a batch. Returns 0 on success, 2 on ENOMEM (state rolled back).
-  int plan(const std::vector<FlatQuery>& qs, PlanHost* out);
+  // Plan a batch. Returns 0 on success, 2 on ENOMEM (state rolled back). Block digests do
+  // not depend on store state, so they are computed first, in parallel on `pool` if given.
+  int plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* pool = nullptr);
   void release(const PlanHost& p);
   void evict_all();
   int32_t lookup(const Digest& d) const;

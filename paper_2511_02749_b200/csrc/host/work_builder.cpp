@@ -2,8 +2,7 @@
 #include "work_builder.h"
 
 #include <algorithm>
-#include <queue>
-#include <tuple>
+#include <cmath>
 
 namespace spq {
 namespace {
@@ -28,51 +27,32 @@ int32_t add_tiles(const PlanHost& p, const Segment& s, int bs, int32_t key_base,
   return first;
 }
 
-struct Pair {
-  double cost;
-  int32_t item, head;
-};
-
-// Longest-processing-time-first assignment of (item, head) pairs to `grid` persistent CTAs.
+// Static schedule of (item, head) pairs over `grid` persistent CTAs: pairs sorted by cost
+// (longest first, heads of one item adjacent so a KV head's tiles are reused from L2), dealt in
+// boustrophedon waves (0..grid-1, grid-1..0, ...) — O(pairs), close to LPT for sorted costs.
 void schedule(const std::vector<double>& item_cost, int hq, int num_sms, AttnWorkHost* w) {
-  std::vector<Pair> pairs;
-  pairs.reserve(item_cost.size() * hq);
-  for (size_t i = 0; i < item_cost.size(); ++i)
-    for (int h = 0; h < hq; ++h) pairs.push_back({item_cost[i], static_cast<int32_t>(i), h});
-  std::stable_sort(pairs.begin(), pairs.end(), [](const Pair& a, const Pair& b) { return a.cost > b.cost; });
-  const int grid = static_cast<int>(std::min<size_t>(num_sms, std::max<size_t>(1, pairs.size())));
-  std::vector<std::vector<int32_t>> lists(grid);
-  using Load = std::pair<double, int>;
-  std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
-  for (int c = 0; c < grid; ++c) heap.push({0.0, c});
-  for (const Pair& pr : pairs) {
-    Load l = heap.top();
-    heap.pop();
-    lists[l.second].push_back(pr.item * hq + pr.head);
-    heap.push({l.first + pr.cost, l.second});
+  std::vector<int32_t> order(item_cost.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int32_t>(i);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int32_t a, int32_t b) { return item_cost[a] > item_cost[b]; });
+  const size_t pairs = item_cost.size() * static_cast<size_t>(hq);
+  const int grid = static_cast<int>(std::min<size_t>(num_sms, std::max<size_t>(1, pairs)));
+  std::vector<int32_t> count(grid, 0);
+  std::vector<int32_t> bin_of(pairs);
+  for (size_t i = 0; i < pairs; ++i) {
+    const size_t wave = i / grid, pos = i % grid;
+    const int b = static_cast<int>((wave & 1) ? grid - 1 - pos : pos);
+    bin_of[i] = b;
+    count[b]++;
   }
   w->grid = grid;
-  w->cta_off.assign(1, 0);
-  w->cta_items.clear();
-  for (int c = 0; c < grid; ++c) {
-    w->cta_items.insert(w->cta_items.end(), lists[c].begin(), lists[c].end());
-    w->cta_off.push_back(static_cast<int32_t>(w->cta_items.size()));
-  }
-}
-
-double lpt_makespan(std::vector<double> costs, int hq, int num_sms) {
-  std::sort(costs.begin(), costs.end(), std::greater<double>());
-  std::priority_queue<double, std::vector<double>, std::greater<double>> heap;
-  for (int c = 0; c < num_sms; ++c) heap.push(0.0);
-  double mk = 0;
-  for (double c : costs)
-    for (int h = 0; h < hq; ++h) {
-      double l = heap.top() + c;
-      heap.pop();
-      heap.push(l);
-      mk = std::max(mk, l);
-    }
-  return mk;
+  w->cta_off.assign(grid + 1, 0);
+  for (int c = 0; c < grid; ++c) w->cta_off[c + 1] = w->cta_off[c] + count[c];
+  w->cta_items.assign(pairs, 0);
+  std::vector<int32_t> fill(w->cta_off.begin(), w->cta_off.end() - 1);
+  size_t i = 0;
+  for (int32_t it : order)
+    for (int h = 0; h < hq; ++h, ++i) w->cta_items[fill[bin_of[i]]++] = it * hq + h;
 }
 
 constexpr double kItemOverhead = 1.0;   // q-prep + epilogue, in KV-tile units
@@ -139,24 +119,25 @@ void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_en
     for (int32_t j = 0; j < c.tok_len; ++j) w->flops += before + j + 1;
   }
   w->flops *= 4.0 * o.d * o.hq;
-  // choose the split count K (same for all q tiles, capped by each tile count) by LPT makespan
+  // choose the split count K (same for all q tiles, capped by each tile count): minimise the
+  // wave-quantised makespan ceil(pairs / SMs) * (largest chunk cost) — closed form, O(K·tiles)
   int best_k = 1;
   if (o.allow_split && !qt.empty()) {
-    const size_t pairs = qt.size() * static_cast<size_t>(o.hq);
-    if (pairs < static_cast<size_t>(4 * o.num_sms)) {
+    const size_t pairs1 = qt.size() * static_cast<size_t>(o.hq);
+    if (pairs1 < static_cast<size_t>(4 * o.num_sms)) {
       double best = 1e300;
       int max_n = 0;
       for (const QTile& q : qt) max_n = std::max(max_n, q.te - q.tb);
       for (int k = 1; k <= std::min(64, max_n); ++k) {
-        std::vector<double> costs;
+        size_t items = 0;
+        double cmax = 0;
         for (const QTile& q : qt) {
           const int n = q.te - q.tb, kk = std::min(k, n);
-          for (int s = 0; s < kk; ++s) {
-            const int a = q.tb + (n * s) / kk, b = q.tb + (n * (s + 1)) / kk;
-            costs.push_back(b - a + kItemOverhead + (kk > 1 ? kSplitOverhead : 0.0));
-          }
+          items += kk;
+          cmax = std::max(cmax, (n + kk - 1) / kk + kItemOverhead + (kk > 1 ? kSplitOverhead : 0.0));
         }
-        const double mk = lpt_makespan(costs, o.hq, o.num_sms);
+        const double waves = std::ceil(static_cast<double>(items * o.hq) / o.num_sms);
+        const double mk = waves * cmax;
         if (mk < best * 0.98) {
           best = mk;
           best_k = k;

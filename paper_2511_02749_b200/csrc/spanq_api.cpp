@@ -10,11 +10,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/spanq.h"
@@ -68,6 +71,7 @@ struct DevWork {  // offsets of one attention work list inside a plan buffer
 struct spq_ctx {
   spq_config cfg;
   std::unique_ptr<spq::Store> store;
+  std::unique_ptr<spq::ThreadPool> pool;  // host planning (block hashing)
   int num_sms = 0;
   float2* rope = nullptr;  // device [max_position][d/2]
   CUtensorMap tmk, tmv;
@@ -260,6 +264,10 @@ spq_status spq_create(const spq_config* cfg, spq_ctx** out) {
   if (g.max_position <= 0 || !(g.rope_base > 0)) return fail(SPQ_EINVAL, "bad rope parameters");
   std::unique_ptr<spq_ctx> c(new spq_ctx());
   c->cfg = g;
+  {
+    const unsigned hw = std::thread::hardware_concurrency();
+    c->pool.reset(new spq::ThreadPool(static_cast<int>(std::min(15u, hw > 1 ? hw - 1 : 0u))));
+  }
   c->store.reset(new spq::Store(g.num_blocks, g.block_size,
                                 spq::root_digest(g.num_q_heads, g.num_kv_heads, g.head_dim, g.block_size,
                                                  g.rope_base, g.model_salt)));
@@ -373,6 +381,16 @@ spq_status spq_insert(spq_ctx* c, const uint8_t* digests, const int32_t* ntok, i
 spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queries, void* stream, spq_plan** out) {
   if (c == nullptr || out == nullptr || (n_queries > 0 && queries == nullptr)) return fail(SPQ_EINVAL, "null argument");
   if (n_queries <= 0) return fail(SPQ_EINVAL, "n_queries must be >= 1");
+  using clk = std::chrono::steady_clock;
+  static const bool prof = std::getenv("SPANQ_PROFILE") != nullptr;
+  auto t0 = clk::now();
+  auto lap = [&](const char* what) {
+    if (!prof) return;
+    auto t = clk::now();
+    std::fprintf(stderr, "[spanq] plan_create %-12s %8.1f us\n", what,
+                 std::chrono::duration<double, std::micro>(t - t0).count());
+    t0 = t;
+  };
   std::vector<spq::FlatQuery> fq(n_queries);
   for (int32_t i = 0; i < n_queries; ++i) {
     std::string err;
@@ -383,8 +401,10 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
     if (n > c->cfg.max_position)
       return fail(SPQ_EINVAL, "query " + std::to_string(i) + " exceeds max_position");
   }
+  lap("normalize");
   std::unique_ptr<spq_plan> p(new spq_plan());
-  if (c->store->plan(fq, &p->host) != 0) return fail(SPQ_ENOMEM, "block pool cannot hold the plan (rolled back)");
+  if (c->store->plan(fq, &p->host, c->pool.get()) != 0) return fail(SPQ_ENOMEM, "block pool cannot hold the plan (rolled back)");
+  lap("store.plan");
   const spq::PlanHost& H = p->host;
   for (const spq::Segment& s : H.segs) {
     p->seg_query.push_back(s.query);
@@ -400,10 +420,14 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
   for (const auto& d : H.digests) p->digests.insert(p->digests.end(), d.b, d.b + 16);
   for (const auto& d : H.join_digests) p->join_digests.insert(p->join_digests.end(), d.b, d.b + 16);
   p->padded_layers.assign(c->cfg.num_layers, 0);
-  spq::WorkOpts o{c->cfg.num_q_heads, c->cfg.head_dim, c->cfg.block_size, std::max(1, c->num_sms),
+  // host-only contexts plan for a B200 (148 SMs) so their work lists match a GPU ctx's
+  spq::WorkOpts o{c->cfg.num_q_heads, c->cfg.head_dim, c->cfg.block_size, c->num_sms > 0 ? c->num_sms : 148,
                   c->cfg.dtype == SPQ_BF16, c->cfg.dtype == SPQ_BF16};
+  lap("view arrays");
   spq::build_prefill_work(H, o, 0, static_cast<int>(H.jobs.size()), &p->pw_host);
+  lap("prefill work");
   spq::build_join_work(H, o, 0, H.n_queries, &p->jw_host);
+  lap("join work");
   p->prefill_flops = p->pw_host.flops;
   p->join_flops = p->jw_host.flops;
   // algorithmic bytes of rope_kv_write: per written row, read k,v and write both pages
@@ -411,6 +435,7 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
   const int64_t row_bytes = 4LL * c->cfg.num_kv_heads * c->cfg.head_dim * elt_size(c);
   for (int64_t s : H.prefill_slot) p->prefill_kv_bytes += 12 + (s >= 0 ? row_bytes : 0);
   for (int64_t s : H.join_slot) p->join_kv_bytes += 12 + (s >= 0 ? row_bytes : 0);
+  lap("flops/bytes");
   if (is_gpu(c)) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     CUDA_TRY(cudaSetDevice(c->cfg.device));
@@ -454,6 +479,7 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
       CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->opart), rows * c->cfg.head_dim * sizeof(float), st));
       CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->lsepart), rows * sizeof(float), st));
     }
+    lap("upload");
   }
   *out = p.release();
   return SPQ_OK;

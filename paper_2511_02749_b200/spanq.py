@@ -172,6 +172,9 @@ class Plan:
         self.ctx = ctx
         self.handle = handle
         self.released = False
+        v = spq_plan_view()
+        _check(lib().spq_plan_view_get(self.handle, C.byref(v)))
+        self.n_jobs, self.n_queries = v.n_jobs, v.n_queries
 
     def view(self) -> Dict[str, object]:
         v = spq_plan_view()
@@ -203,7 +206,7 @@ class Plan:
         return out
 
     def prefill(self, layer, q, k, v, o, lse=None, jobs=None, stream=None):
-        a, b = (0, self.view_n_jobs()) if jobs is None else jobs
+        a, b = (0, self.n_jobs) if jobs is None else jobs
         _check(lib().spq_prefill_jobs(self.ctx.handle, self.handle, layer, a, b, _ptr(q), _ptr(k),
                                       _ptr(v), _ptr(o), _ptr(lse), _stream_ptr(stream)))
 
@@ -211,17 +214,6 @@ class Plan:
         a, b = (0, self.n_queries) if queries is None else queries
         _check(lib().spq_join(self.ctx.handle, self.handle, layer, a, b, _ptr(q), _ptr(k), _ptr(v),
                               _ptr(o), _ptr(lse), _stream_ptr(stream)))
-
-    def view_n_jobs(self) -> int:
-        v = spq_plan_view()
-        _check(lib().spq_plan_view_get(self.handle, C.byref(v)))
-        return v.n_jobs
-
-    @property
-    def n_queries(self) -> int:
-        v = spq_plan_view()
-        _check(lib().spq_plan_view_get(self.handle, C.byref(v)))
-        return v.n_queries
 
     def release(self, stream=None):
         if not self.released:
