@@ -31,7 +31,8 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineDesc* __restr
   const CombineDesc cd = desc[blockIdx.x];
   const int h = blockIdx.y;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  for (int r = warp; r < cd.n_rows; r += blockDim.x / 32) {
+  // grid.z splits the 128 rows of a tile into groups of blockDim/32 rows: one warp per row
+  for (int r = blockIdx.z * (blockDim.x / 32) + warp; r < cd.n_rows; r += gridDim.z * (blockDim.x / 32)) {
     float m = -INFINITY;
     for (int s = 0; s < cd.n_split; ++s)
       m = fmaxf(m, lsepart[(static_cast<int64_t>(cd.part_base + s) * hq + h) * kTileRows + r]);
@@ -65,7 +66,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineDesc* __restr
 
 template <int D, typename TO>
 void launch_dt(const CombineArgs& a, cudaStream_t st) {
-  dim3 grid(a.n_desc, a.hq);
+  dim3 grid(a.n_desc, a.hq, kTileRows / 8);
   combine_kernel<D, TO><<<grid, 256, 0, st>>>(a.desc, a.opart, a.lsepart, static_cast<TO*>(a.o), a.lse, a.hq);
 }
 

@@ -98,13 +98,14 @@ __global__ void __launch_bounds__(256) rope_kv_write_kernel(
       const int p = pos[r];
       const bool first_half = g < G / 2;
       const int i0 = (first_half ? g : g - G / 2) * N;  // pair index of element 0
-      const float2* cs = rope + static_cast<int64_t>(p) * (D / 2) + i0;
+      const float4* cs = reinterpret_cast<const float4*>(rope + static_cast<int64_t>(p) * (D / 2) + i0);
       float out[N];
 #pragma unroll
-      for (int e = 0; e < N; ++e) {
-        const float2 c = __ldg(cs + e);
+      for (int e = 0; e < N; e += 2) {
+        const float4 c = __ldg(cs + e / 2);  // (cos, sin) of pairs i0+e, i0+e+1
         // first half: x*cos - partner*sin ; second half: x*cos + partner*sin
         out[e] = first_half ? fmaf(x[e], c.x, -y[e] * c.y) : fmaf(x[e], c.x, y[e] * c.y);
+        out[e + 1] = first_half ? fmaf(x[e + 1], c.z, -y[e + 1] * c.w) : fmaf(x[e + 1], c.z, y[e + 1] * c.w);
       }
       const int64_t blk = s / bs, off = s % bs;
       const int64_t dst = layer_off + ((blk * hkv + h) * bs + off) * D + g * N;

@@ -190,17 +190,28 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
       const uint32_t scol = tmem + lane_base + kColS0 + sb * 128;
       mbar_wait(&S.s_full[sb], (st >> 1) & 1);
       tc_fence_after();
-      // pass 1: row max
-      float mx = -INFINITY;
+      // pass 1: row max — 8 independent accumulators (no 128-long dependency chain); the
+      // per-key mask is only evaluated when some row of the warp sees a partial tile
+      const bool full = __all_sync(0xffffffffu, lim >= kTileKeys - 1);
+      float mx8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t v[32];
         tmem_ld32(scol + c * 32, v);
         tmem_wait_ld();
+        if (full) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c * 32 + i <= lim) mx = fmaxf(mx, __uint_as_float(v[i]));
+          for (int i = 0; i < 32; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v[i]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c * 32 + i <= lim) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v[i]));
+        }
       }
+      float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       mx *= sl2;
       const float m_new = fmaxf(m, mx);
       const bool resc = m_new > m + kRescaleThreshold;
@@ -208,7 +219,9 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
       const float alpha = resc ? ex2_approx(m - m_new) : 1.f;
       const float msub = (m_use == -INFINITY) ? 0.f : m_use;
       // pass 2: P = exp2(s*scale - m), packed bf16 over the first 64 columns of S
-      float sum = 0.f;
+      float sum8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sum8[i] = 0.f;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t v[32];
@@ -218,13 +231,19 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int j0 = c * 32 + 2 * i;
-          const float p0 = (j0 <= lim) ? ex2_approx(fmaf(__uint_as_float(v[2 * i]), sl2, -msub)) : 0.f;
-          const float p1 = (j0 + 1 <= lim) ? ex2_approx(fmaf(__uint_as_float(v[2 * i + 1]), sl2, -msub)) : 0.f;
-          sum += p0 + p1;
+          float p0 = ex2_approx(fmaf(__uint_as_float(v[2 * i]), sl2, -msub));
+          float p1 = ex2_approx(fmaf(__uint_as_float(v[2 * i + 1]), sl2, -msub));
+          if (!full) {
+            p0 = (j0 <= lim) ? p0 : 0.f;
+            p1 = (j0 + 1 <= lim) ? p1 : 0.f;
+          }
+          sum8[(2 * i) & 7] += p0;
+          sum8[(2 * i + 1) & 7] += p1;
           pk[i] = pack_bf16x2(p0, p1);
         }
         tmem_st16(scol + c * 16, pk);
       }
+      const float sum = ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) + ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
       tmem_wait_st();
       l = l * alpha + sum;
       if (k > 0) {
@@ -326,30 +345,41 @@ __device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_
       uint8_t* qs_base = &S.q[qb][0][0];
       const int rp = min(max(p - rot, 0), a.max_pos - 1);
       const float4* cs = reinterpret_cast<const float4*>(a.rope + static_cast<int64_t>(rp) * (D / 2));
-#pragma unroll 2
-      for (int g = 0; g < D / 16; ++g) {  // 8 rotate-half pairs per step
-        const int i0 = g * 8;
-        uint4 o1 = make_uint4(0, 0, 0, 0), o2 = make_uint4(0, 0, 0, 0);
-        if (valid) {
-          const uint4 u1 = *reinterpret_cast<const uint4*>(qrow + i0);
-          const uint4 u2 = *reinterpret_cast<const uint4*>(qrow + D / 2 + i0);
-          const __nv_bfloat162* b1 = reinterpret_cast<const __nv_bfloat162*>(&u1);
-          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u2);
+      // issue every q load of the row first (latency is paid once), then the cos/sin table in
+      // batches of 8 pairs interleaved with the rotate + swizzled stores
+      uint4 q1[D / 16], q2[D / 16];
+#pragma unroll
+      for (int g = 0; g < D / 16; ++g) {
+        q1[g] = valid ? __ldg(reinterpret_cast<const uint4*>(qrow + g * 8)) : make_uint4(0, 0, 0, 0);
+        q2[g] = valid ? __ldg(reinterpret_cast<const uint4*>(qrow + D / 2 + g * 8)) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int g0 = 0; g0 < D / 16; g0 += 2) {
+        float4 cst[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) cst[e] = valid ? __ldg(cs + g0 * 4 + e) : make_float4(1.f, 0.f, 1.f, 0.f);
+#pragma unroll
+        for (int gg = 0; gg < 2; ++gg) {
+          const int g = g0 + gg;
+          const int i0 = g * 8;
+          uint4 o1, o2;
+          const __nv_bfloat162* b1 = reinterpret_cast<const __nv_bfloat162*>(&q1[g]);
+          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q2[g]);
           uint32_t* w1 = reinterpret_cast<uint32_t*>(&o1);
           uint32_t* w2 = reinterpret_cast<uint32_t*>(&o2);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float4 c = __ldg(cs + (i0 / 2) + e);  // (cos,sin) of pairs i0+2e, i0+2e+1
+            const float4 c = cst[gg * 4 + e];  // (cos,sin) of pairs i0+2e, i0+2e+1
             const float2 x1 = __bfloat1622float2(b1[e]), x2 = __bfloat1622float2(b2[e]);
             w1[e] = pack_bf16x2(x1.x * c.x - x2.x * c.y, x1.y * c.z - x2.y * c.w);
             w2[e] = pack_bf16x2(x2.x * c.x + x1.x * c.y, x2.y * c.z + x1.y * c.w);
           }
+          const int e1 = i0, e2 = D / 2 + i0;
+          *reinterpret_cast<uint4*>(qs_base + (e1 / 64) * TcSmem<D>::kChunkBytes + r * 128 +
+                                    ((((e1 % 64) / 8) ^ (r & 7)) * 16)) = o1;
+          *reinterpret_cast<uint4*>(qs_base + (e2 / 64) * TcSmem<D>::kChunkBytes + r * 128 +
+                                    ((((e2 % 64) / 8) ^ (r & 7)) * 16)) = o2;
         }
-        const int e1 = i0, e2 = D / 2 + i0;
-        *reinterpret_cast<uint4*>(qs_base + (e1 / 64) * TcSmem<D>::kChunkBytes + r * 128 +
-                                  ((((e1 % 64) / 8) ^ (r & 7)) * 16)) = o1;
-        *reinterpret_cast<uint4*>(qs_base + (e2 / 64) * TcSmem<D>::kChunkBytes + r * 128 +
-                                  ((((e2 % 64) / 8) ^ (r & 7)) * 16)) = o2;
       }
       fence_proxy_async_smem();
       mbar_arrive(&S.q_full[qb]);

@@ -286,6 +286,12 @@ spq_status spq_create(const spq_config* cfg, spq_ctx** out) {
       return fail(SPQ_ECUDA, "device is sm_" + std::to_string(prop.major) + std::to_string(prop.minor) +
                                  "; this library is built for sm_100a only");
     c->num_sms = prop.multiProcessorCount;
+    // plans allocate their device arrays with cudaMallocAsync: keep freed memory in the pool
+    // (the default threshold 0 returns it at every sync and re-maps it on the next plan)
+    cudaMemPool_t mp;
+    CUDA_TRY(cudaDeviceGetDefaultMemPool(&mp, g.device));
+    uint64_t thr = UINT64_MAX;
+    CUDA_TRY(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr));
     // RoPE table from fp64: cos/sin(p * base^(-2i/d)) rounded once to fp32
     const int half = g.head_dim / 2;
     std::vector<float2> tab(static_cast<size_t>(g.max_position) * half);

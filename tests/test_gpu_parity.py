@@ -40,9 +40,9 @@ def check(got, exp, fp32, what, abs_tol=BF16_MAX_ABS, bf16_out=False):
     return d.max(), rel
 
 
-def check_lse(got, exp, fp32, what):
+def check_lse(got, exp, fp32, what, scale=1.0):
     g = _np(got)
-    tol = FP32_MAX_ABS * 10 if fp32 else 2e-2
+    tol = FP32_MAX_ABS * 10 if fp32 else 2e-2 * scale
     err = np.abs(g - exp).max() if exp.size else 0.0
     assert err <= tol, f"{what}: lse max abs {err:.3e}"
 
@@ -76,10 +76,10 @@ def run_and_check(w, cuda_dev, nblk=4096, check_pages=True, out_dtype="fp32", ab
     if len(ov.jobs):
         eo, el = oatt.plan_prefill_expected(ov, qs, eq, ek, ev, s.rope_base)
         check(res.o_prefill, eo, fp32, f"{w.name} prefill O", abs_tol, bo)
-        check_lse(res.lse_prefill, el, fp32, f"{w.name} prefill LSE")
+        check_lse(res.lse_prefill, el, fp32, f"{w.name} prefill LSE", abs_tol / BF16_MAX_ABS)
     jo, jl = oatt.plan_join_expected(ov, qs, eq, ek, ev, s.rope_base)
     out = check(res.o_join, jo, fp32, f"{w.name} join O", abs_tol, bo)
-    check_lse(res.lse_join, jl, fp32, f"{w.name} join LSE")
+    check_lse(res.lse_join, jl, fp32, f"{w.name} join LSE", abs_tol / BF16_MAX_ABS)
     if check_pages:
         kp, vp = _np(ctx.k_pool[0]), _np(ctx.v_pool[0])
         kp = kp.transpose(0, 2, 1, 3).reshape(-1, s.hkv, s.d)  # [blk*bs, hkv, d]
