@@ -84,7 +84,7 @@ void build_prefill_work(const PlanHost& p, const WorkOpts& o, int job_begin, int
     for (int64_t i = s.compute_begin; i < s.tok_len; ++i) w->flops += static_cast<double>(i + 1);
   }
   w->flops *= 4.0 * o.d * o.hq;
-  if (o.persistent) schedule(cost, o.hq, o.num_sms, w);
+  if (o.persistent) schedule(cost, o.units, o.num_sms, w);
 }
 
 void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_end, AttnWorkHost* w) {
@@ -123,7 +123,7 @@ void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_en
   // wave-quantised makespan ceil(pairs / SMs) * (largest chunk cost) — closed form, O(K·tiles)
   int best_k = 1;
   if (o.allow_split && !qt.empty()) {
-    const size_t pairs1 = qt.size() * static_cast<size_t>(o.hq);
+    const size_t pairs1 = qt.size() * static_cast<size_t>(o.units);
     if (pairs1 < static_cast<size_t>(4 * o.num_sms)) {
       double best = 1e300;
       int max_n = 0;
@@ -136,7 +136,7 @@ void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_en
           items += kk;
           cmax = std::max(cmax, (n + kk - 1) / kk + kItemOverhead + (kk > 1 ? kSplitOverhead : 0.0));
         }
-        const double waves = std::ceil(static_cast<double>(items * o.hq) / o.num_sms);
+        const double waves = std::ceil(static_cast<double>(items * o.units) / o.num_sms);
         const double mk = waves * cmax;
         if (mk < best * 0.98) {
           best = mk;
@@ -161,7 +161,7 @@ void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_en
     }
     if (kk > 1) w->n_parts += kk;
   }
-  if (o.persistent) schedule(cost, o.hq, o.num_sms, w);
+  if (o.persistent) schedule(cost, o.units, o.num_sms, w);
 }
 
 }  // namespace spq

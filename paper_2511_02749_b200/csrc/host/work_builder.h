@@ -13,7 +13,7 @@ struct AttnWorkHost {
   std::vector<int32_t> tile_blocks;
   std::vector<WorkItem> items;
   std::vector<int32_t> cta_off;    // [grid+1]
-  std::vector<int32_t> cta_items;  // item * Hq + head, per CTA in execution order
+  std::vector<int32_t> cta_items;  // item * units + unit, per CTA in execution order
   std::vector<CombineDesc> combine;
   int32_t n_parts = 0;
   int32_t grid = 0;
@@ -25,6 +25,7 @@ struct WorkOpts {
   int num_sms;       // persistent grid upper bound
   bool allow_split;  // split-KV (join only)
   bool persistent;   // build per-CTA LPT lists
+  int units;         // work units per item: hq (one head each) or hq/2 (GQA head pairs)
 };
 
 // Prefill jobs [job_begin, job_end): rows relative to job_row_off[job_begin].

@@ -48,12 +48,17 @@ struct AttnArgs {
   const void* v_pool;
   const CUtensorMap* tmap_k;  // host copies (bf16 path)
   const CUtensorMap* tmap_v;
+  const CUtensorMap* tmap_q;  // per call: q [rows][hq][d] as 3D {d, hq, rows}, box {64, 1, 128}
   int hq, hkv, d, bs;
   int64_t nblk;
   int layer;
   const float2* rope;
   int max_pos;
   bool out_fp32;  // o is fp32 (else ctx dtype)
+  bool paired;    // tcgen05 path: work codes are (item, GQA head pair) — see span_attn_tc.cu
+  int poly_mask;  // tcgen05 path: share of exp2 on the FMA pipe, in quarters (0..4)
+  float rescale_threshold;  // tcgen05 path: conditional O rescale threshold (log2 units, 8)
+  long long* dbg_trace;     // profiling only: CTA-0 event timeline (null = off)
 };
 cudaError_t launch_span_attn_tc(const AttnArgs& a, cudaStream_t st);   // bf16 tcgen05
 cudaError_t launch_span_attn_f32(const AttnArgs& a, cudaStream_t st);  // fp32 SIMT

@@ -1,35 +1,44 @@
 // span_attn_tc.cu — K2/K3: span-masked flash attention over the paged KV pool on sm_100a
 // tensor cores (SURVEY §8(a) a6 fragment/prefix prefill and a7 join).
 //
-// Semantics (work.h): for each (work item, q head) — up to 128 query rows — stream the item's
-// KV tiles; q of row r is rotated to pos[r] - rot_delta of the tile's segment (fragment KV is
-// cached at span-local positions and never touched: the join counter-rotates Q by Δ_f instead,
-// "ReRoPE" P:610 done on the query side), keys are masked by n_valid and, in causal tiles,
-// key_pos0 + t > pos[r] (block-diagonal fragment attention). O, LSE are written final
-// (bf16, natural log) or as fp32 split-KV partials merged by combine.cu.
+// Semantics (work.h): for each work unit — up to 128 query rows x one q head (or the two q
+// heads of a GQA pair) — stream the item's KV tiles; q of row r is rotated to pos[r] - rot_delta
+// of the tile's segment (fragment KV is cached at span-local positions and never touched: the
+// join counter-rotates Q by Δ_f instead, "ReRoPE" P:610 done on the query side), keys are
+// masked by n_valid and, in causal tiles, key_pos0 + t > pos[r] (block-diagonal fragment
+// attention). O, LSE are written final or as fp32 split-KV partials (combine.cu).
 //
-// B200 design (one persistent CTA per SM, 384 threads, ~193 KB smem, 512 TMEM columns):
-//   warp 0      TMA producer: K and V tiles of 128 keys = 128/bs pool blocks, SWIZZLE_128B boxes
-//               {64 cols, bs rows} from one 2D tensor map over the whole pool (block id -> row);
-//               2-stage ring, separate K/V full/empty mbarriers.
-//   warp 1      MMA issuer (one thread): S = Q K^T (kind::f16 SS, M=N=128, fp32 in TMEM,
-//               double-buffered S at cols 0/128), then O += P V with P read from TMEM (TS form,
-//               bf16 P aliased over its S columns) and V as an MN-major smem operand; order
-//               S_j, PV_{j-1}, S_{j+1}, ... so softmax of tile j overlaps both MMAs.
-//   warps 4-7   softmax/epilogue (thread = row, TMEM lane = row): two TMEM passes (max, then
-//               exp2 + pack + tcgen05.st of P), conditional O rescale only when the running
-//               max grows by > 8 (log2 units) — P stays <= 256, exact after normalisation —
-//               then the epilogue (tcgen05.ld O, 1/l, store).
-//   warps 8-11  Q prep: load pre-RoPE q rows, rotate (fp64-built cos/sin table), write the
-//               SWIZZLE_128B K-major Q tile, double-buffered, re-done when rot_delta changes.
+// B200 design — one persistent CTA per SM, 512 threads, ~225 KB smem, 512 TMEM columns:
+//   * the two q heads h, h+1 of a GQA group share every K/V tile, so one CTA runs them as two
+//     M=128 Q tiles (A, B) against the same TMA-loaded K/V (half the K/V traffic per FLOP)
+//     and ping-pongs them: per KV tile the MMA warp issues PV_A(j-1), S_A(j), PV_B(j-1),
+//     S_B(j), so softmax A(j) overlaps PV_B(j-1)+S_B(j) on the tensor core and vice versa.
+//   * TMEM: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512) (fp32); P (bf16) is written
+//     over the first 64 columns of its S tile and consumed by the TS-form MMA (A from TMEM).
+//     PV_x(j-1) is issued before S_x(j), so when softmax x sees S_x(j) its O_x is stable and
+//     the (rare) rescale needs no extra barrier.
+//   * K/V: a TMA ring (K_j, V_j alternate; 4 slots at d=128, 8 at d=64), SWIZZLE_128B boxes
+//     {64 cols, bs rows} from one 2D tensor map over the whole pool (block id -> row): the
+//     paged gather is done by TMA; K_{j+1} is issued >= 1 tile ahead of its S MMA.
+//   * Q: a 3-slot ring prepared by a dedicated warpgroup (load pre-RoPE q, rotate with the
+//     fp64-built fp32 cos/sin table, write the SWIZZLE_128B K-major tile). An epoch (a work item
+//     or a change of rot_delta) takes slots (2e mod 3, 2e+1 mod 3): head A's tile goes to the
+//     slot left free, head B's to the slot of the previous epoch's A, released right after the
+//     last S_A MMA of that epoch, so both preps overlap the previous epoch's MMAs.
+//   * softmax (one warpgroup per Q tile, thread = row = TMEM lane): two TMEM passes (8-way max,
+//     then exp2 + pack + tcgen05.st), a fixed share of the exponentials on the FMA pipe
+//     (degree-3 Cody-Waite polynomial, rel. error 1e-4 < bf16) to relieve the MUFU, and O
+//     rescaled only when the running max grows by > 8 (log2) so P stays <= 256.
 // Descriptor bit layouts and the TS / MN-major operand forms were validated on the B200 by
 // tools/tc_probe.cu before use.
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 
 #include "launch.h"
 #include "sm100.cuh"
@@ -37,28 +46,37 @@
 namespace spq {
 namespace {
 
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kColS0 = 0, kColO = 256;
-constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr uint32_t kColS = 0, kColO = 256;  // S_x at kColS + 128x, O_x at kColO + 128x
 
 template <int D>
 struct TcSmem {
   static constexpr int kChunks = D / 64;
   static constexpr int kChunkBytes = 128 * 128;  // 128 rows x 128 B
-  alignas(1024) uint8_t q[2][kChunks][kChunkBytes];
-  alignas(1024) uint8_t k[2][kChunks][kChunkBytes];
-  alignas(1024) uint8_t v[2][kChunks][kChunkBytes];
-  uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
-  uint64_t s_full[2], p_full[2], q_full[2], q_empty[2], o_done;
+  static constexpr int kKvSlots = D == 64 ? 6 : 3;
+  static constexpr int kQSlots = 3;
+  alignas(1024) uint8_t q[kQSlots][kChunks][kChunkBytes];
+  alignas(1024) uint8_t kv[kKvSlots][kChunks][kChunkBytes];  // ring: K_0 V_0 K_1 V_1 ...
+  alignas(1024) float stage[8][32 * 32];                       // epilogue transpose, per softmax warp
+  uint64_t kv_full[kKvSlots], kv_empty[kKvSlots];
+  uint64_t q_full[3], q_empty[3], q_load[3];
+  uint64_t s_full[2], p_full[2], o_full[2];
   uint32_t tmem_base;
 };
 
 struct TcParams {
   CUtensorMap tmk;
   CUtensorMap tmv;
+  CUtensorMap tmq;
   AttnArgs a;
   float scale_log2;
+  int paired;     // 1: a unit is a GQA head pair (A = 2u, B = 2u+1); 0: one head (B idle)
+  int poly_mask;  // pair i of a 32-key chunk uses the FMA-pipe exp2 when (i & 3) < poly_mask
+  float rescale_threshold;  // log2 units; O is rescaled when the running max grows by more
+  int dbg_mode;  // profiling only: 1 = softmax does no math, 2 = max pass only,
+                 // 3 = 1 + K/V always from the first block (L2-resident), 4 = 1 + MMA skips K/V waits,
+                 // 5 = 1 + Q prep does no work
 };
 
 template <int D>
@@ -66,40 +84,71 @@ __device__ __forceinline__ TcSmem<D>& smem_ref(uint8_t* raw) {
   return *reinterpret_cast<TcSmem<D>*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
 }
 
+// profiling only: CTA 0 records (event, clock) pairs per role; 1024 events per role
+__device__ __forceinline__ void trace(const TcParams& P, int role, uint32_t& cnt, int ev) {
+  if (P.a.dbg_trace == nullptr || blockIdx.x != 0 || cnt >= 1024) return;
+  long long* t = P.a.dbg_trace + (role * 1024 + cnt) * 2;
+  t[0] = ev;
+  t[1] = clock64();
+  ++cnt;
+}
+
+struct Unit {
+  WorkItem w;
+  int head_a, n_heads;
+};
+
+__device__ __forceinline__ Unit decode(const TcParams& P, int code) {
+  Unit u;
+  const int units = P.paired ? P.a.hq / 2 : P.a.hq;
+  u.w = P.a.items[code / units];
+  const int x = code % units;
+  u.head_a = P.paired ? 2 * x : x;
+  u.n_heads = P.paired ? 2 : 1;
+  return u;
+}
+
+// exp2 on the FMA pipe: x = n + f, n = rint(x) via the 1.5*2^23 trick, 2^f by a degree-3
+// polynomial on [-0.5, 0.5] (max rel. error 1.0e-4), exponent added in the integer domain.
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -120.f);
+  const float t = x + 12582912.f;
+  const float n = t - 12582912.f;
+  const float f = x - n;
+  const float p = fmaf(fmaf(fmaf(0.05500831f, f, 0.24220964f), f, 0.69328305f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+
 // ------------------------------------------------------------------ warp 0: TMA producer
 template <int D>
 __device__ void run_producer(const TcParams& P, TcSmem<D>& S, int it_begin, int it_end) {
   const AttnArgs& a = P.a;
+  constexpr int kSlots = TcSmem<D>::kKvSlots;
   const int group = a.hq / a.hkv;
   const int bpt = kTileKeys / a.bs;
-  constexpr uint32_t kStageBytes = 128 * D * 2;
+  constexpr uint32_t kTileBytes = 128 * D * 2;
   const int64_t layer_rows = static_cast<int64_t>(a.layer) * a.nblk * a.hkv * a.bs;
-  uint32_t kt = 0;
+  uint32_t n = 0;  // load index: K_j = 2j, V_j = 2j+1 over the CTA's whole tile sequence
+  uint32_t tc = 0;
   for (int ii = it_begin; ii < it_end; ++ii) {
-    const int code = a.cta_items[ii];
-    const WorkItem w = a.items[code / a.hq];
-    const int kvh = (code % a.hq) / group;
-    for (int t = w.tile_begin; t < w.tile_end; ++t, ++kt) {
-      const int stage = kt & 1;
-      const uint32_t ph = (kt >> 1) & 1;
+    const Unit u = decode(P, a.cta_items[ii]);
+    const int kvh = u.head_a / group;
+    for (int t = u.w.tile_begin; t < u.w.tile_end; ++t) {
       const int32_t boff = a.tiles[t].blk_off;
-      mbar_wait(&S.k_empty[stage], ph ^ 1);
-      mbar_arrive_expect_tx(&S.k_full[stage], kStageBytes);
-      for (int j = 0; j < bpt; ++j) {
-        const int32_t y = static_cast<int32_t>(
-            layer_rows + (static_cast<int64_t>(a.tile_blocks[boff + j]) * a.hkv + kvh) * a.bs);
+#pragma unroll 1
+      for (int kv = 0; kv < 2; ++kv, ++n) {
+        const int slot = n % kSlots;
+        mbar_wait(&S.kv_empty[slot], ((n / kSlots) & 1) ^ 1);
+        trace(P, 0, tc, 10 + kv);  // 10: K load issued, 11: V load issued
+        mbar_arrive_expect_tx(&S.kv_full[slot], kTileBytes);
+        const CUtensorMap* map = kv == 0 ? &P.tmk : &P.tmv;
+        for (int j = 0; j < bpt; ++j) {
+          const int32_t blk = P.dbg_mode == 3 ? a.tile_blocks[0] : a.tile_blocks[boff + j];
+          const int32_t y = static_cast<int32_t>(layer_rows + (static_cast<int64_t>(blk) * a.hkv + kvh) * a.bs);
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_2d(&S.k[stage][c][j * a.bs * 128], &P.tmk, &S.k_full[stage], c * 64, y);
-      }
-      mbar_wait(&S.v_empty[stage], ph ^ 1);
-      mbar_arrive_expect_tx(&S.v_full[stage], kStageBytes);
-      for (int j = 0; j < bpt; ++j) {
-        const int32_t y = static_cast<int32_t>(
-            layer_rows + (static_cast<int64_t>(a.tile_blocks[boff + j]) * a.hkv + kvh) * a.bs);
-#pragma unroll
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_2d(&S.v[stage][c][j * a.bs * 128], &P.tmv, &S.v_full[stage], c * 64, y);
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_2d(&S.kv[slot][c][j * a.bs * 128], map, &S.kv_full[slot], c * 64, y);
+        }
       }
     }
   }
@@ -109,89 +158,161 @@ __device__ void run_producer(const TcParams& P, TcSmem<D>& S, int it_begin, int 
 template <int D>
 __device__ void run_mma(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_begin, int it_end) {
   const AttnArgs& a = P.a;
+  constexpr int kSlots = TcSmem<D>::kKvSlots;
   constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false);
   constexpr uint32_t idO = idesc_bf16_f32(128, D, false, true);
-  uint32_t kt = 0, st = 0, qs = 0;
-  struct Pend {
-    int stage, sb;
-    uint32_t kt, st;
-    bool first;
-  };
-  auto issue_pv = [&](const Pend& p) {
-    mbar_wait(&S.p_full[p.sb], (p.st >> 1) & 1);
-    mbar_wait(&S.v_full[p.stage], (p.kt >> 1) & 1);
+  uint32_t jg = 0;  // KV tiles consumed (K_j = load 2jg, V_j = load 2jg+1)
+  uint32_t ep = 0;  // Q epochs started
+  uint32_t tc = 0;
+  auto wait_kv = [&](uint32_t n) {
+    if (P.dbg_mode != 4) mbar_wait(&S.kv_full[n % kSlots], (n / kSlots) & 1);
     tc_fence_after();
-    const uint32_t vbase = smem_u32(&S.v[p.stage][0][0]);
+  };
+  auto issue_s = [&](int x, int qslot, int kslot) {
+    const uint32_t qbase = smem_u32(&S.q[qslot][0][0]);
+    const uint32_t kbase = smem_u32(&S.kv[kslot][0][0]);
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      const uint32_t off = (kk / 4) * TcSmem<D>::kChunkBytes + (kk % 4) * 32;
+      mma_ss(tmem + kColS + 128 * x, desc_sw128(qbase + off, 16, 1024), desc_sw128(kbase + off, 16, 1024), idS,
+             kk > 0 ? 1u : 0u);
+    }
+    mma_commit(&S.s_full[x]);
+  };
+  auto issue_pv = [&](int x, int vslot, bool first) {
+    const uint32_t vbase = smem_u32(&S.kv[vslot][0][0]);
 #pragma unroll
     for (int kk = 0; kk < kTileKeys / 16; ++kk) {
       const uint64_t vd = desc_sw128(vbase + kk * 2048, 16384, 1024);
-      mma_ts(tmem + kColO, tmem + kColS0 + p.sb * 128 + kk * 8, vd, idO, (!p.first || kk > 0) ? 1u : 0u);
+      mma_ts(tmem + kColO + 128 * x, tmem + kColS + 128 * x + kk * 8, vd, idO, (!first || kk > 0) ? 1u : 0u);
     }
-    mma_commit(&S.v_empty[p.stage]);
-    mma_commit(&S.o_done);
   };
+  // Q slot index n = 2*epoch + head: slot n % 3, used for the (n / 3)-th time
   for (int ii = it_begin; ii < it_end; ++ii) {
-    const int code = a.cta_items[ii];
-    const WorkItem w = a.items[code / a.hq];
-    int qb = 0;
-    Pend prev{0, 0, 0, 0, true};
-    for (int t = w.tile_begin; t < w.tile_end; ++t) {
-      const int k = t - w.tile_begin;
+    const Unit u = decode(P, a.cta_items[ii]);
+    const bool two = u.n_heads == 2;
+    int qa = 0, qb = 1;
+    const uint32_t j0 = jg;
+    for (int t = u.w.tile_begin; t < u.w.tile_end; ++t, ++jg) {
+      const int k = t - u.w.tile_begin;
+      const uint32_t nk = 2 * jg, nv_prev = 2 * jg - 1;
+      // PV_A of the previous tile frees S_A (P_A is read from it) before S_A(k) overwrites it
+      if (k > 0) {
+        mbar_wait(&S.p_full[0], (jg - 1) & 1);
+        trace(P, 1, tc, 20);  // 20: P_A ready
+        wait_kv(nv_prev);
+        issue_pv(0, nv_prev % kSlots, k == 1);
+      }
       if (k == 0 || a.tiles[t].rot_delta != a.tiles[t - 1].rot_delta) {
-        if (k > 0) mma_commit(&S.q_empty[qb]);
-        qb = qs & 1;
-        mbar_wait(&S.q_full[qb], (qs >> 1) & 1);
-        ++qs;
+        qa = (2 * ep) % 3;
+        qb = (2 * ep + 1) % 3;
+        mbar_wait(&S.q_full[qa], ((2 * ep) / 3) & 1);
+        if (two) mbar_wait(&S.q_full[qb], ((2 * ep + 1) / 3) & 1);
+        trace(P, 1, tc, 21);  // 21: Q ready for new epoch
+        ++ep;
       }
-      const int stage = kt & 1, sb = st & 1;
-      mbar_wait(&S.k_full[stage], (kt >> 1) & 1);
-      tc_fence_after();
-      const uint32_t qbase = smem_u32(&S.q[qb][0][0]);
-      const uint32_t kbase = smem_u32(&S.k[stage][0][0]);
-#pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
-        const uint32_t off = (kk / 4) * TcSmem<D>::kChunkBytes + (kk % 4) * 32;
-        mma_ss(tmem + kColS0 + sb * 128, desc_sw128(qbase + off, 16, 1024),
-               desc_sw128(kbase + off, 16, 1024), idS, kk > 0 ? 1u : 0u);
+      wait_kv(nk);
+      trace(P, 1, tc, 22);  // 22: K ready, S_A issued
+      issue_s(0, qa, nk % kSlots);
+      // last S of this epoch: release each Q tile right after its last MMA is issued, so the
+      // next epoch's head-B tile (which reuses this epoch's A slot) is prepared ~2 tiles early
+      const bool epoch_ends = t + 1 == u.w.tile_end || a.tiles[t + 1].rot_delta != a.tiles[t].rot_delta;
+      if (epoch_ends) mma_commit(&S.q_empty[qa]);
+      if (two) {
+        if (k > 0) {
+          mbar_wait(&S.p_full[1], (jg - 1) & 1);
+          trace(P, 1, tc, 23);  // 23: P_B ready
+          issue_pv(1, nv_prev % kSlots, k == 1);
+        }
+        if (k > 0) mma_commit(&S.kv_empty[nv_prev % kSlots]);  // V_{k-1} consumed
+        issue_s(1, qb, nk % kSlots);
+      } else if (k > 0) {
+        mma_commit(&S.kv_empty[nv_prev % kSlots]);
       }
-      mma_commit(&S.k_empty[stage]);
-      mma_commit(&S.s_full[sb]);
-      if (k > 0) issue_pv(prev);
-      prev = Pend{stage, sb, kt, st, k == 0};
-      ++kt;
-      ++st;
+      mma_commit(&S.kv_empty[nk % kSlots]);  // K_k consumed
+      if (epoch_ends) mma_commit(&S.q_empty[qb]);
     }
-    issue_pv(prev);
-    mma_commit(&S.q_empty[qb]);
+    // drain: PV of the last tile
+    const uint32_t nv_last = 2 * jg - 1;
+    const bool single_tile = jg - j0 == 1;
+    mbar_wait(&S.p_full[0], (jg - 1) & 1);
+    trace(P, 1, tc, 24);  // 24: drain P_A ready
+    wait_kv(nv_last);
+    issue_pv(0, nv_last % kSlots, single_tile);
+    mma_commit(&S.o_full[0]);
+    if (two) {
+      mbar_wait(&S.p_full[1], (jg - 1) & 1);
+      issue_pv(1, nv_last % kSlots, single_tile);
+      mma_commit(&S.o_full[1]);
+    }
+    mma_commit(&S.kv_empty[nv_last % kSlots]);
   }
 }
 
-// ------------------------------------------------------------------ warps 4-7: softmax + epilogue
-template <int D>
-__device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_begin, int it_end) {
+// pass 2 of the softmax over one 128-key S row in TMEM: P = exp2(s*scale - m) written back as
+// packed bf16 over the first 64 columns; per-row sums in 8 independent accumulators.
+template <int PM, bool kMasked>
+__device__ __forceinline__ void exp_pass(uint32_t scol, float sl2, float msub, int lim, float (&sum8)[8]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t v[32];
+    tmem_ld32(scol + c * 32, v);
+    tmem_wait_ld();
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int j0 = c * 32 + 2 * i;
+      const float x0 = fmaf(__uint_as_float(v[2 * i]), sl2, -msub);
+      const float x1 = fmaf(__uint_as_float(v[2 * i + 1]), sl2, -msub);
+      constexpr bool kPoly[4] = {0 < PM, 1 < PM, 2 < PM, 3 < PM};
+      float p0 = kPoly[i & 3] ? exp2_poly(x0) : ex2_approx(x0);
+      float p1 = kPoly[i & 3] ? exp2_poly(x1) : ex2_approx(x1);
+      if (kMasked) {
+        p0 = (j0 <= lim) ? p0 : 0.f;
+        p1 = (j0 + 1 <= lim) ? p1 : 0.f;
+      }
+      sum8[(2 * i) & 7] += p0;
+      sum8[(2 * i + 1) & 7] += p1;
+      pk[i] = pack_bf16x2(p0, p1);
+    }
+    tmem_st16(scol + c * 16, pk);
+  }
+  tmem_wait_st();
+}
+
+// ------------------------------------------------------------------ softmax + epilogue (one WG per head)
+template <int D, int PM>
+__device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_begin, int it_end, int x) {
   const AttnArgs& a = P.a;
-  const int r = threadIdx.x - 128;  // row within the tile == TMEM lane
+  const int r = threadIdx.x & 127;  // row within the tile == TMEM lane
   const uint32_t lane_base = static_cast<uint32_t>((r / 32) * 32) << 16;
   const float sl2 = P.scale_log2;
-  uint32_t st = 0, pvw = 0;
+  const uint32_t scol = tmem + lane_base + kColS + 128 * x;
+  const uint32_t ocol = tmem + lane_base + kColO + 128 * x;
+  uint32_t st = 0, itc = 0;
+  uint32_t tc = 0;
+  const bool tr = (threadIdx.x & 127) == 0;
   for (int ii = it_begin; ii < it_end; ++ii) {
-    const int code = a.cta_items[ii];
-    const int h = code % a.hq;
-    const WorkItem w = a.items[code / a.hq];
+    const Unit u = decode(P, a.cta_items[ii]);
+    if (x >= u.n_heads) continue;  // single-head unit: WG B idles
+    const int h = u.head_a + x;
+    const WorkItem& w = u.w;
     const bool valid = r < w.n_rows;
     const int64_t row = static_cast<int64_t>(w.row0) + r;
     const int p = valid ? a.pos[row] : 0;
     float m = -INFINITY, l = 0.f;
-    for (int t = w.tile_begin; t < w.tile_end; ++t) {
-      const int k = t - w.tile_begin;
+    for (int t = w.tile_begin; t < w.tile_end; ++t, ++st) {
       const KvTile tl = a.tiles[t];
       const int lim = min(tl.n_valid - 1, tl.causal ? p - tl.key_pos0 : kTileKeys - 1);
-      const int sb = st & 1;
-      const uint32_t scol = tmem + lane_base + kColS0 + sb * 128;
-      mbar_wait(&S.s_full[sb], (st >> 1) & 1);
+      mbar_wait(&S.s_full[x], st & 1);
+      if (tr) trace(P, 2 + x, tc, 30);  // 30: S ready
       tc_fence_after();
-      // pass 1: row max — 8 independent accumulators (no 128-long dependency chain); the
-      // per-key mask is only evaluated when some row of the warp sees a partial tile
+      if (P.dbg_mode == 1 || P.dbg_mode >= 3) {
+        tc_fence_before();
+        mbar_arrive(&S.p_full[x]);
+        continue;
+      }
+      // pass 1: row max (8 independent accumulators); masks only on partial tiles
       const bool full = __all_sync(0xffffffffu, lim >= kTileKeys - 1);
       float mx8[8];
 #pragma unroll
@@ -214,100 +335,94 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
                        fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       mx *= sl2;
       const float m_new = fmaxf(m, mx);
-      const bool resc = m_new > m + kRescaleThreshold;
+      const bool resc = m_new > m + P.rescale_threshold;
       const float m_use = resc ? m_new : m;
       const float alpha = resc ? ex2_approx(m - m_new) : 1.f;
       const float msub = (m_use == -INFINITY) ? 0.f : m_use;
-      // pass 2: P = exp2(s*scale - m), packed bf16 over the first 64 columns of S
+      // O_x is stable here (PV_x(j-1) was issued before S_x(j)): rescale it if the max grew
+      if (t > w.tile_begin && __any_sync(0xffffffffu, resc)) {
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(ocol + c * 32, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+          tmem_st32(ocol + c * 32, v);
+        }
+      }
+      if (P.dbg_mode == 2) {
+        l += mx;
+        tc_fence_before();
+        mbar_arrive(&S.p_full[x]);
+        continue;
+      }
+      // pass 2: P = exp2(s*scale - m) -> bf16 over the first 64 columns of S_x; the mask is a
+      // compile-time template flag so fully visible tiles carry no per-key compare/select
       float sum8[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) sum8[i] = 0.f;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld32(scol + c * 32, v);
-        tmem_wait_ld();
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int j0 = c * 32 + 2 * i;
-          float p0 = ex2_approx(fmaf(__uint_as_float(v[2 * i]), sl2, -msub));
-          float p1 = ex2_approx(fmaf(__uint_as_float(v[2 * i + 1]), sl2, -msub));
-          if (!full) {
-            p0 = (j0 <= lim) ? p0 : 0.f;
-            p1 = (j0 + 1 <= lim) ? p1 : 0.f;
-          }
-          sum8[(2 * i) & 7] += p0;
-          sum8[(2 * i + 1) & 7] += p1;
-          pk[i] = pack_bf16x2(p0, p1);
-        }
-        tmem_st16(scol + c * 16, pk);
-      }
+      if (full)
+        exp_pass<PM, false>(scol, sl2, msub, lim, sum8);
+      else
+        exp_pass<PM, true>(scol, sl2, msub, lim, sum8);
       const float sum = ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) + ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
-      tmem_wait_st();
       l = l * alpha + sum;
-      if (k > 0) {
-        mbar_wait(&S.o_done, pvw & 1);  // PV of the previous tile has landed in O
-        ++pvw;
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, resc)) {
-          const uint32_t ocol = tmem + lane_base + kColO;
-#pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t v[32];
-            tmem_ld32(ocol + c * 32, v);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-            tmem_st32(ocol + c * 32, v);
-          }
-          tmem_wait_st();
-        }
-      }
       m = m_use;
       tc_fence_before();
-      mbar_arrive(&S.p_full[sb]);
-      ++st;
+      if (tr) trace(P, 2 + x, tc, 31);  // 31: P written
+      mbar_arrive(&S.p_full[x]);
     }
-    // epilogue: wait for the last PV, normalize, store
-    mbar_wait(&S.o_done, pvw & 1);
-    ++pvw;
+    // epilogue: wait for the last PV of this head, normalise, store
+    mbar_wait(&S.o_full[x], itc & 1);
+    if (tr) trace(P, 2 + x, tc, 32);  // 32: O ready (epilogue start)
+    ++itc;
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     const float lse = l > 0.f ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
-    const uint32_t ocol = tmem + lane_base + kColO;
+    // O tile -> global through a per-warp 32x32 fp32 smem transpose (16 B units XOR-swizzled by
+    // row): each store instruction then writes 4 rows x 128 B of full lines instead of 32 rows
+    // x 16 B scattered 16 KB apart.
+    {
+      const int wr = (threadIdx.x / 32) & 3;  // warp's 32-row slice of the tile
+      const int lane = threadIdx.x & 31;
+      float* stg = S.stage[x * 4 + wr];
+      const int rr_base = wr * 32;
+#pragma unroll 1
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(ocol + c * 32, v);
+        tmem_wait_ld();
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t v[32];
-      tmem_ld32(ocol + c * 32, v);
-      tmem_wait_ld();
-      if (valid) {
-        if (w.part < 0 && a.out_fp32) {
-          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(a.o) + (row * a.hq + h) * D + c * 32);
+        for (int u = 0; u < 8; ++u)
+          *reinterpret_cast<float4*>(stg + lane * 32 + ((u ^ (lane & 7)) * 4)) =
+              make_float4(__uint_as_float(v[4 * u]) * inv, __uint_as_float(v[4 * u + 1]) * inv,
+                          __uint_as_float(v[4 * u + 2]) * inv, __uint_as_float(v[4 * u + 3]) * inv);
+        __syncwarp();
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
-            dst[u] = make_float4(__uint_as_float(v[4 * u]) * inv, __uint_as_float(v[4 * u + 1]) * inv,
-                                 __uint_as_float(v[4 * u + 2]) * inv, __uint_as_float(v[4 * u + 3]) * inv);
-        } else if (w.part < 0) {
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.o) +
-                                                (row * a.hq + h) * D + c * 32);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            uint4 pk;
-            pk.x = pack_bf16x2(__uint_as_float(v[8 * u + 0]) * inv, __uint_as_float(v[8 * u + 1]) * inv);
-            pk.y = pack_bf16x2(__uint_as_float(v[8 * u + 2]) * inv, __uint_as_float(v[8 * u + 3]) * inv);
-            pk.z = pack_bf16x2(__uint_as_float(v[8 * u + 4]) * inv, __uint_as_float(v[8 * u + 5]) * inv);
-            pk.w = pack_bf16x2(__uint_as_float(v[8 * u + 6]) * inv, __uint_as_float(v[8 * u + 7]) * inv);
-            dst[u] = pk;
+        for (int j = 0; j < 8; ++j) {
+          const int rr = j * 4 + (lane >> 3);  // row within the warp's slice
+          const int u = lane & 7;              // 16 B unit = 4 columns
+          const float4 val = *reinterpret_cast<const float4*>(stg + rr * 32 + ((u ^ (rr & 7)) * 4));
+          const int trow = rr_base + rr;
+          if (trow < w.n_rows) {
+            const int col = c * 32 + u * 4;
+            if (w.part >= 0) {
+              *reinterpret_cast<float4*>(a.opart + ((static_cast<int64_t>(w.part) * a.hq + h) * kTileRows + trow) * D +
+                                         col) = val;
+            } else if (a.out_fp32) {
+              *reinterpret_cast<float4*>(static_cast<float*>(a.o) + ((w.row0 + trow) * static_cast<int64_t>(a.hq) + h) * D +
+                                         col) = val;
+            } else {
+              uint2 pk;
+              pk.x = pack_bf16x2(val.x, val.y);
+              pk.y = pack_bf16x2(val.z, val.w);
+              *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.o) +
+                                        ((w.row0 + trow) * static_cast<int64_t>(a.hq) + h) * D + col) = pk;
+            }
           }
-        } else {
-          float4* dst = reinterpret_cast<float4*>(
-              a.opart + ((static_cast<int64_t>(w.part) * a.hq + h) * kTileRows + r) * D + c * 32);
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            dst[u] = make_float4(__uint_as_float(v[4 * u]) * inv, __uint_as_float(v[4 * u + 1]) * inv,
-                                 __uint_as_float(v[4 * u + 2]) * inv, __uint_as_float(v[4 * u + 3]) * inv);
         }
+        __syncwarp();
       }
     }
     if (valid) {
@@ -317,99 +432,180 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
         a.lsepart[(static_cast<int64_t>(w.part) * a.hq + h) * kTileRows + r] = lse;
       }
     }
+    if (tr) trace(P, 2 + x, tc, 33);  // 33: epilogue done
     tc_fence_before();
   }
 }
 
-// ------------------------------------------------------------------ warps 8-11: Q prep
+// ------------------------------------------------------------------ warps 12-15: Q prep
+// The pre-RoPE q tile of one head (128 rows x d, bf16) is TMA-loaded straight into its Q slot in
+// the SWIZZLE_128B K-major layout the MMA reads, then rotated in place: warp wq owns rows
+// [32wq, 32wq+32), one row per step, lane l holding elements [l*E, l*E+E) (E = d/32) — its
+// rotate-half partner sits in lane l^16 (one shuffle) — with the fp32 (cos, sin) of its pairs
+// loaded coalesced from the table, 8 rows per batch. Rows past n_rows are rotated too but never
+// stored by the epilogue; rows past the tensor are zero (TMA out-of-bounds fill).
 template <int D>
-__device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_end) {
-  const AttnArgs& a = P.a;
-  const int r = threadIdx.x - 256;
-  const __nv_bfloat16* qg = static_cast<const __nv_bfloat16*>(a.q);
-  uint32_t qs = 0;
-  for (int ii = it_begin; ii < it_end; ++ii) {
-    const int code = a.cta_items[ii];
-    const int h = code % a.hq;
-    const WorkItem w = a.items[code / a.hq];
-    const bool valid = r < w.n_rows;
-    const int64_t row = static_cast<int64_t>(w.row0) + r;
-    const int p = valid ? a.pos[row] : 0;
-    const __nv_bfloat16* qrow = qg + (row * a.hq + h) * D;
-    for (int t = w.tile_begin; t < w.tile_end; ++t) {
-      const int k = t - w.tile_begin;
-      const int rot = a.tiles[t].rot_delta;
-      if (k > 0 && rot == a.tiles[t - 1].rot_delta) continue;
-      const int qb = qs & 1;
-      mbar_wait(&S.q_empty[qb], ((qs >> 1) & 1) ^ 1);
-      uint8_t* qs_base = &S.q[qb][0][0];
-      const int rp = min(max(p - rot, 0), a.max_pos - 1);
-      const float4* cs = reinterpret_cast<const float4*>(a.rope + static_cast<int64_t>(rp) * (D / 2));
-      // issue every q load of the row first (latency is paid once), then the cos/sin table in
-      // batches of 8 pairs interleaved with the rotate + swizzled stores
-      uint4 q1[D / 16], q2[D / 16];
+__device__ __forceinline__ void rotate_row(uint8_t* qs_base, int r, int lane, const float (&c)[D / 32], const float (&sn)[D / 32]) {
+  constexpr int E = D / 32;
+  const bool hi = lane >= 16;
+  const int e0 = lane * E;
+  const int chunk = e0 / 64, unit = (e0 % 64) / 8, within = (e0 % 8) * 2;
+  uint8_t* ptr = qs_base + chunk * TcSmem<D>::kChunkBytes + r * 128 + ((unit ^ (r & 7)) * 16) + within;
+  uint32_t qv[E / 2];
+  if constexpr (E == 4) {
+    const uint2 t = *reinterpret_cast<const uint2*>(ptr);
+    qv[0] = t.x;
+    qv[1] = t.y;
+  } else {
+    qv[0] = *reinterpret_cast<const uint32_t*>(ptr);
+  }
+  uint32_t out[E / 2];
 #pragma unroll
-      for (int g = 0; g < D / 16; ++g) {
-        q1[g] = valid ? __ldg(reinterpret_cast<const uint4*>(qrow + g * 8)) : make_uint4(0, 0, 0, 0);
-        q2[g] = valid ? __ldg(reinterpret_cast<const uint4*>(qrow + D / 2 + g * 8)) : make_uint4(0, 0, 0, 0);
+  for (int e = 0; e < E / 2; ++e) {
+    const float x0 = __uint_as_float(qv[e] << 16), x1 = __uint_as_float(qv[e] & 0xFFFF0000u);
+    const float y0 = __shfl_xor_sync(0xffffffffu, x0, 16);
+    const float y1 = __shfl_xor_sync(0xffffffffu, x1, 16);
+    // first half: x cos - partner sin ; second half: x cos + partner sin
+    const float o0 = hi ? fmaf(y0, sn[2 * e], x0 * c[2 * e]) : fmaf(-y0, sn[2 * e], x0 * c[2 * e]);
+    const float o1 = hi ? fmaf(y1, sn[2 * e + 1], x1 * c[2 * e + 1]) : fmaf(-y1, sn[2 * e + 1], x1 * c[2 * e + 1]);
+    out[e] = pack_bf16x2(o0, o1);
+  }
+  if constexpr (E == 4) {
+    *reinterpret_cast<uint2*>(ptr) = make_uint2(out[0], out[1]);
+  } else {
+    *reinterpret_cast<uint32_t*>(ptr) = out[0];
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void rotate_q_tile(uint8_t* qs_base, const float2* rope, int my_pos, int my_valid, int rot,
+                                              int max_pos) {
+  constexpr int E = D / 32;
+  const int lane = threadIdx.x & 31;
+  const int wq = (threadIdx.x / 32) & 3;
+  const int pair0 = (lane & 15) * E;
+  const int p_first = __shfl_sync(0xffffffffu, my_pos, 0);
+  // rows of a tile normally have consecutive positions (a job's rows, a query's cross rows):
+  // then (cos, sin) of row r+1 = (cos, sin) of row r rotated by theta — 4 FMAs per pair per
+  // row (fp32, 31 steps: ~1e-6 drift vs bf16's 4e-3) instead of a table row per row.
+  const bool consecutive = __all_sync(0xffffffffu, !my_valid || my_pos == p_first + lane) && p_first - rot >= 0 &&
+                           p_first - rot + 31 < max_pos;
+  float c[E], sn[E];
+  if (consecutive) {
+    float cd[E], sd[E];
+    const float4* cs = reinterpret_cast<const float4*>(rope + static_cast<int64_t>(p_first - rot) * (D / 2) + pair0);
+    const float4* cst = reinterpret_cast<const float4*>(rope + (D / 2) + pair0);  // position 1: (cos th, sin th)
+#pragma unroll
+    for (int e = 0; e < E / 2; ++e) {
+      const float4 v = __ldg(cs + e), dv = __ldg(cst + e);
+      c[2 * e] = v.x;
+      sn[2 * e] = v.y;
+      c[2 * e + 1] = v.z;
+      sn[2 * e + 1] = v.w;
+      cd[2 * e] = dv.x;
+      sd[2 * e] = dv.y;
+      cd[2 * e + 1] = dv.z;
+      sd[2 * e + 1] = dv.w;
+    }
+#pragma unroll 4
+    for (int rr = 0; rr < 32; ++rr) {
+      rotate_row<D>(qs_base, wq * 32 + rr, lane, c, sn);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {  // advance the angle by theta_i
+        const float cn = fmaf(c[e], cd[e], -sn[e] * sd[e]);
+        sn[e] = fmaf(sn[e], cd[e], c[e] * sd[e]);
+        c[e] = cn;
       }
+    }
+  } else {
+#pragma unroll 1
+    for (int rr = 0; rr < 32; ++rr) {
+      const int p = __shfl_sync(0xffffffffu, my_pos, rr);
+      const int rp = min(max(p - rot, 0), max_pos - 1);
+      const float4* cs = reinterpret_cast<const float4*>(rope + static_cast<int64_t>(rp) * (D / 2) + pair0);
 #pragma unroll
-      for (int g0 = 0; g0 < D / 16; g0 += 2) {
-        float4 cst[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) cst[e] = valid ? __ldg(cs + g0 * 4 + e) : make_float4(1.f, 0.f, 1.f, 0.f);
-#pragma unroll
-        for (int gg = 0; gg < 2; ++gg) {
-          const int g = g0 + gg;
-          const int i0 = g * 8;
-          uint4 o1, o2;
-          const __nv_bfloat162* b1 = reinterpret_cast<const __nv_bfloat162*>(&q1[g]);
-          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q2[g]);
-          uint32_t* w1 = reinterpret_cast<uint32_t*>(&o1);
-          uint32_t* w2 = reinterpret_cast<uint32_t*>(&o2);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float4 c = cst[gg * 4 + e];  // (cos,sin) of pairs i0+2e, i0+2e+1
-            const float2 x1 = __bfloat1622float2(b1[e]), x2 = __bfloat1622float2(b2[e]);
-            w1[e] = pack_bf16x2(x1.x * c.x - x2.x * c.y, x1.y * c.z - x2.y * c.w);
-            w2[e] = pack_bf16x2(x2.x * c.x + x1.x * c.y, x2.y * c.z + x1.y * c.w);
-          }
-          const int e1 = i0, e2 = D / 2 + i0;
-          *reinterpret_cast<uint4*>(qs_base + (e1 / 64) * TcSmem<D>::kChunkBytes + r * 128 +
-                                    ((((e1 % 64) / 8) ^ (r & 7)) * 16)) = o1;
-          *reinterpret_cast<uint4*>(qs_base + (e2 / 64) * TcSmem<D>::kChunkBytes + r * 128 +
-                                    ((((e2 % 64) / 8) ^ (r & 7)) * 16)) = o2;
-        }
+      for (int e = 0; e < E / 2; ++e) {
+        const float4 v = __ldg(cs + e);
+        c[2 * e] = v.x;
+        sn[2 * e] = v.y;
+        c[2 * e + 1] = v.z;
+        sn[2 * e + 1] = v.w;
       }
-      fence_proxy_async_smem();
-      mbar_arrive(&S.q_full[qb]);
-      ++qs;
+      rotate_row<D>(qs_base, wq * 32 + rr, lane, c, sn);
     }
   }
 }
 
 template <int D>
+__device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_end) {
+  const AttnArgs& a = P.a;
+  const int r = threadIdx.x & 127;
+  const int lane = threadIdx.x & 31;
+  const int wq = (threadIdx.x / 32) & 3;
+  constexpr uint32_t kQBytes = 128 * D * 2;
+  uint32_t ep = 0;
+  uint32_t tc = 0;
+  uint32_t load_phase = 0;  // bit s: parity of the next q_load[s] completion
+  const bool tr = r == 0;
+  for (int ii = it_begin; ii < it_end; ++ii) {
+    const Unit u = decode(P, a.cta_items[ii]);
+    const WorkItem& w = u.w;
+    const int my_row = wq * 32 + lane;  // this lane's row position, shuffled to the warp per row
+    const int my_pos = my_row < w.n_rows ? a.pos[static_cast<int64_t>(w.row0) + my_row] : 0;
+    for (int t = w.tile_begin; t < w.tile_end; ++t) {
+      const int rot = a.tiles[t].rot_delta;
+      if (t > w.tile_begin && rot == a.tiles[t - 1].rot_delta) continue;
+      for (int x = 0; x < 2; ++x) {
+        const uint32_t n = 2 * ep + x;  // Q slot index: slot n % 3, (n / 3)-th use
+        const int sl = static_cast<int>(n % 3);
+        mbar_wait(&S.q_empty[sl], ((n / 3) & 1) ^ 1);
+        if (tr) trace(P, 4, tc, 40 + x);  // 40/41: slot free for head A/B
+        if (x < u.n_heads && P.dbg_mode != 5) {  // single-head units leave the B slot untouched
+          if (r == 0) {
+            mbar_arrive_expect_tx(&S.q_load[sl], kQBytes);
+#pragma unroll
+            for (int c = 0; c < D / 64; ++c)
+              tma_load_3d(&S.q[sl][c][0], &P.tmq, &S.q_load[sl], c * 64, u.head_a + x, w.row0);
+          }
+          mbar_wait(&S.q_load[sl], (load_phase >> sl) & 1);
+          load_phase ^= 1u << sl;
+          rotate_q_tile<D>(&S.q[sl][0][0], a.rope, my_pos, my_row < w.n_rows, rot, a.max_pos);
+          fence_proxy_async_smem();
+        }
+        if (tr) trace(P, 4, tc, 42 + x);  // 42/43: Q tile A/B written
+        mbar_arrive(&S.q_full[sl]);
+      }
+      ++ep;
+    }
+  }
+}
+
+template <int D, int PM>
 __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_constant__ TcParams P) {
   extern __shared__ uint8_t smem_raw[];
   TcSmem<D>& S = smem_ref<D>(smem_raw);
   const int warp = threadIdx.x / 32;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&S.k_full[i], 1);
-      mbar_init(&S.k_empty[i], 1);
-      mbar_init(&S.v_full[i], 1);
-      mbar_init(&S.v_empty[i], 1);
-      mbar_init(&S.s_full[i], 1);
-      mbar_init(&S.p_full[i], 128);
+    for (int i = 0; i < TcSmem<D>::kKvSlots; ++i) {
+      mbar_init(&S.kv_full[i], 1);
+      mbar_init(&S.kv_empty[i], 1);
+    }
+    for (int i = 0; i < TcSmem<D>::kQSlots; ++i) {
       mbar_init(&S.q_full[i], 128);
       mbar_init(&S.q_empty[i], 1);
+      mbar_init(&S.q_load[i], 1);
     }
-    mbar_init(&S.o_done, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&S.s_full[i], 1);
+      mbar_init(&S.p_full[i], 128);
+      mbar_init(&S.o_full[i], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 0 && (threadIdx.x & 31) == 0) {
     tma_prefetch_desc(&P.tmk);
     tma_prefetch_desc(&P.tmv);
+    tma_prefetch_desc(&P.tmq);
   }
   if (warp == 2) tmem_alloc<kTmemCols>(&S.tmem_base);
   tc_fence_before();
@@ -417,13 +613,19 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
   const int it_begin = P.a.cta_off[blockIdx.x], it_end = P.a.cta_off[blockIdx.x + 1];
-  if (warp == 0) {
-    if (elect_one()) run_producer<D>(P, S, it_begin, it_end);
-  } else if (warp == 1) {
-    if (elect_one()) run_mma<D>(P, S, tmem, it_begin, it_end);
-  } else if (warp >= 4 && warp < 8) {
-    run_softmax<D>(P, S, tmem, it_begin, it_end);
-  } else if (warp >= 8) {
+  // register budget 65536 = 128 x (56 + 136 + 136 + 168): TMA/MMA warps need few
+  if (warp < 4) {
+    reg_dealloc<56>();
+    if (warp == 0) {
+      if (elect_one()) run_producer<D>(P, S, it_begin, it_end);
+    } else if (warp == 1) {
+      if (elect_one()) run_mma<D>(P, S, tmem, it_begin, it_end);
+    }
+  } else if (warp < 12) {
+    reg_alloc<136>();
+    run_softmax<D, PM>(P, S, tmem, it_begin, it_end, warp < 8 ? 0 : 1);
+  } else {
+    reg_alloc<168>();
     run_qprep<D>(P, S, it_begin, it_end);
   }
   tc_fence_before();
@@ -434,22 +636,36 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
   }
 }
 
-template <int D>
-cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
+template <int D, int PM>
+cudaError_t launch_dp(const AttnArgs& a, cudaStream_t st) {
   static bool attr_set = false;
   const int smem = static_cast<int>(sizeof(TcSmem<D>)) + 1024;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(span_attn_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(span_attn_tc_kernel<D, PM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   TcParams p;
   p.tmk = *a.tmap_k;
   p.tmv = *a.tmap_v;
+  p.tmq = *a.tmap_q;
   p.a = a;
   p.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));
-  span_attn_tc_kernel<D><<<a.grid, kThreads, smem, st>>>(p);
+  p.paired = a.paired ? 1 : 0;
+  p.poly_mask = PM;
+  p.rescale_threshold = a.rescale_threshold;
+  p.dbg_mode = getenv("SPANQ_DBG_MODE") ? atoi(getenv("SPANQ_DBG_MODE")) : 0;
+  span_attn_tc_kernel<D, PM><<<a.grid, kThreads, smem, st>>>(p);
   return cudaGetLastError();
+}
+
+template <int D>
+cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
+  switch (a.poly_mask) {
+    case 0: return launch_dp<D, 0>(a, st);
+    case 2: return launch_dp<D, 2>(a, st);
+    default: return launch_dp<D, 1>(a, st);
+  }
 }
 
 }  // namespace
@@ -457,6 +673,7 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
 cudaError_t launch_span_attn_tc(const AttnArgs& a, cudaStream_t st) {
   if (a.n_items == 0 || a.grid == 0) return cudaSuccess;
   if (a.bs < 16 || a.bs > 128 || (a.bs & (a.bs - 1)) != 0) return cudaErrorInvalidValue;
+  if (a.paired && (a.hq / a.hkv) % 2 != 0) return cudaErrorInvalidValue;
   switch (a.d) {
     case 64: return launch_d<64>(a, st);
     case 128: return launch_d<128>(a, st);

@@ -73,7 +73,7 @@ struct spq_ctx {
   std::unique_ptr<spq::Store> store;
   std::unique_ptr<spq::ThreadPool> pool;  // host planning (block hashing)
   int num_sms = 0;
-  float2* rope = nullptr;  // device [max_position][d/2]
+  float2* rope = nullptr;  // device [max_position][d/2] (cos, sin) fp32: K1 (K pages) + fp32 path
   CUtensorMap tmk, tmv;
   bool have_tmap = false;
   std::vector<cudaEvent_t> pending;  // stream-ordered releases
@@ -111,6 +111,29 @@ namespace {
 
 bool is_gpu(const spq_ctx* c) { return c->cfg.device >= 0; }
 
+// tcgen05 path pairs the two q heads of a GQA group (shared K/V) when the group size is even
+bool paired(const spq_ctx* c) {
+  return c->cfg.dtype == SPQ_BF16 && (c->cfg.num_q_heads / c->cfg.num_kv_heads) % 2 == 0;
+}
+
+int poly_mask() {
+  const char* e = std::getenv("SPANQ_POLY_EXP");  // tuning knob: quarters of exp2 on the FMA pipe
+  return e ? std::max(0, std::min(4, std::atoi(e))) : 1;
+}
+
+// host-only contexts plan for a B200 (148 SMs) so their work lists match a GPU ctx's
+spq::WorkOpts work_opts(const spq_ctx* c, bool allow_split) {
+  spq::WorkOpts o{};
+  o.hq = c->cfg.num_q_heads;
+  o.d = c->cfg.head_dim;
+  o.bs = c->cfg.block_size;
+  o.num_sms = c->num_sms > 0 ? c->num_sms : 148;
+  o.allow_split = allow_split;
+  o.persistent = c->cfg.dtype == SPQ_BF16;
+  o.units = paired(c) ? o.hq / 2 : o.hq;
+  return o;
+}
+
 int elt_size(const spq_ctx* c) { return c->cfg.dtype == SPQ_FP32 ? 4 : 2; }
 
 spq_status make_tmap(spq_ctx* c, void* pool, CUtensorMap* out) {
@@ -130,6 +153,28 @@ spq_status make_tmap(spq_ctx* c, void* pool, CUtensorMap* out) {
       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SPQ_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return SPQ_OK;
+}
+
+// per-call TMA map of the packed q rows: 3D {d, hq, rows}, box {64, 1, 128}, SWIZZLE_128B
+spq_status make_qmap(const spq_ctx* c, const void* q, int64_t rows, CUtensorMap* out) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult qr;
+  CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
+  if (fn == nullptr || qr != cudaDriverEntryPointSuccess) return fail(SPQ_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  if (reinterpret_cast<uintptr_t>(q) & 15) return fail(SPQ_EINVAL, "q must be 16-byte aligned");
+  const spq_config& g = c->cfg;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.head_dim), static_cast<cuuint64_t>(g.num_q_heads),
+                        static_cast<cuuint64_t>(std::max<int64_t>(rows, 1))};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.head_dim) * 2,
+                           static_cast<cuuint64_t>(g.head_dim) * 2 * g.num_q_heads};
+  cuuint32_t box[3] = {64, 1, 128};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = reinterpret_cast<EncodeTiledFn>(fn)(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(q), dims,
+                                                   strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SPQ_ECUDA, "cuTensorMapEncodeTiled(q) failed: " + std::to_string(r));
   return SPQ_OK;
 }
 
@@ -174,6 +219,14 @@ void fill_attn(spq_ctx* c, const spq_plan* p, const DevWork& w, spq::AttnArgs* a
   a->opart = p->opart;
   a->lsepart = p->lsepart;
   a->out_fp32 = c->cfg.out_dtype == SPQ_FP32;
+  a->paired = paired(c);
+  a->poly_mask = poly_mask();
+  // tuning/test knob: 0 rescales O on every tile (exercises the rescale path); default 8 (log2)
+  const char* th = std::getenv("SPANQ_RESCALE_THRESHOLD");
+  a->rescale_threshold = th ? static_cast<float>(std::atof(th)) : 8.0f;
+  // profiling only: SPANQ_TRACE=<device address> (from the binding) enables the CTA-0 timeline
+  const char* tr = std::getenv("SPANQ_TRACE");
+  a->dbg_trace = tr ? reinterpret_cast<long long*>(std::strtoull(tr, nullptr, 10)) : nullptr;
 }
 
 spq_status run_attn(spq_ctx* c, const spq::AttnArgs& a, cudaStream_t st) {
@@ -427,8 +480,7 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
   for (const auto& d : H.join_digests) p->join_digests.insert(p->join_digests.end(), d.b, d.b + 16);
   p->padded_layers.assign(c->cfg.num_layers, 0);
   // host-only contexts plan for a B200 (148 SMs) so their work lists match a GPU ctx's
-  spq::WorkOpts o{c->cfg.num_q_heads, c->cfg.head_dim, c->cfg.block_size, c->num_sms > 0 ? c->num_sms : 148,
-                  c->cfg.dtype == SPQ_BF16, c->cfg.dtype == SPQ_BF16};
+  spq::WorkOpts o = work_opts(c, c->cfg.dtype == SPQ_BF16);
   lap("view arrays");
   spq::build_prefill_work(H, o, 0, static_cast<int>(H.jobs.size()), &p->pw_host);
   lap("prefill work");
@@ -552,8 +604,7 @@ spq_status spq_prefill_jobs(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, i
     fill_attn(c, p, p->pw, &args);
   } else {
     spq::AttnWorkHost h;
-    spq::WorkOpts o{c->cfg.num_q_heads, c->cfg.head_dim, c->cfg.block_size, std::max(1, c->num_sms), false,
-                    c->cfg.dtype == SPQ_BF16};
+    spq::WorkOpts o = work_opts(c, false);
     spq::build_prefill_work(p->host, o, a, b, &h);
     s = upload_work(c, h, st, &tw);
     if (s != SPQ_OK) return s;
@@ -568,6 +619,12 @@ spq_status spq_prefill_jobs(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, i
   args.o = o;
   args.lse = lse;
   args.layer = layer;
+  CUtensorMap qmap;
+  if (c->cfg.dtype == SPQ_BF16) {
+    s = make_qmap(c, q, r1 - r0, &qmap);
+    if (s != SPQ_OK) return s;
+    args.tmap_q = &qmap;
+  }
   if (c->timing) CUDA_TRY(cudaEventRecord(c->ev[0], st));
   s = run_attn(c, args, st);
   if (s != SPQ_OK) return s;
@@ -604,8 +661,7 @@ spq_status spq_join(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b
     fill_attn(c, p, p->jw, &args);
   } else {
     spq::AttnWorkHost h;
-    spq::WorkOpts o{c->cfg.num_q_heads, c->cfg.head_dim, c->cfg.block_size, std::max(1, c->num_sms), false,
-                    c->cfg.dtype == SPQ_BF16};
+    spq::WorkOpts o = work_opts(c, false);
     spq::build_join_work(p->host, o, a, b, &h);
     s = upload_work(c, h, st, &tw);
     if (s != SPQ_OK) return s;
@@ -623,6 +679,12 @@ spq_status spq_join(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b
   args.o = o;
   args.lse = lse;
   args.layer = layer;
+  CUtensorMap qmap;
+  if (c->cfg.dtype == SPQ_BF16) {
+    s = make_qmap(c, q, r1 - r0, &qmap);
+    if (s != SPQ_OK) return s;
+    args.tmap_q = &qmap;
+  }
   if (c->timing) CUDA_TRY(cudaEventRecord(c->ev[2], st));
   s = run_attn(c, args, st);
   if (s != SPQ_OK) return s;
