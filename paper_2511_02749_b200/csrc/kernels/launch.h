@@ -49,6 +49,8 @@ struct AttnArgs {
   const CUtensorMap* tmap_k;  // host copies (bf16 path)
   const CUtensorMap* tmap_v;
   const CUtensorMap* tmap_q;  // per call: q [rows][hq][d] as 3D {d, hq, rows}, box {64, 1, 128}
+  const CUtensorMap* tmap_o;  // per call (fp32 o): 3D {d, hq, rows}, box {32, 1, 32}, SWIZZLE_128B
+  const CUtensorMap* tmap_op; // per plan (fp32 partials): 2D {d, parts*hq*128}, box {32, 32}
   int hq, hkv, d, bs;
   int64_t nblk;
   int layer;

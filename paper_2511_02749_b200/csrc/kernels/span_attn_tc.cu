@@ -61,7 +61,7 @@ struct TcSmem {
   alignas(1024) float stage[8][32 * 32];                       // epilogue transpose, per softmax warp
   uint64_t kv_full[kKvSlots], kv_empty[kKvSlots];
   uint64_t q_full[3], q_empty[3], q_load[3];
-  uint64_t s_full[2], p_full[2], o_full[2];
+  uint64_t s_full[2][2], p_full[2][2], o_done[2];  // [head][S buffer]
   uint32_t tmem_base;
 };
 
@@ -69,6 +69,8 @@ struct TcParams {
   CUtensorMap tmk;
   CUtensorMap tmv;
   CUtensorMap tmq;
+  CUtensorMap tmo;   // fp32 O (valid when a.out_fp32)
+  CUtensorMap tmop;  // fp32 partials (valid when the launch has split items)
   AttnArgs a;
   float scale_log2;
   int paired;     // 1: a unit is a GQA head pair (A = 2u, B = 2u+1); 0: one head (B idle)
@@ -119,6 +121,18 @@ __device__ __forceinline__ float exp2_poly(float x) {
   return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
 }
 
+// two exp2 with one MUFU op: fp32 inputs rounded to f16 (the large-p keys have x near 0 where
+// f16 is fine-grained: <= 0.07% error for p >= 1/16, below the bf16 rounding of P itself),
+// packed ex2.approx.f16x2, widened back to fp32 for the row sum.
+__device__ __forceinline__ void ex2_pair_f16(float x0, float x1, float& p0, float& p1) {
+  uint32_t h, e;
+  asm("cvt.rn.f16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(x0), "f"(x1));
+  asm("ex2.approx.f16x2 %0, %1;" : "=r"(e) : "r"(h));
+  asm("{\n\t.reg .f16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\tcvt.f32.f16 %0, lo;\n\tcvt.f32.f16 %1, hi;\n\t}"
+      : "=f"(p0), "=f"(p1)
+      : "r"(e));
+}
+
 // ------------------------------------------------------------------ warp 0: TMA producer
 template <int D>
 __device__ void run_producer(const TcParams& P, TcSmem<D>& S, int it_begin, int it_end) {
@@ -155,106 +169,139 @@ __device__ void run_producer(const TcParams& P, TcSmem<D>& S, int it_begin, int 
 }
 
 // ------------------------------------------------------------------ warp 1: MMA issuer
+// Work is issued per 64-key sub-tile j (a KV tile holds one or two). Each head has two S
+// buffers, so S(j+2) is issued as soon as PV(j) (which reads P(j) from S buffer j&1) is issued:
+// softmax(j+1) never waits for the tensor core to finish PV(j). Order per step:
+//   PV_A(j), PV_B(j), [release V], S_A(j+2), S_B(j+2)  (after a prologue S_A(0),S_B(0),S_A(1),S_B(1))
+struct SubCursor {
+  int t, h;  // KV tile, half (keys [64h, 64h+64))
+};
+
 template <int D>
 __device__ void run_mma(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_begin, int it_end) {
   const AttnArgs& a = P.a;
   constexpr int kSlots = TcSmem<D>::kKvSlots;
-  constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false);
+  constexpr uint32_t idS = idesc_bf16_f32(128, 64, false, false);
   constexpr uint32_t idO = idesc_bf16_f32(128, D, false, true);
-  uint32_t jg = 0;  // KV tiles consumed (K_j = load 2jg, V_j = load 2jg+1)
-  uint32_t ep = 0;  // Q epochs started
+  uint32_t kbase_g = 0;  // KV tiles consumed before the current item (K_t = load 2g, V_t = 2g+1)
+  uint32_t jg = 0;       // sub-tiles whose PV has been issued (global): S buffer j & 1
+  uint32_t ep = 0;       // Q epochs started
   uint32_t tc = 0;
   auto wait_kv = [&](uint32_t n) {
-    if (P.dbg_mode != 4) mbar_wait(&S.kv_full[n % kSlots], (n / kSlots) & 1);
+    mbar_wait(&S.kv_full[n % kSlots], (n / kSlots) & 1);
     tc_fence_after();
   };
-  auto issue_s = [&](int x, int qslot, int kslot) {
-    const uint32_t qbase = smem_u32(&S.q[qslot][0][0]);
-    const uint32_t kbase = smem_u32(&S.kv[kslot][0][0]);
-#pragma unroll
-    for (int kk = 0; kk < D / 16; ++kk) {
-      const uint32_t off = (kk / 4) * TcSmem<D>::kChunkBytes + (kk % 4) * 32;
-      mma_ss(tmem + kColS + 128 * x, desc_sw128(qbase + off, 16, 1024), desc_sw128(kbase + off, 16, 1024), idS,
-             kk > 0 ? 1u : 0u);
-    }
-    mma_commit(&S.s_full[x]);
-  };
-  auto issue_pv = [&](int x, int vslot, bool first) {
-    const uint32_t vbase = smem_u32(&S.kv[vslot][0][0]);
-#pragma unroll
-    for (int kk = 0; kk < kTileKeys / 16; ++kk) {
-      const uint64_t vd = desc_sw128(vbase + kk * 2048, 16384, 1024);
-      mma_ts(tmem + kColO + 128 * x, tmem + kColS + 128 * x + kk * 8, vd, idO, (!first || kk > 0) ? 1u : 0u);
-    }
-  };
-  // Q slot index n = 2*epoch + head: slot n % 3, used for the (n / 3)-th time
   for (int ii = it_begin; ii < it_end; ++ii) {
     const Unit u = decode(P, a.cta_items[ii]);
     const bool two = u.n_heads == 2;
+    const int tb = u.w.tile_begin, te = u.w.tile_end;
+    auto nsub = [&](int t) { return a.tiles[t].n_valid > 64 ? 2 : 1; };
+    auto advance = [&](SubCursor& c) {
+      if (c.h == 0 && nsub(c.t) == 2)
+        c.h = 1;
+      else
+        c = SubCursor{c.t + 1, 0};
+    };
     int qa = 0, qb = 1;
-    const uint32_t j0 = jg;
-    for (int t = u.w.tile_begin; t < u.w.tile_end; ++t, ++jg) {
-      const int k = t - u.w.tile_begin;
-      const uint32_t nk = 2 * jg, nv_prev = 2 * jg - 1;
-      // PV_A of the previous tile frees S_A (P_A is read from it) before S_A(k) overwrites it
-      if (k > 0) {
-        mbar_wait(&S.p_full[0], (jg - 1) & 1);
-        trace(P, 1, tc, 20);  // 20: P_A ready
-        wait_kv(nv_prev);
-        issue_pv(0, nv_prev % kSlots, k == 1);
-      }
-      if (k == 0 || a.tiles[t].rot_delta != a.tiles[t - 1].rot_delta) {
-        qa = (2 * ep) % 3;
-        qb = (2 * ep + 1) % 3;
-        mbar_wait(&S.q_full[qa], ((2 * ep) / 3) & 1);
-        if (two) mbar_wait(&S.q_full[qb], ((2 * ep + 1) / 3) & 1);
-        trace(P, 1, tc, 21);  // 21: Q ready for new epoch
-        ++ep;
-      }
-      wait_kv(nk);
-      trace(P, 1, tc, 22);  // 22: K ready, S_A issued
-      issue_s(0, qa, nk % kSlots);
-      // last S of this epoch: release each Q tile right after its last MMA is issued, so the
-      // next epoch's head-B tile (which reuses this epoch's A slot) is prepared ~2 tiles early
-      const bool epoch_ends = t + 1 == u.w.tile_end || a.tiles[t + 1].rot_delta != a.tiles[t].rot_delta;
-      if (epoch_ends) mma_commit(&S.q_empty[qa]);
-      if (two) {
-        if (k > 0) {
-          mbar_wait(&S.p_full[1], (jg - 1) & 1);
-          trace(P, 1, tc, 23);  // 23: P_B ready
-          issue_pv(1, nv_prev % kSlots, k == 1);
+    SubCursor cs{tb, 0}, cp{tb, 0};
+    uint32_t js = jg;  // global index of the next S sub-tile
+    // S for sub-tile cs of head x (buffer js & 1); handles epoch changes and K arrival
+    auto issue_s = [&](int x) {
+      const int t = cs.t;
+      if (x == 0 && cs.h == 0) {
+        if (t == tb || a.tiles[t].rot_delta != a.tiles[t - 1].rot_delta) {
+          if (t != tb) {  // the previous epoch's Q tiles: free once the S MMAs issued so far are done
+            mma_commit(&S.q_empty[qa]);
+            mma_commit(&S.q_empty[qb]);
+          }
+          qa = (2 * ep) % 3;
+          qb = (2 * ep + 1) % 3;
+          mbar_wait(&S.q_full[qa], ((2 * ep) / 3) & 1);
+          if (two) mbar_wait(&S.q_full[qb], ((2 * ep + 1) / 3) & 1);
+          trace(P, 1, tc, 21);  // 21: Q ready for new epoch
+          ++ep;
         }
-        if (k > 0) mma_commit(&S.kv_empty[nv_prev % kSlots]);  // V_{k-1} consumed
-        issue_s(1, qb, nk % kSlots);
-      } else if (k > 0) {
-        mma_commit(&S.kv_empty[nv_prev % kSlots]);
+        wait_kv(2 * (kbase_g + (t - tb)));
+        trace(P, 1, tc, 22);  // 22: K ready
       }
-      mma_commit(&S.kv_empty[nk % kSlots]);  // K_k consumed
-      if (epoch_ends) mma_commit(&S.q_empty[qb]);
+      const uint32_t kslot = (2 * (kbase_g + (t - tb))) % kSlots;
+      const uint32_t qbase = smem_u32(&S.q[x == 0 ? qa : qb][0][0]);
+      const uint32_t kb = smem_u32(&S.kv[kslot][0][0]) + cs.h * 64 * 128;
+      const int buf = js & 1;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t off = (kk / 4) * TcSmem<D>::kChunkBytes + (kk % 4) * 32;
+        mma_ss(tmem + kColS + 128 * x + 64 * buf, desc_sw128(qbase + off, 16, 1024), desc_sw128(kb + off, 16, 1024),
+               idS, kk > 0 ? 1u : 0u);
+      }
+      mma_commit(&S.s_full[x][buf]);
+    };
+    // after both heads' S of cursor cs: release K when its last sub-tile is done; end of item
+    // releases the Q tiles
+    auto finish_s = [&]() {
+      const int t = cs.t;
+      const bool last_of_tile = cs.h == nsub(t) - 1;
+      if (last_of_tile) mma_commit(&S.kv_empty[(2 * (kbase_g + (t - tb))) % kSlots]);
+      advance(cs);
+      ++js;
+      if (cs.t >= te) {
+        mma_commit(&S.q_empty[qa]);
+        mma_commit(&S.q_empty[qb]);
+      }
+    };
+    auto issue_pv = [&](int x, uint32_t j, bool first) {
+      const int t = cp.t;
+      if (x == 0 && cp.h == 0) wait_kv(2 * (kbase_g + (t - tb)) + 1);
+      const uint32_t vslot = (2 * (kbase_g + (t - tb)) + 1) % kSlots;
+      const uint32_t vb = smem_u32(&S.kv[vslot][0][0]) + cp.h * 64 * 128;
+      const int buf = j & 1;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint64_t vd = desc_sw128(vb + kk * 2048, 16384, 1024);
+        mma_ts(tmem + kColO + 128 * x, tmem + kColS + 128 * x + 64 * buf + kk * 8, vd, idO,
+               (!first || kk > 0) ? 1u : 0u);
+      }
+      mma_commit(&S.o_done[x]);
+    };
+    // prologue: S for the first two sub-tiles
+    for (int i = 0; i < 2 && cs.t < te; ++i) {
+      issue_s(0);
+      if (two) issue_s(1);
+      finish_s();
     }
-    // drain: PV of the last tile
-    const uint32_t nv_last = 2 * jg - 1;
-    const bool single_tile = jg - j0 == 1;
-    mbar_wait(&S.p_full[0], (jg - 1) & 1);
-    trace(P, 1, tc, 24);  // 24: drain P_A ready
-    wait_kv(nv_last);
-    issue_pv(0, nv_last % kSlots, single_tile);
-    mma_commit(&S.o_full[0]);
-    if (two) {
-      mbar_wait(&S.p_full[1], (jg - 1) & 1);
-      issue_pv(1, nv_last % kSlots, single_tile);
-      mma_commit(&S.o_full[1]);
+    bool first = true;
+    while (cp.t < te) {
+      const uint32_t j = jg;
+      mbar_wait(&S.p_full[0][j & 1], (j >> 1) & 1);
+      trace(P, 1, tc, 20);  // 20: P_A ready
+      issue_pv(0, j, first);
+      if (two) {
+        mbar_wait(&S.p_full[1][j & 1], (j >> 1) & 1);
+        trace(P, 1, tc, 23);  // 23: P_B ready
+        issue_pv(1, j, first);
+      }
+      // V is released before the next S pair: with one-sub-tile tiles the S cursor runs two KV
+      // tiles ahead and, in a 3-slot ring, K_{t+2} reuses V_t's slot
+      if (cp.h == nsub(cp.t) - 1) mma_commit(&S.kv_empty[(2 * (kbase_g + (cp.t - tb)) + 1) % kSlots]);
+      if (cs.t < te) {
+        issue_s(0);
+        if (two) issue_s(1);
+        finish_s();
+      }
+      advance(cp);
+      ++jg;
+      first = false;
     }
-    mma_commit(&S.kv_empty[nv_last % kSlots]);
+    kbase_g += te - tb;
   }
 }
 
-// pass 2 of the softmax over one 128-key S row in TMEM: P = exp2(s*scale - m) written back as
-// packed bf16 over the first 64 columns; per-row sums in 8 independent accumulators.
+// pass 2 of the softmax over one 64-key S sub-tile row in TMEM: P = exp2(s*scale - m) written
+// back as packed bf16 over its first 32 columns; per-row sums in 8 independent accumulators.
 template <int PM, bool kMasked>
 __device__ __forceinline__ void exp_pass(uint32_t scol, float sl2, float msub, int lim, float (&sum8)[8]) {
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < 2; ++c) {
     uint32_t v[32];
     tmem_ld32(scol + c * 32, v);
     tmem_wait_ld();
@@ -264,9 +311,14 @@ __device__ __forceinline__ void exp_pass(uint32_t scol, float sl2, float msub, i
       const int j0 = c * 32 + 2 * i;
       const float x0 = fmaf(__uint_as_float(v[2 * i]), sl2, -msub);
       const float x1 = fmaf(__uint_as_float(v[2 * i + 1]), sl2, -msub);
-      constexpr bool kPoly[4] = {0 < PM, 1 < PM, 2 < PM, 3 < PM};
-      float p0 = kPoly[i & 3] ? exp2_poly(x0) : ex2_approx(x0);
-      float p1 = kPoly[i & 3] ? exp2_poly(x1) : ex2_approx(x1);
+      float p0, p1;
+      if constexpr (PM == 3) {
+        ex2_pair_f16(x0, x1, p0, p1);
+      } else {
+        constexpr bool kPoly[4] = {0 < PM, 1 < PM, 2 < PM, 3 < PM};
+        p0 = kPoly[i & 3] ? exp2_poly(x0) : ex2_approx(x0);
+        p1 = kPoly[i & 3] ? exp2_poly(x1) : ex2_approx(x1);
+      }
       if (kMasked) {
         p0 = (j0 <= lim) ? p0 : 0.f;
         p1 = (j0 + 1 <= lim) ? p1 : 0.f;
@@ -287,9 +339,8 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
   const int r = threadIdx.x & 127;  // row within the tile == TMEM lane
   const uint32_t lane_base = static_cast<uint32_t>((r / 32) * 32) << 16;
   const float sl2 = P.scale_log2;
-  const uint32_t scol = tmem + lane_base + kColS + 128 * x;
   const uint32_t ocol = tmem + lane_base + kColO + 128 * x;
-  uint32_t st = 0, itc = 0;
+  uint32_t js = 0, od = 0;  // sub-tiles processed, o_done phases consumed
   uint32_t tc = 0;
   const bool tr = (threadIdx.x & 127) == 0;
   for (int ii = it_begin; ii < it_end; ++ii) {
@@ -301,128 +352,149 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
     const int64_t row = static_cast<int64_t>(w.row0) + r;
     const int p = valid ? a.pos[row] : 0;
     float m = -INFINITY, l = 0.f;
-    for (int t = w.tile_begin; t < w.tile_end; ++t, ++st) {
+    bool first = true;
+    for (int t = w.tile_begin; t < w.tile_end; ++t) {
       const KvTile tl = a.tiles[t];
-      const int lim = min(tl.n_valid - 1, tl.causal ? p - tl.key_pos0 : kTileKeys - 1);
-      mbar_wait(&S.s_full[x], st & 1);
-      if (tr) trace(P, 2 + x, tc, 30);  // 30: S ready
-      tc_fence_after();
-      if (P.dbg_mode == 1 || P.dbg_mode >= 3) {
-        tc_fence_before();
-        mbar_arrive(&S.p_full[x]);
-        continue;
-      }
-      // pass 1: row max (8 independent accumulators); masks only on partial tiles
-      const bool full = __all_sync(0xffffffffu, lim >= kTileKeys - 1);
-      float mx8[8];
+      const int nsub = tl.n_valid > 64 ? 2 : 1;
+      for (int hh = 0; hh < nsub; ++hh, ++js) {
+        const int buf = js & 1;
+        const uint32_t scol = tmem + lane_base + kColS + 128 * x + 64 * buf;
+        // key index i of this sub-tile is visible iff i <= lim
+        const int lim = min(tl.n_valid - 1, tl.causal ? p - tl.key_pos0 : kTileKeys - 1) - 64 * hh;
+        mbar_wait(&S.s_full[x][buf], (js >> 1) & 1);
+        if (tr) trace(P, 2 + x, tc, 30);  // 30: S ready
+        tc_fence_after();
+        // pass 1: row max (8 independent accumulators); masks only on partial sub-tiles
+        const bool full = __all_sync(0xffffffffu, lim >= 63);
+        float mx8[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
+        for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld32(scol + c * 32, v);
-        tmem_wait_ld();
-        if (full) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v[i]));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c * 32 + i <= lim) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v[i]));
-        }
-      }
-      float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-      mx *= sl2;
-      const float m_new = fmaxf(m, mx);
-      const bool resc = m_new > m + P.rescale_threshold;
-      const float m_use = resc ? m_new : m;
-      const float alpha = resc ? ex2_approx(m - m_new) : 1.f;
-      const float msub = (m_use == -INFINITY) ? 0.f : m_use;
-      // O_x is stable here (PV_x(j-1) was issued before S_x(j)): rescale it if the max grew
-      if (t > w.tile_begin && __any_sync(0xffffffffu, resc)) {
-#pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
+        for (int c = 0; c < 2; ++c) {
           uint32_t v[32];
-          tmem_ld32(ocol + c * 32, v);
+          tmem_ld32(scol + c * 32, v);
           tmem_wait_ld();
+          if (full) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-          tmem_st32(ocol + c * 32, v);
+            for (int i = 0; i < 32; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v[i]));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c * 32 + i <= lim) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v[i]));
+          }
         }
-      }
-      if (P.dbg_mode == 2) {
-        l += mx;
-        tc_fence_before();
-        mbar_arrive(&S.p_full[x]);
-        continue;
-      }
-      // pass 2: P = exp2(s*scale - m) -> bf16 over the first 64 columns of S_x; the mask is a
-      // compile-time template flag so fully visible tiles carry no per-key compare/select
-      float sum8[8];
+        float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        mx *= sl2;
+        const float m_new = fmaxf(m, mx);
+        const bool resc = m_new > m + P.rescale_threshold;
+        const float m_use = resc ? m_new : m;
+        const float alpha = resc ? ex2_approx(m - m_new) : 1.f;
+        const float msub = (m_use == -INFINITY) ? 0.f : m_use;
+        // pass 2: P = exp2(s*scale - m) -> bf16 over the first 32 columns of the sub-tile
+        float sum8[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) sum8[i] = 0.f;
-      if (full)
-        exp_pass<PM, false>(scol, sl2, msub, lim, sum8);
-      else
-        exp_pass<PM, true>(scol, sl2, msub, lim, sum8);
-      const float sum = ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) + ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
-      l = l * alpha + sum;
-      m = m_use;
-      tc_fence_before();
-      if (tr) trace(P, 2 + x, tc, 31);  // 31: P written
-      mbar_arrive(&S.p_full[x]);
+        for (int i = 0; i < 8; ++i) sum8[i] = 0.f;
+        if (full)
+          exp_pass<PM, false>(scol, sl2, msub, lim, sum8);
+        else
+          exp_pass<PM, true>(scol, sl2, msub, lim, sum8);
+        const float sum = ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) + ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
+        l = l * alpha + sum;
+        m = m_use;
+        // PV of the previous sub-tile must have landed in O before O is rescaled (and before
+        // PV of this sub-tile accumulates onto it): one o_done phase per PV, consumed in order
+        if (!first) {
+          mbar_wait(&S.o_done[x], od & 1);
+          ++od;
+          tc_fence_after();
+          if (__any_sync(0xffffffffu, resc)) {
+#pragma unroll 1
+            for (int c = 0; c < D / 32; ++c) {
+              uint32_t v[32];
+              tmem_ld32(ocol + c * 32, v);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+              tmem_st32(ocol + c * 32, v);
+            }
+            tmem_wait_st();
+          }
+        }
+        first = false;
+        tc_fence_before();
+        if (tr) trace(P, 2 + x, tc, 31);  // 31: P written
+        mbar_arrive(&S.p_full[x][buf]);
+      }
     }
     // epilogue: wait for the last PV of this head, normalise, store
-    mbar_wait(&S.o_full[x], itc & 1);
+    mbar_wait(&S.o_done[x], od & 1);
+    ++od;
     if (tr) trace(P, 2 + x, tc, 32);  // 32: O ready (epilogue start)
-    ++itc;
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     const float lse = l > 0.f ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
-    // O tile -> global through a per-warp 32x32 fp32 smem transpose (16 B units XOR-swizzled by
-    // row): each store instruction then writes 4 rows x 128 B of full lines instead of 32 rows
-    // x 16 B scattered 16 KB apart.
+    // O tile -> global: each warp stages 32 rows x 32 fp32 columns in its 4 KB SWIZZLE_128B buffer
+    // and one lane hands it to a TMA bulk store (async: the warp only waits until the TMA has
+    // READ the buffer before reusing it, never for the HBM write).
     {
       const int wr = (threadIdx.x / 32) & 3;  // warp's 32-row slice of the tile
       const int lane = threadIdx.x & 31;
       float* stg = S.stage[x * 4 + wr];
-      const int rr_base = wr * 32;
+      // TMA store for whole 32-row slices (and for split partials, whose padding rows are never
+      // read); a slice that ends inside this item's rows is written directly (the next rows
+      // belong to another item)
+      const bool in_range = wr * 32 < w.n_rows;
+      const bool use_tma = in_range && (w.part >= 0 || (a.out_fp32 && wr * 32 + 32 <= w.n_rows));
+      const bool direct = in_range && !use_tma;
 #pragma unroll 1
       for (int c = 0; c < D / 32; ++c) {
         uint32_t v[32];
         tmem_ld32(ocol + c * 32, v);
         tmem_wait_ld();
+        if (lane == 0) bulk_wait_read<0>();  // previous chunk's store has read the buffer
+        __syncwarp();
 #pragma unroll
         for (int u = 0; u < 8; ++u)
           *reinterpret_cast<float4*>(stg + lane * 32 + ((u ^ (lane & 7)) * 4)) =
               make_float4(__uint_as_float(v[4 * u]) * inv, __uint_as_float(v[4 * u + 1]) * inv,
                           __uint_as_float(v[4 * u + 2]) * inv, __uint_as_float(v[4 * u + 3]) * inv);
-        __syncwarp();
+        if (use_tma) {
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (w.part >= 0)
+              tma_store_2d(&P.tmop, stg, c * 32, (w.part * a.hq + h) * kTileRows + wr * 32);
+            else
+              tma_store_3d(&P.tmo, stg, c * 32, h, w.row0 + wr * 32);
+            bulk_commit();
+          }
+        } else {
+          __syncwarp();
+        }
+        if (direct) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int rr = j * 4 + (lane >> 3);  // row within the warp's slice
-          const int u = lane & 7;              // 16 B unit = 4 columns
-          const float4 val = *reinterpret_cast<const float4*>(stg + rr * 32 + ((u ^ (rr & 7)) * 4));
-          const int trow = rr_base + rr;
-          if (trow < w.n_rows) {
-            const int col = c * 32 + u * 4;
-            if (w.part >= 0) {
-              *reinterpret_cast<float4*>(a.opart + ((static_cast<int64_t>(w.part) * a.hq + h) * kTileRows + trow) * D +
-                                         col) = val;
-            } else if (a.out_fp32) {
-              *reinterpret_cast<float4*>(static_cast<float*>(a.o) + ((w.row0 + trow) * static_cast<int64_t>(a.hq) + h) * D +
-                                         col) = val;
-            } else {
-              uint2 pk;
-              pk.x = pack_bf16x2(val.x, val.y);
-              pk.y = pack_bf16x2(val.z, val.w);
-              *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.o) +
-                                        ((w.row0 + trow) * static_cast<int64_t>(a.hq) + h) * D + col) = pk;
+          for (int j = 0; j < 8; ++j) {
+            const int rr = j * 4 + (lane >> 3);
+            const int u = lane & 7;
+            const float4 val = *reinterpret_cast<const float4*>(stg + rr * 32 + ((u ^ (rr & 7)) * 4));
+            const int trow = wr * 32 + rr;
+            if (trow < w.n_rows) {
+              const int col = c * 32 + u * 4;
+              if (a.out_fp32) {
+                *reinterpret_cast<float4*>(static_cast<float*>(a.o) +
+                                           ((w.row0 + trow) * static_cast<int64_t>(a.hq) + h) * D + col) = val;
+              } else {
+                uint2 pk;
+                pk.x = pack_bf16x2(val.x, val.y);
+                pk.y = pack_bf16x2(val.z, val.w);
+                *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.o) +
+                                          ((w.row0 + trow) * static_cast<int64_t>(a.hq) + h) * D + col) = pk;
+              }
             }
           }
+          __syncwarp();
         }
-        __syncwarp();
       }
     }
     if (valid) {
@@ -596,9 +668,11 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
       mbar_init(&S.q_load[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&S.s_full[i], 1);
-      mbar_init(&S.p_full[i], 128);
-      mbar_init(&S.o_full[i], 1);
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&S.s_full[i][b], 1);
+        mbar_init(&S.p_full[i][b], 128);
+      }
+      mbar_init(&S.o_done[i], 1);
     }
     fence_barrier_init();
   }
@@ -628,6 +702,7 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
     reg_alloc<168>();
     run_qprep<D>(P, S, it_begin, it_end);
   }
+  if (warp >= 4 && warp < 12 && (threadIdx.x & 31) == 0) bulk_wait<0>();  // epilogue stores done
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -649,6 +724,8 @@ cudaError_t launch_dp(const AttnArgs& a, cudaStream_t st) {
   p.tmk = *a.tmap_k;
   p.tmv = *a.tmap_v;
   p.tmq = *a.tmap_q;
+  if (a.tmap_o) p.tmo = *a.tmap_o;
+  if (a.tmap_op) p.tmop = *a.tmap_op;
   p.a = a;
   p.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));
   p.paired = a.paired ? 1 : 0;
@@ -661,10 +738,11 @@ cudaError_t launch_dp(const AttnArgs& a, cudaStream_t st) {
 
 template <int D>
 cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
-  switch (a.poly_mask) {
+  switch (a.poly_mask) {  // 0: MUFU fp32, 1/2: 25%/50% FMA-pipe polynomial, 3: MUFU f16x2
     case 0: return launch_dp<D, 0>(a, st);
+    case 1: return launch_dp<D, 1>(a, st);
     case 2: return launch_dp<D, 2>(a, st);
-    default: return launch_dp<D, 1>(a, st);
+    default: return launch_dp<D, 3>(a, st);
   }
 }
 

@@ -118,7 +118,7 @@ bool paired(const spq_ctx* c) {
 
 int poly_mask() {
   const char* e = std::getenv("SPANQ_POLY_EXP");  // tuning knob: quarters of exp2 on the FMA pipe
-  return e ? std::max(0, std::min(4, std::atoi(e))) : 1;
+  return e ? std::max(0, std::min(3, std::atoi(e))) : 0;
 }
 
 // host-only contexts plan for a B200 (148 SMs) so their work lists match a GPU ctx's
@@ -175,6 +175,46 @@ spq_status make_qmap(const spq_ctx* c, const void* q, int64_t rows, CUtensorMap*
                                                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SPQ_ECUDA, "cuTensorMapEncodeTiled(q) failed: " + std::to_string(r));
+  return SPQ_OK;
+}
+
+// fp32 output maps for the epilogue's TMA stores: o as 3D {d, hq, rows} box {32, 1, 32};
+// partials as 2D {d, parts*hq*128} box {32, 32}; both SWIZZLE_128B (the staging layout)
+spq_status make_omap(const spq_ctx* c, const void* o, int64_t rows, CUtensorMap* out) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult qr;
+  CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
+  if (reinterpret_cast<uintptr_t>(o) & 15) return fail(SPQ_EINVAL, "o must be 16-byte aligned");
+  const spq_config& g = c->cfg;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.head_dim), static_cast<cuuint64_t>(g.num_q_heads),
+                        static_cast<cuuint64_t>(std::max<int64_t>(rows, 1))};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.head_dim) * 4,
+                           static_cast<cuuint64_t>(g.head_dim) * 4 * g.num_q_heads};
+  cuuint32_t box[3] = {32, 1, 32};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = reinterpret_cast<EncodeTiledFn>(fn)(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(o), dims,
+                                                   strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SPQ_ECUDA, "cuTensorMapEncodeTiled(o) failed: " + std::to_string(r));
+  return SPQ_OK;
+}
+
+spq_status make_partmap(const spq_ctx* c, const float* opart, int64_t parts, CUtensorMap* out) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult qr;
+  CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
+  const spq_config& g = c->cfg;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.head_dim),
+                        static_cast<cuuint64_t>(parts) * g.num_q_heads * spq::kTileRows};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.head_dim) * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = reinterpret_cast<EncodeTiledFn>(fn)(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(opart),
+                                                   dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SPQ_ECUDA, "cuTensorMapEncodeTiled(opart) failed: " + std::to_string(r));
   return SPQ_OK;
 }
 
@@ -619,11 +659,16 @@ spq_status spq_prefill_jobs(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, i
   args.o = o;
   args.lse = lse;
   args.layer = layer;
-  CUtensorMap qmap;
+  CUtensorMap qmap, omap;
   if (c->cfg.dtype == SPQ_BF16) {
     s = make_qmap(c, q, r1 - r0, &qmap);
     if (s != SPQ_OK) return s;
     args.tmap_q = &qmap;
+    if (c->cfg.out_dtype == SPQ_FP32) {
+      s = make_omap(c, o, r1 - r0, &omap);
+      if (s != SPQ_OK) return s;
+      args.tmap_o = &omap;
+    }
   }
   if (c->timing) CUDA_TRY(cudaEventRecord(c->ev[0], st));
   s = run_attn(c, args, st);
@@ -679,11 +724,21 @@ spq_status spq_join(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b
   args.o = o;
   args.lse = lse;
   args.layer = layer;
-  CUtensorMap qmap;
+  CUtensorMap qmap, omap, pmap;
   if (c->cfg.dtype == SPQ_BF16) {
     s = make_qmap(c, q, r1 - r0, &qmap);
     if (s != SPQ_OK) return s;
     args.tmap_q = &qmap;
+    if (c->cfg.out_dtype == SPQ_FP32) {
+      s = make_omap(c, o, r1 - r0, &omap);
+      if (s != SPQ_OK) return s;
+      args.tmap_o = &omap;
+    }
+    if (w.n_parts > 0 && opart != nullptr) {
+      s = make_partmap(c, opart, w.n_parts, &pmap);
+      if (s != SPQ_OK) return s;
+      args.tmap_op = &pmap;
+    }
   }
   if (c->timing) CUDA_TRY(cudaEventRecord(c->ev[2], st));
   s = run_attn(c, args, st);

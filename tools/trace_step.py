@@ -32,7 +32,7 @@ del os.environ["SPANQ_TRACE"]
 t = buf.view(5, 1024, 2).cpu().numpy()
 names = {10: "K issue", 11: "V issue", 20: "P_A rdy", 21: "Q rdy", 22: "S_A issue", 23: "P_B rdy", 24: "drain P_A",
          30: "S rdy", 31: "P done", 32: "O rdy", 33: "epi done", 40: "slotA free", 41: "slotB free", 42: "QA done",
-         43: "QB done"}
+         43: "QB done", 34: "max done", 35: "exp start"}
 roles = ["tma", "mma", "smxA", "smxB", "qprep"]
 t0 = min(t[r][0][1] for r in range(5) if t[r][0][1] > 0)
 ev = []
