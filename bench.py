@@ -88,6 +88,17 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def ncu_traffic(kernel: str):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed `ncu --set full`
+    capture of this workload (profiles/ncu_traffic.json, written by tools/ncu_summary.py), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)[kernel]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def cpu_baseline(budget_s: float = 15.0):
     """The fp64 oracle (as it stands) on a bounded sample of C2: fragment jobs one by one and
     then join rows in chunks until the time budget is spent; TFLOP/s = algorithmic FLOPs of the
@@ -159,6 +170,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="spanq", choices=["spanq", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--layers", type=int, default=40,
+                    help="attention layers per step (40 = the 8B model's depth; 1 = a single layer)")
     ap.add_argument("--out-dtype", default="fp32", choices=["fp32", "bf16"])
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
@@ -180,11 +193,13 @@ def main():
     from paper_2511_02749_b200 import inputs, runner, spanq
 
     w = inputs.c2(seed=2 + rank)  # each rank: its own independent query (weak scaling)
-    s = w.shape
+    L = args.layers
+    s = inputs.Shape(**{**w.shape.__dict__, "layers": L})
     ctx = spanq.Context(s, 512, device=local, max_position=1 << 15, out_dtype=args.out_dtype)
     stream = torch.cuda.Stream(dev)
     tab = runner.device_tables(s, 0, w.seed, dev)
-    # stage this query's packed q/k/v rows once (resident in HBM during the timed region)
+    # stage this query's packed q/k/v rows once (resident in HBM during the timed region). Every
+    # layer reads the same synthetic q/k/v (> L2 per layer: ~210 MB) into its own KV-pool layer.
     p0 = ctx.plan(w.queries, stream=stream)
     view = p0.view()
     ptok, jtok = runner.prefill_tokens(view, w.queries), runner.join_tokens(view, w.queries)
@@ -196,16 +211,41 @@ def main():
     oj = torch.empty((len(jtok), s.hq, s.d), dtype=odt, device=dev)
     lj = torch.empty((len(jtok), s.hq), dtype=torch.float32, device=dev)
     p0.release(stream=stream)
-    flops = view["prefill_flops"] + view["join_flops"]
+    flops_layer = view["prefill_flops"] + view["join_flops"]
     kv_bytes = view["prefill_kv_bytes"] + view["join_kv_bytes"]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
-    def step(timing_events=None):
+    def step(layers=L, inp=(qp, kp, vp, qj, kj, vj), d2h=None):
         ctx.evict_all()  # cold cache
         plan = ctx.plan(w.queries, stream=stream)
-        plan.prefill(0, qp, kp, vp, op, lp, stream=stream)
-        plan.join(0, qj, kj, vj, oj, lj, stream=stream)
+        for layer in range(layers):
+            plan.prefill(layer, inp[0], inp[1], inp[2], op, lp, stream=stream)
+            plan.join(layer, inp[3], inp[4], inp[5], oj, lj, stream=stream)
+        if d2h is not None:  # the step's result: the join output of the last layer
+            d2h[0].copy_(oj, non_blocking=True)
+            d2h[1].copy_(lj, non_blocking=True)
         plan.release(stream=stream)
+
+    def timed(n, layers=L, pre=None, d2h=None, attn=None):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        for i in range(n):
+            flush.zero_()
+            stream.synchronize()
+            evs[i][0].record(stream)
+            inp = pre() if pre is not None else (qp, kp, vp, qj, kj, vj)
+            step(layers, inp, d2h)
+            evs[i][1].record(stream)
+            stream.synchronize()
+            if attn is not None:
+                attn.append(ctx.last_attn_ms())
+        return [a.elapsed_time(b) for a, b in evs]
+
+    def max_over_ranks(x):
+        if world > 1:
+            t = torch.tensor([x], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            return float(t.item())
+        return x
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
@@ -214,64 +254,41 @@ def main():
         # ---- timed region: K steps, events on the launching stream, L2 flushed between steps
         ctx.set_timing(True)
         n0 = ctx.launch_count()
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         attn_ms = []
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
         with ClockSampler(local) as clk:
-            for i in range(args.steps):
-                flush.zero_()
-                ev[i][0].record(stream)
-                step()
-                ev[i][1].record(stream)
-                stream.synchronize()
-                attn_ms.append(ctx.last_attn_ms())
+            step_ms = timed(args.steps, attn=attn_ms)
         torch.cuda.synchronize()
         launches = ctx.launch_count() - n0
         ctx.set_timing(False)
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = float(sum(step_ms))
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
+        # single-layer TTFT (plan + one layer of prefill + join), same protocol
+        l1_ms = timed(max(3, args.steps // 2), layers=1) if L > 1 else step_ms
+    total_ms = max_over_ranks(float(sum(step_ms)))
     ms_per_step = total_ms / args.steps
+    flops = flops_layer * L
     value = world * flops * args.steps / (total_ms / 1e3) / 1e12
 
-    # ---- e2e through the public API with host buffers: H2D of the step's inputs (pinned) and
-    # D2H of the step's result (join O + LSE) inside the timed region
+    # ---- e2e through the public API with host buffers: H2D of the step's inputs (pinned; the
+    # q/k/v all layers read) and D2H of the step's result (last layer's join O + LSE) inside the
+    # timed region
     hq = [t.cpu().pin_memory() for t in (qp, kp, vp, qj, kj, vj)]
     h2d = sum(t.numel() * t.element_size() for t in hq)
     oj_h = torch.empty(oj.shape, dtype=oj.dtype).pin_memory()
     lj_h = torch.empty(lj.shape, dtype=lj.dtype).pin_memory()
     d2h = oj_h.numel() * oj_h.element_size() + lj_h.numel() * lj_h.element_size()
     dq = [torch.empty_like(t, device=dev) for t in hq]
-    e2e_ms = []
+
+    def upload():
+        for d_, h_ in zip(dq, hq):
+            d_.copy_(h_, non_blocking=True)
+        return dq
+
     with torch.cuda.stream(stream):
-        for i in range(args.warmup + args.steps):
-            flush.zero_()
-            stream.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            for d_, h_ in zip(dq, hq):
-                d_.copy_(h_, non_blocking=True)
-            ctx.evict_all()
-            plan = ctx.plan(w.queries, stream=stream)
-            plan.prefill(0, dq[0], dq[1], dq[2], op, lp, stream=stream)
-            plan.join(0, dq[3], dq[4], dq[5], oj, lj, stream=stream)
-            oj_h.copy_(oj, non_blocking=True)
-            lj_h.copy_(lj, non_blocking=True)
-            plan.release(stream=stream)
-            b.record(stream)
-            stream.synchronize()
-            if i >= args.warmup:
-                e2e_ms.append(a.elapsed_time(b))
-    e2e_total = float(sum(e2e_ms))
-    if world > 1:
-        t = torch.tensor([e2e_total], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_total = float(t.item())
+        timed(args.warmup, pre=upload, d2h=(oj_h, lj_h))
+        e2e_ms = timed(args.steps, pre=upload, d2h=(oj_h, lj_h))
+    e2e_total = max_over_ranks(float(sum(e2e_ms)))
     e2e_value = world * flops * args.steps / (e2e_total / 1e3) / 1e12
 
     peak_burst, peak_sust, hbm, peak_src = peaks()
@@ -283,23 +300,26 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": "C2 RAG span query (configs[1]): P512 + 16x1024 plus-fragments + 256 cross, cold cache",
-                   "model": "8B GQA attention shape Hq32/Hkv8/d128, 1 layer, random tables",
+                   "model": f"8B GQA attention shape Hq32/Hkv8/d128, {L} layers (same synthetic q/k/v per layer, "
+                            "own KV-pool layer each), random tables",
+                   "layers": L,
                    "global_batch": world, "seq_len": int(view["prefill_flops"] > 0) and 17152,
                    "block_size": s.block_size, "out_dtype": args.out_dtype,
                    "parallelism": f"dp{world} (independent queries per rank)",
                    "l2": "flushed between steps (256 MB write)"},
         "ttft_ms": ms_per_step,
+        "ttft_l1_ms": statistics.median(l1_ms),
         "step_ms_p50": statistics.median(step_ms), "step_ms_p99": float(np.percentile(step_ms, 99)),
-        "flops_per_step": flops,
+        "flops_per_step": flops, "flops_per_layer": flops_layer,
         "roofline": {"kernel": "span_attn_tc (fragment+prefix prefill, K2)", "bound": "tensor",
                      "achieved": achieved, "peak": peak_burst, "unit": "TFLOP/s",
-                     "frac": achieved / peak_burst, "traffic": None,
+                     "frac": achieved / peak_burst, "traffic": ncu_traffic("span_attn_tc prefill"),
                      "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)" if peak_src == "measured" else "fallback",
                      "kernel_ms": pre_ms, "algorithmic_flops": view["prefill_flops"]},
         "join_kernel": {"kernel": "span_attn_tc (join, K3)", "ms": join_ms,
                         "achieved": view["join_flops"] / (join_ms / 1e3) / 1e12 if join_ms > 0 else None,
                         "frac": (view["join_flops"] / (join_ms / 1e3) / 1e12) / peak_burst if join_ms > 0 else None},
-        "kv_write_bytes_per_step": kv_bytes,
+        "kv_write_bytes_per_step": kv_bytes * L,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),

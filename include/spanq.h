@@ -58,8 +58,9 @@ typedef struct {
   void *k_pool;         /* device, CALLER-owned, [L][num_blocks][Hkv][bs][d]; must outlive ctx */
   void *v_pool;         /* device, CALLER-owned, same layout                                 */
   int32_t device;       /* CUDA device ordinal; -1 = host-only ctx (planner/store, no kernels) */
-  int32_t rank;         /* reserved (multi-GPU): this rank, 0..world_size-1                  */
-  int32_t world_size;   /* reserved (multi-GPU): must be 1 in this version                   */
+  int32_t rank;         /* this rank, 0..world_size-1 (SURVEY §8(e) partitioning)             */
+  int32_t world_size;   /* ranks sharing a batch: query q is homed on q mod W, fragment f owned
+                           by u64le(s_last(f)[0:8]) mod W; each rank plans only its share       */
   int32_t out_dtype;    /* spq_dtype of o (attention outputs); SPQ_FP32 is allowed with a bf16
                            ctx (bf16 MMAs, fp32 outputs: removes the final bf16 rounding of O)  */
 } spq_config;
@@ -144,6 +145,18 @@ typedef struct {
   double join_flops;          /* same for all joins                                          */
   int64_t prefill_kv_bytes;   /* K/V bytes written by rope_kv_write for prefill rows         */
   int64_t join_kv_bytes;
+  /* world_size > 1: queries homed here (q mod W == rank) and the fragment-KV
+   * exchange lists. Peer w: send_blocks[send_off[w] .. send_off[w+1]) are this rank's blocks of
+   * the fragments it owns that w's joins read; recv_blocks[recv_off[w] .. recv_off[w+1]) are the
+   * plan-private blocks that receive the fragments owned by w. Fragments in first-occurrence
+   * (query, ⊕) order, each fragment's blocks in order — both sides derive the same lists. With
+   * world_size 1 all lists are empty. */
+  int32_t n_join_queries;
+  int32_t world_size;
+  const int64_t *send_off;    /* [world_size+1] */
+  const int32_t *send_blocks;
+  const int64_t *recv_off;    /* [world_size+1] */
+  const int32_t *recv_blocks;
 } spq_plan_view;
 /* Read-only host arrays, valid until spq_plan_release. */
 spq_status spq_plan_view_get(const spq_plan *plan, spq_plan_view *out);
@@ -167,6 +180,17 @@ spq_status spq_prefill_jobs(spq_ctx *ctx, spq_plan *plan, int32_t layer, int32_t
  * same stream (their KV is read here). */
 spq_status spq_join(spq_ctx *ctx, spq_plan *plan, int32_t layer, int32_t q_begin, int32_t q_end,
                     const void *q, const void *k, const void *v, void *o, float *lse, void *stream);
+
+/* Fragment-KV exchange, HBM side. One layer's blocks of the plan's exchange list
+ * for `peer` (see spq_plan_view) are copied between the pool and a packed device buffer laid out
+ * [n][2 (K then V)][Hkv][bs][d] in the pool dtype, n = send (pack) or recv (unpack) block count.
+ * The transfer between ranks is the caller's (one NCCL all-to-all per layer). Pack must follow
+ * the prefill jobs that write those blocks on `stream`; unpack must precede spq_join. Blocks are
+ * copied whole (pads included: the owner zero-filled them). SPQ_ESTATE on a bad peer/layer. */
+spq_status spq_exchange_pack(spq_ctx *ctx, spq_plan *plan, int32_t layer, int32_t peer, void *buf,
+                             void *stream);
+spq_status spq_exchange_unpack(spq_ctx *ctx, spq_plan *plan, int32_t layer, int32_t peer,
+                               const void *buf, void *stream);
 
 /* Stream-ordered release: unpins the plan's blocks and frees its plan-private blocks; later
  * kernel calls on any stream wait for `stream` to pass this point before touching them. */

@@ -68,6 +68,11 @@ class PlanView:
     stats: Dict[str, int]
     pinned: List[int]
     private: List[int]
+    # multi-rank exchange: blocks this rank sends to / receives from each peer,
+    # fragments in first-occurrence order, each fragment's blocks in order
+    send: Dict[int, List[int]] = field(default_factory=dict)
+    recv: Dict[int, List[int]] = field(default_factory=dict)
+    n_join_queries: int = 0
 
 
 class Store:
@@ -125,16 +130,21 @@ class Store:
         return out
 
     # -------------------------------------------------------------- planner
-    def plan(self, queries: Sequence[Tuple[np.ndarray, List[np.ndarray], np.ndarray]]) -> PlanView:
+    def plan(self, queries: Sequence[Tuple[np.ndarray, List[np.ndarray], np.ndarray]],
+             rank: int = 0, world: int = 1) -> PlanView:
+        """Plan a batch. With world > 1 this is rank `rank`'s share: query q is
+        homed on q mod W (its prefix, join and cross run there), fragment f is owned by
+        u64le(s_last[0:8]) mod W (it is prefilled and cached only there); a home rank receives
+        remote-owned fragments into plan-private blocks, in first-occurrence order."""
         saved = copy.deepcopy((self.index, self.meta, self.free, self.pins, self.plan_no,
                                self.stats))
         try:
-            return self._plan(queries)
+            return self._plan(queries, rank, world)
         except OracleENOMEM:
             (self.index, self.meta, self.free, self.pins, self.plan_no, self.stats) = saved
             raise
 
-    def _plan(self, queries) -> PlanView:
+    def _plan(self, queries, rank: int = 0, world: int = 1) -> PlanView:
         bs = self.bs
         self.plan_no += 1
         p = self.plan_no
@@ -163,21 +173,45 @@ class Store:
                 pad_slots.extend(range(b * bs + ntok, b * bs + bs))
             return b
 
-        def new_private(ntok) -> int:
+        def new_private(ntok, pad=True) -> int:
             b = self._alloc()
             private.append(b)
             pin(b)
-            pad_slots.extend(range(b * bs + ntok, b * bs + bs))
+            if pad:
+                pad_slots.extend(range(b * bs + ntok, b * bs + bs))
             return b
+
+        send: Dict[int, List[bytes]] = {}
+        recv: Dict[int, List[bytes]] = {}
+        owned_blocks: Dict[bytes, List[int]] = {}
+        recv_blocks: Dict[bytes, List[int]] = {}
 
         segs: List[Segment] = []
         joins: List[bytes] = []
+        n_home = 0
         for qi, (prefix, frags, cross) in enumerate(queries):
             prefix = np.asarray(prefix)
             cross = np.asarray(cross)
+            home = qi % world
+            is_home = home == rank
+            h = hashing.prefix_chain(prefix, bs, self.root)
+            if not is_home:
+                joins.append(bytes(16))  # join digests are per query; zero where homed elsewhere
+                # only the fragments this rank owns: prefill/cache them and send them home
+                for fi, f in enumerate(frags):
+                    sf = hashing.fragment_chain(f, bs, self.root)
+                    if hashing.owner_rank(sf[-1], world) != rank:
+                        continue
+                    seg = self._frag_segment(qi, fi, f, sf, 0, touch, pin, insert_new)
+                    segs.append(seg)
+                    owned_blocks.setdefault(sf[-1], seg.blocks)
+                    lst = send.setdefault(home, [])
+                    if sf[-1] not in lst:
+                        lst.append(sf[-1])
+                continue
+            n_home += 1
             self.stats["input_tokens"] += len(prefix) + sum(len(f) for f in frags) + len(cross)
             # ---- prefix: chained digests, prefix scan
-            h = hashing.prefix_chain(prefix, bs, self.root)
             blocks, write = [], []
             hit_run, n_hit = True, 0
             for i, dig in enumerate(h):
@@ -213,35 +247,22 @@ class Store:
             off = len(prefix)
             lasts = []
             for fi, f in enumerate(frags):
-                s = hashing.fragment_chain(f, bs, self.root)
-                lasts.append(s[-1])
-                self.stats["lookups"] += 1
-                resident = [self.index.get(dig, -1) for dig in s]
-                if all(b >= 0 for b in resident):
-                    for b in resident:
-                        touch(b)
-                        pin(b)
-                    self.stats["hit_blocks"] += len(s)
-                    self.stats["hit_tokens"] += len(f)
-                    segs.append(Segment(qi, KIND_FRAG, fi, len(f), off, resident, s, 1,
-                                        len(f), [False] * len(s)))
+                sf = hashing.fragment_chain(f, bs, self.root)
+                lasts.append(sf[-1])
+                owner = hashing.owner_rank(sf[-1], world)
+                if owner == rank:
+                    seg = self._frag_segment(qi, fi, f, sf, off, touch, pin, insert_new)
+                    owned_blocks.setdefault(sf[-1], seg.blocks)
                 else:
-                    self.stats["miss_blocks"] += len(s)
-                    # resident blocks are pinned before any allocation of this fragment, so
-                    # an eviction cannot reclaim a block the fragment is about to read
-                    for b in resident:
-                        if b >= 0:
-                            touch(b)
-                            pin(b)
-                    blocks, write = [], []
-                    for i, dig in enumerate(s):
-                        if resident[i] >= 0:
-                            blocks.append(resident[i])
-                            write.append(False)
-                        else:
-                            blocks.append(insert_new(dig, min(bs, len(f) - i * bs)))
-                            write.append(True)
-                    segs.append(Segment(qi, KIND_FRAG, fi, len(f), off, blocks, s, 0, 0, write))
+                    # remote-owned: received into plan-private blocks (owner's pages include
+                    # its zeroed pads), no prefill here
+                    if sf[-1] not in recv_blocks:
+                        recv_blocks[sf[-1]] = [new_private(min(bs, len(f) - i * bs), pad=False)
+                                               for i in range(len(sf))]
+                        recv.setdefault(owner, []).append(sf[-1])
+                    seg = Segment(qi, KIND_FRAG, fi, len(f), off, recv_blocks[sf[-1]], sf, 0,
+                                  len(f), [False] * len(sf))
+                segs.append(seg)
                 off += len(f)
             j = hashing.join_fold(h_last, lasts)
             joins.append(j)
@@ -287,10 +308,42 @@ class Store:
                 jp += a
                 js += b
                 jg += [i] * len(a)
+        send_b = {d: [b for dig in lst for b in owned_blocks[dig]] for d, lst in send.items()}
+        recv_b = {o: [b for dig in lst for b in recv_blocks[dig]] for o, lst in recv.items()}
         return PlanView(segs, joins, np.asarray(pp, np.int32), np.asarray(ps, np.int64),
                         np.asarray(pg, np.int32), np.asarray(jp, np.int32),
                         np.asarray(js, np.int64), np.asarray(jg, np.int32),
-                        np.asarray(pad_slots, np.int64), jobs, dict(self.stats), pinned, private)
+                        np.asarray(pad_slots, np.int64), jobs, dict(self.stats), pinned, private,
+                        send_b, recv_b, n_home)
+
+    def _frag_segment(self, qi, fi, f, s, off, touch, pin, insert_new) -> Segment:
+        """All-or-nothing fragment lookup (R10, R11) with pin-before-alloc (R24)."""
+        bs = self.bs
+        self.stats["lookups"] += 1
+        resident = [self.index.get(dig, -1) for dig in s]
+        if all(b >= 0 for b in resident):
+            for b in resident:
+                touch(b)
+                pin(b)
+            self.stats["hit_blocks"] += len(s)
+            self.stats["hit_tokens"] += len(f)
+            return Segment(qi, KIND_FRAG, fi, len(f), off, resident, s, 1, len(f), [False] * len(s))
+        self.stats["miss_blocks"] += len(s)
+        # resident blocks are pinned before any allocation of this fragment, so an eviction
+        # cannot reclaim a block the fragment is about to read
+        for b in resident:
+            if b >= 0:
+                touch(b)
+                pin(b)
+        blocks, write = [], []
+        for i, dig in enumerate(s):
+            if resident[i] >= 0:
+                blocks.append(resident[i])
+                write.append(False)
+            else:
+                blocks.append(insert_new(dig, min(bs, len(f) - i * bs)))
+                write.append(True)
+        return Segment(qi, KIND_FRAG, fi, len(f), off, blocks, s, 0, 0, write)
 
     def release(self, view: PlanView) -> None:
         """Unpin the plan's blocks and free its plan-private blocks."""

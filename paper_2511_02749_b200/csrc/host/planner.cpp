@@ -4,6 +4,9 @@
 #include "planner.h"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../../include/spanq.h"
@@ -295,9 +298,20 @@ void hash_all(const std::vector<FlatQuery>& qs, int bs, const Digest& root, Thre
 }
 }  // namespace
 
-int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* pool) {
+int owner_rank(const Digest& d, int world) {
+  uint64_t v;
+  std::memcpy(&v, d.b, 8);  // u64 little-endian of s_last[0:8]
+  return static_cast<int>(v % static_cast<uint64_t>(world));
+}
+
+int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* pool, int rank, int world) {
   std::vector<QueryDigests> qd;
+  static const bool prof = std::getenv("SPANQ_PROFILE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
   hash_all(qs, bs_, root_, pool, &qd);
+  if (prof)
+    std::fprintf(stderr, "[spanq]   store.hash_all %8.1f us\n",
+                 std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
   const StoreStats saved_stats = stats_;
   const int64_t saved_plan = plan_no_;
   journal_.clear();
@@ -305,6 +319,7 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
   *out = PlanHost();
   PlanHost& P = *out;
   P.n_queries = static_cast<int32_t>(qs.size());
+  P.join_digests.assign(qs.size(), Digest{});  // zero for queries homed on another rank
   cur_pinned_ = &P.pinned;
   plan_no_++;
   const int bs = bs_;
@@ -331,6 +346,13 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
       P.pad_slots.push_back(s);
     return b;
   };
+  auto new_private_nopad = [&]() -> int32_t {  // received pages carry the owner's zeroed pads
+    const int32_t b = alloc(&ok);
+    if (!ok) return -1;
+    P.priv.push_back(b);
+    pin(b);
+    return b;
+  };
   auto add_seg = [&](int32_t qi, int32_t kind, int32_t fi, int32_t len, int32_t pos0, int32_t hit,
                      int32_t cb, const std::vector<int32_t>& blocks, const std::vector<uint8_t>& wr,
                      const std::vector<Digest>& dig) {
@@ -344,8 +366,61 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
   std::vector<Digest> dig;
   std::vector<int32_t> blocks;
   std::vector<uint8_t> wr;
+  std::unordered_map<Digest, std::vector<int32_t>, DigestHash> owned_blocks, recv_blocks;
+  std::vector<std::vector<Digest>> send_list(world), recv_list(world);
+  // all-or-nothing lookup of one locally owned fragment; pins resident blocks before allocating
+  auto owned_fragment = [&](int32_t qi, int32_t fi, int32_t flen, int32_t off, const std::vector<Digest>& fd) {
+    stats_.lookups++;
+    std::vector<int32_t> res(fd.size());
+    bool all = true;
+    for (size_t i = 0; i < fd.size(); ++i) {
+      res[i] = lookup(fd[i]);
+      all = all && res[i] >= 0;
+    }
+    for (int32_t b : res)
+      if (b >= 0) {
+        pin(b);
+        touch(b);
+      }
+    std::vector<int32_t> fb;
+    std::vector<uint8_t> fw;
+    if (all) {
+      stats_.hit_blocks += static_cast<int64_t>(fd.size());
+      stats_.hit_tokens += flen;
+      fw.assign(fd.size(), 0);
+      add_seg(qi, kFrag, fi, flen, off, 1, flen, res, fw, fd);
+      fb = res;
+    } else {
+      stats_.miss_blocks += static_cast<int64_t>(fd.size());
+      for (size_t i = 0; i < fd.size() && ok; ++i) {
+        if (res[i] >= 0) {
+          fb.push_back(res[i]);
+          fw.push_back(0);
+        } else {
+          fb.push_back(insert_new(fd[i], std::min<int32_t>(bs, flen - static_cast<int32_t>(i) * bs)));
+          fw.push_back(1);
+        }
+      }
+      if (!ok) return;
+      add_seg(qi, kFrag, fi, flen, off, 0, 0, fb, fw, fd);
+    }
+    owned_blocks.emplace(fd.back(), fb);
+  };
   for (int32_t qi = 0; qi < P.n_queries && ok; ++qi) {
     const FlatQuery& q = qs[qi];
+    const int home = qi % world;
+    if (home != rank) {
+      // only the fragments this rank owns: prefill/cache them, send them to the home rank
+      for (size_t fi = 0; fi < q.frags.size() && ok; ++fi) {
+        const std::vector<Digest>& fd = qd[qi].frags[fi];
+        if (owner_rank(fd.back(), world) != rank) continue;
+        owned_fragment(qi, static_cast<int32_t>(fi), static_cast<int32_t>(q.frags[fi].size()), 0, fd);
+        auto& lst = send_list[home];
+        if (std::find(lst.begin(), lst.end(), fd.back()) == lst.end()) lst.push_back(fd.back());
+      }
+      continue;
+    }
+    P.n_join_queries++;
     int64_t ntot = static_cast<int64_t>(q.prefix.size()) + static_cast<int64_t>(q.cross.size());
     for (const auto& f : q.frags) ntot += static_cast<int64_t>(f.size());
     stats_.input_tokens += ntot;
@@ -388,51 +463,33 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
     if (plen > 0)
       add_seg(qi, kPrefix, -1, plen, 0, n_hit, std::min(n_hit * bs, plen), blocks, wr, dig);
     const Digest h_last = dig.empty() ? root_ : dig.back();
-    // ---- fragments: suspended chains, all-or-nothing lookup (R10, R11)
+    // ---- fragments: suspended chains, all-or-nothing lookup (R10, R11); with W > 1
+    // a fragment owned by another rank is received into plan-private blocks (no prefill)
     int32_t off = plen;
     for (size_t fi = 0; fi < q.frags.size() && ok; ++fi) {
-      const auto& f = q.frags[fi];
-      const int32_t flen = static_cast<int32_t>(f.size());
-      dig = qd[qi].frags[fi];
-      stats_.lookups++;
-      std::vector<int32_t> res(dig.size());
-      bool all = true;
-      for (size_t i = 0; i < dig.size(); ++i) {
-        res[i] = lookup(dig[i]);
-        all = all && res[i] >= 0;
-      }
-      for (int32_t b : res)
-        if (b >= 0) {
-          pin(b);
-          touch(b);
-        }
-      blocks.clear();
-      wr.clear();
-      if (all) {
-        stats_.hit_blocks += static_cast<int64_t>(dig.size());
-        stats_.hit_tokens += flen;
-        wr.assign(dig.size(), 0);
-        add_seg(qi, kFrag, static_cast<int32_t>(fi), flen, off, 1, flen, res, wr, dig);
+      const int32_t flen = static_cast<int32_t>(q.frags[fi].size());
+      const std::vector<Digest>& fd = qd[qi].frags[fi];
+      const int owner = owner_rank(fd.back(), world);
+      if (owner == rank) {
+        owned_fragment(qi, static_cast<int32_t>(fi), flen, off, fd);
       } else {
-        stats_.miss_blocks += static_cast<int64_t>(dig.size());
-        for (size_t i = 0; i < dig.size() && ok; ++i) {
-          if (res[i] >= 0) {
-            blocks.push_back(res[i]);
-            wr.push_back(0);
-          } else {
-            blocks.push_back(insert_new(dig[i], std::min<int32_t>(bs, flen - static_cast<int32_t>(i) * bs)));
-            wr.push_back(1);
-          }
+        auto it = recv_blocks.find(fd.back());
+        if (it == recv_blocks.end()) {
+          std::vector<int32_t> rb;
+          for (size_t i = 0; i < fd.size() && ok; ++i) rb.push_back(new_private_nopad());
+          if (!ok) break;
+          it = recv_blocks.emplace(fd.back(), rb).first;
+          recv_list[owner].push_back(fd.back());
         }
-        if (!ok) break;
-        add_seg(qi, kFrag, static_cast<int32_t>(fi), flen, off, 0, 0, blocks, wr, dig);
+        wr.assign(fd.size(), 0);
+        add_seg(qi, kFrag, static_cast<int32_t>(fi), flen, off, 0, flen, it->second, wr, fd);
       }
       off += flen;
     }
     if (!ok) break;
     (void)h_last;
     const Digest J = qd[qi].join;
-    P.join_digests.push_back(J);
+    P.join_digests[qi] = J;
     // ---- cross: always computed; full blocks under the X chain (R9)
     const int32_t clen = static_cast<int32_t>(q.cross.size());
     dig = qd[qi].cross;
@@ -457,6 +514,9 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
     if (!ok) break;
     add_seg(qi, kCross, -1, clen, off, 0, 0, blocks, wr, dig);
   }
+  if (prof)
+    std::fprintf(stderr, "[spanq]   store.segments %8.1f us\n",
+                 std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
   if (!ok) {
     rollback();
     for (int32_t b : P.pinned) pinned_mark_[b] = 0;
@@ -475,15 +535,31 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
   // ---- packed rows (job order for prefill, query order for joins)
   auto rows = [&](const Segment& s, int32_t begin, std::vector<int32_t>* pos,
                   std::vector<int64_t>* slot, std::vector<int32_t>* segi, int32_t si) {
-    for (int32_t t = begin; t < s.tok_len; ++t) {
-      const int32_t b = t / bs, o = t % bs;
-      pos->push_back(s.kind == kCross ? s.pos0 + t : t);
-      slot->push_back(P.block_write[s.block_off + b]
-                          ? static_cast<int64_t>(P.blocks[s.block_off + b]) * bs + o
-                          : -1);
-      segi->push_back(si);
+    const int32_t p0 = s.kind == kCross ? s.pos0 : 0;
+    for (int32_t b = begin / bs; b * bs < s.tok_len; ++b) {
+      const int32_t t0 = std::max(begin, b * bs), t1 = std::min(s.tok_len, (b + 1) * bs);
+      const bool w = P.block_write[s.block_off + b] != 0;
+      const int64_t base = static_cast<int64_t>(P.blocks[s.block_off + b]) * bs - static_cast<int64_t>(b) * bs;
+      for (int32_t t = t0; t < t1; ++t) {
+        pos->push_back(p0 + t);
+        slot->push_back(w ? base + t : -1);
+      }
+      segi->insert(segi->end(), static_cast<size_t>(t1 - t0), si);
     }
   };
+  {
+    int64_t np = 0, nj = 0;
+    for (const Segment& s : P.segs) {
+      if (s.kind == kCross) nj += s.tok_len;
+      else if (s.compute_begin < s.tok_len) np += s.tok_len - s.compute_begin;
+    }
+    P.prefill_pos.reserve(np);
+    P.prefill_slot.reserve(np);
+    P.prefill_seg.reserve(np);
+    P.join_pos.reserve(nj);
+    P.join_slot.reserve(nj);
+    P.join_seg.reserve(nj);
+  }
   P.job_row_off.push_back(0);
   for (size_t i = 0; i < P.segs.size(); ++i) {
     const Segment& s = P.segs[i];
@@ -493,13 +569,34 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
       P.job_row_off.push_back(static_cast<int64_t>(P.prefill_pos.size()));
     }
   }
-  P.query_join_row_off.push_back(0);
-  for (size_t i = 0; i < P.segs.size(); ++i) {
-    const Segment& s = P.segs[i];
-    if (s.kind == kCross) {
-      rows(s, 0, &P.join_pos, &P.join_slot, &P.join_seg, static_cast<int32_t>(i));
-      P.query_join_row_off.push_back(static_cast<int64_t>(P.join_pos.size()));
+  if (prof)
+    std::fprintf(stderr, "[spanq]   store.rows %8.1f us\n",
+                 std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+  // exchange lists: per peer, fragments in first-occurrence order, each fragment's blocks
+  P.send_off.assign(1, 0);
+  P.recv_off.assign(1, 0);
+  for (int w = 0; w < world; ++w) {
+    for (const Digest& d : send_list[w]) {
+      const auto& b = owned_blocks.at(d);
+      P.send_blocks.insert(P.send_blocks.end(), b.begin(), b.end());
     }
+    P.send_off.push_back(static_cast<int64_t>(P.send_blocks.size()));
+    for (const Digest& d : recv_list[w]) {
+      const auto& b = recv_blocks.at(d);
+      P.recv_blocks.insert(P.recv_blocks.end(), b.begin(), b.end());
+    }
+    P.recv_off.push_back(static_cast<int64_t>(P.recv_blocks.size()));
+  }
+  // join rows in query order; query_join_row_off is indexed by the global query id (queries
+  // homed elsewhere have an empty range)
+  std::vector<int32_t> cross_of(P.n_queries, -1);
+  for (size_t i = 0; i < P.segs.size(); ++i)
+    if (P.segs[i].kind == kCross) cross_of[P.segs[i].query] = static_cast<int32_t>(i);
+  P.query_join_row_off.reserve(P.n_queries + 1);
+  P.query_join_row_off.push_back(0);
+  for (int32_t qi = 0; qi < P.n_queries; ++qi) {
+    if (cross_of[qi] >= 0) rows(P.segs[cross_of[qi]], 0, &P.join_pos, &P.join_slot, &P.join_seg, cross_of[qi]);
+    P.query_join_row_off.push_back(static_cast<int64_t>(P.join_pos.size()));
   }
   return 0;
 }

@@ -58,7 +58,14 @@ struct PlanHost {
   std::vector<int32_t> pinned;
   std::vector<int32_t> priv;
   int32_t n_queries = 0;
+  int32_t n_join_queries = 0;  // queries homed on this rank (all when world == 1)
+  // W > 1 fragment exchange: blocks sent to / received from each peer
+  std::vector<int64_t> send_off, recv_off;  // [world+1]
+  std::vector<int32_t> send_blocks, recv_blocks;
 };
+
+// Fragment owner rank: u64le(s_last[0:8]) mod W.
+int owner_rank(const Digest& d, int world);
 
 // Digest chains (hash contract): ROOT, 'P' prefix, 'F' fragment, 'J' fold, 'X' cross.
 Digest root_digest(int hq, int hkv, int d, int bs, double rope_base, uint64_t salt);
@@ -72,7 +79,8 @@ class Store {
 
   // Plan a batch. Returns 0 on success, 2 on ENOMEM (state rolled back). Block digests do
   // not depend on store state, so they are computed first, in parallel on `pool` if given.
-  int plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* pool = nullptr);
+  int plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* pool = nullptr, int rank = 0,
+           int world = 1);
   void release(const PlanHost& p);
   void evict_all();
   int32_t lookup(const Digest& d) const;

@@ -77,4 +77,16 @@ struct CombineArgs {
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);
 
+struct KvExchangeArgs {
+  const int32_t* blocks;  // device [n] block ids
+  int64_t n;
+  void* k_pool;
+  void* v_pool;
+  void* buf;  // device [n][2][Hkv*bs*d] elements
+  int hkv, bs, d, elt, layer, num_sms;
+  int64_t nblk;
+  int scatter;  // 0: pool -> buf (pack), 1: buf -> pool (unpack)
+};
+cudaError_t launch_kv_exchange(const KvExchangeArgs& a, cudaStream_t st);
+
 }  // namespace spq

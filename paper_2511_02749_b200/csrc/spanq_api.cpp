@@ -99,7 +99,7 @@ struct spq_plan {
   int64_t prefill_kv_bytes = 0, join_kv_bytes = 0;
   // device
   uint8_t* dbuf = nullptr;
-  size_t off_ppos = 0, off_pslot = 0, off_pad = 0, off_jpos = 0, off_jslot = 0;
+  size_t off_ppos = 0, off_pslot = 0, off_pad = 0, off_jpos = 0, off_jslot = 0, off_send = 0, off_recv = 0;
   DevWork pw, jw;
   float* opart = nullptr;
   float* lsepart = nullptr;
@@ -353,7 +353,7 @@ spq_status spq_create(const spq_config* cfg, spq_ctx** out) {
   if (g.dtype != SPQ_BF16 && g.dtype != SPQ_FP32) return fail(SPQ_EINVAL, "bad dtype");
   if (g.out_dtype != SPQ_BF16 && g.out_dtype != SPQ_FP32) return fail(SPQ_EINVAL, "bad out_dtype");
   if (g.dtype == SPQ_FP32 && g.out_dtype != SPQ_FP32) return fail(SPQ_EINVAL, "fp32 ctx needs fp32 outputs");
-  if (g.world_size != 1 || g.rank != 0) return fail(SPQ_EINVAL, "world_size must be 1 in this version");
+  if (g.world_size < 1 || g.rank < 0 || g.rank >= g.world_size) return fail(SPQ_EINVAL, "bad rank/world_size");
   if (g.max_position <= 0 || !(g.rope_base > 0)) return fail(SPQ_EINVAL, "bad rope parameters");
   std::unique_ptr<spq_ctx> c(new spq_ctx());
   c->cfg = g;
@@ -502,7 +502,7 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
   }
   lap("normalize");
   std::unique_ptr<spq_plan> p(new spq_plan());
-  if (c->store->plan(fq, &p->host, c->pool.get()) != 0) return fail(SPQ_ENOMEM, "block pool cannot hold the plan (rolled back)");
+  if (c->store->plan(fq, &p->host, c->pool.get(), c->cfg.rank, c->cfg.world_size) != 0) return fail(SPQ_ENOMEM, "block pool cannot hold the plan (rolled back)");
   lap("store.plan");
   const spq::PlanHost& H = p->host;
   for (const spq::Segment& s : H.segs) {
@@ -543,6 +543,8 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
     p->off_pad = pk.add(H.pad_slots);
     p->off_jpos = pk.add(H.join_pos);
     p->off_jslot = pk.add(H.join_slot);
+    p->off_send = pk.add(H.send_blocks);
+    p->off_recv = pk.add(H.recv_blocks);
     auto add_work = [&](const spq::AttnWorkHost& h, DevWork* w) {
       w->tiles = pk.add(h.tiles);
       w->tile_blocks = pk.add(h.tile_blocks);
@@ -620,6 +622,12 @@ spq_status spq_plan_view_get(const spq_plan* p, spq_plan_view* v) {
   v->join_flops = p->join_flops;
   v->prefill_kv_bytes = p->prefill_kv_bytes;
   v->join_kv_bytes = p->join_kv_bytes;
+  v->n_join_queries = H.n_join_queries;
+  v->world_size = static_cast<int32_t>(H.send_off.size()) - 1;
+  v->send_off = H.send_off.data();
+  v->send_blocks = H.send_blocks.data();
+  v->recv_off = H.recv_off.data();
+  v->recv_blocks = H.recv_blocks.data();
   return SPQ_OK;
 }
 
@@ -693,6 +701,7 @@ spq_status spq_join(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b
   s = wait_pending(c, st);
   if (s != SPQ_OK) return s;
   const int64_t r0 = p->host.query_join_row_off[a], r1 = p->host.query_join_row_off[b];
+  if (r0 == r1) return SPQ_OK;  // only queries homed on other ranks
   s = kv_write(c, p, layer, k, v, at<int32_t>(p, p->off_jpos) + r0, at<int64_t>(p, p->off_jslot) + r0, r1 - r0, st);
   if (s != SPQ_OK) return s;
   spq::AttnArgs args{};
@@ -764,6 +773,49 @@ spq_status spq_join(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b
   }
   if (tw.buf) CUDA_TRY(cudaFreeAsync(tw.buf, st));
   return SPQ_OK;
+}
+
+static spq_status exchange(spq_ctx* c, spq_plan* p, int32_t layer, int32_t peer, void* buf, void* stream,
+                           int scatter) {
+  spq_status s = check_call(c, p, layer);
+  if (s != SPQ_OK) return s;
+  const spq::PlanHost& H = p->host;
+  if (peer < 0 || peer >= static_cast<int32_t>(H.send_off.size()) - 1) return fail(SPQ_ESTATE, "peer out of range");
+  const std::vector<int64_t>& off = scatter ? H.recv_off : H.send_off;
+  const int64_t a = off[peer], n = off[peer + 1] - a;
+  if (n == 0) return SPQ_OK;
+  if (buf == nullptr || (reinterpret_cast<uintptr_t>(buf) & 15)) return fail(SPQ_EINVAL, "buf must be 16-byte aligned");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  s = wait_pending(c, st);
+  if (s != SPQ_OK) return s;
+  spq::KvExchangeArgs x{};
+  x.blocks = at<int32_t>(p, scatter ? p->off_recv : p->off_send) + a;
+  x.n = n;
+  x.k_pool = c->cfg.k_pool;
+  x.v_pool = c->cfg.v_pool;
+  x.buf = buf;
+  x.hkv = c->cfg.num_kv_heads;
+  x.bs = c->cfg.block_size;
+  x.d = c->cfg.head_dim;
+  x.elt = elt_size(c);
+  x.layer = layer;
+  x.num_sms = c->num_sms;
+  x.nblk = c->cfg.num_blocks;
+  x.scatter = scatter;
+  cudaError_t e = spq::launch_kv_exchange(x, st);
+  if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("kv_exchange launch: ") + cudaGetErrorString(e));
+  c->launches++;
+  return SPQ_OK;
+}
+
+spq_status spq_exchange_pack(spq_ctx* c, spq_plan* p, int32_t layer, int32_t peer, void* buf, void* stream) {
+  return exchange(c, p, layer, peer, buf, stream, 0);
+}
+
+spq_status spq_exchange_unpack(spq_ctx* c, spq_plan* p, int32_t layer, int32_t peer, const void* buf,
+                               void* stream) {
+  return exchange(c, p, layer, peer, const_cast<void*>(buf), stream, 1);
 }
 
 spq_status spq_plan_release(spq_ctx* c, spq_plan* p, void* stream) {

@@ -1,0 +1,63 @@
+"""Multi-GPU partitioning of a span-query batch — the exchange step.
+
+Each rank plans the same batch with its own (rank, world_size): query q is homed on q mod W (its
+prefix, cross rows and join run there) and fragment f is owned by u64le(s_last(f)[0:8]) mod W
+(only the owner prefills and caches it). After a layer's prefill jobs, every home rank needs the
+KV of the remote-owned fragments its joins read: the plan's exchange lists name them on both sides
+in the same order, so one all-to-all per layer moves them:
+
+    pack (K6 gather, per peer)  ->  dist.all_to_all_single (NCCL over NVLink)  ->  unpack (K6 scatter)
+
+Buffers are laid out [n_blocks][2 (K, V)][Hkv][bs][d] in the pool dtype. Everything here is
+argument marshalling around the C ABI (spq_exchange_pack / spq_exchange_unpack) and the collective.
+"""
+from __future__ import annotations
+
+from typing import Callable, Dict, List, Optional
+
+
+def block_elems(shape) -> int:
+    """Elements of one block of one layer, K and V together."""
+    return 2 * shape.hkv * shape.block_size * shape.d
+
+
+def exchange_counts(view: Dict, world: int):
+    """Per-peer block counts (send, recv) of a plan view."""
+    send = [len(view["send"].get(p, ())) for p in range(world)]
+    recv = [len(view["recv"].get(p, ())) for p in range(world)]
+    return send, recv
+
+
+def _a2a(recvbuf, sendbuf, out_splits: List[int], in_splits: List[int], group=None):
+    import torch.distributed as dist
+
+    dist.all_to_all_single(recvbuf, sendbuf, out_splits, in_splits, group=group)
+
+
+def exchange_layer(plan, view: Dict, layer: int, shape, device, dtype, rank: int, world: int,
+                   group=None, stream=None, transport: Optional[Callable] = None) -> Dict[str, int]:
+    """Move one layer's remote fragment KV to the home ranks. Returns the bytes sent/received.
+
+    `transport(recvbuf, sendbuf, out_splits, in_splits)` defaults to an all-to-all on `group`.
+    """
+    import torch
+
+    be = block_elems(shape)
+    send, recv = exchange_counts(view, world)
+    assert send[rank] == 0 and recv[rank] == 0, "a rank never exchanges with itself"
+    sendbuf = torch.empty(sum(send) * be, dtype=dtype, device=device)
+    recvbuf = torch.empty(sum(recv) * be, dtype=dtype, device=device)
+    off = 0
+    for p in range(world):
+        if send[p]:
+            plan.exchange_pack(layer, p, sendbuf[off:off + send[p] * be], stream=stream)
+        off += send[p] * be
+    (transport or (lambda r, s, o, i: _a2a(r, s, o, i, group)))(
+        recvbuf, sendbuf, [c * be for c in recv], [c * be for c in send])
+    off = 0
+    for p in range(world):
+        if recv[p]:
+            plan.exchange_unpack(layer, p, recvbuf[off:off + recv[p] * be], stream=stream)
+        off += recv[p] * be
+    elt = sendbuf.element_size()
+    return {"sent_bytes": sum(send) * be * elt, "recv_bytes": sum(recv) * be * elt}

@@ -43,8 +43,10 @@ def prefill_tokens(view: Dict, queries, jobs=None) -> np.ndarray:
 
 
 def join_tokens(view: Dict, queries, qrange=None) -> np.ndarray:
+    """Cross rows of queries [a, b) homed on this rank, in query order (the join's packing)."""
     a, b = (0, int(view["n_queries"])) if qrange is None else qrange
-    parts = [np.asarray(queries[i].cross, np.int64) for i in range(a, b)]
+    off = view["query_join_row_off"]
+    parts = [np.asarray(queries[i].cross, np.int64) for i in range(a, b) if off[i + 1] > off[i]]
     return np.concatenate(parts) if parts else np.zeros(0, np.int64)
 
 
@@ -81,8 +83,11 @@ class PassResult:
 
 
 def run_pass(ctx: spanq.Context, queries: Sequence[inputs.SpanQuery], tabs: Sequence[DeviceTables],
-             device, stream=None, release: bool = False) -> PassResult:
-    """Plan `queries` and run every layer's prefill jobs and joins (one pass of the hot path)."""
+             device, stream=None, release: bool = False, exchange=None) -> PassResult:
+    """Plan `queries` and run every layer's prefill jobs and joins (one pass of the hot path).
+
+    With world_size > 1, `exchange(plan, view, layer)` moves the layer's remote fragment KV
+    between the prefill and the join (parallel.exchange_layer over NCCL)."""
     torch = _torch()
     shape = ctx.shape
     odt = torch.bfloat16 if ctx.out_dtype == "bf16" else torch.float32
@@ -97,6 +102,10 @@ def run_pass(ctx: spanq.Context, queries: Sequence[inputs.SpanQuery], tabs: Sequ
         if len(ptok):
             q, k, v = gather(tab, ptok, device)
             plan.prefill(layer, q, k, v, op, lp, stream=stream)
+        if exchange is not None:
+            exchange(plan, view, layer)
+        if not len(jtok):
+            continue
         q, k, v = gather(tab, jtok, device)
         plan.join(layer, q, k, v, oj, lj, stream=stream)
     if release:

@@ -67,6 +67,8 @@ class spq_plan_view(C.Structure):
         ("join_slot", _I64P), ("n_pad_slots", C.c_int64), ("pad_slots", _I64P),
         ("prefill_flops", C.c_double), ("join_flops", C.c_double),
         ("prefill_kv_bytes", C.c_int64), ("join_kv_bytes", C.c_int64),
+        ("n_join_queries", C.c_int32), ("world_size", C.c_int32),
+        ("send_off", _I64P), ("send_blocks", _I32P), ("recv_off", _I64P), ("recv_blocks", _I32P),
     ]
 
 
@@ -93,6 +95,10 @@ SIGNATURES = {
                                    C.c_void_p]),
     "spq_join": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "spq_exchange_pack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
+                                    C.c_void_p]),
+    "spq_exchange_unpack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
+                                      C.c_void_p]),
     "spq_plan_release": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "spq_get_stats": (C.c_int, [C.c_void_p, C.POINTER(spq_stats)]),
     "spq_evict_all": (C.c_int, [C.c_void_p]),
@@ -141,14 +147,19 @@ def _stream_ptr(stream) -> Optional[int]:
     return int(stream)
 
 
+_NODE_DT = np.dtype({"names": ["op", "nc", "b", "n"], "formats": [np.int32, np.int32, np.int64, np.int64],
+                     "offsets": [0, 4, 8, 16], "itemsize": C.sizeof(spq_node)})
+
+
 class _QueryBuf:
     """Keeps the ctypes arrays of one spq_query alive."""
 
     def __init__(self, nodes: np.ndarray, tokens: np.ndarray):
         nodes = np.asarray(nodes, dtype=np.int64).reshape(-1, 4)
         self.nodes = (spq_node * max(1, len(nodes)))()
-        for i, (op, nc, b, n) in enumerate(nodes):
-            self.nodes[i] = spq_node(int(op), int(nc), int(b), int(n))
+        rec = np.zeros(len(nodes), dtype=_NODE_DT)
+        rec["op"], rec["nc"], rec["b"], rec["n"] = nodes[:, 0], nodes[:, 1], nodes[:, 2], nodes[:, 3]
+        C.memmove(self.nodes, rec.ctypes.data, rec.nbytes)
         self.tokens = np.ascontiguousarray(tokens, dtype=np.int32)
         self.q = spq_query(C.cast(self.nodes, C.POINTER(spq_node)), len(nodes),
                            self.tokens.ctypes.data_as(_I32P), len(self.tokens))
@@ -202,8 +213,24 @@ class Plan:
             pad_slots=_arr(v.pad_slots, v.n_pad_slots, np.int64),
             prefill_flops=v.prefill_flops, join_flops=v.join_flops,
             prefill_kv_bytes=v.prefill_kv_bytes, join_kv_bytes=v.join_kv_bytes,
+            n_join_queries=v.n_join_queries, world_size=v.world_size,
         )
+        w = v.world_size
+        so, ro = _arr(v.send_off, w + 1, np.int64), _arr(v.recv_off, w + 1, np.int64)
+        sb, rb = _arr(v.send_blocks, int(so[-1]), np.int32), _arr(v.recv_blocks, int(ro[-1]), np.int32)
+        out["send"] = {p: sb[so[p]:so[p + 1]] for p in range(w) if so[p + 1] > so[p]}
+        out["recv"] = {p: rb[ro[p]:ro[p + 1]] for p in range(w) if ro[p + 1] > ro[p]}
         return out
+
+    def exchange_pack(self, layer, peer, buf, stream=None):
+        """Gather this plan's send blocks for `peer` (one layer) into buf [n, 2, Hkv, bs, d]."""
+        _check(lib().spq_exchange_pack(self.ctx.handle, self.handle, layer, peer, _ptr(buf),
+                                       _stream_ptr(stream)))
+
+    def exchange_unpack(self, layer, peer, buf, stream=None):
+        """Scatter buf [n, 2, Hkv, bs, d] into this plan's recv blocks from `peer` (one layer)."""
+        _check(lib().spq_exchange_unpack(self.ctx.handle, self.handle, layer, peer, _ptr(buf),
+                                         _stream_ptr(stream)))
 
     def prefill(self, layer, q, k, v, o, lse=None, jobs=None, stream=None):
         a, b = (0, self.n_jobs) if jobs is None else jobs
@@ -229,12 +256,14 @@ class Context:
     """
 
     def __init__(self, shape: _inputs.Shape, num_blocks: int, device: int = 0,
-                 max_position: int = 1 << 15, pools=None, out_dtype: Optional[str] = None):
+                 max_position: int = 1 << 15, pools=None, out_dtype: Optional[str] = None,
+                 rank: int = 0, world_size: int = 1):
         self.shape = shape
         self.device = device
         self.num_blocks = num_blocks
         self.k_pool = self.v_pool = None
         self.out_dtype = out_dtype or shape.dtype
+        self.rank, self.world_size = rank, world_size
         if device >= 0:
             import torch
 
@@ -248,7 +277,7 @@ class Context:
         cfg = spq_config(shape.hq, shape.hkv, shape.d, shape.layers, shape.block_size, num_blocks,
                          BF16 if shape.dtype == "bf16" else FP32, float(shape.rope_base),
                          int(max_position), int(shape.model_salt), _ptr(self.k_pool),
-                         _ptr(self.v_pool), device, 0, 1,
+                         _ptr(self.v_pool), device, int(rank), int(world_size),
                          BF16 if self.out_dtype == "bf16" else FP32)
         h = C.c_void_p()
         _check(lib().spq_create(C.byref(cfg), C.byref(h)))

@@ -1,0 +1,99 @@
+"""GPU parity of the partitioned (world_size > 1) path on one GPU.
+
+Two contexts stand for ranks 0 and 1 of W = 2 (each its own KV pool, as on two GPUs). Each plans
+the same batch for its rank and runs its prefill jobs (its home queries' prefixes plus the
+fragments it owns); the K6 pack/unpack kernels then move the remote-owned fragment KV between
+the pools through device buffers (the role NCCL's all-to-all plays across GPUs); each rank then
+runs the joins of its home queries. Checked against the oracle:
+  * each rank's plan is the oracle's `plan(rank, world)` bit for bit (slot maps, exchange lists);
+  * received blocks are bit-identical to the owner's blocks (K and V, pads included);
+  * prefill and join outputs match the fp64 oracle at the north_star tolerances.
+"""
+import numpy as np
+import pytest
+
+from oracle import attention as oatt
+from oracle.store import Store
+from paper_2511_02749_b200 import inputs, parallel, runner, spanq
+
+from test_gpu_parity import check, check_lse
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("dtype,world", [("bf16", 2), ("fp32", 2), ("bf16", 3)])
+def test_partitioned_exchange_parity(cuda_dev, dtype, world):
+    import torch
+
+    fp32 = dtype == "fp32"
+    sh = inputs.Shape(hq=8, hkv=2, d=128 if not fp32 else 64, block_size=16, vocab=512, dtype=dtype)
+    qs = inputs.random_queries(205 + world, 9, vocab=512, max_frag=5, max_len=150, max_prefix=100,
+                               max_cross=120, reuse_p=0.5)
+    seed = 205
+    eq, ek, ev = inputs.layer_tables(sh, 0, seed)
+    tab = runner.device_tables(sh, 0, seed, cuda_dev)
+    flat = [(q.prefix, q.fragments, q.cross) for q in qs]
+    ctxs, plans, views, outs = [], [], [], []
+    for r in range(world):
+        ctx = spanq.Context(sh, 2048, device=0, max_position=1 << 14, out_dtype="fp32", rank=r, world_size=world)
+        plan = ctx.plan(qs)
+        view = plan.view()
+        ov = Store(2048, sh.hq, sh.hkv, sh.d, sh.block_size, sh.rope_base, sh.model_salt).plan(flat, rank=r,
+                                                                                                   world=world)
+        np.testing.assert_array_equal(view["prefill_slot"], ov.prefill_slot)
+        np.testing.assert_array_equal(view["join_slot"], ov.join_slot)
+        for p in range(world):
+            np.testing.assert_array_equal(view["send"].get(p, np.zeros(0, np.int32)), ov.send.get(p, []))
+            np.testing.assert_array_equal(view["recv"].get(p, np.zeros(0, np.int32)), ov.recv.get(p, []))
+        ptok = runner.prefill_tokens(view, qs)
+        op = torch.empty((len(ptok), sh.hq, sh.d), dtype=torch.float32, device=cuda_dev)
+        lp = torch.empty((len(ptok), sh.hq), dtype=torch.float32, device=cuda_dev)
+        if len(ptok):
+            q, k, v = runner.gather(tab, ptok, cuda_dev)
+            plan.prefill(0, q, k, v, op, lp)
+        if len(ov.jobs):
+            eo, el = oatt.plan_prefill_expected(ov, flat, eq, ek, ev, sh.rope_base)
+            check(op, eo, fp32, f"rank {r} prefill O")
+            check_lse(lp, el, fp32, f"rank {r} prefill LSE")
+        ctxs.append(ctx)
+        plans.append(plan)
+        views.append(view)
+    # exchange: rank r packs for p, p unpacks from r (device buffers stand in for NCCL)
+    dt = ctxs[0].k_pool.dtype
+    be = parallel.block_elems(sh)
+    n_moved = 0
+    for r in range(world):
+        for p in range(world):
+            sb = views[r]["send"].get(p, np.zeros(0, np.int32))
+            rb = views[p]["recv"].get(r, np.zeros(0, np.int32))
+            assert len(sb) == len(rb)
+            if not len(sb):
+                continue
+            buf = torch.full((len(sb) * be,), float("nan"), dtype=dt, device=cuda_dev)
+            plans[r].exchange_pack(0, p, buf)
+            plans[p].exchange_unpack(0, r, buf)
+            torch.cuda.synchronize()
+            for a, b in zip(sb.tolist(), rb.tolist()):
+                assert torch.equal(ctxs[r].k_pool[0, a], ctxs[p].k_pool[0, b])
+                assert torch.equal(ctxs[r].v_pool[0, a], ctxs[p].v_pool[0, b])
+            n_moved += len(sb)
+    assert n_moved > 0, "workload exchanged nothing"
+    # joins of each rank's home queries
+    n_join = 0
+    for r in range(world):
+        view = views[r]
+        jtok = runner.join_tokens(view, qs)
+        oj = torch.empty((len(jtok), sh.hq, sh.d), dtype=torch.float32, device=cuda_dev)
+        lj = torch.empty((len(jtok), sh.hq), dtype=torch.float32, device=cuda_dev)
+        q, k, v = runner.gather(tab, jtok, cuda_dev)
+        plans[r].join(0, q, k, v, oj, lj)
+        torch.cuda.synchronize()
+        home = [i for i in range(len(qs)) if i % world == r]
+        exp = [oatt.join_rows(*flat[i], eq, ek, ev, sh.rope_base) for i in home]
+        check(oj, np.concatenate([e[0] for e in exp]), fp32, f"rank {r} join O")
+        check_lse(lj, np.concatenate([e[1] for e in exp]), fp32, f"rank {r} join LSE")
+        n_join += len(jtok)
+    assert n_join == sum(len(q.cross) for q in qs)
+    for p, c in zip(plans, ctxs):
+        p.release()
+        c.close()

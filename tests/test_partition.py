@@ -1,0 +1,198 @@
+"""Multi-rank partitioning of a span-query batch, host side, CPU only.
+
+* The C++ planner in partitioned mode (ctx rank r of W) is bit-exact against the oracle's
+  `Store.plan(rank=r, world=W)` — segments, block tables, slot maps, stats and exchange lists.
+* The exchange lists agree across ranks: what rank r sends to p is, block for block, the
+  fragment KV that p's plan expects from r (same digests, same order).
+* Partitioning covers the batch exactly once: every join runs on one rank, every distinct
+  fragment (cold cache) is prefilled on exactly one rank, its owner.
+* The exchange step itself (parallel.exchange_layer) over a real world-2 gloo group moves the
+  right blocks into the right places (pack/unpack emulated on CPU pools; the CUDA K6 kernel is
+  covered by tests/test_gpu_parity.py).
+"""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle import hashing
+from oracle.store import OracleENOMEM, Store
+from paper_2511_02749_b200 import inputs, parallel, spanq
+
+from test_abi_host import STAT_KEYS, assert_same, flat
+
+
+def seg_digest_map(view):
+    """block id -> digest (bytes) for every block referenced by the view's segments."""
+    m = {}
+    for b, d in zip(view["blocks"], view["digests"]):
+        m.setdefault(int(b), bytes(d))
+    return m
+
+
+def test_owner_rank_definition():
+    d = bytes(range(16))
+    v = sum(d[i] << (8 * i) for i in range(8))  # u64 little-endian of the first 8 bytes
+    for w in (1, 2, 3, 8):
+        assert hashing.owner_rank(d, w) == v % w
+
+
+@pytest.mark.parametrize("world,seed,bs,nblk", [(2, 11, 4, 4096), (3, 12, 8, 4096), (4, 13, 2, 160),
+                                                (2, 14, 16, 64)])
+def test_partitioned_planner_bit_exact_vs_oracle(world, seed, bs, nblk):
+    shape = inputs.Shape(hq=4, hkv=2, d=64, block_size=bs, dtype="fp32", rope_base=5000.0, model_salt=seed)
+    qs = inputs.random_queries(seed, 48, vocab=12, max_len=30)
+    for rank in range(world):
+        ctx = spanq.Context(shape, nblk, device=-1, rank=rank, world_size=world)
+        ost = Store(nblk, 4, 2, 64, bs, 5000.0, seed)
+        g = np.random.default_rng(seed * 10 + rank)
+        live, i, n_plans = [], 0, 0
+        while i < len(qs):
+            k = int(g.integers(1, 6))
+            batch = qs[i:i + k]
+            i += k
+            try:
+                ov = ost.plan([flat(q) for q in batch], rank=rank, world=world)
+            except OracleENOMEM:
+                with pytest.raises(spanq.SpanqError) as e:
+                    ctx.plan(batch)
+                assert e.value.status == spanq.ENOMEM
+                continue
+            cp = ctx.plan(batch)
+            cv = cp.view()
+            assert_same(cv, ov)
+            assert cv["n_join_queries"] == ov.n_join_queries
+            assert cv["world_size"] == world
+            for name, od in (("send", ov.send), ("recv", ov.recv)):
+                assert sorted(cv[name]) == sorted(p for p, b in od.items() if b), name
+                for p, b in od.items():
+                    np.testing.assert_array_equal(cv[name].get(p, np.zeros(0, np.int32)), b, err_msg=name)
+            cs = ctx.stats()
+            for key in STAT_KEYS:
+                assert cs[key] == ost.stats[key], key
+            live.append((cp, ov))
+            n_plans += 1
+            while live and g.random() < 0.5:
+                cp, ov = live.pop(int(g.integers(0, len(live))))
+                cp.release()
+                ost.release(ov)
+        assert n_plans >= 4
+        for cp, ov in live:
+            cp.release()
+        ctx.close()
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_exchange_lists_agree_and_cover_batch(world):
+    shape = inputs.Shape(hq=4, hkv=2, d=64, block_size=8, dtype="fp32")
+    qs = inputs.random_queries(21 + world, 40, vocab=16, max_len=40, reuse_p=0.5)
+    views = []
+    for rank in range(world):
+        ctx = spanq.Context(shape, 1 << 14, device=-1, rank=rank, world_size=world)
+        views.append(ctx.plan(qs).view())
+    maps = [seg_digest_map(v) for v in views]
+    for r in range(world):
+        for p in range(world):
+            sent = [maps[r][int(b)] for b in views[r]["send"].get(p, [])]
+            got = [maps[p][int(b)] for b in views[p]["recv"].get(r, [])]
+            assert sent == got, (r, p)
+        assert r not in views[r]["send"] and r not in views[r]["recv"]
+    # every join on exactly one rank (its home), all queries covered
+    homes = [set(np.nonzero(np.diff(v["query_join_row_off"]))[0].tolist()) for v in views]
+    assert sum(len(h) for h in homes) == len(qs)
+    for r, h in enumerate(homes):
+        assert h == {q for q in range(len(qs)) if q % world == r and len(qs[q].cross)}
+        assert views[r]["n_join_queries"] == len([q for q in range(len(qs)) if q % world == r])
+    # cold cache: every distinct fragment prefilled exactly once, on its owner
+    frag_jobs = {}
+    for r, v in enumerate(views):
+        for j in v["jobs"]:
+            if v["seg_kind"][j] == 1:
+                blk0 = v["seg_block_off"][j]
+                nb = v["seg_n_blocks"][j]
+                last = bytes(v["digests"][blk0 + nb - 1])
+                frag_jobs.setdefault(last, []).append(r)
+    distinct = {hashing.fragment_chain(np.asarray(f), 8, Store(1, 4, 2, 64, 8).root)[-1]
+                for q in qs for f in q.fragments}
+    assert set(frag_jobs) == distinct
+    for last, ranks in frag_jobs.items():
+        assert ranks == [hashing.owner_rank(last, world)]
+
+
+# ---------------------------------------------------------------- exchange over a gloo group
+class _CpuPlan:
+    """pack/unpack of K6 emulated on CPU pools [nblk, 2, E] (E = block elems / 2)."""
+
+    def __init__(self, view, pool):
+        self.view, self.pool = view, pool
+
+    def exchange_pack(self, layer, peer, buf, stream=None):
+        blocks = self.view["send"][peer]
+        buf.view(len(blocks), -1).copy_(self.pool[blocks].reshape(len(blocks), -1))
+
+    def exchange_unpack(self, layer, peer, buf, stream=None):
+        blocks = self.view["recv"][peer]
+        self.pool[blocks] = buf.view(len(blocks), *self.pool.shape[1:])
+
+
+def _fill_from_digest(pool, dmap):
+    import torch
+
+    for b, d in dmap.items():
+        g = np.random.default_rng(int.from_bytes(d[:8], "little"))
+        pool[b] = torch.from_numpy(g.standard_normal(pool.shape[1:]).astype(np.float32))
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        shape = inputs.Shape(hq=4, hkv=2, d=16, block_size=4, dtype="fp32")
+        qs = inputs.random_queries(77, 24, vocab=16, max_len=20, reuse_p=0.5)
+        ctx = spanq.Context(shape, 4096, device=-1, rank=rank, world_size=world)
+        view = ctx.plan(qs).view()
+        be = parallel.block_elems(shape)
+        pool = torch.zeros(4096, 2, be // 2)
+        dmap = seg_digest_map(view)
+        recv_blocks = {int(b) for bl in view["recv"].values() for b in bl}
+        # fill only the blocks this rank computes (owned fragments); received ones stay zero
+        _fill_from_digest(pool, {b: d for b, d in dmap.items() if b not in recv_blocks})
+        stats = parallel.exchange_layer(_CpuPlan(view, pool), view, 0, shape, "cpu", torch.float32,
+                                        rank, world)
+        ref = torch.zeros_like(pool)
+        _fill_from_digest(ref, {b: dmap[b] for b in recv_blocks})
+        for b in recv_blocks:
+            assert torch.equal(pool[b], ref[b]), f"rank {rank}: block {b} got the wrong fragment KV"
+        counts = [None] * world
+        dist.all_gather_object(counts, (stats["sent_bytes"], stats["recv_bytes"], len(recv_blocks)))
+        assert sum(c[0] for c in counts) == sum(c[1] for c in counts)
+        assert sum(c[2] for c in counts) > 0
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover - reported by the parent
+        import traceback
+
+        q.put((rank, traceback.format_exc()))
+
+
+def test_exchange_layer_gloo_world2():
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}, res
