@@ -57,6 +57,7 @@ void schedule(const std::vector<double>& item_cost, int hq, int num_sms, AttnWor
 
 constexpr double kItemOverhead = 1.0;   // q-prep + epilogue, in KV-tile units
 constexpr double kSplitOverhead = 0.5;  // partial write + combine read, per split
+constexpr double kSubOverhead = 3.0;    // per work item, in 64-key sub-tiles (epilogue + Q + pipeline fill)
 
 }  // namespace
 
@@ -119,49 +120,107 @@ void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_en
     for (int32_t j = 0; j < c.tok_len; ++j) w->flops += before + j + 1;
   }
   w->flops *= 4.0 * o.d * o.hq;
-  // choose the split count K (same for all q tiles, capped by each tile count): minimise the
-  // wave-quantised makespan ceil(pairs / SMs) * (largest chunk cost) — closed form, O(K·tiles)
-  int best_k = 1;
-  if (o.allow_split && !qt.empty()) {
-    const size_t pairs1 = qt.size() * static_cast<size_t>(o.units);
-    if (pairs1 < static_cast<size_t>(4 * o.num_sms)) {
-      double best = 1e300;
-      int max_n = 0;
-      for (const QTile& q : qt) max_n = std::max(max_n, q.te - q.tb);
-      for (int k = 1; k <= std::min(64, max_n); ++k) {
-        size_t items = 0;
-        double cmax = 0;
-        for (const QTile& q : qt) {
-          const int n = q.te - q.tb, kk = std::min(k, n);
-          items += kk;
-          cmax = std::max(cmax, (n + kk - 1) / kk + kItemOverhead + (kk > 1 ? kSplitOverhead : 0.0));
-        }
-        const double waves = std::ceil(static_cast<double>(items * o.units) / o.num_sms);
-        const double mk = waves * cmax;
-        if (mk < best * 0.98) {
-          best = mk;
-          best_k = k;
-        }
-      }
-    }
-  }
-  std::vector<double> cost;
-  for (const QTile& q : qt) {
-    const int n = q.te - q.tb, kk = std::min(best_k, n);
-    if (kk > 1) w->combine.push_back({q.row0, q.n_rows, w->n_parts, kk});
-    for (int s = 0; s < kk; ++s) {
+  if (!(o.allow_split && o.persistent) || qt.empty()) {
+    std::vector<double> cost;
+    for (const QTile& q : qt) {
       WorkItem it{};
       it.row0 = q.row0;
       it.n_rows = q.n_rows;
-      it.tile_begin = q.tb + (n * s) / kk;
-      it.tile_end = q.tb + (n * (s + 1)) / kk;
-      it.part = kk > 1 ? w->n_parts + s : -1;
+      it.tile_begin = q.tb;
+      it.tile_end = q.te;
+      it.part = -1;
       w->items.push_back(it);
-      cost.push_back(it.tile_end - it.tile_begin + kItemOverhead + (kk > 1 ? kSplitOverhead : 0.0));
+      cost.push_back(q.te - q.tb + kItemOverhead);
     }
-    if (kk > 1) w->n_parts += kk;
+    if (o.persistent) schedule(cost, o.units, o.num_sms, w);
+    return;
   }
-  if (o.persistent) schedule(cost, o.units, o.num_sms, w);
+  // Stream-K split: the (q tile, unit) pairs' KV sub-tiles, flattened pair-major (units of one q
+  // tile adjacent: the two units of a KV head read the same tiles close in time), are cut into
+  // num_sms contiguous ranges of equal cost (sub-tiles + a per-item overhead). A pair covered by
+  // one CTA writes its final O; a pair cut across CTAs writes partials (per unit: hpu heads)
+  // merged by combine. Every CTA gets <= ceil(range) work and at most a few items.
+  const int hpu = o.hq / o.units;
+  std::vector<int32_t> sub(w->tiles.size());
+  double total = 0;
+  for (size_t t = 0; t < w->tiles.size(); ++t) sub[t] = w->tiles[t].n_valid > 64 ? 2 : 1;
+  for (const QTile& q : qt)
+    for (int t = q.tb; t < q.te; ++t) total += static_cast<double>(sub[t]) * o.units;
+  const int grid = o.num_sms;
+  struct Piece {
+    int cta, t0, t1;
+  };
+  // prefix sums of sub-tile counts per tile (tiles of one q tile are contiguous)
+  std::vector<double> pre(w->tiles.size() + 1, 0.0);
+  for (size_t t = 0; t < w->tiles.size(); ++t) pre[t + 1] = pre[t] + sub[t];
+  // greedy cut at cost budget `target` per CTA; returns the CTAs used (unbounded), pieces per pair
+  auto cut = [&](double target, std::vector<std::vector<Piece>>* out) {
+    int cta = 0;
+    double load = 0;
+    if (out) out->clear();
+    for (const QTile& q : qt) {
+      for (int u = 0; u < o.units; ++u) {
+        if (out) out->emplace_back();
+        int t = q.tb;
+        while (t < q.te) {
+          const double cap = target - load - kSubOverhead;
+          if (cap < 2 && load > 0) {
+            ++cta;
+            load = 0;
+            continue;
+          }
+          // largest t1 > t with pre[t1] - pre[t] <= cap (at least one tile)
+          const double lim = pre[t] + cap;
+          int t1 = static_cast<int>(std::upper_bound(pre.begin() + t + 1, pre.begin() + q.te + 1, lim) - pre.begin()) - 1;
+          t1 = std::max(t1, t + 1);
+          if (out) out->back().push_back({cta, t, t1});
+          load += pre[t1] - pre[t] + kSubOverhead;
+          t = t1;
+        }
+      }
+    }
+    return cta + (load > 0 ? 1 : 0);
+  };
+  // smallest budget whose greedy cut fits in `grid` CTAs (bisection; the cost is monotone enough)
+  double lo = total / grid, hi = total / grid + 4 * kSubOverhead + 64;
+  while (cut(hi, nullptr) > grid) hi *= 1.5;
+  for (int it = 0; it < 24 && hi - lo > 0.25; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (cut(mid, nullptr) <= grid)
+      hi = mid;
+    else
+      lo = mid;
+  }
+  std::vector<std::vector<Piece>> all;
+  cut(hi, &all);
+  std::vector<std::vector<int32_t>> per_cta(grid);
+  size_t pi = 0;
+  for (const QTile& q : qt) {
+    for (int u = 0; u < o.units; ++u, ++pi) {
+      const std::vector<Piece>& pieces = all[pi];
+      const int np = static_cast<int>(pieces.size());
+      if (np > 1) w->combine.push_back({q.row0, q.n_rows, w->n_parts, np, u * hpu, hpu});
+      for (int k = 0; k < np; ++k) {
+        WorkItem it{};
+        it.row0 = q.row0;
+        it.n_rows = q.n_rows;
+        it.tile_begin = pieces[k].t0;
+        it.tile_end = pieces[k].t1;
+        it.part = np > 1 ? w->n_parts + k : -1;
+        per_cta[pieces[k].cta].push_back(static_cast<int32_t>(w->items.size()) * o.units + u);
+        w->items.push_back(it);
+      }
+      if (np > 1) w->n_parts += np;
+    }
+  }
+  int used = grid;
+  while (used > 1 && per_cta[used - 1].empty()) --used;
+  w->grid = used;
+  w->cta_off.assign(used + 1, 0);
+  for (int c = 0; c < used; ++c) {
+    w->cta_off[c + 1] = w->cta_off[c] + static_cast<int32_t>(per_cta[c].size());
+    w->cta_items.insert(w->cta_items.end(), per_cta[c].begin(), per_cta[c].end());
+  }
 }
 
 }  // namespace spq

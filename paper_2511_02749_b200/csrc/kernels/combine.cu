@@ -29,19 +29,20 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineDesc* __restr
                                                       float* __restrict__ lse, int hq) {
   constexpr int E = D / 32;  // columns per lane
   const CombineDesc cd = desc[blockIdx.x];
-  const int h = blockIdx.y;
+  if (static_cast<int>(blockIdx.y) >= cd.n_heads) return;
+  const int h = cd.head0 + blockIdx.y;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // grid.z splits the 128 rows of a tile into groups of blockDim/32 rows: one warp per row
   for (int r = blockIdx.z * (blockDim.x / 32) + warp; r < cd.n_rows; r += gridDim.z * (blockDim.x / 32)) {
     float m = -INFINITY;
     for (int s = 0; s < cd.n_split; ++s)
-      m = fmaxf(m, lsepart[(static_cast<int64_t>(cd.part_base + s) * hq + h) * kTileRows + r]);
+      m = fmaxf(m, lsepart[(static_cast<int64_t>(cd.part_base + s) * cd.n_heads + blockIdx.y) * kTileRows + r]);
     float acc[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) acc[e] = 0.f;
     float tot = 0.f;
     for (int s = 0; s < cd.n_split; ++s) {
-      const int64_t pidx = (static_cast<int64_t>(cd.part_base + s) * hq + h) * kTileRows + r;
+      const int64_t pidx = (static_cast<int64_t>(cd.part_base + s) * cd.n_heads + blockIdx.y) * kTileRows + r;
       const float ls = lsepart[pidx];
       const float w = (ls == -INFINITY) ? 0.f : __expf(ls - m);
       tot += w;
@@ -66,7 +67,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineDesc* __restr
 
 template <int D, typename TO>
 void launch_dt(const CombineArgs& a, cudaStream_t st) {
-  dim3 grid(a.n_desc, a.hq, kTileRows / 8);
+  dim3 grid(a.n_desc, a.heads_per_desc, kTileRows / 8);
   combine_kernel<D, TO><<<grid, 256, 0, st>>>(a.desc, a.opart, a.lsepart, static_cast<TO*>(a.o), a.lse, a.hq);
 }
 

@@ -73,6 +73,7 @@ struct CombineArgs {
   void* o;
   float* lse;
   int hq, d;
+  int heads_per_desc;  // max CombineDesc::n_heads
   bool out_fp32;
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);

@@ -53,15 +53,20 @@ constexpr uint32_t kColS = 0, kColO = 256;  // S_x at kColS + 128x, O_x at kColO
 template <int D>
 struct TcSmem {
   static constexpr int kChunks = D / 64;
-  static constexpr int kChunkBytes = 128 * 128;  // 128 rows x 128 B
-  static constexpr int kKvSlots = D == 64 ? 6 : 3;
+  static constexpr int kChunkBytes = 128 * 128;  // Q: 128 rows x 128 B per 64-column chunk
+  static constexpr int kSubBytes = 64 * 128;     // K/V: 64 keys x 128 B per 64-column chunk
+  // K is needed one step after its slot frees (S(j+2) right after PV(j)), V two steps later:
+  // the K ring is twice as deep as the V ring
+  static constexpr int kKSlots = D == 64 ? 8 : 4;
+  static constexpr int kVSlots = D == 64 ? 4 : 2;
   static constexpr int kQSlots = 3;
   alignas(1024) uint8_t q[kQSlots][kChunks][kChunkBytes];
-  alignas(1024) uint8_t kv[kKvSlots][kChunks][kChunkBytes];  // ring: K_0 V_0 K_1 V_1 ...
-  alignas(1024) float stage[8][32 * 32];                       // epilogue transpose, per softmax warp
-  uint64_t kv_full[kKvSlots], kv_empty[kKvSlots];
+  alignas(1024) uint8_t k[kKSlots][kChunks][kSubBytes];  // ring of 64-key K sub-tiles
+  alignas(1024) uint8_t v[kVSlots][kChunks][kSubBytes];  // ring of 64-key V sub-tiles
+  alignas(1024) float stage[8][32 * 32];                        // epilogue transpose, per softmax warp
+  uint64_t kv_full[2][kKSlots], kv_empty[2][kKSlots];  // [K, V][slot] (V uses the first kVSlots)
   uint64_t q_full[3], q_empty[3], q_load[3];
-  uint64_t s_full[2][2], p_full[2][2], o_done[2];  // [head][S buffer]
+  uint64_t s_full[2][2], p_full[2][2], o_done[2][2];  // [head][S buffer / PV parity j & 1]
   uint32_t tmem_base;
 };
 
@@ -76,6 +81,8 @@ struct TcParams {
   int paired;     // 1: a unit is a GQA head pair (A = 2u, B = 2u+1); 0: one head (B idle)
   int poly_mask;  // pair i of a 32-key chunk uses the FMA-pipe exp2 when (i & 3) < poly_mask
   float rescale_threshold;  // log2 units; O is rescaled when the running max grows by more
+  int pingpong;  // 1: the two softmax warpgroups alternate (named barriers 1, 2)
+  int epi_tma;   // epilogue stores: 1 = TMA bulk stores of 32x32 staging tiles, 0 = coalesced st.global
   int dbg_mode;  // profiling only: 1 = softmax does no math, 2 = max pass only,
                  // 3 = 1 + K/V always from the first block (L2-resident), 4 = 1 + MMA skips K/V waits,
                  // 5 = 1 + Q prep does no work
@@ -86,10 +93,12 @@ __device__ __forceinline__ TcSmem<D>& smem_ref(uint8_t* raw) {
   return *reinterpret_cast<TcSmem<D>*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
 }
 
-// profiling only: CTA 0 records (event, clock) pairs per role; 1024 events per role
-__device__ __forceinline__ void trace(const TcParams& P, int role, uint32_t& cnt, int ev) {
+// profiling only: CTA 0 records (event, clock) pairs per warp (lane 0 / the elected thread);
+// 1024 events per warp
+constexpr int kTraceWarps = 16;
+__device__ __forceinline__ void trace(const TcParams& P, int, uint32_t& cnt, int ev) {
   if (P.a.dbg_trace == nullptr || blockIdx.x != 0 || cnt >= 1024) return;
-  long long* t = P.a.dbg_trace + (role * 1024 + cnt) * 2;
+  long long* t = P.a.dbg_trace + ((threadIdx.x / 32) * 1024 + cnt) * 2;
   t[0] = ev;
   t[1] = clock64();
   ++cnt;
@@ -133,66 +142,80 @@ __device__ __forceinline__ void ex2_pair_f16(float x0, float x1, float& p0, floa
       : "r"(e));
 }
 
-// ------------------------------------------------------------------ warp 0: TMA producer
+// ------------------------------------------------------------------ warps 0 / 3: TMA producers
+// K (warp 0) and V (warp 3) are streamed per 64-key sub-tile (the MMA granularity) into two
+// independent rings, so a K load never queues behind a V slot (S(j+2) needs K(j+2) one step
+// after PV(j); V(j) is needed two steps later). Sub-tile s goes to slot s % (ring depth).
+// Each sub-tile is 64/bs paged blocks (bs <= 64) or half of one 128-row block, gathered by TMA
+// boxes {64 columns, min(bs, 64) rows}.
 template <int D>
-__device__ void run_producer(const TcParams& P, TcSmem<D>& S, int it_begin, int it_end) {
+__device__ void run_producer(const TcParams& P, TcSmem<D>& S, int it_begin, int it_end, int kv) {
   const AttnArgs& a = P.a;
-  constexpr int kSlots = TcSmem<D>::kKvSlots;
+  const int kSlots = kv == 0 ? TcSmem<D>::kKSlots : TcSmem<D>::kVSlots;
   const int group = a.hq / a.hkv;
-  const int bpt = kTileKeys / a.bs;
-  constexpr uint32_t kTileBytes = 128 * D * 2;
+  const int box = min(a.bs, 64);
+  const int bps = 64 / box;  // boxes per sub-tile
+  constexpr uint32_t kSubTileBytes = 64 * D * 2;
   const int64_t layer_rows = static_cast<int64_t>(a.layer) * a.nblk * a.hkv * a.bs;
-  uint32_t n = 0;  // load index: K_j = 2j, V_j = 2j+1 over the CTA's whole tile sequence
+  const CUtensorMap* map = kv == 0 ? &P.tmk : &P.tmv;
+  uint32_t n = 0;
   uint32_t tc = 0;
   for (int ii = it_begin; ii < it_end; ++ii) {
     const Unit u = decode(P, a.cta_items[ii]);
     const int kvh = u.head_a / group;
     for (int t = u.w.tile_begin; t < u.w.tile_end; ++t) {
-      const int32_t boff = a.tiles[t].blk_off;
+      const KvTile tl = a.tiles[t];
+      const int nsub = tl.n_valid > 64 ? 2 : 1;
 #pragma unroll 1
-      for (int kv = 0; kv < 2; ++kv, ++n) {
+      for (int h = 0; h < nsub; ++h, ++n) {
         const int slot = n % kSlots;
-        mbar_wait(&S.kv_empty[slot], ((n / kSlots) & 1) ^ 1);
+        mbar_wait(&S.kv_empty[kv][slot], ((n / kSlots) & 1) ^ 1);
         trace(P, 0, tc, 10 + kv);  // 10: K load issued, 11: V load issued
-        mbar_arrive_expect_tx(&S.kv_full[slot], kTileBytes);
-        const CUtensorMap* map = kv == 0 ? &P.tmk : &P.tmv;
-        for (int j = 0; j < bpt; ++j) {
-          const int32_t blk = P.dbg_mode == 3 ? a.tile_blocks[0] : a.tile_blocks[boff + j];
-          const int32_t y = static_cast<int32_t>(layer_rows + (static_cast<int64_t>(blk) * a.hkv + kvh) * a.bs);
+        mbar_arrive_expect_tx(&S.kv_full[kv][slot], kSubTileBytes);
+        for (int j = 0; j < bps; ++j) {
+          // key 64h + j*box of the tile: block (64h + j*box) / bs, row offset (64h + j*box) % bs
+          const int key = 64 * h + j * box;
+          const int32_t blk = P.dbg_mode == 3 ? a.tile_blocks[0] : a.tile_blocks[tl.blk_off + key / a.bs];
+          const int32_t y = static_cast<int32_t>(layer_rows + (static_cast<int64_t>(blk) * a.hkv + kvh) * a.bs +
+                                                 key % a.bs);
 #pragma unroll
           for (int c = 0; c < D / 64; ++c)
-            tma_load_2d(&S.kv[slot][c][j * a.bs * 128], map, &S.kv_full[slot], c * 64, y);
+            tma_load_2d((kv == 0 ? &S.k[slot][c][0] : &S.v[slot][c][0]) + j * box * 128, map, &S.kv_full[kv][slot],
+                        c * 64, y);
         }
       }
     }
   }
 }
 
-// ------------------------------------------------------------------ warp 1: MMA issuer
-// Work is issued per 64-key sub-tile j (a KV tile holds one or two). Each head has two S
-// buffers, so S(j+2) is issued as soon as PV(j) (which reads P(j) from S buffer j&1) is issued:
-// softmax(j+1) never waits for the tensor core to finish PV(j). Order per step:
-//   PV_A(j), PV_B(j), [release V], S_A(j+2), S_B(j+2)  (after a prologue S_A(0),S_B(0),S_A(1),S_B(1))
+// ------------------------------------------------------------------ warps 1 / 2: MMA issuers
+// One issuing thread per head (warp 1: head A, warp 2: head B), so each head's chain
+// softmax(j) -> PV(j) -> S(j+2) runs at its own pace and the tensor core interleaves the two.
+// Work is issued per 64-key sub-tile j. Each head has two S buffers, so S(j+2) is issued as
+// soon as PV(j) (which reads P(j) from S buffer j&1) is issued: softmax(j+1) never waits for the
+// tensor core to finish PV(j). Per head: S(0), S(1), then PV(j), [release V_j], S(j+2), ...
+// K_j / V_j slots are released when both heads' MMAs reading them are done (2 commits).
 struct SubCursor {
   int t, h;  // KV tile, half (keys [64h, 64h+64))
 };
 
 template <int D>
-__device__ void run_mma(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_begin, int it_end) {
+__device__ void run_mma(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_begin, int it_end, int x) {
   const AttnArgs& a = P.a;
-  constexpr int kSlots = TcSmem<D>::kKvSlots;
+  constexpr int kKS = TcSmem<D>::kKSlots, kVS = TcSmem<D>::kVSlots;
   constexpr uint32_t idS = idesc_bf16_f32(128, 64, false, false);
   constexpr uint32_t idO = idesc_bf16_f32(128, D, false, true);
-  uint32_t kbase_g = 0;  // KV tiles consumed before the current item (K_t = load 2g, V_t = 2g+1)
-  uint32_t jg = 0;       // sub-tiles whose PV has been issued (global): S buffer j & 1
-  uint32_t ep = 0;       // Q epochs started
+  uint32_t jg = 0;  // sub-tiles whose PV has been issued (global): S buffer j & 1, V slot j
+  uint32_t ep = 0;  // Q epochs started
   uint32_t tc = 0;
-  auto wait_kv = [&](uint32_t n) {
-    mbar_wait(&S.kv_full[n % kSlots], (n / kSlots) & 1);
+  auto wait_kv = [&](int kv, uint32_t n) {
+    const uint32_t ns = kv == 0 ? kKS : kVS;
+    mbar_wait(&S.kv_full[kv][n % ns], (n / ns) & 1);
     tc_fence_after();
   };
   for (int ii = it_begin; ii < it_end; ++ii) {
     const Unit u = decode(P, a.cta_items[ii]);
+    if (x >= u.n_heads) continue;  // unpaired launch: the B issuer idles
     const bool two = u.n_heads == 2;
     const int tb = u.w.tile_begin, te = u.w.tile_end;
     auto nsub = [&](int t) { return a.tiles[t].n_valid > 64 ? 2 : 1; };
@@ -202,137 +225,229 @@ __device__ void run_mma(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_b
       else
         c = SubCursor{c.t + 1, 0};
     };
-    int qa = 0, qb = 1;
+    int qa = 0, qb = 1;  // this epoch's Q slots (A's, B's)
     SubCursor cs{tb, 0}, cp{tb, 0};
-    uint32_t js = jg;  // global index of the next S sub-tile
-    // S for sub-tile cs of head x (buffer js & 1); handles epoch changes and K arrival
-    auto issue_s = [&](int x) {
+    uint32_t js = jg;  // global index of the next S sub-tile (K slot js)
+    // the Q slot(s) this issuer owns: its head's; an unpaired launch's A issuer also frees B's
+    auto release_q = [&]() {
+      mma_commit(&S.q_empty[x == 0 ? qa : qb]);
+      if (!two) mma_commit(&S.q_empty[qb]);
+    };
+    auto issue_s = [&]() {
       const int t = cs.t;
-      if (x == 0 && cs.h == 0) {
-        if (t == tb || a.tiles[t].rot_delta != a.tiles[t - 1].rot_delta) {
-          if (t != tb) {  // the previous epoch's Q tiles: free once the S MMAs issued so far are done
-            mma_commit(&S.q_empty[qa]);
-            mma_commit(&S.q_empty[qb]);
-          }
-          qa = (2 * ep) % 3;
-          qb = (2 * ep + 1) % 3;
-          mbar_wait(&S.q_full[qa], ((2 * ep) / 3) & 1);
-          if (two) mbar_wait(&S.q_full[qb], ((2 * ep + 1) / 3) & 1);
-          trace(P, 1, tc, 21);  // 21: Q ready for new epoch
-          ++ep;
-        }
-        wait_kv(2 * (kbase_g + (t - tb)));
-        trace(P, 1, tc, 22);  // 22: K ready
+      if (cs.h == 0 && (t == tb || a.tiles[t].rot_delta != a.tiles[t - 1].rot_delta)) {
+        if (t != tb) release_q();  // the previous epoch's Q tile: free once its S MMAs are done
+        qa = (2 * ep) % 3;
+        qb = (2 * ep + 1) % 3;
+        const int mine = x == 0 ? qa : qb;
+        mbar_wait(&S.q_full[mine], ((2 * ep + x) / 3) & 1);
+        trace(P, 1, tc, 21);  // 21: Q ready for new epoch
+        ++ep;
       }
-      const uint32_t kslot = (2 * (kbase_g + (t - tb))) % kSlots;
+      wait_kv(0, js);
+      trace(P, 1, tc, 22);  // 22: K ready
       const uint32_t qbase = smem_u32(&S.q[x == 0 ? qa : qb][0][0]);
-      const uint32_t kb = smem_u32(&S.kv[kslot][0][0]) + cs.h * 64 * 128;
+      const uint32_t kb = smem_u32(&S.k[js % kKS][0][0]);
       const int buf = js & 1;
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
-        const uint32_t off = (kk / 4) * TcSmem<D>::kChunkBytes + (kk % 4) * 32;
-        mma_ss(tmem + kColS + 128 * x + 64 * buf, desc_sw128(qbase + off, 16, 1024), desc_sw128(kb + off, 16, 1024),
-               idS, kk > 0 ? 1u : 0u);
+        mma_ss(tmem + kColS + 128 * x + 64 * buf,
+               desc_sw128(qbase + (kk / 4) * TcSmem<D>::kChunkBytes + (kk % 4) * 32, 16, 1024),
+               desc_sw128(kb + (kk / 4) * TcSmem<D>::kSubBytes + (kk % 4) * 32, 16, 1024), idS, kk > 0 ? 1u : 0u);
       }
       mma_commit(&S.s_full[x][buf]);
-    };
-    // after both heads' S of cursor cs: release K when its last sub-tile is done; end of item
-    // releases the Q tiles
-    auto finish_s = [&]() {
-      const int t = cs.t;
-      const bool last_of_tile = cs.h == nsub(t) - 1;
-      if (last_of_tile) mma_commit(&S.kv_empty[(2 * (kbase_g + (t - tb))) % kSlots]);
+      mma_commit(&S.kv_empty[0][js % kKS]);  // K_js (one of the heads' two arrivals)
       advance(cs);
       ++js;
-      if (cs.t >= te) {
-        mma_commit(&S.q_empty[qa]);
-        mma_commit(&S.q_empty[qb]);
-      }
+      if (cs.t >= te) release_q();
     };
-    auto issue_pv = [&](int x, uint32_t j, bool first) {
-      const int t = cp.t;
-      if (x == 0 && cp.h == 0) wait_kv(2 * (kbase_g + (t - tb)) + 1);
-      const uint32_t vslot = (2 * (kbase_g + (t - tb)) + 1) % kSlots;
-      const uint32_t vb = smem_u32(&S.kv[vslot][0][0]) + cp.h * 64 * 128;
+    auto issue_pv = [&](uint32_t j, bool first) {
+      wait_kv(1, j);
+      trace(P, 1, tc, 24);  // 24: V ready
+      // V sub-tile, MN-major: 64-column d chunks kSubBytes apart (LBO), 16 keys = 2048 B per K step
+      const uint32_t vb = smem_u32(&S.v[j % kVS][0][0]);
       const int buf = j & 1;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
-        const uint64_t vd = desc_sw128(vb + kk * 2048, 16384, 1024);
+        const uint64_t vd = desc_sw128(vb + kk * 2048, TcSmem<D>::kSubBytes, 1024);
         mma_ts(tmem + kColO + 128 * x, tmem + kColS + 128 * x + 64 * buf + kk * 8, vd, idO,
                (!first || kk > 0) ? 1u : 0u);
       }
-      mma_commit(&S.o_done[x]);
+      mma_commit(&S.o_done[x][j & 1]);
+      mma_commit(&S.kv_empty[1][j % kVS]);  // V_j
     };
     // prologue: S for the first two sub-tiles
-    for (int i = 0; i < 2 && cs.t < te; ++i) {
-      issue_s(0);
-      if (two) issue_s(1);
-      finish_s();
-    }
+    for (int i = 0; i < 2 && cs.t < te; ++i) issue_s();
     bool first = true;
     while (cp.t < te) {
       const uint32_t j = jg;
-      mbar_wait(&S.p_full[0][j & 1], (j >> 1) & 1);
-      trace(P, 1, tc, 20);  // 20: P_A ready
-      issue_pv(0, j, first);
-      if (two) {
-        mbar_wait(&S.p_full[1][j & 1], (j >> 1) & 1);
-        trace(P, 1, tc, 23);  // 23: P_B ready
-        issue_pv(1, j, first);
-      }
-      // V is released before the next S pair: with one-sub-tile tiles the S cursor runs two KV
-      // tiles ahead and, in a 3-slot ring, K_{t+2} reuses V_t's slot
-      if (cp.h == nsub(cp.t) - 1) mma_commit(&S.kv_empty[(2 * (kbase_g + (cp.t - tb)) + 1) % kSlots]);
-      if (cs.t < te) {
-        issue_s(0);
-        if (two) issue_s(1);
-        finish_s();
-      }
+      mbar_wait(&S.p_full[x][j & 1], (j >> 1) & 1);
+      trace(P, 1, tc, 20);  // 20: P ready
+      issue_pv(j, first);
+      if (cs.t < te) issue_s();
       advance(cp);
       ++jg;
       first = false;
     }
-    kbase_g += te - tb;
   }
 }
 
-// pass 2 of the softmax over one 64-key S sub-tile row in TMEM: P = exp2(s*scale - m) written
-// back as packed bf16 over its first 32 columns; per-row sums in 8 independent accumulators.
+// Online softmax over one 64-key S sub-tile row in TMEM, single pass: one LDTM.x64 of the 64
+// fp32 scores, row max with three-input FMNMX3, then P = exp2(s*scale - m) packed to bf16 and
+// written back over the first 32 columns of the sub-tile with one STTM.x32. The running max m
+// only moves when the new max exceeds it by more than `thr` (log2 units: P <= 2^thr), and then
+// *alpha = 2^(m_old - m_new) is the factor for O and l. Returns the row sum of P (fp32, before
+// bf16 rounding; 8 independent accumulators).
 template <int PM, bool kMasked>
-__device__ __forceinline__ void exp_pass(uint32_t scol, float sl2, float msub, int lim, float (&sum8)[8]) {
+__device__ __forceinline__ float softmax_sub(uint32_t scol, float sl2, float thr, int lim, float& m, float& alpha,
+                                             bool& resc) {
+  uint32_t v[64];
+  tmem_ld64(scol, v);
+  tmem_wait_ld();
+  if constexpr (kMasked) {
 #pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    uint32_t v[32];
-    tmem_ld32(scol + c * 32, v);
-    tmem_wait_ld();
-    uint32_t pk[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int j0 = c * 32 + 2 * i;
-      const float x0 = fmaf(__uint_as_float(v[2 * i]), sl2, -msub);
-      const float x1 = fmaf(__uint_as_float(v[2 * i + 1]), sl2, -msub);
-      float p0, p1;
-      if constexpr (PM == 3) {
-        ex2_pair_f16(x0, x1, p0, p1);
-      } else {
-        constexpr bool kPoly[4] = {0 < PM, 1 < PM, 2 < PM, 3 < PM};
-        p0 = kPoly[i & 3] ? exp2_poly(x0) : ex2_approx(x0);
-        p1 = kPoly[i & 3] ? exp2_poly(x1) : ex2_approx(x1);
-      }
-      if (kMasked) {
-        p0 = (j0 <= lim) ? p0 : 0.f;
-        p1 = (j0 + 1 <= lim) ? p1 : 0.f;
-      }
-      sum8[(2 * i) & 7] += p0;
-      sum8[(2 * i + 1) & 7] += p1;
-      pk[i] = pack_bf16x2(p0, p1);
-    }
-    tmem_st16(scol + c * 16, pk);
+    for (int i = 0; i < 64; ++i) v[i] = i <= lim ? v[i] : 0xff800000u;  // -inf
   }
+  float mx4[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) mx4[k] = fmaxf(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
+#pragma unroll
+  for (int i = 4; i < 32; ++i)
+    mx4[i & 3] = fmax3(mx4[i & 3], __uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+  const float mx = fmax3(fmaxf(mx4[0], mx4[1]), mx4[2], mx4[3]) * sl2;
+  const float m_new = fmaxf(m, mx);
+  resc = m_new > m + thr;
+  const float m_use = resc ? m_new : m;
+  alpha = resc ? ex2_approx(m - m_new) : 1.f;
+  m = m_use;
+  const float msub = (m_use == -INFINITY) ? 0.f : m_use;
+  float sum8[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sum8[i] = 0.f;
+  uint32_t pk[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const float x0 = fmaf(__uint_as_float(v[2 * i]), sl2, -msub);
+    const float x1 = fmaf(__uint_as_float(v[2 * i + 1]), sl2, -msub);
+    float p0, p1;
+    if constexpr (PM == 3) {
+      ex2_pair_f16(x0, x1, p0, p1);
+    } else {
+      constexpr bool kPoly[4] = {0 < PM, 1 < PM, 2 < PM, 3 < PM};
+      p0 = kPoly[i & 3] ? exp2_poly(x0) : ex2_approx(x0);
+      p1 = kPoly[i & 3] ? exp2_poly(x1) : ex2_approx(x1);
+    }
+    if constexpr (kMasked) {
+      p0 = (2 * i <= lim) ? p0 : 0.f;
+      p1 = (2 * i + 1 <= lim) ? p1 : 0.f;
+    }
+    sum8[(2 * i) & 7] += p0;
+    sum8[(2 * i + 1) & 7] += p1;
+    pk[i] = pack_bf16x2(p0, p1);
+  }
+  tmem_st32(scol, pk);
   tmem_wait_st();
+  return ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) + ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
 }
 
 // ------------------------------------------------------------------ softmax + epilogue (one WG per head)
+// A finished item whose O sits in TMEM.
+struct Finished {
+  WorkItem w;
+  float m, l;
+  int h, n_heads;
+  uint32_t jlast;  // global index of the item's last sub-tile (its PV is the last write to O)
+};
+
+// Epilogue of one finished item: wait for its last PV, read O from TMEM, normalise, store. Each warp stages 32 rows x 32 fp32 columns in its 4 KB SWIZZLE_128B buffer
+// and one lane hands it to a TMA bulk store (the warp only waits until the TMA has READ the
+// buffer before reusing it, never for the HBM write).
+template <int D>
+__device__ __forceinline__ void epilogue(const TcParams& P, TcSmem<D>& S, uint32_t ocol, int x, const Finished& f,
+                                         uint32_t& tc, bool tr) {
+  const AttnArgs& a = P.a;
+  const WorkItem& w = f.w;
+  const int r = threadIdx.x & 127;
+  mbar_wait(&S.o_done[x][f.jlast & 1], (f.jlast >> 1) & 1);
+  if (tr) trace(P, 2 + x, tc, 32);  // 32: O ready (epilogue start)
+  tc_fence_after();
+  // chunk c+1 is read from TMEM while chunk c is staged and stored
+  uint32_t vv[2][32];
+  tmem_ld32(ocol, vv[0]);
+  tmem_wait_ld();
+  const float inv = f.l > 0.f ? 1.f / f.l : 0.f;
+  const float lse = f.l > 0.f ? (f.m + __log2f(f.l)) * 0.69314718055994531f : -INFINITY;
+  const int wr = (threadIdx.x / 32) & 3;  // warp's 32-row slice of the tile
+  const int lane = threadIdx.x & 31;
+  float* stg = S.stage[x * 4 + wr];
+  // TMA store for whole 32-row slices (and for split partials, whose padding rows are never
+  // read); a slice that ends inside this item's rows is written directly (the next rows belong
+  // to another item)
+  const bool in_range = wr * 32 < w.n_rows;
+  const bool use_tma = P.epi_tma && in_range && (w.part >= 0 || (a.out_fp32 && wr * 32 + 32 <= w.n_rows));
+  const bool direct = in_range && !use_tma;
+#pragma unroll
+  for (int c = 0; c < D / 32; ++c) {
+    if (c + 1 < D / 32) tmem_ld32(ocol + (c + 1) * 32, vv[(c + 1) & 1]);
+    const uint32_t(&v)[32] = vv[c & 1];
+    if (use_tma && lane == 0) bulk_wait_read<0>();  // previous chunk's store has read the buffer
+    __syncwarp();
+#pragma unroll
+    for (int uu = 0; uu < 8; ++uu)
+      *reinterpret_cast<float4*>(stg + lane * 32 + ((uu ^ (lane & 7)) * 4)) =
+          make_float4(__uint_as_float(v[4 * uu]) * inv, __uint_as_float(v[4 * uu + 1]) * inv,
+                      __uint_as_float(v[4 * uu + 2]) * inv, __uint_as_float(v[4 * uu + 3]) * inv);
+    if (use_tma) {
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if (w.part >= 0)
+          tma_store_2d(&P.tmop, stg, c * 32, (w.part * f.n_heads + x) * kTileRows + wr * 32);
+        else
+          tma_store_3d(&P.tmo, stg, c * 32, f.h, w.row0 + wr * 32);
+        bulk_commit();
+      }
+    } else {
+      __syncwarp();
+    }
+    if (direct) {  // coalesced: each store instruction writes 4 rows x 128 B
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int rr = j * 4 + (lane >> 3);
+        const int uu = lane & 7;
+        const float4 val = *reinterpret_cast<const float4*>(stg + rr * 32 + ((uu ^ (rr & 7)) * 4));
+        const int trow = wr * 32 + rr;
+        const int col = c * 32 + uu * 4;
+        if (w.part >= 0) {
+          *reinterpret_cast<float4*>(a.opart + (static_cast<int64_t>(w.part * f.n_heads + x) * kTileRows + trow) * D +
+                                     col) = val;
+        } else if (trow < w.n_rows) {
+          if (a.out_fp32) {
+            *reinterpret_cast<float4*>(static_cast<float*>(a.o) +
+                                       ((w.row0 + trow) * static_cast<int64_t>(a.hq) + f.h) * D + col) = val;
+          } else {
+            uint2 pk;
+            pk.x = pack_bf16x2(val.x, val.y);
+            pk.y = pack_bf16x2(val.z, val.w);
+            *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.o) +
+                                      ((w.row0 + trow) * static_cast<int64_t>(a.hq) + f.h) * D + col) = pk;
+          }
+        }
+      }
+      __syncwarp();
+    }
+    tmem_wait_ld();
+  }
+  if (r < w.n_rows) {
+    if (w.part < 0) {
+      if (a.lse != nullptr) a.lse[(static_cast<int64_t>(w.row0) + r) * a.hq + f.h] = lse;
+    } else {
+      a.lsepart[(static_cast<int64_t>(w.part) * f.n_heads + x) * kTileRows + r] = lse;
+    }
+  }
+  if (tr) trace(P, 2 + x, tc, 33);  // 33: epilogue done
+}
+
 template <int D, int PM>
 __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_begin, int it_end, int x) {
   const AttnArgs& a = P.a;
@@ -340,13 +455,13 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
   const uint32_t lane_base = static_cast<uint32_t>((r / 32) * 32) << 16;
   const float sl2 = P.scale_log2;
   const uint32_t ocol = tmem + lane_base + kColO + 128 * x;
-  uint32_t js = 0, od = 0;  // sub-tiles processed, o_done phases consumed
+  uint32_t js = 0;  // sub-tiles processed (global; == the MMA warps' PV index)
+  bool js_started = false;  // ping-pong: A waits for B's previous step from its second step on
   uint32_t tc = 0;
-  const bool tr = (threadIdx.x & 127) == 0;
+  const bool tr = (threadIdx.x & 31) == 0;
   for (int ii = it_begin; ii < it_end; ++ii) {
     const Unit u = decode(P, a.cta_items[ii]);
     if (x >= u.n_heads) continue;  // single-head unit: WG B idles
-    const int h = u.head_a + x;
     const WorkItem& w = u.w;
     const bool valid = r < w.n_rows;
     const int64_t row = static_cast<int64_t>(w.row0) + r;
@@ -364,149 +479,65 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
         mbar_wait(&S.s_full[x][buf], (js >> 1) & 1);
         if (tr) trace(P, 2 + x, tc, 30);  // 30: S ready
         tc_fence_after();
-        // pass 1: row max (8 independent accumulators); masks only on partial sub-tiles
+        // masks only on partial sub-tiles
         const bool full = __all_sync(0xffffffffu, lim >= 63);
-        float mx8[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t v[32];
-          tmem_ld32(scol + c * 32, v);
-          tmem_wait_ld();
-          if (full) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v[i]));
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (c * 32 + i <= lim) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v[i]));
-          }
-        }
-        float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-        mx *= sl2;
-        const float m_new = fmaxf(m, mx);
-        const bool resc = m_new > m + P.rescale_threshold;
-        const float m_use = resc ? m_new : m;
-        const float alpha = resc ? ex2_approx(m - m_new) : 1.f;
-        const float msub = (m_use == -INFINITY) ? 0.f : m_use;
-        // pass 2: P = exp2(s*scale - m) -> bf16 over the first 32 columns of the sub-tile
-        float sum8[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) sum8[i] = 0.f;
-        if (full)
-          exp_pass<PM, false>(scol, sl2, msub, lim, sum8);
-        else
-          exp_pass<PM, true>(scol, sl2, msub, lim, sum8);
-        const float sum = ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) + ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
-        l = l * alpha + sum;
-        m = m_use;
-        // PV of the previous sub-tile must have landed in O before O is rescaled (and before
-        // PV of this sub-tile accumulates onto it): one o_done phase per PV, consumed in order
-        if (!first) {
-          mbar_wait(&S.o_done[x], od & 1);
-          ++od;
-          tc_fence_after();
-          if (__any_sync(0xffffffffu, resc)) {
-#pragma unroll 1
-            for (int c = 0; c < D / 32; ++c) {
-              uint32_t v[32];
-              tmem_ld32(ocol + c * 32, v);
-              tmem_wait_ld();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-              tmem_st32(ocol + c * 32, v);
-            }
-            tmem_wait_st();
-          }
-        }
-        first = false;
-        tc_fence_before();
-        if (tr) trace(P, 2 + x, tc, 31);  // 31: P written
-        mbar_arrive(&S.p_full[x][buf]);
-      }
-    }
-    // epilogue: wait for the last PV of this head, normalise, store
-    mbar_wait(&S.o_done[x], od & 1);
-    ++od;
-    if (tr) trace(P, 2 + x, tc, 32);  // 32: O ready (epilogue start)
-    tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    const float lse = l > 0.f ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
-    // O tile -> global: each warp stages 32 rows x 32 fp32 columns in its 4 KB SWIZZLE_128B buffer
-    // and one lane hands it to a TMA bulk store (async: the warp only waits until the TMA has
-    // READ the buffer before reusing it, never for the HBM write).
-    {
-      const int wr = (threadIdx.x / 32) & 3;  // warp's 32-row slice of the tile
-      const int lane = threadIdx.x & 31;
-      float* stg = S.stage[x * 4 + wr];
-      // TMA store for whole 32-row slices (and for split partials, whose padding rows are never
-      // read); a slice that ends inside this item's rows is written directly (the next rows
-      // belong to another item)
-      const bool in_range = wr * 32 < w.n_rows;
-      const bool use_tma = in_range && (w.part >= 0 || (a.out_fp32 && wr * 32 + 32 <= w.n_rows));
-      const bool direct = in_range && !use_tma;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(ocol + c * 32, v);
-        tmem_wait_ld();
-        if (lane == 0) bulk_wait_read<0>();  // previous chunk's store has read the buffer
-        __syncwarp();
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          *reinterpret_cast<float4*>(stg + lane * 32 + ((u ^ (lane & 7)) * 4)) =
-              make_float4(__uint_as_float(v[4 * u]) * inv, __uint_as_float(v[4 * u + 1]) * inv,
-                          __uint_as_float(v[4 * u + 2]) * inv, __uint_as_float(v[4 * u + 3]) * inv);
-        if (use_tma) {
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            if (w.part >= 0)
-              tma_store_2d(&P.tmop, stg, c * 32, (w.part * a.hq + h) * kTileRows + wr * 32);
-            else
-              tma_store_3d(&P.tmo, stg, c * 32, h, w.row0 + wr * 32);
-            bulk_commit();
-          }
+        float alpha;
+        bool resc;
+        float sum;
+        if (P.dbg_mode == 1) {  // profiling only: no softmax work (timing of the other roles)
+          alpha = 1.f;
+          resc = false;
+          sum = 1.f;
+          m = 0.f;
         } else {
-          __syncwarp();
+          // ping-pong (paired units): the two heads' softmax steps alternate on the SMSPs' MUFU
+          // (A(j), B(j), A(j+1), ...); barrier 1: "A finished step j", 2: "B finished step j"
+          const bool pp = P.pingpong && u.n_heads == 2;
+          if (pp && x == 1) named_sync(1, 256);
+          if (pp && x == 0 && js_started) named_sync(2, 256);
+          sum = full ? softmax_sub<PM, false>(scol, sl2, P.rescale_threshold, lim, m, alpha, resc)
+                     : softmax_sub<PM, true>(scol, sl2, P.rescale_threshold, lim, m, alpha, resc);
+          if (pp) named_arrive(x == 0 ? 1 : 2, 256);
+          js_started = true;
         }
-        if (direct) {
+        l = l * alpha + sum;
+        // O is only touched when a row's running max moved (rare with the threshold): then PV of
+        // the previous sub-tile must have landed first. PV(j) commits to o_done[x][j & 1], phase
+        // j >> 1; PV(j + 2) cannot complete before this warp releases P(j + 2), so a parity wait
+        // is exact even though most phases are never observed.
+        if (!first && __any_sync(0xffffffffu, resc)) {
+          const uint32_t jp = js - 1;
+          mbar_wait(&S.o_done[x][jp & 1], (jp >> 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld32(ocol + c * 32, v);
+            tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int rr = j * 4 + (lane >> 3);
-            const int u = lane & 7;
-            const float4 val = *reinterpret_cast<const float4*>(stg + rr * 32 + ((u ^ (rr & 7)) * 4));
-            const int trow = wr * 32 + rr;
-            if (trow < w.n_rows) {
-              const int col = c * 32 + u * 4;
-              if (a.out_fp32) {
-                *reinterpret_cast<float4*>(static_cast<float*>(a.o) +
-                                           ((w.row0 + trow) * static_cast<int64_t>(a.hq) + h) * D + col) = val;
-              } else {
-                uint2 pk;
-                pk.x = pack_bf16x2(val.x, val.y);
-                pk.y = pack_bf16x2(val.z, val.w);
-                *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.o) +
-                                          ((w.row0 + trow) * static_cast<int64_t>(a.hq) + h) * D + col) = pk;
-              }
-            }
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+            tmem_st32(ocol + c * 32, v);
           }
-          __syncwarp();
+          tmem_wait_st();
         }
+        if (tr) trace(P, 2 + x, tc, 31);  // 31: P written
+        tc_fence_before();
+        mbar_arrive(&S.p_full[x][buf]);
+        first = false;
       }
     }
-    if (valid) {
-      if (w.part < 0) {
-        if (a.lse != nullptr) a.lse[row * a.hq + h] = lse;
-      } else {
-        a.lsepart[(static_cast<int64_t>(w.part) * a.hq + h) * kTileRows + r] = lse;
-      }
-    }
-    if (tr) trace(P, 2 + x, tc, 33);  // 33: epilogue done
-    tc_fence_before();
+    Finished f;
+    f.w = w;
+    f.m = m;
+    f.l = l;
+    f.h = u.head_a + x;
+    f.n_heads = u.n_heads;
+    f.jlast = js - 1;
+    epilogue<D>(P, S, ocol, x, f, tc, tr);
   }
+  tc_fence_before();
+  // consume B's last ping-pong arrival so no named barrier is left mid-phase
+  if (P.pingpong && P.paired && x == 0 && js_started) named_sync(2, 256);
 }
 
 // ------------------------------------------------------------------ warps 12-15: Q prep
@@ -516,74 +547,74 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
 // rotate-half partner sits in lane l^16 (one shuffle) — with the fp32 (cos, sin) of its pairs
 // loaded coalesced from the table, 8 rows per batch. Rows past n_rows are rotated too but never
 // stored by the epilogue; rows past the tensor are zero (TMA out-of-bounds fill).
+// One step rotates R rows (R = 4 at d=128, 8 at d=64): lane l owns 8 rotate-half pairs
+// (i, i + d/2) of row g = l / (32/R): the 16-byte unit u of the first half and the same unit of
+// the second half (d=128: the same offset in the second 64-column chunk; d=64: unit u + 4), so
+// no shuffles are needed. (cos, sin) of the 8 pairs live in registers.
 template <int D>
-__device__ __forceinline__ void rotate_row(uint8_t* qs_base, int r, int lane, const float (&c)[D / 32], const float (&sn)[D / 32]) {
-  constexpr int E = D / 32;
-  const bool hi = lane >= 16;
-  const int e0 = lane * E;
-  const int chunk = e0 / 64, unit = (e0 % 64) / 8, within = (e0 % 8) * 2;
-  uint8_t* ptr = qs_base + chunk * TcSmem<D>::kChunkBytes + r * 128 + ((unit ^ (r & 7)) * 16) + within;
-  uint32_t qv[E / 2];
-  if constexpr (E == 4) {
-    const uint2 t = *reinterpret_cast<const uint2*>(ptr);
-    qv[0] = t.x;
-    qv[1] = t.y;
+__device__ __forceinline__ void rotate_step(uint8_t* qs_base, int r, int u, const float (&c)[8], const float (&sn)[8]) {
+  uint8_t* p0;
+  uint8_t* p1;
+  if constexpr (D == 128) {
+    p0 = qs_base + r * 128 + ((u ^ (r & 7)) * 16);
+    p1 = p0 + TcSmem<D>::kChunkBytes;
   } else {
-    qv[0] = *reinterpret_cast<const uint32_t*>(ptr);
+    p0 = qs_base + r * 128 + ((u ^ (r & 7)) * 16);
+    p1 = qs_base + r * 128 + (((u + 4) ^ (r & 7)) * 16);
   }
-  uint32_t out[E / 2];
+  const uint4 a = *reinterpret_cast<const uint4*>(p0);
+  const uint4 b = *reinterpret_cast<const uint4*>(p1);
+  const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+  uint32_t oa[4], ob[4];
 #pragma unroll
-  for (int e = 0; e < E / 2; ++e) {
-    const float x0 = __uint_as_float(qv[e] << 16), x1 = __uint_as_float(qv[e] & 0xFFFF0000u);
-    const float y0 = __shfl_xor_sync(0xffffffffu, x0, 16);
-    const float y1 = __shfl_xor_sync(0xffffffffu, x1, 16);
-    // first half: x cos - partner sin ; second half: x cos + partner sin
-    const float o0 = hi ? fmaf(y0, sn[2 * e], x0 * c[2 * e]) : fmaf(-y0, sn[2 * e], x0 * c[2 * e]);
-    const float o1 = hi ? fmaf(y1, sn[2 * e + 1], x1 * c[2 * e + 1]) : fmaf(-y1, sn[2 * e + 1], x1 * c[2 * e + 1]);
-    out[e] = pack_bf16x2(o0, o1);
+  for (int k = 0; k < 4; ++k) {
+    const float x0 = __uint_as_float(av[k] << 16), x1 = __uint_as_float(av[k] & 0xFFFF0000u);
+    const float y0 = __uint_as_float(bv[k] << 16), y1 = __uint_as_float(bv[k] & 0xFFFF0000u);
+    // first half: x cos - y sin ; second half: y cos + x sin
+    oa[k] = pack_bf16x2(fmaf(-y0, sn[2 * k], x0 * c[2 * k]), fmaf(-y1, sn[2 * k + 1], x1 * c[2 * k + 1]));
+    ob[k] = pack_bf16x2(fmaf(x0, sn[2 * k], y0 * c[2 * k]), fmaf(x1, sn[2 * k + 1], y1 * c[2 * k + 1]));
   }
-  if constexpr (E == 4) {
-    *reinterpret_cast<uint2*>(ptr) = make_uint2(out[0], out[1]);
-  } else {
-    *reinterpret_cast<uint32_t*>(ptr) = out[0];
+  *reinterpret_cast<uint4*>(p0) = make_uint4(oa[0], oa[1], oa[2], oa[3]);
+  *reinterpret_cast<uint4*>(p1) = make_uint4(ob[0], ob[1], ob[2], ob[3]);
+}
+
+__device__ __forceinline__ void load_cs8(const float2* rope, int64_t idx, float (&c)[8], float (&sn)[8]) {
+  const float4* t = reinterpret_cast<const float4*>(rope + idx);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float4 v = __ldg(t + e);
+    c[2 * e] = v.x;
+    sn[2 * e] = v.y;
+    c[2 * e + 1] = v.z;
+    sn[2 * e + 1] = v.w;
   }
 }
 
 template <int D>
 __device__ __forceinline__ void rotate_q_tile(uint8_t* qs_base, const float2* rope, int my_pos, int my_valid, int rot,
                                               int max_pos) {
-  constexpr int E = D / 32;
+  constexpr int kLanesPerRow = D / 16;       // 8 pairs per lane
+  constexpr int R = 32 / kLanesPerRow;       // rows per step
   const int lane = threadIdx.x & 31;
   const int wq = (threadIdx.x / 32) & 3;
-  const int pair0 = (lane & 15) * E;
+  const int g = lane / kLanesPerRow, u = lane % kLanesPerRow;
+  const int pair0 = u * 8;
   const int p_first = __shfl_sync(0xffffffffu, my_pos, 0);
   // rows of a tile normally have consecutive positions (a job's rows, a query's cross rows):
-  // then (cos, sin) of row r+1 = (cos, sin) of row r rotated by theta — 4 FMAs per pair per
-  // row (fp32, 31 steps: ~1e-6 drift vs bf16's 4e-3) instead of a table row per row.
+  // then (cos, sin) advance by R*theta per step — 4 FMAs per pair (fp32, <= 7 steps from a
+  // table value: ~1e-6 drift vs bf16's 4e-3) instead of a table row per row.
   const bool consecutive = __all_sync(0xffffffffu, !my_valid || my_pos == p_first + lane) && p_first - rot >= 0 &&
                            p_first - rot + 31 < max_pos;
-  float c[E], sn[E];
+  float c[8], sn[8];
   if (consecutive) {
-    float cd[E], sd[E];
-    const float4* cs = reinterpret_cast<const float4*>(rope + static_cast<int64_t>(p_first - rot) * (D / 2) + pair0);
-    const float4* cst = reinterpret_cast<const float4*>(rope + (D / 2) + pair0);  // position 1: (cos th, sin th)
+    float cd[8], sd[8];
+    load_cs8(rope, static_cast<int64_t>(p_first - rot + g) * (D / 2) + pair0, c, sn);
+    load_cs8(rope, static_cast<int64_t>(R) * (D / 2) + pair0, cd, sd);  // position R: (cos R th, sin R th)
 #pragma unroll
-    for (int e = 0; e < E / 2; ++e) {
-      const float4 v = __ldg(cs + e), dv = __ldg(cst + e);
-      c[2 * e] = v.x;
-      sn[2 * e] = v.y;
-      c[2 * e + 1] = v.z;
-      sn[2 * e + 1] = v.w;
-      cd[2 * e] = dv.x;
-      sd[2 * e] = dv.y;
-      cd[2 * e + 1] = dv.z;
-      sd[2 * e + 1] = dv.w;
-    }
-#pragma unroll 4
-    for (int rr = 0; rr < 32; ++rr) {
-      rotate_row<D>(qs_base, wq * 32 + rr, lane, c, sn);
+    for (int st = 0; st < 32 / R; ++st) {
+      rotate_step<D>(qs_base, wq * 32 + st * R + g, u, c, sn);
 #pragma unroll
-      for (int e = 0; e < E; ++e) {  // advance the angle by theta_i
+      for (int e = 0; e < 8; ++e) {
         const float cn = fmaf(c[e], cd[e], -sn[e] * sd[e]);
         sn[e] = fmaf(sn[e], cd[e], c[e] * sd[e]);
         c[e] = cn;
@@ -591,19 +622,11 @@ __device__ __forceinline__ void rotate_q_tile(uint8_t* qs_base, const float2* ro
     }
   } else {
 #pragma unroll 1
-    for (int rr = 0; rr < 32; ++rr) {
-      const int p = __shfl_sync(0xffffffffu, my_pos, rr);
+    for (int st = 0; st < 32 / R; ++st) {
+      const int p = __shfl_sync(0xffffffffu, my_pos, st * R + g);
       const int rp = min(max(p - rot, 0), max_pos - 1);
-      const float4* cs = reinterpret_cast<const float4*>(rope + static_cast<int64_t>(rp) * (D / 2) + pair0);
-#pragma unroll
-      for (int e = 0; e < E / 2; ++e) {
-        const float4 v = __ldg(cs + e);
-        c[2 * e] = v.x;
-        sn[2 * e] = v.y;
-        c[2 * e + 1] = v.z;
-        sn[2 * e + 1] = v.w;
-      }
-      rotate_row<D>(qs_base, wq * 32 + rr, lane, c, sn);
+      load_cs8(rope, static_cast<int64_t>(rp) * (D / 2) + pair0, c, sn);
+      rotate_step<D>(qs_base, wq * 32 + st * R + g, u, c, sn);
     }
   }
 }
@@ -618,7 +641,7 @@ __device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_
   uint32_t ep = 0;
   uint32_t tc = 0;
   uint32_t load_phase = 0;  // bit s: parity of the next q_load[s] completion
-  const bool tr = r == 0;
+  const bool tr = lane == 0;
   for (int ii = it_begin; ii < it_end; ++ii) {
     const Unit u = decode(P, a.cta_items[ii]);
     const WorkItem& w = u.w;
@@ -641,6 +664,7 @@ __device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_
           }
           mbar_wait(&S.q_load[sl], (load_phase >> sl) & 1);
           load_phase ^= 1u << sl;
+          if (tr) trace(P, 4, tc, 44 + x);  // 44/45: Q tile A/B loaded
           rotate_q_tile<D>(&S.q[sl][0][0], a.rope, my_pos, my_row < w.n_rows, rot, a.max_pos);
           fence_proxy_async_smem();
         }
@@ -658,10 +682,11 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
   TcSmem<D>& S = smem_ref<D>(smem_raw);
   const int warp = threadIdx.x / 32;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < TcSmem<D>::kKvSlots; ++i) {
-      mbar_init(&S.kv_full[i], 1);
-      mbar_init(&S.kv_empty[i], 1);
-    }
+    for (int kv = 0; kv < 2; ++kv)
+      for (int i = 0; i < TcSmem<D>::kKSlots; ++i) {
+        mbar_init(&S.kv_full[kv][i], 1);
+        mbar_init(&S.kv_empty[kv][i], P.paired ? 2 : 1);  // released by each head's issuer
+      }
     for (int i = 0; i < TcSmem<D>::kQSlots; ++i) {
       mbar_init(&S.q_full[i], 128);
       mbar_init(&S.q_empty[i], 1);
@@ -672,7 +697,8 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
         mbar_init(&S.s_full[i][b], 1);
         mbar_init(&S.p_full[i][b], 128);
       }
-      mbar_init(&S.o_done[i], 1);
+      mbar_init(&S.o_done[i][0], 1);
+      mbar_init(&S.o_done[i][1], 1);
     }
     fence_barrier_init();
   }
@@ -687,24 +713,34 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
   const int it_begin = P.a.cta_off[blockIdx.x], it_end = P.a.cta_off[blockIdx.x + 1];
-  // register budget 65536 = 128 x (56 + 136 + 136 + 168): TMA/MMA warps need few
+  if (P.a.dbg_trace != nullptr && threadIdx.x == 0) {  // profiling only: per-CTA start (ns)
+    uint64_t g;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+    P.a.dbg_trace[kTraceWarps * 2048 + 2 * blockIdx.x] = static_cast<long long>(g);
+  }
+  // register budget 65536 >= 128 x (56 + 160 + 160 + 120): TMA/MMA warps need few
   if (warp < 4) {
     reg_dealloc<56>();
-    if (warp == 0) {
-      if (elect_one()) run_producer<D>(P, S, it_begin, it_end);
-    } else if (warp == 1) {
-      if (elect_one()) run_mma<D>(P, S, tmem, it_begin, it_end);
+    if (warp == 0 || warp == 3) {
+      if (elect_one()) run_producer<D>(P, S, it_begin, it_end, warp == 0 ? 0 : 1);
+    } else {
+      if (elect_one()) run_mma<D>(P, S, tmem, it_begin, it_end, warp - 1);
     }
   } else if (warp < 12) {
-    reg_alloc<136>();
+    reg_alloc<160>();
     run_softmax<D, PM>(P, S, tmem, it_begin, it_end, warp < 8 ? 0 : 1);
   } else {
-    reg_alloc<168>();
+    reg_dealloc<120>();
     run_qprep<D>(P, S, it_begin, it_end);
   }
   if (warp >= 4 && warp < 12 && (threadIdx.x & 31) == 0) bulk_wait<0>();  // epilogue stores done
   tc_fence_before();
   __syncthreads();
+  if (P.a.dbg_trace != nullptr && threadIdx.x == 0) {  // profiling only: per-CTA end (ns)
+    uint64_t g;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+    P.a.dbg_trace[kTraceWarps * 2048 + 2 * blockIdx.x + 1] = static_cast<long long>(g);
+  }
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
@@ -732,6 +768,8 @@ cudaError_t launch_dp(const AttnArgs& a, cudaStream_t st) {
   p.poly_mask = PM;
   p.rescale_threshold = a.rescale_threshold;
   p.dbg_mode = getenv("SPANQ_DBG_MODE") ? atoi(getenv("SPANQ_DBG_MODE")) : 0;
+  p.epi_tma = getenv("SPANQ_EPI_TMA") ? atoi(getenv("SPANQ_EPI_TMA")) : 1;
+  p.pingpong = getenv("SPANQ_PINGPONG") ? atoi(getenv("SPANQ_PINGPONG")) : 0;
   span_attn_tc_kernel<D, PM><<<a.grid, kThreads, smem, st>>>(p);
   return cudaGetLastError();
 }

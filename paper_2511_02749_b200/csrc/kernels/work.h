@@ -35,8 +35,10 @@ struct WorkItem {
   int32_t pad0, pad1, pad2;
 };
 
+// Split-KV partials are per work unit: partial slot p holds the unit's heads, rows
+// ((p * n_heads + x) * kTileRows + r) of opart / lsepart (x = head - head0).
 struct CombineDesc {
-  int32_t row0, n_rows, part_base, n_split;
+  int32_t row0, n_rows, part_base, n_split, head0, n_heads;
 };
 
 }  // namespace spq

@@ -116,6 +116,9 @@ bool paired(const spq_ctx* c) {
   return c->cfg.dtype == SPQ_BF16 && (c->cfg.num_q_heads / c->cfg.num_kv_heads) % 2 == 0;
 }
 
+// heads per attention work unit (a split-KV partial slot holds one unit's heads)
+int heads_per_unit(const spq_ctx* c) { return paired(c) ? 2 : 1; }
+
 int poly_mask() {
   const char* e = std::getenv("SPANQ_POLY_EXP");  // tuning knob: quarters of exp2 on the FMA pipe
   return e ? std::max(0, std::min(3, std::atoi(e))) : 0;
@@ -146,7 +149,8 @@ spq_status make_tmap(spq_ctx* c, void* pool, CUtensorMap* out) {
   const uint64_t rows = static_cast<uint64_t>(g.num_layers) * g.num_blocks * g.num_kv_heads * g.block_size;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.head_dim), rows};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.head_dim) * 2};
-  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(g.block_size)};
+  // one box = 64 columns x min(bs, 64) rows: the attention kernel streams 64-key sub-tiles
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(std::min(g.block_size, 64))};
   cuuint32_t es[2] = {1, 1};
   CUresult r = reinterpret_cast<EncodeTiledFn>(fn)(
       out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, pool, dims, strides, box, es,
@@ -206,7 +210,7 @@ spq_status make_partmap(const spq_ctx* c, const float* opart, int64_t parts, CUt
   CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
   const spq_config& g = c->cfg;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.head_dim),
-                        static_cast<cuuint64_t>(parts) * g.num_q_heads * spq::kTileRows};
+                        static_cast<cuuint64_t>(parts) * heads_per_unit(c) * spq::kTileRows};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.head_dim) * 4};
   cuuint32_t box[2] = {32, 32};
   cuuint32_t es[2] = {1, 1};
@@ -526,6 +530,23 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
   lap("prefill work");
   spq::build_join_work(H, o, 0, H.n_queries, &p->jw_host);
   lap("join work");
+  if (prof) {
+    for (const spq::AttnWorkHost* wh : {&p->pw_host, &p->jw_host}) {
+      int64_t mn = INT64_MAX, mx = 0;
+      for (int32_t cta = 0; cta < wh->grid; ++cta) {
+        int64_t subs = 0;
+        for (int32_t i = wh->cta_off[cta]; i < wh->cta_off[cta + 1]; ++i) {
+          const spq::WorkItem& it = wh->items[wh->cta_items[i] / o.units];
+          for (int32_t t = it.tile_begin; t < it.tile_end; ++t) subs += wh->tiles[t].n_valid > 64 ? 2 : 1;
+        }
+        mn = std::min(mn, subs);
+        mx = std::max(mx, subs);
+      }
+      std::fprintf(stderr, "[spanq]   work: items %zu codes %zu grid %d parts %d combine %zu sub-tiles/CTA min %ld max %ld\n",
+                   wh->items.size(), wh->cta_items.size(), wh->grid, wh->n_parts, wh->combine.size(),
+                   static_cast<long>(mn), static_cast<long>(mx));
+    }
+  }
   p->prefill_flops = p->pw_host.flops;
   p->join_flops = p->jw_host.flops;
   // algorithmic bytes of rope_kv_write: per written row, read k,v and write both pages
@@ -575,7 +596,7 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
     CUDA_TRY(cudaMemcpyAsync(p->dbuf, c->staging, pk.host.size(), cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaEventRecord(c->staging_ev, st));
     if (p->jw.n_parts > 0) {
-      const size_t rows = static_cast<size_t>(p->jw.n_parts) * c->cfg.num_q_heads * spq::kTileRows;
+      const size_t rows = static_cast<size_t>(p->jw.n_parts) * heads_per_unit(c) * spq::kTileRows;
       CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->opart), rows * c->cfg.head_dim * sizeof(float), st));
       CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->lsepart), rows * sizeof(float), st));
     }
@@ -765,6 +786,7 @@ spq_status spq_join(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b
     ca.o = o;
     ca.lse = lse;
     ca.hq = c->cfg.num_q_heads;
+    ca.heads_per_desc = heads_per_unit(c);
     ca.d = c->cfg.head_dim;
     ca.out_fp32 = c->cfg.out_dtype == SPQ_FP32;
     cudaError_t e = spq::launch_combine(ca, st);

@@ -40,7 +40,27 @@ __global__ void __launch_bounds__(128, 1) rate(int mode, int iters, long long* o
   constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false);
   constexpr uint32_t idO = idesc_bf16_f32(128, 128, false, true);
   long long t0 = clock64();
-  if (mode < 3) {
+  if (mode >= 4) {
+    // one span_attn period: S_A, S_B (M128 N64 K128 SS: 8 instr each), PV_A, PV_B (M128 N128 K64 TS)
+    constexpr uint32_t idS64 = idesc_bf16_f32(128, 64, false, false);
+    if (t == 0) {
+      for (int it = 0; it < iters; ++it) {
+        for (int x = 0; x < 2; ++x)
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t off = (kk / 4) * 16384 + (kk % 4) * 32;
+            if (mode == 4 || mode == 5)
+              mma_ss(tm + 64 * x, desc_sw128(smem_u32(s.a) + off, 16, 1024),
+                     desc_sw128(smem_u32(s.b) + (kk / 4) * 8192 + (kk % 4) * 32, 16, 1024), idS64, 1u);
+          }
+        for (int x = 0; x < 2; ++x)
+          for (int kk = 0; kk < 4; ++kk)
+            if (mode == 4 || mode == 6)
+              mma_ts(tm + 256 + 128 * x, tm + 128 + kk * 8, desc_sw128(smem_u32(s.b) + kk * 2048, 8192, 1024), idO, 1u);
+      }
+      mma_commit(&s.bar);
+      mbar_wait(&s.bar, 0);
+    }
+  } else if (mode < 3) {
     if (t == 0) {
       for (int it = 0; it < iters; ++it) {
         for (int kk = 0; kk < 8; ++kk) {
@@ -83,8 +103,9 @@ int main() {
   const int smem = sizeof(Sm) + 1024;
   cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const char* names[] = {"SS S=QK^T (8 x 128x128x16)", "TS O+=PV (8 x 128x128x16, B MN-major)", "SS+TS interleaved",
-                         "commit->wait->arrive->wait round trip"};
-  for (int mode = 0; mode < 4; ++mode) {
+                         "commit->wait->arrive->wait round trip", "period: 2x(8 SS N64) + 2x(4 TS N128)",
+                         "period SS part only (16 SS N64)", "period TS part only (8 TS N128)"};
+  for (int mode = 0; mode < 7; ++mode) {
     const int iters = mode == 3 ? 1000 : 2000;
     for (int grid : {1, 148}) {
       rate<<<grid, 128, smem>>>(mode, iters, d);
@@ -94,7 +115,11 @@ int main() {
       double mx = 0;
       for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
       const double per = mx / iters;
-      if (mode < 3) {
+      if (mode >= 4) {
+        const double flops = (mode == 4 ? 2.0 : 1.0) * 16 * 2.0 * 128 * 64 * 16 * (mode == 6 ? 1 : 1);
+        printf("%-40s grid %3d: %8.1f cycles per period, %6.0f flop/cycle/SM (%.0f%% of 8192)\n", names[mode], grid, per,
+               flops / per, 100.0 * flops / per / 8192);
+      } else if (mode < 3) {
         const double flops = (mode == 2 ? 2 : 1) * 8.0 * 2 * 128 * 128 * 16;
         printf("%-40s grid %3d: %8.1f cycles per 8-MMA group, %6.0f flop/cycle/SM (%.0f%% of 8192)\n", names[mode], grid,
                per, flops / per, 100.0 * flops / per / 8192);

@@ -18,28 +18,49 @@ tabs = [runner.device_tables(w.shape, 0, w.seed, dev)]
 for _ in range(2):
     ctx.evict_all()
     runner.run_pass(ctx, w.queries, tabs, dev, release=True)
-buf = torch.zeros(5 * 1024 * 2, dtype=torch.int64, device=dev)
-os.environ["SPANQ_TRACE"] = str(buf.data_ptr())
+NW = 16
+buf = torch.zeros(NW * 1024 * 2 + 2 * 1024, dtype=torch.int64, device=dev)
+which = sys.argv[2] if len(sys.argv) > 2 else "prefill"
 ctx.evict_all()
 plan = ctx.plan(w.queries)
 view = plan.view()
 ptok = runner.prefill_tokens(view, w.queries)
 q, k, v = runner.gather(tabs[0], ptok, dev)
 o = torch.empty((len(ptok), 32, 128), dtype=torch.float32, device=dev)
+if which == "prefill":
+    os.environ["SPANQ_TRACE"] = str(buf.data_ptr())
 plan.prefill(0, q, k, v, o)
+if which == "join":
+    jtok = runner.join_tokens(view, w.queries)
+    qj, kj, vj = runner.gather(tabs[0], jtok, dev)
+    oj = torch.empty((len(jtok), 32, 128), dtype=torch.float32, device=dev)
+    os.environ["SPANQ_TRACE"] = str(buf.data_ptr())
+    plan.join(0, qj, kj, vj, oj)
 torch.cuda.synchronize()
 del os.environ["SPANQ_TRACE"]
-t = buf.view(5, 1024, 2).cpu().numpy()
-names = {10: "K issue", 11: "V issue", 20: "P_A rdy", 21: "Q rdy", 22: "S_A issue", 23: "P_B rdy", 24: "drain P_A",
-         30: "S rdy", 31: "P done", 32: "O rdy", 33: "epi done", 40: "slotA free", 41: "slotB free", 42: "QA done",
-         43: "QB done", 34: "max done", 35: "exp start"}
-roles = ["tma", "mma", "smxA", "smxB", "qprep"]
-t0 = min(t[r][0][1] for r in range(5) if t[r][0][1] > 0)
+allb = buf.cpu().numpy()
+t = allb[:NW * 2048].reshape(NW, 1024, 2)
+spans = allb[NW * 2048:].reshape(-1, 2)
+spans = spans[spans[:, 0] > 0]
+g0 = spans[:, 0].min()
+st, en = (spans[:, 0] - g0) / 1e3, (spans[:, 1] - g0) / 1e3
+busy = en - st
+print(f"# CTAs {len(spans)}: start max {st.max():.1f} us; end min/p50/max {en.min():.1f}/{np.median(en):.1f}/{en.max():.1f} us;"
+      f" busy min/p50/max {busy.min():.1f}/{np.median(busy):.1f}/{busy.max():.1f} us")
+order = np.argsort(en)
+print("# slowest CTAs:", [(int(i), round(float(en[i]), 1)) for i in order[-6:]])
+print("# fastest CTAs:", [(int(i), round(float(en[i]), 1)) for i in order[:6]])
+names = {10: "K issue", 11: "V issue", 20: "P_A rdy", 21: "Q rdy", 22: "K rdy", 23: "P_B rdy", 24: "V rdy",
+         30: "S rdy", 31: "P done", 32: "O rdy", 33: "epi done", 36: "stg free", 37: "stg stored", 40: "slotA free", 41: "slotB free", 42: "QA done",
+         43: "QB done", 44: "QA loaded", 45: "QB loaded", 34: "max done", 35: "exp start"}
+roles = ["tma", "mma", "w2", "w3", "smxA0", "smxA1", "smxA2", "smxA3", "smxB0", "smxB1", "smxB2", "smxB3",
+         "qp0", "qp1", "qp2", "qp3"]
+t0 = min(t[r][0][1] for r in range(NW) if t[r][0][1] > 0)
 ev = []
-for r in range(5):
+for r in range(NW):
     for e, c in t[r]:
         if c > 0:
             ev.append((c - t0, roles[r], names.get(int(e), str(e))))
 ev.sort()
-for c, r, n in ev[:700]:
+for c, r, n in ev[:3000]:
     print(f"{c:9d} {r:6s} {n}")
