@@ -3,6 +3,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 namespace spq {
 namespace {
@@ -27,32 +29,46 @@ int32_t add_tiles(const PlanHost& p, const Segment& s, int bs, int32_t key_base,
   return first;
 }
 
-// Static schedule of (item, head) pairs over `grid` persistent CTAs: pairs sorted by cost
-// (longest first, heads of one item adjacent so a KV head's tiles are reused from L2), dealt in
-// boustrophedon waves (0..grid-1, grid-1..0, ...) — O(pairs), close to LPT for sorted costs.
-void schedule(const std::vector<double>& item_cost, int hq, int num_sms, AttnWorkHost* w) {
+// Schedule of (item, unit) codes over `grid` persistent CTAs: codes sorted by cost, longest
+// first (units of one item adjacent, so a KV head's tiles are reused from L2), claimed at run time
+// by the CTAs with an atomic counter — a CTA takes the next code when it needs one, so the
+// makespan adapts to the real per-item cost (LPT list scheduling, no cost model in the loop).
+void schedule(const std::vector<double>& item_cost, int units, int num_sms, AttnWorkHost* w) {
   std::vector<int32_t> order(item_cost.size());
   for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int32_t>(i);
   std::stable_sort(order.begin(), order.end(),
                    [&](int32_t a, int32_t b) { return item_cost[a] > item_cost[b]; });
-  const size_t pairs = item_cost.size() * static_cast<size_t>(hq);
-  const int grid = static_cast<int>(std::min<size_t>(num_sms, std::max<size_t>(1, pairs)));
-  std::vector<int32_t> count(grid, 0);
-  std::vector<int32_t> bin_of(pairs);
-  for (size_t i = 0; i < pairs; ++i) {
-    const size_t wave = i / grid, pos = i % grid;
-    const int b = static_cast<int>((wave & 1) ? grid - 1 - pos : pos);
-    bin_of[i] = b;
-    count[b]++;
+  const size_t codes = item_cost.size() * static_cast<size_t>(units);
+  w->grid = static_cast<int>(std::min<size_t>(num_sms, std::max<size_t>(1, codes)));
+  static const bool static_sched = [] {
+    const char* e = std::getenv("SPANQ_SCHED");  // tuning knob: "static" = host snake lists
+    return e != nullptr && std::string(e) == "static";
+  }();
+  if (static_sched) {
+    // boustrophedon waves (0..grid-1, grid-1..0, ...) over the sorted codes
+    const int grid = w->grid;
+    std::vector<int32_t> count(grid, 0), bin_of(codes);
+    for (size_t i = 0; i < codes; ++i) {
+      const size_t wave = i / grid, pos = i % grid;
+      bin_of[i] = static_cast<int32_t>((wave & 1) ? grid - 1 - pos : pos);
+      count[bin_of[i]]++;
+    }
+    w->dynamic = false;
+    w->cta_off.assign(grid + 1, 0);
+    for (int c = 0; c < grid; ++c) w->cta_off[c + 1] = w->cta_off[c] + count[c];
+    w->cta_items.assign(codes, 0);
+    std::vector<int32_t> fill(w->cta_off.begin(), w->cta_off.end() - 1);
+    size_t i = 0;
+    for (int32_t it : order)
+      for (int u = 0; u < units; ++u, ++i) w->cta_items[fill[bin_of[i]]++] = it * units + u;
+    return;
   }
-  w->grid = grid;
-  w->cta_off.assign(grid + 1, 0);
-  for (int c = 0; c < grid; ++c) w->cta_off[c + 1] = w->cta_off[c] + count[c];
-  w->cta_items.assign(pairs, 0);
-  std::vector<int32_t> fill(w->cta_off.begin(), w->cta_off.end() - 1);
-  size_t i = 0;
+  w->dynamic = true;
+  w->cta_off.assign({0, static_cast<int32_t>(codes)});
+  w->cta_items.clear();
+  w->cta_items.reserve(codes);
   for (int32_t it : order)
-    for (int h = 0; h < hq; ++h, ++i) w->cta_items[fill[bin_of[i]]++] = it * hq + h;
+    for (int u = 0; u < units; ++u) w->cta_items.push_back(it * units + u);
 }
 
 constexpr double kItemOverhead = 1.0;   // q-prep + epilogue, in KV-tile units

@@ -12,8 +12,10 @@ struct AttnWorkHost {
   std::vector<KvTile> tiles;
   std::vector<int32_t> tile_blocks;
   std::vector<WorkItem> items;
-  std::vector<int32_t> cta_off;    // [grid+1]
-  std::vector<int32_t> cta_items;  // item * units + unit, per CTA in execution order
+  std::vector<int32_t> cta_off;    // [grid+1] static schedule (unused when dynamic)
+  std::vector<int32_t> cta_items;  // item * units + unit: per CTA in execution order (static), or
+                                   // one global list in claim order (dynamic)
+  bool dynamic = false;            // CTAs claim codes from cta_items with an atomic counter
   std::vector<CombineDesc> combine;
   int32_t n_parts = 0;
   int32_t grid = 0;

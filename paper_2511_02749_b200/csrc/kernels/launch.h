@@ -33,9 +33,11 @@ struct AttnArgs {
   const int32_t* tile_blocks;
   const WorkItem* items;
   int32_t n_items;
-  const int32_t* cta_off;  // persistent schedule (tcgen05 kernel)
+  const int32_t* cta_off;  // persistent schedule (tcgen05 kernel): static per-CTA lists, or
   const int32_t* cta_items;
   int32_t grid;
+  int32_t* sched;          // dynamic: {next, done} claim counters (zero between launches), or null
+  int32_t n_codes;         // dynamic: codes in cta_items
   // rows
   const int32_t* pos;  // [rows] position of each query row
   const void* q;       // [rows][hq][d]

@@ -67,6 +67,9 @@ struct TcSmem {
   uint64_t kv_full[2][kKSlots], kv_empty[2][kKSlots];  // [K, V][slot] (V uses the first kVSlots)
   uint64_t q_full[3], q_empty[3], q_load[3];
   uint64_t s_full[2][2], p_full[2][2], o_done[2][2];  // [head][S buffer / PV parity j & 1]
+  static constexpr int kSched = 4;  // dynamic schedule: ring of claimed codes
+  uint64_t sched_full[kSched], sched_empty[kSched];
+  int32_t sched_code[kSched];
   uint32_t tmem_base;
 };
 
@@ -81,8 +84,6 @@ struct TcParams {
   int paired;     // 1: a unit is a GQA head pair (A = 2u, B = 2u+1); 0: one head (B idle)
   int poly_mask;  // pair i of a 32-key chunk uses the FMA-pipe exp2 when (i & 3) < poly_mask
   float rescale_threshold;  // log2 units; O is rescaled when the running max grows by more
-  int pingpong;  // 1: the two softmax warpgroups alternate (named barriers 1, 2)
-  int epi_tma;   // epilogue stores: 1 = TMA bulk stores of 32x32 staging tiles, 0 = coalesced st.global
   int dbg_mode;  // profiling only: 1 = softmax does no math, 2 = max pass only,
                  // 3 = 1 + K/V always from the first block (L2-resident), 4 = 1 + MMA skips K/V waits,
                  // 5 = 1 + Q prep does no work
@@ -118,6 +119,40 @@ __device__ __forceinline__ Unit decode(const TcParams& P, int code) {
   u.n_heads = P.paired ? 2 : 1;
   return u;
 }
+
+// The CTA's sequence of work codes. Static: its slice of cta_items. Dynamic: the K producer
+// claims codes from the launch's counter (atomicAdd) and hands them to the other roles through a
+// smem ring; every role sees the same sequence, ending with -1.
+constexpr int kSchedConsumers = 1 + 2 + 256 + 128;  // V producer, 2 MMA issuers, softmax, Q prep
+template <int D>
+struct ItemSrc {
+  const TcParams& P;
+  TcSmem<D>& S;
+  int it, end;
+  bool claimer;
+  uint32_t k = 0;
+  __device__ ItemSrc(const TcParams& p, TcSmem<D>& s, int b, int e, bool c) : P(p), S(s), it(b), end(e), claimer(c) {}
+  __device__ int next() {
+    if (P.a.sched == nullptr) return it < end ? P.a.cta_items[it++] : -1;
+    constexpr int R = TcSmem<D>::kSched;
+    const int slot = k % R;
+    const uint32_t par = (k / R) & 1;
+    ++k;
+    int code;
+    if (claimer) {
+      mbar_wait(&S.sched_empty[slot], par ^ 1);
+      const int idx = atomicAdd(P.a.sched, 1);
+      code = idx < P.a.n_codes ? P.a.cta_items[idx] : -1;
+      *reinterpret_cast<volatile int32_t*>(&S.sched_code[slot]) = code;
+      mbar_arrive(&S.sched_full[slot]);
+    } else {
+      mbar_wait(&S.sched_full[slot], par);
+      code = *reinterpret_cast<volatile int32_t*>(&S.sched_code[slot]);
+      mbar_arrive(&S.sched_empty[slot]);
+    }
+    return code;
+  }
+};
 
 // exp2 on the FMA pipe: x = n + f, n = rint(x) via the 1.5*2^23 trick, 2^f by a degree-3
 // polynomial on [-0.5, 0.5] (max rel. error 1.0e-4), exponent added in the integer domain.
@@ -160,8 +195,9 @@ __device__ void run_producer(const TcParams& P, TcSmem<D>& S, int it_begin, int 
   const CUtensorMap* map = kv == 0 ? &P.tmk : &P.tmv;
   uint32_t n = 0;
   uint32_t tc = 0;
-  for (int ii = it_begin; ii < it_end; ++ii) {
-    const Unit u = decode(P, a.cta_items[ii]);
+  ItemSrc<D> src(P, S, it_begin, it_end, kv == 0);
+  for (int code; (code = src.next()) >= 0;) {
+    const Unit u = decode(P, code);
     const int kvh = u.head_a / group;
     for (int t = u.w.tile_begin; t < u.w.tile_end; ++t) {
       const KvTile tl = a.tiles[t];
@@ -213,8 +249,9 @@ __device__ void run_mma(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_b
     mbar_wait(&S.kv_full[kv][n % ns], (n / ns) & 1);
     tc_fence_after();
   };
-  for (int ii = it_begin; ii < it_end; ++ii) {
-    const Unit u = decode(P, a.cta_items[ii]);
+  ItemSrc<D> src(P, S, it_begin, it_end, false);
+  for (int code; (code = src.next()) >= 0;) {
+    const Unit u = decode(P, code);
     if (x >= u.n_heads) continue;  // unpaired launch: the B issuer idles
     const bool two = u.n_heads == 2;
     const int tb = u.w.tile_begin, te = u.w.tile_end;
@@ -384,13 +421,13 @@ __device__ __forceinline__ void epilogue(const TcParams& P, TcSmem<D>& S, uint32
   // read); a slice that ends inside this item's rows is written directly (the next rows belong
   // to another item)
   const bool in_range = wr * 32 < w.n_rows;
-  const bool use_tma = P.epi_tma && in_range && (w.part >= 0 || (a.out_fp32 && wr * 32 + 32 <= w.n_rows));
+  const bool use_tma = in_range && (w.part >= 0 || (a.out_fp32 && wr * 32 + 32 <= w.n_rows));
   const bool direct = in_range && !use_tma;
 #pragma unroll
   for (int c = 0; c < D / 32; ++c) {
     if (c + 1 < D / 32) tmem_ld32(ocol + (c + 1) * 32, vv[(c + 1) & 1]);
     const uint32_t(&v)[32] = vv[c & 1];
-    if (use_tma && lane == 0) bulk_wait_read<0>();  // previous chunk's store has read the buffer
+    if (lane == 0) bulk_wait_read<0>();  // previous chunk's store has read the buffer
     __syncwarp();
 #pragma unroll
     for (int uu = 0; uu < 8; ++uu)
@@ -418,10 +455,7 @@ __device__ __forceinline__ void epilogue(const TcParams& P, TcSmem<D>& S, uint32
         const float4 val = *reinterpret_cast<const float4*>(stg + rr * 32 + ((uu ^ (rr & 7)) * 4));
         const int trow = wr * 32 + rr;
         const int col = c * 32 + uu * 4;
-        if (w.part >= 0) {
-          *reinterpret_cast<float4*>(a.opart + (static_cast<int64_t>(w.part * f.n_heads + x) * kTileRows + trow) * D +
-                                     col) = val;
-        } else if (trow < w.n_rows) {
+        if (trow < w.n_rows) {
           if (a.out_fp32) {
             *reinterpret_cast<float4*>(static_cast<float*>(a.o) +
                                        ((w.row0 + trow) * static_cast<int64_t>(a.hq) + f.h) * D + col) = val;
@@ -456,11 +490,11 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
   const float sl2 = P.scale_log2;
   const uint32_t ocol = tmem + lane_base + kColO + 128 * x;
   uint32_t js = 0;  // sub-tiles processed (global; == the MMA warps' PV index)
-  bool js_started = false;  // ping-pong: A waits for B's previous step from its second step on
   uint32_t tc = 0;
   const bool tr = (threadIdx.x & 31) == 0;
-  for (int ii = it_begin; ii < it_end; ++ii) {
-    const Unit u = decode(P, a.cta_items[ii]);
+  ItemSrc<D> src(P, S, it_begin, it_end, false);
+  for (int code; (code = src.next()) >= 0;) {
+    const Unit u = decode(P, code);
     if (x >= u.n_heads) continue;  // single-head unit: WG B idles
     const WorkItem& w = u.w;
     const bool valid = r < w.n_rows;
@@ -490,15 +524,8 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
           sum = 1.f;
           m = 0.f;
         } else {
-          // ping-pong (paired units): the two heads' softmax steps alternate on the SMSPs' MUFU
-          // (A(j), B(j), A(j+1), ...); barrier 1: "A finished step j", 2: "B finished step j"
-          const bool pp = P.pingpong && u.n_heads == 2;
-          if (pp && x == 1) named_sync(1, 256);
-          if (pp && x == 0 && js_started) named_sync(2, 256);
           sum = full ? softmax_sub<PM, false>(scol, sl2, P.rescale_threshold, lim, m, alpha, resc)
                      : softmax_sub<PM, true>(scol, sl2, P.rescale_threshold, lim, m, alpha, resc);
-          if (pp) named_arrive(x == 0 ? 1 : 2, 256);
-          js_started = true;
         }
         l = l * alpha + sum;
         // O is only touched when a row's running max moved (rare with the threshold): then PV of
@@ -536,8 +563,6 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
     epilogue<D>(P, S, ocol, x, f, tc, tr);
   }
   tc_fence_before();
-  // consume B's last ping-pong arrival so no named barrier is left mid-phase
-  if (P.pingpong && P.paired && x == 0 && js_started) named_sync(2, 256);
 }
 
 // ------------------------------------------------------------------ warps 12-15: Q prep
@@ -642,8 +667,9 @@ __device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_
   uint32_t tc = 0;
   uint32_t load_phase = 0;  // bit s: parity of the next q_load[s] completion
   const bool tr = lane == 0;
-  for (int ii = it_begin; ii < it_end; ++ii) {
-    const Unit u = decode(P, a.cta_items[ii]);
+  ItemSrc<D> src(P, S, it_begin, it_end, false);
+  for (int code; (code = src.next()) >= 0;) {
+    const Unit u = decode(P, code);
     const WorkItem& w = u.w;
     const int my_row = wq * 32 + lane;  // this lane's row position, shuffled to the warp per row
     const int my_pos = my_row < w.n_rows ? a.pos[static_cast<int64_t>(w.row0) + my_row] : 0;
@@ -698,6 +724,10 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
         mbar_init(&S.p_full[i][b], 128);
       }
       mbar_init(&S.o_done[i][0], 1);
+      mbar_init(&S.sched_full[2 * i], 1);
+      mbar_init(&S.sched_full[2 * i + 1], 1);
+      mbar_init(&S.sched_empty[2 * i], kSchedConsumers);
+      mbar_init(&S.sched_empty[2 * i + 1], kSchedConsumers);
       mbar_init(&S.o_done[i][1], 1);
     }
     fence_barrier_init();
@@ -712,7 +742,8 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
-  const int it_begin = P.a.cta_off[blockIdx.x], it_end = P.a.cta_off[blockIdx.x + 1];
+  const bool dyn = P.a.sched != nullptr;
+  const int it_begin = dyn ? 0 : P.a.cta_off[blockIdx.x], it_end = dyn ? 0 : P.a.cta_off[blockIdx.x + 1];
   if (P.a.dbg_trace != nullptr && threadIdx.x == 0) {  // profiling only: per-CTA start (ns)
     uint64_t g;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
@@ -736,6 +767,16 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
   if (warp >= 4 && warp < 12 && (threadIdx.x & 31) == 0) bulk_wait<0>();  // epilogue stores done
   tc_fence_before();
   __syncthreads();
+  if (P.a.sched != nullptr && threadIdx.x == 0) {
+    // the last CTA to finish (all claims of all CTAs are done) resets the counters for the next
+    // launch of this work list
+    __threadfence();
+    if (atomicAdd(P.a.sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+      P.a.sched[0] = 0;
+      P.a.sched[1] = 0;
+      __threadfence();
+    }
+  }
   if (P.a.dbg_trace != nullptr && threadIdx.x == 0) {  // profiling only: per-CTA end (ns)
     uint64_t g;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
@@ -768,8 +809,6 @@ cudaError_t launch_dp(const AttnArgs& a, cudaStream_t st) {
   p.poly_mask = PM;
   p.rescale_threshold = a.rescale_threshold;
   p.dbg_mode = getenv("SPANQ_DBG_MODE") ? atoi(getenv("SPANQ_DBG_MODE")) : 0;
-  p.epi_tma = getenv("SPANQ_EPI_TMA") ? atoi(getenv("SPANQ_EPI_TMA")) : 1;
-  p.pingpong = getenv("SPANQ_PINGPONG") ? atoi(getenv("SPANQ_PINGPONG")) : 0;
   span_attn_tc_kernel<D, PM><<<a.grid, kThreads, smem, st>>>(p);
   return cudaGetLastError();
 }

@@ -61,8 +61,9 @@ struct Packer {
 };
 
 struct DevWork {  // offsets of one attention work list inside a plan buffer
-  size_t tiles, tile_blocks, items, cta_off, cta_items, combine;
-  int32_t n_items = 0, grid = 0, n_combine = 0, n_parts = 0;
+  size_t tiles, tile_blocks, items, cta_off, cta_items, combine, sched;
+  int32_t n_items = 0, grid = 0, n_combine = 0, n_parts = 0, n_codes = 0;
+  bool dynamic = false;
   double flops = 0;
 };
 
@@ -248,6 +249,8 @@ void fill_attn(spq_ctx* c, const spq_plan* p, const DevWork& w, spq::AttnArgs* a
   a->n_items = w.n_items;
   a->cta_off = at<int32_t>(p, w.cta_off);
   a->cta_items = at<int32_t>(p, w.cta_items);
+  a->sched = w.dynamic ? at<int32_t>(p, w.sched) : nullptr;
+  a->n_codes = w.n_codes;
   a->grid = w.grid;
   a->k_pool = c->cfg.k_pool;
   a->v_pool = c->cfg.v_pool;
@@ -329,6 +332,9 @@ spq_status upload_work(spq_ctx* c, const spq::AttnWorkHost& h, cudaStream_t st, 
   tw->w.items = pk.add(h.items);
   tw->w.cta_off = pk.add(h.cta_off);
   tw->w.cta_items = pk.add(h.cta_items);
+  tw->w.sched = pk.add(std::vector<int32_t>{0, 0});  // claim counters (self-resetting)
+  tw->w.dynamic = h.dynamic;
+  tw->w.n_codes = static_cast<int32_t>(h.cta_items.size());
   tw->w.combine = pk.add(h.combine);
   tw->w.n_items = static_cast<int32_t>(h.items.size());
   tw->w.grid = h.grid;
@@ -532,8 +538,17 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
   lap("join work");
   if (prof) {
     for (const spq::AttnWorkHost* wh : {&p->pw_host, &p->jw_host}) {
-      int64_t mn = INT64_MAX, mx = 0;
+      if (wh->dynamic) {
+        std::fprintf(stderr, "[spanq]   work: items %zu codes %zu grid %d (dynamic claims)\n", wh->items.size(),
+                     wh->cta_items.size(), wh->grid);
+        continue;
+      }
+      int64_t mn = INT64_MAX, mx = 0, imn = INT64_MAX, imx = 0;
+      double cmx = 0, cmn = 1e30;
       for (int32_t cta = 0; cta < wh->grid; ++cta) {
+        const int64_t ni = wh->cta_off[cta + 1] - wh->cta_off[cta];
+        imn = std::min(imn, ni);
+        imx = std::max(imx, ni);
         int64_t subs = 0;
         for (int32_t i = wh->cta_off[cta]; i < wh->cta_off[cta + 1]; ++i) {
           const spq::WorkItem& it = wh->items[wh->cta_items[i] / o.units];
@@ -541,7 +556,12 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
         }
         mn = std::min(mn, subs);
         mx = std::max(mx, subs);
+        const double cost = static_cast<double>(subs) + 3.5 * static_cast<double>(ni);
+        cmx = std::max(cmx, cost);
+        cmn = std::min(cmn, cost);
       }
+      std::fprintf(stderr, "[spanq]   work: items/CTA min %ld max %ld; cost (sub-tiles + 3.5/item) min %.1f max %.1f\n",
+                   static_cast<long>(imn), static_cast<long>(imx), cmn, cmx);
       std::fprintf(stderr, "[spanq]   work: items %zu codes %zu grid %d parts %d combine %zu sub-tiles/CTA min %ld max %ld\n",
                    wh->items.size(), wh->cta_items.size(), wh->grid, wh->n_parts, wh->combine.size(),
                    static_cast<long>(mn), static_cast<long>(mx));
@@ -572,6 +592,9 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
       w->items = pk.add(h.items);
       w->cta_off = pk.add(h.cta_off);
       w->cta_items = pk.add(h.cta_items);
+      w->sched = pk.add(std::vector<int32_t>{0, 0});  // claim counters (self-resetting)
+      w->dynamic = h.dynamic;
+      w->n_codes = static_cast<int32_t>(h.cta_items.size());
       w->combine = pk.add(h.combine);
       w->n_items = static_cast<int32_t>(h.items.size());
       w->grid = h.grid;

@@ -50,6 +50,7 @@ print(f"# CTAs {len(spans)}: start max {st.max():.1f} us; end min/p50/max {en.mi
 order = np.argsort(en)
 print("# slowest CTAs:", [(int(i), round(float(en[i]), 1)) for i in order[-6:]])
 print("# fastest CTAs:", [(int(i), round(float(en[i]), 1)) for i in order[:6]])
+print("# end_us_by_cta:", " ".join(f"{float(e):.0f}" for e in en))
 names = {10: "K issue", 11: "V issue", 20: "P_A rdy", 21: "Q rdy", 22: "K rdy", 23: "P_B rdy", 24: "V rdy",
          30: "S rdy", 31: "P done", 32: "O rdy", 33: "epi done", 36: "stg free", 37: "stg stored", 40: "slotA free", 41: "slotB free", 42: "QA done",
          43: "QB done", 44: "QA loaded", 45: "QB loaded", 34: "max done", 35: "exp start"}
