@@ -142,6 +142,15 @@ def cpu_baseline(budget_s: float = 15.0):
                       f"{dt:.1f} s on {os.cpu_count()} host cpus"}
 
 
+def c2_config(layers: int, world: int, out_dtype: str = "fp32", block_size: int = 64):
+    return {"workload": "C2 RAG span query (configs[1]): P512 + 16x1024 plus-fragments + 256 cross, cold cache",
+            "model": f"8B GQA attention shape Hq32/Hkv8/d128, {layers} layers (same synthetic q/k/v per layer, "
+                     "own KV-pool layer each), random tables",
+            "layers": layers, "global_batch": world, "seq_len": 17152, "block_size": block_size,
+            "out_dtype": out_dtype, "parallelism": f"dp{world} (independent queries per rank)",
+            "l2": "flushed between steps (256 MB write)"}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -156,8 +165,7 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2 RAG span query (configs[1]) bounded CPU sample",
-                       "global_batch": 1, "seq_len": 17152, "parallelism": "cpu oracle"},
+            "config": c2_config(args.layers, world, args.out_dtype),
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -170,17 +178,24 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="spanq", choices=["spanq", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--layers", type=int, default=40,
-                    help="attention layers per step (40 = the 8B model's depth; 1 = a single layer)")
+    ap.add_argument("--layers", type=int, default=None,
+                    help="attention layers per step (c2 default 40 = the 8B model's depth; c5 default 1)")
     ap.add_argument("--out-dtype", default="fp32", choices=["fp32", "bf16"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
+                    help="c2: one RAG query per rank (weak scaling, default); c5: one shared batch "
+                         "partitioned over the ranks with the NCCL fragment-KV exchange (strong scaling)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.layers is None:
+        args.layers = 40 if args.workload == "c2" else 1
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.workload == "c5":
+        return main_c5(args, rank, world, local)
 
     import torch
 
@@ -299,14 +314,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "C2 RAG span query (configs[1]): P512 + 16x1024 plus-fragments + 256 cross, cold cache",
-                   "model": f"8B GQA attention shape Hq32/Hkv8/d128, {L} layers (same synthetic q/k/v per layer, "
-                            "own KV-pool layer each), random tables",
-                   "layers": L,
-                   "global_batch": world, "seq_len": int(view["prefill_flops"] > 0) and 17152,
-                   "block_size": s.block_size, "out_dtype": args.out_dtype,
-                   "parallelism": f"dp{world} (independent queries per rank)",
-                   "l2": "flushed between steps (256 MB write)"},
+        "config": c2_config(L, world, args.out_dtype, s.block_size),
         "ttft_ms": ms_per_step,
         "ttft_l1_ms": statistics.median(l1_ms),
         "step_ms_p50": statistics.median(step_ms), "step_ms_p99": float(np.percentile(step_ms, 99)),
@@ -327,6 +335,117 @@ def main():
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+C5_PARAMS = dict(n_queries=64, n_frag=16, frag_len=1024, pool=64, shared_per_query=8, n_prefix=512, n_cross=256)
+
+
+def main_c5(args, rank, world, local):
+    """configs[4] (scaled to fit one GPU's inputs): a batch of span queries with 50% cross-query
+    fragment overlap, partitioned over the ranks: query q is homed on q mod W, each
+    distinct fragment is prefilled once on its owner rank (u64le(s_last) mod W) and its KV is moved
+    to the home ranks of the joins that read it by one NCCL all-to-all per layer. One step = plan
+    (every rank, its share) -> prefill (own jobs) -> exchange -> joins (home queries). Strong
+    scaling: total work is fixed, value = the batch's algorithmic FLOPs / max-over-ranks time."""
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2511_02749_b200 import inputs, parallel, runner, spanq
+
+    w = inputs.c5(**C5_PARAMS)
+    s = inputs.Shape(**{**w.shape.__dict__, "layers": args.layers})
+    ntok = sum(len(q.prefix) + sum(len(f) for f in q.fragments) + len(q.cross) for q in w.queries)
+    nblk = ntok // s.block_size + 4 * len(w.queries) * (C5_PARAMS["n_frag"] + 2) + 1024
+    ctx = spanq.Context(s, nblk, device=local, max_position=1 << 15, out_dtype=args.out_dtype,
+                        rank=rank, world_size=world)
+    stream = torch.cuda.Stream(dev)
+    tab = runner.device_tables(s, 0, w.seed, dev)
+    p0 = ctx.plan(w.queries, stream=stream)
+    view = p0.view()
+    ptok, jtok = runner.prefill_tokens(view, w.queries), runner.join_tokens(view, w.queries)
+    qp, kp, vp = runner.gather(tab, ptok, dev)
+    qj, kj, vj = runner.gather(tab, jtok, dev)
+    odt = torch.float32 if args.out_dtype == "fp32" else torch.bfloat16
+    op = torch.empty((max(len(ptok), 1), s.hq, s.d), dtype=odt, device=dev)
+    lp = torch.empty((max(len(ptok), 1), s.hq), dtype=torch.float32, device=dev)
+    oj = torch.empty((max(len(jtok), 1), s.hq, s.d), dtype=odt, device=dev)
+    lj = torch.empty((max(len(jtok), 1), s.hq), dtype=torch.float32, device=dev)
+    p0.release(stream=stream)
+    flops_rank = view["prefill_flops"] + view["join_flops"]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    xbytes = [0]
+
+    def step():
+        ctx.evict_all()
+        plan = ctx.plan(w.queries, stream=stream)
+        v = plan.view() if world > 1 else None
+        for layer in range(args.layers):
+            if len(ptok):
+                plan.prefill(layer, qp, kp, vp, op, lp, stream=stream)
+            if world > 1:
+                st = parallel.exchange_layer(plan, v, layer, s, dev, ctx.k_pool.dtype, rank, world, stream=stream)
+                xbytes[0] = st["sent_bytes"]
+            if len(jtok):
+                plan.join(layer, qj, kj, vj, oj, lj, stream=stream)
+        plan.release(stream=stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        n0 = ctx.launch_count()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        with ClockSampler(local) as clk:
+            for i in range(args.steps):
+                flush.zero_()
+                stream.synchronize()
+                evs[i][0].record(stream)
+                step()
+                evs[i][1].record(stream)
+                stream.synchronize()
+        torch.cuda.synchronize()
+        launches = ctx.launch_count() - n0
+    ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = float(sum(ms))
+    flops_total = flops_rank * args.layers
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+        f = torch.tensor([flops_total], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(f)
+        flops_total = float(f.item())
+    value = flops_total * args.steps / (total_ms / 1e3) / 1e12
+    peak_burst, _, _, peak_src = peaks()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "C5 (configs[4], scaled: %(n_queries)d queries x %(n_frag)d fragments x "
+                               "%(frag_len)d tokens, %(shared_per_query)d shared from a pool of %(pool)d, "
+                               "P%(n_prefix)d, cross %(n_cross)d), cold cache" % C5_PARAMS,
+                   "model": f"8B GQA attention shape Hq32/Hkv8/d128, {args.layers} layers",
+                   "layers": args.layers, "global_batch": len(w.queries), "block_size": s.block_size,
+                   "out_dtype": args.out_dtype,
+                   "parallelism": f"partitioned over {world} ranks (home q mod W, fragment owner "
+                                  "u64le(s_last) mod W, NCCL all-to-all KV exchange per layer)",
+                   "l2": "flushed between steps (256 MB write)"},
+        "flops_per_step": flops_total, "exchange_bytes_per_step_rank0": xbytes[0] * args.layers,
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+        "peak_bf16_tflops": peak_burst, "frac_of_peak": value / world / peak_burst, "peak_source": peak_src,
+    }
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
