@@ -247,3 +247,49 @@ def test_tree_normalization_and_errors():
             normalize(np.array(b), np.array([1, 2, 3]))
     with pytest.raises(TreeError):
         normalize(np.array([(2, 1, 0, 0), (0, 0, 0, 1)]), np.array([-1]))
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_partition_covers_the_single_rank_plan(world):
+    # Partitioning (home q mod W, fragment owner u64le(s_last) mod W) must split, not change, the
+    # work of the W = 1 plan: with cold stores, (1) every distinct fragment is prefilled on exactly
+    # one rank — its owner — with the same rows as in the W = 1 plan, (2) every query's join rows
+    # are on exactly its home rank with the same positions, (3) the prefix rows follow their
+    # query, and (4) what a rank receives from an owner is exactly what that owner sends it.
+    qs = [(q.prefix, q.fragments, q.cross) for q in inputs.random_queries(40 + world, 24, vocab=10, max_len=18,
+                                                                          reuse_p=0.5)]
+    mk = lambda: Store(1 << 14, 4, 2, 16, 4, 10000.0, 0)
+    one = mk().plan(qs)
+    parts = [mk().plan(qs, rank=r, world=world) for r in range(world)]
+
+    def frag_rows(v):
+        out = {}
+        for j in v.jobs:
+            s = v.segments[j]
+            if s.kind == KIND_FRAG:
+                out[s.digests[-1]] = out.get(s.digests[-1], 0) + (s.tok_len - s.compute_begin)
+        return out
+
+    base = frag_rows(one)
+    seen = {}
+    for r, v in enumerate(parts):
+        for d, n in frag_rows(v).items():
+            assert hashing.owner_rank(d, world) == r
+            assert d not in seen
+            seen[d] = n
+    assert seen == base
+    for qi in range(len(qs)):
+        home = qi % world
+        for r, v in enumerate(parts):
+            cross = [s for s in v.segments if s.kind == KIND_CROSS and s.query == qi]
+            pref = [s for s in v.segments if s.kind == KIND_PREFIX and s.query == qi]
+            assert len(cross) == (1 if r == home else 0)
+            assert (len(pref) > 0) == (r == home and len(qs[qi][0]) > 0)
+    join_pos = np.concatenate([v.join_pos for v in parts])
+    assert sorted(join_pos.tolist()) == sorted(one.join_pos.tolist())
+    assert sum(v.n_join_queries for v in parts) == len(qs)
+    # exchange lists: counts agree pairwise, and receivers hold blocks for exactly the remote
+    # fragments their joins read
+    for r in range(world):
+        for p in range(world):
+            assert len(parts[r].send.get(p, [])) == len(parts[p].recv.get(r, []))
