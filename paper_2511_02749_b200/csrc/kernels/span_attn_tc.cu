@@ -84,6 +84,7 @@ struct TcParams {
   int paired;     // 1: a unit is a GQA head pair (A = 2u, B = 2u+1); 0: one head (B idle)
   int poly_mask;  // pair i of a 32-key chunk uses the FMA-pipe exp2 when (i & 3) < poly_mask
   float rescale_threshold;  // log2 units; O is rescaled when the running max grows by more
+  int qrot_table;  // Q prep: 1 = (cos, sin) table row per step, 0 = angle recurrence
   int dbg_mode;  // profiling only: 1 = softmax does no math, 2 = max pass only,
                  // 3 = 1 + K/V always from the first block (L2-resident), 4 = 1 + MMA skips K/V waits,
                  // 5 = 1 + Q prep does no work
@@ -617,7 +618,7 @@ __device__ __forceinline__ void load_cs8(const float2* rope, int64_t idx, float 
 
 template <int D>
 __device__ __forceinline__ void rotate_q_tile(uint8_t* qs_base, const float2* rope, int my_pos, int my_valid, int rot,
-                                              int max_pos) {
+                                              int max_pos, bool table) {
   constexpr int kLanesPerRow = D / 16;       // 8 pairs per lane
   constexpr int R = 32 / kLanesPerRow;       // rows per step
   const int lane = threadIdx.x & 31;
@@ -631,7 +632,22 @@ __device__ __forceinline__ void rotate_q_tile(uint8_t* qs_base, const float2* ro
   const bool consecutive = __all_sync(0xffffffffu, !my_valid || my_pos == p_first + lane) && p_first - rot >= 0 &&
                            p_first - rot + 31 < max_pos;
   float c[8], sn[8];
-  if (consecutive) {
+  if (consecutive && table) {
+    // table rows per step (4 x 16 B loads, the next step's prefetched) instead of the recurrence
+    float c2[8], s2[8];
+    const int64_t base = static_cast<int64_t>(p_first - rot + g) * (D / 2) + pair0;
+    load_cs8(rope, base, c, sn);
+#pragma unroll
+    for (int st = 0; st < 32 / R; ++st) {
+      if (st + 1 < 32 / R) load_cs8(rope, base + static_cast<int64_t>((st + 1) * R) * (D / 2), c2, s2);
+      rotate_step<D>(qs_base, wq * 32 + st * R + g, u, c, sn);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        c[e] = c2[e];
+        sn[e] = s2[e];
+      }
+    }
+  } else if (consecutive) {
     float cd[8], sd[8];
     load_cs8(rope, static_cast<int64_t>(p_first - rot + g) * (D / 2) + pair0, c, sn);
     load_cs8(rope, static_cast<int64_t>(R) * (D / 2) + pair0, cd, sd);  // position R: (cos R th, sin R th)
@@ -691,7 +707,7 @@ __device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_
           mbar_wait(&S.q_load[sl], (load_phase >> sl) & 1);
           load_phase ^= 1u << sl;
           if (tr) trace(P, 4, tc, 44 + x);  // 44/45: Q tile A/B loaded
-          rotate_q_tile<D>(&S.q[sl][0][0], a.rope, my_pos, my_row < w.n_rows, rot, a.max_pos);
+          rotate_q_tile<D>(&S.q[sl][0][0], a.rope, my_pos, my_row < w.n_rows, rot, a.max_pos, P.qrot_table);
           fence_proxy_async_smem();
         }
         if (tr) trace(P, 4, tc, 42 + x);  // 42/43: Q tile A/B written
@@ -809,6 +825,7 @@ cudaError_t launch_dp(const AttnArgs& a, cudaStream_t st) {
   p.poly_mask = PM;
   p.rescale_threshold = a.rescale_threshold;
   p.dbg_mode = getenv("SPANQ_DBG_MODE") ? atoi(getenv("SPANQ_DBG_MODE")) : 0;
+  p.qrot_table = getenv("SPANQ_QROT_TABLE") ? atoi(getenv("SPANQ_QROT_TABLE")) : 0;
   span_attn_tc_kernel<D, PM><<<a.grid, kThreads, smem, st>>>(p);
   return cudaGetLastError();
 }

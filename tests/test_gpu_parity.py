@@ -232,3 +232,69 @@ def test_full_size_c2_sampled_rows(cuda_dev):
         got = res.o_prefill[torch.from_numpy(off + r).to(cuda_dev)][:, heads]
         check(got, eo, False, f"C2 prefill seg {si}")
     ctx.close()
+
+
+def test_multi_layer_plan_reuse(cuda_dev):
+    # one plan, three layers (each its own tables and KV-pool layer): the per-launch work
+    # counters of the dynamic schedule and the pad zeroing are per launch / per layer
+    import torch
+
+    sh = inputs.Shape(hq=8, hkv=2, d=128, block_size=32, vocab=1024, layers=3)
+    w = inputs.make_rag(109, sh, 100, 3, [300, 129, 260], 200)
+    ctx = spanq.Context(sh, 1024, device=0, max_position=1 << 14, out_dtype="fp32")
+    plan = ctx.plan(w.queries)
+    view = plan.view()
+    ov = oracle_plan(w, w.queries)
+    qs = [(q.prefix, q.fragments, q.cross) for q in w.queries]
+    ptok, jtok = runner.prefill_tokens(view, w.queries), runner.join_tokens(view, w.queries)
+    for layer in range(3):
+        tab = runner.device_tables(sh, layer, w.seed, cuda_dev)
+        op = torch.empty((len(ptok), sh.hq, sh.d), dtype=torch.float32, device=cuda_dev)
+        oj = torch.empty((len(jtok), sh.hq, sh.d), dtype=torch.float32, device=cuda_dev)
+        plan.prefill(layer, *runner.gather(tab, ptok, cuda_dev), op)
+        plan.join(layer, *runner.gather(tab, jtok, cuda_dev), oj)
+        torch.cuda.synchronize()
+        eq, ek, ev = inputs.layer_tables(sh, layer, w.seed)
+        eo, _ = oatt.plan_prefill_expected(ov, qs, eq, ek, ev, sh.rope_base)
+        jo, _ = oatt.plan_join_expected(ov, qs, eq, ek, ev, sh.rope_base)
+        check(op, eo, False, f"layer {layer} prefill O")
+        check(oj, jo, False, f"layer {layer} join O")
+    plan.release()
+    ctx.close()
+
+
+def test_sub_range_calls(cuda_dev):
+    # prefill jobs and joins issued in two ranges each (the per-call work lists uploaded by the
+    # ABI) give the full-range results: prefill bit for bit, joins within tolerance of the oracle
+    import torch
+
+    sh = inputs.Shape(hq=8, hkv=2, d=128, block_size=16, vocab=256)
+    qs = inputs.random_queries(110, 6, vocab=256, max_frag=5, max_len=200, max_prefix=150,
+                               max_cross=180, reuse_p=0.5)
+    w = inputs.Workload("batch", sh, qs, 110)
+    tab = runner.device_tables(sh, 0, w.seed, cuda_dev)
+    full = runner.run_pass(spanq.Context(sh, 2048, device=0, out_dtype="fp32"), qs, [tab], cuda_dev)
+    ctx = spanq.Context(sh, 2048, device=0, out_dtype="fp32")
+    plan = ctx.plan(qs)
+    view = plan.view()
+    nj, nq = view["n_jobs"], view["n_queries"]
+    jr = view["job_row_off"]
+    qr = view["query_join_row_off"]
+    op = torch.empty_like(full.o_prefill)
+    oj = torch.empty_like(full.o_join)
+    for a, b in [(0, nj // 2), (nj // 2, nj)]:
+        toks = runner.prefill_tokens(view, qs, (a, b))
+        if len(toks):
+            plan.prefill(0, *runner.gather(tab, toks, cuda_dev), op[jr[a]:jr[b]], jobs=(a, b))
+    for a, b in [(0, nq // 2), (nq // 2, nq)]:
+        toks = runner.join_tokens(view, qs, (a, b))
+        if len(toks):
+            plan.join(0, *runner.gather(tab, toks, cuda_dev), oj[qr[a]:qr[b]], queries=(a, b))
+    torch.cuda.synchronize()
+    assert torch.equal(op, full.o_prefill)
+    ov = oracle_plan(w, qs)
+    eq, ek, ev = inputs.layer_tables(sh, 0, w.seed)
+    jo, _ = oatt.plan_join_expected(ov, [(q.prefix, q.fragments, q.cross) for q in qs], eq, ek, ev, sh.rope_base)
+    check(oj, jo, False, "sub-range join O")
+    plan.release()
+    ctx.close()
