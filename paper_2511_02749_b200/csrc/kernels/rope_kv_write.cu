@@ -75,14 +75,19 @@ __global__ void __launch_bounds__(256) rope_kv_write_kernel(
   const bool main_row = gid < total;
   int64_t r = 0, src = 0;
   int h = 0, g = 0;
-  uint4 ku = make_uint4(0, 0, 0, 0);
+  uint4 ku = make_uint4(0, 0, 0, 0), vu = make_uint4(0, 0, 0, 0);
+  int64_t s = -1;
   if (main_row) {
     r = gid / per_row;
     const int rem = static_cast<int>(gid - r * per_row);
     h = rem / G;
     g = rem % G;
     src = (r * hkv + h) * D + g * N;
+    // all loads issued up front and independent of each other (slot, pos, k, v; the table
+    // below): rows with slot -1 (rare: resident blocks) load k/v for nothing
+    s = slot[r];
     ku = __ldg(reinterpret_cast<const uint4*>(k + src));
+    vu = __ldg(reinterpret_cast<const uint4*>(v + src));
   }
   uint4 pu;
   pu.x = __shfl_xor_sync(0xffffffffu, ku.x, G / 2);
@@ -93,7 +98,6 @@ __global__ void __launch_bounds__(256) rope_kv_write_kernel(
     float x[N], y[N];
     Vec<T>::unpack(ku, x);
     Vec<T>::unpack(pu, y);
-    const int64_t s = slot[r];
     if (s >= 0) {
       const int p = pos[r];
       const bool first_half = g < G / 2;
@@ -110,7 +114,7 @@ __global__ void __launch_bounds__(256) rope_kv_write_kernel(
       const int64_t blk = s / bs, off = s % bs;
       const int64_t dst = layer_off + ((blk * hkv + h) * bs + off) * D + g * N;
       *reinterpret_cast<uint4*>(k_pool + dst) = Vec<T>::pack(out);
-      *reinterpret_cast<uint4*>(v_pool + dst) = __ldg(reinterpret_cast<const uint4*>(v + src));
+      *reinterpret_cast<uint4*>(v_pool + dst) = vu;
     }
     return;
   }
