@@ -34,24 +34,45 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineDesc* __restr
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // grid.z splits the 128 rows of a tile into groups of blockDim/32 rows: one warp per row
   for (int r = blockIdx.z * (blockDim.x / 32) + warp; r < cd.n_rows; r += gridDim.z * (blockDim.x / 32)) {
+    const int64_t base = (static_cast<int64_t>(cd.part_base) * cd.n_heads + blockIdx.y) * kTileRows + r;
+    const int64_t pstride = static_cast<int64_t>(cd.n_heads) * kTileRows;  // next split, same (head, row)
     float m = -INFINITY;
-    for (int s = 0; s < cd.n_split; ++s)
-      m = fmaxf(m, lsepart[(static_cast<int64_t>(cd.part_base + s) * cd.n_heads + blockIdx.y) * kTileRows + r]);
     float acc[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) acc[e] = 0.f;
     float tot = 0.f;
-    for (int s = 0; s < cd.n_split; ++s) {
-      const int64_t pidx = (static_cast<int64_t>(cd.part_base + s) * cd.n_heads + blockIdx.y) * kTileRows + r;
-      const float ls = lsepart[pidx];
-      const float w = (ls == -INFINITY) ? 0.f : __expf(ls - m);
-      tot += w;
-      const float* src = opart + pidx * D + lane * E;
+    // up to 8 splits with every load issued before the arithmetic (latency-bound otherwise)
+    constexpr int kU = 8;
+    for (int s0 = 0; s0 < cd.n_split; s0 += kU) {
+      float ls[kU];
+      float2 ov[kU][E / 2];
 #pragma unroll
-      for (int e = 0; e < E; e += 2) {
-        const float2 v = *reinterpret_cast<const float2*>(src + e);
-        acc[e] = fmaf(w, v.x, acc[e]);
-        acc[e + 1] = fmaf(w, v.y, acc[e + 1]);
+      for (int u = 0; u < kU; ++u) {
+        const bool ok = s0 + u < cd.n_split;
+        const int64_t pidx = base + (s0 + u) * pstride;
+        ls[u] = ok ? lsepart[pidx] : -INFINITY;
+#pragma unroll
+        for (int e = 0; e < E; e += 2)
+          ov[u][e / 2] = ok ? *reinterpret_cast<const float2*>(opart + pidx * D + lane * E + e) : make_float2(0.f, 0.f);
+      }
+      float mb = m;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) mb = fmaxf(mb, ls[u]);
+      // rescale what was accumulated under the previous max (only when n_split > 8)
+      const float c = (m == -INFINITY) ? 0.f : __expf(m - mb);
+      tot *= c;
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[e] *= c;
+      m = mb;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const float w = (ls[u] == -INFINITY) ? 0.f : __expf(ls[u] - m);
+        tot += w;
+#pragma unroll
+        for (int e = 0; e < E; e += 2) {
+          acc[e] = fmaf(w, ov[u][e / 2].x, acc[e]);
+          acc[e + 1] = fmaf(w, ov[u][e / 2].y, acc[e + 1]);
+        }
       }
     }
     const float inv = 1.f / tot;
