@@ -59,13 +59,14 @@ struct TcSmem {
   // the K ring is twice as deep as the V ring
   static constexpr int kKSlots = D == 64 ? 8 : 4;
   static constexpr int kVSlots = D == 64 ? 4 : 2;
-  static constexpr int kQSlots = 3;
+  static constexpr int kQSlots = 2;  // slot x = head x (the next epoch's tile is loaded after
+                                     // this epoch's last S MMA: ~2 steps before the item ends)
   alignas(1024) uint8_t q[kQSlots][kChunks][kChunkBytes];
   alignas(1024) uint8_t k[kKSlots][kChunks][kSubBytes];  // ring of 64-key K sub-tiles
   alignas(1024) uint8_t v[kVSlots][kChunks][kSubBytes];  // ring of 64-key V sub-tiles
-  alignas(1024) float stage[8][32 * 32];                        // epilogue transpose, per softmax warp
+  alignas(1024) float stage[8][2][32 * 32];  // epilogue transpose: 2 x 4 KB per softmax warp
   uint64_t kv_full[2][kKSlots], kv_empty[2][kKSlots];  // [K, V][slot] (V uses the first kVSlots)
-  uint64_t q_full[3], q_empty[3], q_load[3];
+  uint64_t q_full[2], q_empty[2], q_load[2];
   uint64_t s_full[2][2], p_full[2][2], o_done[2][2];  // [head][S buffer / PV parity j & 1]
   static constexpr int kSched = 4;  // dynamic schedule: ring of claimed codes
   uint64_t sched_full[kSched], sched_empty[kSched];
@@ -263,28 +264,24 @@ __device__ void run_mma(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_b
       else
         c = SubCursor{c.t + 1, 0};
     };
-    int qa = 0, qb = 1;  // this epoch's Q slots (A's, B's)
     SubCursor cs{tb, 0}, cp{tb, 0};
     uint32_t js = jg;  // global index of the next S sub-tile (K slot js)
-    // the Q slot(s) this issuer owns: its head's; an unpaired launch's A issuer also frees B's
+    // Q: slot x holds head x's tile of the current epoch (an item or a change of rot_delta)
     auto release_q = [&]() {
-      mma_commit(&S.q_empty[x == 0 ? qa : qb]);
-      if (!two) mma_commit(&S.q_empty[qb]);
+      mma_commit(&S.q_empty[x]);
+      if (!two) mma_commit(&S.q_empty[1]);  // an unpaired launch's A issuer also frees B's slot
     };
     auto issue_s = [&]() {
       const int t = cs.t;
       if (cs.h == 0 && (t == tb || a.tiles[t].rot_delta != a.tiles[t - 1].rot_delta)) {
         if (t != tb) release_q();  // the previous epoch's Q tile: free once its S MMAs are done
-        qa = (2 * ep) % 3;
-        qb = (2 * ep + 1) % 3;
-        const int mine = x == 0 ? qa : qb;
-        mbar_wait(&S.q_full[mine], ((2 * ep + x) / 3) & 1);
+        mbar_wait(&S.q_full[x], ep & 1);
         trace(P, 1, tc, 21);  // 21: Q ready for new epoch
         ++ep;
       }
       wait_kv(0, js);
       trace(P, 1, tc, 22);  // 22: K ready
-      const uint32_t qbase = smem_u32(&S.q[x == 0 ? qa : qb][0][0]);
+      const uint32_t qbase = smem_u32(&S.q[x][0][0]);
       const uint32_t kb = smem_u32(&S.k[js % kKS][0][0]);
       const int buf = js & 1;
 #pragma unroll
@@ -417,7 +414,7 @@ __device__ __forceinline__ void epilogue(const TcParams& P, TcSmem<D>& S, uint32
   const float lse = f.l > 0.f ? (f.m + __log2f(f.l)) * 0.69314718055994531f : -INFINITY;
   const int wr = (threadIdx.x / 32) & 3;  // warp's 32-row slice of the tile
   const int lane = threadIdx.x & 31;
-  float* stg = S.stage[x * 4 + wr];
+  float* const stg2 = &S.stage[x * 4 + wr][0][0];  // two 4 KB buffers, chunk c uses buffer c & 1
   // TMA store for whole 32-row slices (and for split partials, whose padding rows are never
   // read); a slice that ends inside this item's rows is written directly (the next rows belong
   // to another item)
@@ -428,7 +425,8 @@ __device__ __forceinline__ void epilogue(const TcParams& P, TcSmem<D>& S, uint32
   for (int c = 0; c < D / 32; ++c) {
     if (c + 1 < D / 32) tmem_ld32(ocol + (c + 1) * 32, vv[(c + 1) & 1]);
     const uint32_t(&v)[32] = vv[c & 1];
-    if (lane == 0) bulk_wait_read<0>();  // previous chunk's store has read the buffer
+    float* stg = stg2 + (c & 1) * 1024;
+    if (lane == 0) bulk_wait_read<1>();  // the store of chunk c-2 (same buffer) has read it
     __syncwarp();
 #pragma unroll
     for (int uu = 0; uu < 8; ++uu)
@@ -693,9 +691,8 @@ __device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_
       const int rot = a.tiles[t].rot_delta;
       if (t > w.tile_begin && rot == a.tiles[t - 1].rot_delta) continue;
       for (int x = 0; x < 2; ++x) {
-        const uint32_t n = 2 * ep + x;  // Q slot index: slot n % 3, (n / 3)-th use
-        const int sl = static_cast<int>(n % 3);
-        mbar_wait(&S.q_empty[sl], ((n / 3) & 1) ^ 1);
+        const int sl = x;  // slot x = head x, its ep-th use
+        mbar_wait(&S.q_empty[sl], (ep & 1) ^ 1);
         if (tr) trace(P, 4, tc, 40 + x);  // 40/41: slot free for head A/B
         if (x < u.n_heads && P.dbg_mode != 5) {  // single-head units leave the B slot untouched
           if (r == 0) {

@@ -14,7 +14,9 @@ import numpy as np
 
 from . import inputs as _inputs
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libspanq.so")
+# SPANQ_LIB (tuning / A/B only) points at an alternative build of the same library
+_LIB_PATH = os.environ.get("SPANQ_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
+                                                        "libspanq.so")
 _lib = None
 
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, ESTATE = range(6)
