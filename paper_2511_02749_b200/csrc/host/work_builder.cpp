@@ -200,7 +200,7 @@ void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_en
   // smallest budget whose greedy cut fits in `grid` CTAs (bisection; the cost is monotone enough)
   double lo = total / grid, hi = total / grid + 4 * kSubOverhead + 64;
   while (cut(hi, nullptr) > grid) hi *= 1.5;
-  for (int it = 0; it < 24 && hi - lo > 0.25; ++it) {
+  for (int it = 0; it < 16 && hi - lo > 0.5; ++it) {
     const double mid = 0.5 * (lo + hi);
     if (cut(mid, nullptr) <= grid)
       hi = mid;

@@ -48,17 +48,25 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// One device buffer holding several arrays (one H2D copy).
+// One device buffer holding several arrays (one H2D copy): offsets are assigned first, the bytes
+// are copied once, straight into the destination (pinned staging). Sources must outlive write().
 struct Packer {
-  std::vector<uint8_t> host;
+  size_t size = 0;
+  std::vector<std::pair<size_t, std::pair<const void*, size_t>>> parts;
   template <typename T>
   size_t add(const std::vector<T>& v) {
-    const size_t off = align_up(host.size(), 256);
-    host.resize(off + v.size() * sizeof(T));
-    if (!v.empty()) std::memcpy(host.data() + off, v.data(), v.size() * sizeof(T));
+    const size_t off = align_up(size, 256);
+    parts.push_back({off, {v.data(), v.size() * sizeof(T)}});
+    size = off + v.size() * sizeof(T);
     return off;
   }
+  void write(uint8_t* dst) const {
+    for (const auto& p : parts)
+      if (p.second.second) std::memcpy(dst + p.first, p.second.first, p.second.second);
+  }
 };
+
+const std::vector<int32_t> kZeros2 = {0, 0};  // claim counters of a dynamic work list
 
 struct DevWork {  // offsets of one attention work list inside a plan buffer
   size_t tiles, tile_blocks, items, cta_off, cta_items, combine, sched;
@@ -332,7 +340,7 @@ spq_status upload_work(spq_ctx* c, const spq::AttnWorkHost& h, cudaStream_t st, 
   tw->w.items = pk.add(h.items);
   tw->w.cta_off = pk.add(h.cta_off);
   tw->w.cta_items = pk.add(h.cta_items);
-  tw->w.sched = pk.add(std::vector<int32_t>{0, 0});  // claim counters (self-resetting)
+  tw->w.sched = pk.add(kZeros2);  // claim counters (self-resetting)
   tw->w.dynamic = h.dynamic;
   tw->w.n_codes = static_cast<int32_t>(h.cta_items.size());
   tw->w.combine = pk.add(h.combine);
@@ -340,8 +348,10 @@ spq_status upload_work(spq_ctx* c, const spq::AttnWorkHost& h, cudaStream_t st, 
   tw->w.grid = h.grid;
   tw->w.n_combine = static_cast<int32_t>(h.combine.size());
   tw->w.n_parts = h.n_parts;
-  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&tw->buf), std::max<size_t>(pk.host.size(), 256), st));
-  CUDA_TRY(cudaMemcpyAsync(tw->buf, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice, st));
+  std::vector<uint8_t> host(pk.size);
+  pk.write(host.data());
+  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&tw->buf), std::max<size_t>(pk.size, 256), st));
+  CUDA_TRY(cudaMemcpyAsync(tw->buf, host.data(), pk.size, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaStreamSynchronize(st));  // pageable source: keep it alive until the copy is done
   return SPQ_OK;
 }
@@ -572,8 +582,14 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
   // algorithmic bytes of rope_kv_write: per written row, read k,v and write both pages
   // (4*Hkv*d*elt), plus 12 B of pos/slot metadata per row
   const int64_t row_bytes = 4LL * c->cfg.num_kv_heads * c->cfg.head_dim * elt_size(c);
-  for (int64_t s : H.prefill_slot) p->prefill_kv_bytes += 12 + (s >= 0 ? row_bytes : 0);
-  for (int64_t s : H.join_slot) p->join_kv_bytes += 12 + (s >= 0 ? row_bytes : 0);
+  {
+    int64_t written = 0;
+    for (int64_t s : H.prefill_slot) written += s >= 0;
+    p->prefill_kv_bytes = 12 * static_cast<int64_t>(H.prefill_slot.size()) + written * row_bytes;
+    written = 0;
+    for (int64_t s : H.join_slot) written += s >= 0;
+    p->join_kv_bytes = 12 * static_cast<int64_t>(H.join_slot.size()) + written * row_bytes;
+  }
   lap("flops/bytes");
   if (is_gpu(c)) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -592,7 +608,7 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
       w->items = pk.add(h.items);
       w->cta_off = pk.add(h.cta_off);
       w->cta_items = pk.add(h.cta_items);
-      w->sched = pk.add(std::vector<int32_t>{0, 0});  // claim counters (self-resetting)
+      w->sched = pk.add(kZeros2);  // claim counters (self-resetting)
       w->dynamic = h.dynamic;
       w->n_codes = static_cast<int32_t>(h.cta_items.size());
       w->combine = pk.add(h.combine);
@@ -604,24 +620,31 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
     };
     add_work(p->pw_host, &p->pw);
     add_work(p->jw_host, &p->jw);
-    const size_t bytes = std::max<size_t>(pk.host.size(), 256);
+    // one device allocation: packed arrays, then the split-KV partials (O, LSE)
+    size_t bytes = std::max<size_t>(pk.size, 256);
+    size_t off_opart = 0, off_lsepart = 0;
+    if (p->jw.n_parts > 0) {
+      const size_t rows = static_cast<size_t>(p->jw.n_parts) * heads_per_unit(c) * spq::kTileRows;
+      off_opart = align_up(bytes, 1024);
+      off_lsepart = align_up(off_opart + rows * c->cfg.head_dim * sizeof(float), 1024);
+      bytes = off_lsepart + rows * sizeof(float);
+    }
     // pinned staging, reused once its previous upload has completed
-    if (c->staging_size < bytes) {
+    if (c->staging_size < pk.size) {
       CUDA_TRY(cudaEventSynchronize(c->staging_ev));
       if (c->staging) CUDA_TRY(cudaFreeHost(c->staging));
-      c->staging_size = std::max(bytes, static_cast<size_t>(1) << 20);
+      c->staging_size = std::max(pk.size, static_cast<size_t>(1) << 20);
       CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&c->staging), c->staging_size));
     } else {
       CUDA_TRY(cudaEventSynchronize(c->staging_ev));
     }
-    std::memcpy(c->staging, pk.host.data(), pk.host.size());
+    pk.write(c->staging);
     CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->dbuf), bytes, st));
-    CUDA_TRY(cudaMemcpyAsync(p->dbuf, c->staging, pk.host.size(), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(p->dbuf, c->staging, pk.size, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaEventRecord(c->staging_ev, st));
     if (p->jw.n_parts > 0) {
-      const size_t rows = static_cast<size_t>(p->jw.n_parts) * heads_per_unit(c) * spq::kTileRows;
-      CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->opart), rows * c->cfg.head_dim * sizeof(float), st));
-      CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->lsepart), rows * sizeof(float), st));
+      p->opart = reinterpret_cast<float*>(p->dbuf + off_opart);
+      p->lsepart = reinterpret_cast<float*>(p->dbuf + off_lsepart);
     }
     lap("upload");
   }
@@ -876,8 +899,7 @@ spq_status spq_plan_release(spq_ctx* c, spq_plan* p, void* stream) {
     CUDA_TRY(cudaEventRecord(e, st));
     c->pending.push_back(e);
     if (p->dbuf) CUDA_TRY(cudaFreeAsync(p->dbuf, st));
-    if (p->opart) CUDA_TRY(cudaFreeAsync(p->opart, st));
-    if (p->lsepart) CUDA_TRY(cudaFreeAsync(p->lsepart, st));
+    // opart / lsepart live inside dbuf
   }
   delete p;
   return SPQ_OK;
