@@ -178,6 +178,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="spanq", choices=["spanq", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-locality", action="store_true", help="skip the C3-warm / dense-causal TTFT lines")
     ap.add_argument("--layers", type=int, default=None,
                     help="attention layers per step (c2 default 40 = the 8B model's depth; c5 default 1)")
     ap.add_argument("--out-dtype", default="fp32", choices=["fp32", "bf16"])
@@ -306,6 +307,14 @@ def main():
     e2e_total = max_over_ranks(float(sum(e2e_ms)))
     e2e_value = world * flops * args.steps / (e2e_total / 1e3) / 1e12
 
+    # ---- locality (paper P:33: span queries vs stock prefill), one layer, same protocol:
+    # configs[2] (C3: 75% of the fragments cached, permuted) after its warm-up query, and an
+    # ordinary causal prefill of the same 17,152 tokens (what a prefix cache cannot reuse)
+    locality = None
+    if not args.no_locality:
+        with torch.cuda.stream(stream):
+            locality = measure_locality(ctx, s, tab, dev, stream, flush, args)
+
     peak_burst, peak_sust, hbm, peak_src = peaks()
     pre_ms = statistics.median(a for a, _ in attn_ms)
     join_ms = statistics.median(b for _, b in attn_ms)
@@ -333,12 +342,80 @@ def main():
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": e2e_total / args.steps},
     }
+    if locality is not None:
+        locality["c2_cold_ttft_l1_ms"] = line["ttft_l1_ms"]
+        locality["dense_over_span_ttft"] = locality["dense_causal_ttft_l1_ms"] / line["ttft_l1_ms"]
+        locality["c2_cold_over_c3_warm_ttft"] = line["ttft_l1_ms"] / locality["c3_warm_ttft_l1_ms"]
+        line["locality"] = locality
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def measure_locality(ctx, s, tab, dev, stream, flush, args, reps: int = 5):
+    """TTFT (plan + one layer of attention, cold L2) of (a) configs[2] C3 right after its warm-up
+    query filled the store (75% fragment hits, permuted: only the new fragments, the partial
+    prefix tail and the join are computed) and (b) the same number of tokens as one ordinary
+    causal prefill (a 17,151-token prefix + 1 cross token: what a stock engine computes)."""
+    import torch
+
+    from paper_2511_02749_b200 import inputs, runner
+
+    c3 = inputs.c3()
+    c2q = inputs.c2(seed=2).queries[0]
+    toks = np.concatenate([c2q.prefix] + list(c2q.fragments) + [c2q.cross])
+    dense = inputs.SpanQuery(toks[:-1], [], toks[-1:])
+    odt = torch.float32 if args.out_dtype == "fp32" else torch.bfloat16
+
+    def fill(warm):
+        ctx.evict_all()
+        for q in warm:  # fills the store (untimed)
+            w_plan = ctx.plan([q], stream=stream)
+            wv = w_plan.view()
+            wpt, wjt = runner.prefill_tokens(wv, [q]), runner.join_tokens(wv, [q])
+            if len(wpt):
+                w_plan.prefill(0, *runner.gather(tab, wpt, dev), torch.empty((len(wpt), s.hq, s.d), dtype=odt,
+                                                                             device=dev), stream=stream)
+            w_plan.join(0, *runner.gather(tab, wjt, dev), torch.empty((len(wjt), s.hq, s.d), dtype=odt,
+                                                                      device=dev), stream=stream)
+            w_plan.release(stream=stream)
+
+    def run(queries, warm):
+        fill(warm)  # the timed plan's view (rows to compute) depends on what the warm-up cached
+        plan = ctx.plan(queries, stream=stream)
+        v = plan.view()
+        pt, jt = runner.prefill_tokens(v, queries), runner.join_tokens(v, queries)
+        ins = (runner.gather(tab, pt, dev) if len(pt) else None, runner.gather(tab, jt, dev))
+        op = torch.empty((max(len(pt), 1), s.hq, s.d), dtype=odt, device=dev)
+        oj = torch.empty((len(jt), s.hq, s.d), dtype=odt, device=dev)
+        plan.release(stream=stream)
+        ms = []
+        for _ in range(reps + 1):
+            fill(warm)
+            flush.zero_()
+            stream.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            plan = ctx.plan(queries, stream=stream)
+            if ins[0] is not None:
+                plan.prefill(0, *ins[0], op, stream=stream)
+            plan.join(0, *ins[1], oj, stream=stream)
+            plan.release(stream=stream)
+            b.record(stream)
+            stream.synchronize()
+            ms.append(a.elapsed_time(b))
+        return statistics.median(ms[1:]), v["prefill_flops"] + v["join_flops"]
+
+    c3_ms, c3_flops = run(c3.queries, c3.warmup_queries)
+    dense_ms, dense_flops = run([dense], [])
+    return {"c3_warm_ttft_l1_ms": c3_ms, "c3_warm_flops": c3_flops,
+            "dense_causal_ttft_l1_ms": dense_ms, "dense_causal_flops": dense_flops,
+            "dense_causal_tflops": dense_flops / (dense_ms / 1e3) / 1e12,
+            "note": "one layer; C3 = configs[2] after its warm-up query (75% fragment hits); dense = "
+                    "ordinary causal prefill of the same 17,152 tokens"}
 
 
 C5_PARAMS = dict(n_queries=64, n_frag=16, frag_len=1024, pool=64, shared_per_query=8, n_prefix=512, n_cross=256)
