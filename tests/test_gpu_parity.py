@@ -298,3 +298,38 @@ def test_sub_range_calls(cuda_dev):
     check(oj, jo, False, "sub-range join O")
     plan.release()
     ctx.close()
+
+
+def test_bf16_d64_block128(cuda_dev):
+    # d = 64 (8-slot K / 4-slot V rings of 8 KB sub-tiles) with 128-token blocks (a 64-key
+    # sub-tile is half a block: TMA boxes at row offset 0 / 64)
+    sh = inputs.Shape(hq=8, hkv=2, d=64, block_size=128, vocab=1024)
+    w = inputs.make_rag(111, sh, 200, 3, [300, 129, 257], 190)
+    run_and_check(w, cuda_dev)
+
+
+def test_full_size_c4_sampled_rows(cuda_dev):
+    """configs[3] (judge/generator, 2B shape, 8 x 2048 + 512) at full size; sampled outputs."""
+    import torch
+
+    w = inputs.c4()
+    s = w.shape
+    ctx = spanq.Context(s, 1024, device=0, max_position=1 << 15, out_dtype="fp32")
+    res = runner.run_pass(ctx, w.queries, [runner.device_tables(s, 0, w.seed, cuda_dev)], cuda_dev)
+    torch.cuda.synchronize()
+    eq, ek, ev = inputs.layer_tables(s, 0, w.seed)
+    q = w.queries[0]
+    g = np.random.default_rng(8)
+    heads = [0, 3, s.hq - 1]
+    rows = g.choice(len(q.cross), 12, replace=False)
+    jo, _ = oatt.join_rows(q.prefix, q.fragments, q.cross, eq, ek, ev, s.rope_base, rows, heads)
+    check(res.o_join[torch.from_numpy(rows).to(cuda_dev)][:, heads], jo, False, "C4 join sampled")
+    view = res.view
+    si = int(view["jobs"][5])
+    toks = runner.segment_tokens(view, w.queries, si)
+    j = list(view["jobs"]).index(si)
+    r = g.choice(len(toks), 10, replace=False)
+    eo, _ = oatt.segment_causal(toks, eq, ek, ev, s.rope_base, r, heads)
+    off = int(view["job_row_off"][j])
+    check(res.o_prefill[torch.from_numpy(off + r).to(cuda_dev)][:, heads], eo, False, "C4 prefill sampled")
+    ctx.close()
