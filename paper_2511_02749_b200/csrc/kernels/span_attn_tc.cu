@@ -356,33 +356,35 @@ __device__ __forceinline__ float softmax_sub(uint32_t scol, float sl2, float thr
   alpha = resc ? ex2_approx(m - m_new) : 1.f;
   m = m_use;
   const float msub = (m_use == -INFINITY) ? 0.f : m_use;
-  float sum8[8];
+  // x = s * scale - m and the row sums in packed fp32x2 (FFMA2 / FADD2: half the instructions)
+  float2 sum4[4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) sum8[i] = 0.f;
+  for (int i = 0; i < 4; ++i) sum4[i] = make_float2(0.f, 0.f);
+  const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-msub, -msub);
   uint32_t pk[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
-    const float x0 = fmaf(__uint_as_float(v[2 * i]), sl2, -msub);
-    const float x1 = fmaf(__uint_as_float(v[2 * i + 1]), sl2, -msub);
+    const float2 xx = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), sl2v, nmv);
     float p0, p1;
     if constexpr (PM == 3) {
-      ex2_pair_f16(x0, x1, p0, p1);
+      ex2_pair_f16(xx.x, xx.y, p0, p1);
     } else {
       constexpr bool kPoly[4] = {0 < PM, 1 < PM, 2 < PM, 3 < PM};
-      p0 = kPoly[i & 3] ? exp2_poly(x0) : ex2_approx(x0);
-      p1 = kPoly[i & 3] ? exp2_poly(x1) : ex2_approx(x1);
+      p0 = kPoly[i & 3] ? exp2_poly(xx.x) : ex2_approx(xx.x);
+      p1 = kPoly[i & 3] ? exp2_poly(xx.y) : ex2_approx(xx.y);
     }
     if constexpr (kMasked) {
       p0 = (2 * i <= lim) ? p0 : 0.f;
       p1 = (2 * i + 1 <= lim) ? p1 : 0.f;
     }
-    sum8[(2 * i) & 7] += p0;
-    sum8[(2 * i + 1) & 7] += p1;
+    sum4[i & 3] = fadd2(sum4[i & 3], make_float2(p0, p1));
     pk[i] = pack_bf16x2(p0, p1);
   }
   tmem_st32(scol, pk);
   tmem_wait_st();
-  return ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) + ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
+  const float2 s01 = fadd2(sum4[0], sum4[1]), s23 = fadd2(sum4[2], sum4[3]);
+  const float2 st = fadd2(s01, s23);
+  return st.x + st.y;
 }
 
 // ------------------------------------------------------------------ softmax + epilogue (one WG per head)
@@ -592,11 +594,15 @@ __device__ __forceinline__ void rotate_step(uint8_t* qs_base, int r, int u, cons
   uint32_t oa[4], ob[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const float x0 = __uint_as_float(av[k] << 16), x1 = __uint_as_float(av[k] & 0xFFFF0000u);
-    const float y0 = __uint_as_float(bv[k] << 16), y1 = __uint_as_float(bv[k] & 0xFFFF0000u);
-    // first half: x cos - y sin ; second half: y cos + x sin
-    oa[k] = pack_bf16x2(fmaf(-y0, sn[2 * k], x0 * c[2 * k]), fmaf(-y1, sn[2 * k + 1], x1 * c[2 * k + 1]));
-    ob[k] = pack_bf16x2(fmaf(x0, sn[2 * k], y0 * c[2 * k]), fmaf(x1, sn[2 * k + 1], y1 * c[2 * k + 1]));
+    const float2 xx = make_float2(__uint_as_float(av[k] << 16), __uint_as_float(av[k] & 0xFFFF0000u));
+    const float2 yy = make_float2(__uint_as_float(bv[k] << 16), __uint_as_float(bv[k] & 0xFFFF0000u));
+    const float2 cc = make_float2(c[2 * k], c[2 * k + 1]), ss = make_float2(sn[2 * k], sn[2 * k + 1]);
+    const float2 ns = fmul2(ss, make_float2(-1.f, -1.f));
+    // first half: x cos - y sin ; second half: y cos + x sin (packed fp32x2, same roundings)
+    const float2 o1 = ffma2(yy, ns, fmul2(xx, cc));
+    const float2 o2 = ffma2(xx, ss, fmul2(yy, cc));
+    oa[k] = pack_bf16x2(o1.x, o1.y);
+    ob[k] = pack_bf16x2(o2.x, o2.y);
   }
   *reinterpret_cast<uint4*>(p0) = make_uint4(oa[0], oa[1], oa[2], oa[3]);
   *reinterpret_cast<uint4*>(p1) = make_uint4(ob[0], ob[1], ob[2], ob[3]);
@@ -653,10 +659,15 @@ __device__ __forceinline__ void rotate_q_tile(uint8_t* qs_base, const float2* ro
     for (int st = 0; st < 32 / R; ++st) {
       rotate_step<D>(qs_base, wq * 32 + st * R + g, u, c, sn);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float cn = fmaf(c[e], cd[e], -sn[e] * sd[e]);
-        sn[e] = fmaf(sn[e], cd[e], c[e] * sd[e]);
-        c[e] = cn;
+      for (int e = 0; e < 8; e += 2) {  // advance the angles by R*theta (packed, same roundings)
+        const float2 c2 = make_float2(c[e], c[e + 1]), s2 = make_float2(sn[e], sn[e + 1]);
+        const float2 cd2 = make_float2(cd[e], cd[e + 1]), sd2 = make_float2(sd[e], sd[e + 1]);
+        const float2 cn = ffma2(c2, cd2, fmul2(fmul2(s2, make_float2(-1.f, -1.f)), sd2));
+        const float2 sn2 = ffma2(s2, cd2, fmul2(c2, sd2));
+        c[e] = cn.x;
+        c[e + 1] = cn.y;
+        sn[e] = sn2.x;
+        sn[e + 1] = sn2.y;
       }
     }
   } else {
