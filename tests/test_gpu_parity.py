@@ -25,7 +25,7 @@ def _np(t):
     return t.float().cpu().numpy().astype(np.float64)
 
 
-def check(got, exp, fp32, what, abs_tol=BF16_MAX_ABS, bf16_out=False, rel_tol=BF16_REL_L2):
+def check(got, exp, fp32, what, abs_tol=BF16_MAX_ABS, bf16_out=False, rel_tol=BF16_REL_L2):  # noqa: ARG001
     g = _np(got)
     if not exp.size:
         return 0.0, 0.0
@@ -34,7 +34,10 @@ def check(got, exp, fp32, what, abs_tol=BF16_MAX_ABS, bf16_out=False, rel_tol=BF
     if fp32:
         assert d.max() <= FP32_MAX_ABS, f"{what}: max abs {d.max():.3e}"
         return d.max(), rel
-    bound = abs_tol + (2.0 ** -9 * np.abs(exp) if bf16_out else 0.0)
+    # bf16 compute: Q, K (cache) and P are bf16, so even an exactly rounded computation errs by
+    # up to ~2^-9 |O| on peaky rows (reading R29: the fp64 emulation of those roundings alone
+    # reaches 1.03e-2 on the smoke case); the bar is 1e-2 + half a bf16 ulp of |O_ref|
+    bound = abs_tol + 2.0 ** -9 * np.abs(exp)
     assert (d <= bound).all() and rel <= rel_tol, \
         f"{what}: max abs {d.max():.3e} (worst err/bound {np.max(d / bound):.3f}) rel-L2 {rel:.3e}"
     return d.max(), rel
@@ -332,4 +335,51 @@ def test_full_size_c4_sampled_rows(cuda_dev):
     eo, _ = oatt.segment_causal(toks, eq, ek, ev, s.rope_base, r, heads)
     off = int(view["job_row_off"][j])
     check(res.o_prefill[torch.from_numpy(off + r).to(cuda_dev)][:, heads], eo, False, "C4 prefill sampled")
+    ctx.close()
+
+
+def test_bf16_matches_rounding_emulation(cuda_dev):
+    # The bf16 kernel is as accurate as its formats allow: against an fp64 computation that only
+    # rounds the rotated Q, the cached K and P to bf16 (test-side emulation built on the oracle's
+    # RoPE), the fragment-prefill outputs agree to 4e-3 (measured 2.5e-3: the kernel's P is taken
+    # against a running max that may lag by up to 2^8, so its roundings differ) — while both sit
+    # ~1e-2 from the exact fp64 result on this case (reading R29)
+    import torch
+
+    from oracle import rope as orope
+
+    s = inputs.Shape(**inputs.SHAPE_8B, block_size=64, vocab=2048)
+    w = inputs.make_rag(11, s, 130, 3, [200, 128, 77], 140)
+    ctx = spanq.Context(s, 1024, device=0, max_position=1 << 14, out_dtype="fp32")
+    res = runner.run_pass(ctx, w.queries, [runner.device_tables(s, 0, w.seed, cuda_dev)], cuda_dev)
+    torch.cuda.synchronize()
+    eq, ek, ev = inputs.layer_tables(s, 0, w.seed)
+    bf = lambda x: torch.from_numpy(np.asarray(x, np.float32)).to(torch.bfloat16).double().numpy()
+    view = res.view
+    worst_emul = worst_exact = 0.0
+    for j, si in enumerate(view["jobs"]):
+        toks = runner.segment_tokens(view, w.queries, int(si))
+        cb = int(view["seg_compute_begin"][si])
+        L = len(toks)
+        pos = np.arange(L)[:, None]
+        Q = orope.rope(eq[toks].astype(np.float64), pos, s.rope_base)
+        K = np.repeat(orope.rope(ek[toks].astype(np.float64), pos, s.rope_base), s.hq // s.hkv, axis=1)
+        V = np.repeat(ev[toks].astype(np.float64), s.hq // s.hkv, axis=1)
+        mask = np.tril(np.ones((L, L), bool))
+
+        def attn(Qx, Kx, round_p):
+            S = np.where(mask[None], np.einsum("qhd,khd->hqk", Qx, Kx) / np.sqrt(s.d), -np.inf)
+            P = np.exp(S - S.max(-1, keepdims=True))
+            lsum = P.sum(-1, keepdims=True)
+            P = bf(P) if round_p else P
+            return np.einsum("hqk,khd->qhd", P, V) / lsum.transpose(1, 0, 2)
+
+        r0, r1 = int(view["job_row_off"][j]), int(view["job_row_off"][j + 1])
+        got = res.o_prefill[r0:r1].double().cpu().numpy()
+        emul = attn(bf(Q), bf(K), True)[cb:]
+        exact = attn(Q, K, False)[cb:]
+        worst_emul = max(worst_emul, float(np.abs(got - emul).max()))
+        worst_exact = max(worst_exact, float(np.abs(got - exact).max()))
+    assert worst_emul <= 4e-3, worst_emul
+    assert worst_exact > 5e-3  # the emulation, not luck, explains the distance to fp64
     ctx.close()
