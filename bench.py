@@ -231,9 +231,13 @@ def main():
     kv_bytes = view["prefill_kv_bytes"] + view["join_kv_bytes"]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
+    plan_host_ms = []
+
     def step(layers=L, inp=(qp, kp, vp, qj, kj, vj), d2h=None):
         ctx.evict_all()  # cold cache
+        t0 = time.perf_counter()
         plan = ctx.plan(w.queries, stream=stream)
+        plan_host_ms.append((time.perf_counter() - t0) * 1e3)
         for layer in range(layers):
             plan.prefill(layer, inp[0], inp[1], inp[2], op, lp, stream=stream)
             plan.join(layer, inp[3], inp[4], inp[5], oj, lj, stream=stream)
@@ -326,6 +330,7 @@ def main():
         "config": c2_config(L, world, args.out_dtype, s.block_size),
         "ttft_ms": ms_per_step,
         "ttft_l1_ms": statistics.median(l1_ms),
+        "plan_host_ms": statistics.median(plan_host_ms),
         "step_ms_p50": statistics.median(step_ms), "step_ms_p99": float(np.percentile(step_ms, 99)),
         "flops_per_step": flops, "flops_per_layer": flops_layer,
         "roofline": {"kernel": "span_attn_tc (fragment+prefix prefill, K2)", "bound": "tensor",

@@ -204,6 +204,12 @@ typedef struct {
 spq_status spq_get_stats(const spq_ctx *ctx, spq_stats *out); /* hit rate = hit/input tokens */
 /* Drop every unpinned resident block (cold-cache reset). */
 spq_status spq_evict_all(spq_ctx *ctx);
+/* Copy the K and V pages of blocks ids[0..n) of one layer out of the pool (inspection / parity,
+ * SURVEY §8(b)): k and v are caller-owned device buffers [n][Hkv][bs][d] in the pool dtype,
+ * stream-ordered on `stream`. SPQ_EINVAL on a null buffer or an id outside [0, num_blocks),
+ * SPQ_ESTATE on a host-only ctx or a bad layer. */
+spq_status spq_read_blocks(spq_ctx *ctx, int32_t layer, const int32_t *block_ids /*host*/, int64_t n,
+                           void *k, void *v, void *stream);
 
 /* Instrumentation: kernel launches issued by this ctx so far, and the CUDA events bracketing
  * the most recent attention launch (for roofline timing on the launching stream). */

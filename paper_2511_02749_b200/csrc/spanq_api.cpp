@@ -928,6 +928,28 @@ spq_status spq_evict_all(spq_ctx* c) {
   return SPQ_OK;
 }
 
+spq_status spq_read_blocks(spq_ctx* c, int32_t layer, const int32_t* ids, int64_t n, void* k, void* v,
+                           void* stream) {
+  if (c == nullptr || (n > 0 && (ids == nullptr || k == nullptr || v == nullptr)))
+    return fail(SPQ_EINVAL, "null argument");
+  if (!is_gpu(c)) return fail(SPQ_ESTATE, "host-only ctx (device < 0) has no pool");
+  if (layer < 0 || layer >= c->cfg.num_layers) return fail(SPQ_ESTATE, "layer out of range");
+  for (int64_t i = 0; i < n; ++i)
+    if (ids[i] < 0 || ids[i] >= c->cfg.num_blocks) return fail(SPQ_EINVAL, "block id out of range");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  const size_t blk = static_cast<size_t>(c->cfg.num_kv_heads) * c->cfg.block_size * c->cfg.head_dim * elt_size(c);
+  const size_t layer_off = static_cast<size_t>(layer) * c->cfg.num_blocks * blk;
+  for (int64_t i = 0; i < n; ++i) {
+    const size_t src = layer_off + static_cast<size_t>(ids[i]) * blk;
+    CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(k) + i * blk, static_cast<const uint8_t*>(c->cfg.k_pool) + src, blk,
+                             cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(v) + i * blk, static_cast<const uint8_t*>(c->cfg.v_pool) + src, blk,
+                             cudaMemcpyDeviceToDevice, st));
+  }
+  return SPQ_OK;
+}
+
 spq_status spq_launch_count(const spq_ctx* c, int64_t* n) {
   if (c == nullptr || n == nullptr) return fail(SPQ_EINVAL, "null argument");
   *n = c->launches;

@@ -104,6 +104,8 @@ SIGNATURES = {
     "spq_plan_release": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "spq_get_stats": (C.c_int, [C.c_void_p, C.POINTER(spq_stats)]),
     "spq_evict_all": (C.c_int, [C.c_void_p]),
+    "spq_read_blocks": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                  C.c_void_p]),
     "spq_launch_count": (C.c_int, [C.c_void_p, _I64P]),
     "spq_last_attn_ms": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "spq_set_timing": (C.c_int, [C.c_void_p, C.c_int32]),
@@ -323,6 +325,19 @@ class Context:
         ids = np.zeros(len(d), np.int32)
         _check(lib().spq_insert(self.handle, d.ctypes.data, nt.ctypes.data, len(d), ids.ctypes.data))
         return ids
+
+    def read_blocks(self, layer: int, block_ids, stream=None):
+        """K and V pages of the given blocks of one layer: two device tensors [n, Hkv, bs, d]."""
+        import torch
+
+        ids = np.ascontiguousarray(block_ids, dtype=np.int32)
+        s = self.shape
+        dt = torch.bfloat16 if s.dtype == "bf16" else torch.float32
+        k = torch.empty((len(ids), s.hkv, s.block_size, s.d), dtype=dt, device=f"cuda:{self.device}")
+        v = torch.empty_like(k)
+        _check(lib().spq_read_blocks(self.handle, layer, ids.ctypes.data, len(ids), _ptr(k), _ptr(v),
+                                     _stream_ptr(stream)))
+        return k, v
 
     def stats(self) -> Dict[str, int]:
         s = spq_stats()

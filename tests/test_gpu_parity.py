@@ -383,3 +383,22 @@ def test_bf16_matches_rounding_emulation(cuda_dev):
     assert worst_emul <= 4e-3, worst_emul
     assert worst_exact > 5e-3  # the emulation, not luck, explains the distance to fp64
     ctx.close()
+
+
+def test_read_blocks(cuda_dev):
+    import torch
+
+    sh = inputs.Shape(hq=8, hkv=2, d=128, block_size=32, vocab=512, layers=2)
+    w = inputs.make_rag(112, sh, 40, 2, [100, 70], 30)
+    ctx = spanq.Context(sh, 256, device=0)
+    res = runner.run_pass(ctx, w.queries, [runner.device_tables(sh, l, w.seed, cuda_dev) for l in range(2)], cuda_dev)
+    ids = res.view["blocks"][:5]
+    for layer in range(2):
+        k, v = ctx.read_blocks(layer, ids)
+        torch.cuda.synchronize()
+        assert torch.equal(k, ctx.k_pool[layer, torch.from_numpy(ids.astype(np.int64)).to(cuda_dev)])
+        assert torch.equal(v, ctx.v_pool[layer, torch.from_numpy(ids.astype(np.int64)).to(cuda_dev)])
+    with pytest.raises(spanq.SpanqError):
+        ctx.read_blocks(0, [300])
+    res.plan.release()
+    ctx.close()
