@@ -18,6 +18,8 @@ Modules
              [P:94; SURVEY §8(c) R8-R13]
   attention  dense masked brute force (the plain definition) and the segment-wise form
              (fragments causal at span-local positions, join at global positions) [P:672]
+  cidra      block repositioning (ReRoPE moves, chains, cycles, duplicates), the plain
+             out-of-place definition                                          [P:610, P:618-627]
 
 Parity status per function is listed in DESIGN.md §"Oracle pins"; every function here is pinned
 by a `-m "not gpu"` test in tests/test_oracle_*.py except where its docstring says
