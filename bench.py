@@ -320,6 +320,9 @@ def main():
             locality = measure_locality(ctx, s, tab, dev, stream, flush, args)
 
     peak_burst, peak_sust, hbm, peak_src = peaks()
+    # ---- CIDRA: in-place repositioning of the C2 query's blocks, all layers
+    with torch.cuda.stream(stream):
+        reposition = measure_reposition(ctx, s, stream, flush, len(view["blocks"]), hbm)
     pre_ms = statistics.median(a for a, _ in attn_ms)
     join_ms = statistics.median(b for _, b in attn_ms)
     achieved = view["prefill_flops"] / (pre_ms / 1e3) / 1e12
@@ -347,6 +350,7 @@ def main():
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": e2e_total / args.steps},
     }
+    line["reposition"] = reposition
     if locality is not None:
         locality["c2_cold_ttft_l1_ms"] = line["ttft_l1_ms"]
         locality["dense_over_span_ttft"] = locality["dense_causal_ttft_l1_ms"] / line["ttft_l1_ms"]
@@ -358,6 +362,40 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def measure_reposition(ctx, s, stream, flush, n_blocks, hbm_gbs, reps: int = 10):
+    """CIDRA (K8): a random permutation of `n_blocks` pool blocks (C2's block count),
+    each moved with a random position shift in [-8192, 8192], in place over all L layers — cycles
+    of every length, the worst case for an in-place algorithm. Device time per call (host
+    schedule + H2D of the ops + one kernel), L2 flushed before each; algorithmic bytes = read +
+    write of K and V of every moved block in every layer."""
+    import torch
+
+    g = np.random.default_rng(7)
+    dst = g.permutation(n_blocks).astype(np.int32)
+    src = np.arange(n_blocks, dtype=np.int32)
+    delta = g.integers(-8192, 8193, size=n_blocks).astype(np.int32)
+    st = ctx.reposition(src, dst, delta, stream=stream)  # warm-up
+    ms = []
+    for _ in range(reps):
+        flush.zero_()
+        stream.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ctx.reposition(src, dst, delta, stream=stream)
+        b.record(stream)
+        stream.synchronize()
+        ms.append(a.elapsed_time(b))
+    ctx.evict_all()  # the moved blocks no longer hold what the store's index says
+    t = statistics.median(ms)
+    elt = 2 if s.dtype == "bf16" else 4
+    nbytes = 2 * 2 * n_blocks * s.layers * s.hkv * s.block_size * s.d * elt
+    return {"kernel": "cidra (K8)", "moves": n_blocks, "layers": s.layers, "cycles": st["cycles"],
+            "components": st["components"], "ms": t, "tokens_per_ms": n_blocks * s.block_size / t,
+            "achieved_gbs": nbytes / (t / 1e3) / 1e9, "peak_gbs": hbm_gbs,
+            "frac": nbytes / (t / 1e3) / 1e9 / hbm_gbs, "bytes": nbytes,
+            "note": "paper: up to 500 tokens/ms on its own hardware and model (P:648), context only"}
 
 
 def measure_locality(ctx, s, tab, dev, stream, flush, args, reps: int = 5):

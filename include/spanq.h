@@ -211,6 +211,33 @@ spq_status spq_evict_all(spq_ctx *ctx);
 spq_status spq_read_blocks(spq_ctx *ctx, int32_t layer, const int32_t *block_ids /*host*/, int64_t n,
                            void *k, void *v, void *stream);
 
+/* ------------------------------------------------------------------ CIDRA repositioning
+ * PAPER.md §5.5.1 "Concurrent In-place Duplicating ReRoPE": for consumers that need
+ * cached KV at absolute positions (the span path itself never does — the join counter-rotates Q,
+ * SURVEY §8(f) f2). Move i: block dst[i] of every layer in [layer_begin, layer_end) ends
+ * up holding the ORIGINAL content of block src[i], K re-encoded delta[i] positions later (ReRoPE
+ * P:610, rotate-half pairs; all tokens of a block share delta) and V copied — the result of the
+ * out-of-place definition (SPEC), reached in place: the move graph is split into
+ * independent components (trees, and cycles with trees attached); inside one a block is
+ * overwritten only after every move reading it, and a cycle rotates through one scratch slot.
+ * A source may feed several destinations ("duplication"); a destination appears once.
+ * src/dst/delta are HOST arrays of n entries; the pools are the ctx's; stream-ordered on
+ * `stream`. Blocks referenced by a live plan are the caller's to avoid. SPQ_EINVAL: null array,
+ * id outside [0, num_blocks), a destination written twice, |delta| >= max_position, head_dim not
+ * 64/128; SPQ_ESTATE: host-only ctx or bad layer range; SPQ_ECUDA: launch failure. */
+typedef struct {
+  int64_t moves, components, cycles, duplicates, ops, max_component_ops;
+} spq_cidra_stats;
+spq_status spq_reposition(spq_ctx *ctx, const int32_t *src, const int32_t *dst, const int32_t *delta, int64_t n,
+                          int32_t layer_begin, int32_t layer_end, void *stream, spq_cidra_stats *stats /*or null*/);
+/* The in-place schedule spq_reposition runs (host only; inspection / tests): ops[cap][4] =
+ * {dst, src, delta, mode} with mode 0: dst <- R(src), 1: scratch <- src, 2: dst <- R(scratch);
+ * comp_off[comp_cap] = component boundaries (n_comp + 1 entries). SPQ_EINVAL as above, or when
+ * a capacity is too small (*n_ops / *n_comp still report the sizes needed). */
+spq_status spq_cidra_schedule(const spq_ctx *ctx, const int32_t *src, const int32_t *dst, const int32_t *delta,
+                              int64_t n, int32_t *ops, int64_t cap, int64_t *n_ops, int32_t *comp_off,
+                              int64_t comp_cap, int64_t *n_comp, spq_cidra_stats *stats /*or null*/);
+
 /* Instrumentation: kernel launches issued by this ctx so far, and the CUDA events bracketing
  * the most recent attention launch (for roofline timing on the launching stream). */
 spq_status spq_launch_count(const spq_ctx *ctx, int64_t *n);

@@ -74,6 +74,11 @@ void schedule(const std::vector<double>& item_cost, int units, int num_sms, Attn
 constexpr double kItemOverhead = 1.0;   // q-prep + epilogue, in KV-tile units
 constexpr double kSplitOverhead = 0.5;  // partial write + combine read, per split
 constexpr double kSubOverhead = 3.0;    // per work item, in 64-key sub-tiles (epilogue + Q + pipeline fill)
+// per Q-rotation change inside a join piece, in sub-tiles (tuning knob SPANQ_EPOCH_COST)
+const double kEpochCost = [] {
+  const char* e = std::getenv("SPANQ_EPOCH_COST");
+  return e ? std::atof(e) : 1.5;
+}();
 
 }  // namespace
 
@@ -160,15 +165,18 @@ void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_en
   std::vector<int32_t> sub(w->tiles.size());
   double total = 0;
   for (size_t t = 0; t < w->tiles.size(); ++t) sub[t] = w->tiles[t].n_valid > 64 ? 2 : 1;
-  for (const QTile& q : qt)
-    for (int t = q.tb; t < q.te; ++t) total += static_cast<double>(sub[t]) * o.units;
   const int grid = o.num_sms;
   struct Piece {
     int cta, t0, t1;
   };
-  // prefix sums of sub-tile counts per tile (tiles of one q tile are contiguous)
+  // prefix sums of the cost per tile (tiles of one q tile are contiguous): its sub-tiles, plus
+  // kEpochCost where the Q rotation changes (a new fragment segment: the Q tiles are reloaded and
+  // re-rotated inside the piece)
   std::vector<double> pre(w->tiles.size() + 1, 0.0);
-  for (size_t t = 0; t < w->tiles.size(); ++t) pre[t + 1] = pre[t] + sub[t];
+  for (size_t t = 0; t < w->tiles.size(); ++t)
+    pre[t + 1] = pre[t] + sub[t] +
+                 (t > 0 && w->tiles[t].rot_delta != w->tiles[t - 1].rot_delta ? kEpochCost : 0.0);
+  for (const QTile& q : qt) total += (pre[q.te] - pre[q.tb]) * o.units;
   // greedy cut at cost budget `target` per CTA; returns the CTAs used (unbounded), pieces per pair
   auto cut = [&](double target, std::vector<std::vector<Piece>>* out) {
     int cta = 0;

@@ -1,0 +1,148 @@
+// cidra.cu — K8: CIDRA in-place block repositioning (§5.5.1).
+//
+// Executes the host schedule (host/cidra.h): per component, a sequence of ops
+//   mode 0: block dst <- R(block src, delta)    mode 1: tmp <- block src    mode 2: dst <- R(tmp, delta)
+// where R rotates K by delta positions (ReRoPE P:610: k' = rope(k, +delta), rotate-half pairs
+// (i, i + d/2), reading R15) and copies V. The order inside a component is what makes the
+// update safe in place; components are independent.
+//
+// B200 design: HBM-bound element-parallel work, no shared memory and no block-level sync.
+// Every element of a (block, layer, kv head) tile is touched by the same thread in every op of
+// its component (the same row t and columns in each block), so the in-place dependencies are
+// plain program order inside one thread — the "scratch block" of a cycle is a few registers.
+// CTA (component, layer x kv head); a thread owns rows t and a 16-byte unit u of the first half
+// of d plus its rotate-half partner unit in the second half (8 pairs for bf16, 4 for fp32):
+// 128-bit loads/stores, a warp covers whole rows contiguously. cos/sin of delta * theta_i come
+// from the ctx's fp64-built table at |delta| (sin negated for delta < 0).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "launch.h"
+
+namespace spq {
+namespace {
+
+template <typename T>
+struct V16;
+template <>
+struct V16<__nv_bfloat16> {
+  static constexpr int N = 8;  // elements per 16-byte unit
+  __device__ static void unpack(const uint4& u, float (&f)[8]) {
+    const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 t = __bfloat1622float2(p[i]);
+      f[2 * i] = t.x;
+      f[2 * i + 1] = t.y;
+    }
+  }
+  __device__ static uint4 pack(const float (&f)[8]) {
+    uint4 u;
+    __nv_bfloat162* p = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) p[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    return u;
+  }
+};
+template <>
+struct V16<float> {
+  static constexpr int N = 4;
+  __device__ static void unpack(const uint4& u, float (&f)[4]) {
+    f[0] = __uint_as_float(u.x);
+    f[1] = __uint_as_float(u.y);
+    f[2] = __uint_as_float(u.z);
+    f[3] = __uint_as_float(u.w);
+  }
+  __device__ static uint4 pack(const float (&f)[4]) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]), __float_as_uint(f[3]));
+  }
+};
+
+template <typename T, int D>
+__global__ void __launch_bounds__(256) cidra_kernel(const int4* __restrict__ ops, const int32_t* __restrict__ comp_off,
+                                                    T* k_pool, T* v_pool, const float2* __restrict__ rope, int hkv,
+                                                    int bs, int64_t nblk, int layer0) {
+  constexpr int N = V16<T>::N;
+  constexpr int U = D / 2 / N;  // units per half row
+  const int comp = blockIdx.x;
+  const int layer = layer0 + static_cast<int>(blockIdx.y) / hkv;
+  const int h = static_cast<int>(blockIdx.y) % hkv;
+  const int o0 = comp_off[comp], o1 = comp_off[comp + 1];
+  // element offset of (block b, this layer/head, row t, column c): ((layer*nblk + b)*hkv + h)*bs*D + t*D + c
+  const int64_t lh = static_cast<int64_t>(layer) * nblk;
+  auto tile = [&](int32_t b) { return ((lh + b) * hkv + h) * static_cast<int64_t>(bs) * D; };
+  for (int idx = threadIdx.x; idx < bs * U; idx += blockDim.x) {
+    const int t = idx / U, u = idx % U;
+    const int c0 = t * D + u * N;  // first-half unit; partner at + D/2
+    uint4 tk0 = make_uint4(0, 0, 0, 0), tk1 = tk0, tv0 = tk0, tv1 = tk0;  // the cycle's scratch
+    for (int o = o0; o < o1; ++o) {
+      const int4 op = ops[o];  // {dst, src, delta, mode}
+      uint4 k0, k1, v0, v1;
+      if (op.w == 2) {
+        k0 = tk0, k1 = tk1, v0 = tv0, v1 = tv1;
+      } else {
+        const int64_t s = tile(op.y) + c0;
+        k0 = *reinterpret_cast<const uint4*>(k_pool + s);
+        k1 = *reinterpret_cast<const uint4*>(k_pool + s + D / 2);
+        v0 = *reinterpret_cast<const uint4*>(v_pool + s);
+        v1 = *reinterpret_cast<const uint4*>(v_pool + s + D / 2);
+        if (op.w == 1) {
+          tk0 = k0, tk1 = k1, tv0 = v0, tv1 = v1;
+          continue;
+        }
+      }
+      float x[N], y[N];
+      V16<T>::unpack(k0, x);
+      V16<T>::unpack(k1, y);
+      const int ad = op.z < 0 ? -op.z : op.z;
+      const float sg = op.z < 0 ? -1.f : 1.f;
+      const float2* cs = rope + static_cast<int64_t>(ad) * (D / 2) + u * N;
+#pragma unroll
+      for (int e = 0; e < N; ++e) {
+        const float2 a = __ldg(cs + e);
+        const float sn = sg * a.y;
+        const float xr = x[e] * a.x - y[e] * sn;  // first half: x cos - y sin
+        const float yr = y[e] * a.x + x[e] * sn;  // second half: y cos + x sin
+        x[e] = xr;
+        y[e] = yr;
+      }
+      const int64_t d = tile(op.x) + c0;
+      *reinterpret_cast<uint4*>(k_pool + d) = V16<T>::pack(x);
+      *reinterpret_cast<uint4*>(k_pool + d + D / 2) = V16<T>::pack(y);
+      *reinterpret_cast<uint4*>(v_pool + d) = v0;
+      *reinterpret_cast<uint4*>(v_pool + d + D / 2) = v1;
+    }
+  }
+}
+
+template <typename T, int D>
+cudaError_t launch_t(const CidraArgs& a, cudaStream_t st) {
+  const dim3 grid(static_cast<unsigned>(a.n_comp), static_cast<unsigned>((a.layer_end - a.layer_begin) * a.hkv));
+  const int units = a.bs * (D / 2 / V16<T>::N);
+  const int threads = units >= 256 ? 256 : ((units + 31) / 32) * 32;
+  cidra_kernel<T, D><<<grid, threads, 0, st>>>(a.ops, a.comp_off, static_cast<T*>(a.k_pool), static_cast<T*>(a.v_pool),
+                                               a.rope, a.hkv, a.bs, a.nblk, a.layer_begin);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_cidra(const CidraArgs& a, cudaStream_t st) {
+  if (a.n_comp == 0 || a.layer_end <= a.layer_begin) return cudaSuccess;
+  if (a.fp32) {
+    switch (a.d) {
+      case 64: return launch_t<float, 64>(a, st);
+      case 128: return launch_t<float, 128>(a, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  switch (a.d) {
+    case 64: return launch_t<__nv_bfloat16, 64>(a, st);
+    case 128: return launch_t<__nv_bfloat16, 128>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace spq

@@ -60,6 +60,7 @@ struct AttnArgs {
   int max_pos;
   bool out_fp32;  // o is fp32 (else ctx dtype)
   bool paired;    // tcgen05 path: work codes are (item, GQA head pair) — see span_attn_tc.cu
+  bool join;      // tcgen05 path: a join launch (2-deep Q ring, register epilogue)
   int poly_mask;  // tcgen05 path: share of exp2 on the FMA pipe, in quarters (0..4)
   float rescale_threshold;  // tcgen05 path: conditional O rescale threshold (log2 units, 8)
   long long* dbg_trace;     // profiling only: CTA-0 event timeline (null = off)
@@ -91,5 +92,19 @@ struct KvExchangeArgs {
   int scatter;  // 0: pool -> buf (pack), 1: buf -> pool (unpack)
 };
 cudaError_t launch_kv_exchange(const KvExchangeArgs& a, cudaStream_t st);
+
+struct CidraArgs {
+  const int4* ops;         // device [n_ops] {dst, src, delta, mode} (host/cidra.h)
+  const int32_t* comp_off; // device [n_comp + 1]
+  int32_t n_comp;
+  void* k_pool;
+  void* v_pool;
+  const float2* rope;      // [max_pos][d/2] (cos, sin)
+  int hkv, d, bs;
+  int64_t nblk;
+  int layer_begin, layer_end;
+  bool fp32;
+};
+cudaError_t launch_cidra(const CidraArgs& a, cudaStream_t st);  // in-place repositioning (K8)
 
 }  // namespace spq

@@ -8,27 +8,27 @@
 // masked by n_valid and, in causal tiles, key_pos0 + t > pos[r] (block-diagonal fragment
 // attention). O, LSE are written final or as fp32 split-KV partials (combine.cu).
 //
-// B200 design — one persistent CTA per SM, 512 threads, ~225 KB smem, 512 TMEM columns:
+// B200 design — one persistent CTA per SM, 512 threads, ~225 KB smem, 512 TMEM columns
+// (DESIGN.md §6 has the measurements behind each choice):
 //   * the two q heads h, h+1 of a GQA group share every K/V tile, so one CTA runs them as two
-//     M=128 Q tiles (A, B) against the same TMA-loaded K/V (half the K/V traffic per FLOP)
-//     and ping-pongs them: per KV tile the MMA warp issues PV_A(j-1), S_A(j), PV_B(j-1),
-//     S_B(j), so softmax A(j) overlaps PV_B(j-1)+S_B(j) on the tensor core and vice versa.
-//   * TMEM: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512) (fp32); P (bf16) is written
-//     over the first 64 columns of its S tile and consumed by the TS-form MMA (A from TMEM).
-//     PV_x(j-1) is issued before S_x(j), so when softmax x sees S_x(j) its O_x is stable and
-//     the (rare) rescale needs no extra barrier.
-//   * K/V: a TMA ring (K_j, V_j alternate; 4 slots at d=128, 8 at d=64), SWIZZLE_128B boxes
-//     {64 cols, bs rows} from one 2D tensor map over the whole pool (block id -> row): the
-//     paged gather is done by TMA; K_{j+1} is issued >= 1 tile ahead of its S MMA.
-//   * Q: a 3-slot ring prepared by a dedicated warpgroup (load pre-RoPE q, rotate with the
-//     fp64-built fp32 cos/sin table, write the SWIZZLE_128B K-major tile). An epoch (a work item
-//     or a change of rot_delta) takes slots (2e mod 3, 2e+1 mod 3): head A's tile goes to the
-//     slot left free, head B's to the slot of the previous epoch's A, released right after the
-//     last S_A MMA of that epoch, so both preps overlap the previous epoch's MMAs.
-//   * softmax (one warpgroup per Q tile, thread = row = TMEM lane): two TMEM passes (8-way max,
-//     then exp2 + pack + tcgen05.st), a fixed share of the exponentials on the FMA pipe
-//     (degree-3 Cody-Waite polynomial, rel. error 1e-4 < bf16) to relieve the MUFU, and O
-//     rescaled only when the running max grows by > 8 (log2) so P stays <= 256.
+//     M=128 Q tiles (A, B) against the same TMA-loaded K/V (half the K/V traffic per FLOP), with
+//     one MMA-issuing thread per head (warps 1 / 2) so each head's chain runs at its own pace.
+//   * work is streamed in 64-key sub-tiles. TMEM: S_A [0,128) S_B [128,256) as two 64-column S
+//     buffers per head, O_A [256,384) O_B [384,512) (fp32). P (bf16) is written over the first
+//     32 columns of its S buffer and consumed by the TS-form MMA (A from TMEM). Per head the
+//     issuer runs S(0), S(1), then PV(j), S(j+2), ...: softmax(j+1) never waits for PV(j).
+//   * K/V: two TMA rings of 64-key sub-tiles (K 4 slots, V 2 at d=128; 8 / 4 at d=64), each with
+//     its own producer warp (0 / 3), SWIZZLE_128B boxes {64 cols, min(bs, 64) rows} from one 2D
+//     tensor map over the whole pool (block id -> row): the paged gather is done by TMA.
+//   * work: prefill codes are claimed at run time (atomic counter, smem ring shared by all
+//     roles, longest-first order); joins use a static stream-K cut with fp32 partials (combine.cu).
+//   * Q: slot x = head x, prepared by warps 12-15 (TMA load of the pre-RoPE tile, in-place
+//     rotate-half with the fp64-built fp32 table and an fp32 angle recurrence, packed fp32x2);
+//     an epoch (an item or a change of rot_delta) reloads it once its last S MMA has completed.
+//   * softmax (warps 4-7 head A, 8-11 head B; thread = row = TMEM lane): one pass per sub-tile
+//     (LDTM.x64, FMNMX3 row max, exp2 on MUFU, packed FFMA2/FADD2, STTM.x32); O rescaled only
+//     when the running max grows by > 8 (log2), so P <= 256; then the epilogue (TMEM -> swizzled
+//     smem staging -> TMA bulk store, or fp32 split partials).
 // Descriptor bit layouts and the TS / MN-major operand forms were validated on the B200 by
 // tools/tc_probe.cu before use.
 #include <cuda.h>
@@ -64,9 +64,13 @@ struct TcSmem {
   alignas(1024) uint8_t q[kQSlots][kChunks][kChunkBytes];
   alignas(1024) uint8_t k[kKSlots][kChunks][kSubBytes];  // ring of 64-key K sub-tiles
   alignas(1024) uint8_t v[kVSlots][kChunks][kSubBytes];  // ring of 64-key V sub-tiles
-  alignas(1024) float stage[8][2][32 * 32];  // epilogue transpose: 2 x 4 KB per softmax warp
+  // prefill: epilogue transpose, 2 x 4 KB per softmax warp. join: the second Q slot of each
+  // head (q2), so the next fragment's counter-rotated Q is prepared a whole epoch ahead; the
+  // join epilogue stores from registers instead
+  alignas(1024) float stage[8][2][32 * 32];
   uint64_t kv_full[2][kKSlots], kv_empty[2][kKSlots];  // [K, V][slot] (V uses the first kVSlots)
-  uint64_t q_full[2], q_empty[2], q_load[2];
+  uint64_t q_full[2][2], q_empty[2][2], q_load[2][2];  // [head][Q ring slot]
+  __device__ uint8_t* q2(int x) { return reinterpret_cast<uint8_t*>(&stage[0][0][0]) + x * kChunks * kChunkBytes; }
   uint64_t s_full[2][2], p_full[2][2], o_done[2][2];  // [head][S buffer / PV parity j & 1]
   static constexpr int kSched = 4;  // dynamic schedule: ring of claimed codes
   uint64_t sched_full[kSched], sched_empty[kSched];
@@ -86,6 +90,8 @@ struct TcParams {
   int poly_mask;  // pair i of a 32-key chunk uses the FMA-pipe exp2 when (i & 3) < poly_mask
   float rescale_threshold;  // log2 units; O is rescaled when the running max grows by more
   int qrot_table;  // Q prep: 1 = (cos, sin) table row per step, 0 = angle recurrence
+  int qprep_mode;  // Q prep: bit 0 = issue head B's load early, bit 1 = L2-prefetch the next item's q
+  int join;        // 1: 2-deep Q ring per head in the staging area, epilogue staged in Q slots
   int dbg_mode;  // profiling only: 1 = softmax does no math, 2 = max pass only,
                  // 3 = 1 + K/V always from the first block (L2-resident), 4 = 1 + MMA skips K/V waits,
                  // 5 = 1 + Q prep does no work
@@ -94,6 +100,21 @@ struct TcParams {
 template <int D>
 __device__ __forceinline__ TcSmem<D>& smem_ref(uint8_t* raw) {
   return *reinterpret_cast<TcSmem<D>*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+}
+
+// Q ring of head x: epoch e uses slot e % depth (depth 1 for prefill, 2 for joins), its
+// (e / depth)-th use
+// (J = P.join: a runtime flag, so prefill and join launches run the same kernel binary — two
+// binaries alternating per layer measured ~2% slower, their code evicting each other's)
+__device__ __forceinline__ int q_slot(bool J, uint32_t e) {
+  return J ? static_cast<int>(e & 1) : 0;
+}
+__device__ __forceinline__ uint32_t q_par(bool J, uint32_t e) {
+  return (J ? e >> 1 : e) & 1;
+}
+template <int D>
+__device__ __forceinline__ uint8_t* q_tile(TcSmem<D>& S, bool J, int x, uint32_t e) {
+  return q_slot(J, e) ? S.q2(x) : &S.q[x][0][0];
 }
 
 // profiling only: CTA 0 records (event, clock) pairs per warp (lane 0 / the elected thread);
@@ -240,11 +261,13 @@ struct SubCursor {
 template <int D>
 __device__ void run_mma(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_begin, int it_end, int x) {
   const AttnArgs& a = P.a;
+  const bool J = P.join != 0;
   constexpr int kKS = TcSmem<D>::kKSlots, kVS = TcSmem<D>::kVSlots;
   constexpr uint32_t idS = idesc_bf16_f32(128, 64, false, false);
   constexpr uint32_t idO = idesc_bf16_f32(128, D, false, true);
   uint32_t jg = 0;  // sub-tiles whose PV has been issued (global): S buffer j & 1, V slot j
-  uint32_t ep = 0;  // Q epochs started
+  uint32_t ep = 0;    // Q epochs started
+  uint32_t qcur = 0;  // the epoch whose Q tile the S MMAs read
   uint32_t tc = 0;
   auto wait_kv = [&](int kv, uint32_t n) {
     const uint32_t ns = kv == 0 ? kKS : kVS;
@@ -268,20 +291,21 @@ __device__ void run_mma(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_b
     uint32_t js = jg;  // global index of the next S sub-tile (K slot js)
     // Q: slot x holds head x's tile of the current epoch (an item or a change of rot_delta)
     auto release_q = [&]() {
-      mma_commit(&S.q_empty[x]);
-      if (!two) mma_commit(&S.q_empty[1]);  // an unpaired launch's A issuer also frees B's slot
+      const int sl = q_slot(J, qcur);
+      mma_commit(&S.q_empty[x][sl]);
+      if (!two) mma_commit(&S.q_empty[1][sl]);  // an unpaired launch's A issuer also frees B's slot
     };
     auto issue_s = [&]() {
       const int t = cs.t;
       if (cs.h == 0 && (t == tb || a.tiles[t].rot_delta != a.tiles[t - 1].rot_delta)) {
         if (t != tb) release_q();  // the previous epoch's Q tile: free once its S MMAs are done
-        mbar_wait(&S.q_full[x], ep & 1);
+        mbar_wait(&S.q_full[x][q_slot(J, ep)], q_par(J, ep));
         trace(P, 1, tc, 21);  // 21: Q ready for new epoch
-        ++ep;
+        qcur = ep++;
       }
       wait_kv(0, js);
       trace(P, 1, tc, 22);  // 22: K ready
-      const uint32_t qbase = smem_u32(&S.q[x][0][0]);
+      const uint32_t qbase = smem_u32(q_tile<D>(S, J, x, qcur));
       const uint32_t kb = smem_u32(&S.k[js % kKS][0][0]);
       const int buf = js & 1;
 #pragma unroll
@@ -394,6 +418,7 @@ struct Finished {
   float m, l;
   int h, n_heads;
   uint32_t jlast;  // global index of the item's last sub-tile (its PV is the last write to O)
+  uint32_t elast;  // Q epoch of the item's last sub-tile (join: its slot stages the epilogue)
 };
 
 // Epilogue of one finished item: wait for its last PV, read O from TMEM, normalise, store. Each warp stages 32 rows x 32 fp32 columns in its 4 KB SWIZZLE_128B buffer
@@ -403,6 +428,7 @@ template <int D>
 __device__ __forceinline__ void epilogue(const TcParams& P, TcSmem<D>& S, uint32_t ocol, int x, const Finished& f,
                                          uint32_t& tc, bool tr) {
   const AttnArgs& a = P.a;
+  const bool J = P.join != 0;
   const WorkItem& w = f.w;
   const int r = threadIdx.x & 127;
   mbar_wait(&S.o_done[x][f.jlast & 1], (f.jlast >> 1) & 1);
@@ -416,7 +442,12 @@ __device__ __forceinline__ void epilogue(const TcParams& P, TcSmem<D>& S, uint32
   const float lse = f.l > 0.f ? (f.m + __log2f(f.l)) * 0.69314718055994531f : -INFINITY;
   const int wr = (threadIdx.x / 32) & 3;  // warp's 32-row slice of the tile
   const int lane = threadIdx.x & 31;
-  float* const stg2 = &S.stage[x * 4 + wr][0][0];  // two 4 KB buffers, chunk c uses buffer c & 1
+  // 4 KB staging buffers per warp, chunk c uses buffer c % kBufs. Prefill: the staging area. Join:
+  // the Q slot of the item's last epoch (its S MMAs are done: they precede the last PV), handed
+  // back to the Q prep only once the stores below have read it
+  const int kBufs = (J && D == 64) ? 1 : 2;
+  float* const stg2 = J ? reinterpret_cast<float*>(q_tile<D>(S, J, x, f.elast)) + wr * kBufs * 1024
+                        : &S.stage[x * 4 + wr][0][0];
   // TMA store for whole 32-row slices (and for split partials, whose padding rows are never
   // read); a slice that ends inside this item's rows is written directly (the next rows belong
   // to another item)
@@ -427,8 +458,13 @@ __device__ __forceinline__ void epilogue(const TcParams& P, TcSmem<D>& S, uint32
   for (int c = 0; c < D / 32; ++c) {
     if (c + 1 < D / 32) tmem_ld32(ocol + (c + 1) * 32, vv[(c + 1) & 1]);
     const uint32_t(&v)[32] = vv[c & 1];
-    float* stg = stg2 + (c & 1) * 1024;
-    if (lane == 0) bulk_wait_read<1>();  // the store of chunk c-2 (same buffer) has read it
+    float* stg = stg2 + (c % kBufs) * 1024;
+    if (lane == 0) {  // the store of chunk c-kBufs (same buffer) has read it
+      if (kBufs == 1)
+        bulk_wait_read<0>();
+      else
+        bulk_wait_read<1>();
+    }
     __syncwarp();
 #pragma unroll
     for (int uu = 0; uu < 8; ++uu)
@@ -480,17 +516,26 @@ __device__ __forceinline__ void epilogue(const TcParams& P, TcSmem<D>& S, uint32
       a.lsepart[(static_cast<int64_t>(w.part) * f.n_heads + x) * kTileRows + r] = lse;
     }
   }
+  if (J) {  // the Q slot is free again once this warp's stores have read it
+    if (lane == 0) {
+      bulk_wait_read<0>();
+      mbar_arrive(&S.q_empty[x][q_slot(J, f.elast)]);
+    }
+    __syncwarp();
+  }
   if (tr) trace(P, 2 + x, tc, 33);  // 33: epilogue done
 }
 
 template <int D, int PM>
 __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_begin, int it_end, int x) {
   const AttnArgs& a = P.a;
+  const bool J = P.join != 0;
   const int r = threadIdx.x & 127;  // row within the tile == TMEM lane
   const uint32_t lane_base = static_cast<uint32_t>((r / 32) * 32) << 16;
   const float sl2 = P.scale_log2;
   const uint32_t ocol = tmem + lane_base + kColO + 128 * x;
   uint32_t js = 0;  // sub-tiles processed (global; == the MMA warps' PV index)
+  uint32_t eps = 0, ecur = 0;  // Q epochs seen / current (join: Q slots are also epilogue staging)
   uint32_t tc = 0;
   const bool tr = (threadIdx.x & 31) == 0;
   ItemSrc<D> src(P, S, it_begin, it_end, false);
@@ -506,6 +551,11 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
     for (int t = w.tile_begin; t < w.tile_end; ++t) {
       const KvTile tl = a.tiles[t];
       const int nsub = tl.n_valid > 64 ? 2 : 1;
+      if (J && (t == w.tile_begin || tl.rot_delta != a.tiles[t - 1].rot_delta)) {
+        // a new epoch: this warp has no use for the previous epoch's Q slot (mid-item)
+        if (t != w.tile_begin && tr) mbar_arrive(&S.q_empty[x][q_slot(J, ecur)]);
+        ecur = eps++;
+      }
       for (int hh = 0; hh < nsub; ++hh, ++js) {
         const int buf = js & 1;
         const uint32_t scol = tmem + lane_base + kColS + 128 * x + 64 * buf;
@@ -561,6 +611,7 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
     f.h = u.head_a + x;
     f.n_heads = u.n_heads;
     f.jlast = js - 1;
+    f.elast = ecur;
     epilogue<D>(P, S, ocol, x, f, tc, tr);
   }
   tc_fence_before();
@@ -684,45 +735,85 @@ __device__ __forceinline__ void rotate_q_tile(uint8_t* qs_base, const float2* ro
 template <int D>
 __device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_end) {
   const AttnArgs& a = P.a;
+  const bool J = P.join != 0;
   const int r = threadIdx.x & 127;
   const int lane = threadIdx.x & 31;
   const int wq = (threadIdx.x / 32) & 3;
   constexpr uint32_t kQBytes = 128 * D * 2;
   uint32_t ep = 0;
   uint32_t tc = 0;
-  uint32_t load_phase = 0;  // bit s: parity of the next q_load[s] completion
+  uint32_t load_phase = 0;  // bit 2x + s: parity of the next q_load[x][s] completion
   const bool tr = lane == 0;
   ItemSrc<D> src(P, S, it_begin, it_end, false);
-  for (int code; (code = src.next()) >= 0;) {
+  const bool early_b = (P.qprep_mode & 1) != 0, prefetch = (P.qprep_mode & 2) != 0;
+  // thread 0: TMA of head x's pre-RoPE tile into its slot of epoch ep
+  auto load = [&](int x, const Unit& u) {
+    uint64_t* bar = &S.q_load[x][q_slot(J, ep)];
+    uint8_t* dst = q_tile<D>(S, J, x, ep);
+    mbar_arrive_expect_tx(bar, kQBytes);
+#pragma unroll
+    for (int c = 0; c < D / 64; ++c)
+      tma_load_3d(dst + c * TcSmem<D>::kChunkBytes, &P.tmq, bar, c * 64, u.head_a + x, u.w.row0);
+  };
+  int code = src.next();
+  while (code >= 0) {
     const Unit u = decode(P, code);
     const WorkItem& w = u.w;
     const int my_row = wq * 32 + lane;  // this lane's row position, shuffled to the warp per row
     const int my_pos = my_row < w.n_rows ? a.pos[static_cast<int64_t>(w.row0) + my_row] : 0;
+    const bool work = P.dbg_mode != 5;
     for (int t = w.tile_begin; t < w.tile_end; ++t) {
       const int rot = a.tiles[t].rot_delta;
       if (t > w.tile_begin && rot == a.tiles[t - 1].rot_delta) continue;
+      // warp 12 (converged: a warp never splits across two long waits) waits for slot A and its
+      // lane 0 issues head A's load, and head B's right away if slot B is already free too (both
+      // loads then overlap A's rotation); the other warps only wait for the data
+      const int sl = q_slot(J, ep);
+      const uint32_t epar = q_par(J, ep) ^ 1;
+      bool b_issued = false;  // (warp 12 only, warp-uniform)
+      if (wq == 0) {
+        mbar_wait(&S.q_empty[0][sl], epar);
+        if (tr) trace(P, 4, tc, 40);  // 40: slot free for head A
+        if (work && lane == 0) load(0, u);
+        if (work && early_b && u.n_heads == 2) {
+          const bool free_b = lane == 0 && mbar_try_wait(&S.q_empty[1][sl], epar);
+          b_issued = __shfl_sync(0xffffffffu, free_b, 0);
+          if (b_issued && lane == 0) load(1, u);
+        }
+        __syncwarp();
+      }
       for (int x = 0; x < 2; ++x) {
-        const int sl = x;  // slot x = head x, its ep-th use
-        mbar_wait(&S.q_empty[sl], (ep & 1) ^ 1);
-        if (tr) trace(P, 4, tc, 40 + x);  // 40/41: slot free for head A/B
-        if (x < u.n_heads && P.dbg_mode != 5) {  // single-head units leave the B slot untouched
-          if (r == 0) {
-            mbar_arrive_expect_tx(&S.q_load[sl], kQBytes);
-#pragma unroll
-            for (int c = 0; c < D / 64; ++c)
-              tma_load_3d(&S.q[sl][c][0], &P.tmq, &S.q_load[sl], c * 64, u.head_a + x, w.row0);
+        if (x < u.n_heads && work) {  // single-head units leave the B slot untouched
+          if (x == 1 && wq == 0 && !b_issued) {
+            mbar_wait(&S.q_empty[1][sl], epar);
+            if (tr) trace(P, 4, tc, 41);  // 41: slot free for head B
+            if (lane == 0) load(1, u);
+            __syncwarp();
           }
-          mbar_wait(&S.q_load[sl], (load_phase >> sl) & 1);
-          load_phase ^= 1u << sl;
+          // the load is issued only once the slot is free, so its completion implies that
+          const int bit = 2 * x + sl;
+          mbar_wait(&S.q_load[x][sl], (load_phase >> bit) & 1);
+          load_phase ^= 1u << bit;
           if (tr) trace(P, 4, tc, 44 + x);  // 44/45: Q tile A/B loaded
-          rotate_q_tile<D>(&S.q[sl][0][0], a.rope, my_pos, my_row < w.n_rows, rot, a.max_pos, P.qrot_table);
+          rotate_q_tile<D>(q_tile<D>(S, J, x, ep), a.rope, my_pos, my_row < w.n_rows, rot, a.max_pos, P.qrot_table);
           fence_proxy_async_smem();
+        } else {
+          mbar_wait(&S.q_empty[x][sl], epar);
         }
         if (tr) trace(P, 4, tc, 42 + x);  // 42/43: Q tile A/B written
-        mbar_arrive(&S.q_full[sl]);
+        mbar_arrive(&S.q_full[x][sl]);
       }
       ++ep;
     }
+    // the next item's code is known long before its Q slots free: warm L2 with its q tiles
+    code = src.next();
+    if (prefetch && code >= 0 && r == 0 && work) {
+      const Unit n = decode(P, code);
+      for (int x = 0; x < n.n_heads; ++x)
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) tma_prefetch_3d(&P.tmq, c * 64, n.head_a + x, n.w.row0);
+    }
+    __syncwarp();
   }
 }
 
@@ -737,11 +828,12 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
         mbar_init(&S.kv_full[kv][i], 1);
         mbar_init(&S.kv_empty[kv][i], P.paired ? 2 : 1);  // released by each head's issuer
       }
-    for (int i = 0; i < TcSmem<D>::kQSlots; ++i) {
-      mbar_init(&S.q_full[i], 128);
-      mbar_init(&S.q_empty[i], 1);
-      mbar_init(&S.q_load[i], 1);
-    }
+    for (int i = 0; i < TcSmem<D>::kQSlots; ++i)
+      for (int sl = 0; sl < 2; ++sl) {
+        mbar_init(&S.q_full[i][sl], 128);
+        mbar_init(&S.q_empty[i][sl], P.join ? 1 + 4 : 1);  // join: + the 4 epilogue warps of head i
+        mbar_init(&S.q_load[i][sl], 1);
+      }
     for (int i = 0; i < 2; ++i) {
       for (int b = 0; b < 2; ++b) {
         mbar_init(&S.s_full[i][b], 1);
@@ -834,6 +926,10 @@ cudaError_t launch_dp(const AttnArgs& a, cudaStream_t st) {
   p.rescale_threshold = a.rescale_threshold;
   p.dbg_mode = getenv("SPANQ_DBG_MODE") ? atoi(getenv("SPANQ_DBG_MODE")) : 0;
   p.qrot_table = getenv("SPANQ_QROT_TABLE") ? atoi(getenv("SPANQ_QROT_TABLE")) : 0;
+  p.qprep_mode = getenv("SPANQ_QPREP") ? atoi(getenv("SPANQ_QPREP")) : 3;
+  // joins of paired launches use the 2-deep Q ring (knob SPANQ_JOIN_QRING=0 turns it off, for A/B)
+  static const bool ring = getenv("SPANQ_JOIN_QRING") == nullptr || atoi(getenv("SPANQ_JOIN_QRING")) != 0;
+  p.join = a.join && a.paired && ring ? 1 : 0;
   span_attn_tc_kernel<D, PM><<<a.grid, kThreads, smem, st>>>(p);
   return cudaGetLastError();
 }

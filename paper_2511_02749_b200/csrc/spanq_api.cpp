@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "../../include/spanq.h"
+#include "host/cidra.h"
 #include "host/planner.h"
 #include "host/work_builder.h"
 #include "kernels/launch.h"
@@ -796,6 +797,7 @@ spq_status spq_join(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b
   args.opart = opart;
   args.lsepart = lsepart;
   args.pos = at<int32_t>(p, p->off_jpos) + r0;
+  args.join = true;
   args.q = q;
   args.o = o;
   args.lse = lse;
@@ -947,6 +949,90 @@ spq_status spq_read_blocks(spq_ctx* c, int32_t layer, const int32_t* ids, int64_
     CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(v) + i * blk, static_cast<const uint8_t*>(c->cfg.v_pool) + src, blk,
                              cudaMemcpyDeviceToDevice, st));
   }
+  return SPQ_OK;
+}
+
+// ------------------------------------------------------------------ CIDRA
+namespace {
+spq_status cidra_plan(const spq_ctx* c, const int32_t* src, const int32_t* dst, const int32_t* delta, int64_t n,
+                      spq::CidraSchedule* sch, spq_cidra_stats* stats) {
+  if (c == nullptr || (n > 0 && (src == nullptr || dst == nullptr || delta == nullptr)))
+    return fail(SPQ_EINVAL, "null argument");
+  if (n < 0) return fail(SPQ_EINVAL, "negative move count");
+  for (int64_t i = 0; i < n; ++i)
+    if (delta[i] <= -c->cfg.max_position || delta[i] >= c->cfg.max_position)
+      return fail(SPQ_EINVAL, "|delta| >= max_position (no RoPE table row)");
+  std::string err;
+  if (!spq::cidra_schedule(src, dst, delta, n, c->cfg.num_blocks, sch, &err)) return fail(SPQ_EINVAL, err);
+  if (stats != nullptr) {
+    stats->moves = n;
+    stats->components = static_cast<int64_t>(sch->comp_off.size()) - 1;
+    stats->cycles = sch->cycles;
+    stats->duplicates = sch->duplicates;
+    stats->ops = static_cast<int64_t>(sch->ops.size());
+    stats->max_component_ops = sch->max_component_ops;
+  }
+  return SPQ_OK;
+}
+}  // namespace
+
+spq_status spq_cidra_schedule(const spq_ctx* c, const int32_t* src, const int32_t* dst, const int32_t* delta,
+                              int64_t n, int32_t* ops, int64_t cap, int64_t* n_ops, int32_t* comp_off,
+                              int64_t comp_cap, int64_t* n_comp, spq_cidra_stats* stats) {
+  if (n_ops == nullptr || n_comp == nullptr) return fail(SPQ_EINVAL, "null argument");
+  spq::CidraSchedule sch;
+  spq_status s = cidra_plan(c, src, dst, delta, n, &sch, stats);
+  if (s != SPQ_OK) return s;
+  *n_ops = static_cast<int64_t>(sch.ops.size());
+  *n_comp = static_cast<int64_t>(sch.comp_off.size()) - 1;
+  if (*n_ops > cap || *n_comp + 1 > comp_cap || (*n_ops > 0 && ops == nullptr) || comp_off == nullptr)
+    return fail(SPQ_EINVAL, "schedule capacity too small");
+  std::memcpy(ops, sch.ops.data(), sch.ops.size() * sizeof(spq::CidraOp));
+  std::memcpy(comp_off, sch.comp_off.data(), sch.comp_off.size() * sizeof(int32_t));
+  return SPQ_OK;
+}
+
+spq_status spq_reposition(spq_ctx* c, const int32_t* src, const int32_t* dst, const int32_t* delta, int64_t n,
+                          int32_t layer_begin, int32_t layer_end, void* stream, spq_cidra_stats* stats) {
+  spq::CidraSchedule sch;
+  spq_status s = cidra_plan(c, src, dst, delta, n, &sch, stats);
+  if (s != SPQ_OK) return s;
+  if (!is_gpu(c)) return fail(SPQ_ESTATE, "host-only ctx (device < 0) has no pool");
+  if (layer_begin < 0 || layer_end > c->cfg.num_layers || layer_begin > layer_end)
+    return fail(SPQ_ESTATE, "layer range out of bounds");
+  if (c->cfg.head_dim != 64 && c->cfg.head_dim != 128) return fail(SPQ_EINVAL, "head_dim must be 64 or 128");
+  const int64_t n_comp = static_cast<int64_t>(sch.comp_off.size()) - 1;
+  if (n_comp == 0 || layer_begin == layer_end) return SPQ_OK;
+  if (n_comp > INT32_MAX || static_cast<int64_t>(layer_end - layer_begin) * c->cfg.num_kv_heads > 65535)
+    return fail(SPQ_EINVAL, "too many components or layers x kv heads for one launch");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  s = wait_pending(c, st);
+  if (s != SPQ_OK) return s;
+  // one stream-ordered device buffer: ops then component offsets (pageable H2D: staged before return)
+  const size_t ob = sch.ops.size() * sizeof(spq::CidraOp), cb = sch.comp_off.size() * sizeof(int32_t);
+  void* buf = nullptr;
+  CUDA_TRY(cudaMallocAsync(&buf, ob + cb, st));
+  CUDA_TRY(cudaMemcpyAsync(buf, sch.ops.data(), ob, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(buf) + ob, sch.comp_off.data(), cb, cudaMemcpyHostToDevice, st));
+  spq::CidraArgs a{};
+  a.ops = static_cast<const int4*>(buf);
+  a.comp_off = reinterpret_cast<const int32_t*>(static_cast<uint8_t*>(buf) + ob);
+  a.n_comp = static_cast<int32_t>(n_comp);
+  a.k_pool = c->cfg.k_pool;
+  a.v_pool = c->cfg.v_pool;
+  a.rope = c->rope;
+  a.hkv = c->cfg.num_kv_heads;
+  a.d = c->cfg.head_dim;
+  a.bs = c->cfg.block_size;
+  a.nblk = c->cfg.num_blocks;
+  a.layer_begin = layer_begin;
+  a.layer_end = layer_end;
+  a.fp32 = c->cfg.dtype == SPQ_FP32;
+  cudaError_t e = spq::launch_cidra(a, st);
+  if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("cidra launch: ") + cudaGetErrorString(e));
+  c->launches++;
+  CUDA_TRY(cudaFreeAsync(buf, st));
   return SPQ_OK;
 }
 

@@ -80,6 +80,11 @@ class spq_stats(C.Structure):
         "inserted_blocks", "resident_blocks", "free_blocks", "pinned_blocks", "plans")]
 
 
+class spq_cidra_stats(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in (
+        "moves", "components", "cycles", "duplicates", "ops", "max_component_ops")]
+
+
 # name -> (restype, argtypes) for every entry point of include/spanq.h
 SIGNATURES = {
     "spq_create": (C.c_int, [C.POINTER(spq_config), C.POINTER(C.c_void_p)]),
@@ -106,6 +111,11 @@ SIGNATURES = {
     "spq_evict_all": (C.c_int, [C.c_void_p]),
     "spq_read_blocks": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                   C.c_void_p]),
+    "spq_reposition": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
+                                 C.c_int32, C.c_void_p, C.POINTER(spq_cidra_stats)]),
+    "spq_cidra_schedule": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                     C.c_int64, _I64P, C.c_void_p, C.c_int64, _I64P,
+                                     C.POINTER(spq_cidra_stats)]),
     "spq_launch_count": (C.c_int, [C.c_void_p, _I64P]),
     "spq_last_attn_ms": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "spq_set_timing": (C.c_int, [C.c_void_p, C.c_int32]),
@@ -338,6 +348,38 @@ class Context:
         _check(lib().spq_read_blocks(self.handle, layer, ids.ctypes.data, len(ids), _ptr(k), _ptr(v),
                                      _stream_ptr(stream)))
         return k, v
+
+    @staticmethod
+    def _moves(src, dst, delta):
+        a = [np.ascontiguousarray(x, dtype=np.int32) for x in (src, dst, delta)]
+        if not (len(a[0]) == len(a[1]) == len(a[2])):
+            raise ValueError("src, dst, delta must have the same length")
+        return a
+
+    def reposition(self, src, dst, delta, layers=None, stream=None) -> Dict[str, int]:
+        """CIDRA: block dst[i] <- block src[i] with K re-encoded delta[i] positions
+        later, V copied, in place on the ctx's pools for layers [begin, end). Returns the stats."""
+        s_, d_, dl = self._moves(src, dst, delta)
+        lb, le = layers if layers is not None else (0, self.shape.layers)
+        st = spq_cidra_stats()
+        _check(lib().spq_reposition(self.handle, s_.ctypes.data, d_.ctypes.data, dl.ctypes.data, len(s_), lb, le,
+                                    _stream_ptr(stream), C.byref(st)))
+        return {n: getattr(st, n) for n, _ in spq_cidra_stats._fields_}
+
+    def cidra_schedule(self, src, dst, delta):
+        """The in-place schedule spq_reposition would run: (ops [n_ops, 4] = dst, src, delta, mode;
+        comp_off [n_comp + 1]; stats)."""
+        s_, d_, dl = self._moves(src, dst, delta)
+        cap = 2 * len(s_) + 8
+        ops = np.zeros((cap, 4), np.int32)
+        off = np.zeros(len(s_) + 2, np.int32)
+        n_ops, n_comp = C.c_int64(), C.c_int64()
+        st = spq_cidra_stats()
+        _check(lib().spq_cidra_schedule(self.handle, s_.ctypes.data, d_.ctypes.data, dl.ctypes.data, len(s_),
+                                        ops.ctypes.data, cap, C.byref(n_ops), off.ctypes.data, len(off),
+                                        C.byref(n_comp), C.byref(st)))
+        return (ops[: n_ops.value].copy(), off[: n_comp.value + 1].copy(),
+                {n: getattr(st, n) for n, _ in spq_cidra_stats._fields_})
 
     def stats(self) -> Dict[str, int]:
         s = spq_stats()

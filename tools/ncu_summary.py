@@ -67,7 +67,7 @@ def launches(path: str):
 
 
 def short(name: str) -> str:
-    for k in ("span_attn_tc", "span_attn_f32", "rope_kv_write", "combine_kernel", "kv_exchange"):
+    for k in ("span_attn_tc", "span_attn_f32", "rope_kv_write", "combine_kernel", "kv_exchange", "cidra_kernel"):
         if k in name:
             return k
     return name.split("(")[0][-60:]
@@ -83,7 +83,7 @@ def main():
               " times under ncu are serialised and cold-cache: compare shares, not absolutes.", ""]
     traffic = OrderedDict()
     names = {"attn": ["span_attn_tc prefill", "span_attn_tc join"], "kvwrite": ["rope_kv_write prefill"],
-             "combine": ["combine join"], "exchange": ["kv_exchange"]}
+             "combine": ["combine join"], "exchange": ["kv_exchange"], "cidra": ["cidra reposition"]}
     for rep, labels in names.items():
         path = os.path.join(prof, rep + ".ncu-rep")
         if not os.path.exists(path):

@@ -13,5 +13,7 @@ timeout 300 ncu --set full --clock-control none -k regex:rope_kv_write -s 2 -c 1
   -o gpurun_out/prof/kvwrite python tools/profile_step.py 2 > gpurun_out/prof/ncu_kv.log 2>&1
 timeout 300 ncu --set full --clock-control none -k regex:combine -s 1 -c 1 \
   -o gpurun_out/prof/combine python tools/profile_step.py 2 > gpurun_out/prof/ncu_comb.log 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:cidra -s 1 -c 1 \
+  -o gpurun_out/prof/cidra python tools/profile_cidra.py 2 > gpurun_out/prof/ncu_cidra.log 2>&1
 timeout 600 python bench.py > gpurun_out/prof/bench.json 2> gpurun_out/prof/bench.err
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/prof/bench_ref.json 2> gpurun_out/prof/bench_ref.err
