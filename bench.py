@@ -394,7 +394,7 @@ def measure_reposition(ctx, s, stream, flush, n_blocks, hbm_gbs, reps: int = 10)
     return {"kernel": "cidra (K8)", "moves": n_blocks, "layers": s.layers, "cycles": st["cycles"],
             "components": st["components"], "ms": t, "tokens_per_ms": n_blocks * s.block_size / t,
             "achieved_gbs": nbytes / (t / 1e3) / 1e9, "peak_gbs": hbm_gbs,
-            "frac": nbytes / (t / 1e3) / 1e9 / hbm_gbs, "bytes": nbytes,
+            "frac": nbytes / (t / 1e3) / 1e9 / hbm_gbs, "bytes": nbytes, "traffic": ncu_traffic("cidra reposition"),
             "note": "paper: up to 500 tokens/ms on its own hardware and model (P:648), context only"}
 
 

@@ -73,7 +73,11 @@ void schedule(const std::vector<double>& item_cost, int units, int num_sms, Attn
 
 constexpr double kItemOverhead = 1.0;   // q-prep + epilogue, in KV-tile units
 constexpr double kSplitOverhead = 0.5;  // partial write + combine read, per split
-constexpr double kSubOverhead = 3.0;    // per work item, in 64-key sub-tiles (epilogue + Q + pipeline fill)
+// per work item, in 64-key sub-tiles (epilogue + Q + pipeline fill; tuning knob SPANQ_SUB_OVERHEAD)
+const double kSubOverhead = [] {
+  const char* e = std::getenv("SPANQ_SUB_OVERHEAD");
+  return e ? std::atof(e) : 3.0;
+}();
 // per Q-rotation change inside a join piece, in sub-tiles (tuning knob SPANQ_EPOCH_COST)
 const double kEpochCost = [] {
   const char* e = std::getenv("SPANQ_EPOCH_COST");
