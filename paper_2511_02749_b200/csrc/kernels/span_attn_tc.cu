@@ -466,6 +466,7 @@ __device__ __forceinline__ void epilogue(const TcParams& P, TcSmem<D>& S, uint32
         bulk_wait_read<1>();
     }
     __syncwarp();
+    if (tr) trace(P, 2 + x, tc, 50 + c);  // 50+c: staging buffer of chunk c free
 #pragma unroll
     for (int uu = 0; uu < 8; ++uu)
       *reinterpret_cast<float4*>(stg + lane * 32 + ((uu ^ (lane & 7)) * 4)) =
