@@ -928,9 +928,10 @@ cudaError_t launch_dp(const AttnArgs& a, cudaStream_t st) {
   p.dbg_mode = getenv("SPANQ_DBG_MODE") ? atoi(getenv("SPANQ_DBG_MODE")) : 0;
   p.qrot_table = getenv("SPANQ_QROT_TABLE") ? atoi(getenv("SPANQ_QROT_TABLE")) : 0;
   p.qprep_mode = getenv("SPANQ_QPREP") ? atoi(getenv("SPANQ_QPREP")) : 3;
-  // joins of paired launches use the 2-deep Q ring (knob SPANQ_JOIN_QRING=0 turns it off, for A/B)
-  static const bool ring = getenv("SPANQ_JOIN_QRING") == nullptr || atoi(getenv("SPANQ_JOIN_QRING")) != 0;
-  p.join = a.join && a.paired && ring ? 1 : 0;
+  // 2-deep Q ring (paired launches): knob SPANQ_QRING2 = 0 off, 1 joins only (default), 2 joins and
+  // prefill (A/B: the prefill gains nothing — its epilogue then contends with the next item's S MMAs)
+  static const int ring = getenv("SPANQ_QRING2") ? atoi(getenv("SPANQ_QRING2")) : 1;
+  p.join = a.paired && (ring >= 2 || (ring == 1 && a.join)) ? 1 : 0;
   span_attn_tc_kernel<D, PM><<<a.grid, kThreads, smem, st>>>(p);
   return cudaGetLastError();
 }
