@@ -3,6 +3,9 @@
 // counter, final-block flag, parameter block {digest length, key length 0, fanout 1, depth 1}.
 #include "blake2b.h"
 
+#include <immintrin.h>
+
+#include <cstdlib>
 #include <cstring>
 
 namespace spq {
@@ -85,6 +88,83 @@ void compress(uint64_t* h, const uint8_t* block, uint64_t t_lo, uint64_t t_hi, b
 #undef SPQ_ROUND
 #undef SPQ_G
 
+// The same compression with the 16-word state as four 256-bit rows (v0..3 | v4..7 | v8..11 |
+// v12..15): the four column G's of a round run as one vector G, then the rows are rotated so the
+// four diagonal G's do too (RFC 7693 §3.2's order of G applications, 4 at a time). Runtime
+// dispatch: used only when the host CPU has AVX2 (the test suite checks both against hashlib).
+__attribute__((target("avx2"))) inline __m256i rotr32(__m256i x) { return _mm256_shuffle_epi32(x, 0xB1); }
+__attribute__((target("avx2"))) inline __m256i rotr24(__m256i x) {
+  const __m256i r = _mm256_setr_epi8(3, 4, 5, 6, 7, 0, 1, 2, 11, 12, 13, 14, 15, 8, 9, 10, 3, 4, 5, 6, 7, 0, 1, 2, 11,
+                                     12, 13, 14, 15, 8, 9, 10);
+  return _mm256_shuffle_epi8(x, r);
+}
+__attribute__((target("avx2"))) inline __m256i rotr16(__m256i x) {
+  const __m256i r = _mm256_setr_epi8(2, 3, 4, 5, 6, 7, 0, 1, 10, 11, 12, 13, 14, 15, 8, 9, 2, 3, 4, 5, 6, 7, 0, 1, 10,
+                                     11, 12, 13, 14, 15, 8, 9);
+  return _mm256_shuffle_epi8(x, r);
+}
+__attribute__((target("avx2"))) inline __m256i rotr63(__m256i x) {
+  return _mm256_or_si256(_mm256_srli_epi64(x, 63), _mm256_add_epi64(x, x));
+}
+
+__attribute__((target("avx2"))) void compress_avx2(uint64_t* h, const uint8_t* block, uint64_t t_lo, uint64_t t_hi,
+                                                   bool last) {
+  uint64_t m[16];
+  for (int i = 0; i < 16; ++i) m[i] = load64(block + 8 * i);
+  const __m256i h0 = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(h));
+  const __m256i h1 = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(h + 4));
+  __m256i a = h0, b = h1;
+  __m256i c = _mm256_setr_epi64x(static_cast<long long>(kIV[0]), static_cast<long long>(kIV[1]),
+                                 static_cast<long long>(kIV[2]), static_cast<long long>(kIV[3]));
+  __m256i d = _mm256_setr_epi64x(static_cast<long long>(kIV[4] ^ t_lo), static_cast<long long>(kIV[5] ^ t_hi),
+                                 static_cast<long long>(last ? ~kIV[6] : kIV[6]), static_cast<long long>(kIV[7]));
+  for (int r = 0; r < 12; ++r) {
+    const uint8_t* s = kSigma[r];
+    // columns: G(i) for i = 0..3 on lanes i, message words s[2i], s[2i+1]
+    __m256i x = _mm256_setr_epi64x(static_cast<long long>(m[s[0]]), static_cast<long long>(m[s[2]]),
+                                   static_cast<long long>(m[s[4]]), static_cast<long long>(m[s[6]]));
+    __m256i y = _mm256_setr_epi64x(static_cast<long long>(m[s[1]]), static_cast<long long>(m[s[3]]),
+                                   static_cast<long long>(m[s[5]]), static_cast<long long>(m[s[7]]));
+    a = _mm256_add_epi64(_mm256_add_epi64(a, b), x);
+    d = rotr32(_mm256_xor_si256(d, a));
+    c = _mm256_add_epi64(c, d);
+    b = rotr24(_mm256_xor_si256(b, c));
+    a = _mm256_add_epi64(_mm256_add_epi64(a, b), y);
+    d = rotr16(_mm256_xor_si256(d, a));
+    c = _mm256_add_epi64(c, d);
+    b = rotr63(_mm256_xor_si256(b, c));
+    // diagonals: lane j holds (v[j], v[4 + (j+1)%4], v[8 + (j+2)%4], v[12 + (j+3)%4])
+    b = _mm256_permute4x64_epi64(b, _MM_SHUFFLE(0, 3, 2, 1));
+    c = _mm256_permute4x64_epi64(c, _MM_SHUFFLE(1, 0, 3, 2));
+    d = _mm256_permute4x64_epi64(d, _MM_SHUFFLE(2, 1, 0, 3));
+    x = _mm256_setr_epi64x(static_cast<long long>(m[s[8]]), static_cast<long long>(m[s[10]]),
+                           static_cast<long long>(m[s[12]]), static_cast<long long>(m[s[14]]));
+    y = _mm256_setr_epi64x(static_cast<long long>(m[s[9]]), static_cast<long long>(m[s[11]]),
+                           static_cast<long long>(m[s[13]]), static_cast<long long>(m[s[15]]));
+    a = _mm256_add_epi64(_mm256_add_epi64(a, b), x);
+    d = rotr32(_mm256_xor_si256(d, a));
+    c = _mm256_add_epi64(c, d);
+    b = rotr24(_mm256_xor_si256(b, c));
+    a = _mm256_add_epi64(_mm256_add_epi64(a, b), y);
+    d = rotr16(_mm256_xor_si256(d, a));
+    c = _mm256_add_epi64(c, d);
+    b = rotr63(_mm256_xor_si256(b, c));
+    b = _mm256_permute4x64_epi64(b, _MM_SHUFFLE(2, 1, 0, 3));
+    c = _mm256_permute4x64_epi64(c, _MM_SHUFFLE(1, 0, 3, 2));
+    d = _mm256_permute4x64_epi64(d, _MM_SHUFFLE(0, 3, 2, 1));
+  }
+  _mm256_storeu_si256(reinterpret_cast<__m256i*>(h), _mm256_xor_si256(h0, _mm256_xor_si256(a, c)));
+  _mm256_storeu_si256(reinterpret_cast<__m256i*>(h + 4), _mm256_xor_si256(h1, _mm256_xor_si256(b, d)));
+}
+
+using CompressFn = void (*)(uint64_t*, const uint8_t*, uint64_t, uint64_t, bool);
+CompressFn pick_compress() {
+  const char* e = std::getenv("SPANQ_BLAKE2B_SCALAR");  // test knob: force the scalar path
+  if (e == nullptr && __builtin_cpu_supports("avx2")) return compress_avx2;
+  return compress;
+}
+const CompressFn kCompress = pick_compress();
+
 }  // namespace
 
 void blake2b(uint8_t* out, size_t outlen, const void* data, size_t len) {
@@ -96,14 +176,14 @@ void blake2b(uint8_t* out, size_t outlen, const void* data, size_t len) {
   // all full blocks except the last one
   while (len > 128) {
     t += 128;
-    compress(h, p, t, 0, false);
+    kCompress(h, p, t, 0, false);
     p += 128;
     len -= 128;
   }
   uint8_t last[128] = {0};
   std::memcpy(last, p, len);
   t += len;
-  compress(h, last, t, 0, true);
+  kCompress(h, last, t, 0, true);
   uint8_t full[64];
   std::memcpy(full, h, 64);
   std::memcpy(out, full, outlen);
