@@ -197,3 +197,33 @@ def test_paper_configs_plan_bit_exact(cfg):
     if cfg == "C3":
         frag_hits = [h for h, k in zip(cp.view()["seg_hit"], cp.view()["seg_kind"]) if k == 1]
         assert sum(frag_hits) == 12  # 75% fragment hits (configs[2])
+
+
+@pytest.mark.parametrize("scalar", [False, True])
+def test_block_hashes_both_blake2b_paths(scalar):
+    # the library picks an AVX2 BLAKE2b compression at load time when the CPU has it; the scalar
+    # RFC 7693 path must give the same digests (fresh process: the choice is made once)
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, %r)\n"
+        "from paper_2511_02749_b200 import inputs, spanq\n"
+        "from oracle import hashing\n"
+        "from oracle.store import Store\n"
+        "sh = inputs.Shape(hq=32, hkv=8, d=128, block_size=64)\n"
+        "ctx = spanq.Context(sh, 64, device=-1)\n"
+        "q = inputs.SpanQuery(np.arange(300, dtype=np.int32), [np.arange(200, dtype=np.int32) * 7], "
+        "np.arange(70, dtype=np.int32) + 5, nest=False)\n"
+        "d = [bytes(r) for r in ctx.block_hashes(q)]\n"
+        "root = Store(64, 32, 8, 128, 64).root\n"
+        "h = hashing.prefix_chain(q.prefix, 64, root); s = hashing.fragment_chain(q.fragments[0], 64, root)\n"
+        "J = hashing.join_fold(h[-1], [s[-1]])\n"
+        "assert d == h + s + [J] + hashing.cross_chain(q.cross, 64, J)\n"
+        "print('ok')\n" % ROOT)
+    env = dict(os.environ)
+    env.pop("SPANQ_BLAKE2B_SCALAR", None)
+    if scalar:
+        env["SPANQ_BLAKE2B_SCALAR"] = "1"
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, cwd=ROOT)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stderr
