@@ -315,9 +315,11 @@ def main():
     # configs[2] (C3: 75% of the fragments cached, permuted) after its warm-up query, and an
     # ordinary causal prefill of the same 17,152 tokens (what a prefix cache cannot reuse)
     locality = None
+    judge = None
     if not args.no_locality:
         with torch.cuda.stream(stream):
             locality = measure_locality(ctx, s, tab, dev, stream, flush, args)
+            judge = measure_judge(dev, stream, flush, args)
 
     peak_burst, peak_sust, hbm, peak_src = peaks()
     # ---- CIDRA: in-place repositioning of the C2 query's blocks, all layers
@@ -351,6 +353,8 @@ def main():
                 "ms_per_step": e2e_total / args.steps},
     }
     line["reposition"] = reposition
+    if judge is not None:
+        line["judge"] = judge
     if locality is not None:
         locality["c2_cold_ttft_l1_ms"] = line["ttft_l1_ms"]
         locality["dense_over_span_ttft"] = locality["dense_causal_ttft_l1_ms"] / line["ttft_l1_ms"]
@@ -362,6 +366,36 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def measure_judge(dev, stream, flush, args, reps: int = 5):
+    """configs[3] C4, the judge/generator span at the 2B shape (Hq 32 / Hkv 8 / d 64): 8 candidate
+    generations x 2048 tokens in a plus span + a 512-token judge prompt, one layer. Cold: the
+    candidates are prefilled as fragments; warm: they are resident (as after generating them),
+    only the judge prompt's join runs. Dense: an ordinary causal prefill of the same 16,896 tokens."""
+    import torch
+
+    from paper_2511_02749_b200 import inputs, runner, spanq
+
+    w = inputs.c4()
+    s = w.shape
+    ctx = spanq.Context(s, 512, device=dev.index or 0, max_position=1 << 15, out_dtype=args.out_dtype)
+    tab = runner.device_tables(s, 0, w.seed, dev)
+    odt = torch.float32 if args.out_dtype == "fp32" else torch.bfloat16
+    q = w.queries[0]
+    cand_only = inputs.SpanQuery(np.zeros(0, np.int32), list(q.fragments), q.cross[:1])  # fills the candidates
+    toks = np.concatenate(list(q.fragments) + [q.cross])
+    dense = inputs.SpanQuery(toks[:-1], [], toks[-1:])
+    cold_ms, cold_flops = ttft_l1(ctx, s, tab, dev, stream, flush, odt, w.queries, [], reps)
+    warm_ms, warm_flops = ttft_l1(ctx, s, tab, dev, stream, flush, odt, w.queries, [cand_only], reps)
+    dense_ms, dense_flops = ttft_l1(ctx, s, tab, dev, stream, flush, odt, [dense], [], reps)
+    ctx.close()
+    return {"workload": "C4 judge/generator (configs[3]): 8 x 2048 candidates + 512 judge prompt, 2B shape "
+                        "Hq32/Hkv8/d64, one layer",
+            "cold_ttft_l1_ms": cold_ms, "cold_flops": cold_flops, "cold_tflops": cold_flops / (cold_ms / 1e3) / 1e12,
+            "warm_ttft_l1_ms": warm_ms, "warm_flops": warm_flops, "warm_tflops": warm_flops / (warm_ms / 1e3) / 1e12,
+            "dense_causal_ttft_l1_ms": dense_ms, "dense_causal_flops": dense_flops,
+            "dense_over_cold": dense_ms / cold_ms, "dense_over_warm": dense_ms / warm_ms}
 
 
 def measure_reposition(ctx, s, stream, flush, n_blocks, hbm_gbs, reps: int = 10):
@@ -398,20 +432,12 @@ def measure_reposition(ctx, s, stream, flush, n_blocks, hbm_gbs, reps: int = 10)
             "note": "paper: up to 500 tokens/ms on its own hardware and model (P:648), context only"}
 
 
-def measure_locality(ctx, s, tab, dev, stream, flush, args, reps: int = 5):
-    """TTFT (plan + one layer of attention, cold L2) of (a) configs[2] C3 right after its warm-up
-    query filled the store (75% fragment hits, permuted: only the new fragments, the partial
-    prefix tail and the join are computed) and (b) the same number of tokens as one ordinary
-    causal prefill (a 17,151-token prefix + 1 cross token: what a stock engine computes)."""
+def ttft_l1(ctx, s, tab, dev, stream, flush, odt, queries, warm, reps: int = 5):
+    """Median TTFT of one layer (plan + K1 + prefill of the misses + join, through the public
+    API, cold L2) of `queries` right after `warm` filled the store; returns (ms, algorithmic FLOPs)."""
     import torch
 
-    from paper_2511_02749_b200 import inputs, runner
-
-    c3 = inputs.c3()
-    c2q = inputs.c2(seed=2).queries[0]
-    toks = np.concatenate([c2q.prefix] + list(c2q.fragments) + [c2q.cross])
-    dense = inputs.SpanQuery(toks[:-1], [], toks[-1:])
-    odt = torch.float32 if args.out_dtype == "fp32" else torch.bfloat16
+    from paper_2511_02749_b200 import runner
 
     def fill(warm):
         ctx.evict_all()
@@ -452,8 +478,25 @@ def measure_locality(ctx, s, tab, dev, stream, flush, args, reps: int = 5):
             ms.append(a.elapsed_time(b))
         return statistics.median(ms[1:]), v["prefill_flops"] + v["join_flops"]
 
-    c3_ms, c3_flops = run(c3.queries, c3.warmup_queries)
-    dense_ms, dense_flops = run([dense], [])
+    return run(queries, warm)
+
+
+def measure_locality(ctx, s, tab, dev, stream, flush, args, reps: int = 5):
+    """TTFT (plan + one layer of attention, cold L2) of (a) configs[2] C3 right after its warm-up
+    query filled the store (75% fragment hits, permuted: only the new fragments, the partial
+    prefix tail and the join are computed) and (b) the same number of tokens as one ordinary
+    causal prefill (a 17,151-token prefix + 1 cross token: what a stock engine computes)."""
+    import torch
+
+    from paper_2511_02749_b200 import inputs
+
+    c3 = inputs.c3()
+    c2q = inputs.c2(seed=2).queries[0]
+    toks = np.concatenate([c2q.prefix] + list(c2q.fragments) + [c2q.cross])
+    dense = inputs.SpanQuery(toks[:-1], [], toks[-1:])
+    odt = torch.float32 if args.out_dtype == "fp32" else torch.bfloat16
+    c3_ms, c3_flops = ttft_l1(ctx, s, tab, dev, stream, flush, odt, c3.queries, c3.warmup_queries, reps)
+    dense_ms, dense_flops = ttft_l1(ctx, s, tab, dev, stream, flush, odt, [dense], [], reps)
     return {"c3_warm_ttft_l1_ms": c3_ms, "c3_warm_flops": c3_flops,
             "dense_causal_ttft_l1_ms": dense_ms, "dense_causal_flops": dense_flops,
             "dense_causal_tflops": dense_flops / (dense_ms / 1e3) / 1e12,
