@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(256) rope_kv_write_kernel(
   int h = 0, g = 0;
   uint4 ku = make_uint4(0, 0, 0, 0), vu = make_uint4(0, 0, 0, 0);
   int64_t s = -1;
+  int p = 0;
   if (main_row) {
     r = gid / per_row;
     const int rem = static_cast<int>(gid - r * per_row);
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(256) rope_kv_write_kernel(
     // all loads issued up front and independent of each other (slot, pos, k, v; the table
     // below): rows with slot -1 (rare: resident blocks) load k/v for nothing
     s = slot[r];
+    p = pos[r];  // unconditional: not serialized behind the slot test
     ku = __ldg(reinterpret_cast<const uint4*>(k + src));
     vu = __ldg(reinterpret_cast<const uint4*>(v + src));
   }
@@ -99,7 +101,6 @@ __global__ void __launch_bounds__(256) rope_kv_write_kernel(
     Vec<T>::unpack(ku, x);
     Vec<T>::unpack(pu, y);
     if (s >= 0) {
-      const int p = pos[r];
       const bool first_half = g < G / 2;
       const int i0 = (first_half ? g : g - G / 2) * N;  // pair index of element 0
       const float4* cs = reinterpret_cast<const float4*>(rope + static_cast<int64_t>(p) * (D / 2) + i0);
