@@ -26,6 +26,7 @@ CASES = [
     dict(hq=32, hkv=8, d=128, block_size=64, dtype="bf16", layers=2, nblk=96, n=80),
     dict(hq=32, hkv=8, d=64, block_size=16, dtype="bf16", layers=2, nblk=64, n=64),
     dict(hq=2, hkv=2, d=64, block_size=16, dtype="fp32", layers=1, nblk=48, n=40),
+    dict(hq=8, hkv=2, d=128, block_size=128, dtype="fp32", layers=2, nblk=24, n=24),
 ]
 
 
