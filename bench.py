@@ -547,6 +547,8 @@ def main_c5(args, rank, world, local):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     xbytes = [0]
 
+    comm = torch.cuda.Stream(dev)
+
     def step():
         ctx.evict_all()
         plan = ctx.plan(w.queries, stream=stream)
@@ -555,9 +557,18 @@ def main_c5(args, rank, world, local):
             if len(ptok):
                 plan.prefill(layer, qp, kp, vp, op, lp, stream=stream)
             if world > 1:
-                st = parallel.exchange_layer(plan, v, layer, s, dev, ctx.k_pool.dtype, rank, world, stream=stream)
+                # the exchange (comm stream, after this layer's prefill) overlaps join phase 0 over
+                # the segments this rank holds; phase 1 (received fragments + combine) waits for it
+                comm.wait_stream(stream)
+                if len(jtok):
+                    plan.join_phase(layer, 0, qj, kj, vj, oj, lj, stream=stream)
+                with torch.cuda.stream(comm):
+                    st = parallel.exchange_layer(plan, v, layer, s, dev, ctx.k_pool.dtype, rank, world, stream=comm)
                 xbytes[0] = st["sent_bytes"]
-            if len(jtok):
+                stream.wait_stream(comm)
+                if len(jtok):
+                    plan.join_phase(layer, 1, qj, kj, vj, oj, lj, stream=stream)
+            elif len(jtok):
                 plan.join(layer, qj, kj, vj, oj, lj, stream=stream)
         plan.release(stream=stream)
 

@@ -192,6 +192,18 @@ spq_status spq_exchange_pack(spq_ctx *ctx, spq_plan *plan, int32_t layer, int32_
 spq_status spq_exchange_unpack(spq_ctx *ctx, spq_plan *plan, int32_t layer, int32_t peer,
                                const void *buf, void *stream);
 
+/* The same join of all of the plan's home queries in two launches, so that on W > 1 the
+ * fragment-KV exchange overlaps the first: phase 0 = rope_kv_write of the cross
+ * rows and the attention over the segments this rank holds (prefix, locally owned fragments,
+ * cross causal); phase 1 — after spq_exchange_unpack of this layer — the attention over the
+ * received fragments and the combine of both phases' fp32 split partials into o / lse (in a
+ * fixed order: phase-0 pieces, then phase-1 pieces). A plan without received fragments, or on
+ * the fp32 path (no split partials), runs the whole join in phase 1 and phase 0 is a no-op.
+ * Arguments as spq_join over [0, n_queries); phase must be 0 or 1 (SPQ_EINVAL). Both phases
+ * must be issued, in order, for the layer. */
+spq_status spq_join_phase(spq_ctx *ctx, spq_plan *plan, int32_t layer, int32_t phase, const void *q,
+                          const void *k, const void *v, void *o, float *lse, void *stream);
+
 /* Stream-ordered release: unpins the plan's blocks and frees its plan-private blocks; later
  * kernel calls on any stream wait for `stream` to pass this point before touching them. */
 spq_status spq_plan_release(spq_ctx *ctx, spq_plan *plan, void *stream);

@@ -113,32 +113,41 @@ void build_prefill_work(const PlanHost& p, const WorkOpts& o, int job_begin, int
   if (o.persistent) schedule(cost, o.units, o.num_sms, w);
 }
 
-void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_end, AttnWorkHost* w) {
+void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_end, AttnWorkHost* w,
+                     const JoinPhase* ph) {
   *w = AttnWorkHost();
   const int64_t base = p.query_join_row_off[q_begin];
   struct QTile {
     int32_t row0, n_rows, tb, te;
+    bool force;  // write partials even when one piece covers it (its other phase adds more)
   };
   std::vector<QTile> qt;
+  const int sel = ph ? ph->sel : 0;
   for (size_t si = 0; si < p.segs.size(); ++si) {
     const Segment& c = p.segs[si];
     if (c.kind != kCross || c.query < q_begin || c.query >= q_end) continue;
-    int32_t first = -1;
+    int32_t first = -1, last = -1;
     // the query's segments precede its cross segment contiguously
     size_t s0 = si;
     while (s0 > 0 && p.segs[s0 - 1].query == c.query) --s0;
+    bool has_remote = false;
+    for (size_t k = s0; k < si; ++k) has_remote |= ph && ph->remote[k] != 0;
+    if (sel == 2 && !has_remote) continue;  // nothing of this query arrives by the exchange
     for (size_t k = s0; k < si; ++k) {
       const Segment& s = p.segs[k];
+      if (sel == 1 && ph->remote[k]) continue;  // phase 1: the segments this rank holds
+      if (sel == 2 && !ph->remote[k]) continue;  // phase 2: the received fragments
       const int32_t t = s.kind == kPrefix ? add_tiles(p, s, o.bs, 0, 0, 0, w)
                                           : add_tiles(p, s, o.bs, s.pos0, s.pos0, 0, w);
       if (first < 0) first = t;
+      last = static_cast<int32_t>(w->tiles.size());
     }
-    const int32_t tc = add_tiles(p, c, o.bs, c.pos0, 0, 1, w);
+    const int32_t tc = sel == 2 ? -1 : add_tiles(p, c, o.bs, c.pos0, 0, 1, w);
     if (first < 0) first = tc;
     const int64_t row_off = p.query_join_row_off[c.query] - base;
     for (int32_t r = 0; r < c.tok_len; r += kTileRows) {
       QTile q{static_cast<int32_t>(row_off + r), std::min(kTileRows, c.tok_len - r), first,
-              tc + r / kTileKeys + 1};
+              sel == 2 ? last : tc + r / kTileKeys + 1, has_remote};
       qt.push_back(q);
     }
     const double before = static_cast<double>(c.pos0);
@@ -227,18 +236,29 @@ void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_en
     for (int u = 0; u < o.units; ++u, ++pi) {
       const std::vector<Piece>& pieces = all[pi];
       const int np = static_cast<int>(pieces.size());
-      if (np > 1) w->combine.push_back({q.row0, q.n_rows, w->n_parts, np, u * hpu, hpu});
+      const bool part = np > 1 || q.force;
+      const int32_t pb = (ph ? ph->part_base : 0) + w->n_parts;  // global partial slot of piece 0
+      if (part) {
+        if (sel == 1 && q.force) {
+          (*ph->ranges)[{q.row0, u}] = {pb, np};  // merged after phase 2
+        } else if (sel == 2) {
+          const std::pair<int32_t, int32_t> r1 = ph->ranges->at({q.row0, u});
+          w->combine.push_back({q.row0, q.n_rows, r1.first, r1.second, u * hpu, hpu, pb, np});
+        } else {
+          w->combine.push_back({q.row0, q.n_rows, pb, np, u * hpu, hpu, 0, 0});
+        }
+      }
       for (int k = 0; k < np; ++k) {
         WorkItem it{};
         it.row0 = q.row0;
         it.n_rows = q.n_rows;
         it.tile_begin = pieces[k].t0;
         it.tile_end = pieces[k].t1;
-        it.part = np > 1 ? w->n_parts + k : -1;
+        it.part = part ? pb + k : -1;
         per_cta[pieces[k].cta].push_back(static_cast<int32_t>(w->items.size()) * o.units + u);
         w->items.push_back(it);
       }
-      if (np > 1) w->n_parts += np;
+      if (part) w->n_parts += np;
     }
   }
   int used = grid;

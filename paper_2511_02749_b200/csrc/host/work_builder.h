@@ -1,6 +1,8 @@
 // work_builder.h — turn a plan's segments into attention work lists.
 #pragma once
 #include <cstdint>
+#include <map>
+#include <utility>
 #include <vector>
 
 #include "../kernels/work.h"
@@ -33,7 +35,21 @@ struct WorkOpts {
 // Prefill jobs [job_begin, job_end): rows relative to job_row_off[job_begin].
 void build_prefill_work(const PlanHost& p, const WorkOpts& o, int job_begin, int job_end,
                         AttnWorkHost* w);
-// Joins of queries [q_begin, q_end): rows relative to query_join_row_off[q_begin].
-void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_end, AttnWorkHost* w);
+// W > 1 joins in two launches around the fragment-KV exchange: sel 1 = the
+// segments this rank holds (prefix, local fragments, cross), sel 2 = the received fragments.
+// remote[s] marks plan segment s as received. A query with received fragments writes partials
+// in both phases (ranges[(row0, unit)] = its phase-1 (first slot, count)), merged by phase 2's
+// combine list; partial slots of phase 2 start at part_base (= phase 1's n_parts).
+struct JoinPhase {
+  int sel;
+  const std::vector<uint8_t>& remote;
+  int32_t part_base;
+  std::map<std::pair<int32_t, int32_t>, std::pair<int32_t, int32_t>>* ranges;
+};
+
+// Joins of queries [q_begin, q_end): rows relative to query_join_row_off[q_begin]. ph == null: one
+// launch over every segment.
+void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_end, AttnWorkHost* w,
+                     const JoinPhase* ph = nullptr);
 
 }  // namespace spq

@@ -34,8 +34,10 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineDesc* __restr
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // grid.z splits the 128 rows of a tile into groups of blockDim/32 rows: one warp per row
   for (int r = blockIdx.z * (blockDim.x / 32) + warp; r < cd.n_rows; r += gridDim.z * (blockDim.x / 32)) {
-    const int64_t base = (static_cast<int64_t>(cd.part_base) * cd.n_heads + blockIdx.y) * kTileRows + r;
     const int64_t pstride = static_cast<int64_t>(cd.n_heads) * kTileRows;  // next split, same (head, row)
+    const int64_t base = (static_cast<int64_t>(cd.part_base) * cd.n_heads + blockIdx.y) * kTileRows + r;
+    const int64_t base2 = (static_cast<int64_t>(cd.part_base2) * cd.n_heads + blockIdx.y) * kTileRows + r;
+    const int n_all = cd.n_split + cd.n_split2;
     float m = -INFINITY;
     float acc[E];
 #pragma unroll
@@ -43,13 +45,14 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineDesc* __restr
     float tot = 0.f;
     // up to 8 splits with every load issued before the arithmetic (latency-bound otherwise)
     constexpr int kU = 8;
-    for (int s0 = 0; s0 < cd.n_split; s0 += kU) {
+    for (int s0 = 0; s0 < n_all; s0 += kU) {
       float ls[kU];
       float2 ov[kU][E / 2];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const bool ok = s0 + u < cd.n_split;
-        const int64_t pidx = base + (s0 + u) * pstride;
+        const int si = s0 + u;
+        const bool ok = si < n_all;
+        const int64_t pidx = si < cd.n_split ? base + si * pstride : base2 + (si - cd.n_split) * pstride;
         ls[u] = ok ? lsepart[pidx] : -INFINITY;
 #pragma unroll
         for (int e = 0; e < E; e += 2)

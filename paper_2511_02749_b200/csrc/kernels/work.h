@@ -36,9 +36,11 @@ struct WorkItem {
 };
 
 // Split-KV partials are per work unit: partial slot p holds the unit's heads, rows
-// ((p * n_heads + x) * kTileRows + r) of opart / lsepart (x = head - head0).
+// ((p * n_heads + x) * kTileRows + r) of opart / lsepart (x = head - head0). A (q tile, unit)'s
+// partials are the slots [part_base, part_base + n_split) followed by [part_base2, part_base2 +
+// n_split2) (the second range: the remote-segment phase of a W > 1 join), merged in that order.
 struct CombineDesc {
-  int32_t row0, n_rows, part_base, n_split, head0, n_heads;
+  int32_t row0, n_rows, part_base, n_split, head0, n_heads, part_base2, n_split2;
 };
 
 }  // namespace spq

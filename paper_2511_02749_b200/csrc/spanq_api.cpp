@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
+#include <unordered_set>
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
@@ -111,6 +113,9 @@ struct spq_plan {
   uint8_t* dbuf = nullptr;
   size_t off_ppos = 0, off_pslot = 0, off_pad = 0, off_jpos = 0, off_jslot = 0, off_send = 0, off_recv = 0;
   DevWork pw, jw;
+  bool phased = false;  // W > 1 with received fragments: the join also as two phases (jw1, jw2)
+  DevWork jw1, jw2;
+  spq::AttnWorkHost jw1_host, jw2_host;
   float* opart = nullptr;
   float* lsepart = nullptr;
   std::vector<uint8_t> padded_layers;
@@ -546,6 +551,22 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
   spq::build_prefill_work(H, o, 0, static_cast<int>(H.jobs.size()), &p->pw_host);
   lap("prefill work");
   spq::build_join_work(H, o, 0, H.n_queries, &p->jw_host);
+  // W > 1: the join again as two phases around the exchange (held segments, then the received
+  // fragments), for spq_join_phase; needs split partials (the persistent bf16 path)
+  if (is_gpu(c) && o.allow_split && o.persistent && !H.recv_blocks.empty()) {
+    std::vector<uint8_t> remote(H.segs.size(), 0);
+    std::unordered_set<int32_t> rs(H.recv_blocks.begin(), H.recv_blocks.end());
+    for (size_t i = 0; i < H.segs.size(); ++i) {
+      const spq::Segment& sg = H.segs[i];
+      remote[i] = sg.kind == spq::kFrag && sg.n_blocks > 0 && rs.count(H.blocks[sg.block_off]) ? 1 : 0;
+    }
+    std::map<std::pair<int32_t, int32_t>, std::pair<int32_t, int32_t>> ranges;
+    const spq::JoinPhase ph1{1, remote, 0, &ranges};
+    spq::build_join_work(H, o, 0, H.n_queries, &p->jw1_host, &ph1);
+    const spq::JoinPhase ph2{2, remote, p->jw1_host.n_parts, &ranges};
+    spq::build_join_work(H, o, 0, H.n_queries, &p->jw2_host, &ph2);
+    p->phased = true;
+  }
   lap("join work");
   if (prof) {
     for (const spq::AttnWorkHost* wh : {&p->pw_host, &p->jw_host}) {
@@ -621,11 +642,16 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
     };
     add_work(p->pw_host, &p->pw);
     add_work(p->jw_host, &p->jw);
+    if (p->phased) {
+      add_work(p->jw1_host, &p->jw1);
+      add_work(p->jw2_host, &p->jw2);
+    }
     // one device allocation: packed arrays, then the split-KV partials (O, LSE)
     size_t bytes = std::max<size_t>(pk.size, 256);
     size_t off_opart = 0, off_lsepart = 0;
-    if (p->jw.n_parts > 0) {
-      const size_t rows = static_cast<size_t>(p->jw.n_parts) * heads_per_unit(c) * spq::kTileRows;
+    const int32_t n_parts = std::max(p->jw.n_parts, p->jw1.n_parts + p->jw2.n_parts);
+    if (n_parts > 0) {
+      const size_t rows = static_cast<size_t>(n_parts) * heads_per_unit(c) * spq::kTileRows;
       off_opart = align_up(bytes, 1024);
       off_lsepart = align_up(off_opart + rows * c->cfg.head_dim * sizeof(float), 1024);
       bytes = off_lsepart + rows * sizeof(float);
@@ -643,7 +669,7 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
     CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->dbuf), bytes, st));
     CUDA_TRY(cudaMemcpyAsync(p->dbuf, c->staging, pk.size, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaEventRecord(c->staging_ev, st));
-    if (p->jw.n_parts > 0) {
+    if (n_parts > 0) {
       p->opart = reinterpret_cast<float*>(p->dbuf + off_opart);
       p->lsepart = reinterpret_cast<float*>(p->dbuf + off_lsepart);
     }
@@ -757,8 +783,11 @@ spq_status spq_prefill_jobs(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, i
   return SPQ_OK;
 }
 
-spq_status spq_join(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b, const void* q, const void* k,
-                    const void* v, void* o, float* lse, void* stream) {
+namespace {
+// mode -1: the whole join of queries [a, b) (spq_join); 0 / 1: phase 0 / 1 of a phased plan's
+// join (spq_join_phase: K1 + the held segments, then the received fragments + the combine)
+spq_status join_impl(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b, const void* q, const void* k,
+                     const void* v, void* o, float* lse, void* stream, int mode) {
   spq_status s = check_call(c, p, layer);
   if (s != SPQ_OK) return s;
   const int32_t nq = p->host.n_queries;
@@ -770,17 +799,25 @@ spq_status spq_join(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b
   if (s != SPQ_OK) return s;
   const int64_t r0 = p->host.query_join_row_off[a], r1 = p->host.query_join_row_off[b];
   if (r0 == r1) return SPQ_OK;  // only queries homed on other ranks
-  s = kv_write(c, p, layer, k, v, at<int32_t>(p, p->off_jpos) + r0, at<int64_t>(p, p->off_jslot) + r0, r1 - r0, st);
-  if (s != SPQ_OK) return s;
+  if (mode != 1) {
+    s = kv_write(c, p, layer, k, v, at<int32_t>(p, p->off_jpos) + r0, at<int64_t>(p, p->off_jslot) + r0, r1 - r0, st);
+    if (s != SPQ_OK) return s;
+  }
   spq::AttnArgs args{};
   TempWork tw;
   float* opart = p->opart;
   float* lsepart = p->lsepart;
   const bool full = (a == 0 && b == nq);
   DevWork w;
-  if (full) {
+  int32_t part_extent = 0;  // partial slots the launch may address
+  if (mode >= 0) {
+    w = mode == 0 ? p->jw1 : p->jw2;
+    fill_attn(c, p, w, &args);
+    part_extent = p->jw1.n_parts + p->jw2.n_parts;
+  } else if (full) {
     w = p->jw;
     fill_attn(c, p, p->jw, &args);
+    part_extent = w.n_parts;
   } else {
     spq::AttnWorkHost h;
     spq::WorkOpts o = work_opts(c, false);
@@ -793,6 +830,7 @@ spq_status spq_join(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b
     tmp_view.lsepart = nullptr;
     fill_attn(c, &tmp_view, tw.w, &args);
     w = tw.w;
+    part_extent = w.n_parts;
   }
   args.opart = opart;
   args.lsepart = lsepart;
@@ -813,7 +851,7 @@ spq_status spq_join(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b
       args.tmap_o = &omap;
     }
     if (w.n_parts > 0 && opart != nullptr) {
-      s = make_partmap(c, opart, w.n_parts, &pmap);
+      s = make_partmap(c, opart, part_extent, &pmap);
       if (s != SPQ_OK) return s;
       args.tmap_op = &pmap;
     }
@@ -827,7 +865,7 @@ spq_status spq_join(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b
   }
   if (w.n_combine > 0) {
     spq::CombineArgs ca{};
-    ca.desc = reinterpret_cast<const spq::CombineDesc*>((full ? p->dbuf : tw.buf) + w.combine);
+    ca.desc = reinterpret_cast<const spq::CombineDesc*>((full || mode >= 0 ? p->dbuf : tw.buf) + w.combine);
     ca.n_desc = w.n_combine;
     ca.opart = opart;
     ca.lsepart = lsepart;
@@ -843,6 +881,23 @@ spq_status spq_join(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b
   }
   if (tw.buf) CUDA_TRY(cudaFreeAsync(tw.buf, st));
   return SPQ_OK;
+}
+}  // namespace
+
+spq_status spq_join(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b, const void* q, const void* k,
+                    const void* v, void* o, float* lse, void* stream) {
+  return join_impl(c, p, layer, a, b, q, k, v, o, lse, stream, -1);
+}
+
+spq_status spq_join_phase(spq_ctx* c, spq_plan* p, int32_t layer, int32_t phase, const void* q, const void* k,
+                          const void* v, void* o, float* lse, void* stream) {
+  if (phase != 0 && phase != 1) return fail(SPQ_EINVAL, "phase must be 0 or 1");
+  spq_status s = check_call(c, p, layer);
+  if (s != SPQ_OK) return s;
+  const int32_t nq = p->host.n_queries;
+  if (p->phased) return join_impl(c, p, layer, 0, nq, q, k, v, o, lse, stream, phase);
+  // not split (no received fragments, or a path without partials): the whole join in phase 1
+  return phase == 0 ? SPQ_OK : join_impl(c, p, layer, 0, nq, q, k, v, o, lse, stream, -1);
 }
 
 static spq_status exchange(spq_ctx* c, spq_plan* p, int32_t layer, int32_t peer, void* buf, void* stream,

@@ -102,6 +102,8 @@ SIGNATURES = {
                                    C.c_void_p]),
     "spq_join": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "spq_join_phase": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "spq_exchange_pack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
                                     C.c_void_p]),
     "spq_exchange_unpack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
@@ -255,6 +257,11 @@ class Plan:
         a, b = (0, self.n_queries) if queries is None else queries
         _check(lib().spq_join(self.ctx.handle, self.handle, layer, a, b, _ptr(q), _ptr(k), _ptr(v),
                               _ptr(o), _ptr(lse), _stream_ptr(stream)))
+
+    def join_phase(self, layer, phase, q, k, v, o, lse=None, stream=None):
+        """Phase 0 / 1 of the join of all home queries (W > 1: around the fragment-KV exchange)."""
+        _check(lib().spq_join_phase(self.ctx.handle, self.handle, layer, phase, _ptr(q), _ptr(k), _ptr(v),
+                                    _ptr(o), _ptr(lse), _stream_ptr(stream)))
 
     def release(self, stream=None):
         if not self.released:

@@ -21,8 +21,11 @@ from test_gpu_parity import check, check_lse
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("dtype,world", [("bf16", 2), ("fp32", 2), ("bf16", 3)])
-def test_partitioned_exchange_parity(cuda_dev, dtype, world):
+@pytest.mark.parametrize("dtype,world,phased", [("bf16", 2, False), ("fp32", 2, False), ("bf16", 3, False),
+                                                ("bf16", 2, True), ("bf16", 3, True), ("fp32", 2, True)])
+def test_partitioned_exchange_parity(cuda_dev, dtype, world, phased):
+    # phased: each home rank runs join phase 0 (held segments) BEFORE the exchange — with its
+    # received blocks poisoned with NaN, so reading one early would show — then phase 1 after it
     import torch
 
     fp32 = dtype == "fp32"
@@ -58,6 +61,19 @@ def test_partitioned_exchange_parity(cuda_dev, dtype, world):
         ctxs.append(ctx)
         plans.append(plan)
         views.append(view)
+    joins = []
+    for r in range(world):
+        jtok = runner.join_tokens(views[r], qs)
+        oj = torch.empty((len(jtok), sh.hq, sh.d), dtype=torch.float32, device=cuda_dev)
+        lj = torch.empty((len(jtok), sh.hq), dtype=torch.float32, device=cuda_dev)
+        joins.append((*runner.gather(tab, jtok, cuda_dev), oj, lj))
+        if phased:
+            rid = [views[r]["recv"].get(p, np.zeros(0, np.int32)) for p in range(world)]
+            rid = torch.from_numpy(np.concatenate(rid).astype(np.int64)).to(cuda_dev)
+            if len(rid):
+                ctxs[r].k_pool[0, rid] = float("nan")
+                ctxs[r].v_pool[0, rid] = float("nan")
+            plans[r].join_phase(0, 0, *joins[r])
     # exchange: rank r packs for p, p unpacks from r (device buffers stand in for NCCL)
     dt = ctxs[0].k_pool.dtype
     be = parallel.block_elems(sh)
@@ -81,18 +97,17 @@ def test_partitioned_exchange_parity(cuda_dev, dtype, world):
     # joins of each rank's home queries
     n_join = 0
     for r in range(world):
-        view = views[r]
-        jtok = runner.join_tokens(view, qs)
-        oj = torch.empty((len(jtok), sh.hq, sh.d), dtype=torch.float32, device=cuda_dev)
-        lj = torch.empty((len(jtok), sh.hq), dtype=torch.float32, device=cuda_dev)
-        q, k, v = runner.gather(tab, jtok, cuda_dev)
-        plans[r].join(0, q, k, v, oj, lj)
+        q, k, v, oj, lj = joins[r]
+        if phased:
+            plans[r].join_phase(0, 1, q, k, v, oj, lj)
+        else:
+            plans[r].join(0, q, k, v, oj, lj)
         torch.cuda.synchronize()
         home = [i for i in range(len(qs)) if i % world == r]
         exp = [oatt.join_rows(*flat[i], eq, ek, ev, sh.rope_base) for i in home]
         check(oj, np.concatenate([e[0] for e in exp]), fp32, f"rank {r} join O")
         check_lse(lj, np.concatenate([e[1] for e in exp]), fp32, f"rank {r} join LSE")
-        n_join += len(jtok)
+        n_join += len(q)
     assert n_join == sum(len(q.cross) for q in qs)
     for p, c in zip(plans, ctxs):
         p.release()
