@@ -40,11 +40,11 @@ struct TreeParser {
     if (n.op != SPQ_TOKENS || n.num_children != 0) return fail("expected TOKENS leaf");
     if (n.tok_len <= 0) return fail("empty token leaf");
     if (n.tok_begin < 0 || n.tok_begin + n.tok_len > q.num_tokens) return fail("token range out of bounds");
-    for (int64_t t = 0; t < n.tok_len; ++t) {
-      const int32_t v = q.tokens[n.tok_begin + t];
-      if (v < 0) return fail("negative token id");
-      out->push_back(v);
-    }
+    const int32_t* t0 = q.tokens + n.tok_begin;
+    int32_t mn = 0;
+    for (int64_t t = 0; t < n.tok_len; ++t) mn = std::min(mn, t0[t]);
+    if (mn < 0) return fail("negative token id");
+    out->insert(out->end(), t0, t0 + n.tok_len);
     return true;
   }
   // fragments under a PLUS node (nested PLUS flattened); *next = index after it
@@ -166,7 +166,7 @@ Store::Store(int64_t num_blocks, int block_size, const Digest& root)
   for (auto& m : meta_) m = Meta{Digest{}, 0, 0, false};
   pins_.assign(num_blocks, 0);
   pinned_mark_.assign(num_blocks, 0);
-  for (int64_t b = 0; b < num_blocks; ++b) free_.insert(static_cast<int32_t>(b));
+  free_.init(num_blocks);
 }
 
 int64_t Store::pinned_count() const {
@@ -189,8 +189,7 @@ void Store::set_evictable(int32_t b, bool on) {
 
 int32_t Store::alloc(bool* ok) {
   if (!free_.empty()) {
-    const int32_t b = *free_.begin();
-    free_.erase(free_.begin());
+    const int32_t b = free_.pop_lowest();
     if (journaling_) journal_.push_back({kUndoFreePop, b, Meta{}});
     return b;
   }
@@ -536,15 +535,21 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
   auto rows = [&](const Segment& s, int32_t begin, std::vector<int32_t>* pos,
                   std::vector<int64_t>* slot, std::vector<int32_t>* segi, int32_t si) {
     const int32_t p0 = s.kind == kCross ? s.pos0 : 0;
+    const size_t n0 = pos->size();
+    const size_t n = static_cast<size_t>(std::max(0, s.tok_len - begin));
+    pos->resize(n0 + n);
+    slot->resize(n0 + n);
+    segi->resize(n0 + n, si);
+    int32_t* pp = pos->data() + n0;
+    int64_t* sp = slot->data() + n0;
     for (int32_t b = begin / bs; b * bs < s.tok_len; ++b) {
       const int32_t t0 = std::max(begin, b * bs), t1 = std::min(s.tok_len, (b + 1) * bs);
       const bool w = P.block_write[s.block_off + b] != 0;
       const int64_t base = static_cast<int64_t>(P.blocks[s.block_off + b]) * bs - static_cast<int64_t>(b) * bs;
       for (int32_t t = t0; t < t1; ++t) {
-        pos->push_back(p0 + t);
-        slot->push_back(w ? base + t : -1);
+        *pp++ = p0 + t;
+        *sp++ = w ? base + t : -1;
       }
-      segi->insert(segi->end(), static_cast<size_t>(t1 - t0), si);
     }
   };
   {

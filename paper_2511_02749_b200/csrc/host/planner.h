@@ -5,6 +5,7 @@
 // cross chain), prefix-scan / all-or-nothing lookup, in-plan dedupe, lowest-id allocation, LRU
 // eviction of unpinned blocks, pinning, rollback on ENOMEM. Readings R8-R13.
 #pragma once
+#include <algorithm>
 #include <cstdint>
 #include <set>
 #include <string>
@@ -73,6 +74,40 @@ void chain(char tag, const Digest& seed, const int32_t* tok, int64_t n, int bs,
            std::vector<Digest>* out);
 Digest join_fold(const Digest& h_last, const std::vector<Digest>& frag_lasts);
 
+// Free block ids with O(1) amortized "pop the lowest" (a bitmap plus a hint: every word before
+// `hint_` is empty) — the lowest-id allocation policy (R12) without a tree node per block.
+class FreeSet {
+ public:
+  void init(int64_t n) {
+    bits_.assign(static_cast<size_t>((n + 63) / 64), ~0ULL);
+    if (n % 64) bits_.back() = (1ULL << (n % 64)) - 1;
+    count_ = n;
+    hint_ = 0;
+  }
+  bool empty() const { return count_ == 0; }
+  int64_t size() const { return count_; }
+  void insert(int32_t b) {
+    uint64_t& w = bits_[static_cast<size_t>(b) >> 6];
+    const uint64_t m = 1ULL << (b & 63);
+    if (w & m) return;
+    w |= m;
+    ++count_;
+    hint_ = std::min<int64_t>(hint_, b >> 6);
+  }
+  int32_t pop_lowest() {  // requires !empty()
+    while (bits_[static_cast<size_t>(hint_)] == 0) ++hint_;
+    uint64_t& w = bits_[static_cast<size_t>(hint_)];
+    const int bit = __builtin_ctzll(w);
+    w &= w - 1;
+    --count_;
+    return static_cast<int32_t>(hint_ * 64 + bit);
+  }
+
+ private:
+  std::vector<uint64_t> bits_;
+  int64_t count_ = 0, hint_ = 0;
+};
+
 class Store {
  public:
   Store(int64_t num_blocks, int block_size, const Digest& root);
@@ -122,7 +157,7 @@ class Store {
   std::unordered_map<Digest, int32_t, DigestHash> index_;
   std::vector<Meta> meta_;
   std::vector<int32_t> pins_;
-  std::set<int32_t> free_;
+  FreeSet free_;
   std::set<std::pair<int64_t, int32_t>> evictable_;  // (last_use, id), resident & unpinned
   int64_t plan_no_ = 0;
   StoreStats stats_;

@@ -163,21 +163,20 @@ def _stream_ptr(stream) -> Optional[int]:
     return int(stream)
 
 
-_NODE_DT = np.dtype({"names": ["op", "nc", "b", "n"], "formats": [np.int32, np.int32, np.int64, np.int64],
-                     "offsets": [0, 4, 8, 16], "itemsize": C.sizeof(spq_node)})
-
 
 class _QueryBuf:
     """Keeps the ctypes arrays of one spq_query alive."""
 
     def __init__(self, nodes: np.ndarray, tokens: np.ndarray):
         nodes = np.asarray(nodes, dtype=np.int64).reshape(-1, 4)
-        self.nodes = (spq_node * max(1, len(nodes)))()
-        rec = np.zeros(len(nodes), dtype=_NODE_DT)
-        rec["op"], rec["nc"], rec["b"], rec["n"] = nodes[:, 0], nodes[:, 1], nodes[:, 2], nodes[:, 3]
-        C.memmove(self.nodes, rec.ctypes.data, rec.nbytes)
+        # spq_node = {int32 op, int32 num_children, int64 tok_begin, int64 tok_len}: three
+        # little-endian int64 words per node (op | num_children << 32, tok_begin, tok_len)
+        assert C.sizeof(spq_node) == 24
+        self.nodes = np.empty((max(1, len(nodes)), 3), dtype=np.int64)
+        self.nodes[: len(nodes), 0] = (nodes[:, 0] & 0xFFFFFFFF) | (nodes[:, 1] << 32)
+        self.nodes[: len(nodes), 1:] = nodes[:, 2:]
         self.tokens = np.ascontiguousarray(tokens, dtype=np.int32)
-        self.q = spq_query(C.cast(self.nodes, C.POINTER(spq_node)), len(nodes),
+        self.q = spq_query(self.nodes.ctypes.data_as(C.POINTER(spq_node)), len(nodes),
                            self.tokens.ctypes.data_as(_I32P), len(self.tokens))
 
 
