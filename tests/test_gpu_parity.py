@@ -402,3 +402,35 @@ def test_read_blocks(cuda_dev):
         ctx.read_blocks(0, [300])
     res.plan.release()
     ctx.close()
+
+
+def test_full_size_c3_warm_sampled_rows(cuda_dev):
+    """configs[2] at full size: C3's query right after its C2-like warm-up query (12 of 16
+    fragments cached, permuted, 4 new, new cross), in the bench's launch configuration: the hits
+    are read at their new Δ_f without being rewritten; sampled join rows against the oracle's
+    dense definition over the query as written, plus hit statistics."""
+    import torch
+
+    w = inputs.c3()
+    s = w.shape
+    ctx = spanq.Context(s, 1024, device=0, max_position=1 << 15, out_dtype="fp32")
+    tabs = [runner.device_tables(s, 0, w.seed, cuda_dev)]
+    for q0 in w.warmup_queries:
+        runner.run_pass(ctx, [q0], tabs, cuda_dev, release=True)
+    st0 = ctx.stats()
+    res = runner.run_pass(ctx, w.queries, tabs, cuda_dev)
+    torch.cuda.synchronize()
+    st1 = ctx.stats()
+    q = w.queries[0]
+    frag_tokens = sum(len(f) for f in q.fragments)
+    hit = st1["hit_tokens"] - st0["hit_tokens"]
+    # 12 of 16 fragments plus the full prefix blocks are hits (P:123 hit rate = hit / input tokens)
+    assert hit >= 0.75 * frag_tokens, (hit, frag_tokens)
+    eq, ek, ev = inputs.layer_tables(s, 0, w.seed)
+    g = np.random.default_rng(9)
+    rows = g.choice(len(q.cross), 12, replace=False)
+    heads = [1, 8, 30]
+    jo, _ = oatt.join_rows(q.prefix, q.fragments, q.cross, eq, ek, ev, s.rope_base, rows, heads)
+    check(res.o_join[torch.from_numpy(rows).to(cuda_dev)][:, heads], jo, False, "C3 warm join sampled")
+    res.plan.release()
+    ctx.close()
