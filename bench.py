@@ -386,8 +386,12 @@ def measure_judge(dev, stream, flush, args, reps: int = 5):
     cand_only = inputs.SpanQuery(np.zeros(0, np.int32), list(q.fragments), q.cross[:1])  # fills the candidates
     toks = np.concatenate(list(q.fragments) + [q.cross])
     dense = inputs.SpanQuery(toks[:-1], [], toks[-1:])
+    ctx.set_timing(True)
     cold_ms, cold_flops = ttft_l1(ctx, s, tab, dev, stream, flush, odt, w.queries, [], reps)
+    pre_ms, join_ms = ctx.last_attn_ms()  # attention kernels of the last cold repetition
+    pre_fl, join_fl = ttft_l1.last_flops
     warm_ms, warm_flops = ttft_l1(ctx, s, tab, dev, stream, flush, odt, w.queries, [cand_only], reps)
+    ctx.set_timing(False)
     dense_ms, dense_flops = ttft_l1(ctx, s, tab, dev, stream, flush, odt, [dense], [], reps)
     ctx.close()
     return {"workload": "C4 judge/generator (configs[3]): 8 x 2048 candidates + 512 judge prompt, 2B shape "
@@ -395,7 +399,9 @@ def measure_judge(dev, stream, flush, args, reps: int = 5):
             "cold_ttft_l1_ms": cold_ms, "cold_flops": cold_flops, "cold_tflops": cold_flops / (cold_ms / 1e3) / 1e12,
             "warm_ttft_l1_ms": warm_ms, "warm_flops": warm_flops, "warm_tflops": warm_flops / (warm_ms / 1e3) / 1e12,
             "dense_causal_ttft_l1_ms": dense_ms, "dense_causal_flops": dense_flops,
-            "dense_over_cold": dense_ms / cold_ms, "dense_over_warm": dense_ms / warm_ms}
+            "dense_over_cold": dense_ms / cold_ms, "dense_over_warm": dense_ms / warm_ms,
+            "prefill_kernel_ms": pre_ms, "prefill_kernel_tflops": pre_fl / (pre_ms / 1e3) / 1e12,
+            "join_kernel_ms": join_ms, "join_kernel_tflops": join_fl / (join_ms / 1e3) / 1e12}
 
 
 def measure_reposition(ctx, s, stream, flush, n_blocks, hbm_gbs, reps: int = 10):
@@ -476,9 +482,12 @@ def ttft_l1(ctx, s, tab, dev, stream, flush, odt, queries, warm, reps: int = 5):
             b.record(stream)
             stream.synchronize()
             ms.append(a.elapsed_time(b))
+        run.flops = (v["prefill_flops"], v["join_flops"])
         return statistics.median(ms[1:]), v["prefill_flops"] + v["join_flops"]
 
-    return run(queries, warm)
+    out = run(queries, warm)
+    ttft_l1.last_flops = run.flops  # (prefill, join) algorithmic FLOPs of the timed plan
+    return out
 
 
 def measure_locality(ctx, s, tab, dev, stream, flush, args, reps: int = 5):
