@@ -25,6 +25,8 @@
 //   * Q: slot x = head x, prepared by warps 12-15 (TMA load of the pre-RoPE tile, in-place
 //     rotate-half with the fp64-built fp32 table and an fp32 angle recurrence, packed fp32x2);
 //     an epoch (an item or a change of rot_delta) reloads it once its last S MMA has completed.
+//     Joins (an epoch per fragment segment) keep a 2-deep ring per head whose second slot is the
+//     staging area, so the next fragment's Q is ready a whole epoch ahead.
 //   * softmax (warps 4-7 head A, 8-11 head B; thread = row = TMEM lane): one pass per sub-tile
 //     (LDTM.x64, FMNMX3 row max, exp2 on MUFU, packed FFMA2/FADD2, STTM.x32); O rescaled only
 //     when the running max grows by > 8 (log2), so P <= 256; then the epilogue (TMEM -> swizzled
@@ -66,7 +68,7 @@ struct TcSmem {
   alignas(1024) uint8_t v[kVSlots][kChunks][kSubBytes];  // ring of 64-key V sub-tiles
   // prefill: epilogue transpose, 2 x 4 KB per softmax warp. join: the second Q slot of each
   // head (q2), so the next fragment's counter-rotated Q is prepared a whole epoch ahead; the
-  // join epilogue stores from registers instead
+  // join epilogue stages in the Q slot of its item's last epoch instead
   alignas(1024) float stage[8][2][32 * 32];
   uint64_t kv_full[2][kKSlots], kv_empty[2][kKSlots];  // [K, V][slot] (V uses the first kVSlots)
   uint64_t q_full[2][2], q_empty[2][2], q_load[2][2];  // [head][Q ring slot]
