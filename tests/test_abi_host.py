@@ -32,6 +32,10 @@ def test_no_gpu_calls_fail_loudly_on_host_only_ctx():
     with pytest.raises(spanq.SpanqError) as e:
         p.prefill(0, None, None, None, None)
     assert e.value.status == spanq.ESTATE
+    for phase, status in [(0, spanq.ESTATE), (1, spanq.ESTATE), (2, spanq.EINVAL), (-1, spanq.EINVAL)]:
+        with pytest.raises(spanq.SpanqError) as e:
+            p.join_phase(0, phase, None, None, None, None)
+        assert e.value.status == status
     p.release()
 
 
