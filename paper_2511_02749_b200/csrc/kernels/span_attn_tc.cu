@@ -280,7 +280,6 @@ __device__ void run_mma(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_b
   for (int code; (code = src.next()) >= 0;) {
     const Unit u = decode(P, code);
     if (x >= u.n_heads) continue;  // unpaired launch: the B issuer idles
-    const bool two = u.n_heads == 2;
     const int tb = u.w.tile_begin, te = u.w.tile_end;
     auto nsub = [&](int t) { return a.tiles[t].n_valid > 64 ? 2 : 1; };
     auto advance = [&](SubCursor& c) {
@@ -295,7 +294,6 @@ __device__ void run_mma(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_b
     auto release_q = [&]() {
       const int sl = q_slot(J, qcur);
       mma_commit(&S.q_empty[x][sl]);
-      if (!two) mma_commit(&S.q_empty[1][sl]);  // an unpaired launch's A issuer also frees B's slot
     };
     auto issue_s = [&]() {
       const int t = cs.t;
@@ -785,8 +783,12 @@ __device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_
         }
         __syncwarp();
       }
-      for (int x = 0; x < 2; ++x) {
-        if (x < u.n_heads && work) {  // single-head units leave the B slot untouched
+      // an unpaired launch never touches slot B: no issuer waits on it, and waiting on its empty
+      // barrier (committed once per epoch by the A issuer) could be lapped — the A issuer can
+      // finish a one-sub-tile epoch and complete the next phase before a late warp arrives, and
+      // a parity wait then blocks on a phase that needs this warp's next Q (a deadlock)
+      for (int x = 0; x < u.n_heads; ++x) {
+        if (work) {
           if (x == 1 && wq == 0 && !b_issued) {
             mbar_wait(&S.q_empty[1][sl], epar);
             if (tr) trace(P, 4, tc, 41);  // 41: slot free for head B
