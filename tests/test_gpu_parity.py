@@ -434,3 +434,15 @@ def test_full_size_c3_warm_sampled_rows(cuda_dev):
     check(res.o_join[torch.from_numpy(rows).to(cuda_dev)][:, heads], jo, False, "C3 warm join sampled")
     res.plan.release()
     ctx.close()
+
+
+@pytest.mark.parametrize("hq,hkv,d", [(3, 3, 64), (6, 2, 128), (8, 2, 64)])
+def test_many_tiny_epochs_stress(cuda_dev, hq, hkv, d):
+    """Many one-sub-tile Q epochs (fragments of 1-20 tokens, many queries) in unpaired (odd GQA
+    group) and paired launches, repeated: the Q-ring barrier protocol under its tightest timing
+    (the unpaired slot-B wait once lapped and deadlocked here)."""
+    sh = inputs.Shape(hq=hq, hkv=hkv, d=d, block_size=16, vocab=128)
+    for rep in range(3):
+        qs = inputs.random_queries(300 + rep, 12, vocab=128, max_frag=6, max_len=20, max_prefix=24,
+                                   max_cross=40, reuse_p=0.3)
+        run_and_check(inputs.Workload("tiny", sh, qs, 300 + rep), cuda_dev, nblk=2048)
