@@ -7,9 +7,9 @@
 // RoPE positions: span-local for fragments (reading R2), global for prefix/cross (§5.5
 // P:610). cos/sin come from the fp64-built table [max_pos][d/2] (float2).
 //
-// HBM-bound, no reuse: one thread moves one 16-byte vector of k and of v; the rotate-half
-// partner vector (element i <-> i + d/2) sits d/16 (bf16) or d/8 (fp32) lanes away in the same
-// warp and is fetched with one __shfl_xor. Loads/stores are 128-bit and fully coalesced per row.
+// HBM-bound, no reuse: one thread moves a 16-byte vector of k and of v from each half of d —
+// a rotate-half pair (element i <-> i + d/2) — so the (cos, sin) row is read once per pair and
+// no shuffle is needed. Loads/stores are 128-bit; a warp covers whole rows contiguously.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -57,7 +57,9 @@ struct Vec<float> {
   }
 };
 
-// G = d / N vectors per (row, head); lanes of one (row, head) are G consecutive lanes.
+// G = d / N vectors per (row, head). A thread owns vector u < G/2 of the first half of d and its
+// rotate-half partner u + G/2 (the same (cos, sin) pairs), so the table row is read once per
+// pair and no shuffle is needed; the lanes of one (row, head) are G/2 consecutive lanes.
 template <typename T, int D>
 __global__ void __launch_bounds__(256) rope_kv_write_kernel(
     const T* __restrict__ k, const T* __restrict__ v, const int32_t* __restrict__ pos,
@@ -66,57 +68,45 @@ __global__ void __launch_bounds__(256) rope_kv_write_kernel(
     int layer, const float2* __restrict__ rope) {
   constexpr int N = Vec<T>::N;
   constexpr int G = D / N;
-  static_assert(G <= 32 && (G & (G - 1)) == 0, "d/N must be a power of two <= 32");
+  constexpr int H = G / 2;  // threads per (row, head)
+  static_assert(G <= 32 && (G & (G - 1)) == 0 && G >= 2, "d/N must be a power of two in [2, 32]");
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t per_row = static_cast<int64_t>(hkv) * G;
+  const int64_t per_row = static_cast<int64_t>(hkv) * H;
   const int64_t total = rows * per_row;
   const int64_t layer_off = static_cast<int64_t>(layer) * nblk * hkv * bs * D;
-  // every lane takes part in the partner shuffle (whole warps), then branches
-  const bool main_row = gid < total;
-  int64_t r = 0, src = 0;
-  int h = 0, g = 0;
-  uint4 ku = make_uint4(0, 0, 0, 0), vu = make_uint4(0, 0, 0, 0);
-  int64_t s = -1;
-  int p = 0;
-  if (main_row) {
-    r = gid / per_row;
+  if (gid < total) {
+    const int64_t r = gid / per_row;
     const int rem = static_cast<int>(gid - r * per_row);
-    h = rem / G;
-    g = rem % G;
-    src = (r * hkv + h) * D + g * N;
-    // all loads issued up front and independent of each other (slot, pos, k, v; the table
-    // below): rows with slot -1 (rare: resident blocks) load k/v for nothing
-    s = slot[r];
-    p = pos[r];  // unconditional: not serialized behind the slot test
-    ku = __ldg(reinterpret_cast<const uint4*>(k + src));
-    vu = __ldg(reinterpret_cast<const uint4*>(v + src));
-  }
-  uint4 pu;
-  pu.x = __shfl_xor_sync(0xffffffffu, ku.x, G / 2);
-  pu.y = __shfl_xor_sync(0xffffffffu, ku.y, G / 2);
-  pu.z = __shfl_xor_sync(0xffffffffu, ku.z, G / 2);
-  pu.w = __shfl_xor_sync(0xffffffffu, ku.w, G / 2);
-  if (main_row) {
-    float x[N], y[N];
-    Vec<T>::unpack(ku, x);
-    Vec<T>::unpack(pu, y);
-    if (s >= 0) {
-      const bool first_half = g < G / 2;
-      const int i0 = (first_half ? g : g - G / 2) * N;  // pair index of element 0
-      const float4* cs = reinterpret_cast<const float4*>(rope + static_cast<int64_t>(p) * (D / 2) + i0);
-      float out[N];
+    const int h = rem / H, u = rem % H;
+    const int64_t src = (r * hkv + h) * D + u * N;
+    // every load issued up front, independent of the others (rows with slot -1 — resident
+    // blocks — load for nothing)
+    const int64_t s = slot[r];
+    const int p = pos[r];
+    const uint4 k0 = __ldg(reinterpret_cast<const uint4*>(k + src));
+    const uint4 k1 = __ldg(reinterpret_cast<const uint4*>(k + src + D / 2));
+    const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(v + src));
+    const uint4 v1 = __ldg(reinterpret_cast<const uint4*>(v + src + D / 2));
+    if (s < 0) return;
+    const float4* cs = reinterpret_cast<const float4*>(rope + static_cast<int64_t>(p) * (D / 2) + u * N);
+    float x[N], y[N], ox[N], oy[N];
+    Vec<T>::unpack(k0, x);
+    Vec<T>::unpack(k1, y);
 #pragma unroll
-      for (int e = 0; e < N; e += 2) {
-        const float4 c = __ldg(cs + e / 2);  // (cos, sin) of pairs i0+e, i0+e+1
-        // first half: x*cos - partner*sin ; second half: x*cos + partner*sin
-        out[e] = first_half ? fmaf(x[e], c.x, -y[e] * c.y) : fmaf(x[e], c.x, y[e] * c.y);
-        out[e + 1] = first_half ? fmaf(x[e + 1], c.z, -y[e + 1] * c.w) : fmaf(x[e + 1], c.z, y[e + 1] * c.w);
-      }
-      const int64_t blk = s / bs, off = s % bs;
-      const int64_t dst = layer_off + ((blk * hkv + h) * bs + off) * D + g * N;
-      *reinterpret_cast<uint4*>(k_pool + dst) = Vec<T>::pack(out);
-      *reinterpret_cast<uint4*>(v_pool + dst) = vu;
+    for (int e = 0; e < N; e += 2) {
+      const float4 c = __ldg(cs + e / 2);  // (cos, sin) of pairs u*N+e, u*N+e+1
+      // first half: x cos - y sin ; second half: y cos + x sin
+      ox[e] = fmaf(x[e], c.x, -y[e] * c.y);
+      oy[e] = fmaf(y[e], c.x, x[e] * c.y);
+      ox[e + 1] = fmaf(x[e + 1], c.z, -y[e + 1] * c.w);
+      oy[e + 1] = fmaf(y[e + 1], c.z, x[e + 1] * c.w);
     }
+    const int64_t blk = s / bs, off = s % bs;
+    const int64_t dst = layer_off + ((blk * hkv + h) * bs + off) * D + u * N;
+    *reinterpret_cast<uint4*>(k_pool + dst) = Vec<T>::pack(ox);
+    *reinterpret_cast<uint4*>(k_pool + dst + D / 2) = Vec<T>::pack(oy);
+    *reinterpret_cast<uint4*>(v_pool + dst) = v0;
+    *reinterpret_cast<uint4*>(v_pool + dst + D / 2) = v1;
     return;
   }
   // pad slots: zero K and V of every head
@@ -124,18 +114,21 @@ __global__ void __launch_bounds__(256) rope_kv_write_kernel(
   if (pid >= n_pad * per_row) return;
   const int64_t pr = pid / per_row;
   const int prem = static_cast<int>(pid - pr * per_row);
-  const int ph = prem / G, pg = prem % G;
+  const int ph = prem / H, pu = prem % H;
   const int64_t ps = pad_slots[pr];
   const int64_t pblk = ps / bs, poff = ps % bs;
-  const int64_t dst = layer_off + ((pblk * hkv + ph) * bs + poff) * D + pg * N;
-  *reinterpret_cast<uint4*>(k_pool + dst) = make_uint4(0, 0, 0, 0);
-  *reinterpret_cast<uint4*>(v_pool + dst) = make_uint4(0, 0, 0, 0);
+  const int64_t dst = layer_off + ((pblk * hkv + ph) * bs + poff) * D + pu * N;
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  *reinterpret_cast<uint4*>(k_pool + dst) = z;
+  *reinterpret_cast<uint4*>(k_pool + dst + D / 2) = z;
+  *reinterpret_cast<uint4*>(v_pool + dst) = z;
+  *reinterpret_cast<uint4*>(v_pool + dst + D / 2) = z;
 }
 
 template <typename T, int D>
 cudaError_t launch_t(const KvWriteArgs& a, cudaStream_t st) {
-  constexpr int G = D / Vec<T>::N;
-  const int64_t threads = (a.rows + a.n_pad) * static_cast<int64_t>(a.hkv) * G;
+  constexpr int H = D / Vec<T>::N / 2;
+  const int64_t threads = (a.rows + a.n_pad) * static_cast<int64_t>(a.hkv) * H;
   if (threads == 0) return cudaSuccess;
   const int64_t blocks = (threads + 255) / 256;
   rope_kv_write_kernel<T, D><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
