@@ -50,6 +50,12 @@ def check(ctx, moves):
     assert st["moves"] == len(moves) and st["ops"] == len(moves) + st["cycles"]
     assert st["duplicates"] == out_degree_duplicates([(s, d, 0, 0) for s, d, _ in moves])
     assert st["components"] == len(off) - 1
+    # the kernel issues op i+1's loads before op i's stores: op i+1 never reads what op i writes
+    for c in range(len(off) - 1):
+        seq = ops[off[c]: off[c + 1]]
+        for a, b in zip(seq[:-1], seq[1:]):
+            if a[3] != 1 and b[3] != 2:
+                assert b[1] != a[0], (a, b)
     # components touch disjoint blocks (they run in parallel)
     seen = {}
     for c in range(len(off) - 1):
