@@ -50,7 +50,8 @@ def check(ctx, moves):
     assert st["moves"] == len(moves) and st["ops"] == len(moves) + st["cycles"]
     assert st["duplicates"] == out_degree_duplicates([(s, d, 0, 0) for s, d, _ in moves])
     assert st["components"] == len(off) - 1
-    # the kernel issues op i+1's loads before op i's stores: op i+1 never reads what op i writes
+    # reads precede writes block by block, so op i+1 never reads what op i writes (a kernel may
+    # issue op i+1's loads before op i's stores)
     for c in range(len(off) - 1):
         seq = ops[off[c]: off[c + 1]]
         for a, b in zip(seq[:-1], seq[1:]):
