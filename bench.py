@@ -272,16 +272,20 @@ def main():
             step()
         torch.cuda.synchronize()
         # ---- timed region: K steps, events on the launching stream, L2 flushed between steps
-        ctx.set_timing(True)
         n0 = ctx.launch_count()
-        attn_ms = []
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
         with ClockSampler(local) as clk:
-            step_ms = timed(args.steps, attn=attn_ms)
+            step_ms = timed(args.steps)
         torch.cuda.synchronize()
         launches = ctx.launch_count() - n0
+        # per-kernel times for the roofline, in separate steps: the ABI's CUDA events around the
+        # attention kernels sit between K1 and the attention launch and so disable the
+        # programmatic-dependent-launch overlap — they are kept out of the timed steps above
+        ctx.set_timing(True)
+        attn_ms = []
+        timed(max(3, args.steps // 4), attn=attn_ms)
         ctx.set_timing(False)
         # single-layer TTFT (plan + one layer of prefill + join), same protocol
         l1_ms = timed(max(3, args.steps // 2), layers=1) if L > 1 else step_ms
@@ -386,11 +390,12 @@ def measure_judge(dev, stream, flush, args, reps: int = 5):
     cand_only = inputs.SpanQuery(np.zeros(0, np.int32), list(q.fragments), q.cross[:1])  # fills the candidates
     toks = np.concatenate(list(q.fragments) + [q.cross])
     dense = inputs.SpanQuery(toks[:-1], [], toks[-1:])
-    ctx.set_timing(True)
     cold_ms, cold_flops = ttft_l1(ctx, s, tab, dev, stream, flush, odt, w.queries, [], reps)
-    pre_ms, join_ms = ctx.last_attn_ms()  # attention kernels of the last cold repetition
     pre_fl, join_fl = ttft_l1.last_flops
     warm_ms, warm_flops = ttft_l1(ctx, s, tab, dev, stream, flush, odt, w.queries, [cand_only], reps)
+    ctx.set_timing(True)  # attention kernel times of a separate cold pass (see the main timed region)
+    ttft_l1(ctx, s, tab, dev, stream, flush, odt, w.queries, [], 1)
+    pre_ms, join_ms = ctx.last_attn_ms()
     ctx.set_timing(False)
     dense_ms, dense_flops = ttft_l1(ctx, s, tab, dev, stream, flush, odt, [dense], [], reps)
     ctx.close()

@@ -60,7 +60,8 @@ struct AttnArgs {
   int max_pos;
   bool out_fp32;  // o is fp32 (else ctx dtype)
   bool paired;    // tcgen05 path: work codes are (item, GQA head pair) — see span_attn_tc.cu
-  bool join;      // tcgen05 path: a join launch (2-deep Q ring, register epilogue)
+  bool join;      // tcgen05 path: a join launch (2-deep Q ring, epilogue staged in Q slots)
+  bool pdl;       // tcgen05 path: launch as a programmatic dependent of the preceding K1
   int poly_mask;  // tcgen05 path: share of exp2 on the FMA pipe, in quarters (0..4)
   float rescale_threshold;  // tcgen05 path: conditional O rescale threshold (log2 units, 8)
   long long* dbg_trace;     // profiling only: CTA-0 event timeline (null = off)

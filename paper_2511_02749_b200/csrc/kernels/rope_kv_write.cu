@@ -70,6 +70,9 @@ __global__ void __launch_bounds__(256) rope_kv_write_kernel(
   constexpr int G = D / N;
   constexpr int H = G / 2;  // threads per (row, head)
   static_assert(G <= 32 && (G & (G - 1)) == 0 && G >= 2, "d/N must be a power of two in [2, 32]");
+  // the attention launch that reads these pages may start its prologue now (it waits for this
+  // grid's completion before touching the pool: griddepcontrol.wait in span_attn_tc)
+  asm volatile("griddepcontrol.launch_dependents;");
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t per_row = static_cast<int64_t>(hkv) * H;
   const int64_t total = rows * per_row;

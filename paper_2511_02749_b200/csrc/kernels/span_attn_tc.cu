@@ -213,6 +213,10 @@ __device__ __forceinline__ void ex2_pair_f16(float x0, float x1, float& p0, floa
 template <int D>
 __device__ void run_producer(const TcParams& P, TcSmem<D>& S, int it_begin, int it_end, int kv) {
   const AttnArgs& a = P.a;
+  // programmatic dependent launch: the pages this launch reads are written by the preceding
+  // rope_kv_write — everything before this point (barriers, TMEM, work claims, Q loads and
+  // rotation) may overlap that kernel's tail; the pool is read only after it has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int kSlots = kv == 0 ? TcSmem<D>::kKSlots : TcSmem<D>::kVSlots;
   const int group = a.hq / a.hkv;
   const int box = min(a.bs, 64);
@@ -938,8 +942,21 @@ cudaError_t launch_dp(const AttnArgs& a, cudaStream_t st) {
   // prefill (A/B: the prefill gains nothing — its epilogue then contends with the next item's S MMAs)
   static const int ring = getenv("SPANQ_QRING2") ? atoi(getenv("SPANQ_QRING2")) : 1;
   p.join = a.paired && (ring >= 2 || (ring == 1 && a.join)) ? 1 : 0;
-  span_attn_tc_kernel<D, PM><<<a.grid, kThreads, smem, st>>>(p);
-  return cudaGetLastError();
+  // launched as a programmatic dependent of the preceding K1 when the caller says it directly
+  // precedes (a.pdl; knob SPANQ_PDL=0 turns it off): the prologue and Q preparation overlap
+  // K1's tail (see run_producer)
+  static const bool pdl = getenv("SPANQ_PDL") == nullptr || atoi(getenv("SPANQ_PDL")) != 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(a.grid));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl && a.pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, span_attn_tc_kernel<D, PM>, p);
 }
 
 template <int D>

@@ -298,7 +298,9 @@ spq_status run_attn(spq_ctx* c, const spq::AttnArgs& a, cudaStream_t st) {
 }
 
 spq_status kv_write(spq_ctx* c, spq_plan* p, int32_t layer, const void* k, const void* v,
-                    const int32_t* pos, const int64_t* slot, int64_t rows, cudaStream_t st) {
+                    const int32_t* pos, const int64_t* slot, int64_t rows, cudaStream_t st,
+                    bool* launched = nullptr) {
+  if (launched) *launched = false;
   spq::KvWriteArgs w{};
   w.k = k;
   w.v = v;
@@ -322,6 +324,7 @@ spq_status kv_write(spq_ctx* c, spq_plan* p, int32_t layer, const void* k, const
   if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("rope_kv_write launch: ") + cudaGetErrorString(e));
   p->padded_layers[layer] = 1;
   c->launches++;
+  if (launched) *launched = true;
   return SPQ_OK;
 }
 
@@ -737,7 +740,9 @@ spq_status spq_prefill_jobs(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, i
   s = wait_pending(c, st);
   if (s != SPQ_OK) return s;
   const int64_t r0 = p->host.job_row_off[a], r1 = p->host.job_row_off[b];
-  s = kv_write(c, p, layer, k, v, at<int32_t>(p, p->off_ppos) + r0, at<int64_t>(p, p->off_pslot) + r0, r1 - r0, st);
+  bool k1 = false;
+  s = kv_write(c, p, layer, k, v, at<int32_t>(p, p->off_ppos) + r0, at<int64_t>(p, p->off_pslot) + r0, r1 - r0, st,
+               &k1);
   if (s != SPQ_OK) return s;
   spq::AttnArgs args{};
   TempWork tw;
@@ -761,6 +766,9 @@ spq_status spq_prefill_jobs(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, i
   args.o = o;
   args.lse = lse;
   args.layer = layer;
+  // programmatic dependent launch only right behind our own K1 (nothing else in between on the
+  // stream: no work-list upload, no timing event) — then every input but the pool is complete
+  args.pdl = k1 && full && !c->timing;
   CUtensorMap qmap, omap;
   if (c->cfg.dtype == SPQ_BF16) {
     s = make_qmap(c, q, r1 - r0, &qmap);
@@ -799,8 +807,10 @@ spq_status join_impl(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t 
   if (s != SPQ_OK) return s;
   const int64_t r0 = p->host.query_join_row_off[a], r1 = p->host.query_join_row_off[b];
   if (r0 == r1) return SPQ_OK;  // only queries homed on other ranks
+  bool k1 = false;
   if (mode != 1) {
-    s = kv_write(c, p, layer, k, v, at<int32_t>(p, p->off_jpos) + r0, at<int64_t>(p, p->off_jslot) + r0, r1 - r0, st);
+    s = kv_write(c, p, layer, k, v, at<int32_t>(p, p->off_jpos) + r0, at<int64_t>(p, p->off_jslot) + r0, r1 - r0, st,
+                 &k1);
     if (s != SPQ_OK) return s;
   }
   spq::AttnArgs args{};
@@ -836,6 +846,7 @@ spq_status join_impl(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t 
   args.lsepart = lsepart;
   args.pos = at<int32_t>(p, p->off_jpos) + r0;
   args.join = true;
+  args.pdl = k1 && (full || mode >= 0) && !c->timing;  // see spq_prefill_jobs
   args.q = q;
   args.o = o;
   args.lse = lse;
