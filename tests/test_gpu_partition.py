@@ -21,9 +21,11 @@ from test_gpu_parity import check, check_lse
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("dtype,world,phased", [("bf16", 2, False), ("fp32", 2, False), ("bf16", 3, False),
-                                                ("bf16", 2, True), ("bf16", 3, True), ("fp32", 2, True)])
-def test_partitioned_exchange_parity(cuda_dev, dtype, world, phased):
+@pytest.mark.parametrize("dtype,world,phased,out", [("bf16", 2, False, "fp32"), ("fp32", 2, False, "fp32"),
+                                                    ("bf16", 3, False, "fp32"), ("bf16", 2, True, "fp32"),
+                                                    ("bf16", 3, True, "fp32"), ("fp32", 2, True, "fp32"),
+                                                    ("bf16", 2, True, "bf16")])
+def test_partitioned_exchange_parity(cuda_dev, dtype, world, phased, out):
     # phased: each home rank runs join phase 0 (held segments) BEFORE the exchange — with its
     # received blocks poisoned with NaN, so reading one early would show — then phase 1 after it
     import torch
@@ -38,7 +40,7 @@ def test_partitioned_exchange_parity(cuda_dev, dtype, world, phased):
     flat = [(q.prefix, q.fragments, q.cross) for q in qs]
     ctxs, plans, views, outs = [], [], [], []
     for r in range(world):
-        ctx = spanq.Context(sh, 2048, device=0, max_position=1 << 14, out_dtype="fp32", rank=r, world_size=world)
+        ctx = spanq.Context(sh, 2048, device=0, max_position=1 << 14, out_dtype=out, rank=r, world_size=world)
         plan = ctx.plan(qs)
         view = plan.view()
         ov = Store(2048, sh.hq, sh.hkv, sh.d, sh.block_size, sh.rope_base, sh.model_salt).plan(flat, rank=r,
@@ -49,7 +51,8 @@ def test_partitioned_exchange_parity(cuda_dev, dtype, world, phased):
             np.testing.assert_array_equal(view["send"].get(p, np.zeros(0, np.int32)), ov.send.get(p, []))
             np.testing.assert_array_equal(view["recv"].get(p, np.zeros(0, np.int32)), ov.recv.get(p, []))
         ptok = runner.prefill_tokens(view, qs)
-        op = torch.empty((len(ptok), sh.hq, sh.d), dtype=torch.float32, device=cuda_dev)
+        odt = torch.bfloat16 if out == "bf16" else torch.float32
+        op = torch.empty((len(ptok), sh.hq, sh.d), dtype=odt, device=cuda_dev)
         lp = torch.empty((len(ptok), sh.hq), dtype=torch.float32, device=cuda_dev)
         if len(ptok):
             q, k, v = runner.gather(tab, ptok, cuda_dev)
@@ -64,7 +67,8 @@ def test_partitioned_exchange_parity(cuda_dev, dtype, world, phased):
     joins = []
     for r in range(world):
         jtok = runner.join_tokens(views[r], qs)
-        oj = torch.empty((len(jtok), sh.hq, sh.d), dtype=torch.float32, device=cuda_dev)
+        oj = torch.empty((len(jtok), sh.hq, sh.d), dtype=torch.bfloat16 if out == "bf16" else torch.float32,
+                         device=cuda_dev)
         lj = torch.empty((len(jtok), sh.hq), dtype=torch.float32, device=cuda_dev)
         joins.append((*runner.gather(tab, jtok, cuda_dev), oj, lj))
         if phased:
