@@ -28,6 +28,9 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineDesc* __restr
                                                       TO* __restrict__ o,
                                                       float* __restrict__ lse, int hq) {
   constexpr int E = D / 32;  // columns per lane
+  // launched as a programmatic dependent of the join it merges (when nothing sits between them):
+  // the partials are read only once that grid has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const CombineDesc cd = desc[blockIdx.x];
   if (static_cast<int>(blockIdx.y) >= cd.n_heads) return;
   const int h = cd.head0 + blockIdx.y;
@@ -92,7 +95,16 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineDesc* __restr
 template <int D, typename TO>
 void launch_dt(const CombineArgs& a, cudaStream_t st) {
   dim3 grid(a.n_desc, a.heads_per_desc, kTileRows / 8);
-  combine_kernel<D, TO><<<grid, 256, 0, st>>>(a.desc, a.opart, a.lsepart, static_cast<TO*>(a.o), a.lse, a.hq);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = a.pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, combine_kernel<D, TO>, a.desc, a.opart, a.lsepart, static_cast<TO*>(a.o), a.lse, a.hq);
 }
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {

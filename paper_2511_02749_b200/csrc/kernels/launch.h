@@ -79,6 +79,7 @@ struct CombineArgs {
   int hq, d;
   int heads_per_desc;  // max CombineDesc::n_heads
   bool out_fp32;
+  bool pdl;  // launch as a programmatic dependent of the join kernel right before it
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);
 

@@ -154,6 +154,12 @@ spq::WorkOpts work_opts(const spq_ctx* c, bool allow_split) {
 
 int elt_size(const spq_ctx* c) { return c->cfg.dtype == SPQ_FP32 ? 4 : 2; }
 
+// programmatic dependent launches (knob SPANQ_PDL=0 turns them off, for A/B)
+bool pdl_enabled() {
+  static const bool on = std::getenv("SPANQ_PDL") == nullptr || std::atoi(std::getenv("SPANQ_PDL")) != 0;
+  return on;
+}
+
 spq_status make_tmap(spq_ctx* c, void* pool, CUtensorMap* out) {
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
@@ -886,6 +892,8 @@ spq_status join_impl(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t 
     ca.heads_per_desc = heads_per_unit(c);
     ca.d = c->cfg.head_dim;
     ca.out_fp32 = c->cfg.out_dtype == SPQ_FP32;
+    // the join kernel is the preceding stream operation unless a timing event sits between
+    ca.pdl = !c->timing && c->cfg.dtype == SPQ_BF16 && pdl_enabled();
     cudaError_t e = spq::launch_combine(ca, st);
     if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("combine launch: ") + cudaGetErrorString(e));
     c->launches++;
