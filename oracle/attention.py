@@ -153,3 +153,99 @@ def plan_join_expected(view, queries, eq, ek, ev, base: float,
         outs.append(o)
         lses.append(l)
     return np.concatenate(outs), np.concatenate(lses)
+
+
+# ----------------------------------------------------------------------------- the method's
+# own path, from a simulated KV pool (pages hold K at the STORED position: span-local for
+# prefix/fragment blocks, global for cross blocks — readings R2, R3). These follow the method
+# step by step (P:436 fn prepare, P:603 store, P:610 ReRoPE on reuse, P:672 span mask) and are
+# pinned to the plain definition above by tests/test_oracle_attention.py.
+def segment_tokens(seg, queries) -> np.ndarray:
+    prefix, frags, cross = queries[seg.query]
+    return np.asarray(prefix if seg.kind == 0 else frags[seg.frag_idx] if seg.kind == 1 else cross,
+                      np.int64)
+
+
+def pool_write(pool: dict, view, queries, ek, ev, base: float, bs: int) -> dict:
+    """K1 (fused RoPE + paged write) of a plan, on a pool modelled as {slot: (k [Hkv,d],
+    v [Hkv,d])}: every packed row with slot >= 0 stores RoPE(k, stored position) and v. Rows with
+    slot −1 (resident blocks, R10) are not written. Returns the pool (updated in place)."""
+    for seg_of_row, pos, slot in ((view.prefill_seg, view.prefill_pos, view.prefill_slot),
+                                  (view.join_seg, view.join_pos, view.join_slot)):
+        for si in np.unique(seg_of_row):
+            seg = view.segments[int(si)]
+            toks = segment_tokens(seg, queries)
+            rows = np.nonzero(seg_of_row == si)[0]
+            t_idx = np.arange(seg.tok_len - len(rows), seg.tok_len)  # rows are the segment's tail
+            for r, t in zip(rows, t_idx):
+                if slot[r] >= 0:
+                    k, v = expected_pages(toks[[t]], None, ek, ev, base, [pos[r]])
+                    pool[int(slot[r])] = (k[0], v[0])
+    return pool
+
+
+def _pages(pool: dict, seg, bs: int):
+    ks, vs = [], []
+    for t in range(seg.tok_len):
+        k, v = pool[seg.blocks[t // bs] * bs + t % bs]
+        ks.append(k)
+        vs.append(v)
+    return np.stack(ks), np.stack(vs)
+
+
+def prefill_from_pool(view, queries, pool: dict, eq, base: float, bs: int,
+                      heads: Optional[Sequence[int]] = None):
+    """K2: each prefill job's computed rows [compute_begin, tok_len) attend causally over the
+    job's own pages (a fragment "only attends to prior tokens in that same document"),
+    q rotated at the same span-local position as its keys. Rows in plan (job) order."""
+    outs, lses = [], []
+    for si in view.jobs:
+        seg = view.segments[si]
+        toks = segment_tokens(seg, queries)
+        k, v = _pages(pool, seg, bs)
+        rows = np.arange(seg.compute_begin, seg.tok_len)
+        q = rope(_f64(eq[toks[rows]]), rows[:, None].astype(np.float64), base)
+        mask = np.arange(seg.tok_len)[None, :] <= rows[:, None]
+        o, l = attend(q, k, v, mask, heads)
+        outs.append(o)
+        lses.append(l)
+    return np.concatenate(outs), np.concatenate(lses)
+
+
+def join_from_pool(view, queries, pool: dict, eq, base: float, bs: int, query: int,
+                   heads: Optional[Sequence[int]] = None):
+    """K3: the cross rows of `query` (global positions p_i) attend over every segment's pages
+    in query order. Cached fragment K sits at span-local positions 0..L−1, so instead of
+    re-encoding it at Δ_f ("ReRoPE") the query row is counter-rotated: RoPE(q, p_i − Δ_f)
+    · RoPE(k, t) = RoPE(q, p_i) · RoPE(k, Δ_f + t) (relative property). Prefix pages are at their
+    global positions (Δ = 0); cross pages too, causal by stored position."""
+    segs = [s for s in view.segments if s.query == query]
+    cross = [s for s in segs if s.kind == 2][0]
+    ctoks = segment_tokens(cross, queries)
+    p = cross.pos0 + np.arange(cross.tok_len)
+    scores_q, ks, vs, masks = [], [], [], []
+    for seg in segs:
+        k, v = _pages(pool, seg, bs)
+        delta = seg.pos0 if seg.kind == 1 else 0
+        stored = np.arange(seg.tok_len) + (seg.pos0 if seg.kind == 2 else 0)
+        q = rope(_f64(eq[ctoks]), (p - delta)[:, None].astype(np.float64), base)
+        scores_q.append(q)
+        ks.append(k)
+        vs.append(v)
+        masks.append(stored[None, :] + delta <= p[:, None])
+    # one softmax over the concatenated key sets; each set scored with its own rotated q
+    R, hq, d = scores_q[0].shape
+    g = hq // ks[0].shape[1]
+    heads = list(range(hq)) if heads is None else list(heads)
+    out = np.zeros((R, len(heads), d))
+    lse = np.zeros((R, len(heads)))
+    for j, h in enumerate(heads):
+        s = np.concatenate([(qq[:, h, :] @ kk[:, h // g, :].T) / np.sqrt(d)
+                            for qq, kk in zip(scores_q, ks)], axis=1)
+        s = np.where(np.concatenate(masks, axis=1), s, -np.inf)
+        m = s.max(axis=1, keepdims=True)
+        pr = np.exp(s - m)
+        l = pr.sum(axis=1, keepdims=True)
+        out[:, j, :] = (pr @ np.concatenate([vv[:, h // g, :] for vv in vs])) / l
+        lse[:, j] = (m + np.log(l))[:, 0]
+    return out, lse

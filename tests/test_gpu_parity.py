@@ -1,12 +1,15 @@
 """GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle on the same seeded inputs.
 
 Tolerances (BASELINE.json north_star): fp32 path max-abs <= 1e-5; bf16 path max-abs <= 1e-2 and
-relative L2 <= 5e-3 on attention outputs. The bf16 path is measured (bench.py) with fp32 outputs
-(out_dtype, reading R22): bf16 MMAs and a bf16 KV cache, no final bf16 rounding of O
-— that rounding alone is up to 0.0078 for |O| in [2, 4), which with the bf16 Q/K/P roundings
-would exceed 1e-2 on a few rows. With bf16 outputs the bound is 1e-2 + half a bf16 ulp of |O|. Block tables / slot maps are bit-exact (the planner
-is checked on CPU in test_abi_host.py and again here on the exact plans the GPU runs); V pages
-bit-exact, K pages within 1 bf16 ulp of the fp64 RoPE.
+relative L2 <= 5e-3 on attention outputs. With bf16 arithmetic (bf16 Q after RoPE, bf16 KV cache,
+bf16 P) even an exactly rounded computation misses fp64 by up to ~2^-9 |O| on peaky rows
+(reading R29; the premise is asserted on CPU in tests/test_tolerance_reading.py), so
+every bf16-compute check — fp32 or bf16 outputs alike — applies, per element,
+max-abs <= 1e-2 + 2^-9 |O_ref| (half a bf16 ulp of the reference), rel-L2 <= 5e-3 unchanged, and
+bounds the share of elements above the flat 1e-2 by 1e-4 (each check reports that share).
+Block tables / slot maps are bit-exact (the planner is checked on CPU in test_abi_host.py and
+again here on the exact plans the GPU runs); V pages bit-exact, K pages within 1 bf16 ulp of the
+fp64 RoPE.
 """
 import numpy as np
 import pytest
@@ -25,7 +28,10 @@ def _np(t):
     return t.float().cpu().numpy().astype(np.float64)
 
 
-def check(got, exp, fp32, what, abs_tol=BF16_MAX_ABS, bf16_out=False, rel_tol=BF16_REL_L2):  # noqa: ARG001
+FLAT_SHARE_MAX = 1e-4  # share of bf16-path elements allowed above the flat 1e-2 (R29)
+
+
+def check(got, exp, fp32, what, abs_tol=BF16_MAX_ABS, rel_tol=BF16_REL_L2):
     g = _np(got)
     if not exp.size:
         return 0.0, 0.0
@@ -34,12 +40,15 @@ def check(got, exp, fp32, what, abs_tol=BF16_MAX_ABS, bf16_out=False, rel_tol=BF
     if fp32:
         assert d.max() <= FP32_MAX_ABS, f"{what}: max abs {d.max():.3e}"
         return d.max(), rel
-    # bf16 compute: Q, K (cache) and P are bf16, so even an exactly rounded computation errs by
-    # up to ~2^-9 |O| on peaky rows (reading R29: the fp64 emulation of those roundings alone
-    # reaches 1.03e-2 on the smoke case); the bar is 1e-2 + half a bf16 ulp of |O_ref|
+    # bf16 compute (reading R29): 1e-2 + half a bf16 ulp of |O_ref| per element, and only a
+    # tiny share of the elements may use the widening at all
     bound = abs_tol + 2.0 ** -9 * np.abs(exp)
+    share = float((d > abs_tol).mean())
+    print(f"{what}: max abs {d.max():.3e} rel-L2 {rel:.3e} share above {abs_tol:g}: {share:.2e} "
+          f"({int((d > abs_tol).sum())} of {d.size})")
     assert (d <= bound).all() and rel <= rel_tol, \
         f"{what}: max abs {d.max():.3e} (worst err/bound {np.max(d / bound):.3f}) rel-L2 {rel:.3e}"
+    assert share <= FLAT_SHARE_MAX, f"{what}: {share:.2e} of the elements exceed {abs_tol:g}"
     return d.max(), rel
 
 
@@ -63,7 +72,6 @@ def run_and_check(w, cuda_dev, nblk=4096, check_pages=True, out_dtype="fp32", ab
     s = w.shape
     fp32 = s.dtype == "fp32"
     ctx = spanq.Context(s, nblk, device=0, max_position=1 << 15, out_dtype=out_dtype)
-    bo = out_dtype == "bf16"
     tabs = [runner.device_tables(s, 0, w.seed, cuda_dev, w.peaky)]
     for q in w.warmup_queries:
         runner.run_pass(ctx, [q], tabs, cuda_dev, release=True)
@@ -79,10 +87,10 @@ def run_and_check(w, cuda_dev, nblk=4096, check_pages=True, out_dtype="fp32", ab
     qs = [(q.prefix, q.fragments, q.cross) for q in w.queries]
     if len(ov.jobs):
         eo, el = oatt.plan_prefill_expected(ov, qs, eq, ek, ev, s.rope_base)
-        check(res.o_prefill, eo, fp32, f"{w.name} prefill O", abs_tol, bo, rel_tol)
+        check(res.o_prefill, eo, fp32, f"{w.name} prefill O", abs_tol, rel_tol)
         check_lse(res.lse_prefill, el, fp32, f"{w.name} prefill LSE", abs_tol / BF16_MAX_ABS)
     jo, jl = oatt.plan_join_expected(ov, qs, eq, ek, ev, s.rope_base)
-    out = check(res.o_join, jo, fp32, f"{w.name} join O", abs_tol, bo, rel_tol)
+    out = check(res.o_join, jo, fp32, f"{w.name} join O", abs_tol, rel_tol)
     check_lse(res.lse_join, jl, fp32, f"{w.name} join LSE", abs_tol / BF16_MAX_ABS)
     if check_pages:
         kp, vp = _np(ctx.k_pool[0]), _np(ctx.v_pool[0])
@@ -237,6 +245,34 @@ def test_full_size_c2_sampled_rows(cuda_dev):
     ctx.close()
 
 
+@pytest.mark.parametrize("out_dtype", ["fp32", "bf16"])
+def test_full_size_c2_all_rows(cuda_dev, out_dtype):
+    """configs[1] at full size in the bench's launch configuration (512-block pool, the bench's
+    output dtypes), EVERY output element: all 17,152 prefill rows and all 256 join rows, all 32
+    heads, against the fp64 oracle (the whole C2 in a few seconds on the host)."""
+    import torch
+
+    w = inputs.c2()
+    s = w.shape
+    ctx = spanq.Context(s, 512, device=0, max_position=1 << 15, out_dtype=out_dtype)
+    tabs = [runner.device_tables(s, 0, w.seed, cuda_dev)]
+    res = runner.run_pass(ctx, w.queries, tabs, cuda_dev)
+    torch.cuda.synchronize()
+    eq, ek, ev = inputs.layer_tables(s, 0, w.seed)
+    ov = oracle_plan(w, w.queries)
+    np.testing.assert_array_equal(res.view["prefill_slot"], ov.prefill_slot)
+    qs = [(q.prefix, q.fragments, q.cross) for q in w.queries]
+    eo, el = oatt.plan_prefill_expected(ov, qs, eq, ek, ev, s.rope_base)
+    assert eo.shape == tuple(res.o_prefill.shape) == (17152 - 256, 32, 128)
+    check(res.o_prefill, eo, False, f"C2 prefill O all rows ({out_dtype})")
+    check_lse(res.lse_prefill, el, False, "C2 prefill LSE all rows")
+    jo, jl = oatt.plan_join_expected(ov, qs, eq, ek, ev, s.rope_base)
+    assert jo.shape == tuple(res.o_join.shape) == (256, 32, 128)
+    check(res.o_join, jo, False, f"C2 join O all rows ({out_dtype})")
+    check_lse(res.lse_join, jl, False, "C2 join LSE all rows")
+    ctx.close()
+
+
 def test_multi_layer_plan_reuse(cuda_dev):
     # one plan, three layers (each its own tables and KV-pool layer): the per-launch work
     # counters of the dynamic schedule and the pad zeroing are per launch / per layer
@@ -342,8 +378,9 @@ def test_bf16_matches_rounding_emulation(cuda_dev):
     # The bf16 kernel is as accurate as its formats allow: against an fp64 computation that only
     # rounds the rotated Q, the cached K and P to bf16 (test-side emulation built on the oracle's
     # RoPE), the fragment-prefill outputs agree to 4e-3 (measured 2.5e-3: the kernel's P is taken
-    # against a running max that may lag by up to 2^8, so its roundings differ) — while both sit
-    # ~1e-2 from the exact fp64 result on this case (reading R29)
+    # against a running max that may lag by up to 2^8, so its roundings differ). That the
+    # emulation itself sits >= 1e-2 from fp64 on this case (reading R29) is asserted on CPU in
+    # tests/test_tolerance_reading.py
     import torch
 
     from oracle import rope as orope
@@ -380,8 +417,8 @@ def test_bf16_matches_rounding_emulation(cuda_dev):
         exact = attn(Q, K, False)[cb:]
         worst_emul = max(worst_emul, float(np.abs(got - emul).max()))
         worst_exact = max(worst_exact, float(np.abs(got - exact).max()))
+    print(f"kernel vs bf16-rounding emulation {worst_emul:.3e}, vs exact fp64 {worst_exact:.3e}")
     assert worst_emul <= 4e-3, worst_emul
-    assert worst_exact > 5e-3  # the emulation, not luck, explains the distance to fp64
     ctx.close()
 
 
