@@ -84,6 +84,14 @@ const double kEpochCost = [] {
   return e ? std::atof(e) : 1.5;
 }();
 
+// Per-item sub-tile counts (the kernel's roles need them without walking the tiles).
+void count_subtiles(AttnWorkHost* w) {
+  for (WorkItem& it : w->items) {
+    it.n_sub = 0;
+    for (int32_t t = it.tile_begin; t < it.tile_end; ++t) it.n_sub += w->tiles[t].n_valid > 64 ? 2 : 1;
+  }
+}
+
 }  // namespace
 
 void build_prefill_work(const PlanHost& p, const WorkOpts& o, int job_begin, int job_end,
@@ -110,6 +118,7 @@ void build_prefill_work(const PlanHost& p, const WorkOpts& o, int job_begin, int
     for (int64_t i = s.compute_begin; i < s.tok_len; ++i) w->flops += static_cast<double>(i + 1);
   }
   w->flops *= 4.0 * o.d * o.hq;
+  count_subtiles(w);
   if (o.persistent) schedule(cost, o.units, o.num_sms, w);
 }
 
@@ -166,6 +175,7 @@ void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_en
       w->items.push_back(it);
       cost.push_back(q.te - q.tb + kItemOverhead);
     }
+    count_subtiles(w);
     if (o.persistent) schedule(cost, o.units, o.num_sms, w);
     return;
   }
@@ -261,6 +271,7 @@ void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_en
       if (part) w->n_parts += np;
     }
   }
+  count_subtiles(w);
   int used = grid;
   while (used > 1 && per_cta[used - 1].empty()) --used;
   w->grid = used;

@@ -38,6 +38,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <climits>
 #include <cmath>
 #include <cstdlib>
@@ -76,6 +77,12 @@ struct TcSmem {
   uint64_t q_full[2][2], q_empty[2][2], q_load[2][2];  // [head][Q ring slot]
   __device__ uint8_t* q2(int x) { return reinterpret_cast<uint8_t*>(&stage[0][0][0]) + x * kChunks * kChunkBytes; }
   uint64_t s_full[2][2], p_full[2][2], o_done[2][2];  // [head][S buffer / PV parity j & 1]
+  // prefill: the epilogue runs on the Q-prep warps (12-15). The softmax WG of head x hands over
+  // 1/l of every row through fin_inv[x][item & 1] (fin_full: 128 arrivals), the epilogue warps
+  // drain O_x from TMEM into the staging area and arrive o_free[x] (4 warps), which the issuer
+  // waits for before the next item's first PV overwrites O_x
+  uint64_t o_free[2], fin_full[2][2];
+  float fin_inv[2][2][128];
   static constexpr int kSched = 4;  // dynamic schedule: ring of claimed codes
   uint64_t sched_full[kSched], sched_empty[kSched];
   int32_t sched_code[kSched];
@@ -93,17 +100,21 @@ struct TcParams {
   int paired;     // 1: a unit is a GQA head pair (A = 2u, B = 2u+1); 0: one head (B idle)
   int poly_mask;  // pair i of a 32-key chunk uses the FMA-pipe exp2 when (i & 3) < poly_mask
   float rescale_threshold;  // log2 units; O is rescaled when the running max grows by more
-  int qrot_table;  // Q prep: 1 = (cos, sin) table row per step, 0 = angle recurrence
   int qprep_mode;  // Q prep: bit 0 = issue head B's load early, bit 1 = L2-prefetch the next item's q
   int join;        // 1: 2-deep Q ring per head in the staging area, epilogue staged in Q slots
+  int epi_q;       // 1 (prefill launches): the epilogue runs on the Q-prep warps (prefill_epilogue)
   int dbg_mode;  // profiling only: 1 = softmax does no math, 2 = max pass only,
                  // 3 = 1 + K/V always from the first block (L2-resident), 4 = 1 + MMA skips K/V waits,
                  // 5 = 1 + Q prep does no work
 };
 
+// The dynamic shared memory window starts 1024-byte aligned when a kernel has no static shared
+// memory (SWIZZLE_128B operands need it); the launch requests exactly sizeof(TcSmem) (d=128 uses
+// the whole 227 KB), so a misaligned base would be a fatal configuration error: trap loudly.
 template <int D>
 __device__ __forceinline__ TcSmem<D>& smem_ref(uint8_t* raw) {
-  return *reinterpret_cast<TcSmem<D>*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  if (smem_u32(raw) & 1023u) __trap();
+  return *reinterpret_cast<TcSmem<D>*>(raw);
 }
 
 // Q ring of head x: epoch e uses slot e % depth (depth 1 for prefill, 2 for joins), its
@@ -151,7 +162,7 @@ __device__ __forceinline__ Unit decode(const TcParams& P, int code) {
 // claims codes from the launch's counter (atomicAdd) and hands them to the other roles through a
 // smem ring; every role sees the same sequence, ending with -1.
 constexpr int kSchedConsumers = 1 + 2 + 256 + 128;  // V producer, 2 MMA issuers, softmax, Q prep
-template <int D>
+template <int D, bool EPI>
 struct ItemSrc {
   const TcParams& P;
   TcSmem<D>& S;
@@ -159,20 +170,36 @@ struct ItemSrc {
   bool claimer;
   uint32_t k = 0;
   __device__ ItemSrc(const TcParams& p, TcSmem<D>& s, int b, int e, bool c) : P(p), S(s), it(b), end(e), claimer(c) {}
+  int ahead = -1;  // claimer: the code published one entry ahead of the one it is working on
+  // claim the next code of the launch and publish it as entry n of the ring
+  __device__ int publish(uint32_t n) {
+    constexpr int R = TcSmem<D>::kSched;
+    const int slot = n % R;
+    mbar_wait(&S.sched_empty[slot], ((n / R) & 1) ^ 1);
+    const int idx = atomicAdd(P.a.sched, 1);
+    const int code = idx < P.a.n_codes ? P.a.cta_items[idx] : -1;
+    *reinterpret_cast<volatile int32_t*>(&S.sched_code[slot]) = code;
+    mbar_arrive(&S.sched_full[slot]);
+    return code;
+  }
   __device__ int next() {
     if (P.a.sched == nullptr) return it < end ? P.a.cta_items[it++] : -1;
+    if (claimer) {
+      // epi_q launches: one code of look-ahead, so the other roles learn item k+1 when the producer
+      // starts item k (its Q is then prepared a whole item ahead)
+      if (!EPI) return publish(k++);
+      if (k == 0) ahead = publish(0);
+      const int mine = ahead;
+      if (mine >= 0) ahead = publish(k + 1);
+      ++k;
+      return mine;
+    }
     constexpr int R = TcSmem<D>::kSched;
     const int slot = k % R;
     const uint32_t par = (k / R) & 1;
     ++k;
     int code;
-    if (claimer) {
-      mbar_wait(&S.sched_empty[slot], par ^ 1);
-      const int idx = atomicAdd(P.a.sched, 1);
-      code = idx < P.a.n_codes ? P.a.cta_items[idx] : -1;
-      *reinterpret_cast<volatile int32_t*>(&S.sched_code[slot]) = code;
-      mbar_arrive(&S.sched_full[slot]);
-    } else {
+    {
       mbar_wait(&S.sched_full[slot], par);
       code = *reinterpret_cast<volatile int32_t*>(&S.sched_code[slot]);
       mbar_arrive(&S.sched_empty[slot]);
@@ -210,7 +237,7 @@ __device__ __forceinline__ void ex2_pair_f16(float x0, float x1, float& p0, floa
 // after PV(j); V(j) is needed two steps later). Sub-tile s goes to slot s % (ring depth).
 // Each sub-tile is 64/bs paged blocks (bs <= 64) or half of one 128-row block, gathered by TMA
 // boxes {64 columns, min(bs, 64) rows}.
-template <int D>
+template <int D, bool EPI>
 __device__ void run_producer(const TcParams& P, TcSmem<D>& S, int it_begin, int it_end, int kv) {
   const AttnArgs& a = P.a;
   // programmatic dependent launch: the pages this launch reads are written by the preceding
@@ -226,7 +253,7 @@ __device__ void run_producer(const TcParams& P, TcSmem<D>& S, int it_begin, int 
   const CUtensorMap* map = kv == 0 ? &P.tmk : &P.tmv;
   uint32_t n = 0;
   uint32_t tc = 0;
-  ItemSrc<D> src(P, S, it_begin, it_end, kv == 0);
+  ItemSrc<D, EPI> src(P, S, it_begin, it_end, kv == 0);
   for (int code; (code = src.next()) >= 0;) {
     const Unit u = decode(P, code);
     const int kvh = u.head_a / group;
@@ -266,23 +293,24 @@ struct SubCursor {
   int t, h;  // KV tile, half (keys [64h, 64h+64))
 };
 
-template <int D>
+template <int D, bool EPI>
 __device__ void run_mma(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_begin, int it_end, int x) {
   const AttnArgs& a = P.a;
-  const bool J = P.join != 0;
+  const bool J = EPI || P.join != 0;  // 2-deep Q ring
   constexpr int kKS = TcSmem<D>::kKSlots, kVS = TcSmem<D>::kVSlots;
   constexpr uint32_t idS = idesc_bf16_f32(128, 64, false, false);
   constexpr uint32_t idO = idesc_bf16_f32(128, D, false, true);
   uint32_t jg = 0;  // sub-tiles whose PV has been issued (global): S buffer j & 1, V slot j
   uint32_t ep = 0;    // Q epochs started
   uint32_t qcur = 0;  // the epoch whose Q tile the S MMAs read
+  uint32_t n_items = 0;  // items of this head completed (prefill: o_free completions awaited)
   uint32_t tc = 0;
   auto wait_kv = [&](int kv, uint32_t n) {
     const uint32_t ns = kv == 0 ? kKS : kVS;
     mbar_wait(&S.kv_full[kv][n % ns], (n / ns) & 1);
     tc_fence_after();
   };
-  ItemSrc<D> src(P, S, it_begin, it_end, false);
+  ItemSrc<D, EPI> src(P, S, it_begin, it_end, false);
   for (int code; (code = src.next()) >= 0;) {
     const Unit u = decode(P, code);
     if (x >= u.n_heads) continue;  // unpaired launch: the B issuer idles
@@ -348,12 +376,21 @@ __device__ void run_mma(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_b
       const uint32_t j = jg;
       mbar_wait(&S.p_full[x][j & 1], (j >> 1) & 1);
       trace(P, 1, tc, 20);  // 20: P ready
+      if (EPI && first && n_items > 0) {
+        // prefill: the previous item's O has been drained by the epilogue warps. Completion
+        // n_items - 1 is the latest possible one (this thread waited for n_items - 2 before the
+        // previous item's first PV), so the parity wait cannot be lapped
+        mbar_wait(&S.o_free[x], (n_items - 1) & 1);
+        tc_fence_after();
+        trace(P, 1, tc, 26);  // 26: O free for the next item
+      }
       issue_pv(j, first);
       if (cs.t < te) issue_s();
       advance(cp);
       ++jg;
       first = false;
     }
+    ++n_items;
   }
 }
 
@@ -533,7 +570,124 @@ __device__ __forceinline__ void epilogue(const TcParams& P, TcSmem<D>& S, uint32
   if (tr) trace(P, 2 + x, tc, 33);  // 33: epilogue done
 }
 
-template <int D, int PM>
+// Prefill epilogue, run by the Q-prep warps (warp wq = 12 + i reads TMEM lanes [32i, 32i+32)) so
+// that it overlaps the softmax WGs' next item: per head x, wait for the row stats and the item's
+// last PV, drain O_x (times 1/l) from TMEM into the item's own Q slot of head x (free since the
+// item's last S MMA: the next item's Q is in the other slot of the 2-deep ring), release O_x
+// (o_free) as soon as the last TMEM load has landed, and store: TMA bulk stores of whole 32-row
+// slices, coalesced st.global for a ragged last slice (the rows after it belong to another item).
+// The slot goes back to the Q prep (q_empty) once the stores have read it. Staging per warp: the
+// warp's quarter of the slot (8 KB at d=128, 4 KB at d=64) as 4 KB chunks of 32 rows x 128 B,
+// SWIZZLE_128B (fp32: 32 columns per chunk, bf16: 64); bf16 O always fits, fp32 O cycles through
+// the chunk buffers (a chunk waits for the store of the chunk that used its buffer before).
+template <int D>
+__device__ void prefill_epilogue(const TcParams& P, TcSmem<D>& S, uint32_t tmem, const Unit& u, uint32_t jlast,
+                                 uint32_t k, uint32_t& tc) {
+  const AttnArgs& a = P.a;
+  const WorkItem& w = u.w;
+  const bool tr = (threadIdx.x & 31) == 0;
+  const int lane = threadIdx.x & 31;
+  const int wq = (threadIdx.x / 32) & 3;
+  const int r = wq * 32 + lane;
+  const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
+  const bool in_range = wq * 32 < w.n_rows;
+  const bool use_tma = in_range && wq * 32 + 32 <= w.n_rows;
+  const bool direct = in_range && !use_tma;
+  const bool f32 = a.out_fp32;
+  constexpr int kBufs = D / 64;  // 4 KB chunk buffers per warp in its quarter of a Q slot
+  const int n_chunks = f32 ? D / 32 : D / 64;
+  for (int x = 0; x < u.n_heads; ++x) {
+    uint8_t* const stg = q_tile<D>(S, true, x, k) + wq * kBufs * 4096;
+    mbar_wait(&S.fin_full[x][k & 1], (k >> 1) & 1);
+    const float inv = S.fin_inv[x][k & 1][r];
+    if (tr) trace(P, 4, tc, 60 + 4 * x);  // 60/64: row stats of head A/B ready
+    mbar_wait(&S.o_done[x][jlast & 1], (jlast >> 1) & 1);
+    tc_fence_after();
+    if (tr) trace(P, 4, tc, 61 + 4 * x);  // 61/65: O ready
+    const uint32_t ocol = tmem + lane_base + kColO + 128 * x;
+    const int h = u.head_a + x;
+    uint32_t vv[2][32];
+    tmem_ld32(ocol, vv[0]);
+    tmem_wait_ld();
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      if (c + 1 < D / 32) tmem_ld32(ocol + (c + 1) * 32, vv[(c + 1) & 1]);
+      const uint32_t(&v)[32] = vv[c & 1];
+      if (c + 1 == D / 32) {
+        // the last TMEM load has landed (waited at the end of the previous iteration): O_x is free
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.o_free[x]);
+        if (tr) trace(P, 4, tc, 62 + 4 * x);  // 62/66: O drained (o_free)
+      }
+      const int chunk = f32 ? c : c / 2;
+      uint8_t* ch = stg + (chunk % kBufs) * 4096;
+      if (f32 && chunk >= kBufs) {  // this buffer's previous chunk must have been read
+        if (lane == 0) {
+          if constexpr (kBufs == 1)
+            bulk_wait_read<0>();
+          else
+            bulk_wait_read<kBufs - 1>();
+        }
+        __syncwarp();
+      }
+      if (f32) {
+#pragma unroll
+        for (int uu = 0; uu < 8; ++uu)
+          *reinterpret_cast<float4*>(ch + lane * 128 + ((uu ^ (lane & 7)) * 16)) =
+              make_float4(__uint_as_float(v[4 * uu]) * inv, __uint_as_float(v[4 * uu + 1]) * inv,
+                          __uint_as_float(v[4 * uu + 2]) * inv, __uint_as_float(v[4 * uu + 3]) * inv);
+      } else {  // 64 columns (two fp32 chunks) per 128-byte row, 16-byte unit = 8 columns
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int uu = (c & 1) * 4 + q;
+          uint4 pk;
+          pk.x = pack_bf16x2(__uint_as_float(v[8 * q]) * inv, __uint_as_float(v[8 * q + 1]) * inv);
+          pk.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
+          pk.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv);
+          pk.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv);
+          *reinterpret_cast<uint4*>(ch + lane * 128 + ((uu ^ (lane & 7)) * 16)) = pk;
+        }
+      }
+      const bool chunk_done = f32 || (c & 1);
+      if (chunk_done && use_tma) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&P.tmo, ch, f32 ? c * 32 : (c / 2) * 64, h, w.row0 + wq * 32);
+          bulk_commit();
+        }
+      } else if (chunk_done && direct) {
+        __syncwarp();
+        // coalesced: 8 lanes cover one 128-byte staging row, 4 rows per instruction
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int rr = j * 4 + (lane >> 3);
+          const int uu = lane & 7;
+          const int trow = wq * 32 + rr;
+          if (trow < w.n_rows) {
+            const uint4 val = *reinterpret_cast<const uint4*>(ch + rr * 128 + ((uu ^ (rr & 7)) * 16));
+            const int64_t base = (static_cast<int64_t>(w.row0) + trow) * a.hq + h;
+            if (f32)
+              *reinterpret_cast<uint4*>(static_cast<float*>(a.o) + base * D + c * 32 + uu * 4) = val;
+            else
+              *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.o) + base * D + (c / 2) * 64 + uu * 8) = val;
+          }
+        }
+        __syncwarp();
+      }
+      tmem_wait_ld();
+    }
+    // the slot returns to the Q prep once this warp's stores have read it
+    if (lane == 0) {
+      bulk_wait_read<0>();
+      mbar_arrive(&S.q_empty[x][k & 1]);
+    }
+    __syncwarp();
+  }
+}
+
+template <int D, int PM, bool EPI>
 __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_begin, int it_end, int x) {
   const AttnArgs& a = P.a;
   const bool J = P.join != 0;
@@ -543,9 +697,10 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
   const uint32_t ocol = tmem + lane_base + kColO + 128 * x;
   uint32_t js = 0;  // sub-tiles processed (global; == the MMA warps' PV index)
   uint32_t eps = 0, ecur = 0;  // Q epochs seen / current (join: Q slots are also epilogue staging)
+  uint32_t ni = 0;             // prefill: items finished by this WG (fin_inv buffer ni & 1)
   uint32_t tc = 0;
   const bool tr = (threadIdx.x & 31) == 0;
-  ItemSrc<D> src(P, S, it_begin, it_end, false);
+  ItemSrc<D, EPI> src(P, S, it_begin, it_end, false);
   for (int code; (code = src.next()) >= 0;) {
     const Unit u = decode(P, code);
     if (x >= u.n_heads) continue;  // single-head unit: WG B idles
@@ -611,6 +766,19 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
         first = false;
       }
     }
+    if constexpr (EPI) {
+      // prefill: LSE straight from the row's thread; 1/l to the epilogue warps (Q prep), which
+      // drain O_x while this WG starts the next item. Buffer ni & 1 is rewritten two items
+      // later, which needs S of that item, issued only after the next item's first PV — after
+      // the epilogue warps arrived o_free, i.e. after they read this buffer
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      if (valid && a.lse != nullptr)
+        a.lse[row * a.hq + u.head_a + x] = l > 0.f ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
+      S.fin_inv[x][ni & 1][r] = inv;
+      mbar_arrive(&S.fin_full[x][ni & 1]);
+      ++ni;
+      continue;
+    }
     Finished f;
     f.w = w;
     f.m = m;
@@ -635,8 +803,11 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
 // (i, i + d/2) of row g = l / (32/R): the 16-byte unit u of the first half and the same unit of
 // the second half (d=128: the same offset in the second 64-column chunk; d=64: unit u + 4), so
 // no shuffles are needed. (cos, sin) of the 8 pairs live in registers.
+// (cos, sin) of a lane's 8 pairs are kept as float2 pairs of adjacent pairs — cc[k] = (cos of
+// pair 2k, cos of pair 2k+1), ss[k] likewise — the operand layout of the packed fp32x2
+// instructions, so the rotation and the angle recurrence need no register shuffles.
 template <int D>
-__device__ __forceinline__ void rotate_step(uint8_t* qs_base, int r, int u, const float (&c)[8], const float (&sn)[8]) {
+__device__ __forceinline__ void rotate_step(uint8_t* qs_base, int r, int u, const float2 (&cc)[4], const float2 (&ss)[4]) {
   uint8_t* p0;
   uint8_t* p1;
   if constexpr (D == 128) {
@@ -654,11 +825,9 @@ __device__ __forceinline__ void rotate_step(uint8_t* qs_base, int r, int u, cons
   for (int k = 0; k < 4; ++k) {
     const float2 xx = make_float2(__uint_as_float(av[k] << 16), __uint_as_float(av[k] & 0xFFFF0000u));
     const float2 yy = make_float2(__uint_as_float(bv[k] << 16), __uint_as_float(bv[k] & 0xFFFF0000u));
-    const float2 cc = make_float2(c[2 * k], c[2 * k + 1]), ss = make_float2(sn[2 * k], sn[2 * k + 1]);
-    const float2 ns = fmul2(ss, make_float2(-1.f, -1.f));
     // first half: x cos - y sin ; second half: y cos + x sin (packed fp32x2, same roundings)
-    const float2 o1 = ffma2(yy, ns, fmul2(xx, cc));
-    const float2 o2 = ffma2(xx, ss, fmul2(yy, cc));
+    const float2 o1 = ffma2(yy, fmul2(ss[k], make_float2(-1.f, -1.f)), fmul2(xx, cc[k]));
+    const float2 o2 = ffma2(xx, ss[k], fmul2(yy, cc[k]));
     oa[k] = pack_bf16x2(o1.x, o1.y);
     ob[k] = pack_bf16x2(o2.x, o2.y);
   }
@@ -666,21 +835,20 @@ __device__ __forceinline__ void rotate_step(uint8_t* qs_base, int r, int u, cons
   *reinterpret_cast<uint4*>(p1) = make_uint4(ob[0], ob[1], ob[2], ob[3]);
 }
 
-__device__ __forceinline__ void load_cs8(const float2* rope, int64_t idx, float (&c)[8], float (&sn)[8]) {
+// the (cos, sin) table entries of 8 consecutive pairs, regrouped into cos / sin pairs
+__device__ __forceinline__ void load_cs8(const float2* rope, int64_t idx, float2 (&cc)[4], float2 (&ss)[4]) {
   const float4* t = reinterpret_cast<const float4*>(rope + idx);
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const float4 v = __ldg(t + e);
-    c[2 * e] = v.x;
-    sn[2 * e] = v.y;
-    c[2 * e + 1] = v.z;
-    sn[2 * e + 1] = v.w;
+    const float4 v = __ldg(t + e);  // (cos i, sin i, cos i+1, sin i+1)
+    cc[e] = make_float2(v.x, v.z);
+    ss[e] = make_float2(v.y, v.w);
   }
 }
 
 template <int D>
 __device__ __forceinline__ void rotate_q_tile(uint8_t* qs_base, const float2* rope, int my_pos, int my_valid, int rot,
-                                              int max_pos, bool table) {
+                                              int max_pos) {
   constexpr int kLanesPerRow = D / 16;       // 8 pairs per lane
   constexpr int R = 32 / kLanesPerRow;       // rows per step
   const int lane = threadIdx.x & 31;
@@ -693,39 +861,22 @@ __device__ __forceinline__ void rotate_q_tile(uint8_t* qs_base, const float2* ro
   // table value: ~1e-6 drift vs bf16's 4e-3) instead of a table row per row.
   const bool consecutive = __all_sync(0xffffffffu, !my_valid || my_pos == p_first + lane) && p_first - rot >= 0 &&
                            p_first - rot + 31 < max_pos;
-  float c[8], sn[8];
-  if (consecutive && table) {
-    // table rows per step (4 x 16 B loads, the next step's prefetched) instead of the recurrence
-    float c2[8], s2[8];
-    const int64_t base = static_cast<int64_t>(p_first - rot + g) * (D / 2) + pair0;
-    load_cs8(rope, base, c, sn);
-#pragma unroll
-    for (int st = 0; st < 32 / R; ++st) {
-      if (st + 1 < 32 / R) load_cs8(rope, base + static_cast<int64_t>((st + 1) * R) * (D / 2), c2, s2);
-      rotate_step<D>(qs_base, wq * 32 + st * R + g, u, c, sn);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        c[e] = c2[e];
-        sn[e] = s2[e];
-      }
-    }
-  } else if (consecutive) {
-    float cd[8], sd[8];
-    load_cs8(rope, static_cast<int64_t>(p_first - rot + g) * (D / 2) + pair0, c, sn);
+  float2 cc[4], ss[4];
+  if (consecutive) {
+    float2 cd[4], sd[4];
+    load_cs8(rope, static_cast<int64_t>(p_first - rot + g) * (D / 2) + pair0, cc, ss);
     load_cs8(rope, static_cast<int64_t>(R) * (D / 2) + pair0, cd, sd);  // position R: (cos R th, sin R th)
+    float2 sdn[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sdn[e] = fmul2(sd[e], make_float2(-1.f, -1.f));
 #pragma unroll
     for (int st = 0; st < 32 / R; ++st) {
-      rotate_step<D>(qs_base, wq * 32 + st * R + g, u, c, sn);
+      rotate_step<D>(qs_base, wq * 32 + st * R + g, u, cc, ss);
 #pragma unroll
-      for (int e = 0; e < 8; e += 2) {  // advance the angles by R*theta (packed, same roundings)
-        const float2 c2 = make_float2(c[e], c[e + 1]), s2 = make_float2(sn[e], sn[e + 1]);
-        const float2 cd2 = make_float2(cd[e], cd[e + 1]), sd2 = make_float2(sd[e], sd[e + 1]);
-        const float2 cn = ffma2(c2, cd2, fmul2(fmul2(s2, make_float2(-1.f, -1.f)), sd2));
-        const float2 sn2 = ffma2(s2, cd2, fmul2(c2, sd2));
-        c[e] = cn.x;
-        c[e + 1] = cn.y;
-        sn[e] = sn2.x;
-        sn[e + 1] = sn2.y;
+      for (int e = 0; e < 4; ++e) {  // advance the angles by R*theta (packed, same roundings)
+        const float2 cn = ffma2(cc[e], cd[e], fmul2(ss[e], sdn[e]));  // c cosR - s sinR
+        ss[e] = ffma2(ss[e], cd[e], fmul2(cc[e], sd[e]));            // s cosR + c sinR
+        cc[e] = cn;
       }
     }
   } else {
@@ -733,13 +884,13 @@ __device__ __forceinline__ void rotate_q_tile(uint8_t* qs_base, const float2* ro
     for (int st = 0; st < 32 / R; ++st) {
       const int p = __shfl_sync(0xffffffffu, my_pos, st * R + g);
       const int rp = min(max(p - rot, 0), max_pos - 1);
-      load_cs8(rope, static_cast<int64_t>(rp) * (D / 2) + pair0, c, sn);
-      rotate_step<D>(qs_base, wq * 32 + st * R + g, u, c, sn);
+      load_cs8(rope, static_cast<int64_t>(rp) * (D / 2) + pair0, cc, ss);
+      rotate_step<D>(qs_base, wq * 32 + st * R + g, u, cc, ss);
     }
   }
 }
 
-template <int D>
+template <int D, bool EPI>
 __device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_end) {
   const AttnArgs& a = P.a;
   const bool J = P.join != 0;
@@ -751,7 +902,7 @@ __device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_
   uint32_t tc = 0;
   uint32_t load_phase = 0;  // bit 2x + s: parity of the next q_load[x][s] completion
   const bool tr = lane == 0;
-  ItemSrc<D> src(P, S, it_begin, it_end, false);
+  ItemSrc<D, EPI> src(P, S, it_begin, it_end, false);
   const bool early_b = (P.qprep_mode & 1) != 0, prefetch = (P.qprep_mode & 2) != 0;
   // thread 0: TMA of head x's pre-RoPE tile into its slot of epoch ep
   auto load = [&](int x, const Unit& u) {
@@ -806,7 +957,7 @@ __device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_
           mbar_wait(&S.q_load[x][sl], (load_phase >> bit) & 1);
           load_phase ^= 1u << bit;
           if (tr) trace(P, 4, tc, 44 + x);  // 44/45: Q tile A/B loaded
-          rotate_q_tile<D>(q_tile<D>(S, J, x, ep), a.rope, my_pos, my_row < w.n_rows, rot, a.max_pos, P.qrot_table);
+          rotate_q_tile<D>(q_tile<D>(S, J, x, ep), a.rope, my_pos, my_row < w.n_rows, rot, a.max_pos);
           fence_proxy_async_smem();
         } else {
           mbar_wait(&S.q_empty[x][sl], epar);
@@ -828,7 +979,80 @@ __device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_
   }
 }
 
-template <int D, int PM>
+// Prefill launches (paired heads): Q prep through a 2-deep ring (item k in slot k & 1, prepared
+// while item k - 1 runs: the rotation is off the item boundary) and the epilogue of every item
+// (prefill_epilogue, staged in that item's own slot). Order: Q(0); then per item k: Q(k+1), the
+// epilogue of k. Q(k+1) waits for slot (k+1) & 1, released by the epilogue of k - 1 (done in the
+// previous iteration) and item k - 1's last S MMA; the epilogue of k waits for item k's last PV.
+template <int D, bool EPI>
+__device__ void run_qprep_epi(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_begin, int it_end) {
+  const AttnArgs& a = P.a;
+  const int lane = threadIdx.x & 31;
+  const int wq = (threadIdx.x / 32) & 3;
+  constexpr uint32_t kQBytes = 128 * D * 2;
+  uint32_t tc = 0;
+  uint32_t load_phase = 0;  // bit 2x + s: parity of the next q_load[x][s] completion
+  const bool tr = lane == 0;
+  ItemSrc<D, EPI> src(P, S, it_begin, it_end, false);
+  const int my_row = wq * 32 + lane;
+  // prepare the (single-epoch) Q tiles of item e in slot e & 1
+  auto prep = [&](const Unit& u, uint32_t e) {
+    const WorkItem& w = u.w;
+    const int sl = static_cast<int>(e & 1);
+    const uint32_t epar = ((e >> 1) & 1) ^ 1;
+    const int my_pos = my_row < w.n_rows ? a.pos[static_cast<int64_t>(w.row0) + my_row] : 0;
+    if (wq == 0) {
+      // warp 12 waits for both slots (converged), lane 0 issues both loads (they overlap A's rotation)
+      for (int x = 0; x < u.n_heads; ++x) {
+        mbar_wait(&S.q_empty[x][sl], epar);
+        if (tr) trace(P, 4, tc, 40 + x);  // 40/41: slot free for head A/B
+        if (lane == 0) {
+          uint64_t* bar = &S.q_load[x][sl];
+          uint8_t* dst = q_tile<D>(S, true, x, e);
+          mbar_arrive_expect_tx(bar, kQBytes);
+#pragma unroll
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_3d(dst + c * TcSmem<D>::kChunkBytes, &P.tmq, bar, c * 64, u.head_a + x, w.row0);
+        }
+        __syncwarp();
+      }
+    }
+    for (int x = 0; x < u.n_heads; ++x) {
+      const int bit = 2 * x + sl;
+      mbar_wait(&S.q_load[x][sl], (load_phase >> bit) & 1);
+      load_phase ^= 1u << bit;
+      if (tr) trace(P, 4, tc, 44 + x);  // 44/45: Q tile A/B loaded
+      rotate_q_tile<D>(q_tile<D>(S, true, x, e), a.rope, my_pos, my_row < w.n_rows, 0, a.max_pos);
+      fence_proxy_async_smem();
+      if (tr) trace(P, 4, tc, 42 + x);  // 42/43: Q tile A/B written
+      mbar_arrive(&S.q_full[x][sl]);
+    }
+  };
+  int code = src.next();
+  if (code < 0) return;
+  Unit cur = decode(P, code);
+  uint32_t jtot = static_cast<uint32_t>(cur.w.n_sub);
+  uint32_t cur_jlast = jtot - 1;
+  prep(cur, 0);
+  for (uint32_t k = 0;; ++k) {
+    code = src.next();
+    const bool more = code >= 0;
+    Unit nxt{};
+    uint32_t nxt_jlast = 0;
+    if (more) {
+      nxt = decode(P, code);
+      jtot += static_cast<uint32_t>(nxt.w.n_sub);
+      nxt_jlast = jtot - 1;
+      prep(nxt, k + 1);
+    }
+    prefill_epilogue<D>(P, S, tmem, cur, cur_jlast, k, tc);
+    if (!more) break;
+    cur = nxt;
+    cur_jlast = nxt_jlast;
+  }
+}
+
+template <int D, int PM, bool EPI>
 __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_constant__ TcParams P) {
   extern __shared__ uint8_t smem_raw[];
   TcSmem<D>& S = smem_ref<D>(smem_raw);
@@ -842,7 +1066,9 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
     for (int i = 0; i < TcSmem<D>::kQSlots; ++i)
       for (int sl = 0; sl < 2; ++sl) {
         mbar_init(&S.q_full[i][sl], 128);
-        mbar_init(&S.q_empty[i][sl], P.join ? 1 + 4 : 1);  // join: + the 4 epilogue warps of head i
+        // 2-deep ring: + the 4 warps whose epilogue stages in the slot (join: softmax WG of head i,
+        // prefill: the Q-prep warps)
+        mbar_init(&S.q_empty[i][sl], (EPI || P.join) ? 1 + 4 : 1);
         mbar_init(&S.q_load[i][sl], 1);
       }
     for (int i = 0; i < 2; ++i) {
@@ -856,6 +1082,9 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
       mbar_init(&S.sched_empty[2 * i], kSchedConsumers);
       mbar_init(&S.sched_empty[2 * i + 1], kSchedConsumers);
       mbar_init(&S.o_done[i][1], 1);
+      mbar_init(&S.o_free[i], 4);  // one arrival per epilogue (Q-prep) warp
+      mbar_init(&S.fin_full[i][0], 128);
+      mbar_init(&S.fin_full[i][1], 128);
     }
     fence_barrier_init();
   }
@@ -880,18 +1109,21 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
   if (warp < 4) {
     reg_dealloc<56>();
     if (warp == 0 || warp == 3) {
-      if (elect_one()) run_producer<D>(P, S, it_begin, it_end, warp == 0 ? 0 : 1);
+      if (elect_one()) run_producer<D, EPI>(P, S, it_begin, it_end, warp == 0 ? 0 : 1);
     } else {
-      if (elect_one()) run_mma<D>(P, S, tmem, it_begin, it_end, warp - 1);
+      if (elect_one()) run_mma<D, EPI>(P, S, tmem, it_begin, it_end, warp - 1);
     }
   } else if (warp < 12) {
     reg_alloc<160>();
-    run_softmax<D, PM>(P, S, tmem, it_begin, it_end, warp < 8 ? 0 : 1);
+    run_softmax<D, PM, EPI>(P, S, tmem, it_begin, it_end, warp < 8 ? 0 : 1);
   } else {
     reg_dealloc<120>();
-    run_qprep<D>(P, S, it_begin, it_end);
+    if constexpr (EPI)
+      run_qprep_epi<D, EPI>(P, S, tmem, it_begin, it_end);
+    else
+      run_qprep<D, EPI>(P, S, it_begin, it_end);
   }
-  if (warp >= 4 && warp < 12 && (threadIdx.x & 31) == 0) bulk_wait<0>();  // epilogue stores done
+  if (warp >= 4 && (threadIdx.x & 31) == 0) bulk_wait<0>();  // epilogue stores done
   tc_fence_before();
   __syncthreads();
   if (P.a.sched != nullptr && threadIdx.x == 0) {
@@ -915,14 +1147,20 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
   }
 }
 
-template <int D, int PM>
+template <int D, int PM, bool EPI>
 cudaError_t launch_dp(const AttnArgs& a, cudaStream_t st) {
-  static bool attr_set = false;
-  const int smem = static_cast<int>(sizeof(TcSmem<D>)) + 1024;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(span_attn_tc_kernel<D, PM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  // the large-smem attribute is per device: one bit per device ordinal that has it set
+  static std::atomic<uint64_t> attr_set{0};
+  const int smem = static_cast<int>(sizeof(TcSmem<D>));
+  static_assert(sizeof(TcSmem<D>) <= 232448, "shared memory budget (227 KB per CTA)");
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_set.load() & bit)) {
+    e = cudaFuncSetAttribute(span_attn_tc_kernel<D, PM, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set.fetch_or(bit);
   }
   TcParams p;
   p.tmk = *a.tmap_k;
@@ -936,12 +1174,10 @@ cudaError_t launch_dp(const AttnArgs& a, cudaStream_t st) {
   p.poly_mask = PM;
   p.rescale_threshold = a.rescale_threshold;
   p.dbg_mode = getenv("SPANQ_DBG_MODE") ? atoi(getenv("SPANQ_DBG_MODE")) : 0;
-  p.qrot_table = getenv("SPANQ_QROT_TABLE") ? atoi(getenv("SPANQ_QROT_TABLE")) : 0;
-  p.qprep_mode = getenv("SPANQ_QPREP") ? atoi(getenv("SPANQ_QPREP")) : 3;
-  // 2-deep Q ring (paired launches): knob SPANQ_QRING2 = 0 off, 1 joins only (default), 2 joins and
-  // prefill (A/B: the prefill gains nothing — its epilogue then contends with the next item's S MMAs)
-  static const int ring = getenv("SPANQ_QRING2") ? atoi(getenv("SPANQ_QRING2")) : 1;
-  p.join = a.paired && (ring >= 2 || (ring == 1 && a.join)) ? 1 : 0;
+  p.qprep_mode = 3;
+  // joins of paired launches: 2-deep Q ring per head in the staging area
+  p.join = a.paired && a.join ? 1 : 0;
+  p.epi_q = EPI ? 1 : 0;
   // launched as a programmatic dependent of the preceding K1 when the caller says it directly
   // precedes (a.pdl; knob SPANQ_PDL=0 turns it off): the prologue and Q preparation overlap
   // K1's tail (see run_producer)
@@ -956,17 +1192,19 @@ cudaError_t launch_dp(const AttnArgs& a, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl && a.pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, span_attn_tc_kernel<D, PM>, p);
+  return cudaLaunchKernelEx(&cfg, span_attn_tc_kernel<D, PM, EPI>, p);
 }
 
 template <int D>
 cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
-  switch (a.poly_mask) {  // 0: MUFU fp32, 1/2: 25%/50% FMA-pipe polynomial, 3: MUFU f16x2
-    case 0: return launch_dp<D, 0>(a, st);
-    case 1: return launch_dp<D, 1>(a, st);
-    case 2: return launch_dp<D, 2>(a, st);
-    default: return launch_dp<D, 3>(a, st);
-  }
+  // Q-prep-warp epilogue + 2-deep Q ring (a separate kernel instance, EPI) for the prefill
+  // launches where it measured faster: bf16 O (C2 prefill 0.270 -> 0.256 ms) and d = 64 (C4
+  // 0.311 -> 0.296 ms); fp32 O at d = 128 keeps the softmax-WG epilogue (its fp32 drain cycles
+  // through 2 x 4 KB per warp of the Q slot, and measured 0.255 vs 0.247 ms)
+  const bool epi = a.paired && !a.join && (!a.out_fp32 || D == 64);
+  // exp2: 0 = MUFU ex2 (fp32), else MUFU ex2.f16x2 (two exponentials per op)
+  if (a.poly_mask == 0) return epi ? launch_dp<D, 0, true>(a, st) : launch_dp<D, 0, false>(a, st);
+  return epi ? launch_dp<D, 3, true>(a, st) : launch_dp<D, 3, false>(a, st);
 }
 
 }  // namespace

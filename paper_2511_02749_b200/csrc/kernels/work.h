@@ -32,7 +32,8 @@ struct WorkItem {
   int32_t tile_begin;  // KV tile range [tile_begin, tile_end)
   int32_t tile_end;
   int32_t part;        // -1: write final O/LSE; >= 0: split-KV partial slot
-  int32_t pad0, pad1, pad2;
+  int32_t n_sub;       // 64-key sub-tiles of the item (tiles with n_valid > 64 count twice)
+  int32_t pad1, pad2;
 };
 
 // Split-KV partials are per work unit: partial slot p holds the unit's heads, rows

@@ -203,8 +203,9 @@ spq_status make_qmap(const spq_ctx* c, const void* q, int64_t rows, CUtensorMap*
   return SPQ_OK;
 }
 
-// fp32 output maps for the epilogue's TMA stores: o as 3D {d, hq, rows} box {32, 1, 32};
-// partials as 2D {d, parts*hq*128} box {32, 32}; both SWIZZLE_128B (the staging layout)
+// output maps for the epilogue's TMA stores: o as 3D {d, hq, rows}, box {32, 1, 32} (fp32) or
+// {64, 1, 32} (bf16): 128-byte rows; partials as 2D {d, parts*hq*128} box {32, 32}; all
+// SWIZZLE_128B (the staging layout)
 spq_status make_omap(const spq_ctx* c, const void* o, int64_t rows, CUtensorMap* out) {
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult qr;
@@ -213,11 +214,13 @@ spq_status make_omap(const spq_ctx* c, const void* o, int64_t rows, CUtensorMap*
   const spq_config& g = c->cfg;
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.head_dim), static_cast<cuuint64_t>(g.num_q_heads),
                         static_cast<cuuint64_t>(std::max<int64_t>(rows, 1))};
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.head_dim) * 4,
-                           static_cast<cuuint64_t>(g.head_dim) * 4 * g.num_q_heads};
-  cuuint32_t box[3] = {32, 1, 32};
+  const bool f32 = g.out_dtype == SPQ_FP32;
+  const cuuint64_t elt = f32 ? 4 : 2;
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.head_dim) * elt,
+                           static_cast<cuuint64_t>(g.head_dim) * elt * g.num_q_heads};
+  cuuint32_t box[3] = {f32 ? 32u : 64u, 1, 32};
   cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = reinterpret_cast<EncodeTiledFn>(fn)(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(o), dims,
+  CUresult r = reinterpret_cast<EncodeTiledFn>(fn)(out, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(o), dims,
                                                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -780,11 +783,9 @@ spq_status spq_prefill_jobs(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, i
     s = make_qmap(c, q, r1 - r0, &qmap);
     if (s != SPQ_OK) return s;
     args.tmap_q = &qmap;
-    if (c->cfg.out_dtype == SPQ_FP32) {
-      s = make_omap(c, o, r1 - r0, &omap);
-      if (s != SPQ_OK) return s;
-      args.tmap_o = &omap;
-    }
+    s = make_omap(c, o, r1 - r0, &omap);  // prefill epilogue: TMA stores in either out dtype
+    if (s != SPQ_OK) return s;
+    args.tmap_o = &omap;
   }
   if (c->timing) CUDA_TRY(cudaEventRecord(c->ev[0], st));
   s = run_attn(c, args, st);

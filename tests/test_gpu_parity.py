@@ -124,10 +124,12 @@ def test_c1_fp32(cuda_dev, variant):
     run_and_check(inputs.c1(variant=variant), cuda_dev)
 
 
+@pytest.mark.parametrize("out_dtype", ["fp32", "bf16"])
 @pytest.mark.parametrize("bs", [16, 64, 128])
-def test_bf16_small_rag(cuda_dev, bs):
+def test_bf16_small_rag(cuda_dev, bs, out_dtype):
+    # fp32 / bf16 O at d = 128 take different prefill epilogues (softmax WG vs Q-prep warps)
     w = inputs.make_rag(101, inputs.Shape(**inputs.SHAPE_8B, block_size=bs), 96, 3, [130, 256, 77], 150)
-    run_and_check(w, cuda_dev)
+    run_and_check(w, cuda_dev, out_dtype=out_dtype)
 
 
 def test_bf16_ragged_gqa1_d64(cuda_dev):
@@ -168,12 +170,13 @@ def test_bf16_exp2_mufu_and_poly(cuda_dev, monkeypatch, poly):
     run_and_check(w, cuda_dev)
 
 
-def test_bf16_multi_query_batch(cuda_dev):
+@pytest.mark.parametrize("out_dtype", ["fp32", "bf16"])
+def test_bf16_multi_query_batch(cuda_dev, out_dtype):
     sh = inputs.Shape(hq=8, hkv=2, d=128, block_size=16, vocab=256)
     qs = inputs.random_queries(104, 6, vocab=256, max_frag=5, max_len=200, max_prefix=150,
                                max_cross=180, reuse_p=0.5)
     w = inputs.Workload("batch", sh, qs, 104)
-    run_and_check(w, cuda_dev)
+    run_and_check(w, cuda_dev, out_dtype=out_dtype)
 
 
 def test_c3_shrunk_reuse_and_permutation(cuda_dev):
@@ -181,8 +184,9 @@ def test_c3_shrunk_reuse_and_permutation(cuda_dev):
     run_and_check(w, cuda_dev)
 
 
-def test_c4_shrunk_judge(cuda_dev):
-    run_and_check(inputs.c4(scale=0.125), cuda_dev)
+@pytest.mark.parametrize("out_dtype", ["fp32", "bf16"])
+def test_c4_shrunk_judge(cuda_dev, out_dtype):
+    run_and_check(inputs.c4(scale=0.125), cuda_dev, out_dtype=out_dtype)
 
 
 def test_hit_join_equals_recompute_join_bitexact(cuda_dev):
@@ -473,8 +477,9 @@ def test_full_size_c3_warm_sampled_rows(cuda_dev):
     ctx.close()
 
 
-@pytest.mark.parametrize("hq,hkv,d", [(3, 3, 64), (6, 2, 128), (8, 2, 64)])
-def test_many_tiny_epochs_stress(cuda_dev, hq, hkv, d):
+@pytest.mark.parametrize("hq,hkv,d,out_dtype", [(3, 3, 64, "fp32"), (6, 2, 128, "fp32"), (8, 2, 64, "fp32"),
+                                                (6, 2, 128, "bf16"), (8, 2, 64, "bf16")])
+def test_many_tiny_epochs_stress(cuda_dev, hq, hkv, d, out_dtype):
     """Many one-sub-tile Q epochs (fragments of 1-20 tokens, many queries) in unpaired (odd GQA
     group) and paired launches, repeated: the Q-ring barrier protocol under its tightest timing
     (the unpaired slot-B wait once lapped and deadlocked here)."""
@@ -482,4 +487,4 @@ def test_many_tiny_epochs_stress(cuda_dev, hq, hkv, d):
     for rep in range(3):
         qs = inputs.random_queries(300 + rep, 12, vocab=128, max_frag=6, max_len=20, max_prefix=24,
                                    max_cross=40, reuse_p=0.3)
-        run_and_check(inputs.Workload("tiny", sh, qs, 300 + rep), cuda_dev, nblk=2048)
+        run_and_check(inputs.Workload("tiny", sh, qs, 300 + rep), cuda_dev, nblk=2048, out_dtype=out_dtype)
