@@ -37,7 +37,7 @@ typedef enum {
   SPQ_EINVAL = 1, /* bad argument, tree shape, op code, arity, empty leaf, negative token   */
   SPQ_ENOMEM = 2, /* the block pool cannot hold the plan's blocks; the plan is rolled back  */
   SPQ_ECUDA = 3,  /* CUDA launch/runtime failure, or no usable sm_100 device               */
-  SPQ_ENCCL = 4,  /* reserved for the multi-GPU exchange                                    */
+  SPQ_ENCCL = 4,  /* NCCL failure in the library's own exchange (spq_exchange_nccl)          */
   SPQ_ESTATE = 5  /* plan used after release, job/query range out of bounds, wrong mode     */
 } spq_status;
 
@@ -205,7 +205,10 @@ spq_status spq_join_phase(spq_ctx *ctx, spq_plan *plan, int32_t layer, int32_t p
                           const void *k, const void *v, void *o, float *lse, void *stream);
 
 /* Stream-ordered release: unpins the plan's blocks and frees its plan-private blocks; later
- * kernel calls on any stream wait for `stream` to pass this point before touching them. */
+ * kernel calls on any stream wait for `stream` to pass this point before touching them. The
+ * handle stays reserved (emptied) for the next 1024 releases of the ctx: any call on it in that
+ * window returns SPQ_ESTATE ("plan used after release"); after it the handle must not be used.
+ * Plans never released are freed by spq_destroy. */
 spq_status spq_plan_release(spq_ctx *ctx, spq_plan *plan, void *stream);
 
 /* ------------------------------------------------------------------ store admin / stats */
@@ -234,9 +237,12 @@ spq_status spq_read_blocks(spq_ctx *ctx, int32_t layer, const int32_t *block_ids
  * overwritten only after every move reading it, and a cycle rotates through one scratch slot.
  * A source may feed several destinations ("duplication"); a destination appears once.
  * src/dst/delta are HOST arrays of n entries; the pools are the ctx's; stream-ordered on
- * `stream`. Blocks referenced by a live plan are the caller's to avoid. SPQ_EINVAL: null array,
- * id outside [0, num_blocks), a destination written twice, |delta| >= max_position, head_dim not
- * 64/128; SPQ_ESTATE: host-only ctx or bad layer range; SPQ_ECUDA: launch failure. */
+ * `stream`. Store effect: every destination block is dropped from the content-hash index (it no
+ * longer holds what its digest names; it becomes a free block whose moved content the caller
+ * owns until a later plan allocates it), so no later plan can hit stale KV. SPQ_EINVAL: null
+ * array, id outside [0, num_blocks), a destination written twice, |delta| >= max_position,
+ * head_dim not 64/128; SPQ_ESTATE: host-only ctx, bad layer range, or a source/destination block
+ * pinned by a live plan (nothing is moved); SPQ_ECUDA: launch failure. */
 typedef struct {
   int64_t moves, components, cycles, duplicates, ops, max_component_ops;
 } spq_cidra_stats;
@@ -249,6 +255,25 @@ spq_status spq_reposition(spq_ctx *ctx, const int32_t *src, const int32_t *dst, 
 spq_status spq_cidra_schedule(const spq_ctx *ctx, const int32_t *src, const int32_t *dst, const int32_t *delta,
                               int64_t n, int32_t *ops, int64_t cap, int64_t *n_ops, int32_t *comp_off,
                               int64_t comp_cap, int64_t *n_comp, spq_cidra_stats *stats /*or null*/);
+
+/* ------------------------------------------------------------------ options */
+typedef enum {
+  SPQ_OPT_EXP2 = 1,              /* softmax exp2 on MUFU: 0 = ex2 fp32 (default), 1 = ex2.f16x2
+                                    (two exponentials per op; inputs rounded to f16)           */
+  SPQ_OPT_RESCALE_THRESHOLD = 2, /* O is rescaled when a row max grows by more than this (log2
+                                    units, default 8; 0 = on every growth). Exact either way  */
+  SPQ_OPT_PDL = 3,               /* 1 (default): attention/combine launched as programmatic
+                                    dependents of the kernel before them; 0: plain launches  */
+  SPQ_OPT_HASH_SCALAR = 4        /* process-wide: 1 = scalar BLAKE2b compression even with AVX2
+                                    (same digests; lets tests cover both), 0 = default        */
+} spq_option;
+/* Set a ctx option (applies to later calls). SPQ_EINVAL on an unknown key or a bad value. */
+spq_status spq_set_option(spq_ctx *ctx, int32_t key, double value);
+/* Profiling builds only (build.py --profiling defines SPANQ_PROFILING): a device buffer of
+ * int64 [16 warps][1024][2] (event, clock64) + [2 * grid] (%globaltimer per CTA) that the
+ * attention kernel's CTA 0 fills, and a timing-variant mode (0 = off). The product library
+ * returns SPQ_EINVAL. */
+spq_status spq_set_trace(spq_ctx *ctx, void *device_buf, int32_t mode);
 
 /* Instrumentation: kernel launches issued by this ctx so far, and the CUDA events bracketing
  * the most recent attention launch (for roofline timing on the launching stream). */

@@ -2,6 +2,8 @@
 
     python -m paper_2511_02749_b200.build            # build if stale
     python -m paper_2511_02749_b200.build --force
+    python -m paper_2511_02749_b200.build --profiling  # lib/libspanq_prof.so (tools/ only:
+                                                       # CTA-0 timelines, timing variants)
 
 The library links the CUDA runtime statically and resolves the driver entry point for TMA
 descriptors at run time (cudaGetDriverEntryPoint), so it loads on CPU-only hosts too (the
@@ -40,18 +42,18 @@ def headers():
     return hs
 
 
-def _obj(src):
+def _obj(src, profiling=False):
     rel = os.path.relpath(src, CSRC).replace(os.sep, "_")
-    return os.path.join(BUILD, rel + ".o")
+    return os.path.join(BUILD + ("_prof" if profiling else ""), rel + ".o")
 
 
-def _compile(src, hdr_mtime, force, verbose_ptxas):
-    obj = _obj(src)
+def _compile(src, hdr_mtime, force, verbose_ptxas, profiling=False):
+    obj = _obj(src, profiling)
     if not force and os.path.exists(obj):
         m = os.path.getmtime(obj)
         if m >= os.path.getmtime(src) and m >= hdr_mtime:
             return obj, None
-    cmd = [NVCC] + ARCH + COMMON + ["-c", src, "-o", obj]
+    cmd = [NVCC] + ARCH + COMMON + (["-DSPANQ_PROFILING"] if profiling else []) + ["-c", src, "-o", obj]
     if src.endswith(".cu"):
         cmd += ["-Xptxas", "-v"] if verbose_ptxas else []
     else:
@@ -62,34 +64,38 @@ def _compile(src, hdr_mtime, force, verbose_ptxas):
     return obj, (r.stderr if verbose_ptxas and src.endswith(".cu") else None)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, profiling: bool = False) -> str:
+    """Build lib/libspanq.so (or, with profiling=True, lib/libspanq_prof.so: -DSPANQ_PROFILING
+    compiles in the CTA-0 trace and the timing variants that spq_set_trace drives)."""
+    os.makedirs(BUILD + ("_prof" if profiling else ""), exist_ok=True)
     os.makedirs(LIBDIR, exist_ok=True)
+    lib_path = os.path.join(LIBDIR, "libspanq_prof.so") if profiling else LIB
     cu, cpp = sources()
     hdr_mtime = max(os.path.getmtime(h) for h in headers())
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        futs = [ex.submit(_compile, s, hdr_mtime, force, verbose) for s in cu + cpp]
+        futs = [ex.submit(_compile, s, hdr_mtime, force, verbose, profiling) for s in cu + cpp]
         results = [f.result() for f in futs]
     objs = [o for o, _ in results]
     if verbose:
         for _, log in results:
             if log:
                 sys.stderr.write(log)
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
-        return LIB
-    cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs + ["-lpthread", "-ldl", "-lrt"]
+    if not force and os.path.exists(lib_path) and os.path.getmtime(lib_path) >= max(os.path.getmtime(o) for o in objs):
+        return lib_path
+    cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", lib_path] + objs + ["-lpthread", "-ldl", "-lrt"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
-    return LIB
+    return lib_path
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", "--verbose", action="store_true", help="print ptxas resource usage")
+    ap.add_argument("--profiling", action="store_true", help="build lib/libspanq_prof.so (tools only)")
     a = ap.parse_args()
-    print(build(force=a.force, verbose=a.verbose))
+    print(build(force=a.force, verbose=a.verbose, profiling=a.profiling))
 
 
 if __name__ == "__main__":

@@ -3,6 +3,8 @@
 // counter, final-block flag, parameter block {digest length, key length 0, fanout 1, depth 1}.
 #include "blake2b.h"
 
+#include <atomic>
+
 #include <immintrin.h>
 
 #include <cstdlib>
@@ -158,14 +160,12 @@ __attribute__((target("avx2"))) void compress_avx2(uint64_t* h, const uint8_t* b
 }
 
 using CompressFn = void (*)(uint64_t*, const uint8_t*, uint64_t, uint64_t, bool);
-CompressFn pick_compress() {
-  const char* e = std::getenv("SPANQ_BLAKE2B_SCALAR");  // test knob: force the scalar path
-  if (e == nullptr && __builtin_cpu_supports("avx2")) return compress_avx2;
-  return compress;
-}
-const CompressFn kCompress = pick_compress();
+const bool kHaveAvx2 = __builtin_cpu_supports("avx2");
+std::atomic<bool> g_force_scalar{false};  // SPQ_OPT_HASH_SCALAR (tests: both compressions)
 
 }  // namespace
+
+void blake2b_force_scalar(bool on) { g_force_scalar.store(on); }
 
 void blake2b(uint8_t* out, size_t outlen, const void* data, size_t len) {
   uint64_t h[8];
@@ -173,6 +173,7 @@ void blake2b(uint8_t* out, size_t outlen, const void* data, size_t len) {
   h[0] ^= 0x01010000ULL ^ static_cast<uint64_t>(outlen);  // fanout 1, depth 1, no key
   const uint8_t* p = static_cast<const uint8_t*>(data);
   uint64_t t = 0;
+  const CompressFn kCompress = kHaveAvx2 && !g_force_scalar.load(std::memory_order_relaxed) ? compress_avx2 : compress;
   // all full blocks except the last one
   while (len > 128) {
     t += 128;

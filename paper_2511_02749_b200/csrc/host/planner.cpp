@@ -305,7 +305,11 @@ int owner_rank(const Digest& d, int world) {
 
 int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* pool, int rank, int world) {
   std::vector<QueryDigests> qd;
-  static const bool prof = std::getenv("SPANQ_PROFILE") != nullptr;
+#ifdef SPANQ_PROFILING
+  static const bool prof = std::getenv("SPANQ_PROFILE") != nullptr;  // profiling builds only
+#else
+  constexpr bool prof = false;
+#endif
   auto t0 = std::chrono::steady_clock::now();
   hash_all(qs, bs_, root_, pool, &qd);
   if (prof)
@@ -612,6 +616,26 @@ void Store::release(const PlanHost& p) {
     if (pins_[b] == 0 && meta_[b].resident) set_evictable(b, true);
   }
   for (int32_t b : p.priv) free_.insert(b);
+}
+
+void Store::abort(const PlanHost& p) {
+  release(p);
+  std::vector<uint8_t> priv(static_cast<size_t>(nblocks_), 0);
+  for (int32_t b : p.priv) priv[b] = 1;
+  for (size_t i = 0; i < p.blocks.size(); ++i) {
+    const int32_t b = p.blocks[i];
+    if (!p.block_write[i] || priv[b] || !meta_[b].resident) continue;
+    auto it = index_.find(p.digests[i]);
+    if (it != index_.end() && it->second == b && pins_[b] == 0) drop(b);
+  }
+}
+
+void Store::drop(int32_t b) {
+  if (!meta_[b].resident) return;
+  set_evictable(b, false);
+  index_.erase(meta_[b].dig);
+  meta_[b].resident = false;
+  free_.insert(b);
 }
 
 void Store::evict_all() {

@@ -117,6 +117,13 @@ class Store {
   int plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* pool = nullptr, int rank = 0,
            int world = 1);
   void release(const PlanHost& p);
+  // Undo a committed plan whose device side failed: release it and forget the blocks it inserted
+  // (their KV was never written, so their digests must not produce cache hits).
+  void abort(const PlanHost& p);
+  // Forget the digest held by block b (its content was rewritten in place): resident -> free.
+  // Pinned blocks are the caller's to exclude.
+  void drop(int32_t b);
+  bool is_pinned(int32_t b) const { return pins_[b] > 0; }
   void evict_all();
   int32_t lookup(const Digest& d) const;
   // Low-level insert: returns 0 or 2 (ENOMEM, rolled back).

@@ -40,11 +40,10 @@ void schedule(const std::vector<double>& item_cost, int units, int num_sms, Attn
                    [&](int32_t a, int32_t b) { return item_cost[a] > item_cost[b]; });
   const size_t codes = item_cost.size() * static_cast<size_t>(units);
   w->grid = static_cast<int>(std::min<size_t>(num_sms, std::max<size_t>(1, codes)));
-  static const bool static_sched = [] {
-    const char* e = std::getenv("SPANQ_SCHED");  // tuning knob: "static" = host snake lists
-    return e != nullptr && std::string(e) == "static";
-  }();
-  if (static_sched) {
+  // host-built static lists (boustrophedon waves) measured slower than run-time claims
+  // (0.296 vs 0.276 ms); kept for hosts that build lists without a counter
+  constexpr bool kStaticSched = false;
+  if (kStaticSched) {
     // boustrophedon waves (0..grid-1, grid-1..0, ...) over the sorted codes
     const int grid = w->grid;
     std::vector<int32_t> count(grid, 0), bin_of(codes);
@@ -73,16 +72,10 @@ void schedule(const std::vector<double>& item_cost, int units, int num_sms, Attn
 
 constexpr double kItemOverhead = 1.0;   // q-prep + epilogue, in KV-tile units
 constexpr double kSplitOverhead = 0.5;  // partial write + combine read, per split
-// per work item, in 64-key sub-tiles (epilogue + Q + pipeline fill; tuning knob SPANQ_SUB_OVERHEAD)
-const double kSubOverhead = [] {
-  const char* e = std::getenv("SPANQ_SUB_OVERHEAD");
-  return e ? std::atof(e) : 3.0;
-}();
-// per Q-rotation change inside a join piece, in sub-tiles (tuning knob SPANQ_EPOCH_COST)
-const double kEpochCost = [] {
-  const char* e = std::getenv("SPANQ_EPOCH_COST");
-  return e ? std::atof(e) : 1.5;
-}();
+// per work item, in 64-key sub-tiles (epilogue + Q + pipeline fill; measured)
+constexpr double kSubOverhead = 3.0;
+// per Q-rotation change inside a join piece, in sub-tiles
+constexpr double kEpochCost = 1.5;
 
 // Per-item sub-tile counts (the kernel's roles need them without walking the tiles).
 void count_subtiles(AttnWorkHost* w) {

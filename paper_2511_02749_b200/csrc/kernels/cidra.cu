@@ -10,13 +10,19 @@
 // Every element of a (block, layer, kv head) tile is touched by the same thread in every op of
 // its component (the same row t and columns in each block), so the in-place dependencies are
 // plain program order inside one thread — the "scratch block" of a cycle is a few registers.
-// CTA (component, layer x kv head); a thread owns rows t and a 16-byte unit u of the first half
-// of d plus its rotate-half partner unit in the second half (8 pairs for bf16, 4 for fp32):
-// 128-bit loads/stores, a warp covers whole rows contiguously. cos/sin of delta * theta_i come
-// from the ctx's fp64-built table at |delta| (sin negated for delta < 0).
+// CTA (component, layer x kv head, slice of rows); a thread owns rows t and a 16-byte unit u of
+// the first half of d plus its rotate-half partner unit in the second half (8 pairs for bf16, 4
+// for fp32): 128-bit loads/stores, a warp covers whole rows contiguously. Rows are split over
+// grid.z when components x layers x heads alone would not fill the GPU (one long cycle at L = 1
+// is 8 CTAs otherwise); small grids also load the next op's source while the current op is
+// rotated and stored (legal: the schedule reads every block before any op writes it — only the
+// scratch of mode 2 comes from an earlier op — so a thread's chain of ops is latency-bound, not
+// order-bound). cos/sin of delta * theta_i come from the ctx's fp64-built table at |delta| (sin
+// negated for delta < 0).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "launch.h"
@@ -60,10 +66,10 @@ struct V16<float> {
   }
 };
 
-template <typename T, int D>
+template <typename T, int D, bool AHEAD>
 __global__ void __launch_bounds__(256) cidra_kernel(const int4* __restrict__ ops, const int32_t* __restrict__ comp_off,
                                                     T* k_pool, T* v_pool, const float2* __restrict__ rope, int hkv,
-                                                    int bs, int64_t nblk, int layer0) {
+                                                    int bs, int64_t nblk, int layer0, int units_per_cta) {
   constexpr int N = V16<T>::N;
   constexpr int U = D / 2 / N;  // units per half row
   const int comp = blockIdx.x;
@@ -73,21 +79,38 @@ __global__ void __launch_bounds__(256) cidra_kernel(const int4* __restrict__ ops
   // element offset of (block b, this layer/head, row t, column c): ((layer*nblk + b)*hkv + h)*bs*D + t*D + c
   const int64_t lh = static_cast<int64_t>(layer) * nblk;
   auto tile = [&](int32_t b) { return ((lh + b) * hkv + h) * static_cast<int64_t>(bs) * D; };
-  for (int idx = threadIdx.x; idx < bs * U; idx += blockDim.x) {
+  const int i0 = static_cast<int>(blockIdx.z) * units_per_cta, i1 = min(bs * U, i0 + units_per_cta);
+  for (int idx = i0 + threadIdx.x; idx < i1; idx += blockDim.x) {
     const int t = idx / U, u = idx % U;
     const int c0 = t * D + u * N;  // first-half unit; partner at + D/2
     uint4 tk0 = make_uint4(0, 0, 0, 0), tk1 = tk0, tv0 = tk0, tv1 = tk0;  // the cycle's scratch
+    // AHEAD: the source units of op o are loaded during op o - 1
+    uint4 nk0 = tk0, nk1 = tk0, nv0 = tk0, nv1 = tk0;
+    auto load_src = [&](const int4& op, uint4& k0, uint4& k1, uint4& v0, uint4& v1) {
+      const int64_t s = tile(op.y) + c0;
+      k0 = *reinterpret_cast<const uint4*>(k_pool + s);
+      k1 = *reinterpret_cast<const uint4*>(k_pool + s + D / 2);
+      v0 = *reinterpret_cast<const uint4*>(v_pool + s);
+      v1 = *reinterpret_cast<const uint4*>(v_pool + s + D / 2);
+    };
+    int4 nop = o0 < o1 ? ops[o0] : make_int4(0, 0, 0, 2);
+    if (AHEAD && nop.w != 2) load_src(nop, nk0, nk1, nv0, nv1);
     for (int o = o0; o < o1; ++o) {
-      const int4 op = ops[o];  // {dst, src, delta, mode}
+      const int4 op = nop;  // {dst, src, delta, mode}
       uint4 k0, k1, v0, v1;
+      if (AHEAD) {
+        k0 = nk0, k1 = nk1, v0 = nv0, v1 = nv1;
+        if (o + 1 < o1) {
+          nop = ops[o + 1];
+          if (nop.w != 2) load_src(nop, nk0, nk1, nv0, nv1);
+        }
+      } else if (o + 1 < o1) {
+        nop = ops[o + 1];
+      }
       if (op.w == 2) {
         k0 = tk0, k1 = tk1, v0 = tv0, v1 = tv1;
       } else {
-        const int64_t s = tile(op.y) + c0;
-        k0 = *reinterpret_cast<const uint4*>(k_pool + s);
-        k1 = *reinterpret_cast<const uint4*>(k_pool + s + D / 2);
-        v0 = *reinterpret_cast<const uint4*>(v_pool + s);
-        v1 = *reinterpret_cast<const uint4*>(v_pool + s + D / 2);
+        if (!AHEAD) load_src(op, k0, k1, v0, v1);
         if (op.w == 1) {
           tk0 = k0, tk1 = k1, tv0 = v0, tv1 = v1;
           continue;
@@ -119,11 +142,26 @@ __global__ void __launch_bounds__(256) cidra_kernel(const int4* __restrict__ ops
 
 template <typename T, int D>
 cudaError_t launch_t(const CidraArgs& a, cudaStream_t st) {
-  const dim3 grid(static_cast<unsigned>(a.n_comp), static_cast<unsigned>((a.layer_end - a.layer_begin) * a.hkv));
+  const int64_t tiles = static_cast<int64_t>(a.n_comp) * (a.layer_end - a.layer_begin) * a.hkv;
   const int units = a.bs * (D / 2 / V16<T>::N);
-  const int threads = units >= 256 ? 256 : ((units + 31) / 32) * 32;
-  cidra_kernel<T, D><<<grid, threads, 0, st>>>(a.ops, a.comp_off, static_cast<T*>(a.k_pool), static_cast<T*>(a.v_pool),
-                                               a.rope, a.hkv, a.bs, a.nblk, a.layer_begin);
+  // rows split over grid.z until the grid holds ~2 CTAs per SM (slices of >= 64 units)
+  const int64_t want = 2LL * (a.num_sms > 0 ? a.num_sms : 148);
+  int splits = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (want + tiles - 1) / tiles), std::max(1, units / 64)));
+  const int per = ((units + splits - 1) / splits + 31) / 32 * 32;
+  splits = (units + per - 1) / per;
+  const dim3 grid(static_cast<unsigned>(a.n_comp), static_cast<unsigned>((a.layer_end - a.layer_begin) * a.hkv),
+                  static_cast<unsigned>(splits));
+  const int threads = per >= 256 ? 256 : per;
+  // small grids are latency-bound on each thread's chain of ops: load one op ahead there (with
+  // 40 layers of work the look-ahead measured slower: 1.22 vs 1.11 ms)
+  if (tiles < want)
+    cidra_kernel<T, D, true><<<grid, threads, 0, st>>>(a.ops, a.comp_off, static_cast<T*>(a.k_pool),
+                                                       static_cast<T*>(a.v_pool), a.rope, a.hkv, a.bs, a.nblk,
+                                                       a.layer_begin, per);
+  else
+    cidra_kernel<T, D, false><<<grid, threads, 0, st>>>(a.ops, a.comp_off, static_cast<T*>(a.k_pool),
+                                                        static_cast<T*>(a.v_pool), a.rope, a.hkv, a.bs, a.nblk,
+                                                        a.layer_begin, per);
   return cudaGetLastError();
 }
 

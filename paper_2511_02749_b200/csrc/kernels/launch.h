@@ -62,9 +62,10 @@ struct AttnArgs {
   bool paired;    // tcgen05 path: work codes are (item, GQA head pair) — see span_attn_tc.cu
   bool join;      // tcgen05 path: a join launch (2-deep Q ring, epilogue staged in Q slots)
   bool pdl;       // tcgen05 path: launch as a programmatic dependent of the preceding K1
-  int poly_mask;  // tcgen05 path: share of exp2 on the FMA pipe, in quarters (0..4)
+  int poly_mask;  // tcgen05 path: exp2 on MUFU: 0 = ex2 fp32, else ex2.f16x2 (SPQ_OPT_EXP2)
   float rescale_threshold;  // tcgen05 path: conditional O rescale threshold (log2 units, 8)
-  long long* dbg_trace;     // profiling only: CTA-0 event timeline (null = off)
+  long long* dbg_trace;     // profiling builds only: CTA-0 event timeline (null = off)
+  int dbg_mode;             // profiling builds only: timing variants (0 = off)
 };
 cudaError_t launch_span_attn_tc(const AttnArgs& a, cudaStream_t st);   // bf16 tcgen05
 cudaError_t launch_span_attn_f32(const AttnArgs& a, cudaStream_t st);  // fp32 SIMT
@@ -106,6 +107,7 @@ struct CidraArgs {
   int64_t nblk;
   int layer_begin, layer_end;
   bool fp32;
+  int num_sms;
 };
 cudaError_t launch_cidra(const CidraArgs& a, cudaStream_t st);  // in-place repositioning (K8)
 

@@ -103,7 +103,7 @@ struct TcParams {
   int qprep_mode;  // Q prep: bit 0 = issue head B's load early, bit 1 = L2-prefetch the next item's q
   int join;        // 1: 2-deep Q ring per head in the staging area, epilogue staged in Q slots
   int epi_q;       // 1 (prefill launches): the epilogue runs on the Q-prep warps (prefill_epilogue)
-  int dbg_mode;  // profiling only: 1 = softmax does no math, 2 = max pass only,
+  int dbg_mode;  // profiling builds only: 1 = softmax does no math, 2 = max pass only,
                  // 3 = 1 + K/V always from the first block (L2-resident), 4 = 1 + MMA skips K/V waits,
                  // 5 = 1 + Q prep does no work
 };
@@ -135,12 +135,23 @@ __device__ __forceinline__ uint8_t* q_tile(TcSmem<D>& S, bool J, int x, uint32_t
 // profiling only: CTA 0 records (event, clock) pairs per warp (lane 0 / the elected thread);
 // 1024 events per warp
 constexpr int kTraceWarps = 16;
+// (profiling builds only: -DSPANQ_PROFILING, tools/; compiled out of the product library)
 __device__ __forceinline__ void trace(const TcParams& P, int, uint32_t& cnt, int ev) {
+#ifdef SPANQ_PROFILING
   if (P.a.dbg_trace == nullptr || blockIdx.x != 0 || cnt >= 1024) return;
   long long* t = P.a.dbg_trace + ((threadIdx.x / 32) * 1024 + cnt) * 2;
   t[0] = ev;
   t[1] = clock64();
   ++cnt;
+#endif
+}
+// profiling builds: timing variants of the kernel (spq_set_trace); 0 in the product library
+__device__ __forceinline__ int dbg_mode(const TcParams& P) {
+#ifdef SPANQ_PROFILING
+  return P.dbg_mode;
+#else
+  return 0;
+#endif
 }
 
 struct Unit {
@@ -269,7 +280,7 @@ __device__ void run_producer(const TcParams& P, TcSmem<D>& S, int it_begin, int 
         for (int j = 0; j < bps; ++j) {
           // key 64h + j*box of the tile: block (64h + j*box) / bs, row offset (64h + j*box) % bs
           const int key = 64 * h + j * box;
-          const int32_t blk = P.dbg_mode == 3 ? a.tile_blocks[0] : a.tile_blocks[tl.blk_off + key / a.bs];
+          const int32_t blk = dbg_mode(P) == 3 ? a.tile_blocks[0] : a.tile_blocks[tl.blk_off + key / a.bs];
           const int32_t y = static_cast<int32_t>(layer_rows + (static_cast<int64_t>(blk) * a.hkv + kvh) * a.bs +
                                                  key % a.bs);
 #pragma unroll
@@ -731,7 +742,7 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
         float alpha;
         bool resc;
         float sum;
-        if (P.dbg_mode == 1) {  // profiling only: no softmax work (timing of the other roles)
+        if (dbg_mode(P) == 1) {  // profiling only: no softmax work (timing of the other roles)
           alpha = 1.f;
           resc = false;
           sum = 1.f;
@@ -919,7 +930,7 @@ __device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_
     const WorkItem& w = u.w;
     const int my_row = wq * 32 + lane;  // this lane's row position, shuffled to the warp per row
     const int my_pos = my_row < w.n_rows ? a.pos[static_cast<int64_t>(w.row0) + my_row] : 0;
-    const bool work = P.dbg_mode != 5;
+    const bool work = dbg_mode(P) != 5;
     for (int t = w.tile_begin; t < w.tile_end; ++t) {
       const int rot = a.tiles[t].rot_delta;
       if (t > w.tile_begin && rot == a.tiles[t - 1].rot_delta) continue;
@@ -1100,11 +1111,13 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
   const uint32_t tmem = S.tmem_base;
   const bool dyn = P.a.sched != nullptr;
   const int it_begin = dyn ? 0 : P.a.cta_off[blockIdx.x], it_end = dyn ? 0 : P.a.cta_off[blockIdx.x + 1];
+#ifdef SPANQ_PROFILING
   if (P.a.dbg_trace != nullptr && threadIdx.x == 0) {  // profiling only: per-CTA start (ns)
     uint64_t g;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
     P.a.dbg_trace[kTraceWarps * 2048 + 2 * blockIdx.x] = static_cast<long long>(g);
   }
+#endif
   // register budget 65536 >= 128 x (56 + 160 + 160 + 120): TMA/MMA warps need few
   if (warp < 4) {
     reg_dealloc<56>();
@@ -1136,11 +1149,13 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
       __threadfence();
     }
   }
+#ifdef SPANQ_PROFILING
   if (P.a.dbg_trace != nullptr && threadIdx.x == 0) {  // profiling only: per-CTA end (ns)
     uint64_t g;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
     P.a.dbg_trace[kTraceWarps * 2048 + 2 * blockIdx.x + 1] = static_cast<long long>(g);
   }
+#endif
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
@@ -1173,15 +1188,14 @@ cudaError_t launch_dp(const AttnArgs& a, cudaStream_t st) {
   p.paired = a.paired ? 1 : 0;
   p.poly_mask = PM;
   p.rescale_threshold = a.rescale_threshold;
-  p.dbg_mode = getenv("SPANQ_DBG_MODE") ? atoi(getenv("SPANQ_DBG_MODE")) : 0;
+  p.dbg_mode = a.dbg_mode;
   p.qprep_mode = 3;
   // joins of paired launches: 2-deep Q ring per head in the staging area
   p.join = a.paired && a.join ? 1 : 0;
   p.epi_q = EPI ? 1 : 0;
   // launched as a programmatic dependent of the preceding K1 when the caller says it directly
-  // precedes (a.pdl; knob SPANQ_PDL=0 turns it off): the prologue and Q preparation overlap
-  // K1's tail (see run_producer)
-  static const bool pdl = getenv("SPANQ_PDL") == nullptr || atoi(getenv("SPANQ_PDL")) != 0;
+  // precedes (a.pdl; the ctx option SPQ_OPT_PDL = 0 turns it off): the prologue and Q
+  // preparation overlap K1's tail (see run_producer)
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(a.grid));
   cfg.blockDim = dim3(kThreads);
@@ -1191,7 +1205,7 @@ cudaError_t launch_dp(const AttnArgs& a, cudaStream_t st) {
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl && a.pdl ? 1 : 0;
+  cfg.numAttrs = a.pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, span_attn_tc_kernel<D, PM, EPI>, p);
 }
 

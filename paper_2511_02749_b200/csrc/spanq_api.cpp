@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <deque>
 #include <map>
 #include <unordered_set>
 #include <chrono>
@@ -98,7 +99,19 @@ struct spq_ctx {
   uint8_t* staging = nullptr;
   size_t staging_size = 0;
   cudaEvent_t staging_ev = nullptr;
+  // options (spq_set_option)
+  int exp2_mode = 0;               // SPQ_OPT_EXP2
+  float rescale_threshold = 8.0f;  // SPQ_OPT_RESCALE_THRESHOLD (log2 units)
+  bool pdl = true;                 // SPQ_OPT_PDL
+  // profiling builds only (spq_set_trace)
+  long long* trace = nullptr;
+  int dbg_mode = 0;
+  // plan handles: live plans, and released ones kept (emptied) for kQuarantine more releases so
+  // that a call on a released handle reports SPQ_ESTATE instead of touching freed memory
+  std::unordered_set<spq_plan*> live;
+  std::deque<spq_plan*> quarantine;
 };
+constexpr size_t kQuarantine = 1024;
 
 struct spq_plan {
   spq::PlanHost host;
@@ -134,11 +147,6 @@ bool paired(const spq_ctx* c) {
 // heads per attention work unit (a split-KV partial slot holds one unit's heads)
 int heads_per_unit(const spq_ctx* c) { return paired(c) ? 2 : 1; }
 
-int poly_mask() {
-  const char* e = std::getenv("SPANQ_POLY_EXP");  // tuning knob: quarters of exp2 on the FMA pipe
-  return e ? std::max(0, std::min(3, std::atoi(e))) : 0;
-}
-
 // host-only contexts plan for a B200 (148 SMs) so their work lists match a GPU ctx's
 spq::WorkOpts work_opts(const spq_ctx* c, bool allow_split) {
   spq::WorkOpts o{};
@@ -153,12 +161,6 @@ spq::WorkOpts work_opts(const spq_ctx* c, bool allow_split) {
 }
 
 int elt_size(const spq_ctx* c) { return c->cfg.dtype == SPQ_FP32 ? 4 : 2; }
-
-// programmatic dependent launches (knob SPANQ_PDL=0 turns them off, for A/B)
-bool pdl_enabled() {
-  static const bool on = std::getenv("SPANQ_PDL") == nullptr || std::atoi(std::getenv("SPANQ_PDL")) != 0;
-  return on;
-}
 
 spq_status make_tmap(spq_ctx* c, void* pool, CUtensorMap* out) {
   void* fn = nullptr;
@@ -290,13 +292,10 @@ void fill_attn(spq_ctx* c, const spq_plan* p, const DevWork& w, spq::AttnArgs* a
   a->lsepart = p->lsepart;
   a->out_fp32 = c->cfg.out_dtype == SPQ_FP32;
   a->paired = paired(c);
-  a->poly_mask = poly_mask();
-  // tuning/test knob: 0 rescales O on every tile (exercises the rescale path); default 8 (log2)
-  const char* th = std::getenv("SPANQ_RESCALE_THRESHOLD");
-  a->rescale_threshold = th ? static_cast<float>(std::atof(th)) : 8.0f;
-  // profiling only: SPANQ_TRACE=<device address> (from the binding) enables the CTA-0 timeline
-  const char* tr = std::getenv("SPANQ_TRACE");
-  a->dbg_trace = tr ? reinterpret_cast<long long*>(std::strtoull(tr, nullptr, 10)) : nullptr;
+  a->poly_mask = c->exp2_mode;
+  a->rescale_threshold = c->rescale_threshold;
+  a->dbg_trace = c->trace;  // null unless a profiling build set it (spq_set_trace)
+  a->dbg_mode = c->dbg_mode;
 }
 
 spq_status run_attn(spq_ctx* c, const spq::AttnArgs& a, cudaStream_t st) {
@@ -339,8 +338,8 @@ spq_status kv_write(spq_ctx* c, spq_plan* p, int32_t layer, const void* k, const
 
 spq_status check_call(spq_ctx* c, spq_plan* p, int32_t layer) {
   if (c == nullptr || p == nullptr) return fail(SPQ_EINVAL, "null ctx/plan");
+  if (!c->live.count(p)) return fail(SPQ_ESTATE, "plan used after release (or not a plan of this ctx)");
   if (!is_gpu(c)) return fail(SPQ_ESTATE, "host-only ctx (device < 0) cannot run kernels");
-  if (p->released) return fail(SPQ_ESTATE, "plan used after release");
   if (layer < 0 || layer >= c->cfg.num_layers) return fail(SPQ_ESTATE, "layer out of range");
   return SPQ_OK;
 }
@@ -461,6 +460,11 @@ void spq_destroy(spq_ctx* c) {
     if (c->staging) cudaFreeHost(c->staging);
     if (c->rope) cudaFree(c->rope);
   }
+  for (spq_plan* p : c->live) {  // plans never released: their device arrays go with the ctx
+    if (p->dbuf) cudaFree(p->dbuf);
+    delete p;
+  }
+  for (spq_plan* p : c->quarantine) delete p;
   delete c;
 }
 
@@ -519,7 +523,11 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
   if (c == nullptr || out == nullptr || (n_queries > 0 && queries == nullptr)) return fail(SPQ_EINVAL, "null argument");
   if (n_queries <= 0) return fail(SPQ_EINVAL, "n_queries must be >= 1");
   using clk = std::chrono::steady_clock;
-  static const bool prof = std::getenv("SPANQ_PROFILE") != nullptr;
+#ifdef SPANQ_PROFILING
+  static const bool prof = std::getenv("SPANQ_PROFILE") != nullptr;  // profiling builds only
+#else
+  constexpr bool prof = false;
+#endif
   auto t0 = clk::now();
   auto lap = [&](const char* what) {
     if (!prof) return;
@@ -541,6 +549,17 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
   lap("normalize");
   std::unique_ptr<spq_plan> p(new spq_plan());
   if (c->store->plan(fq, &p->host, c->pool.get(), c->cfg.rank, c->cfg.world_size) != 0) return fail(SPQ_ENOMEM, "block pool cannot hold the plan (rolled back)");
+  // from here on the store holds the plan's pins and inserted digests: any failure undoes them
+  struct Guard {
+    spq_ctx* c;
+    spq_plan* p;
+    bool armed = true;
+    ~Guard() {
+      if (!armed) return;
+      c->store->abort(p->host);
+      if (p->dbuf) cudaFree(p->dbuf);
+    }
+  } guard{c, p.get()};
   lap("store.plan");
   const spq::PlanHost& H = p->host;
   for (const spq::Segment& s : H.segs) {
@@ -687,6 +706,8 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
     }
     lap("upload");
   }
+  guard.armed = false;
+  c->live.insert(p.get());
   *out = p.release();
   return SPQ_OK;
 }
@@ -777,7 +798,7 @@ spq_status spq_prefill_jobs(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, i
   args.layer = layer;
   // programmatic dependent launch only right behind our own K1 (nothing else in between on the
   // stream: no work-list upload, no timing event) — then every input but the pool is complete
-  args.pdl = k1 && full && !c->timing;
+  args.pdl = k1 && full && !c->timing && c->pdl;
   CUtensorMap qmap, omap;
   if (c->cfg.dtype == SPQ_BF16) {
     s = make_qmap(c, q, r1 - r0, &qmap);
@@ -853,7 +874,7 @@ spq_status join_impl(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t 
   args.lsepart = lsepart;
   args.pos = at<int32_t>(p, p->off_jpos) + r0;
   args.join = true;
-  args.pdl = k1 && (full || mode >= 0) && !c->timing;  // see spq_prefill_jobs
+  args.pdl = k1 && (full || mode >= 0) && !c->timing && c->pdl;  // see spq_prefill_jobs
   args.q = q;
   args.o = o;
   args.lse = lse;
@@ -894,7 +915,7 @@ spq_status join_impl(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t 
     ca.d = c->cfg.head_dim;
     ca.out_fp32 = c->cfg.out_dtype == SPQ_FP32;
     // the join kernel is the preceding stream operation unless a timing event sits between
-    ca.pdl = !c->timing && c->cfg.dtype == SPQ_BF16 && pdl_enabled();
+    ca.pdl = !c->timing && c->cfg.dtype == SPQ_BF16 && c->pdl;
     cudaError_t e = spq::launch_combine(ca, st);
     if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("combine launch: ") + cudaGetErrorString(e));
     c->launches++;
@@ -965,9 +986,7 @@ spq_status spq_exchange_unpack(spq_ctx* c, spq_plan* p, int32_t layer, int32_t p
 
 spq_status spq_plan_release(spq_ctx* c, spq_plan* p, void* stream) {
   if (c == nullptr || p == nullptr) return fail(SPQ_EINVAL, "null argument");
-  if (p->released) return fail(SPQ_ESTATE, "plan released twice");
-  c->store->release(p->host);
-  p->released = true;
+  if (!c->live.count(p)) return fail(SPQ_ESTATE, "plan released twice (or not a plan of this ctx)");
   if (is_gpu(c)) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     CUDA_TRY(cudaSetDevice(c->cfg.device));
@@ -977,8 +996,18 @@ spq_status spq_plan_release(spq_ctx* c, spq_plan* p, void* stream) {
     c->pending.push_back(e);
     if (p->dbuf) CUDA_TRY(cudaFreeAsync(p->dbuf, st));
     // opart / lsepart live inside dbuf
+    p->dbuf = nullptr;
   }
-  delete p;
+  c->store->release(p->host);
+  c->live.erase(p);
+  // keep the (emptied) object for a while: a later call on this handle reports SPQ_ESTATE
+  *p = spq_plan();
+  p->released = true;
+  c->quarantine.push_back(p);
+  if (c->quarantine.size() > kQuarantine) {
+    delete c->quarantine.front();
+    c->quarantine.pop_front();
+  }
   return SPQ_OK;
 }
 
@@ -1080,6 +1109,11 @@ spq_status spq_reposition(spq_ctx* c, const int32_t* src, const int32_t* dst, co
   if (n_comp == 0 || layer_begin == layer_end) return SPQ_OK;
   if (n_comp > INT32_MAX || static_cast<int64_t>(layer_end - layer_begin) * c->cfg.num_kv_heads > 65535)
     return fail(SPQ_EINVAL, "too many components or layers x kv heads for one launch");
+  // blocks a live plan reads or writes must not move under it
+  for (int64_t i = 0; i < n; ++i)
+    if (c->store->is_pinned(src[i]) || c->store->is_pinned(dst[i]))
+      return fail(SPQ_ESTATE, "block " + std::to_string(c->store->is_pinned(src[i]) ? src[i] : dst[i]) +
+                                  " is pinned by a live plan");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   CUDA_TRY(cudaSetDevice(c->cfg.device));
   s = wait_pending(c, st);
@@ -1104,11 +1138,50 @@ spq_status spq_reposition(spq_ctx* c, const int32_t* src, const int32_t* dst, co
   a.layer_begin = layer_begin;
   a.layer_end = layer_end;
   a.fp32 = c->cfg.dtype == SPQ_FP32;
+  a.num_sms = c->num_sms;
   cudaError_t e = spq::launch_cidra(a, st);
   if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("cidra launch: ") + cudaGetErrorString(e));
   c->launches++;
   CUDA_TRY(cudaFreeAsync(buf, st));
+  // a destination now holds other KV than its digest names: the store forgets it (no later plan
+  // may hit it); the caller owns the moved content from here on
+  for (int64_t i = 0; i < n; ++i) c->store->drop(dst[i]);
   return SPQ_OK;
+}
+
+spq_status spq_set_option(spq_ctx* c, int32_t key, double value) {
+  if (c == nullptr) return fail(SPQ_EINVAL, "null argument");
+  switch (key) {
+    case SPQ_OPT_EXP2:
+      if (value != 0 && value != 1) return fail(SPQ_EINVAL, "SPQ_OPT_EXP2 must be 0 or 1");
+      c->exp2_mode = value != 0 ? 3 : 0;
+      return SPQ_OK;
+    case SPQ_OPT_RESCALE_THRESHOLD:
+      if (!(value >= 0 && value <= 64)) return fail(SPQ_EINVAL, "SPQ_OPT_RESCALE_THRESHOLD must be in [0, 64]");
+      c->rescale_threshold = static_cast<float>(value);
+      return SPQ_OK;
+    case SPQ_OPT_PDL:
+      c->pdl = value != 0;
+      return SPQ_OK;
+    case SPQ_OPT_HASH_SCALAR:
+      spq::blake2b_force_scalar(value != 0);
+      return SPQ_OK;
+    default:
+      return fail(SPQ_EINVAL, "unknown option " + std::to_string(key));
+  }
+}
+
+spq_status spq_set_trace(spq_ctx* c, void* buf, int32_t mode) {
+  if (c == nullptr) return fail(SPQ_EINVAL, "null argument");
+#ifdef SPANQ_PROFILING
+  c->trace = static_cast<long long*>(buf);
+  c->dbg_mode = mode;
+  return SPQ_OK;
+#else
+  (void)buf;
+  (void)mode;
+  return fail(SPQ_EINVAL, "tracing needs a profiling build (build.py --profiling)");
+#endif
 }
 
 spq_status spq_launch_count(const spq_ctx* c, int64_t* n) {

@@ -111,3 +111,15 @@ def run_pass(ctx: spanq.Context, queries: Sequence[inputs.SpanQuery], tabs: Sequ
     if release:
         plan.release(stream=stream)
     return PassResult(plan, view, op, lp, oj, lj)
+
+
+def random_tables(shape: inputs.Shape, seed: int, device) -> DeviceTables:
+    """Bench-only stand-in tables drawn on the device (torch's CUDA generator, N(0,1) rounded to
+    the ctx dtype): per-layer inputs for many layers without the host-side draws of
+    inputs.layer_tables (which the parity tests and the oracle use)."""
+    torch = _torch()
+    dt = torch.bfloat16 if shape.dtype == "bf16" else torch.float32
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+    mk = lambda h: torch.randn((shape.vocab, h, shape.d), generator=g, device=device, dtype=torch.float32).to(dt)
+    return DeviceTables(mk(shape.hq), mk(shape.hkv), mk(shape.hkv))

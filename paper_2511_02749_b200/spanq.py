@@ -21,6 +21,8 @@ _lib = None
 
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, ESTATE = range(6)
 BF16, FP32 = 0, 1
+# spq_option keys (include/spanq.h)
+OPT_EXP2, OPT_RESCALE_THRESHOLD, OPT_PDL, OPT_HASH_SCALAR = 1, 2, 3, 4
 
 
 class SpanqError(RuntimeError):
@@ -121,6 +123,8 @@ SIGNATURES = {
     "spq_launch_count": (C.c_int, [C.c_void_p, _I64P]),
     "spq_last_attn_ms": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "spq_set_timing": (C.c_int, [C.c_void_p, C.c_int32]),
+    "spq_set_option": (C.c_int, [C.c_void_p, C.c_int32, C.c_double]),
+    "spq_set_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
 }
 
 
@@ -155,9 +159,16 @@ def _ptr(x) -> Optional[int]:
     return x.ctypes.data
 
 
-def _stream_ptr(stream) -> Optional[int]:
+def _stream_ptr(stream, device: int = -1) -> Optional[int]:
+    """Stream handle for the ABI. None means torch's current stream of the ctx's device (so the
+    kernels are ordered after the torch work that produced their inputs), never the legacy
+    default stream; host-only contexts pass NULL."""
     if stream is None:
-        return None
+        if device < 0:
+            return None
+        import torch
+
+        return torch.cuda.current_stream(device).cuda_stream
     if hasattr(stream, "cuda_stream"):
         return stream.cuda_stream
     return int(stream)
@@ -240,31 +251,31 @@ class Plan:
     def exchange_pack(self, layer, peer, buf, stream=None):
         """Gather this plan's send blocks for `peer` (one layer) into buf [n, 2, Hkv, bs, d]."""
         _check(lib().spq_exchange_pack(self.ctx.handle, self.handle, layer, peer, _ptr(buf),
-                                       _stream_ptr(stream)))
+                                       _stream_ptr(stream, self.ctx.device)))
 
     def exchange_unpack(self, layer, peer, buf, stream=None):
         """Scatter buf [n, 2, Hkv, bs, d] into this plan's recv blocks from `peer` (one layer)."""
         _check(lib().spq_exchange_unpack(self.ctx.handle, self.handle, layer, peer, _ptr(buf),
-                                         _stream_ptr(stream)))
+                                         _stream_ptr(stream, self.ctx.device)))
 
     def prefill(self, layer, q, k, v, o, lse=None, jobs=None, stream=None):
         a, b = (0, self.n_jobs) if jobs is None else jobs
         _check(lib().spq_prefill_jobs(self.ctx.handle, self.handle, layer, a, b, _ptr(q), _ptr(k),
-                                      _ptr(v), _ptr(o), _ptr(lse), _stream_ptr(stream)))
+                                      _ptr(v), _ptr(o), _ptr(lse), _stream_ptr(stream, self.ctx.device)))
 
     def join(self, layer, q, k, v, o, lse=None, queries=None, stream=None):
         a, b = (0, self.n_queries) if queries is None else queries
         _check(lib().spq_join(self.ctx.handle, self.handle, layer, a, b, _ptr(q), _ptr(k), _ptr(v),
-                              _ptr(o), _ptr(lse), _stream_ptr(stream)))
+                              _ptr(o), _ptr(lse), _stream_ptr(stream, self.ctx.device)))
 
     def join_phase(self, layer, phase, q, k, v, o, lse=None, stream=None):
         """Phase 0 / 1 of the join of all home queries (W > 1: around the fragment-KV exchange)."""
         _check(lib().spq_join_phase(self.ctx.handle, self.handle, layer, phase, _ptr(q), _ptr(k), _ptr(v),
-                                    _ptr(o), _ptr(lse), _stream_ptr(stream)))
+                                    _ptr(o), _ptr(lse), _stream_ptr(stream, self.ctx.device)))
 
     def release(self, stream=None):
         if not self.released:
-            _check(lib().spq_plan_release(self.ctx.handle, self.handle, _stream_ptr(stream)))
+            _check(lib().spq_plan_release(self.ctx.handle, self.handle, _stream_ptr(stream, self.ctx.device)))
             self.released = True
 
 
@@ -318,7 +329,7 @@ class Context:
         bufs = [to_query(q) for q in queries]
         arr = (spq_query * len(bufs))(*[b.q for b in bufs])
         h = C.c_void_p()
-        _check(lib().spq_plan_create(self.handle, arr, len(bufs), _stream_ptr(stream), C.byref(h)))
+        _check(lib().spq_plan_create(self.handle, arr, len(bufs), _stream_ptr(stream, self.device), C.byref(h)))
         return Plan(self, h.value)
 
     def block_hashes(self, query) -> np.ndarray:
@@ -352,7 +363,7 @@ class Context:
         k = torch.empty((len(ids), s.hkv, s.block_size, s.d), dtype=dt, device=f"cuda:{self.device}")
         v = torch.empty_like(k)
         _check(lib().spq_read_blocks(self.handle, layer, ids.ctypes.data, len(ids), _ptr(k), _ptr(v),
-                                     _stream_ptr(stream)))
+                                     _stream_ptr(stream, self.device)))
         return k, v
 
     @staticmethod
@@ -369,7 +380,7 @@ class Context:
         lb, le = layers if layers is not None else (0, self.shape.layers)
         st = spq_cidra_stats()
         _check(lib().spq_reposition(self.handle, s_.ctypes.data, d_.ctypes.data, dl.ctypes.data, len(s_), lb, le,
-                                    _stream_ptr(stream), C.byref(st)))
+                                    _stream_ptr(stream, self.device), C.byref(st)))
         return {n: getattr(st, n) for n, _ in spq_cidra_stats._fields_}
 
     def cidra_schedule(self, src, dst, delta):
@@ -394,6 +405,14 @@ class Context:
 
     def evict_all(self):
         _check(lib().spq_evict_all(self.handle))
+
+    def set_option(self, key: int, value: float):
+        """spq_set_option (OPT_EXP2, OPT_RESCALE_THRESHOLD, OPT_PDL, OPT_HASH_SCALAR)."""
+        _check(lib().spq_set_option(self.handle, int(key), float(value)))
+
+    def set_trace(self, buf, mode: int = 0):
+        """Profiling builds only (SPANQ_LIB=.../libspanq_prof.so): CTA-0 timeline buffer + mode."""
+        _check(lib().spq_set_trace(self.handle, _ptr(buf), int(mode)))
 
     def launch_count(self) -> int:
         n = C.c_int64()

@@ -39,6 +39,43 @@ def test_no_gpu_calls_fail_loudly_on_host_only_ctx():
     p.release()
 
 
+def test_released_plan_handle_reports_estate():
+    # spq_plan_release keeps the emptied handle reserved: later calls return SPQ_ESTATE instead
+    # of touching freed memory (spanq.h), and the store has no pins left
+    import ctypes as C
+
+    ctx = spanq.Context(inputs.Shape(hq=2, hkv=1, d=64, block_size=16, dtype="fp32"), 64, device=-1)
+    p = ctx.plan([inputs.c1().queries[0]])
+    assert ctx.stats()["pinned_blocks"] > 0
+    h = p.handle
+    p.release()
+    assert ctx.stats()["pinned_blocks"] == 0
+    L = spanq.lib()
+    assert L.spq_plan_view_get(h, C.byref(spanq.spq_plan_view())) == spanq.ESTATE
+    assert L.spq_plan_release(ctx.handle, h, None) == spanq.ESTATE
+    assert L.spq_join_phase(ctx.handle, h, 0, 1, None, None, None, None, None, None) == spanq.ESTATE
+    assert b"after release" in L.spq_last_error()
+    # many plans later (inside the 1024-release window) the first handle is still reported
+    for _ in range(50):
+        ctx.plan([inputs.c1().queries[0]]).release()
+    assert L.spq_plan_release(ctx.handle, h, None) == spanq.ESTATE
+
+
+def test_options_validate():
+    ctx = spanq.Context(inputs.Shape(hq=2, hkv=1, d=64, block_size=16), 64, device=-1)
+    for key, value in [(spanq.OPT_EXP2, 0), (spanq.OPT_EXP2, 1), (spanq.OPT_RESCALE_THRESHOLD, 0),
+                       (spanq.OPT_RESCALE_THRESHOLD, 8), (spanq.OPT_PDL, 0), (spanq.OPT_PDL, 1)]:
+        ctx.set_option(key, value)
+    for key, value in [(spanq.OPT_EXP2, 2), (spanq.OPT_RESCALE_THRESHOLD, -1), (99, 0)]:
+        with pytest.raises(spanq.SpanqError) as e:
+            ctx.set_option(key, value)
+        assert e.value.status == spanq.EINVAL
+    # the product library has no tracing (only the profiling build, tools/)
+    with pytest.raises(spanq.SpanqError) as e:
+        ctx.set_trace(None, 1)
+    assert e.value.status == spanq.EINVAL
+
+
 def oracle_arrays(view):
     segs = view.segments
     return dict(
@@ -205,29 +242,20 @@ def test_paper_configs_plan_bit_exact(cfg):
 
 @pytest.mark.parametrize("scalar", [False, True])
 def test_block_hashes_both_blake2b_paths(scalar):
-    # the library picks an AVX2 BLAKE2b compression at load time when the CPU has it; the scalar
-    # RFC 7693 path must give the same digests (fresh process: the choice is made once)
-    import subprocess
-    import sys
-
-    code = (
-        "import numpy as np, sys; sys.path.insert(0, %r)\n"
-        "from paper_2511_02749_b200 import inputs, spanq\n"
-        "from oracle import hashing\n"
-        "from oracle.store import Store\n"
-        "sh = inputs.Shape(hq=32, hkv=8, d=128, block_size=64)\n"
-        "ctx = spanq.Context(sh, 64, device=-1)\n"
-        "q = inputs.SpanQuery(np.arange(300, dtype=np.int32), [np.arange(200, dtype=np.int32) * 7], "
-        "np.arange(70, dtype=np.int32) + 5, nest=False)\n"
-        "d = [bytes(r) for r in ctx.block_hashes(q)]\n"
-        "root = Store(64, 32, 8, 128, 64).root\n"
-        "h = hashing.prefix_chain(q.prefix, 64, root); s = hashing.fragment_chain(q.fragments[0], 64, root)\n"
-        "J = hashing.join_fold(h[-1], [s[-1]])\n"
-        "assert d == h + s + [J] + hashing.cross_chain(q.cross, 64, J)\n"
-        "print('ok')\n" % ROOT)
-    env = dict(os.environ)
-    env.pop("SPANQ_BLAKE2B_SCALAR", None)
-    if scalar:
-        env["SPANQ_BLAKE2B_SCALAR"] = "1"
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, cwd=ROOT)
-    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stderr
+    # the library uses an AVX2 BLAKE2b compression when the CPU has it; the scalar RFC 7693 path
+    # (SPQ_OPT_HASH_SCALAR, process-wide — set before the ctx computes its root digest) must give
+    # the same digests
+    sh = inputs.Shape(hq=32, hkv=8, d=128, block_size=64)
+    spanq.Context(sh, 64, device=-1).set_option(spanq.OPT_HASH_SCALAR, 1 if scalar else 0)
+    try:
+        ctx = spanq.Context(sh, 64, device=-1)
+        q = inputs.SpanQuery(np.arange(300, dtype=np.int32), [np.arange(200, dtype=np.int32) * 7],
+                             np.arange(70, dtype=np.int32) + 5, nest=False)
+        d = [bytes(r) for r in ctx.block_hashes(q)]
+        root = Store(64, 32, 8, 128, 64).root
+        h = hashing.prefix_chain(q.prefix, 64, root)
+        s = hashing.fragment_chain(q.fragments[0], 64, root)
+        J = hashing.join_fold(h[-1], [s[-1]])
+        assert d == h + s + [J] + hashing.cross_chain(q.cross, 64, J)
+    finally:
+        spanq.Context(sh, 64, device=-1).set_option(spanq.OPT_HASH_SCALAR, 0)

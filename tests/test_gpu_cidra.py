@@ -84,3 +84,26 @@ def test_layer_range_and_launches():
     assert torch.equal(ctx.v_pool, v0)
     assert (ctx.k_pool.float() - k0.float()).abs().max().item() <= 2 ** -7 * k0.float().abs().max().item()
     ctx.close()
+
+
+def test_reposition_store_effects():
+    # moved-into blocks leave the content-hash index (they no longer hold what their digest
+    # names), and blocks pinned by a live plan refuse to move (SPQ_ESTATE, nothing moved)
+    shape = inputs.Shape(hq=8, hkv=2, d=128, block_size=64, vocab=512)
+    ctx = spanq.Context(shape, 64, device=0, max_position=1 << 14)
+    q = inputs.make_rag(5, shape, 0, 2, [128, 128], 64).queries[0]
+    plan = ctx.plan([q])
+    view = plan.view()
+    frag_blocks = [int(b) for b in view["blocks"][view["seg_block_off"][0]:][:2]]
+    digests = view["digests"][:2]
+    with pytest.raises(spanq.SpanqError) as e:
+        ctx.reposition([frag_blocks[0]], [60], [5])
+    assert e.value.status == spanq.ESTATE
+    plan.release()
+    torch.cuda.synchronize()
+    assert (ctx.lookup(digests) == np.array(frag_blocks)).all()
+    ctx.reposition([frag_blocks[0]], [frag_blocks[1]], [5])  # block 1 now holds R(block 0)
+    torch.cuda.synchronize()
+    ids = ctx.lookup(digests)
+    assert ids[0] == frag_blocks[0] and ids[1] == -1
+    ctx.close()

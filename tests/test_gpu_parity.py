@@ -68,10 +68,12 @@ def oracle_plan(w, queries, warm=()):
 
 
 def run_and_check(w, cuda_dev, nblk=4096, check_pages=True, out_dtype="fp32", abs_tol=BF16_MAX_ABS,
-                  rel_tol=BF16_REL_L2):
+                  rel_tol=BF16_REL_L2, options=None):
     s = w.shape
     fp32 = s.dtype == "fp32"
     ctx = spanq.Context(s, nblk, device=0, max_position=1 << 15, out_dtype=out_dtype)
+    for key, value in (options or {}).items():
+        ctx.set_option(key, value)
     tabs = [runner.device_tables(s, 0, w.seed, cuda_dev, w.peaky)]
     for q in w.warmup_queries:
         runner.run_pass(ctx, [q], tabs, cuda_dev, release=True)
@@ -153,21 +155,20 @@ def test_bf16_peaky_softmax(cuda_dev):
     run_and_check(w, cuda_dev, abs_tol=BF16_MAX_ABS * w.peaky ** 1.5, rel_tol=BF16_REL_L2 * w.peaky ** 0.5)
 
 
-def test_bf16_rescale_every_tile(cuda_dev, monkeypatch):
+@pytest.mark.parametrize("out_dtype", ["fp32", "bf16"])
+def test_bf16_rescale_every_tile(cuda_dev, out_dtype):
     # threshold 0: the conditional O rescale runs on every tile whose max grows, at the normal
     # (unscaled) tolerance — the rescale path itself is exact up to rounding
-    monkeypatch.setenv("SPANQ_RESCALE_THRESHOLD", "0")
     w = inputs.make_rag(107, inputs.Shape(hq=8, hkv=2, d=128, block_size=32, vocab=1024), 130, 3,
                         [300, 129, 260], 200)
-    run_and_check(w, cuda_dev)
+    run_and_check(w, cuda_dev, out_dtype=out_dtype, options={spanq.OPT_RESCALE_THRESHOLD: 0})
 
 
-@pytest.mark.parametrize("poly", ["0", "4"])
-def test_bf16_exp2_mufu_and_poly(cuda_dev, monkeypatch, poly):
-    # all exponentials on MUFU (0) or all on the FMA-pipe polynomial (4)
-    monkeypatch.setenv("SPANQ_POLY_EXP", poly)
+@pytest.mark.parametrize("exp2", [0, 1])
+def test_bf16_exp2_modes(cuda_dev, exp2):
+    # SPQ_OPT_EXP2: MUFU ex2 in fp32 (0, default) or ex2.f16x2, two exponentials per op (1)
     w = inputs.make_rag(108, inputs.Shape(**inputs.SHAPE_8B, block_size=64), 64, 2, [256, 200], 140)
-    run_and_check(w, cuda_dev)
+    run_and_check(w, cuda_dev, options={spanq.OPT_EXP2: exp2})
 
 
 @pytest.mark.parametrize("out_dtype", ["fp32", "bf16"])

@@ -1,19 +1,24 @@
 """Profiling only: CTA-0 event timeline of the span_attn_tc kernel for one C2 prefill launch.
-Usage: python tools/trace_step.py [dbg_mode] > gpurun_out/trace.txt"""
+Needs the profiling build (python -m paper_2511_02749_b200.build --profiling); uses it unless
+SPANQ_LIB points elsewhere.
+Usage: python tools/trace_step.py [dbg_mode] [prefill|join] [fp32|bf16] > gpurun_out/trace.txt"""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("SPANQ_LIB", os.path.join(ROOT, "paper_2511_02749_b200", "lib", "libspanq_prof.so"))
 import numpy as np
 import torch
 
 from paper_2511_02749_b200 import inputs, runner, spanq
 
-mode = sys.argv[1] if len(sys.argv) > 1 else "0"
-os.environ["SPANQ_DBG_MODE"] = mode
+mode = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+out_dtype = sys.argv[3] if len(sys.argv) > 3 else "fp32"
 dev = torch.device("cuda:0")
 w = inputs.c2()
-ctx = spanq.Context(w.shape, 1024, device=0, max_position=1 << 15, out_dtype="fp32")
+ctx = spanq.Context(w.shape, 1024, device=0, max_position=1 << 15, out_dtype=out_dtype)
+ctx.set_trace(None, mode)
 tabs = [runner.device_tables(w.shape, 0, w.seed, dev)]
 for _ in range(2):
     ctx.evict_all()
@@ -26,18 +31,18 @@ plan = ctx.plan(w.queries)
 view = plan.view()
 ptok = runner.prefill_tokens(view, w.queries)
 q, k, v = runner.gather(tabs[0], ptok, dev)
-o = torch.empty((len(ptok), 32, 128), dtype=torch.float32, device=dev)
+o = torch.empty((len(ptok), 32, 128), dtype=torch.float32 if out_dtype == "fp32" else torch.bfloat16, device=dev)
 if which == "prefill":
-    os.environ["SPANQ_TRACE"] = str(buf.data_ptr())
+    ctx.set_trace(buf, mode)
 plan.prefill(0, q, k, v, o)
 if which == "join":
     jtok = runner.join_tokens(view, w.queries)
     qj, kj, vj = runner.gather(tabs[0], jtok, dev)
-    oj = torch.empty((len(jtok), 32, 128), dtype=torch.float32, device=dev)
-    os.environ["SPANQ_TRACE"] = str(buf.data_ptr())
+    oj = torch.empty((len(jtok), 32, 128), dtype=torch.float32 if out_dtype == "fp32" else torch.bfloat16, device=dev)
+    ctx.set_trace(buf, mode)
     plan.join(0, qj, kj, vj, oj)
 torch.cuda.synchronize()
-del os.environ["SPANQ_TRACE"]
+ctx.set_trace(None, 0)
 allb = buf.cpu().numpy()
 t = allb[:NW * 2048].reshape(NW, 1024, 2)
 spans = allb[NW * 2048:].reshape(-1, 2)
