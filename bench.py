@@ -486,25 +486,31 @@ def measure_reposition(ctx, s, stream, flush, n_blocks, hbm_gbs, reps: int = 10)
     dst = g.permutation(n_blocks).astype(np.int32)
     src = np.arange(n_blocks, dtype=np.int32)
     delta = g.integers(-8192, 8193, size=n_blocks).astype(np.int32)
-    st = ctx.reposition(src, dst, delta, stream=stream)  # warm-up
-    ms = []
-    for _ in range(reps):
-        flush.zero_()
-        stream.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        ctx.reposition(src, dst, delta, stream=stream)
-        b.record(stream)
-        stream.synchronize()
-        ms.append(a.elapsed_time(b))
-    ctx.evict_all()  # the moved blocks no longer hold what the store's index says
-    t = statistics.median(ms)
+    def timed(layers):
+        st = ctx.reposition(src, dst, delta, layers=layers, stream=stream)  # warm-up
+        ms = []
+        for _ in range(reps):
+            flush.zero_()
+            stream.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ctx.reposition(src, dst, delta, layers=layers, stream=stream)
+            b.record(stream)
+            stream.synchronize()
+            ms.append(a.elapsed_time(b))
+        return st, statistics.median(ms)
+
+    ctx.evict_all()  # the moves drop their destinations from the store (spq_reposition)
+    st, t = timed((0, s.layers))
+    _, t1 = timed((0, 1))  # one layer: few CTAs per component, rows split over the grid
     elt = 2 if s.dtype == "bf16" else 4
     nbytes = 2 * 2 * n_blocks * s.layers * s.hkv * s.block_size * s.d * elt
+    nb1 = nbytes // s.layers
     return {"kernel": "cidra (K8)", "moves": n_blocks, "layers": s.layers, "cycles": st["cycles"],
             "components": st["components"], "ms": t, "tokens_per_ms": n_blocks * s.block_size / t,
             "achieved_gbs": nbytes / (t / 1e3) / 1e9, "peak_gbs": hbm_gbs,
             "frac": nbytes / (t / 1e3) / 1e9 / hbm_gbs, "bytes": nbytes, "traffic": ncu_traffic("cidra reposition"),
+            "l1": {"ms": t1, "achieved_gbs": nb1 / (t1 / 1e3) / 1e9, "frac": nb1 / (t1 / 1e3) / 1e9 / hbm_gbs},
             "note": "paper: up to 500 tokens/ms on its own hardware and model (P:648), context only"}
 
 
