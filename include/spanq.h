@@ -204,6 +204,41 @@ spq_status spq_exchange_unpack(spq_ctx *ctx, spq_plan *plan, int32_t layer, int3
 spq_status spq_join_phase(spq_ctx *ctx, spq_plan *plan, int32_t layer, int32_t phase, const void *q,
                           const void *k, const void *v, void *o, float *lse, void *stream);
 
+/* ------------------------------------------------------------------ decode after the join
+ * Token generation G over a span query (§4.1, Def. "Span Query" P:205-207; nested
+ * generation P:170). Generated token t of home query q
+ * sits at position N_q + t (N_q = P + S + C, reading R3) and its KV continues the cross
+ * segment's blocks (the partial cross tail block, then plan-private generation blocks).
+ *
+ * Reserve generation blocks for max_new tokens of every home query of the plan (rows in query
+ * order) and build the decode work lists (one H2D). Call once per plan, after spq_plan_create.
+ * SPQ_ENOMEM: the pool cannot hold them (nothing reserved); SPQ_EINVAL: max_new < 1 or a query
+ * would exceed max_position; SPQ_ESTATE: released plan, reserved twice, or no home query. */
+spq_status spq_decode_reserve(spq_ctx *ctx, spq_plan *plan, int32_t max_new);
+/* Decode step t (0 <= t < max_new) of layer `layer` for every home query: rope_kv_write of the
+ * new token's k/v at position N_q + t into its reserved slot, then its row attends over
+ * [prefix | every fragment at Δ_f (Q counter-rotated) | cross + generated 0..t] (K9,
+ * split-KV + combine). q: device [rows, Hq, d], k/v: device [rows, Hkv, d] (pre-RoPE, ctx
+ * dtype), o: device [rows, Hq, d] (out dtype), lse: device [rows, Hq] fp32 or NULL; rows = the
+ * plan's home queries in query order. Steps of a layer must be issued in order t = 0, 1, ...
+ * after that layer's spq_join (same stream). SPQ_ESTATE: not reserved, t out of range, bad layer,
+ * released plan, host-only ctx. */
+spq_status spq_decode_step(spq_ctx *ctx, spq_plan *plan, int32_t layer, int32_t t, const void *q,
+                           const void *k, const void *v, void *o, float *lse, void *stream);
+/* Plus distribution: commit query `query`'s sequence — its cross tokens followed by
+ * its first n_gen generated tokens (host array, the caller's sampled ids) — as a cached
+ * fragment: its blocks are indexed under the fragment chain ('F', DESIGN.md hash contract) of
+ * those tokens, so a later query with the sequence as a ⊕ fragment hits without prefill (the KV
+ * is already at span-local positions 0..len-1). crop = 1 drops the trailing partial block
+ * (the paper's cropping); crop = 0 keeps it with its true token count (reading R8).
+ * *n_committed = tokens committed (the fragment the caller must use). The query must have no
+ * prefix and no fragments (an inner generate ⋈[input], positions from 0): SPQ_EINVAL otherwise.
+ * The decode steps 0..n_gen-1 of every layer must have been issued. The blocks stay pinned until
+ * the plan's release, then are ordinary cached blocks (LRU). SPQ_ESTATE: released plan or n_gen
+ * beyond the reservation. */
+spq_status spq_commit_span(spq_ctx *ctx, spq_plan *plan, int32_t query, const int32_t *gen_tokens /*host*/,
+                           int32_t n_gen, int32_t crop, int32_t *n_committed /*or NULL*/);
+
 /* Stream-ordered release: unpins the plan's blocks and frees its plan-private blocks; later
  * kernel calls on any stream wait for `stream` to pass this point before touching them. The
  * handle stays reserved (emptied) for the next 1024 releases of the ctx: any call on it in that

@@ -119,6 +119,16 @@ def join_rows(prefix, frags, cross, eq, ek, ev, base: float,
     return attend(q, k, v, mask, heads)
 
 
+def decode_row(prefix, frags, cross, gen, t: int, eq, ek, ev, base: float,
+               heads: Optional[Sequence[int]] = None):
+    """Token generation after the join (§4.1 "G"): generated token t sits
+    right after the cross tokens and the t tokens generated before it (global position
+    P+S+C+t, reading R3) and, being the next ordered token, attends to everything before it and
+    itself — the plain definition's cross row of the query whose cross is cross ‖ gen[0..t]."""
+    ext = np.concatenate([np.asarray(cross, np.int64), np.asarray(gen[: t + 1], np.int64)])
+    return join_rows(prefix, frags, ext, eq, ek, ev, base, rows=[len(cross) + t], heads=heads)
+
+
 def expected_pages(tokens, eq_unused, ek, ev, base: float, positions) -> Tuple[np.ndarray, np.ndarray]:
     """K/V rows as stored in the pool: RoPE(k, stored position), v unrotated (R15: RoPE on q, k)."""
     t = np.asarray(tokens, np.int64)

@@ -630,6 +630,55 @@ void Store::abort(const PlanHost& p) {
   }
 }
 
+int Store::extend_private(PlanHost* p, int64_t n, std::vector<int32_t>* out) {
+  std::vector<int32_t> got;
+  journal_.clear();
+  journaling_ = true;
+  bool ok = true;
+  for (int64_t i = 0; i < n && ok; ++i) {
+    const int32_t b = alloc(&ok);
+    if (ok) got.push_back(b);
+  }
+  if (!ok) {
+    rollback();
+    journaling_ = false;
+    return 2;
+  }
+  journal_.clear();
+  journaling_ = false;
+  for (int32_t b : got) {
+    p->priv.push_back(b);
+    p->pinned.push_back(b);
+    pins_[b]++;
+  }
+  out->insert(out->end(), got.begin(), got.end());
+  return 0;
+}
+
+int64_t Store::commit(PlanHost* p, const int32_t* blocks, const Digest* dig, const int32_t* ntok, int64_t n) {
+  int64_t done = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t b = blocks[i];
+    auto it = index_.find(dig[i]);
+    if (it != index_.end()) continue;  // resident already (here or in an equal-content block)
+    if (meta_[b].resident) {           // re-key (e.g. a full cross block under its X digest)
+      if (pins_[b] == 0) set_evictable(b, false);
+      index_.erase(meta_[b].dig);
+    }
+    index_[dig[i]] = b;
+    meta_[b] = Meta{dig[i], ntok[i], plan_no_, true};
+    auto pv = std::find(p->priv.begin(), p->priv.end(), b);
+    if (pv != p->priv.end()) p->priv.erase(pv);
+    if (std::find(p->pinned.begin(), p->pinned.end(), b) == p->pinned.end()) {
+      p->pinned.push_back(b);
+      pins_[b]++;
+    }
+    stats_.inserted_blocks++;
+    ++done;
+  }
+  return done;
+}
+
 void Store::drop(int32_t b) {
   if (!meta_[b].resident) return;
   set_evictable(b, false);

@@ -124,6 +124,15 @@ class Store {
   // Pinned blocks are the caller's to exclude.
   void drop(int32_t b);
   bool is_pinned(int32_t b) const { return pins_[b] > 0; }
+  // Allocate n more plan-private blocks for a live plan (lowest free id, LRU eviction; pinned,
+  // freed at release). All-or-nothing: returns 2 (ENOMEM, nothing allocated) or 0.
+  int extend_private(PlanHost* p, int64_t n, std::vector<int32_t>* out);
+  // Plus distribution: index blocks[i] under dig[i] (ntok[i] tokens) as cached KV of a
+  // live plan. A block already indexed under another digest is re-keyed; a digest already
+  // resident elsewhere is left alone (the two blocks hold the same content); plan-private blocks
+  // leave the plan's private list (they are no longer freed at release, only unpinned).
+  // Returns the number of blocks indexed.
+  int64_t commit(PlanHost* p, const int32_t* blocks, const Digest* dig, const int32_t* ntok, int64_t n);
   void evict_all();
   int32_t lookup(const Digest& d) const;
   // Low-level insert: returns 0 or 2 (ENOMEM, rolled back).

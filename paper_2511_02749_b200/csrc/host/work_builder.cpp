@@ -9,24 +9,31 @@
 namespace spq {
 namespace {
 
-// Append the KV tiles of one segment; returns the index of its first tile.
-int32_t add_tiles(const PlanHost& p, const Segment& s, int bs, int32_t key_base, int32_t rot,
-                  int32_t causal, AttnWorkHost* w) {
-  const int32_t first = static_cast<int32_t>(w->tiles.size());
+// Append the KV tiles of n_tok tokens held densely in blocks[0..]; returns the first tile index.
+int32_t append_tiles(const int32_t* blocks, int32_t n_tok, int bs, int32_t key_base, int32_t rot, int32_t causal,
+                     std::vector<KvTile>* tiles, std::vector<int32_t>* tile_blocks) {
+  const int32_t first = static_cast<int32_t>(tiles->size());
   const int bpt = kTileKeys / bs;
-  for (int32_t t0 = 0; t0 < s.tok_len; t0 += kTileKeys) {
+  for (int32_t t0 = 0; t0 < n_tok; t0 += kTileKeys) {
     KvTile k{};
-    k.blk_off = static_cast<int32_t>(w->tile_blocks.size());
-    k.n_valid = std::min(kTileKeys, s.tok_len - t0);
+    k.blk_off = static_cast<int32_t>(tile_blocks->size());
+    k.n_valid = std::min(kTileKeys, n_tok - t0);
     k.key_pos0 = key_base + t0;
     k.rot_delta = rot;
     k.causal = causal;
     const int32_t b0 = t0 / bs;
     const int32_t nb = (k.n_valid + bs - 1) / bs;
-    for (int j = 0; j < bpt; ++j) w->tile_blocks.push_back(p.blocks[s.block_off + b0 + std::min(j, nb - 1)]);
-    w->tiles.push_back(k);
+    for (int j = 0; j < bpt; ++j) tile_blocks->push_back(blocks[b0 + std::min(j, nb - 1)]);
+    tiles->push_back(k);
   }
   return first;
+}
+
+// Append the KV tiles of one segment; returns the index of its first tile.
+int32_t add_tiles(const PlanHost& p, const Segment& s, int bs, int32_t key_base, int32_t rot,
+                  int32_t causal, AttnWorkHost* w) {
+  return append_tiles(p.blocks.data() + s.block_off, s.tok_len, bs, key_base, rot, causal, &w->tiles,
+                      &w->tile_blocks);
 }
 
 // Schedule of (item, unit) codes over `grid` persistent CTAs: codes sorted by cost, longest
@@ -272,6 +279,46 @@ void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_en
   for (int c = 0; c < used; ++c) {
     w->cta_off[c + 1] = w->cta_off[c] + static_cast<int32_t>(per_cta[c].size());
     w->cta_items.insert(w->cta_items.end(), per_cta[c].begin(), per_cta[c].end());
+  }
+}
+
+std::pair<int32_t, int32_t> decode_row_tiles(const PlanHost& p, int32_t query, const std::vector<int32_t>& cross_gen_blocks,
+                                             int32_t gen_ctx, int bs, DecodeWorkHost* w) {
+  const int32_t first = static_cast<int32_t>(w->tiles.size());
+  for (const Segment& s : p.segs) {
+    if (s.query != query) continue;
+    const int32_t* blk = p.blocks.data() + s.block_off;
+    if (s.kind == kPrefix)
+      append_tiles(blk, s.tok_len, bs, 0, 0, 0, &w->tiles, &w->tile_blocks);
+    else if (s.kind == kFrag)
+      append_tiles(blk, s.tok_len, bs, s.pos0, s.pos0, 0, &w->tiles, &w->tile_blocks);
+    else
+      append_tiles(cross_gen_blocks.data(), gen_ctx, bs, s.pos0, 0, 1, &w->tiles, &w->tile_blocks);
+  }
+  return {first, static_cast<int32_t>(w->tiles.size())};
+}
+
+void decode_items(const std::vector<std::pair<int32_t, int32_t>>& row_tiles, int hkv, int group, int chunk_tiles,
+                  DecodeWorkHost* w) {
+  for (size_t r = 0; r < row_tiles.size(); ++r) {
+    const int32_t tb = row_tiles[r].first, te = row_tiles[r].second;
+    const int32_t n = std::max<int32_t>(1, (te - tb + chunk_tiles - 1) / chunk_tiles);
+    for (int32_t h = 0; h < hkv; ++h) {
+      const int32_t pb = n > 1 ? w->n_parts : -1;
+      for (int32_t c = 0; c < n; ++c) {
+        DecodeItemHost it{};
+        it.row = static_cast<int32_t>(r);
+        it.kvh = h;
+        it.tile_begin = tb + c * chunk_tiles;
+        it.tile_end = std::min(te, tb + (c + 1) * chunk_tiles);
+        it.part = n > 1 ? pb + c : -1;
+        w->items.push_back(it);
+      }
+      if (n > 1) {
+        w->combine.push_back({static_cast<int32_t>(r), 1, pb, n, h * group, group, 0, 0});
+        w->n_parts += n;
+      }
+    }
   }
 }
 

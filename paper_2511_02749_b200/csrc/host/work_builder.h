@@ -10,6 +10,11 @@
 
 namespace spq {
 
+struct DecodeItemHost {
+  int32_t row, kvh, tile_begin, tile_end, part;  // mirrors kernels/launch.h DecodeItem
+  int32_t pad0, pad1, pad2;
+};
+
 struct AttnWorkHost {
   std::vector<KvTile> tiles;
   std::vector<int32_t> tile_blocks;
@@ -51,5 +56,24 @@ struct JoinPhase {
 // launch over every segment.
 void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_end, AttnWorkHost* w,
                      const JoinPhase* ph = nullptr);
+
+// Decode after the join: the KV tiles of one home query for its generated
+// rows — prefix (non-causal), fragments at Δ_f (non-causal, Q counter-rotated), then the cross +
+// generated tokens as one causal segment of gen_ctx tokens over `cross_gen_blocks` — split per kv
+// head into chunks of <= chunk_tiles tiles (K9 items; a (row, kv head) with several chunks writes
+// partials merged by combine, rows_per_part = 1).
+struct DecodeWorkHost {
+  std::vector<KvTile> tiles;
+  std::vector<int32_t> tile_blocks;
+  std::vector<DecodeItemHost> items;
+  std::vector<CombineDesc> combine;
+  int32_t n_parts = 0;
+};
+// Tiles of one decode row, appended to w; returns [first, end) tile range.
+std::pair<int32_t, int32_t> decode_row_tiles(const PlanHost& p, int32_t query, const std::vector<int32_t>& cross_gen_blocks,
+                                             int32_t gen_ctx, int bs, DecodeWorkHost* w);
+// Items for rows whose tile ranges are given: chunks of <= chunk_tiles per (row, kv head).
+void decode_items(const std::vector<std::pair<int32_t, int32_t>>& row_tiles, int hkv, int group, int chunk_tiles,
+                  DecodeWorkHost* w);
 
 }  // namespace spq

@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineDesc* __restr
                                                       const float* __restrict__ opart,
                                                       const float* __restrict__ lsepart,
                                                       TO* __restrict__ o,
-                                                      float* __restrict__ lse, int hq) {
+                                                      float* __restrict__ lse, int hq, int rpp) {
   constexpr int E = D / 32;  // columns per lane
   // launched as a programmatic dependent of the join it merges (when nothing sits between them):
   // the partials are read only once that grid has completed
@@ -35,11 +35,12 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineDesc* __restr
   if (static_cast<int>(blockIdx.y) >= cd.n_heads) return;
   const int h = cd.head0 + blockIdx.y;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // grid.z splits the 128 rows of a tile into groups of blockDim/32 rows: one warp per row
+  // grid.z splits the rows of a tile into groups of blockDim/32 rows: one warp per row. A partial
+  // slot holds rpp rows per head (kTileRows for joins, 1 for decode)
   for (int r = blockIdx.z * (blockDim.x / 32) + warp; r < cd.n_rows; r += gridDim.z * (blockDim.x / 32)) {
-    const int64_t pstride = static_cast<int64_t>(cd.n_heads) * kTileRows;  // next split, same (head, row)
-    const int64_t base = (static_cast<int64_t>(cd.part_base) * cd.n_heads + blockIdx.y) * kTileRows + r;
-    const int64_t base2 = (static_cast<int64_t>(cd.part_base2) * cd.n_heads + blockIdx.y) * kTileRows + r;
+    const int64_t pstride = static_cast<int64_t>(cd.n_heads) * rpp;  // next split, same (head, row)
+    const int64_t base = (static_cast<int64_t>(cd.part_base) * cd.n_heads + blockIdx.y) * rpp + r;
+    const int64_t base2 = (static_cast<int64_t>(cd.part_base2) * cd.n_heads + blockIdx.y) * rpp + r;
     const int n_all = cd.n_split + cd.n_split2;
     float m = -INFINITY;
     float acc[E];
@@ -94,7 +95,8 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineDesc* __restr
 
 template <int D, typename TO>
 void launch_dt(const CombineArgs& a, cudaStream_t st) {
-  dim3 grid(a.n_desc, a.heads_per_desc, kTileRows / 8);
+  const int rpp = a.rows_per_part > 0 ? a.rows_per_part : kTileRows;
+  dim3 grid(a.n_desc, a.heads_per_desc, (rpp + 7) / 8);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(256);
@@ -104,7 +106,7 @@ void launch_dt(const CombineArgs& a, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = a.pdl ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, combine_kernel<D, TO>, a.desc, a.opart, a.lsepart, static_cast<TO*>(a.o), a.lse, a.hq);
+  cudaLaunchKernelEx(&cfg, combine_kernel<D, TO>, a.desc, a.opart, a.lsepart, static_cast<TO*>(a.o), a.lse, a.hq, rpp);
 }
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {

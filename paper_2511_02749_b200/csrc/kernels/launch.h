@@ -79,9 +79,38 @@ struct CombineArgs {
   float* lse;
   int hq, d;
   int heads_per_desc;  // max CombineDesc::n_heads
+  int rows_per_part;   // rows of one (partial slot, head): kTileRows (joins) or 1 (decode)
   bool out_fp32;
   bool pdl;  // launch as a programmatic dependent of the join kernel right before it
 };
+
+// K9 decode (decode.cu): one work item = (home query row, kv head, chunk of KV tiles)
+struct DecodeItem {
+  int32_t row, kvh, tile_begin, tile_end, part;  // part -1: write o / lse directly
+  int32_t pad0, pad1, pad2;
+};
+struct DecodeArgs {
+  const DecodeItem* items;
+  int32_t n_items;
+  const KvTile* tiles;
+  const int32_t* tile_blocks;
+  const int32_t* pos_base;  // [rows] N_q: position of generated token 0
+  int32_t step;             // generated token t: the row sits at pos_base + t
+  const void* q;            // [rows][hq][d] pre-RoPE, pool dtype
+  void* o;                  // [rows][hq][d] out dtype
+  float* lse;               // [rows][hq] or null
+  float* opart;             // [parts][g][d]
+  float* lsepart;           // [parts][g]
+  const void* k_pool;
+  const void* v_pool;
+  const float2* rope;
+  int max_pos;
+  int hq, hkv, d, bs;
+  int64_t nblk;
+  int layer;
+  bool fp32, out_fp32;
+};
+cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t st);
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);
 
 struct KvExchangeArgs {

@@ -133,7 +133,21 @@ struct spq_plan {
   float* lsepart = nullptr;
   std::vector<uint8_t> padded_layers;
   spq::AttnWorkHost pw_host, jw_host;  // kept for sub-range rebuilds / inspection
+  std::vector<std::vector<int32_t>> cross_tokens;  // per query (plus distribution: commit)
+  // decode after the join (spq_decode_reserve / spq_decode_step / spq_commit_span)
+  struct Decode {
+    int32_t max_new = 0;
+    std::vector<int32_t> rows;                      // home query of each decode row
+    std::vector<std::vector<int32_t>> blocks;       // per row: cross blocks + generation blocks
+    uint8_t* dbuf = nullptr;
+    size_t off_tiles = 0, off_tb = 0, off_items = 0, off_comb = 0, off_posb = 0, off_kpos = 0, off_kslot = 0;
+    float* opart = nullptr;
+    float* lsepart = nullptr;
+    int32_t n_items = 0, n_comb = 0;
+  } dec;
 };
+
+using Decode = spq_plan::Decode;
 
 namespace {
 
@@ -462,6 +476,7 @@ void spq_destroy(spq_ctx* c) {
   }
   for (spq_plan* p : c->live) {  // plans never released: their device arrays go with the ctx
     if (p->dbuf) cudaFree(p->dbuf);
+    if (p->dec.dbuf) cudaFree(p->dec.dbuf);
     delete p;
   }
   for (spq_plan* p : c->quarantine) delete p;
@@ -573,6 +588,7 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
     p->seg_block_off.push_back(s.block_off);
     p->seg_n_blocks.push_back(s.n_blocks);
   }
+  for (const auto& q : fq) p->cross_tokens.push_back(q.cross);
   for (const auto& d : H.digests) p->digests.insert(p->digests.end(), d.b, d.b + 16);
   for (const auto& d : H.join_digests) p->join_digests.insert(p->join_digests.end(), d.b, d.b + 16);
   p->padded_layers.assign(c->cfg.num_layers, 0);
@@ -995,8 +1011,10 @@ spq_status spq_plan_release(spq_ctx* c, spq_plan* p, void* stream) {
     CUDA_TRY(cudaEventRecord(e, st));
     c->pending.push_back(e);
     if (p->dbuf) CUDA_TRY(cudaFreeAsync(p->dbuf, st));
+    if (p->dec.dbuf) CUDA_TRY(cudaFreeAsync(p->dec.dbuf, st));
     // opart / lsepart live inside dbuf
     p->dbuf = nullptr;
+    p->dec.dbuf = nullptr;
   }
   c->store->release(p->host);
   c->live.erase(p);
@@ -1008,6 +1026,209 @@ spq_status spq_plan_release(spq_ctx* c, spq_plan* p, void* stream) {
     delete c->quarantine.front();
     c->quarantine.pop_front();
   }
+  return SPQ_OK;
+}
+
+// ------------------------------------------------------------------ decode after the join (f3)
+spq_status spq_decode_reserve(spq_ctx* c, spq_plan* p, int32_t max_new) {
+  if (c == nullptr || p == nullptr) return fail(SPQ_EINVAL, "null argument");
+  if (!c->live.count(p)) return fail(SPQ_ESTATE, "plan used after release (or not a plan of this ctx)");
+  if (max_new < 1) return fail(SPQ_EINVAL, "max_new must be >= 1");
+  if (p->dec.max_new > 0) return fail(SPQ_ESTATE, "decode already reserved for this plan");
+  const spq::PlanHost& H = p->host;
+  const int bs = c->cfg.block_size;
+  // decode rows: home queries in query order; generation blocks continue each cross segment
+  std::vector<int32_t> rows, cross_seg;
+  int64_t extra = 0;
+  for (size_t i = 0; i < H.segs.size(); ++i) {
+    const spq::Segment& sg = H.segs[i];
+    if (sg.kind != spq::kCross) continue;
+    if (static_cast<int64_t>(sg.pos0) + sg.tok_len + max_new > c->cfg.max_position)
+      return fail(SPQ_EINVAL, "query " + std::to_string(sg.query) + ": generation exceeds max_position");
+    rows.push_back(sg.query);
+    cross_seg.push_back(static_cast<int32_t>(i));
+    extra += (static_cast<int64_t>(sg.tok_len) + max_new + bs - 1) / bs - sg.n_blocks;
+  }
+  if (rows.empty()) return fail(SPQ_ESTATE, "no query of the plan is homed on this rank");
+  std::vector<int32_t> fresh;
+  if (c->store->extend_private(&p->host, extra, &fresh) != 0)
+    return fail(SPQ_ENOMEM, "block pool cannot hold the generation blocks (nothing reserved)");
+  Decode& D = p->dec;
+  D.rows = rows;
+  D.blocks.assign(rows.size(), {});
+  const int64_t B = static_cast<int64_t>(rows.size());
+  std::vector<int32_t> pos_base(B), kpos(static_cast<size_t>(max_new) * B);
+  std::vector<int64_t> kslot(static_cast<size_t>(max_new) * B);
+  spq::DecodeWorkHost w;
+  std::vector<std::pair<int32_t, int32_t>> row_tiles;
+  size_t fi = 0;
+  for (int64_t b = 0; b < B; ++b) {
+    const spq::Segment& sg = H.segs[cross_seg[b]];
+    std::vector<int32_t>& bl = D.blocks[b];
+    bl.assign(H.blocks.begin() + sg.block_off, H.blocks.begin() + sg.block_off + sg.n_blocks);
+    const int64_t need = (static_cast<int64_t>(sg.tok_len) + max_new + bs - 1) / bs - sg.n_blocks;
+    for (int64_t i = 0; i < need; ++i) bl.push_back(fresh[fi++]);
+    pos_base[b] = sg.pos0 + sg.tok_len;
+    for (int32_t t = 0; t < max_new; ++t) {
+      const int64_t idx = static_cast<int64_t>(sg.tok_len) + t;
+      kpos[t * B + b] = pos_base[b] + t;
+      kslot[t * B + b] = static_cast<int64_t>(bl[idx / bs]) * bs + idx % bs;
+    }
+    row_tiles.push_back(spq::decode_row_tiles(H, sg.query, bl, sg.tok_len + max_new, bs, &w));
+  }
+  // chunks of <= T tiles per (row, kv head): ~4 CTAs per SM over the whole batch
+  int64_t tiles = 0;
+  for (const auto& rt : row_tiles) tiles += rt.second - rt.first;
+  const int64_t target = 4LL * (c->num_sms > 0 ? c->num_sms : 148);
+  const int chunk = static_cast<int>(std::max<int64_t>(1, (tiles * c->cfg.num_kv_heads + target - 1) / target));
+  spq::decode_items(row_tiles, c->cfg.num_kv_heads, c->cfg.num_q_heads / c->cfg.num_kv_heads, chunk, &w);
+  D.max_new = max_new;
+  D.n_items = static_cast<int32_t>(w.items.size());
+  D.n_comb = static_cast<int32_t>(w.combine.size());
+  if (!is_gpu(c)) return SPQ_OK;
+  Packer pk;
+  D.off_tiles = pk.add(w.tiles);
+  D.off_tb = pk.add(w.tile_blocks);
+  D.off_items = pk.add(w.items);
+  D.off_comb = pk.add(w.combine);
+  D.off_posb = pk.add(pos_base);
+  D.off_kpos = pk.add(kpos);
+  D.off_kslot = pk.add(kslot);
+  const int g = c->cfg.num_q_heads / c->cfg.num_kv_heads;
+  const size_t off_op = align_up(pk.size, 256);
+  const size_t off_lp = align_up(off_op + static_cast<size_t>(w.n_parts) * g * c->cfg.head_dim * sizeof(float), 256);
+  const size_t bytes = off_lp + static_cast<size_t>(w.n_parts) * g * sizeof(float) + 256;
+  std::vector<uint8_t> host(pk.size);
+  pk.write(host.data());
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  CUDA_TRY(cudaMalloc(&D.dbuf, bytes));
+  CUDA_TRY(cudaMemcpy(D.dbuf, host.data(), pk.size, cudaMemcpyHostToDevice));
+  D.opart = reinterpret_cast<float*>(D.dbuf + off_op);
+  D.lsepart = reinterpret_cast<float*>(D.dbuf + off_lp);
+  return SPQ_OK;
+}
+
+spq_status spq_decode_step(spq_ctx* c, spq_plan* p, int32_t layer, int32_t t, const void* q, const void* k,
+                           const void* v, void* o, float* lse, void* stream) {
+  spq_status s = check_call(c, p, layer);
+  if (s != SPQ_OK) return s;
+  Decode& D = p->dec;
+  if (D.max_new == 0) return fail(SPQ_ESTATE, "spq_decode_reserve was not called for this plan");
+  if (t < 0 || t >= D.max_new) return fail(SPQ_ESTATE, "step outside the reserved generation range");
+  if (q == nullptr || k == nullptr || v == nullptr || o == nullptr) return fail(SPQ_EINVAL, "null buffer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  s = wait_pending(c, st);
+  if (s != SPQ_OK) return s;
+  const int64_t B = static_cast<int64_t>(D.rows.size());
+  // K1: the new tokens' K (RoPE at N_q + t) and V into their reserved slots
+  spq::KvWriteArgs kw{};
+  kw.k = k;
+  kw.v = v;
+  kw.pos = reinterpret_cast<const int32_t*>(D.dbuf + D.off_kpos) + t * B;
+  kw.slot = reinterpret_cast<const int64_t*>(D.dbuf + D.off_kslot) + t * B;
+  kw.rows = B;
+  kw.n_pad = 0;
+  kw.k_pool = c->cfg.k_pool;
+  kw.v_pool = c->cfg.v_pool;
+  kw.hkv = c->cfg.num_kv_heads;
+  kw.d = c->cfg.head_dim;
+  kw.bs = c->cfg.block_size;
+  kw.nblk = c->cfg.num_blocks;
+  kw.layer = layer;
+  kw.rope = c->rope;
+  kw.fp32 = c->cfg.dtype == SPQ_FP32;
+  cudaError_t e = spq::launch_rope_kv_write(kw, st);
+  if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("rope_kv_write launch: ") + cudaGetErrorString(e));
+  c->launches++;
+  // K9: the new rows over every segment, split-KV
+  spq::DecodeArgs a{};
+  a.items = reinterpret_cast<const spq::DecodeItem*>(D.dbuf + D.off_items);
+  a.n_items = D.n_items;
+  a.tiles = reinterpret_cast<const spq::KvTile*>(D.dbuf + D.off_tiles);
+  a.tile_blocks = reinterpret_cast<const int32_t*>(D.dbuf + D.off_tb);
+  a.pos_base = reinterpret_cast<const int32_t*>(D.dbuf + D.off_posb);
+  a.step = t;
+  a.q = q;
+  a.o = o;
+  a.lse = lse;
+  a.opart = D.opart;
+  a.lsepart = D.lsepart;
+  a.k_pool = c->cfg.k_pool;
+  a.v_pool = c->cfg.v_pool;
+  a.rope = c->rope;
+  a.max_pos = c->cfg.max_position;
+  a.hq = c->cfg.num_q_heads;
+  a.hkv = c->cfg.num_kv_heads;
+  a.d = c->cfg.head_dim;
+  a.bs = c->cfg.block_size;
+  a.nblk = c->cfg.num_blocks;
+  a.layer = layer;
+  a.fp32 = c->cfg.dtype == SPQ_FP32;
+  a.out_fp32 = c->cfg.out_dtype == SPQ_FP32;
+  e = spq::launch_decode(a, st);
+  if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("decode launch: ") + cudaGetErrorString(e));
+  c->launches++;
+  if (D.n_comb > 0) {
+    spq::CombineArgs ca{};
+    ca.desc = reinterpret_cast<const spq::CombineDesc*>(D.dbuf + D.off_comb);
+    ca.n_desc = D.n_comb;
+    ca.opart = D.opart;
+    ca.lsepart = D.lsepart;
+    ca.o = o;
+    ca.lse = lse;
+    ca.hq = c->cfg.num_q_heads;
+    ca.heads_per_desc = c->cfg.num_q_heads / c->cfg.num_kv_heads;
+    ca.rows_per_part = 1;
+    ca.d = c->cfg.head_dim;
+    ca.out_fp32 = c->cfg.out_dtype == SPQ_FP32;
+    ca.pdl = false;
+    e = spq::launch_combine(ca, st);
+    if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("combine launch: ") + cudaGetErrorString(e));
+    c->launches++;
+  }
+  return SPQ_OK;
+}
+
+spq_status spq_commit_span(spq_ctx* c, spq_plan* p, int32_t query, const int32_t* gen_tokens, int32_t n_gen,
+                           int32_t crop, int32_t* n_committed) {
+  if (c == nullptr || p == nullptr || (n_gen > 0 && gen_tokens == nullptr)) return fail(SPQ_EINVAL, "null argument");
+  if (!c->live.count(p)) return fail(SPQ_ESTATE, "plan used after release (or not a plan of this ctx)");
+  const spq::PlanHost& H = p->host;
+  if (query < 0 || query >= H.n_queries) return fail(SPQ_EINVAL, "query out of range");
+  const Decode& D = p->dec;
+  int64_t row = -1;
+  for (size_t b = 0; b < D.rows.size(); ++b)
+    if (D.rows[b] == query) row = static_cast<int64_t>(b);
+  if (n_gen < 0 || (n_gen > 0 && row < 0) || n_gen > D.max_new)
+    return fail(SPQ_ESTATE, "n_gen outside the reserved generation range of this query");
+  for (const spq::Segment& sg : H.segs)
+    if (sg.query == query && sg.kind != spq::kCross)
+      return fail(SPQ_EINVAL, "only a query without prefix and fragments (an inner generate ⋈[input]) "
+                              "is a span at positions 0..: plus distribution needs its KV span-local");
+  const int bs = c->cfg.block_size;
+  std::vector<int32_t> toks = p->cross_tokens[query];
+  for (int32_t i = 0; i < n_gen; ++i) {
+    if (gen_tokens[i] < 0) return fail(SPQ_EINVAL, "negative token");
+    toks.push_back(gen_tokens[i]);
+  }
+  int64_t keep = static_cast<int64_t>(toks.size());
+  if (crop) keep = keep / bs * bs;  // trailing partial block cropped
+  if (n_committed) *n_committed = static_cast<int32_t>(keep);
+  if (keep == 0) return SPQ_OK;
+  std::vector<int32_t> blocks;
+  if (row >= 0) {
+    blocks = D.blocks[row];
+  } else {  // no generation reserved: the cross blocks themselves
+    for (const spq::Segment& sg : H.segs)
+      if (sg.query == query && sg.kind == spq::kCross)
+        blocks.assign(H.blocks.begin() + sg.block_off, H.blocks.begin() + sg.block_off + sg.n_blocks);
+  }
+  std::vector<spq::Digest> dig;
+  spq::chain('F', c->store->root(), toks.data(), keep, bs, &dig);
+  std::vector<int32_t> ntok(dig.size());
+  for (size_t i = 0; i < dig.size(); ++i) ntok[i] = static_cast<int32_t>(std::min<int64_t>(bs, keep - static_cast<int64_t>(i) * bs));
+  c->store->commit(&p->host, blocks.data(), dig.data(), ntok.data(), static_cast<int64_t>(dig.size()));
   return SPQ_OK;
 }
 

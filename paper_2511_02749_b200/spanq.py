@@ -123,6 +123,11 @@ SIGNATURES = {
     "spq_launch_count": (C.c_int, [C.c_void_p, _I64P]),
     "spq_last_attn_ms": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "spq_set_timing": (C.c_int, [C.c_void_p, C.c_int32]),
+    "spq_decode_reserve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "spq_decode_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "spq_commit_span": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32,
+                                  _I32P]),
     "spq_set_option": (C.c_int, [C.c_void_p, C.c_int32, C.c_double]),
     "spq_set_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
 }
@@ -272,6 +277,25 @@ class Plan:
         """Phase 0 / 1 of the join of all home queries (W > 1: around the fragment-KV exchange)."""
         _check(lib().spq_join_phase(self.ctx.handle, self.handle, layer, phase, _ptr(q), _ptr(k), _ptr(v),
                                     _ptr(o), _ptr(lse), _stream_ptr(stream, self.ctx.device)))
+
+    def decode_reserve(self, max_new: int):
+        """Reserve generation blocks for max_new tokens per home query (rows in query order)."""
+        _check(lib().spq_decode_reserve(self.ctx.handle, self.handle, int(max_new)))
+        self.max_new = int(max_new)
+
+    def decode_step(self, layer, t, q, k, v, o, lse=None, stream=None):
+        """Generated token t of every home query: K1 of its k/v, then its row over the whole span."""
+        _check(lib().spq_decode_step(self.ctx.handle, self.handle, layer, t, _ptr(q), _ptr(k), _ptr(v), _ptr(o),
+                                     _ptr(lse), _stream_ptr(stream, self.ctx.device)))
+
+    def commit_span(self, query: int, gen_tokens, crop: bool = False) -> int:
+        """Plus distribution: index the query's (cross ‖ generated) tokens as a cached fragment;
+        returns the tokens committed (the trailing partial block is dropped with crop=True)."""
+        g = np.ascontiguousarray(gen_tokens, dtype=np.int32)
+        n = C.c_int32()
+        _check(lib().spq_commit_span(self.ctx.handle, self.handle, int(query), g.ctypes.data if len(g) else None,
+                                     len(g), 1 if crop else 0, C.byref(n)))
+        return n.value
 
     def release(self, stream=None):
         if not self.released:

@@ -259,3 +259,61 @@ def test_block_hashes_both_blake2b_paths(scalar):
         assert d == h + s + [J] + hashing.cross_chain(q.cross, 64, J)
     finally:
         spanq.Context(sh, 64, device=-1).set_option(spanq.OPT_HASH_SCALAR, 0)
+
+
+@pytest.mark.parametrize("crop", [False, True])
+def test_commit_span_plus_distribution(crop):
+    # plus distribution: an inner generate ⋈[input] whose input and generated tokens
+    # are committed as a span is found by a later query that uses (input ‖ output) as a ⊕
+    # fragment — the F-chain digests of those tokens (oracle hashing) point at the inner plan's
+    # own blocks, which survive its release as cached blocks. crop drops the trailing partial
+    # block: the committed fragment is the full blocks only.
+    bs = 16
+    sh = inputs.Shape(hq=2, hkv=1, d=64, block_size=bs)
+    ctx = spanq.Context(sh, 256, device=-1)
+    g = np.random.default_rng(9)
+    inp, gen = g.integers(0, 500, 40).astype(np.int32), g.integers(0, 500, 30).astype(np.int32)
+    inner = inputs.SpanQuery(np.zeros(0, np.int32), [], inp)
+    p = ctx.plan([inner])
+    v = p.view()
+    cross_blocks = list(v["blocks"])
+    p.decode_reserve(32)
+    n = p.commit_span(0, gen, crop=crop)
+    span = np.concatenate([inp, gen])
+    assert n == (len(span) // bs * bs if crop else len(span))
+    root = Store(16, 2, 1, 64, bs).root
+    dig = hashing.fragment_chain(span[:n], bs, root)
+    ids = ctx.lookup(np.frombuffer(b"".join(dig), np.uint8))
+    assert (ids >= 0).all() and len(set(ids.tolist())) == len(ids)
+    assert ids[:len(cross_blocks)].tolist() == cross_blocks  # the input's own blocks, in order
+    p.release()
+    assert (ctx.lookup(np.frombuffer(b"".join(dig), np.uint8)) == ids).all()  # cached, not freed
+    outer = inputs.SpanQuery(g.integers(0, 500, 8).astype(np.int32), [span[:n]], g.integers(0, 500, 5).astype(np.int32))
+    ov = ctx.plan([outer]).view()
+    frag = [i for i, k in enumerate(ov["seg_kind"]) if k == 1][0]
+    assert ov["seg_hit"][frag] == 1 and ov["n_jobs"] == 1  # only the outer prefix is prefilled
+    if crop:  # the uncropped span misses (its trailing partial block was never committed)
+        o2 = ctx.plan([inputs.SpanQuery(outer.prefix, [span], outer.cross)]).view()
+        assert o2["seg_hit"][[i for i, k in enumerate(o2["seg_kind"]) if k == 1][0]] == 0
+
+
+def test_decode_reserve_and_commit_errors():
+    ctx = spanq.Context(inputs.Shape(hq=2, hkv=1, d=64, block_size=16), 64, device=-1)
+    q = inputs.c1().queries[0]  # has fragments: its cross is not at span-local positions
+    p = ctx.plan([inputs.SpanQuery(q.prefix, q.fragments, q.cross)])
+    with pytest.raises(spanq.SpanqError) as e:
+        p.decode_reserve(0)
+    assert e.value.status == spanq.EINVAL
+    p.decode_reserve(4)
+    with pytest.raises(spanq.SpanqError) as e:
+        p.decode_reserve(4)
+    assert e.value.status == spanq.ESTATE
+    with pytest.raises(spanq.SpanqError) as e:
+        p.commit_span(0, [1, 2])
+    assert e.value.status == spanq.EINVAL
+    with pytest.raises(spanq.SpanqError) as e:
+        p.decode_step(0, 0, None, None, None, None)
+    assert e.value.status == spanq.ESTATE  # host-only ctx
+    with pytest.raises(spanq.SpanqError) as e:  # more than reserved
+        ctx.plan([inputs.SpanQuery(np.zeros(0, np.int32), [], q.cross)]).commit_span(0, [1] * 9)
+    assert e.value.status == spanq.ESTATE

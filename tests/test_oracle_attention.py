@@ -325,3 +325,21 @@ def test_workload_shapes():
     kept = sum(any(np.array_equal(f, g) for g in w3.warmup_queries[0].fragments)
                for f in w3.queries[0].fragments)
     assert kept == 12
+
+
+def test_decode_row_is_the_last_row_of_the_extended_query():
+    from oracle import attention as oatt
+    # decode_row (generated token t) == the plain definition's last row of the query whose
+    # ordered cross segment is cross ‖ gen[0..t] (dense masked attention, written out)
+    from paper_2511_02749_b200 import inputs
+
+    sh = inputs.Shape(hq=4, hkv=2, d=16, block_size=4, vocab=64, dtype="fp32")
+    eq, ek, ev = inputs.layer_tables(sh, 0, 77)
+    g = np.random.default_rng(5)
+    prefix, frags, cross = g.integers(0, 64, 5), [g.integers(0, 64, 7), g.integers(0, 64, 3)], g.integers(0, 64, 4)
+    gen = g.integers(0, 64, 6)
+    for t in range(len(gen)):
+        o, lse = oatt.decode_row(prefix, frags, cross, gen, t, eq, ek, ev, sh.rope_base)
+        do, dl, _ = oatt.dense_masked(prefix, frags, np.concatenate([cross, gen[: t + 1]]), eq, ek, ev, sh.rope_base)
+        np.testing.assert_allclose(o[0], do[-1], atol=1e-12)
+        np.testing.assert_allclose(lse[0], dl[-1], atol=1e-12)
