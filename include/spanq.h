@@ -239,6 +239,39 @@ spq_status spq_decode_step(spq_ctx *ctx, spq_plan *plan, int32_t layer, int32_t 
 spq_status spq_commit_span(spq_ctx *ctx, spq_plan *plan, int32_t query, const int32_t *gen_tokens /*host*/,
                            int32_t n_gen, int32_t crop, int32_t *n_committed /*or NULL*/);
 
+/* Plus distribution for an inner generate whose output feeds a later span (the k-ary judge
+ * reduction, §6): commit only the n_gen generated tokens of `query` as a
+ * cached fragment. They sit at positions N_q + t; their K is re-encoded to the span-local
+ * positions t (CIDRA / ReRoPE by -N_q, in place on every layer, on `stream`)
+ * and their blocks are indexed under the fragment chain of gen_tokens (host). Needs block
+ * alignment: the cross length must be a multiple of block_size (SPQ_EINVAL
+ * otherwise). Ends the query's generation (its KV has moved). The decode steps 0..n_gen-1 of
+ * every layer must precede on `stream`. SPQ_ESTATE: no reservation covering n_gen, released plan,
+ * host-only ctx. */
+spq_status spq_commit_output(spq_ctx *ctx, spq_plan *plan, int32_t query, const int32_t *gen_tokens /*host*/,
+                             int32_t n_gen, void *stream, int32_t *n_committed /*or NULL*/);
+
+/* The k-ary judge reduction (§6, Fig. 13 "3 2-way judge steps"; SPEC
+ * reduce_for_attention) as a schedule: items 0..n-1 are the candidates, judge j is item n + j.
+ * Each ply groups its items k at a time, in order, under one judge; a lone last item passes up
+ * unjudged (reading R33); plies repeat until one item remains (n <= k: one judge over all n).
+ * Judges are numbered ply by ply: ply p = judges [ply_off[p], ply_off[p+1]), judge j reads items
+ * children[child_off[j] .. child_off[j+1]). Host only. SPQ_EINVAL: n < 1, k < 2, or a capacity
+ * too small (*n_plies / *n_judges still report the sizes: ply_off needs n_plies + 1 entries,
+ * child_off n_judges + 1, children <= n + n_judges). */
+spq_status spq_reduce_tree(int32_t n, int32_t k, int32_t *ply_off, int64_t ply_cap, int32_t *child_off,
+                           int32_t *children, int64_t judge_cap, int32_t *n_plies, int32_t *n_judges);
+
+/* Bulk execution order (§5.8: "a greedy heuristic that clusters the requests in a
+ * given bulk to increase temporal locality"), reading R34: a query's cached units are its
+ * fragments (s_last digests) and its whole prefix (h_last); the pool is taken to hold the last
+ * W queries' units, W = window_blocks (0: the ctx's capacity) / the bulk's mean blocks per
+ * query; starting from query 0, repeatedly schedule the unscheduled query sharing the most units
+ * with those W (ties: lowest index). order: host [n], a permutation of 0..n-1. Host only; the
+ * store is not touched. SPQ_EINVAL: invalid tree, null argument. */
+spq_status spq_bulk_order(const spq_ctx *ctx, const spq_query *queries, int32_t n, int64_t window_blocks,
+                          int32_t *order);
+
 /* Stream-ordered release: unpins the plan's blocks and frees its plan-private blocks; later
  * kernel calls on any stream wait for `stream` to pass this point before touching them. The
  * handle stays reserved (emptied) for the next 1024 releases of the ctx: any call on it in that

@@ -1317,27 +1317,16 @@ spq_status spq_cidra_schedule(const spq_ctx* c, const int32_t* src, const int32_
   return SPQ_OK;
 }
 
-spq_status spq_reposition(spq_ctx* c, const int32_t* src, const int32_t* dst, const int32_t* delta, int64_t n,
-                          int32_t layer_begin, int32_t layer_end, void* stream, spq_cidra_stats* stats) {
-  spq::CidraSchedule sch;
-  spq_status s = cidra_plan(c, src, dst, delta, n, &sch, stats);
-  if (s != SPQ_OK) return s;
-  if (!is_gpu(c)) return fail(SPQ_ESTATE, "host-only ctx (device < 0) has no pool");
-  if (layer_begin < 0 || layer_end > c->cfg.num_layers || layer_begin > layer_end)
-    return fail(SPQ_ESTATE, "layer range out of bounds");
-  if (c->cfg.head_dim != 64 && c->cfg.head_dim != 128) return fail(SPQ_EINVAL, "head_dim must be 64 or 128");
+namespace {
+// Run a CIDRA schedule on the ctx's pools for layers [lb, le) (K8), stream-ordered.
+spq_status cidra_run(spq_ctx* c, const spq::CidraSchedule& sch, int32_t layer_begin, int32_t layer_end, void* stream) {
   const int64_t n_comp = static_cast<int64_t>(sch.comp_off.size()) - 1;
   if (n_comp == 0 || layer_begin == layer_end) return SPQ_OK;
   if (n_comp > INT32_MAX || static_cast<int64_t>(layer_end - layer_begin) * c->cfg.num_kv_heads > 65535)
     return fail(SPQ_EINVAL, "too many components or layers x kv heads for one launch");
-  // blocks a live plan reads or writes must not move under it
-  for (int64_t i = 0; i < n; ++i)
-    if (c->store->is_pinned(src[i]) || c->store->is_pinned(dst[i]))
-      return fail(SPQ_ESTATE, "block " + std::to_string(c->store->is_pinned(src[i]) ? src[i] : dst[i]) +
-                                  " is pinned by a live plan");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   CUDA_TRY(cudaSetDevice(c->cfg.device));
-  s = wait_pending(c, st);
+  spq_status s = wait_pending(c, st);
   if (s != SPQ_OK) return s;
   // one stream-ordered device buffer: ops then component offsets (pageable H2D: staged before return)
   const size_t ob = sch.ops.size() * sizeof(spq::CidraOp), cb = sch.comp_off.size() * sizeof(int32_t);
@@ -1364,9 +1353,173 @@ spq_status spq_reposition(spq_ctx* c, const int32_t* src, const int32_t* dst, co
   if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("cidra launch: ") + cudaGetErrorString(e));
   c->launches++;
   CUDA_TRY(cudaFreeAsync(buf, st));
+  return SPQ_OK;
+}
+}  // namespace
+
+spq_status spq_reposition(spq_ctx* c, const int32_t* src, const int32_t* dst, const int32_t* delta, int64_t n,
+                          int32_t layer_begin, int32_t layer_end, void* stream, spq_cidra_stats* stats) {
+  spq::CidraSchedule sch;
+  spq_status s = cidra_plan(c, src, dst, delta, n, &sch, stats);
+  if (s != SPQ_OK) return s;
+  if (!is_gpu(c)) return fail(SPQ_ESTATE, "host-only ctx (device < 0) has no pool");
+  if (layer_begin < 0 || layer_end > c->cfg.num_layers || layer_begin > layer_end)
+    return fail(SPQ_ESTATE, "layer range out of bounds");
+  if (c->cfg.head_dim != 64 && c->cfg.head_dim != 128) return fail(SPQ_EINVAL, "head_dim must be 64 or 128");
+  // blocks a live plan reads or writes must not move under it
+  for (int64_t i = 0; i < n; ++i)
+    if (c->store->is_pinned(src[i]) || c->store->is_pinned(dst[i]))
+      return fail(SPQ_ESTATE, "block " + std::to_string(c->store->is_pinned(src[i]) ? src[i] : dst[i]) +
+                                  " is pinned by a live plan");
+  s = cidra_run(c, sch, layer_begin, layer_end, stream);
+  if (s != SPQ_OK) return s;
   // a destination now holds other KV than its digest names: the store forgets it (no later plan
   // may hit it); the caller owns the moved content from here on
   for (int64_t i = 0; i < n; ++i) c->store->drop(dst[i]);
+  return SPQ_OK;
+}
+
+spq_status spq_commit_output(spq_ctx* c, spq_plan* p, int32_t query, const int32_t* gen_tokens, int32_t n_gen,
+                             void* stream, int32_t* n_committed) {
+  if (c == nullptr || p == nullptr || (n_gen > 0 && gen_tokens == nullptr)) return fail(SPQ_EINVAL, "null argument");
+  if (!c->live.count(p)) return fail(SPQ_ESTATE, "plan used after release (or not a plan of this ctx)");
+  if (!is_gpu(c)) return fail(SPQ_ESTATE, "host-only ctx (device < 0) has no pool");
+  const spq::PlanHost& H = p->host;
+  const Decode& D = p->dec;
+  int64_t row = -1;
+  for (size_t b = 0; b < D.rows.size(); ++b)
+    if (D.rows[b] == query) row = static_cast<int64_t>(b);
+  if (row < 0 || n_gen < 1 || n_gen > D.max_new)
+    return fail(SPQ_ESTATE, "query has no reserved generation range holding n_gen tokens");
+  const int bs = c->cfg.block_size;
+  int32_t C = 0, pos0 = 0;
+  for (const spq::Segment& sg : H.segs)
+    if (sg.query == query && sg.kind == spq::kCross) {
+      C = sg.tok_len;
+      pos0 = sg.pos0;
+    }
+  if (C % bs != 0)
+    return fail(SPQ_EINVAL, "the generated tokens must start a block: cross length a multiple of block_size "
+                            "(block alignment, P:565-568)");
+  for (int32_t i = 0; i < n_gen; ++i)
+    if (gen_tokens[i] < 0) return fail(SPQ_EINVAL, "negative token");
+  // the output's blocks: generated token t sits at N_q + t; re-encode its K to position t (ReRoPE
+  // by -N_q, in place: CIDRA self-moves) on every layer, then index it under its fragment chain
+  const std::vector<int32_t>& bl = D.blocks[row];
+  const int32_t b0 = C / bs, b1 = (C + n_gen + bs - 1) / bs;
+  std::vector<int32_t> ids(bl.begin() + b0, bl.begin() + b1), dl(ids.size(), -(pos0 + C));
+  spq::CidraSchedule sch;
+  spq_status s = cidra_plan(c, ids.data(), ids.data(), dl.data(), static_cast<int64_t>(ids.size()), &sch, nullptr);
+  if (s != SPQ_OK) return s;
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  s = wait_pending(c, static_cast<cudaStream_t>(stream));
+  if (s != SPQ_OK) return s;
+  s = cidra_run(c, sch, 0, c->cfg.num_layers, stream);
+  if (s != SPQ_OK) return s;
+  std::vector<spq::Digest> dig;
+  spq::chain('F', c->store->root(), gen_tokens, n_gen, bs, &dig);
+  std::vector<int32_t> ntok(dig.size());
+  for (size_t i = 0; i < dig.size(); ++i) ntok[i] = std::min<int32_t>(bs, n_gen - static_cast<int32_t>(i) * bs);
+  c->store->commit(&p->host, ids.data(), dig.data(), ntok.data(), static_cast<int64_t>(dig.size()));
+  if (n_committed) *n_committed = n_gen;
+  return SPQ_OK;
+}
+
+spq_status spq_bulk_order(const spq_ctx* c, const spq_query* queries, int32_t n, int64_t window_blocks,
+                          int32_t* order) {
+  if (c == nullptr || order == nullptr || (n > 0 && queries == nullptr)) return fail(SPQ_EINVAL, "null argument");
+  if (n < 0) return fail(SPQ_EINVAL, "negative query count");
+  const int bs = c->cfg.block_size;
+  const spq::Digest& root = c->store->root();
+  // per query: its set of cached units — each fragment's identity (s_last) and its whole prefix
+  // (h_last) — and its block count
+  std::vector<std::vector<spq::Digest>> units(n);
+  int64_t blocks_total = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    spq::FlatQuery fq;
+    std::string err;
+    if (!spq::normalize_tree(queries[i], &fq, &err)) return fail(SPQ_EINVAL, "query " + std::to_string(i) + ": " + err);
+    std::vector<spq::Digest> tmp;
+    if (!fq.prefix.empty()) {
+      spq::chain('P', root, fq.prefix.data(), static_cast<int64_t>(fq.prefix.size()), bs, &tmp);
+      units[i].push_back(tmp.back());
+      blocks_total += static_cast<int64_t>(tmp.size());
+    }
+    for (const auto& f : fq.frags) {
+      tmp.clear();
+      spq::chain('F', root, f.data(), static_cast<int64_t>(f.size()), bs, &tmp);
+      units[i].push_back(tmp.back());
+      blocks_total += static_cast<int64_t>(tmp.size());
+    }
+    std::sort(units[i].begin(), units[i].end(), [](const spq::Digest& a, const spq::Digest& b) {
+      return std::memcmp(a.b, b.b, 16) < 0;
+    });
+    units[i].erase(std::unique(units[i].begin(), units[i].end()), units[i].end());
+  }
+  // window: how many recent queries' blocks the pool holds (reading R34)
+  const int64_t cap = window_blocks > 0 ? window_blocks : c->cfg.num_blocks;
+  const int64_t per_q = n > 0 ? std::max<int64_t>(1, blocks_total / n) : 1;
+  const int64_t win = std::max<int64_t>(1, cap / per_q);
+  std::vector<uint8_t> done(n, 0);
+  std::unordered_map<spq::Digest, int32_t, spq::DigestHash> recent;  // unit -> count in window
+  std::vector<int32_t> out;
+  for (int32_t step = 0; step < n; ++step) {
+    int32_t best = -1;
+    int64_t best_ov = -1;
+    for (int32_t i = 0; i < n; ++i) {
+      if (done[i]) continue;
+      int64_t ov = 0;
+      for (const spq::Digest& d : units[i]) ov += recent.count(d) ? 1 : 0;
+      if (ov > best_ov) {  // ties: lowest index (arrival order)
+        best_ov = ov;
+        best = i;
+      }
+    }
+    done[best] = 1;
+    out.push_back(best);
+    for (const spq::Digest& d : units[best]) recent[d]++;
+    if (static_cast<int64_t>(out.size()) > win) {  // slide: forget the query leaving the window
+      for (const spq::Digest& d : units[out[out.size() - 1 - win]]) {
+        auto it = recent.find(d);
+        if (--it->second == 0) recent.erase(it);
+      }
+    }
+  }
+  std::memcpy(order, out.data(), out.size() * sizeof(int32_t));
+  return SPQ_OK;
+}
+
+spq_status spq_reduce_tree(int32_t n, int32_t k, int32_t* ply_off, int64_t ply_cap, int32_t* child_off,
+                           int32_t* children, int64_t judge_cap, int32_t* n_plies, int32_t* n_judges) {
+  if (n_plies == nullptr || n_judges == nullptr) return fail(SPQ_EINVAL, "null argument");
+  if (n < 1 || k < 2) return fail(SPQ_EINVAL, "need n >= 1 candidates and branching factor k >= 2");
+  std::vector<int32_t> po{0}, co{0}, ch;
+  std::vector<int32_t> level(n);
+  for (int32_t i = 0; i < n; ++i) level[i] = i;  // items of the current ply: candidates 0..n-1
+  int32_t next_id = n;
+  do {  // n <= k: one judge over every candidate (the query unchanged)
+    std::vector<int32_t> up;
+    for (size_t g = 0; g < level.size(); g += static_cast<size_t>(k)) {
+      const size_t e = std::min(level.size(), g + static_cast<size_t>(k));
+      if (e - g == 1 && level.size() > 1) {  // a lone item passes up unjudged (reading R33)
+        up.push_back(level[g]);
+        continue;
+      }
+      ch.insert(ch.end(), level.begin() + static_cast<std::ptrdiff_t>(g), level.begin() + static_cast<std::ptrdiff_t>(e));
+      co.push_back(static_cast<int32_t>(ch.size()));
+      up.push_back(next_id++);
+    }
+    po.push_back(static_cast<int32_t>(co.size()) - 1);
+    level.swap(up);
+  } while (level.size() > 1);
+  *n_plies = static_cast<int32_t>(po.size()) - 1;
+  *n_judges = static_cast<int32_t>(co.size()) - 1;
+  if (ply_cap < static_cast<int64_t>(po.size()) || judge_cap < static_cast<int64_t>(co.size()) ||
+      ply_off == nullptr || child_off == nullptr || children == nullptr)
+    return fail(SPQ_EINVAL, "capacity too small (n_plies / n_judges report the sizes)");
+  std::memcpy(ply_off, po.data(), po.size() * sizeof(int32_t));
+  std::memcpy(child_off, co.data(), co.size() * sizeof(int32_t));
+  std::memcpy(children, ch.data(), ch.size() * sizeof(int32_t));
   return SPQ_OK;
 }
 

@@ -128,6 +128,10 @@ SIGNATURES = {
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "spq_commit_span": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32,
                                   _I32P]),
+    "spq_commit_output": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, _I32P]),
+    "spq_reduce_tree": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
+                                  _I32P, _I32P]),
+    "spq_bulk_order": (C.c_int, [C.c_void_p, C.POINTER(spq_query), C.c_int32, C.c_int64, C.c_void_p]),
     "spq_set_option": (C.c_int, [C.c_void_p, C.c_int32, C.c_double]),
     "spq_set_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
 }
@@ -297,6 +301,14 @@ class Plan:
                                      len(g), 1 if crop else 0, C.byref(n)))
         return n.value
 
+    def commit_output(self, query: int, gen_tokens, stream=None) -> int:
+        """Commit only the query's generated tokens as a span (K re-encoded to 0.. by CIDRA)."""
+        g = np.ascontiguousarray(gen_tokens, dtype=np.int32)
+        n = C.c_int32()
+        _check(lib().spq_commit_output(self.ctx.handle, self.handle, int(query), g.ctypes.data, len(g),
+                                       _stream_ptr(stream, self.ctx.device), C.byref(n)))
+        return n.value
+
     def release(self, stream=None):
         if not self.released:
             _check(lib().spq_plan_release(self.ctx.handle, self.handle, _stream_ptr(stream, self.ctx.device)))
@@ -430,6 +442,14 @@ class Context:
     def evict_all(self):
         _check(lib().spq_evict_all(self.handle))
 
+    def bulk_order(self, queries: Sequence, window_blocks: int = 0) -> np.ndarray:
+        """spq_bulk_order: the greedy locality order of a bulk of queries (a permutation)."""
+        bufs = [to_query(q) for q in queries]
+        arr = (spq_query * max(1, len(bufs)))(*[b.q for b in bufs])
+        order = np.zeros(len(bufs), np.int32)
+        _check(lib().spq_bulk_order(self.handle, arr, len(bufs), int(window_blocks), order.ctypes.data))
+        return order
+
     def set_option(self, key: int, value: float):
         """spq_set_option (OPT_EXP2, OPT_RESCALE_THRESHOLD, OPT_PDL, OPT_HASH_SCALAR)."""
         _check(lib().spq_set_option(self.handle, int(key), float(value)))
@@ -450,3 +470,17 @@ class Context:
         a, b = C.c_float(), C.c_float()
         _check(lib().spq_last_attn_ms(self.handle, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+
+def reduce_tree(n: int, k: int):
+    """spq_reduce_tree: the k-ary judge reduction schedule. Returns (plies, children) where
+    plies[p] = the judge ids of ply p (judge j is item n + j) and children[j] = the items judge j
+    reads (candidates 0..n-1, judges n..)."""
+    np_, nj = C.c_int32(), C.c_int32()
+    cap = 2 * n + 8
+    po, co, ch = np.zeros(cap, np.int32), np.zeros(cap, np.int32), np.zeros(2 * cap, np.int32)
+    _check(lib().spq_reduce_tree(int(n), int(k), po.ctypes.data, cap, co.ctypes.data, ch.ctypes.data, cap,
+                                 C.byref(np_), C.byref(nj)))
+    plies = [list(range(po[p], po[p + 1])) for p in range(np_.value)]
+    children = [ch[co[j]:co[j + 1]].tolist() for j in range(nj.value)]
+    return plies, children
