@@ -429,6 +429,11 @@ def main():
     elif not args.no_c5:
         with torch.cuda.stream(stream):
             line["c5"] = measure_c5(dev, stream, args)
+    if world == 1 and not args.no_locality:
+        with torch.cuda.stream(stream):
+            line["decode"] = measure_decode(dev, stream, args)
+            line["judge_tree"] = measure_judge_tree(dev, stream, args)
+            line["bulk"] = measure_bulk(dev, stream, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
     if rank == 0:
@@ -472,6 +477,139 @@ def measure_judge(dev, stream, flush, args, reps: int = 5):
             "dense_over_cold": dense_ms / cold_ms, "dense_over_warm": dense_ms / warm_ms,
             "prefill_kernel_ms": pre_ms, "prefill_kernel_tflops": pre_fl / (pre_ms / 1e3) / 1e12,
             "join_kernel_ms": join_ms, "join_kernel_tflops": join_fl / (join_ms / 1e3) / 1e12}
+
+
+def measure_decode(dev, stream, args, n_gen: int = 64):
+    """Decode after the join (f3, K9): the C2 query (one layer) generates n_gen tokens; each step
+    = K1 of the new token + decode attention over [prefix | 16 fragments at Δ_f | cross + gen]
+    + combine. Also a batch of 8 C2-shaped queries decoding together. HBM-bound: bytes per step
+    = K + V of every visible key (the kernel's algorithmic traffic)."""
+    import torch
+
+    from paper_2511_02749_b200 import inputs, runner, spanq
+
+    _, _, hbm, _ = peaks()
+    out = {}
+    for name, seeds in (("c2", [2]), ("c2_batch8", list(range(20, 28)))):
+        qs = [inputs.c2(seed=sd).queries[0] for sd in seeds]
+        s = inputs.Shape(**{**inputs.c2().shape.__dict__, "layers": 1})
+        ctx = spanq.Context(s, 400 * len(qs) + 64, device=dev.index or 0, max_position=1 << 15, out_dtype=args.out_dtype)
+        tab = runner.device_tables(s, 0, 2, dev)
+        res = runner.run_pass(ctx, qs, [tab], dev, stream=stream)
+        plan = res.plan
+        plan.decode_reserve(n_gen)
+        g = np.random.default_rng(5)
+        odt = torch.float32 if args.out_dtype == "fp32" else torch.bfloat16
+        ins = [runner.gather(tab, g.integers(0, s.vocab, len(qs)), dev) for _ in range(n_gen)]
+        o = torch.empty((len(qs), s.hq, s.d), dtype=odt, device=dev)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_gen)]
+        n0 = ctx.launch_count()
+        stream.synchronize()
+        for t in range(n_gen):
+            ev[t][0].record(stream)
+            plan.decode_step(0, t, *ins[t], o, stream=stream)
+            ev[t][1].record(stream)
+        stream.synchronize()
+        ms = [a.elapsed_time(b) for a, b in ev]
+        ctx_tokens = [q.n_tokens for q in qs]
+        t_mid = n_gen // 2
+        nbytes = sum(2 * (nt + t_mid + 1) * s.hkv * s.d * 2 for nt in ctx_tokens)
+        med = statistics.median(ms[4:])
+        out[name] = {"queries": len(qs), "context_tokens": int(np.mean(ctx_tokens)), "steps": n_gen,
+                     "step_ms_p50": med, "step_ms_p99": float(np.percentile(ms[4:], 99)),
+                     "kv_bytes_per_step": nbytes, "achieved_gbs": nbytes / (med / 1e3) / 1e9,
+                     "peak_gbs": hbm, "frac": nbytes / (med / 1e3) / 1e9 / hbm,
+                     "launches_per_step": (ctx.launch_count() - n0) / n_gen}
+        plan.release(stream=stream)
+        ctx.close()
+    out["note"] = ("per step: K1 of the new tokens + K9 split-KV decode + combine, one layer; bytes = K and V "
+                   "of every visible key (HBM-bound)")
+    return out
+
+
+def measure_judge_tree(dev, stream, args, gen_len: int = 64):
+    """f4 on configs[3]'s shape (C4: 2B GQA d 64, 8 candidates x 2048, 512-token judge prompt),
+    candidates resident (as after generating them): (a) one 8-way judge — join over all 8 + gen_len
+    generated tokens; (b) the 2-way reduction of PAPER §6 Fig. 13 — 3 plies (4 + 2 + 1 judges),
+    each judge a join over its 2 children + gen_len tokens, outputs committed as spans for the next
+    ply. Device time of the whole orchestration (host planning included: it is on the critical
+    path), per ply; and keys each final judge attends (attention locality)."""
+    import torch
+
+    from paper_2511_02749_b200 import inputs, judge, runner, spanq
+
+    w = inputs.c4()
+    s = inputs.Shape(**{**w.shape.__dict__, "layers": 1})
+    q = w.queries[0]
+    cands, prompt = list(q.fragments), q.cross
+    g = np.random.default_rng(8)
+    gen_ids = g.integers(0, s.vocab, (64, gen_len))
+    tab = runner.device_tables(s, 0, w.seed, dev)
+    res = {}
+    for name, k in (("single_8way", 8), ("reduce_2way", 2)):
+        ctx = spanq.Context(s, 2048, device=dev.index or 0, max_position=1 << 15, out_dtype=args.out_dtype)
+        warm = inputs.SpanQuery(np.zeros(0, np.int32), cands, prompt[:1])  # candidates resident
+        runner.run_pass(ctx, [warm], [tab], dev, stream=stream, release=True)
+        stream.synchronize()
+        marks = []
+
+        def on_ply(ply):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            marks.append(e)
+
+        t0 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        out = judge.run_judge_tree(ctx, cands, np.zeros(0, np.int32), prompt, k, gen_len, [tab], dev,
+                                   lambda j, t: int(gen_ids[j, t]), stream=stream, on_ply=on_ply)
+        stream.synchronize()
+        ply_ms = [t0.elapsed_time(marks[0])] + [marks[i - 1].elapsed_time(marks[i]) for i in range(1, len(marks))]
+        final_keys = sum(len(cands[c]) if c < len(cands) else gen_len for c in out["children"][-1]) + len(prompt)
+        res[name] = {"plies": len(out["plies"]), "judges": len(out["children"]), "total_ms": sum(ply_ms),
+                     "ply_ms": ply_ms, "final_judge_keys": final_keys}
+        ctx.close()
+    res["workload"] = ("C4 shape (configs[3]): 8 resident candidates x 2048 + 512-token judge prompt, 2B GQA d 64, "
+                       f"one layer, {gen_len} generated tokens per judge")
+    res["note"] = "PAPER §6: the reduction is for attention locality (accuracy); times are context"
+    return res
+
+
+def measure_bulk(dev, stream, args):
+    """P:763 bulk scheduling under capacity pressure: the scaled configs[4] batch (C5_PARAMS, 50%
+    cross-query overlap) served one plan per query with the KV pool at ~1/3 of the batch's unique
+    working set; arrival order vs spq_bulk_order (greedy locality clustering). One layer."""
+    import torch
+
+    from paper_2511_02749_b200 import inputs, runner, spanq
+
+    w = inputs.c5(**C5_PARAMS)
+    s = inputs.Shape(**{**w.shape.__dict__, "layers": 1})
+    uniq = {bytes(f.tobytes()) for q in w.queries for f in q.fragments}
+    work_blocks = len(uniq) * C5_PARAMS["frag_len"] // s.block_size
+    per_q = (C5_PARAMS["n_frag"] * C5_PARAMS["frag_len"] + C5_PARAMS["n_prefix"] + C5_PARAMS["n_cross"]) // s.block_size
+    nblk = max(work_blocks // 3, 3 * per_q)
+    tab = runner.device_tables(s, 0, w.seed, dev)
+    out = {}
+    for name in ("arrival", "clustered"):
+        ctx = spanq.Context(s, nblk, device=dev.index or 0, max_position=1 << 15, out_dtype=args.out_dtype)
+        order = list(range(len(w.queries))) if name == "arrival" else ctx.bulk_order(w.queries).tolist()
+        stream.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in order:
+            runner.run_pass(ctx, [w.queries[i]], [tab], dev, stream=stream, release=True)
+        b.record(stream)
+        stream.synchronize()
+        st = ctx.stats()
+        out[name] = {"makespan_ms": a.elapsed_time(b), "hit_rate": st["hit_tokens"] / max(1, st["input_tokens"]),
+                     "evictions": st["evictions"]}
+        ctx.close()
+    out["workload"] = ("C5 scaled (%(n_queries)d queries x %(n_frag)d x %(frag_len)d, %(shared_per_query)d shared "
+                       "from %(pool)d), one layer" % C5_PARAMS)
+    out["kv_pool_blocks"] = nblk
+    out["unique_working_set_blocks"] = work_blocks
+    out["note"] = "makespan includes input staging (gathers) per query; hit rate = hit tokens / input tokens"
+    return out
 
 
 def measure_reposition(ctx, s, stream, flush, n_blocks, hbm_gbs, reps: int = 10):

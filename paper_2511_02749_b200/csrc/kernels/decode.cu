@@ -10,10 +10,11 @@
 // B200 design: HBM-bound (one row per query: per key, g dot products of length d against
 // 2·d·elt bytes of K and V), so CUDA cores, not tensor cores. Split-KV: a CTA = (query, kv head,
 // chunk of <= T KV tiles of 128 keys), 128 threads; the g = Hq/Hkv q heads of the kv head share
-// every K/V tile (loaded once into shared memory with 16-byte vector loads). Per tile: thread =
-// key for the scores (g fp32 accumulators, q rotated once per segment in fp32 from the fp64-built
-// table), one warp per head for the online-softmax max/sum, thread = (head, column slice) for
-// P·V. Chunks write fp32 partials (normalized O, natural-log LSE) merged by K4 (combine.cu) in a
+// every K/V sub-tile of 64 keys, double-buffered in shared memory by cp.async (16-byte, no
+// register round trip). Per sub-tile: thread = (key, half of the heads) for the scores (fp32
+// accumulators, q rotated once per segment in fp32 from the fp64-built table, float4 broadcast
+// reads), one warp per head for the online-softmax max/sum, thread = (head, 4 consecutive
+// columns) for P·V. Chunks write fp32 partials (normalized O, natural-log LSE) merged by K4 (combine.cu) in a
 // fixed order; an unsplit (query, kv head) writes O / LSE directly.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -27,7 +28,6 @@ namespace spq {
 namespace {
 
 constexpr int kThreads = 128;
-constexpr int kTileK = 128;  // keys per KV tile (work.h kTileKeys)
 constexpr int kMaxG = 8;     // q heads per kv head
 
 template <typename T>
@@ -52,22 +52,38 @@ __device__ __forceinline__ void store_out(float* p, float x) {
   *p = x;
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+constexpr int kSub = 64;  // keys per pipelined sub-tile (half a KV tile)
+
 // T: pool / q dtype; TO: output dtype. D: head dim; G: q heads per kv head.
+// Sub-tiles of 64 keys are double-buffered: cp.async (16-byte, no register round trip) loads
+// sub-tile s+1 while s is scored, so a CTA keeps ~34 KB (d = 128, bf16) of K/V in flight.
 template <typename T, typename TO, int D, int G>
 __global__ void __launch_bounds__(kThreads) decode_kernel(const DecodeArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   constexpr int KP = D + 16 / static_cast<int>(sizeof(T));  // padded K row (bank spread)
-  T* Ks = reinterpret_cast<T*>(smem_raw);                     // [kTileK][KP]
-  T* Vs = Ks + kTileK * KP;                                   // [kTileK][D]
-  float* qr = reinterpret_cast<float*>(Vs + kTileK * D);      // [G][D] rotated q (fp32)
-  float* ps = qr + G * D;                                     // [G][kTileK] scores / P
-  float* st = ps + G * kTileK;                                // [G][3] m, l, alpha
+  constexpr int kBufElems = kSub * KP + kSub * D;             // K then V of one sub-tile
+  T* bufs = reinterpret_cast<T*>(smem_raw);                   // [2][kBufElems]
+  float* qr = reinterpret_cast<float*>(bufs + 2 * kBufElems);  // [G][D] rotated q (fp32)
+  float* ps = qr + G * D;                                      // [G][kSub] scores / P
+  float* st = ps + G * kSub;                                   // [G][3] m, l, alpha
   const DecodeItem it = a.items[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int pos = a.pos_base[it.row] + a.step;
   const int h0 = it.kvh * G;
   constexpr int VEC = 16 / sizeof(T);  // elements per 16-byte vector
   constexpr int OUT = (G * D + kThreads - 1) / kThreads;  // P·V outputs per thread
+  constexpr int HPT = (G + 1) / 2;                         // score heads per thread (2 threads per key)
   float acc[OUT];
 #pragma unroll
   for (int e = 0; e < OUT; ++e) acc[e] = 0.f;
@@ -77,13 +93,52 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const DecodeArgs a) {
   }
   const T* qg = static_cast<const T*>(a.q) + (static_cast<int64_t>(it.row) * a.hq + h0) * D;
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));
-  int cur_rot = INT32_MIN;
   const int64_t layer_rows = static_cast<int64_t>(a.layer) * a.nblk * a.hkv * a.bs;
-  for (int t = it.tile_begin; t < it.tile_end; ++t) {
+  // the item's sub-tiles in order: (tile, half); causal tiles of the cross+gen segment end the
+  // list at the row's position (later keys are not generated yet)
+  auto n_vis_of = [&](int t) {
     const KvTile tl = a.tiles[t];
-    const int n_vis = tl.causal ? min(tl.n_valid, pos - tl.key_pos0 + 1) : tl.n_valid;
-    if (n_vis <= 0) continue;  // uniform across the CTA
-    __syncthreads();           // the previous tile's smem is no longer read
+    return tl.causal ? min(tl.n_valid, pos - tl.key_pos0 + 1) : tl.n_valid;
+  };
+  auto issue = [&](int t, int hh, int buf) {  // cp.async of sub-tile (t, hh) into buffer buf
+    const KvTile tl = a.tiles[t];
+    const int nk = min(kSub, n_vis_of(t) - hh * kSub);
+    T* Kb = bufs + buf * kBufElems;
+    T* Vb = Kb + kSub * KP;
+    for (int i = tid; i < nk * (D / VEC); i += kThreads) {
+      const int key = i / (D / VEC), u = i % (D / VEC);
+      const int kk = hh * kSub + key;
+      const int32_t blk = a.tile_blocks[tl.blk_off + kk / a.bs];
+      const int64_t row = layer_rows + (static_cast<int64_t>(blk) * a.hkv + it.kvh) * a.bs + kk % a.bs;
+      cp_async16(Kb + key * KP + u * VEC, static_cast<const T*>(a.k_pool) + row * D + u * VEC);
+      cp_async16(Vb + key * D + u * VEC, static_cast<const T*>(a.v_pool) + row * D + u * VEC);
+    }
+    cp_async_commit();
+  };
+  auto next_sub = [&](int& t, int& hh) {  // advance (t, hh); t = tile_end when done
+    if (hh == 0 && n_vis_of(t) > kSub) {
+      hh = 1;
+      return;
+    }
+    hh = 0;
+    ++t;
+    if (t < it.tile_end && n_vis_of(t) <= 0) t = it.tile_end;
+  };
+  int t = it.tile_begin, hh = 0;
+  if (t < it.tile_end && n_vis_of(t) <= 0) t = it.tile_end;
+  if (t < it.tile_end) issue(t, hh, 0);
+  int cur_rot = INT32_MIN;
+  for (int buf = 0; t < it.tile_end; buf ^= 1) {
+    int t2 = t, hh2 = hh;
+    next_sub(t2, hh2);
+    if (t2 < it.tile_end) {
+      issue(t2, hh2, buf ^ 1);  // the other buffer was released by the previous sub-tile's end sync
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    const KvTile tl = a.tiles[t];
+    const int nk = min(kSub, n_vis_of(t) - hh * kSub);
     if (tl.rot_delta != cur_rot) {  // a new segment: q rotated to pos - Δ (rotate-half pairs)
       cur_rot = tl.rot_delta;
       const int rp = min(max(pos - cur_rot, 0), a.max_pos - 1);
@@ -95,49 +150,54 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const DecodeArgs a) {
         qr[h * D + c + D / 2] = y * cs.x + x * cs.y;
       }
     }
-    // K / V rows [0, n_vis) of the tile -> smem (16-byte vectors, a warp covers whole rows)
-    for (int i = tid; i < n_vis * (D / VEC); i += kThreads) {
-      const int key = i / (D / VEC), u = i % (D / VEC);
-      const int32_t blk = a.tile_blocks[tl.blk_off + key / a.bs];
-      const int64_t row = layer_rows + (static_cast<int64_t>(blk) * a.hkv + it.kvh) * a.bs + key % a.bs;
-      *reinterpret_cast<uint4*>(Ks + key * KP + u * VEC) =
-          *reinterpret_cast<const uint4*>(static_cast<const T*>(a.k_pool) + row * D + u * VEC);
-      *reinterpret_cast<uint4*>(Vs + key * D + u * VEC) =
-          *reinterpret_cast<const uint4*>(static_cast<const T*>(a.v_pool) + row * D + u * VEC);
-    }
-    __syncthreads();
-    // scores: thread = key
-    if (tid < n_vis) {
-      float s[G];
+    __syncthreads();  // this sub-tile's K/V (every thread's cp.async) and q are in smem
+    const T* Kb = bufs + buf * kBufElems;
+    const T* Vb = Kb + kSub * KP;
+    // scores: thread = (key, half of the heads)
+    {
+      const int key = tid % kSub, hs = (tid / kSub) * HPT;
+      if (key < nk && hs < G) {
+        float s[HPT];
 #pragma unroll
-      for (int h = 0; h < G; ++h) s[h] = 0.f;
-#pragma unroll 4
-      for (int c = 0; c < D; c += VEC) {
-        const uint4 kv = *reinterpret_cast<const uint4*>(Ks + tid * KP + c);
-        const T* ke = reinterpret_cast<const T*>(&kv);
+        for (int j = 0; j < HPT; ++j) s[j] = 0.f;
+#pragma unroll 2
+        for (int c = 0; c < D; c += VEC) {
+          const uint4 kv = *reinterpret_cast<const uint4*>(Kb + key * KP + c);
+          const T* ke = reinterpret_cast<const T*>(&kv);
+          float kf[VEC];
 #pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          const float kf = to_f(ke[e]);
+          for (int e = 0; e < VEC; ++e) kf[e] = to_f(ke[e]);
 #pragma unroll
-          for (int h = 0; h < G; ++h) s[h] = fmaf(qr[h * D + c + e], kf, s[h]);
+          for (int j = 0; j < HPT; ++j) {
+            if (hs + j >= G) continue;
+#pragma unroll
+            for (int e = 0; e < VEC; e += 4) {  // q as float4 broadcasts
+              const float4 q4 = *reinterpret_cast<const float4*>(qr + (hs + j) * D + c + e);
+              s[j] = fmaf(q4.x, kf[e], s[j]);
+              s[j] = fmaf(q4.y, kf[e + 1], s[j]);
+              s[j] = fmaf(q4.z, kf[e + 2], s[j]);
+              s[j] = fmaf(q4.w, kf[e + 3], s[j]);
+            }
+          }
         }
-      }
 #pragma unroll
-      for (int h = 0; h < G; ++h) ps[h * kTileK + tid] = s[h] * scale_log2;
+        for (int j = 0; j < HPT; ++j)
+          if (hs + j < G) ps[(hs + j) * kSub + key] = s[j] * scale_log2;
+      }
     }
     __syncthreads();
     // online softmax: one warp per head (heads h, h + 4, ...)
     for (int h = warp; h < G; h += kThreads / 32) {
       float mx = -INFINITY;
-      for (int i = lane; i < n_vis; i += 32) mx = fmaxf(mx, ps[h * kTileK + i]);
+      for (int i = lane; i < nk; i += 32) mx = fmaxf(mx, ps[h * kSub + i]);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       const float m_old = st[h * 3 + 0];
       const float m_new = fmaxf(m_old, mx);
       float sum = 0.f;
-      for (int i = lane; i < n_vis; i += 32) {
-        const float p = exp2f(ps[h * kTileK + i] - m_new);
-        ps[h * kTileK + i] = p;
+      for (int i = lane; i < nk; i += 32) {
+        const float p = exp2f(ps[h * kSub + i] - m_new);
+        ps[h * kSub + i] = p;
         sum += p;
       }
 #pragma unroll
@@ -152,19 +212,36 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const DecodeArgs a) {
     }
     __syncthreads();
     // O = O * alpha + P V: thread = (head, OUT consecutive columns)
+    if (tid * OUT < G * D) {  // OUT consecutive columns of one head (OUT divides D)
+      const int f0 = tid * OUT, h = f0 / D, c0 = f0 % D;
+      const float alpha = st[h * 3 + 2];
 #pragma unroll
-    for (int e = 0; e < OUT; ++e) {
-      const int f = tid * OUT + e;
-      if (f < G * D) {
-        const int h = f / D, c = f % D;
-        float o = acc[e] * st[h * 3 + 2];
-        const float* pr = ps + h * kTileK;
-        for (int i = 0; i < n_vis; ++i) o = fmaf(pr[i], to_f(Vs[i * D + c]), o);
-        acc[e] = o;
+      for (int e = 0; e < OUT; ++e) acc[e] *= alpha;
+      const float* pr = ps + h * kSub;
+#pragma unroll 4
+      for (int i = 0; i < nk; ++i) {
+        const float p = pr[i];
+        if constexpr (OUT % 4 == 0 && sizeof(T) == 2) {
+#pragma unroll
+          for (int e = 0; e < OUT; e += 4) {
+            const uint2 u = *reinterpret_cast<const uint2*>(Vb + i * D + c0 + e);
+            const float2 v01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+            const float2 v23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+            acc[e] = fmaf(p, v01.x, acc[e]);
+            acc[e + 1] = fmaf(p, v01.y, acc[e + 1]);
+            acc[e + 2] = fmaf(p, v23.x, acc[e + 2]);
+            acc[e + 3] = fmaf(p, v23.y, acc[e + 3]);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < OUT; ++e) acc[e] = fmaf(p, to_f(Vb[i * D + c0 + e]), acc[e]);
+        }
       }
     }
+    __syncthreads();  // buffer buf and ps are free for the next sub-tile
+    t = t2;
+    hh = hh2;
   }
-  __syncthreads();
   // normalized O and natural-log LSE: final, or a split partial merged by combine
 #pragma unroll
   for (int e = 0; e < OUT; ++e) {
@@ -191,9 +268,8 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const DecodeArgs a) {
 template <typename T, typename TO, int D, int G>
 cudaError_t launch_g(const DecodeArgs& a, cudaStream_t st) {
   constexpr int KP = D + 16 / static_cast<int>(sizeof(T));
-  const size_t smem = sizeof(T) * (kTileK * KP + kTileK * D) + sizeof(float) * (G * D + G * kTileK + G * 3);
-  static_assert(sizeof(T) * (kTileK * (D + 16 / sizeof(T)) + kTileK * D) + sizeof(float) * (G * D + G * kTileK + G * 3) <= 232448,
-                "decode smem");
+  constexpr size_t smem = sizeof(T) * 2 * (kSub * KP + kSub * D) + sizeof(float) * (G * D + G * kSub + G * 3);
+  static_assert(smem <= 232448, "decode smem");
   cudaError_t e = cudaFuncSetAttribute(decode_kernel<T, TO, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
