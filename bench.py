@@ -206,6 +206,8 @@ def main():
     ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
                     help="c2: one RAG query per rank (weak scaling, default); c5: one shared batch "
                          "partitioned over the ranks with the NCCL fragment-KV exchange (strong scaling)")
+    ap.add_argument("--split-join", action="store_true",
+                    help="c5 workload at N > 1: owner-side split join instead of the fragment-KV exchange")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.layers is None:
@@ -230,7 +232,7 @@ def main():
 
         dist.init_process_group("nccl", device_id=dev)
     if args.workload == "c5":
-        line = run_partitioned(args, rank, world, dev)
+        line = run_partitioned(args, rank, world, dev, split=args.split_join)
         if rank == 0:
             print(json.dumps(line), flush=True)
         if world > 1:
@@ -426,6 +428,7 @@ def main():
         # the §8(e) path on this node: a C5-shaped batch partitioned over the ranks (owner
         # prefill, fragment-KV exchange overlapped with join phase 0)
         line["partitioned"] = run_partitioned(args, rank, world, dev, layers=1)
+        line["partitioned_split"] = run_partitioned(args, rank, world, dev, layers=1, split=True)
     elif not args.no_c5:
         with torch.cuda.stream(stream):
             line["c5"] = measure_c5(dev, stream, args)
@@ -743,7 +746,7 @@ def measure_locality(ctx, s, tab, dev, stream, flush, args, reps: int = 5):
 C5_PARAMS = dict(n_queries=64, n_frag=16, frag_len=1024, pool=64, shared_per_query=8, n_prefix=512, n_cross=256)
 
 
-def run_partitioned(args, rank, world, dev, layers=None):
+def run_partitioned(args, rank, world, dev, layers=None, split=False):
     """configs[4]-shaped batch (scaled to fit one GPU's inputs: C5_PARAMS) with 50% cross-query
     fragment overlap, partitioned over the ranks: query q is homed on q mod W, each
     distinct fragment is prefilled once on its owner rank (u64le(s_last) mod W) and its KV is moved
@@ -762,7 +765,7 @@ def run_partitioned(args, rank, world, dev, layers=None):
     ntok = sum(len(q.prefix) + sum(len(f) for f in q.fragments) + len(q.cross) for q in w.queries)
     nblk = ntok // s.block_size + 4 * len(w.queries) * (C5_PARAMS["n_frag"] + 2) + 1024
     ctx = spanq.Context(s, nblk, device=local, max_position=1 << 15, out_dtype=args.out_dtype,
-                        rank=rank, world_size=world)
+                        rank=rank, world_size=world, split_join=split)
     stream = torch.cuda.Stream(dev)
     tab = runner.device_tables(s, 0, w.seed, dev)
     p0 = ctx.plan(w.queries, stream=stream)
@@ -789,7 +792,25 @@ def run_partitioned(args, rank, world, dev, layers=None):
         for layer in range(L):
             if len(ptok):
                 plan.prefill(layer, qp, kp, vp, op, lp, stream=stream)
-            if world > 1:
+            if world > 1 and split:
+                # owner-side split join (f1): Q rows to the owners, their partials back (comm
+                # stream); the local join overlaps it on the main stream, then the merge
+                comm.wait_stream(stream)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(comm):
+                    e0.record(comm)
+                    st = parallel.split_exchange_layer(
+                        plan, v, layer, s, dev, qj, rank, world, stream=comm,
+                        local_join=(lambda: plan.split_join_local(layer, qj, kj, vj, stream=stream)) if len(jtok) else None)
+                    e1.record(comm)
+                xev[0] = (e0, e1)
+                xbytes[0] = st["q_bytes"] + st["partial_bytes"]
+                stream.wait_stream(comm)
+                st["part_o"].record_stream(stream)
+                st["part_lse"].record_stream(stream)
+                if len(jtok):
+                    plan.split_merge(st["part_o"], st["part_lse"], oj, lj, stream=stream)
+            elif world > 1:
                 # the exchange (comm stream, after this layer's prefill) overlaps join phase 0 over
                 # the segments this rank holds; phase 1 (received fragments + combine) waits for it
                 comm.wait_stream(stream)
@@ -856,7 +877,8 @@ def run_partitioned(args, rank, world, dev, layers=None):
                    "layers": L, "global_batch": len(w.queries), "block_size": s.block_size,
                    "out_dtype": args.out_dtype,
                    "parallelism": f"partitioned over {world} ranks (home q mod W, fragment owner "
-                                  "u64le(s_last) mod W, NCCL all-to-all KV exchange per layer)",
+                                  "u64le(s_last) mod W, " + ("owner-side split join: Q and fp32 partials by "
+                                  "NCCL all-to-all per layer)" if split else "NCCL all-to-all KV exchange per layer)"),
                    "l2": "flushed between steps (256 MB write)"},
         "batch_ttft_ms": total_ms / args.steps,
         "flops_per_step": flops_total, "exchange_bytes_per_layer_rank": xbytes[0],

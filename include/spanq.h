@@ -63,6 +63,10 @@ typedef struct {
                            by u64le(s_last(f)[0:8]) mod W; each rank plans only its share       */
   int32_t out_dtype;    /* spq_dtype of o (attention outputs); SPQ_FP32 is allowed with a bf16
                            ctx (bf16 MMAs, fp32 outputs: removes the final bf16 rounding of O)  */
+  int32_t split_join;   /* world_size > 1: 0 = remote fragments' KV moves to the home rank
+                           (spq_exchange_*), 1 = owner-side split join: the home query's cross Q
+                           moves to the fragment owners and their partial (O, LSE) come back
+                           (spq_split_*)                                       */
 } spq_config;
 
 typedef struct spq_ctx spq_ctx;
@@ -157,6 +161,15 @@ typedef struct {
   const int32_t *send_blocks;
   const int64_t *recv_off;    /* [world_size+1] */
   const int32_t *recv_blocks;
+  /* split_join: the tasks this rank computes for other homes, [n_tasks][6] = {query, home,
+   * n_rows (the query's cross rows), pos0 (global position of cross row 0), seg_begin, seg_end
+   * (its fragment segments owned here, pos0 = Δ_f)}, in (home, query) order; and per peer w the
+   * home queries whose cross Q this rank sends to w and whose partials w returns:
+   * xq_queries[xq_off[w] .. xq_off[w+1]), query order. Empty unless split_join. */
+  int32_t n_tasks;
+  const int32_t *tasks;
+  const int32_t *xq_off;      /* [world_size+1] */
+  const int32_t *xq_queries;
 } spq_plan_view;
 /* Read-only host arrays, valid until spq_plan_release. */
 spq_status spq_plan_view_get(const spq_plan *plan, spq_plan_view *out);
@@ -271,6 +284,35 @@ spq_status spq_reduce_tree(int32_t n, int32_t k, int32_t *ply_off, int64_t ply_c
  * store is not touched. SPQ_EINVAL: invalid tree, null argument. */
 spq_status spq_bulk_order(const spq_ctx *ctx, const spq_query *queries, int32_t n, int64_t window_blocks,
                           int32_t *order);
+
+/* ------------------------------------------------------------------ owner-side split join
+ * (cfg.split_join = 1, world_size > 1; §4.3: independent
+ * sub-trees run in parallel). Per layer, with the transfers done by the caller's collective (one
+ * all-to-all each way, NCCL):
+ *   home:  spq_split_pack_q(q_join -> qsend)         [Q all-to-all]    spq_split_join_local(...)
+ *   owner: spq_split_task_join(qrecv -> partials)    [partial all-to-all]
+ *   home:  spq_split_merge(partials_recv -> o, lse)
+ * Buffer layouts (row = one query row, all Hq heads): qsend = for each owner peer w (rank order),
+ * the rows of the home queries xq_queries[xq_off[w]..) (query order) — [rows][Hq][d], ctx dtype,
+ * pre-RoPE; qrecv = for each home peer h (rank order) the rows of this rank's tasks with home h
+ * (task order = the view's tasks) — the same layout as the tasks' row space; partials:
+ * O [rows][Hq][d] fp32 (normalized) and LSE [rows][Hq] fp32 (natural log), sent back in the same
+ * row order (partials_recv laid out like qsend). All calls: SPQ_ESTATE on a plan that is not a
+ * split-join plan, a released plan or a host-only ctx; SPQ_EINVAL on a null buffer. */
+spq_status spq_split_pack_q(spq_ctx *ctx, spq_plan *plan, const void *q_join /*[join rows][Hq][d]*/,
+                            void *qsend, void *stream);
+/* The tasks' join: each task's query rows attend over its fragments owned here (Q counter-rotated
+ * by Δ_f, the join kernel + combine) -> fp32 partials. */
+spq_status spq_split_task_join(spq_ctx *ctx, spq_plan *plan, int32_t layer, const void *qrecv, float *part_o,
+                               float *part_lse, void *stream);
+/* Home side: rope_kv_write of the cross rows + the join over the segments held here (prefix,
+ * locally owned fragments, cross causal) into a plan-owned fp32 result (overlaps the exchange). */
+spq_status spq_split_join_local(spq_ctx *ctx, spq_plan *plan, int32_t layer, const void *q, const void *k,
+                                const void *v, void *stream);
+/* Home side: o / lse = LSE merge of the local result and the owners' partials, in a fixed order
+ * (local, then owners by rank): every home query row, out dtype. */
+spq_status spq_split_merge(spq_ctx *ctx, spq_plan *plan, const float *part_o_recv, const float *part_lse_recv,
+                           void *o, float *lse, void *stream);
 
 /* Stream-ordered release: unpins the plan's blocks and frees its plan-private blocks; later
  * kernel calls on any stream wait for `stream` to pass this point before touching them. The

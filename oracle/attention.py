@@ -129,6 +129,39 @@ def decode_row(prefix, frags, cross, gen, t: int, eq, ek, ev, base: float,
     return join_rows(prefix, frags, ext, eq, ek, ev, base, rows=[len(cross) + t], heads=heads)
 
 
+def join_rows_subset(prefix, frags, cross, eq, ek, ev, base: float, local: bool, frag_mask: Sequence[bool],
+                     heads: Optional[Sequence[int]] = None):
+    """The join's cross rows restricted to a subset of the key columns — the prefix and cross
+    columns when `local`, fragment f's columns when frag_mask[f] — normalized over that subset:
+    the partial (O, LSE) one rank of an owner-side split join computes."""
+    toks = np.concatenate([np.asarray(prefix, np.int64)] + [np.asarray(f, np.int64) for f in frags]
+                          + [np.asarray(cross, np.int64)])
+    N, C, P = len(toks), len(cross), len(prefix)
+    gpos = (N - C) + np.arange(C)
+    keep = np.zeros(N, bool)
+    keep[:P] = local
+    keep[N - C:] = local
+    off = P
+    for f, m in zip(frags, frag_mask):
+        keep[off:off + len(f)] = m
+        off += len(f)
+    q = rope(_f64(eq[toks[gpos]]), gpos[:, None].astype(np.float64), base)
+    k = rope(_f64(ek[toks]), np.arange(N, dtype=np.float64)[:, None], base)
+    mask = (np.arange(N)[None, :] <= gpos[:, None]) & keep[None, :]
+    return attend(q, k, _f64(ev[toks]), mask, heads)
+
+
+def merge_lse(parts: Sequence[Tuple[np.ndarray, np.ndarray]]) -> Tuple[np.ndarray, np.ndarray]:
+    """Merge partial attention results over disjoint key sets (normalized O_i, natural-log LSE_i):
+    LSE = log Σ_i exp(LSE_i), O = Σ_i exp(LSE_i − LSE) · O_i (written out)."""
+    lses = np.stack([l for _, l in parts])  # [n, rows, heads]
+    m = np.max(lses, axis=0)
+    w = np.exp(lses - m)
+    tot = w.sum(axis=0)
+    o = sum(w[i][..., None] * parts[i][0] for i in range(len(parts))) / tot[..., None]
+    return o, m + np.log(tot)
+
+
 def expected_pages(tokens, eq_unused, ek, ev, base: float, positions) -> Tuple[np.ndarray, np.ndarray]:
     """K/V rows as stored in the pool: RoPE(k, stored position), v unrotated (R15: RoPE on q, k)."""
     t = np.asarray(tokens, np.int64)

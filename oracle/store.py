@@ -73,6 +73,12 @@ class PlanView:
     send: Dict[int, List[int]] = field(default_factory=dict)
     recv: Dict[int, List[int]] = field(default_factory=dict)
     n_join_queries: int = 0
+    # owner-side split join (split=True): tasks this rank computes for other
+    # homes, (home, query) order: (query, home, n_rows, pos0 of the cross rows, first and end
+    # segment index of the query's fragments owned here); per peer owner, the home queries whose
+    # cross Q this rank sends to it and whose partial (O, LSE) comes back (query order)
+    tasks: List[Tuple[int, int, int, int, int, int]] = field(default_factory=list)
+    xq: Dict[int, List[int]] = field(default_factory=dict)
 
 
 class Store:
@@ -131,20 +137,25 @@ class Store:
 
     # -------------------------------------------------------------- planner
     def plan(self, queries: Sequence[Tuple[np.ndarray, List[np.ndarray], np.ndarray]],
-             rank: int = 0, world: int = 1) -> PlanView:
+             rank: int = 0, world: int = 1, split: bool = False) -> PlanView:
         """Plan a batch. With world > 1 this is rank `rank`'s share: query q is
         homed on q mod W (its prefix, join and cross run there), fragment f is owned by
         u64le(s_last[0:8]) mod W (it is prefilled and cached only there); a home rank receives
-        remote-owned fragments into plan-private blocks, in first-occurrence order."""
+        remote-owned fragments into plan-private blocks, in first-occurrence order.
+
+        split=True (owner-side split join; §4.3, parallel
+        sub-trees): no KV moves. An owner keeps each owned fragment's segment at its place in the
+        query (pos0 = Δ_f) and computes the home query's cross rows over its owned fragments as a
+        task; the home rank keeps only its local segments and merges the owners' partials."""
         saved = copy.deepcopy((self.index, self.meta, self.free, self.pins, self.plan_no,
                                self.stats))
         try:
-            return self._plan(queries, rank, world)
+            return self._plan(queries, rank, world, split)
         except OracleENOMEM:
             (self.index, self.meta, self.free, self.pins, self.plan_no, self.stats) = saved
             raise
 
-    def _plan(self, queries, rank: int = 0, world: int = 1) -> PlanView:
+    def _plan(self, queries, rank: int = 0, world: int = 1, split: bool = False) -> PlanView:
         bs = self.bs
         self.plan_no += 1
         p = self.plan_no
@@ -189,6 +200,8 @@ class Store:
         segs: List[Segment] = []
         joins: List[bytes] = []
         n_home = 0
+        tasks: List[Tuple[int, int, int, int, int, int]] = []
+        xq: Dict[int, List[int]] = {}
         for qi, (prefix, frags, cross) in enumerate(queries):
             prefix = np.asarray(prefix)
             cross = np.asarray(cross)
@@ -197,17 +210,26 @@ class Store:
             h = hashing.prefix_chain(prefix, bs, self.root)
             if not is_home:
                 joins.append(bytes(16))  # join digests are per query; zero where homed elsewhere
-                # only the fragments this rank owns: prefill/cache them and send them home
+                # only the fragments this rank owns: prefill/cache them and send them home (split:
+                # keep them at their offset in the query for this rank's task)
+                first = len(segs)
+                off = len(prefix)
                 for fi, f in enumerate(frags):
                     sf = hashing.fragment_chain(f, bs, self.root)
+                    delta = off
+                    off += len(f)
                     if hashing.owner_rank(sf[-1], world) != rank:
                         continue
-                    seg = self._frag_segment(qi, fi, f, sf, 0, touch, pin, insert_new)
+                    seg = self._frag_segment(qi, fi, f, sf, delta if split else 0, touch, pin, insert_new)
                     segs.append(seg)
                     owned_blocks.setdefault(sf[-1], seg.blocks)
+                    if split:
+                        continue
                     lst = send.setdefault(home, [])
                     if sf[-1] not in lst:
                         lst.append(sf[-1])
+                if split and len(segs) > first:
+                    tasks.append((qi, home, len(cross), off, first, len(segs)))
                 continue
             n_home += 1
             self.stats["input_tokens"] += len(prefix) + sum(len(f) for f in frags) + len(cross)
@@ -253,6 +275,11 @@ class Store:
                 if owner == rank:
                     seg = self._frag_segment(qi, fi, f, sf, off, touch, pin, insert_new)
                     owned_blocks.setdefault(sf[-1], seg.blocks)
+                elif split:  # computed by its owner (a task there); this rank merges its partial
+                    if qi not in xq.setdefault(owner, []):
+                        xq[owner].append(qi)
+                    off += len(f)
+                    continue
                 else:
                     # remote-owned: received into plan-private blocks (owner's pages include
                     # its zeroed pads), no prefill here
@@ -314,7 +341,7 @@ class Store:
                         np.asarray(pg, np.int32), np.asarray(jp, np.int32),
                         np.asarray(js, np.int64), np.asarray(jg, np.int32),
                         np.asarray(pad_slots, np.int64), jobs, dict(self.stats), pinned, private,
-                        send_b, recv_b, n_home)
+                        send_b, recv_b, n_home, sorted(tasks, key=lambda t: (t[1], t[0])), xq)
 
     def _frag_segment(self, qi, fi, f, s, off, touch, pin, insert_new) -> Segment:
         """All-or-nothing fragment lookup (R10, R11) with pin-before-alloc (R24)."""

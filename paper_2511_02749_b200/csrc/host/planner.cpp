@@ -303,7 +303,7 @@ int owner_rank(const Digest& d, int world) {
   return static_cast<int>(v % static_cast<uint64_t>(world));
 }
 
-int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* pool, int rank, int world) {
+int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* pool, int rank, int world, bool split) {
   std::vector<QueryDigests> qd;
 #ifdef SPANQ_PROFILING
   static const bool prof = std::getenv("SPANQ_PROFILE") != nullptr;  // profiling builds only
@@ -371,6 +371,7 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
   std::vector<uint8_t> wr;
   std::unordered_map<Digest, std::vector<int32_t>, DigestHash> owned_blocks, recv_blocks;
   std::vector<std::vector<Digest>> send_list(world), recv_list(world);
+  std::vector<std::vector<int32_t>> xq(world);  // split mode: home queries per owner peer
   // all-or-nothing lookup of one locally owned fragment; pins resident blocks before allocating
   auto owned_fragment = [&](int32_t qi, int32_t fi, int32_t flen, int32_t off, const std::vector<Digest>& fd) {
     stats_.lookups++;
@@ -413,14 +414,23 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
     const FlatQuery& q = qs[qi];
     const int home = qi % world;
     if (home != rank) {
-      // only the fragments this rank owns: prefill/cache them, send them to the home rank
+      // only the fragments this rank owns: prefill/cache them, send them to the home rank (split
+      // mode: keep them at their offset Δ_f in the query, for this rank's task)
+      const int32_t first = static_cast<int32_t>(P.segs.size());
+      int32_t off = static_cast<int32_t>(q.prefix.size());
       for (size_t fi = 0; fi < q.frags.size() && ok; ++fi) {
         const std::vector<Digest>& fd = qd[qi].frags[fi];
+        const int32_t delta = off;
+        off += static_cast<int32_t>(q.frags[fi].size());
         if (owner_rank(fd.back(), world) != rank) continue;
-        owned_fragment(qi, static_cast<int32_t>(fi), static_cast<int32_t>(q.frags[fi].size()), 0, fd);
+        owned_fragment(qi, static_cast<int32_t>(fi), static_cast<int32_t>(q.frags[fi].size()), split ? delta : 0, fd);
+        if (split) continue;
         auto& lst = send_list[home];
         if (std::find(lst.begin(), lst.end(), fd.back()) == lst.end()) lst.push_back(fd.back());
       }
+      if (split && ok && static_cast<int32_t>(P.segs.size()) > first)
+        P.tasks.push_back({qi, static_cast<int32_t>(home), static_cast<int32_t>(q.cross.size()), off, first,
+                           static_cast<int32_t>(P.segs.size())});
       continue;
     }
     P.n_join_queries++;
@@ -475,6 +485,8 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
       const int owner = owner_rank(fd.back(), world);
       if (owner == rank) {
         owned_fragment(qi, static_cast<int32_t>(fi), flen, off, fd);
+      } else if (split) {  // computed by its owner (a task there); this rank merges the partial
+        if (xq[owner].empty() || xq[owner].back() != qi) xq[owner].push_back(qi);
       } else {
         auto it = recv_blocks.find(fd.back());
         if (it == recv_blocks.end()) {
@@ -595,6 +607,14 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
       P.recv_blocks.insert(P.recv_blocks.end(), b.begin(), b.end());
     }
     P.recv_off.push_back(static_cast<int64_t>(P.recv_blocks.size()));
+  }
+  std::stable_sort(P.tasks.begin(), P.tasks.end(), [](const PlanHost::Task& a, const PlanHost::Task& b) {
+    return a.home != b.home ? a.home < b.home : a.query < b.query;
+  });
+  P.xq_off.assign(1, 0);
+  for (int w = 0; w < world; ++w) {
+    P.xq_queries.insert(P.xq_queries.end(), xq[w].begin(), xq[w].end());
+    P.xq_off.push_back(static_cast<int32_t>(P.xq_queries.size()));
   }
   // join rows in query order; query_join_row_off is indexed by the global query id (queries
   // homed elsewhere have an empty range)

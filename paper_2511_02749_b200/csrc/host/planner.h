@@ -63,6 +63,16 @@ struct PlanHost {
   // W > 1 fragment exchange: blocks sent to / received from each peer
   std::vector<int64_t> send_off, recv_off;  // [world+1]
   std::vector<int32_t> send_blocks, recv_blocks;
+  // owner-side split join (split mode): tasks this rank computes for other homes
+  // in (home, query) order — the home query's cross rows over the fragments of it owned here
+  // (segments [seg_begin, seg_end), pos0 = Δ_f) — and, per peer owner, the home queries whose
+  // cross Q this rank sends there and whose partials come back (query order)
+  struct Task {
+    int32_t query, home, n_rows, pos0, seg_begin, seg_end;
+  };
+  std::vector<Task> tasks;
+  std::vector<int32_t> xq_off;  // [world+1]
+  std::vector<int32_t> xq_queries;
 };
 
 // Fragment owner rank: u64le(s_last[0:8]) mod W.
@@ -115,7 +125,7 @@ class Store {
   // Plan a batch. Returns 0 on success, 2 on ENOMEM (state rolled back). Block digests do
   // not depend on store state, so they are computed first, in parallel on `pool` if given.
   int plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* pool = nullptr, int rank = 0,
-           int world = 1);
+           int world = 1, bool split = false);
   void release(const PlanHost& p);
   // Undo a committed plan whose device side failed: release it and forget the blocks it inserted
   // (their KV was never written, so their digests must not produce cache hits).

@@ -122,14 +122,40 @@ void build_prefill_work(const PlanHost& p, const WorkOpts& o, int job_begin, int
   if (o.persistent) schedule(cost, o.units, o.num_sms, w);
 }
 
+namespace {
+struct QTile {
+  int32_t row0, n_rows, tb, te;
+  bool force;  // write partials even when one piece covers it (its other phase adds more)
+};
+void finish_join(const std::vector<QTile>& qt, const WorkOpts& o, const JoinPhase* ph, AttnWorkHost* w);
+}  // namespace
+
+void build_task_join_work(const PlanHost& p, const WorkOpts& o, AttnWorkHost* w) {
+  *w = AttnWorkHost();
+  std::vector<QTile> qt;
+  int64_t row = 0;
+  for (const PlanHost::Task& t : p.tasks) {
+    const int32_t first = static_cast<int32_t>(w->tiles.size());
+    int64_t keys = 0;
+    for (int32_t si = t.seg_begin; si < t.seg_end; ++si) {
+      const Segment& s = p.segs[si];
+      add_tiles(p, s, o.bs, s.pos0, s.pos0, 0, w);
+      keys += s.tok_len;
+    }
+    const int32_t last = static_cast<int32_t>(w->tiles.size());
+    for (int32_t r = 0; r < t.n_rows; r += kTileRows)
+      qt.push_back({static_cast<int32_t>(row + r), std::min(kTileRows, t.n_rows - r), first, last, false});
+    w->flops += static_cast<double>(keys) * t.n_rows;
+    row += t.n_rows;
+  }
+  w->flops *= 4.0 * o.d * o.hq;
+  finish_join(qt, o, nullptr, w);
+}
+
 void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_end, AttnWorkHost* w,
                      const JoinPhase* ph) {
   *w = AttnWorkHost();
   const int64_t base = p.query_join_row_off[q_begin];
-  struct QTile {
-    int32_t row0, n_rows, tb, te;
-    bool force;  // write partials even when one piece covers it (its other phase adds more)
-  };
   std::vector<QTile> qt;
   const int sel = ph ? ph->sel : 0;
   for (size_t si = 0; si < p.segs.size(); ++si) {
@@ -163,6 +189,14 @@ void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_en
     for (int32_t j = 0; j < c.tok_len; ++j) w->flops += before + j + 1;
   }
   w->flops *= 4.0 * o.d * o.hq;
+  finish_join(qt, o, ph, w);
+}
+
+namespace {
+// Items of a join work list from its q tiles: one item per (q tile, unit), or (allow_split +
+// persistent) the stream-K cut into <= num_sms equal-cost contiguous ranges.
+void finish_join(const std::vector<QTile>& qt, const WorkOpts& o, const JoinPhase* ph, AttnWorkHost* w) {
+  const int sel = ph ? ph->sel : 0;
   if (!(o.allow_split && o.persistent) || qt.empty()) {
     std::vector<double> cost;
     for (const QTile& q : qt) {
@@ -274,6 +308,7 @@ void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_en
   count_subtiles(w);
   int used = grid;
   while (used > 1 && per_cta[used - 1].empty()) --used;
+  (void)sel;
   w->grid = used;
   w->cta_off.assign(used + 1, 0);
   for (int c = 0; c < used; ++c) {
@@ -281,6 +316,8 @@ void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_en
     w->cta_items.insert(w->cta_items.end(), per_cta[c].begin(), per_cta[c].end());
   }
 }
+
+}  // namespace
 
 std::pair<int32_t, int32_t> decode_row_tiles(const PlanHost& p, int32_t query, const std::vector<int32_t>& cross_gen_blocks,
                                              int32_t gen_ctx, int bs, DecodeWorkHost* w) {

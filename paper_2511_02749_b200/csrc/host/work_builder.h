@@ -57,6 +57,10 @@ struct JoinPhase {
 void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_end, AttnWorkHost* w,
                      const JoinPhase* ph = nullptr);
 
+// Owner-side split join: the plan's tasks — each a home query's cross rows
+// (rows in task order, packed) over the fragments of it owned here at Δ_f — as one join work list.
+void build_task_join_work(const PlanHost& p, const WorkOpts& o, AttnWorkHost* w);
+
 // Decode after the join: the KV tiles of one home query for its generated
 // rows — prefix (non-causal), fragments at Δ_f (non-causal, Q counter-rotated), then the cross +
 // generated tokens as one causal segment of gen_ctx tokens over `cross_gen_blocks` — split per kv

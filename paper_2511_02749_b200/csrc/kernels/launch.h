@@ -111,6 +111,29 @@ struct DecodeArgs {
   bool fp32, out_fp32;
 };
 cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t st);
+
+// owner-side split join (split_join.cu): K10 row gather (Q send buffer) and K11 merge
+cudaError_t launch_gather_rows(const int32_t* rows, int64_t n, const void* src, void* dst, int64_t row_bytes,
+                               int num_sms, cudaStream_t st);
+struct SplitMergeDesc {  // one home query: join rows [row0, row0 + n_rows), partial sources
+  int64_t row0;
+  int32_t n_rows, src_begin, src_end, pad;  // merge_src[src_begin, src_end): first partial row per owner
+};
+struct SplitMergeArgs {
+  const SplitMergeDesc* desc;
+  int32_t n_desc;
+  const int64_t* src;   // [..] row offsets into o_rem / lse_rem
+  const float* o_loc;   // [rows][hq][d] local join (normalized), fp32
+  const float* lse_loc; // [rows][hq]
+  const float* o_rem;   // [recv rows][hq][d] owners' partials (normalized), fp32
+  const float* lse_rem; // [recv rows][hq]
+  void* o;              // [rows][hq][d] out dtype
+  float* lse;           // [rows][hq] or null
+  int hq, d, num_sms;
+  int64_t total_rows;
+  bool out_fp32;
+};
+cudaError_t launch_merge_split(const SplitMergeArgs& a, cudaStream_t st);
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);
 
 struct KvExchangeArgs {

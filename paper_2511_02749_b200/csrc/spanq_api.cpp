@@ -134,6 +134,17 @@ struct spq_plan {
   std::vector<uint8_t> padded_layers;
   spq::AttnWorkHost pw_host, jw_host;  // kept for sub-range rebuilds / inspection
   std::vector<std::vector<int32_t>> cross_tokens;  // per query (plus distribution: commit)
+  // owner-side split join (world > 1, cfg.split_join)
+  bool split = false;
+  spq::AttnWorkHost tw_host;  // the tasks' join (owner side)
+  struct Split {
+    DevWork tw;
+    int64_t task_rows = 0, xq_rows = 0, home_rows = 0;
+    size_t off_tpos = 0, off_xrows = 0, off_mdesc = 0, off_msrc = 0;
+    int32_t n_mdesc = 0;
+    float *o_loc = nullptr, *lse_loc = nullptr;    // home: the local join, fp32
+    float *topart = nullptr, *tlsepart = nullptr;  // owner: split pieces of the task join
+  } sp;
   // decode after the join (spq_decode_reserve / spq_decode_step / spq_commit_span)
   struct Decode {
     int32_t max_new = 0;
@@ -222,7 +233,7 @@ spq_status make_qmap(const spq_ctx* c, const void* q, int64_t rows, CUtensorMap*
 // output maps for the epilogue's TMA stores: o as 3D {d, hq, rows}, box {32, 1, 32} (fp32) or
 // {64, 1, 32} (bf16): 128-byte rows; partials as 2D {d, parts*hq*128} box {32, 32}; all
 // SWIZZLE_128B (the staging layout)
-spq_status make_omap(const spq_ctx* c, const void* o, int64_t rows, CUtensorMap* out) {
+spq_status make_omap(const spq_ctx* c, const void* o, int64_t rows, CUtensorMap* out, int f32_override = -1) {
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult qr;
   CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
@@ -230,7 +241,7 @@ spq_status make_omap(const spq_ctx* c, const void* o, int64_t rows, CUtensorMap*
   const spq_config& g = c->cfg;
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.head_dim), static_cast<cuuint64_t>(g.num_q_heads),
                         static_cast<cuuint64_t>(std::max<int64_t>(rows, 1))};
-  const bool f32 = g.out_dtype == SPQ_FP32;
+  const bool f32 = f32_override >= 0 ? f32_override != 0 : g.out_dtype == SPQ_FP32;
   const cuuint64_t elt = f32 ? 4 : 2;
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.head_dim) * elt,
                            static_cast<cuuint64_t>(g.head_dim) * elt * g.num_q_heads};
@@ -563,7 +574,9 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
   }
   lap("normalize");
   std::unique_ptr<spq_plan> p(new spq_plan());
-  if (c->store->plan(fq, &p->host, c->pool.get(), c->cfg.rank, c->cfg.world_size) != 0) return fail(SPQ_ENOMEM, "block pool cannot hold the plan (rolled back)");
+  if (c->store->plan(fq, &p->host, c->pool.get(), c->cfg.rank, c->cfg.world_size,
+                     c->cfg.world_size > 1 && c->cfg.split_join != 0) != 0)
+    return fail(SPQ_ENOMEM, "block pool cannot hold the plan (rolled back)");
   // from here on the store holds the plan's pins and inserted digests: any failure undoes them
   struct Guard {
     spq_ctx* c;
@@ -613,6 +626,41 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
     const spq::JoinPhase ph2{2, remote, p->jw1_host.n_parts, &ranges};
     spq::build_join_work(H, o, 0, H.n_queries, &p->jw2_host, &ph2);
     p->phased = true;
+  }
+  // split join: the tasks' join work (owner side) and the exchange / merge tables (home side)
+  std::vector<int32_t> task_pos, xq_rows;
+  std::vector<spq::SplitMergeDesc> mdesc;
+  std::vector<int64_t> msrc;
+  if (c->cfg.world_size > 1 && c->cfg.split_join) {
+    p->split = true;
+    spq::build_task_join_work(H, o, &p->tw_host);
+    for (const spq::PlanHost::Task& t : H.tasks)
+      for (int32_t i = 0; i < t.n_rows; ++i) task_pos.push_back(t.pos0 + i);
+    std::vector<std::vector<int64_t>> first_row(H.n_queries);  // per home query: source rows (peer order)
+    int64_t off = 0;
+    for (int w = 0; w < c->cfg.world_size; ++w)
+      for (int32_t k = H.xq_off[w]; k < H.xq_off[w + 1]; ++k) {
+        const int32_t qi = H.xq_queries[k];
+        first_row[qi].push_back(off);
+        for (int64_t r = H.query_join_row_off[qi]; r < H.query_join_row_off[qi + 1]; ++r)
+          xq_rows.push_back(static_cast<int32_t>(r));
+        off += H.query_join_row_off[qi + 1] - H.query_join_row_off[qi];
+      }
+    for (int32_t qi = 0; qi < H.n_queries; ++qi) {
+      const int64_t r0 = H.query_join_row_off[qi], r1 = H.query_join_row_off[qi + 1];
+      if (r0 == r1) continue;
+      spq::SplitMergeDesc d{};
+      d.row0 = r0;
+      d.n_rows = static_cast<int32_t>(r1 - r0);
+      d.src_begin = static_cast<int32_t>(msrc.size());
+      msrc.insert(msrc.end(), first_row[qi].begin(), first_row[qi].end());
+      d.src_end = static_cast<int32_t>(msrc.size());
+      mdesc.push_back(d);
+    }
+    p->sp.task_rows = static_cast<int64_t>(task_pos.size());
+    p->sp.xq_rows = static_cast<int64_t>(xq_rows.size());
+    p->sp.home_rows = H.query_join_row_off.empty() ? 0 : H.query_join_row_off.back();
+    p->sp.n_mdesc = static_cast<int32_t>(mdesc.size());
   }
   lap("join work");
   if (prof) {
@@ -693,6 +741,13 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
       add_work(p->jw1_host, &p->jw1);
       add_work(p->jw2_host, &p->jw2);
     }
+    if (p->split) {
+      add_work(p->tw_host, &p->sp.tw);
+      p->sp.off_tpos = pk.add(task_pos);
+      p->sp.off_xrows = pk.add(xq_rows);
+      p->sp.off_mdesc = pk.add(mdesc);
+      p->sp.off_msrc = pk.add(msrc);
+    }
     // one device allocation: packed arrays, then the split-KV partials (O, LSE)
     size_t bytes = std::max<size_t>(pk.size, 256);
     size_t off_opart = 0, off_lsepart = 0;
@@ -702,6 +757,17 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
       off_opart = align_up(bytes, 1024);
       off_lsepart = align_up(off_opart + rows * c->cfg.head_dim * sizeof(float), 1024);
       bytes = off_lsepart + rows * sizeof(float);
+    }
+    size_t off_oloc = 0, off_lloc = 0, off_top = 0, off_tlp = 0;
+    if (p->split) {  // fp32 local join result (home) and the task join's split pieces (owner)
+      const size_t hr = static_cast<size_t>(p->sp.home_rows) * c->cfg.num_q_heads;
+      off_oloc = align_up(bytes, 1024);
+      off_lloc = align_up(off_oloc + hr * c->cfg.head_dim * sizeof(float), 1024);
+      bytes = off_lloc + hr * sizeof(float);
+      const size_t tr = static_cast<size_t>(p->sp.tw.n_parts) * heads_per_unit(c) * spq::kTileRows;
+      off_top = align_up(bytes, 1024);
+      off_tlp = align_up(off_top + tr * c->cfg.head_dim * sizeof(float), 1024);
+      bytes = off_tlp + tr * sizeof(float) + 256;
     }
     // pinned staging, reused once its previous upload has completed
     if (c->staging_size < pk.size) {
@@ -719,6 +785,12 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
     if (n_parts > 0) {
       p->opart = reinterpret_cast<float*>(p->dbuf + off_opart);
       p->lsepart = reinterpret_cast<float*>(p->dbuf + off_lsepart);
+    }
+    if (p->split) {
+      p->sp.o_loc = reinterpret_cast<float*>(p->dbuf + off_oloc);
+      p->sp.lse_loc = reinterpret_cast<float*>(p->dbuf + off_lloc);
+      p->sp.topart = reinterpret_cast<float*>(p->dbuf + off_top);
+      p->sp.tlsepart = reinterpret_cast<float*>(p->dbuf + off_tlp);
     }
     lap("upload");
   }
@@ -771,6 +843,10 @@ spq_status spq_plan_view_get(const spq_plan* p, spq_plan_view* v) {
   v->send_blocks = H.send_blocks.data();
   v->recv_off = H.recv_off.data();
   v->recv_blocks = H.recv_blocks.data();
+  v->n_tasks = static_cast<int32_t>(H.tasks.size());
+  v->tasks = H.tasks.empty() ? nullptr : &H.tasks[0].query;
+  v->xq_off = H.xq_off.data();
+  v->xq_queries = H.xq_queries.data();
   return SPQ_OK;
 }
 
@@ -838,8 +914,69 @@ spq_status spq_prefill_jobs(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, i
 namespace {
 // mode -1: the whole join of queries [a, b) (spq_join); 0 / 1: phase 0 / 1 of a phased plan's
 // join (spq_join_phase: K1 + the held segments, then the received fragments + the combine)
+// One join-shaped launch (K3 + K4) of work list w (device arrays in `buf`): rows of q at pos,
+// output o / lse in fp32 (f32) or the ctx out dtype; split pieces in opart / lsepart.
+spq_status launch_join_list(spq_ctx* c, const DevWork& w, uint8_t* buf, spq::AttnArgs& args, float* opart,
+                            float* lsepart, int32_t part_extent, const void* q, const int32_t* pos, int64_t rows,
+                            int32_t layer, void* o, float* lse, bool f32, bool pdl, cudaStream_t st) {
+  spq_status s = SPQ_OK;
+  args.opart = opart;
+  args.lsepart = lsepart;
+  args.pos = pos;
+  args.join = true;
+  args.pdl = pdl;  // see spq_prefill_jobs
+  args.q = q;
+  args.o = o;
+  args.lse = lse;
+  args.layer = layer;
+  args.out_fp32 = f32;
+  CUtensorMap qmap, omap, pmap;
+  if (c->cfg.dtype == SPQ_BF16) {
+    s = make_qmap(c, q, rows, &qmap);
+    if (s != SPQ_OK) return s;
+    args.tmap_q = &qmap;
+    if (f32) {
+      s = make_omap(c, o, rows, &omap, 1);
+      if (s != SPQ_OK) return s;
+      args.tmap_o = &omap;
+    }
+    if (w.n_parts > 0 && opart != nullptr) {
+      s = make_partmap(c, opart, part_extent, &pmap);
+      if (s != SPQ_OK) return s;
+      args.tmap_op = &pmap;
+    }
+  }
+  if (c->timing) CUDA_TRY(cudaEventRecord(c->ev[2], st));
+  s = run_attn(c, args, st);
+  if (s != SPQ_OK) return s;
+  if (c->timing) {
+    CUDA_TRY(cudaEventRecord(c->ev[3], st));
+    c->join_timed = true;
+  }
+  if (w.n_combine > 0) {
+    spq::CombineArgs ca{};
+    ca.desc = reinterpret_cast<const spq::CombineDesc*>(buf + w.combine);
+    ca.n_desc = w.n_combine;
+    ca.opart = opart;
+    ca.lsepart = lsepart;
+    ca.o = o;
+    ca.lse = lse;
+    ca.hq = c->cfg.num_q_heads;
+    ca.heads_per_desc = heads_per_unit(c);
+    ca.d = c->cfg.head_dim;
+    ca.out_fp32 = f32;
+    // the join kernel is the preceding stream operation unless a timing event sits between
+    ca.pdl = !c->timing && c->cfg.dtype == SPQ_BF16 && c->pdl;
+    cudaError_t e = spq::launch_combine(ca, st);
+    if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("combine launch: ") + cudaGetErrorString(e));
+    c->launches++;
+  }
+  return SPQ_OK;
+}
+
 spq_status join_impl(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b, const void* q, const void* k,
-                     const void* v, void* o, float* lse, void* stream, int mode) {
+                     const void* v, void* o, float* lse, void* stream, int mode, float* split_out = nullptr,
+                     float* split_lse = nullptr) {
   spq_status s = check_call(c, p, layer);
   if (s != SPQ_OK) return s;
   const int32_t nq = p->host.n_queries;
@@ -886,56 +1023,11 @@ spq_status join_impl(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t 
     w = tw.w;
     part_extent = w.n_parts;
   }
-  args.opart = opart;
-  args.lsepart = lsepart;
-  args.pos = at<int32_t>(p, p->off_jpos) + r0;
-  args.join = true;
-  args.pdl = k1 && (full || mode >= 0) && !c->timing && c->pdl;  // see spq_prefill_jobs
-  args.q = q;
-  args.o = o;
-  args.lse = lse;
-  args.layer = layer;
-  CUtensorMap qmap, omap, pmap;
-  if (c->cfg.dtype == SPQ_BF16) {
-    s = make_qmap(c, q, r1 - r0, &qmap);
-    if (s != SPQ_OK) return s;
-    args.tmap_q = &qmap;
-    if (c->cfg.out_dtype == SPQ_FP32) {
-      s = make_omap(c, o, r1 - r0, &omap);
-      if (s != SPQ_OK) return s;
-      args.tmap_o = &omap;
-    }
-    if (w.n_parts > 0 && opart != nullptr) {
-      s = make_partmap(c, opart, part_extent, &pmap);
-      if (s != SPQ_OK) return s;
-      args.tmap_op = &pmap;
-    }
-  }
-  if (c->timing) CUDA_TRY(cudaEventRecord(c->ev[2], st));
-  s = run_attn(c, args, st);
+  const bool f32 = split_out != nullptr || c->cfg.out_dtype == SPQ_FP32;
+  s = launch_join_list(c, w, full || mode >= 0 ? p->dbuf : tw.buf, args, opart, lsepart, part_extent, q,
+                       at<int32_t>(p, p->off_jpos) + r0, r1 - r0, layer, split_out ? split_out : o,
+                       split_out ? split_lse : lse, f32, k1 && (full || mode >= 0) && !c->timing && c->pdl, st);
   if (s != SPQ_OK) return s;
-  if (c->timing) {
-    CUDA_TRY(cudaEventRecord(c->ev[3], st));
-    c->join_timed = true;
-  }
-  if (w.n_combine > 0) {
-    spq::CombineArgs ca{};
-    ca.desc = reinterpret_cast<const spq::CombineDesc*>((full || mode >= 0 ? p->dbuf : tw.buf) + w.combine);
-    ca.n_desc = w.n_combine;
-    ca.opart = opart;
-    ca.lsepart = lsepart;
-    ca.o = o;
-    ca.lse = lse;
-    ca.hq = c->cfg.num_q_heads;
-    ca.heads_per_desc = heads_per_unit(c);
-    ca.d = c->cfg.head_dim;
-    ca.out_fp32 = c->cfg.out_dtype == SPQ_FP32;
-    // the join kernel is the preceding stream operation unless a timing event sits between
-    ca.pdl = !c->timing && c->cfg.dtype == SPQ_BF16 && c->pdl;
-    cudaError_t e = spq::launch_combine(ca, st);
-    if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("combine launch: ") + cudaGetErrorString(e));
-    c->launches++;
-  }
   if (tw.buf) CUDA_TRY(cudaFreeAsync(tw.buf, st));
   return SPQ_OK;
 }
@@ -943,7 +1035,83 @@ spq_status join_impl(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t 
 
 spq_status spq_join(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b, const void* q, const void* k,
                     const void* v, void* o, float* lse, void* stream) {
+  if (p != nullptr && c != nullptr && c->live.count(p) && p->split)
+    return fail(SPQ_ESTATE, "split-join plan: use spq_split_join_local / spq_split_merge");
   return join_impl(c, p, layer, a, b, q, k, v, o, lse, stream, -1);
+}
+
+// ------------------------------------------------------------------ owner-side split join (f1)
+spq_status spq_split_pack_q(spq_ctx* c, spq_plan* p, const void* q, void* sendbuf, void* stream) {
+  spq_status s = check_call(c, p, 0);
+  if (s != SPQ_OK) return s;
+  if (!p->split) return fail(SPQ_ESTATE, "not a split-join plan");
+  if (p->sp.xq_rows == 0) return SPQ_OK;
+  if (q == nullptr || sendbuf == nullptr) return fail(SPQ_EINVAL, "null buffer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  const int64_t row_bytes = static_cast<int64_t>(c->cfg.num_q_heads) * c->cfg.head_dim * elt_size(c);
+  cudaError_t e = spq::launch_gather_rows(at<int32_t>(p, p->sp.off_xrows), p->sp.xq_rows, q, sendbuf, row_bytes,
+                                          c->num_sms, st);
+  if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("gather_rows launch: ") + cudaGetErrorString(e));
+  c->launches++;
+  return SPQ_OK;
+}
+
+spq_status spq_split_task_join(spq_ctx* c, spq_plan* p, int32_t layer, const void* q_recv, float* part_o,
+                               float* part_lse, void* stream) {
+  spq_status s = check_call(c, p, layer);
+  if (s != SPQ_OK) return s;
+  if (!p->split) return fail(SPQ_ESTATE, "not a split-join plan");
+  if (p->sp.task_rows == 0) return SPQ_OK;
+  if (q_recv == nullptr || part_o == nullptr || part_lse == nullptr) return fail(SPQ_EINVAL, "null buffer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  s = wait_pending(c, st);
+  if (s != SPQ_OK) return s;
+  spq::AttnArgs args{};
+  fill_attn(c, p, p->sp.tw, &args);
+  return launch_join_list(c, p->sp.tw, p->dbuf, args, p->sp.topart, p->sp.tlsepart, p->sp.tw.n_parts, q_recv,
+                          at<int32_t>(p, p->sp.off_tpos), p->sp.task_rows, layer, part_o, part_lse, true, false, st);
+}
+
+spq_status spq_split_join_local(spq_ctx* c, spq_plan* p, int32_t layer, const void* q, const void* k, const void* v,
+                                void* stream) {
+  spq_status s = check_call(c, p, layer);
+  if (s != SPQ_OK) return s;
+  if (!p->split) return fail(SPQ_ESTATE, "not a split-join plan");
+  return join_impl(c, p, layer, 0, p->host.n_queries, q, k, v, nullptr, nullptr, stream, -1, p->sp.o_loc,
+                   p->sp.lse_loc);
+}
+
+spq_status spq_split_merge(spq_ctx* c, spq_plan* p, const float* part_o_recv, const float* part_lse_recv, void* o,
+                           float* lse, void* stream) {
+  spq_status s = check_call(c, p, 0);
+  if (s != SPQ_OK) return s;
+  if (!p->split) return fail(SPQ_ESTATE, "not a split-join plan");
+  if (p->sp.home_rows == 0) return SPQ_OK;
+  if (o == nullptr || (p->sp.xq_rows > 0 && (part_o_recv == nullptr || part_lse_recv == nullptr)))
+    return fail(SPQ_EINVAL, "null buffer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  spq::SplitMergeArgs m{};
+  m.desc = at<spq::SplitMergeDesc>(p, p->sp.off_mdesc);
+  m.n_desc = p->sp.n_mdesc;
+  m.src = at<int64_t>(p, p->sp.off_msrc);
+  m.o_loc = p->sp.o_loc;
+  m.lse_loc = p->sp.lse_loc;
+  m.o_rem = part_o_recv;
+  m.lse_rem = part_lse_recv;
+  m.o = o;
+  m.lse = lse;
+  m.hq = c->cfg.num_q_heads;
+  m.d = c->cfg.head_dim;
+  m.num_sms = c->num_sms;
+  m.total_rows = p->sp.home_rows;
+  m.out_fp32 = c->cfg.out_dtype == SPQ_FP32;
+  cudaError_t e = spq::launch_merge_split(m, st);
+  if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("merge_split launch: ") + cudaGetErrorString(e));
+  c->launches++;
+  return SPQ_OK;
 }
 
 spq_status spq_join_phase(spq_ctx* c, spq_plan* p, int32_t layer, int32_t phase, const void* q, const void* k,

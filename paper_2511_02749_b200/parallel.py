@@ -61,3 +61,47 @@ def exchange_layer(plan, view: Dict, layer: int, shape, device, dtype, rank: int
         off += recv[p] * be
     elt = sendbuf.element_size()
     return {"sent_bytes": sum(send) * be * elt, "recv_bytes": sum(recv) * be * elt}
+
+
+# ---------------------------------------------------------------- owner-side split join (f1)
+def split_rows(view: Dict, world: int):
+    """Rows per peer of the two split-join exchanges: (qsend[w] = rows of the home queries whose Q
+    goes to owner w = partial rows coming back from w, qrecv[h] = rows of this rank's tasks homed
+    on h = partial rows going back to h)."""
+    off = view["query_join_row_off"]
+    qsend = [sum(int(off[q + 1] - off[q]) for q in view["xq"].get(w, [])) for w in range(world)]
+    qrecv = [0] * world
+    for (query, home, n_rows, _pos0, _b, _e) in view["tasks"]:
+        qrecv[home] += n_rows
+    return qsend, qrecv
+
+
+def split_exchange_layer(plan, view: Dict, layer: int, shape, device, q_join, rank: int, world: int,
+                         group=None, stream=None, transport: Optional[Callable] = None,
+                         local_join: Optional[Callable] = None) -> Dict[str, int]:
+    """One layer of the owner-side split join around the C-ABI calls: pack Q -> all-to-all ->
+    task join (owner) -> all-to-all of the fp32 partials -> the caller's merge input. Returns the
+    partial buffers to pass to spq_split_merge (and the bytes moved). `local_join()` (the home's
+    spq_split_join_local) is issued right after the Q exchange so it overlaps the task joins of
+    the owners."""
+    import torch
+
+    qsend_rows, qrecv_rows = split_rows(view, world)
+    hq, d = shape.hq, shape.d
+    send = torch.empty((sum(qsend_rows), hq, d), dtype=q_join.dtype, device=device)
+    recv = torch.empty((sum(qrecv_rows), hq, d), dtype=q_join.dtype, device=device)
+    plan.split_pack_q(q_join, send, stream=stream)
+    tr = transport or (lambda r, s_, o, i: _a2a(r, s_, o, i, group))
+    tr(recv.view(-1), send.view(-1), [n * hq * d for n in qrecv_rows], [n * hq * d for n in qsend_rows])
+    if local_join is not None:
+        local_join()
+    po = torch.empty((sum(qrecv_rows), hq, d), dtype=torch.float32, device=device)
+    pl = torch.empty((sum(qrecv_rows), hq), dtype=torch.float32, device=device)
+    plan.split_task_join(layer, recv, po, pl, stream=stream)
+    ro = torch.empty((sum(qsend_rows), hq, d), dtype=torch.float32, device=device)
+    rl = torch.empty((sum(qsend_rows), hq), dtype=torch.float32, device=device)
+    tr(ro.view(-1), po.view(-1), [n * hq * d for n in qsend_rows], [n * hq * d for n in qrecv_rows])
+    tr(rl.view(-1), pl.view(-1), [n * hq for n in qsend_rows], [n * hq for n in qrecv_rows])
+    qb = send.numel() * send.element_size()
+    pb = po.numel() * 4 + pl.numel() * 4
+    return {"part_o": ro, "part_lse": rl, "q_bytes": qb, "partial_bytes": pb}

@@ -38,7 +38,7 @@ class spq_config(C.Structure):
         ("dtype", C.c_int32), ("rope_base", C.c_double), ("max_position", C.c_int32),
         ("model_salt", C.c_uint64), ("k_pool", C.c_void_p), ("v_pool", C.c_void_p),
         ("device", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32),
-        ("out_dtype", C.c_int32),
+        ("out_dtype", C.c_int32), ("split_join", C.c_int32),
     ]
 
 
@@ -73,6 +73,7 @@ class spq_plan_view(C.Structure):
         ("prefill_kv_bytes", C.c_int64), ("join_kv_bytes", C.c_int64),
         ("n_join_queries", C.c_int32), ("world_size", C.c_int32),
         ("send_off", _I64P), ("send_blocks", _I32P), ("recv_off", _I64P), ("recv_blocks", _I32P),
+        ("n_tasks", C.c_int32), ("tasks", _I32P), ("xq_off", _I32P), ("xq_queries", _I32P),
     ]
 
 
@@ -132,6 +133,13 @@ SIGNATURES = {
     "spq_reduce_tree": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
                                   _I32P, _I32P]),
     "spq_bulk_order": (C.c_int, [C.c_void_p, C.POINTER(spq_query), C.c_int32, C.c_int64, C.c_void_p]),
+    "spq_split_pack_q": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "spq_split_task_join": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_void_p]),
+    "spq_split_join_local": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_void_p]),
+    "spq_split_merge": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.c_void_p]),
     "spq_set_option": (C.c_int, [C.c_void_p, C.c_int32, C.c_double]),
     "spq_set_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
 }
@@ -255,6 +263,10 @@ class Plan:
         sb, rb = _arr(v.send_blocks, int(so[-1]), np.int32), _arr(v.recv_blocks, int(ro[-1]), np.int32)
         out["send"] = {p: sb[so[p]:so[p + 1]] for p in range(w) if so[p + 1] > so[p]}
         out["recv"] = {p: rb[ro[p]:ro[p + 1]] for p in range(w) if ro[p + 1] > ro[p]}
+        out["tasks"] = [tuple(int(x) for x in r) for r in _arr(v.tasks, 6 * v.n_tasks, np.int32).reshape(-1, 6)]
+        xo = _arr(v.xq_off, w + 1, np.int32) if v.xq_off else np.zeros(w + 1, np.int32)
+        xqq = _arr(v.xq_queries, int(xo[-1]), np.int32)
+        out["xq"] = {p: xqq[xo[p]:xo[p + 1]].tolist() for p in range(w) if xo[p + 1] > xo[p]}
         return out
 
     def exchange_pack(self, layer, peer, buf, stream=None):
@@ -309,6 +321,23 @@ class Plan:
                                        _stream_ptr(stream, self.ctx.device), C.byref(n)))
         return n.value
 
+    # ---- owner-side split join (W > 1, split_join=True)
+    def split_pack_q(self, q_join, qsend, stream=None):
+        _check(lib().spq_split_pack_q(self.ctx.handle, self.handle, _ptr(q_join), _ptr(qsend),
+                                      _stream_ptr(stream, self.ctx.device)))
+
+    def split_task_join(self, layer, qrecv, part_o, part_lse, stream=None):
+        _check(lib().spq_split_task_join(self.ctx.handle, self.handle, layer, _ptr(qrecv), _ptr(part_o),
+                                         _ptr(part_lse), _stream_ptr(stream, self.ctx.device)))
+
+    def split_join_local(self, layer, q, k, v, stream=None):
+        _check(lib().spq_split_join_local(self.ctx.handle, self.handle, layer, _ptr(q), _ptr(k), _ptr(v),
+                                          _stream_ptr(stream, self.ctx.device)))
+
+    def split_merge(self, part_o_recv, part_lse_recv, o, lse=None, stream=None):
+        _check(lib().spq_split_merge(self.ctx.handle, self.handle, _ptr(part_o_recv), _ptr(part_lse_recv), _ptr(o),
+                                     _ptr(lse), _stream_ptr(stream, self.ctx.device)))
+
     def release(self, stream=None):
         if not self.released:
             _check(lib().spq_plan_release(self.ctx.handle, self.handle, _stream_ptr(stream, self.ctx.device)))
@@ -324,7 +353,7 @@ class Context:
 
     def __init__(self, shape: _inputs.Shape, num_blocks: int, device: int = 0,
                  max_position: int = 1 << 15, pools=None, out_dtype: Optional[str] = None,
-                 rank: int = 0, world_size: int = 1):
+                 rank: int = 0, world_size: int = 1, split_join: bool = False):
         self.shape = shape
         self.device = device
         self.num_blocks = num_blocks
@@ -345,7 +374,7 @@ class Context:
                          BF16 if shape.dtype == "bf16" else FP32, float(shape.rope_base),
                          int(max_position), int(shape.model_salt), _ptr(self.k_pool),
                          _ptr(self.v_pool), device, int(rank), int(world_size),
-                         BF16 if self.out_dtype == "bf16" else FP32)
+                         BF16 if self.out_dtype == "bf16" else FP32, 1 if split_join else 0)
         h = C.c_void_p()
         _check(lib().spq_create(C.byref(cfg), C.byref(h)))
         self.handle = h.value

@@ -116,3 +116,78 @@ def test_partitioned_exchange_parity(cuda_dev, dtype, world, phased, out):
     for p, c in zip(plans, ctxs):
         p.release()
         c.close()
+
+
+@pytest.mark.parametrize("dtype,world,out", [("bf16", 2, "fp32"), ("bf16", 3, "bf16"), ("fp32", 2, "fp32"),
+                                             ("bf16", 4, "fp32")])
+def test_split_join_parity(cuda_dev, dtype, world, out):
+    """Owner-side split join (f1) with W contexts on one GPU: each home packs its queries' cross Q
+    for their fragments' owners, each owner runs its tasks (the home query's rows over its
+    fragments at Δ_f) into fp32 partials, each home merges them with its local join; the
+    device-to-device copies stand in for the two NCCL all-to-alls. Every home query's join
+    output must match the oracle's plain join (no KV moved: the owners' pages never leave)."""
+    import torch
+
+    fp32 = dtype == "fp32"
+    sh = inputs.Shape(hq=8, hkv=2, d=128 if not fp32 else 64, block_size=16, vocab=512, dtype=dtype)
+    qs = inputs.random_queries(305 + world, 10, vocab=512, max_frag=6, max_len=170, max_prefix=90,
+                               max_cross=140, reuse_p=0.5)
+    seed = 305
+    eq, ek, ev = inputs.layer_tables(sh, 0, seed)
+    tab = runner.device_tables(sh, 0, seed, cuda_dev)
+    flat = [(q.prefix, q.fragments, q.cross) for q in qs]
+    odt = torch.bfloat16 if out == "bf16" else torch.float32
+    ctxs, plans, views, qjoin = [], [], [], []
+    for r in range(world):
+        ctx = spanq.Context(sh, 2048, device=0, max_position=1 << 14, out_dtype=out, rank=r, world_size=world,
+                            split_join=True)
+        plan = ctx.plan(qs)
+        view = plan.view()
+        ptok = runner.prefill_tokens(view, qs)
+        if len(ptok):
+            plan.prefill(0, *runner.gather(tab, ptok, cuda_dev), torch.empty((len(ptok), sh.hq, sh.d), dtype=odt,
+                                                                             device=cuda_dev))
+        jtok = runner.join_tokens(view, qs)
+        qjoin.append(runner.gather(tab, jtok, cuda_dev))
+        ctxs.append(ctx)
+        plans.append(plan)
+        views.append(view)
+    rows = [parallel.split_rows(v, world) for v in views]
+    # Q exchange: home h packs (owner-major); owner w receives the chunks of every home (rank order)
+    qsend = []
+    for h in range(world):
+        buf = torch.full((sum(rows[h][0]), sh.hq, sh.d), float("nan"), dtype=qjoin[h][0].dtype, device=cuda_dev)
+        plans[h].split_pack_q(qjoin[h][0], buf)
+        qsend.append(buf)
+    chunks = lambda x, counts: list(torch.split(x, counts)) if len(counts) else []
+    qrecv = [torch.cat([chunks(qsend[h], rows[h][0])[w] for h in range(world)]) for w in range(world)]
+    for w in range(world):
+        assert qrecv[w].shape[0] == sum(rows[w][1])
+    # homes: K1 + local join (before the owners' partials exist); owners: task joins
+    for h in range(world):
+        plans[h].split_join_local(0, *qjoin[h])
+    parts = []
+    for w in range(world):
+        po = torch.full((qrecv[w].shape[0], sh.hq, sh.d), float("nan"), device=cuda_dev)
+        pl = torch.full((qrecv[w].shape[0], sh.hq), float("nan"), device=cuda_dev)
+        plans[w].split_task_join(0, qrecv[w], po, pl)
+        parts.append((po, pl))
+    torch.cuda.synchronize()
+    n_tasks = sum(len(v["tasks"]) for v in views)
+    assert n_tasks > 0, "no remote work"
+    # partials back: owner w's rows homed on h -> h, which lays them out owner-major
+    for h in range(world):
+        ro = torch.cat([chunks(parts[w][0], rows[w][1])[h] for w in range(world)])
+        rl = torch.cat([chunks(parts[w][1], rows[w][1])[h] for w in range(world)])
+        n = int(views[h]["query_join_row_off"][-1])
+        oj = torch.empty((n, sh.hq, sh.d), dtype=odt, device=cuda_dev)
+        lj = torch.empty((n, sh.hq), dtype=torch.float32, device=cuda_dev)
+        plans[h].split_merge(ro, rl, oj, lj)
+        torch.cuda.synchronize()
+        home = [i for i in range(len(qs)) if i % world == h]
+        exp = [oatt.join_rows(*flat[i], eq, ek, ev, sh.rope_base) for i in home]
+        check(oj, np.concatenate([e[0] for e in exp]), fp32, f"rank {h} split join O")
+        check_lse(lj, np.concatenate([e[1] for e in exp]), fp32, f"rank {h} split join LSE")
+    for p, c in zip(plans, ctxs):
+        p.release()
+        c.close()

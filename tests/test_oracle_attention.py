@@ -343,3 +343,31 @@ def test_decode_row_is_the_last_row_of_the_extended_query():
         do, dl, _ = oatt.dense_masked(prefix, frags, np.concatenate([cross, gen[: t + 1]]), eq, ek, ev, sh.rope_base)
         np.testing.assert_allclose(o[0], do[-1], atol=1e-12)
         np.testing.assert_allclose(lse[0], dl[-1], atol=1e-12)
+
+
+def test_split_join_partials_merge_to_the_join():
+    # owner-side split join (f1): the home's partial over prefix + its local fragments + cross and
+    # each owner's partial over its fragments, merged by LSE, is the join (the plain definition's
+    # cross rows) — and leaving any one part out is not
+    from oracle import attention as oatt
+    from paper_2511_02749_b200 import inputs
+
+    sh = inputs.Shape(hq=4, hkv=2, d=16, block_size=4, vocab=64, dtype="fp32")
+    eq, ek, ev = inputs.layer_tables(sh, 0, 91)
+    g = np.random.default_rng(12)
+    for trial in range(6):
+        prefix = g.integers(0, 64, int(g.integers(0, 7)))
+        frags = [g.integers(0, 64, int(g.integers(1, 9))) for _ in range(int(g.integers(1, 6)))]
+        cross = g.integers(0, 64, int(g.integers(1, 6)))
+        owner = g.integers(0, 3, len(frags))  # 0 = the home rank
+        parts = [oatt.join_rows_subset(prefix, frags, cross, eq, ek, ev, sh.rope_base, True, owner == 0)]
+        for w in (1, 2):
+            if (owner == w).any():
+                parts.append(oatt.join_rows_subset(prefix, frags, cross, eq, ek, ev, sh.rope_base, False, owner == w))
+        o, lse = oatt.merge_lse(parts)
+        jo, jl = oatt.join_rows(prefix, frags, cross, eq, ek, ev, sh.rope_base)
+        np.testing.assert_allclose(o, jo, atol=1e-12)
+        np.testing.assert_allclose(lse, jl, atol=1e-12)
+        if len(parts) > 1:
+            o2, _ = oatt.merge_lse(parts[:-1])
+            assert np.abs(o2 - jo).max() > 1e-6

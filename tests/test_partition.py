@@ -196,3 +196,136 @@ def test_exchange_layer_gloo_world2():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: "ok", 1: "ok"}, res
+
+
+# ---------------------------------------------------------------- owner-side split join (f1)
+@pytest.mark.parametrize("world,seed,bs", [(2, 31, 4), (3, 32, 8), (5, 33, 2)])
+def test_split_planner_bit_exact_vs_oracle(world, seed, bs):
+    shape = inputs.Shape(hq=4, hkv=2, d=64, block_size=bs, dtype="fp32", model_salt=seed)
+    qs = inputs.random_queries(seed, 30, vocab=12, max_len=30, reuse_p=0.5)
+    for rank in range(world):
+        ctx = spanq.Context(shape, 4096, device=-1, rank=rank, world_size=world, split_join=True)
+        ost = Store(4096, 4, 2, 64, bs, shape.rope_base, seed)
+        for i in range(0, len(qs), 7):
+            batch = qs[i:i + 7]
+            ov = ost.plan([flat(q) for q in batch], rank=rank, world=world, split=True)
+            cv = ctx.plan(batch).view()
+            assert_same(cv, ov)
+            np.testing.assert_array_equal(cv["seg_pos0"], [s.pos0 for s in ov.segments])
+            assert cv["tasks"] == ov.tasks
+            assert cv["xq"] == {p: q for p, q in ov.xq.items() if q}
+            assert not cv["send"] and not cv["recv"]  # no KV moves in split mode
+        ctx.close()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_split_lists_agree_and_cover_batch(world):
+    shape = inputs.Shape(hq=4, hkv=2, d=64, block_size=8, dtype="fp32")
+    qs = inputs.random_queries(41 + world, 40, vocab=16, max_len=40, reuse_p=0.5)
+    views = [spanq.Context(shape, 1 << 14, device=-1, rank=r, world_size=world, split_join=True).plan(qs).view()
+             for r in range(world)]
+    root = Store(1, 4, 2, 64, 8).root
+    for h in range(world):
+        for w in range(world):
+            # what home h sends to owner w is what w's tasks homed on h read, in the same order
+            mine = views[h]["xq"].get(w, [])
+            theirs = [t[0] for t in views[w]["tasks"] if t[1] == h]
+            assert mine == theirs, (h, w)
+            rows_h = sum(int(views[h]["query_join_row_off"][q + 1] - views[h]["query_join_row_off"][q]) for q in mine)
+            assert rows_h == sum(t[2] for t in views[w]["tasks"] if t[1] == h)
+    # every (query, fragment occurrence) attended exactly once: on the home (a local segment) or
+    # by the owner's task for that query, at the fragment's offset Δ_f in the query
+    for qi, q in enumerate(qs):
+        h = qi % world
+        want, off = [], len(q.prefix)
+        for f in q.fragments:
+            want.append((hashing.fragment_chain(np.asarray(f), 8, root)[-1], off))
+            off += len(f)
+        got = []
+        v = views[h]
+        for s in range(len(v["seg_kind"])):
+            if v["seg_query"][s] == qi and v["seg_kind"][s] == 1:
+                blk = v["seg_block_off"][s] + v["seg_n_blocks"][s] - 1
+                got.append((bytes(v["digests"][blk]), int(v["seg_pos0"][s])))
+        for w in range(world):
+            for (tq, th, n_rows, pos0, sb, se) in views[w]["tasks"]:
+                if tq != qi:
+                    continue
+                assert th == h and n_rows == len(q.cross) and pos0 == off
+                for s in range(sb, se):
+                    vw = views[w]
+                    assert vw["seg_query"][s] == qi and vw["seg_kind"][s] == 1
+                    blk = vw["seg_block_off"][s] + vw["seg_n_blocks"][s] - 1
+                    d = bytes(vw["digests"][blk])
+                    assert hashing.owner_rank(d, world) == w
+                    got.append((d, int(vw["seg_pos0"][s])))
+        assert sorted(got) == sorted(want), qi
+
+
+class _CpuSplitPlan:
+    """split_pack_q / split_task_join emulated on CPU: the 'partial' of a task row is the received
+    q row itself (fp32) and its LSE the task's query id, so the home can check that every row came
+    back from the right owner in the right order."""
+
+    def __init__(self, view):
+        self.view = view
+
+    def split_pack_q(self, q_join, qsend, stream=None):
+        off = self.view["query_join_row_off"]
+        rows = [r for w in sorted(self.view["xq"]) for q in self.view["xq"][w] for r in range(off[q], off[q + 1])]
+        qsend.copy_(q_join[rows])
+
+    def split_task_join(self, layer, qrecv, part_o, part_lse, stream=None):
+        import torch
+
+        part_o.copy_(qrecv.float())
+        qid = [t[0] for t in self.view["tasks"] for _ in range(t[2])]
+        part_lse.copy_(torch.tensor(qid, dtype=torch.float32)[:, None].expand_as(part_lse))
+
+
+def _gloo_split_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        shape = inputs.Shape(hq=2, hkv=1, d=8, block_size=4, dtype="fp32")
+        qs = inputs.random_queries(88, 20, vocab=16, max_len=20, reuse_p=0.5)
+        ctx = spanq.Context(shape, 4096, device=-1, rank=rank, world_size=world, split_join=True)
+        view = ctx.plan(qs).view()
+        n = int(view["query_join_row_off"][-1])
+        q_join = torch.arange(n * 2 * 8, dtype=torch.float32).reshape(n, 2, 8) + 1000 * rank
+        out = parallel.split_exchange_layer(_CpuSplitPlan(view), view, 0, shape, "cpu", q_join, rank, world)
+        off = view["query_join_row_off"]
+        r = 0
+        for w in sorted(view["xq"]):
+            for qq in view["xq"][w]:
+                k = off[qq + 1] - off[qq]
+                assert torch.equal(out["part_o"][r:r + k], q_join[off[qq]:off[qq + 1]]), (rank, w, qq)
+                assert (out["part_lse"][r:r + k] == qq).all()
+                r += k
+        assert r == out["part_o"].shape[0]
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception:  # pragma: no cover - reported by the parent
+        import traceback
+
+        q.put((rank, traceback.format_exc()))
+
+
+def test_split_exchange_gloo_world2():
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_split_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}, res
