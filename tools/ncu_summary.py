@@ -30,6 +30,9 @@ METRICS = [
     ("sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg", "tensor hmma subpipe cycles (realtime)"),
     ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor memory (TMEM) active %"),
     ("sm__cycles_elapsed.avg", "SM cycles elapsed"),
+    ("smsp__sass_inst_executed_op_utcmma.sum", "tcgen05.mma (UTCMMA) instructions"),
+    ("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "issue active %"),
+    ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem -> tensor core wavefronts %"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
     ("launch__registers_per_thread", "registers/thread"),
     ("launch__shared_mem_per_block_dynamic", "dyn smem/block"),
@@ -67,7 +70,8 @@ def launches(path: str):
 
 
 def short(name: str) -> str:
-    for k in ("span_attn_tc", "span_attn_f32", "rope_kv_write", "combine_kernel", "kv_exchange", "cidra_kernel"):
+    for k in ("span_attn_tc", "span_attn_f32", "rope_kv_write", "combine_kernel", "kv_exchange", "cidra_kernel",
+              "decode_kernel", "gather_rows", "merge_split"):
         if k in name:
             return k
     return name.split("(")[0][-60:]
@@ -78,17 +82,21 @@ def main():
     prof = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out", "prof")
     out_md = [f"# ncu summary, round {tag}", "",
               "Source: `tools/profile_round.sh` on one B200 (`ncu --set full --clock-control none`"
-              " captures of `tools/profile_step.py`, C2 cold, 1 layer; launch list of `bench.py"
-              " --steps 2 --warmup 1` under `ncu --metrics gpu__time_duration.sum`). Per-launch"
+              " captures of `tools/profile_step.py`, C2 cold, 1 layer, bf16 O; launch list of `bench.py"
+              " --steps 2 --warmup 3` under `ncu --metrics gpu__time_duration.sum`). Per-launch"
               " times under ncu are serialised and cold-cache: compare shares, not absolutes.", ""]
     traffic = OrderedDict()
     names = {"attn": ["span_attn_tc prefill", "span_attn_tc join"], "kvwrite": ["rope_kv_write prefill"],
-             "combine": ["combine join"], "exchange": ["kv_exchange"], "cidra": ["cidra reposition"]}
+             "combine": ["combine join"], "exchange": ["kv_exchange"], "cidra": ["cidra reposition"],
+             "decode": ["decode (K9)"]}
+    # executed tensor FLOPs of one tcgen05.mma of the attention kernel at d = 128 (C2): per 64-key
+    # step and head, 8 S MMAs (M128 N64 K16) + 4 PV MMAs (M128 N128 K16)
+    flop_per_mma = (8 * 128 * 64 * 16 * 2 + 4 * 128 * 128 * 16 * 2) / 12
     for rep, labels in names.items():
         path = os.path.join(prof, rep + ".ncu-rep")
         if not os.path.exists(path):
             continue
-        shutil.copy(path, os.path.join(ROOT, "profiles", f"{tag}_{rep}.ncu-rep"))
+        shutil.copy(path, os.path.join(ROOT, "profiles", f"{tag}_{rep}.ncu-rep"))  # untracked (.gitignore)
         for i, rec in enumerate(raw(path)):
             label = labels[i] if i < len(labels) else f"{rep} #{i}"
             out_md += [f"## {label}", "", f"`{rec['Kernel Name'][1][:120]}`", "", "| metric | value |", "|---|---|"]
@@ -105,6 +113,13 @@ def main():
                     else:
                         txt = f"{v} {u}"
                     out_md.append(f"| {what} (`{key}`) | {txt} |")
+            if "smsp__sass_inst_executed_op_utcmma.sum" in rec and rep == "attn":
+                n_mma, _ = value(rec, "smsp__sass_inst_executed_op_utcmma.sum")
+                cyc, _ = value(rec, "sm__cycles_elapsed.avg")
+                if isinstance(n_mma, float) and isinstance(cyc, float) and cyc > 0:
+                    util = n_mma * flop_per_mma / (cyc * 148 * 8192)
+                    out_md.append(f"| tensor pipe utilization (UTCMMA x {flop_per_mma / 1e3:.1f} kFLOP / "
+                                  f"(cycles x 148 SMs x 8192 FLOP/clk)) | {util:.1%} |")
             rd, _ = value(rec, "dram__bytes_read.sum")
             wr, _ = value(rec, "dram__bytes_write.sum")
             dur, _ = value(rec, "gpu__time_duration.sum")
