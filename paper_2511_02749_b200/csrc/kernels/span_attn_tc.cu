@@ -79,7 +79,7 @@ struct TcSmem {
   uint64_t s_full[2][2], p_full[2][2], o_done[2][2];  // [head][S buffer / PV parity j & 1]
   // prefill: the epilogue runs on the Q-prep warps (12-15). The softmax WG of head x hands over
   // 1/l of every row through fin_inv[x][item & 1] (fin_full: 128 arrivals), the epilogue warps
-  // drain O_x from TMEM into the staging area and arrive o_free[x] (4 warps), which the issuer
+  // drain O_x from TMEM into the staging area and arrive o_free[x] (128 threads), which the issuer
   // waits for before the next item's first PV overwrites O_x
   uint64_t o_free[2], fin_full[2][2];
   float fin_inv[2][2][128];
@@ -572,11 +572,9 @@ __device__ __forceinline__ void epilogue(const TcParams& P, TcSmem<D>& S, uint32
     }
   }
   if (J) {  // the Q slot is free again once this warp's stores have read it
-    if (lane == 0) {
-      bulk_wait_read<0>();
-      mbar_arrive(&S.q_empty[x][q_slot(J, f.elast)]);
-    }
+    if (lane == 0) bulk_wait_read<0>();
     __syncwarp();
+    mbar_arrive(&S.q_empty[x][q_slot(J, f.elast)]);  // every lane (its staging writes are released)
   }
   if (tr) trace(P, 2 + x, tc, 33);  // 33: epilogue done
 }
@@ -627,8 +625,7 @@ __device__ void prefill_epilogue(const TcParams& P, TcSmem<D>& S, uint32_t tmem,
       if (c + 1 == D / 32) {
         // the last TMEM load has landed (waited at the end of the previous iteration): O_x is free
         tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&S.o_free[x]);
+        mbar_arrive(&S.o_free[x]);  // every lane: its TMEM loads and fin_inv read are done
         if (tr) trace(P, 4, tc, 62 + 4 * x);  // 62/66: O drained (o_free)
       }
       const int chunk = f32 ? c : c / 2;
@@ -689,12 +686,11 @@ __device__ void prefill_epilogue(const TcParams& P, TcSmem<D>& S, uint32_t tmem,
       }
       tmem_wait_ld();
     }
-    // the slot returns to the Q prep once this warp's stores have read it
-    if (lane == 0) {
-      bulk_wait_read<0>();
-      mbar_arrive(&S.q_empty[x][k & 1]);
-    }
+    // the slot returns to the Q prep once this warp's stores have read it (every lane arrives, so
+    // each lane's own staging writes are released by its own arrive)
+    if (lane == 0) bulk_wait_read<0>();
     __syncwarp();
+    mbar_arrive(&S.q_empty[x][k & 1]);
   }
 }
 
@@ -726,7 +722,7 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
       const int nsub = tl.n_valid > 64 ? 2 : 1;
       if (J && (t == w.tile_begin || tl.rot_delta != a.tiles[t - 1].rot_delta)) {
         // a new epoch: this warp has no use for the previous epoch's Q slot (mid-item)
-        if (t != w.tile_begin && tr) mbar_arrive(&S.q_empty[x][q_slot(J, ecur)]);
+        if (t != w.tile_begin) mbar_arrive(&S.q_empty[x][q_slot(J, ecur)]);
         ecur = eps++;
       }
       for (int hh = 0; hh < nsub; ++hh, ++js) {
@@ -1077,9 +1073,9 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
     for (int i = 0; i < TcSmem<D>::kQSlots; ++i)
       for (int sl = 0; sl < 2; ++sl) {
         mbar_init(&S.q_full[i][sl], 128);
-        // 2-deep ring: + the 4 warps whose epilogue stages in the slot (join: softmax WG of head i,
-        // prefill: the Q-prep warps)
-        mbar_init(&S.q_empty[i][sl], (EPI || P.join) ? 1 + 4 : 1);
+        // 2-deep ring: + the 128 threads whose epilogue stages in the slot (join: softmax WG of
+        // head i, prefill: the Q-prep warps)
+        mbar_init(&S.q_empty[i][sl], (EPI || P.join) ? 1 + 128 : 1);
         mbar_init(&S.q_load[i][sl], 1);
       }
     for (int i = 0; i < 2; ++i) {
@@ -1093,7 +1089,7 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
       mbar_init(&S.sched_empty[2 * i], kSchedConsumers);
       mbar_init(&S.sched_empty[2 * i + 1], kSchedConsumers);
       mbar_init(&S.o_done[i][1], 1);
-      mbar_init(&S.o_free[i], 4);  // one arrival per epilogue (Q-prep) warp
+      mbar_init(&S.o_free[i], 128);  // every epilogue (Q-prep) thread
       mbar_init(&S.fin_full[i][0], 128);
       mbar_init(&S.fin_full[i][1], 128);
     }

@@ -18,6 +18,8 @@ dev = torch.device("cuda:0")
 w = inputs.c2(scale=0.125) if cfg == "C2s" else inputs.CONFIGS[cfg]()
 out = out or ("fp32" if w.shape.dtype == "fp32" else "bf16")
 ctx = spanq.Context(w.shape, 4096, device=0, max_position=1 << 15, out_dtype=out)
+if os.environ.get("PROFILE_PDL") == "0":  # sanitizer A/B: attention/combine not launched as PDL dependents
+    ctx.set_option(spanq.OPT_PDL, 0)
 tabs = [runner.device_tables(w.shape, 0, w.seed, dev)]
 for q in w.warmup_queries:
     runner.run_pass(ctx, [q], tabs, dev, release=True)
