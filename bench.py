@@ -150,8 +150,8 @@ def cpu_baseline(budget_s: float = 15.0):
 
 def c2_config(layers: int, world: int, out_dtype: str = "fp32", block_size: int = 64):
     return {"workload": "C2 RAG span query (configs[1]): P512 + 16x1024 plus-fragments + 256 cross, cold cache",
-            "model": f"8B GQA attention shape Hq32/Hkv8/d128, {layers} layers (same synthetic q/k/v per layer, "
-                     "own KV-pool layer each), random tables",
+            "model": f"8B GQA attention shape Hq32/Hkv8/d128, {layers} layers (distinct synthetic q/k/v per "
+                     "layer from per-layer random tables, own KV-pool layer each)",
             "layers": layers, "global_batch": world, "seq_len": 17152, "block_size": block_size,
             "out_dtype": out_dtype, "parallelism": f"dp{world} (independent queries per rank)",
             "l2": "flushed between steps (256 MB write)"}

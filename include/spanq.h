@@ -37,7 +37,7 @@ typedef enum {
   SPQ_EINVAL = 1, /* bad argument, tree shape, op code, arity, empty leaf, negative token   */
   SPQ_ENOMEM = 2, /* the block pool cannot hold the plan's blocks; the plan is rolled back  */
   SPQ_ECUDA = 3,  /* CUDA launch/runtime failure, or no usable sm_100 device               */
-  SPQ_ENCCL = 4,  /* NCCL failure in the library's own exchange (spq_exchange_nccl)          */
+  SPQ_ENCCL = 4,  /* reserved: the library issues no collective (reading R35)     */
   SPQ_ESTATE = 5  /* plan used after release, job/query range out of bounds, wrong mode     */
 } spq_status;
 
