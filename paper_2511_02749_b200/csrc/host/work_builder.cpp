@@ -40,9 +40,22 @@ int32_t add_tiles(const PlanHost& p, const Segment& s, int bs, int32_t key_base,
 // first (units of one item adjacent, so a KV head's tiles are reused from L2), claimed at run time
 // by the CTAs with an atomic counter — a CTA takes the next code when it needs one, so the
 // makespan adapts to the real per-item cost (LPT list scheduling, no cost model in the loop).
-void schedule(const std::vector<double>& item_cost, int units, int num_sms, AttnWorkHost* w) {
+void schedule(const std::vector<double>& item_cost, int units, int num_sms, AttnWorkHost* w,
+              const std::vector<int32_t>* group = nullptr) {
   std::vector<int32_t> order(item_cost.size());
   for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int32_t>(i);
+#ifdef SPANQ_SCHED_GROUP
+  // A/B: the items of one job (segment) claimed together, longest first inside the job, so the
+  // CTAs reading one segment's K/V run at the same time (L2 reuse)
+  if (group != nullptr) {
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+      if ((*group)[a] != (*group)[b]) return (*group)[a] < (*group)[b];
+      return item_cost[a] > item_cost[b];
+    });
+  } else
+#else
+  (void)group;
+#endif
   std::stable_sort(order.begin(), order.end(),
                    [&](int32_t a, int32_t b) { return item_cost[a] > item_cost[b]; });
   const size_t codes = item_cost.size() * static_cast<size_t>(units);
@@ -99,6 +112,7 @@ void build_prefill_work(const PlanHost& p, const WorkOpts& o, int job_begin, int
   *w = AttnWorkHost();
   const int64_t base = p.job_row_off[job_begin];
   std::vector<double> cost;
+  std::vector<int32_t> group;  // the item's job
   for (int j = job_begin; j < job_end; ++j) {
     const Segment& s = p.segs[p.jobs[j]];
     const int32_t t0 = add_tiles(p, s, o.bs, 0, 0, 1, w);
@@ -114,12 +128,13 @@ void build_prefill_work(const PlanHost& p, const WorkOpts& o, int job_begin, int
       it.part = -1;
       w->items.push_back(it);
       cost.push_back(it.tile_end - it.tile_begin + kItemOverhead);
+      group.push_back(j);
     }
     for (int64_t i = s.compute_begin; i < s.tok_len; ++i) w->flops += static_cast<double>(i + 1);
   }
   w->flops *= 4.0 * o.d * o.hq;
   count_subtiles(w);
-  if (o.persistent) schedule(cost, o.units, o.num_sms, w);
+  if (o.persistent) schedule(cost, o.units, o.num_sms, w, &group);
 }
 
 namespace {

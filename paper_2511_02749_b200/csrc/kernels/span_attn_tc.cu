@@ -264,6 +264,9 @@ __device__ void run_producer(const TcParams& P, TcSmem<D>& S, int it_begin, int 
   const CUtensorMap* map = kv == 0 ? &P.tmk : &P.tmv;
   uint32_t n = 0;
   uint32_t tc = 0;
+#ifdef SPANQ_L2HINT
+  const uint64_t pol = policy_evict_last();
+#endif
   ItemSrc<D, EPI> src(P, S, it_begin, it_end, kv == 0);
   for (int code; (code = src.next()) >= 0;) {
     const Unit u = decode(P, code);
@@ -284,9 +287,15 @@ __device__ void run_producer(const TcParams& P, TcSmem<D>& S, int it_begin, int 
           const int32_t y = static_cast<int32_t>(layer_rows + (static_cast<int64_t>(blk) * a.hkv + kvh) * a.bs +
                                                  key % a.bs);
 #pragma unroll
-          for (int c = 0; c < D / 64; ++c)
+          for (int c = 0; c < D / 64; ++c) {
+#ifdef SPANQ_L2HINT  // A/B: K/V pages kept in L2 (each is read by every q tile of its segment)
+            tma_load_2d_hint((kv == 0 ? &S.k[slot][c][0] : &S.v[slot][c][0]) + j * box * 128, map,
+                             &S.kv_full[kv][slot], c * 64, y, pol);
+#else
             tma_load_2d((kv == 0 ? &S.k[slot][c][0] : &S.v[slot][c][0]) + j * box * 128, map, &S.kv_full[kv][slot],
                         c * 64, y);
+#endif
+          }
         }
       }
     }
@@ -662,7 +671,11 @@ __device__ void prefill_epilogue(const TcParams& P, TcSmem<D>& S, uint32_t tmem,
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
+#ifdef SPANQ_L2HINT  // O is written once
+          tma_store_3d_hint(&P.tmo, ch, f32 ? c * 32 : (c / 2) * 64, h, w.row0 + wq * 32, policy_evict_first());
+#else
           tma_store_3d(&P.tmo, ch, f32 ? c * 32 : (c / 2) * 64, h, w.row0 + wq * 32);
+#endif
           bulk_commit();
         }
       } else if (chunk_done && direct) {
@@ -1018,8 +1031,14 @@ __device__ void run_qprep_epi(const TcParams& P, TcSmem<D>& S, uint32_t tmem, in
           uint8_t* dst = q_tile<D>(S, true, x, e);
           mbar_arrive_expect_tx(bar, kQBytes);
 #pragma unroll
-          for (int c = 0; c < D / 64; ++c)
+          for (int c = 0; c < D / 64; ++c) {
+#ifdef SPANQ_L2HINT  // q rows are read once
+            tma_load_3d_hint(dst + c * TcSmem<D>::kChunkBytes, &P.tmq, bar, c * 64, u.head_a + x, w.row0,
+                             policy_evict_first());
+#else
             tma_load_3d(dst + c * TcSmem<D>::kChunkBytes, &P.tmq, bar, c * 64, u.head_a + x, w.row0);
+#endif
+          }
         }
         __syncwarp();
       }
