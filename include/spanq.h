@@ -374,8 +374,12 @@ typedef enum {
                                     units, default 8; 0 = on every growth). Exact either way  */
   SPQ_OPT_PDL = 3,               /* 1 (default): attention/combine launched as programmatic
                                     dependents of the kernel before them; 0: plain launches  */
-  SPQ_OPT_HASH_SCALAR = 4        /* process-wide: 1 = scalar BLAKE2b compression even with AVX2
+  SPQ_OPT_HASH_SCALAR = 4,       /* process-wide: 1 = scalar BLAKE2b compression even with AVX2
                                     (same digests; lets tests cover both), 0 = default        */
+  SPQ_OPT_PAIR = 5               /* 1: prefill of d = 128, GQA 4k, bf16 O on CTA pairs
+                                    (cta_group::2, M = 256); 0 (default, measured faster): one
+                                    CTA per head pair. Read when a plan is created (its prefill
+                                    work list fixes the launch shape)                         */
 } spq_option;
 /* Set a ctx option (applies to later calls). SPQ_EINVAL on an unknown key or a bad value. */
 spq_status spq_set_option(spq_ctx *ctx, int32_t key, double value);

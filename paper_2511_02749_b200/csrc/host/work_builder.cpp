@@ -41,7 +41,7 @@ int32_t add_tiles(const PlanHost& p, const Segment& s, int bs, int32_t key_base,
 // by the CTAs with an atomic counter — a CTA takes the next code when it needs one, so the
 // makespan adapts to the real per-item cost (LPT list scheduling, no cost model in the loop).
 void schedule(const std::vector<double>& item_cost, int units, int num_sms, AttnWorkHost* w,
-              const std::vector<int32_t>* group = nullptr) {
+              const std::vector<int32_t>* group = nullptr, int cluster = 1) {
   std::vector<int32_t> order(item_cost.size());
   for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int32_t>(i);
 #ifdef SPANQ_SCHED_GROUP
@@ -59,7 +59,9 @@ void schedule(const std::vector<double>& item_cost, int units, int num_sms, Attn
   std::stable_sort(order.begin(), order.end(),
                    [&](int32_t a, int32_t b) { return item_cost[a] > item_cost[b]; });
   const size_t codes = item_cost.size() * static_cast<size_t>(units);
-  w->grid = static_cast<int>(std::min<size_t>(num_sms, std::max<size_t>(1, codes)));
+  // a cluster (CTA pair) takes one code at a time: at most num_sms / cluster clusters
+  w->cluster = cluster;
+  w->grid = cluster * static_cast<int>(std::min<size_t>(num_sms / cluster, std::max<size_t>(1, codes)));
   // host-built static lists (boustrophedon waves) measured slower than run-time claims
   // (0.296 vs 0.276 ms); kept for hosts that build lists without a counter
   constexpr bool kStaticSched = false;
@@ -134,7 +136,7 @@ void build_prefill_work(const PlanHost& p, const WorkOpts& o, int job_begin, int
   }
   w->flops *= 4.0 * o.d * o.hq;
   count_subtiles(w);
-  if (o.persistent) schedule(cost, o.units, o.num_sms, w, &group);
+  if (o.persistent) schedule(cost, o.units, o.num_sms, w, &group, o.cluster);
 }
 
 namespace {

@@ -26,6 +26,7 @@ struct AttnWorkHost {
   std::vector<CombineDesc> combine;
   int32_t n_parts = 0;
   int32_t grid = 0;
+  int32_t cluster = 1;  // 2: CTA-pair launch (codes are 4-head units, grid even)
   double flops = 0;  // algorithmic 4·d·Hq·visible pairs
 };
 
@@ -34,7 +35,9 @@ struct WorkOpts {
   int num_sms;       // persistent grid upper bound
   bool allow_split;  // split-KV (join only)
   bool persistent;   // build per-CTA LPT lists
-  int units;         // work units per item: hq (one head each) or hq/2 (GQA head pairs)
+  int units;         // work units per item: hq (one head each), hq/2 (GQA head pairs) or hq/4
+                     // (CTA pairs: 4 heads of a GQA group, cluster = 2)
+  int cluster = 1;   // CTAs per cluster of the launch (grid a multiple of it)
 };
 
 // Prefill jobs [job_begin, job_end): rows relative to job_row_off[job_begin].

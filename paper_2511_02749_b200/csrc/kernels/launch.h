@@ -49,6 +49,7 @@ struct AttnArgs {
   const void* k_pool;
   const void* v_pool;
   const CUtensorMap* tmap_k;  // host copies (bf16 path)
+  const CUtensorMap* tmap_k2; // K with boxes of min(bs, 32) rows (CTA-pair kernel), or null
   const CUtensorMap* tmap_v;
   const CUtensorMap* tmap_q;  // per call: q [rows][hq][d] as 3D {d, hq, rows}, box {64, 1, 128}
   const CUtensorMap* tmap_o;  // per call (fp32 o): 3D {d, hq, rows}, box {32, 1, 32}, SWIZZLE_128B
@@ -60,6 +61,7 @@ struct AttnArgs {
   int max_pos;
   bool out_fp32;  // o is fp32 (else ctx dtype)
   bool paired;    // tcgen05 path: work codes are (item, GQA head pair) — see span_attn_tc.cu
+  int cluster;    // tcgen05 path: 2 = CTA-pair kernel, codes are (item, 4-head unit), grid even
   bool join;      // tcgen05 path: a join launch (2-deep Q ring, epilogue staged in Q slots)
   bool pdl;       // tcgen05 path: launch as a programmatic dependent of the preceding K1
   int poly_mask;  // tcgen05 path: exp2 on MUFU: 0 = ex2 fp32, else ex2.f16x2 (SPQ_OPT_EXP2)

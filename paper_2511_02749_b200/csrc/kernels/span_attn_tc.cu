@@ -53,22 +53,27 @@ constexpr int kThreads = 512;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColS = 0, kColO = 256;  // S_x at kColS + 128x, O_x at kColO + 128x
 
-template <int D>
+template <int D, bool PR = false>
 struct TcSmem {
   static constexpr int kChunks = D / 64;
   static constexpr int kChunkBytes = 128 * 128;  // Q: 128 rows x 128 B per 64-column chunk
   static constexpr int kSubBytes = 64 * 128;     // K/V: 64 keys x 128 B per 64-column chunk
+  // CTA pair (PR): each CTA holds half of every K sub-tile (32 of its 64 keys, all d columns)
+  // and half of every V sub-tile (all 64 keys, its 64 of the d columns), so the rings are twice
+  // as deep in the same bytes
+  static constexpr int kKChunkBytes = (PR ? 32 : 64) * 128;
+  static constexpr int kVChunks = PR ? 1 : kChunks;
   // K(j+2) is needed one step after its slot frees (S(j+2) right after PV(j)), V(j) two steps
   // later. d=128: 3 + 3 slots measured faster than 4 + 2 (A/B on one GPU: prefill 0.248 ->
   // 0.245 ms, join 0.095 -> 0.093 ms) — the V producer no longer stalls the K stream's release
-  static constexpr int kKSlots = D == 64 ? 8 : 3;
-  static constexpr int kVSlots = D == 64 ? 4 : 3;
+  static constexpr int kKSlots = PR ? 7 : (D == 64 ? 8 : 3);
+  static constexpr int kVSlots = PR ? 5 : (D == 64 ? 4 : 3);
   static_assert(kVSlots <= kKSlots, "V uses the first kVSlots of the [K, V][kKSlots] barriers");
   static constexpr int kQSlots = 2;  // slot x = head x (the next epoch's tile is loaded after
                                      // this epoch's last S MMA: ~2 steps before the item ends)
   alignas(1024) uint8_t q[kQSlots][kChunks][kChunkBytes];
-  alignas(1024) uint8_t k[kKSlots][kChunks][kSubBytes];  // ring of 64-key K sub-tiles
-  alignas(1024) uint8_t v[kVSlots][kChunks][kSubBytes];  // ring of 64-key V sub-tiles
+  alignas(1024) uint8_t k[kKSlots][kChunks][kKChunkBytes];  // ring of 64-key K sub-tiles
+  alignas(1024) uint8_t v[kVSlots][kVChunks][kSubBytes];    // ring of 64-key V sub-tiles
   // prefill: epilogue transpose, 2 x 4 KB per softmax warp. join: the second Q slot of each
   // head (q2), so the next fragment's counter-rotated Q is prepared a whole epoch ahead; the
   // join epilogue stages in the Q slot of its item's last epoch instead
@@ -91,6 +96,7 @@ struct TcSmem {
 
 struct TcParams {
   CUtensorMap tmk;
+  CUtensorMap tmk2;  // CTA pair: K boxes of min(bs, 32) rows (each CTA loads 32 keys per sub-tile)
   CUtensorMap tmv;
   CUtensorMap tmq;
   CUtensorMap tmo;   // fp32 O (valid when a.out_fp32)
@@ -111,10 +117,10 @@ struct TcParams {
 // The dynamic shared memory window starts 1024-byte aligned when a kernel has no static shared
 // memory (SWIZZLE_128B operands need it); the launch requests exactly sizeof(TcSmem) (d=128 uses
 // the whole 227 KB), so a misaligned base would be a fatal configuration error: trap loudly.
-template <int D>
-__device__ __forceinline__ TcSmem<D>& smem_ref(uint8_t* raw) {
+template <int D, bool PR>
+__device__ __forceinline__ TcSmem<D, PR>& smem_ref(uint8_t* raw) {
   if (smem_u32(raw) & 1023u) __trap();
-  return *reinterpret_cast<TcSmem<D>*>(raw);
+  return *reinterpret_cast<TcSmem<D, PR>*>(raw);
 }
 
 // Q ring of head x: epoch e uses slot e % depth (depth 1 for prefill, 2 for joins), its
@@ -127,8 +133,8 @@ __device__ __forceinline__ int q_slot(bool J, uint32_t e) {
 __device__ __forceinline__ uint32_t q_par(bool J, uint32_t e) {
   return (J ? e >> 1 : e) & 1;
 }
-template <int D>
-__device__ __forceinline__ uint8_t* q_tile(TcSmem<D>& S, bool J, int x, uint32_t e) {
+template <int D, bool PR>
+__device__ __forceinline__ uint8_t* q_tile(TcSmem<D, PR>& S, bool J, int x, uint32_t e) {
   return q_slot(J, e) ? S.q2(x) : &S.q[x][0][0];
 }
 
@@ -138,7 +144,8 @@ constexpr int kTraceWarps = 16;
 // (profiling builds only: -DSPANQ_PROFILING, tools/; compiled out of the product library)
 __device__ __forceinline__ void trace(const TcParams& P, int, uint32_t& cnt, int ev) {
 #ifdef SPANQ_PROFILING
-  if (P.a.dbg_trace == nullptr || blockIdx.x != 0 || cnt >= 1024) return;
+  // (mode bits 8+: the CTA to record, default 0)
+  if (P.a.dbg_trace == nullptr || blockIdx.x != static_cast<unsigned>(P.dbg_mode >> 8) || cnt >= 1024) return;
   long long* t = P.a.dbg_trace + ((threadIdx.x / 32) * 1024 + cnt) * 2;
   t[0] = ev;
   t[1] = clock64();
@@ -148,7 +155,7 @@ __device__ __forceinline__ void trace(const TcParams& P, int, uint32_t& cnt, int
 // profiling builds: timing variants of the kernel (spq_set_trace); 0 in the product library
 __device__ __forceinline__ int dbg_mode(const TcParams& P) {
 #ifdef SPANQ_PROFILING
-  return P.dbg_mode;
+  return P.dbg_mode & 255;
 #else
   return 0;
 #endif
@@ -159,37 +166,100 @@ struct Unit {
   int head_a, n_heads;
 };
 
+// CTA pair (PR): a unit is the 4 q heads 4x .. 4x+3 of a GQA group (one K/V stream); CTA rank r of
+// the pair runs heads 4x + 2r and 4x + 2r + 1 as its A / B tiles
+template <bool PR>
 __device__ __forceinline__ Unit decode(const TcParams& P, int code) {
   Unit u;
-  const int units = P.paired ? P.a.hq / 2 : P.a.hq;
+  const int units = PR ? P.a.hq / 4 : (P.paired ? P.a.hq / 2 : P.a.hq);
   u.w = P.a.items[code / units];
   const int x = code % units;
-  u.head_a = P.paired ? 2 * x : x;
-  u.n_heads = P.paired ? 2 : 1;
+  if constexpr (PR) {
+    u.head_a = 4 * x + 2 * static_cast<int>(cluster_rank());
+    u.n_heads = 2;
+  } else {
+    u.head_a = P.paired ? 2 * x : x;
+    u.n_heads = P.paired ? 2 : 1;
+  }
   return u;
+}
+
+// Barriers that only the leader CTA of a pair waits on (its MMA issuers / claimer) but that both
+// CTAs arrive on: arrivals go to the leader's copy (cluster scope), waits acquire at cluster scope.
+// Outside a pair these are the plain CTA-local forms.
+template <bool PR>
+__device__ __forceinline__ void arrive_lead(uint64_t* bar) {
+  if constexpr (PR)
+    mbar_arrive_cl(cluster_addr(bar, 0));
+  else
+    mbar_arrive(bar);
+}
+// Warp-wide form (all 32 lanes call it, converged): a pair sends ONE remote arrival per warp
+// (after __syncwarp, which orders the lanes' earlier accesses before lane 0's release) — 32
+// cluster-scope arrivals per warp cost DSMEM round trips on the step's critical path; the leader
+// barrier then counts warps (kLeadUnit = 1 per warp), a single CTA keeps one arrival per thread
+template <bool PR>
+__device__ __forceinline__ void arrive_lead_warp(uint64_t* bar) {
+  if constexpr (PR) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive_cl(cluster_addr(bar, 0));
+  } else {
+    mbar_arrive(bar);
+  }
+}
+template <bool PR>
+__device__ __forceinline__ void wait_lead(uint64_t* bar, uint32_t parity) {
+  if constexpr (PR)
+    mbar_wait_cl(bar, parity);
+  else
+    mbar_wait(bar, parity);
+}
+// spin (no suspend-time hint) — A/B of the wake-up latency on the step's critical path
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// MMA completion: in a pair the commit arrives on the barrier of both CTAs
+template <bool PR>
+__device__ __forceinline__ void commit_x(uint64_t* bar) {
+  if constexpr (PR)
+    mma_commit2(bar);
+  else
+    mma_commit(bar);
 }
 
 // The CTA's sequence of work codes. Static: its slice of cta_items. Dynamic: the K producer
 // claims codes from the launch's counter (atomicAdd) and hands them to the other roles through a
 // smem ring; every role sees the same sequence, ending with -1.
 constexpr int kSchedConsumers = 1 + 2 + 256 + 128;  // V producer, 2 MMA issuers, softmax, Q prep
-template <int D, bool EPI>
+// CTA pair: the leader's ring entry is free once the leader's consumers and the peer's (K and V
+// producers, softmax, Q prep; its MMA warps idle) have read it
+// (arrivals: one per producer / issuer thread, one per softmax / Q-prep warp)
+constexpr int kSchedConsumersPair = (1 + 2 + 8 + 4) + (1 + 1 + 8 + 4);
+template <int D, bool EPI, bool PR>
 struct ItemSrc {
   const TcParams& P;
-  TcSmem<D>& S;
+  TcSmem<D, PR>& S;
   int it, end;
   bool claimer;
+  bool warp_wide;  // the caller is a whole converged warp (softmax, Q prep), not one elected thread
   uint32_t k = 0;
-  __device__ ItemSrc(const TcParams& p, TcSmem<D>& s, int b, int e, bool c) : P(p), S(s), it(b), end(e), claimer(c) {}
+  __device__ ItemSrc(const TcParams& p, TcSmem<D, PR>& s, int b, int e, bool c, bool ww = false)
+      : P(p), S(s), it(b), end(e), claimer(c), warp_wide(ww) {}
   int ahead = -1;  // claimer: the code published one entry ahead of the one it is working on
-  // claim the next code of the launch and publish it as entry n of the ring
+  // claim the next code of the launch and publish it as entry n of the ring (a pair: the leader
+  // claims for both CTAs and publishes into the peer's ring too)
   __device__ int publish(uint32_t n) {
-    constexpr int R = TcSmem<D>::kSched;
+    constexpr int R = TcSmem<D, PR>::kSched;
     const int slot = n % R;
-    mbar_wait(&S.sched_empty[slot], ((n / R) & 1) ^ 1);
+    wait_lead<PR>(&S.sched_empty[slot], ((n / R) & 1) ^ 1);
     const int idx = atomicAdd(P.a.sched, 1);
     const int code = idx < P.a.n_codes ? P.a.cta_items[idx] : -1;
     *reinterpret_cast<volatile int32_t*>(&S.sched_code[slot]) = code;
+    if constexpr (PR) {
+      st_cluster_u32(cluster_addr(&S.sched_code[slot], 1), static_cast<uint32_t>(code));
+      mbar_arrive_cl(cluster_addr(&S.sched_full[slot], 1));
+    }
     mbar_arrive(&S.sched_full[slot]);
     return code;
   }
@@ -205,15 +275,21 @@ struct ItemSrc {
       ++k;
       return mine;
     }
-    constexpr int R = TcSmem<D>::kSched;
+    constexpr int R = TcSmem<D, PR>::kSched;
     const int slot = k % R;
     const uint32_t par = (k / R) & 1;
     ++k;
     int code;
     {
-      mbar_wait(&S.sched_full[slot], par);
+      if constexpr (PR)
+        mbar_wait_cl(&S.sched_full[slot], par);  // the peer's entries are written by the leader
+      else
+        mbar_wait(&S.sched_full[slot], par);
       code = *reinterpret_cast<volatile int32_t*>(&S.sched_code[slot]);
-      mbar_arrive(&S.sched_empty[slot]);
+      if (warp_wide)
+        arrive_lead_warp<PR>(&S.sched_empty[slot]);
+      else
+        arrive_lead<PR>(&S.sched_empty[slot]);
     }
     return code;
   }
@@ -248,28 +324,30 @@ __device__ __forceinline__ void ex2_pair_f16(float x0, float x1, float& p0, floa
 // after PV(j); V(j) is needed two steps later). Sub-tile s goes to slot s % (ring depth).
 // Each sub-tile is 64/bs paged blocks (bs <= 64) or half of one 128-row block, gathered by TMA
 // boxes {64 columns, min(bs, 64) rows}.
-template <int D, bool EPI>
-__device__ void run_producer(const TcParams& P, TcSmem<D>& S, int it_begin, int it_end, int kv) {
+template <int D, bool EPI, bool PR>
+__device__ void run_producer(const TcParams& P, TcSmem<D, PR>& S, int it_begin, int it_end, int kv) {
   const AttnArgs& a = P.a;
   // programmatic dependent launch: the pages this launch reads are written by the preceding
   // rope_kv_write — everything before this point (barriers, TMEM, work claims, Q loads and
   // rotation) may overlap that kernel's tail; the pool is read only after it has completed
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int kSlots = kv == 0 ? TcSmem<D>::kKSlots : TcSmem<D>::kVSlots;
+  const int kSlots = kv == 0 ? TcSmem<D, PR>::kKSlots : TcSmem<D, PR>::kVSlots;
   const int group = a.hq / a.hkv;
   const int box = min(a.bs, 64);
   const int bps = 64 / box;  // boxes per sub-tile
-  constexpr uint32_t kSubTileBytes = 64 * D * 2;
+  constexpr uint32_t kSubTileBytes = 64 * D * 2;  // (a pair: both CTAs' halves together)
   const int64_t layer_rows = static_cast<int64_t>(a.layer) * a.nblk * a.hkv * a.bs;
-  const CUtensorMap* map = kv == 0 ? &P.tmk : &P.tmv;
+  const CUtensorMap* map = kv == 0 ? (PR ? &P.tmk2 : &P.tmk) : &P.tmv;
+  const uint32_t rank = PR ? cluster_rank() : 0;
   uint32_t n = 0;
   uint32_t tc = 0;
 #ifdef SPANQ_L2HINT
   const uint64_t pol = policy_evict_last();
 #endif
-  ItemSrc<D, EPI> src(P, S, it_begin, it_end, kv == 0);
+  // a pair: the leader claims the work codes (K producer), the peer's K producer consumes them
+  ItemSrc<D, EPI, PR> src(P, S, it_begin, it_end, kv == 0 && rank == 0);
   for (int code; (code = src.next()) >= 0;) {
-    const Unit u = decode(P, code);
+    const Unit u = decode<PR>(P, code);
     const int kvh = u.head_a / group;
     for (int t = u.w.tile_begin; t < u.w.tile_end; ++t) {
       const KvTile tl = a.tiles[t];
@@ -279,6 +357,33 @@ __device__ void run_producer(const TcParams& P, TcSmem<D>& S, int it_begin, int 
         const int slot = n % kSlots;
         mbar_wait(&S.kv_empty[kv][slot], ((n / kSlots) & 1) ^ 1);
         trace(P, 0, tc, 10 + kv);  // 10: K load issued, 11: V load issued
+        if constexpr (PR) {
+          // this CTA's half: K keys [64h + 32 rank, +32) (all d columns), V all 64 keys of its
+          // d columns [64 rank, +64); completion counted on the leader's barrier, which expects
+          // both halves
+          if (rank == 0) mbar_arrive_expect_tx(&S.kv_full[kv][slot], kSubTileBytes);
+          const uint32_t bar = cluster_addr(&S.kv_full[kv][slot], 0);
+          if (kv == 0) {
+            const int kbox = min(a.bs, 32);
+            for (int j = 0; j < 32 / kbox; ++j) {
+              const int key = 64 * h + 32 * static_cast<int>(rank) + j * kbox;
+              const int32_t blk = a.tile_blocks[tl.blk_off + key / a.bs];
+              const int32_t y =
+                  static_cast<int32_t>(layer_rows + (static_cast<int64_t>(blk) * a.hkv + kvh) * a.bs + key % a.bs);
+#pragma unroll
+              for (int c = 0; c < D / 64; ++c) tma_load_2d_pair(&S.k[slot][c][0] + j * kbox * 128, map, bar, c * 64, y);
+            }
+          } else {
+            for (int j = 0; j < bps; ++j) {
+              const int key = 64 * h + j * box;
+              const int32_t blk = a.tile_blocks[tl.blk_off + key / a.bs];
+              const int32_t y =
+                  static_cast<int32_t>(layer_rows + (static_cast<int64_t>(blk) * a.hkv + kvh) * a.bs + key % a.bs);
+              tma_load_2d_pair(&S.v[slot][0][0] + j * box * 128, map, bar, 64 * static_cast<int>(rank), y);
+            }
+          }
+          continue;
+        }
         mbar_arrive_expect_tx(&S.kv_full[kv][slot], kSubTileBytes);
         for (int j = 0; j < bps; ++j) {
           // key 64h + j*box of the tile: block (64h + j*box) / bs, row offset (64h + j*box) % bs
@@ -313,13 +418,17 @@ struct SubCursor {
   int t, h;  // KV tile, half (keys [64h, 64h+64))
 };
 
-template <int D, bool EPI>
-__device__ void run_mma(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_begin, int it_end, int x) {
+// A pair (PR): only the leader runs this; its M = 256 MMAs take A rows 0-127 from its own smem /
+// TMEM and rows 128-255 from the peer's at the same offsets, B halves from both, and write D into
+// both CTAs' TMEM; commits arrive on both CTAs' barriers.
+template <int D, bool EPI, bool PR>
+__device__ void run_mma(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, int it_begin, int it_end, int x) {
   const AttnArgs& a = P.a;
   const bool J = EPI || P.join != 0;  // 2-deep Q ring
-  constexpr int kKS = TcSmem<D>::kKSlots, kVS = TcSmem<D>::kVSlots;
-  constexpr uint32_t idS = idesc_bf16_f32(128, 64, false, false);
-  constexpr uint32_t idO = idesc_bf16_f32(128, D, false, true);
+  using Sm = TcSmem<D, PR>;
+  constexpr int kKS = Sm::kKSlots, kVS = Sm::kVSlots;
+  constexpr uint32_t idS = idesc_bf16_f32(PR ? 256 : 128, 64, false, false);
+  constexpr uint32_t idO = idesc_bf16_f32(PR ? 256 : 128, D, false, true);
   uint32_t jg = 0;  // sub-tiles whose PV has been issued (global): S buffer j & 1, V slot j
   uint32_t ep = 0;    // Q epochs started
   uint32_t qcur = 0;  // the epoch whose Q tile the S MMAs read
@@ -327,12 +436,12 @@ __device__ void run_mma(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_b
   uint32_t tc = 0;
   auto wait_kv = [&](int kv, uint32_t n) {
     const uint32_t ns = kv == 0 ? kKS : kVS;
-    mbar_wait(&S.kv_full[kv][n % ns], (n / ns) & 1);
+    wait_lead<PR>(&S.kv_full[kv][n % ns], (n / ns) & 1);
     tc_fence_after();
   };
-  ItemSrc<D, EPI> src(P, S, it_begin, it_end, false);
+  ItemSrc<D, EPI, PR> src(P, S, it_begin, it_end, false);
   for (int code; (code = src.next()) >= 0;) {
-    const Unit u = decode(P, code);
+    const Unit u = decode<PR>(P, code);
     if (x >= u.n_heads) continue;  // unpaired launch: the B issuer idles
     const int tb = u.w.tile_begin, te = u.w.tile_end;
     auto nsub = [&](int t) { return a.tiles[t].n_valid > 64 ? 2 : 1; };
@@ -347,29 +456,32 @@ __device__ void run_mma(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_b
     // Q: slot x holds head x's tile of the current epoch (an item or a change of rot_delta)
     auto release_q = [&]() {
       const int sl = q_slot(J, qcur);
-      mma_commit(&S.q_empty[x][sl]);
+      commit_x<PR>(&S.q_empty[x][sl]);
     };
     auto issue_s = [&]() {
       const int t = cs.t;
       if (cs.h == 0 && (t == tb || a.tiles[t].rot_delta != a.tiles[t - 1].rot_delta)) {
         if (t != tb) release_q();  // the previous epoch's Q tile: free once its S MMAs are done
-        mbar_wait(&S.q_full[x][q_slot(J, ep)], q_par(J, ep));
+        wait_lead<PR>(&S.q_full[x][q_slot(J, ep)], q_par(J, ep));
         trace(P, 1, tc, 21);  // 21: Q ready for new epoch
         qcur = ep++;
       }
       wait_kv(0, js);
       trace(P, 1, tc, 22);  // 22: K ready
-      const uint32_t qbase = smem_u32(q_tile<D>(S, J, x, qcur));
+      const uint32_t qbase = smem_u32(q_tile<D, PR>(S, J, x, qcur));
       const uint32_t kb = smem_u32(&S.k[js % kKS][0][0]);
       const int buf = js & 1;
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
-        mma_ss(tmem + kColS + 128 * x + 64 * buf,
-               desc_sw128(qbase + (kk / 4) * TcSmem<D>::kChunkBytes + (kk % 4) * 32, 16, 1024),
-               desc_sw128(kb + (kk / 4) * TcSmem<D>::kSubBytes + (kk % 4) * 32, 16, 1024), idS, kk > 0 ? 1u : 0u);
+        const uint64_t ad = desc_sw128(qbase + (kk / 4) * Sm::kChunkBytes + (kk % 4) * 32, 16, 1024);
+        const uint64_t bd = desc_sw128(kb + (kk / 4) * Sm::kKChunkBytes + (kk % 4) * 32, 16, 1024);
+        if constexpr (PR)
+          mma2_ss(tmem + kColS + 128 * x + 64 * buf, ad, bd, idS, kk > 0 ? 1u : 0u);
+        else
+          mma_ss(tmem + kColS + 128 * x + 64 * buf, ad, bd, idS, kk > 0 ? 1u : 0u);
       }
-      mma_commit(&S.s_full[x][buf]);
-      mma_commit(&S.kv_empty[0][js % kKS]);  // K_js (one of the heads' two arrivals)
+      commit_x<PR>(&S.s_full[x][buf]);
+      commit_x<PR>(&S.kv_empty[0][js % kKS]);  // K_js (one of the heads' two arrivals)
       advance(cs);
       ++js;
       if (cs.t >= te) release_q();
@@ -382,25 +494,83 @@ __device__ void run_mma(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_b
       const int buf = j & 1;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
-        const uint64_t vd = desc_sw128(vb + kk * 2048, TcSmem<D>::kSubBytes, 1024);
-        mma_ts(tmem + kColO + 128 * x, tmem + kColS + 128 * x + 64 * buf + kk * 8, vd, idO,
-               (!first || kk > 0) ? 1u : 0u);
+        const uint64_t vd = desc_sw128(vb + kk * 2048, Sm::kSubBytes, 1024);
+        if constexpr (PR)
+          mma2_ts(tmem + kColO + 128 * x, tmem + kColS + 128 * x + 64 * buf + kk * 8, vd, idO,
+                  (!first || kk > 0) ? 1u : 0u);
+        else
+          mma_ts(tmem + kColO + 128 * x, tmem + kColS + 128 * x + 64 * buf + kk * 8, vd, idO,
+                 (!first || kk > 0) ? 1u : 0u);
       }
-      mma_commit(&S.o_done[x][j & 1]);
-      mma_commit(&S.kv_empty[1][j % kVS]);  // V_j
+      commit_x<PR>(&S.o_done[x][j & 1]);
+      commit_x<PR>(&S.kv_empty[1][j % kVS]);  // V_j
     };
+    if constexpr (EPI) {
+      // prefill items are one epoch (rot_delta 0 on every tile) of w.n_sub sub-tiles: the issuer
+      // walks them by count, with no work-list reads on its critical path (each tile read is an
+      // L1-miss-prone global load: ~40-600 cycles per step otherwise)
+      const int ns = u.w.n_sub;
+      int si = 0;  // S sub-tiles issued for this item
+      auto issue_s_cnt = [&]() {
+        if (si == 0) {
+          wait_lead<PR>(&S.q_full[x][q_slot(J, ep)], q_par(J, ep));
+          trace(P, 1, tc, 21);  // 21: Q ready for new epoch
+          qcur = ep++;
+        }
+        wait_kv(0, js);
+        trace(P, 1, tc, 22);  // 22: K ready
+        const uint32_t qbase = smem_u32(q_tile<D, PR>(S, J, x, qcur));
+        const uint32_t kb = smem_u32(&S.k[js % kKS][0][0]);
+        const int buf = js & 1;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint64_t ad = desc_sw128(qbase + (kk / 4) * Sm::kChunkBytes + (kk % 4) * 32, 16, 1024);
+          const uint64_t bd = desc_sw128(kb + (kk / 4) * Sm::kKChunkBytes + (kk % 4) * 32, 16, 1024);
+          if constexpr (PR)
+            mma2_ss(tmem + kColS + 128 * x + 64 * buf, ad, bd, idS, kk > 0 ? 1u : 0u);
+          else
+            mma_ss(tmem + kColS + 128 * x + 64 * buf, ad, bd, idS, kk > 0 ? 1u : 0u);
+        }
+        commit_x<PR>(&S.s_full[x][buf]);
+        commit_x<PR>(&S.kv_empty[0][js % kKS]);
+        ++js;
+        if (++si == ns) release_q();
+      };
+      for (int i = 0; i < 2 && si < ns; ++i) issue_s_cnt();
+      for (int pi = 0; pi < ns; ++pi) {
+        const uint32_t j = jg;
+#ifdef SPANQ_SPIN_ISSUER
+        if constexpr (!PR) mbar_wait_spin(&S.p_full[x][j & 1], (j >> 1) & 1); else
+#endif
+        wait_lead<PR>(&S.p_full[x][j & 1], (j >> 1) & 1);
+        trace(P, 1, tc, 20);  // 20: P ready
+        if (pi == 0 && n_items > 0) {
+          // the previous item's O has been drained by the epilogue warps. Completion n_items - 1
+          // is the latest possible one (this thread waited for n_items - 2 before the previous
+          // item's first PV), so the parity wait cannot be lapped
+          wait_lead<PR>(&S.o_free[x], (n_items - 1) & 1);
+          tc_fence_after();
+          trace(P, 1, tc, 26);  // 26: O free for the next item
+        }
+        issue_pv(j, pi == 0);
+        if (si < ns) issue_s_cnt();
+        ++jg;
+      }
+      ++n_items;
+      continue;
+    }
     // prologue: S for the first two sub-tiles
     for (int i = 0; i < 2 && cs.t < te; ++i) issue_s();
     bool first = true;
     while (cp.t < te) {
       const uint32_t j = jg;
-      mbar_wait(&S.p_full[x][j & 1], (j >> 1) & 1);
+      wait_lead<PR>(&S.p_full[x][j & 1], (j >> 1) & 1);
       trace(P, 1, tc, 20);  // 20: P ready
       if (EPI && first && n_items > 0) {
         // prefill: the previous item's O has been drained by the epilogue warps. Completion
         // n_items - 1 is the latest possible one (this thread waited for n_items - 2 before the
         // previous item's first PV), so the parity wait cannot be lapped
-        mbar_wait(&S.o_free[x], (n_items - 1) & 1);
+        wait_lead<PR>(&S.o_free[x], (n_items - 1) & 1);
         tc_fence_after();
         trace(P, 1, tc, 26);  // 26: O free for the next item
       }
@@ -487,8 +657,8 @@ struct Finished {
 // Epilogue of one finished item: wait for its last PV, read O from TMEM, normalise, store. Each warp stages 32 rows x 32 fp32 columns in its 4 KB SWIZZLE_128B buffer
 // and one lane hands it to a TMA bulk store (the warp only waits until the TMA has READ the
 // buffer before reusing it, never for the HBM write).
-template <int D>
-__device__ __forceinline__ void epilogue(const TcParams& P, TcSmem<D>& S, uint32_t ocol, int x, const Finished& f,
+template <int D, bool PR>
+__device__ __forceinline__ void epilogue(const TcParams& P, TcSmem<D, PR>& S, uint32_t ocol, int x, const Finished& f,
                                          uint32_t& tc, bool tr) {
   const AttnArgs& a = P.a;
   const bool J = P.join != 0;
@@ -509,7 +679,7 @@ __device__ __forceinline__ void epilogue(const TcParams& P, TcSmem<D>& S, uint32
   // the Q slot of the item's last epoch (its S MMAs are done: they precede the last PV), handed
   // back to the Q prep only once the stores below have read it
   const int kBufs = (J && D == 64) ? 1 : 2;
-  float* const stg2 = J ? reinterpret_cast<float*>(q_tile<D>(S, J, x, f.elast)) + wr * kBufs * 1024
+  float* const stg2 = J ? reinterpret_cast<float*>(q_tile<D, PR>(S, J, x, f.elast)) + wr * kBufs * 1024
                         : &S.stage[x * 4 + wr][0][0];
   // TMA store for whole 32-row slices (and for split partials, whose padding rows are never
   // read); a slice that ends inside this item's rows is written directly (the next rows belong
@@ -598,8 +768,8 @@ __device__ __forceinline__ void epilogue(const TcParams& P, TcSmem<D>& S, uint32
 // warp's quarter of the slot (8 KB at d=128, 4 KB at d=64) as 4 KB chunks of 32 rows x 128 B,
 // SWIZZLE_128B (fp32: 32 columns per chunk, bf16: 64); bf16 O always fits, fp32 O cycles through
 // the chunk buffers (a chunk waits for the store of the chunk that used its buffer before).
-template <int D>
-__device__ void prefill_epilogue(const TcParams& P, TcSmem<D>& S, uint32_t tmem, const Unit& u, uint32_t jlast,
+template <int D, bool PR>
+__device__ void prefill_epilogue(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, const Unit& u, uint32_t jlast,
                                  uint32_t k, uint32_t& tc) {
   const AttnArgs& a = P.a;
   const WorkItem& w = u.w;
@@ -615,7 +785,7 @@ __device__ void prefill_epilogue(const TcParams& P, TcSmem<D>& S, uint32_t tmem,
   constexpr int kBufs = D / 64;  // 4 KB chunk buffers per warp in its quarter of a Q slot
   const int n_chunks = f32 ? D / 32 : D / 64;
   for (int x = 0; x < u.n_heads; ++x) {
-    uint8_t* const stg = q_tile<D>(S, true, x, k) + wq * kBufs * 4096;
+    uint8_t* const stg = q_tile<D, PR>(S, true, x, k) + wq * kBufs * 4096;
     mbar_wait(&S.fin_full[x][k & 1], (k >> 1) & 1);
     const float inv = S.fin_inv[x][k & 1][r];
     if (tr) trace(P, 4, tc, 60 + 4 * x);  // 60/64: row stats of head A/B ready
@@ -634,7 +804,7 @@ __device__ void prefill_epilogue(const TcParams& P, TcSmem<D>& S, uint32_t tmem,
       if (c + 1 == D / 32) {
         // the last TMEM load has landed (waited at the end of the previous iteration): O_x is free
         tc_fence_before();
-        mbar_arrive(&S.o_free[x]);  // every lane: its TMEM loads and fin_inv read are done
+        arrive_lead_warp<PR>(&S.o_free[x]);  // every lane: its TMEM loads and fin_inv read are done
         if (tr) trace(P, 4, tc, 62 + 4 * x);  // 62/66: O drained (o_free)
       }
       const int chunk = f32 ? c : c / 2;
@@ -707,8 +877,8 @@ __device__ void prefill_epilogue(const TcParams& P, TcSmem<D>& S, uint32_t tmem,
   }
 }
 
-template <int D, int PM, bool EPI>
-__device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_begin, int it_end, int x) {
+template <int D, int PM, bool EPI, bool PR>
+__device__ void run_softmax(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, int it_begin, int it_end, int x) {
   const AttnArgs& a = P.a;
   const bool J = P.join != 0;
   const int r = threadIdx.x & 127;  // row within the tile == TMEM lane
@@ -720,9 +890,9 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
   uint32_t ni = 0;             // prefill: items finished by this WG (fin_inv buffer ni & 1)
   uint32_t tc = 0;
   const bool tr = (threadIdx.x & 31) == 0;
-  ItemSrc<D, EPI> src(P, S, it_begin, it_end, false);
+  ItemSrc<D, EPI, PR> src(P, S, it_begin, it_end, false, true);
   for (int code; (code = src.next()) >= 0;) {
-    const Unit u = decode(P, code);
+    const Unit u = decode<PR>(P, code);
     if (x >= u.n_heads) continue;  // single-head unit: WG B idles
     const WorkItem& w = u.w;
     const bool valid = r < w.n_rows;
@@ -743,7 +913,11 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
         const uint32_t scol = tmem + lane_base + kColS + 128 * x + 64 * buf;
         // key index i of this sub-tile is visible iff i <= lim
         const int lim = min(tl.n_valid - 1, tl.causal ? p - tl.key_pos0 : kTileKeys - 1) - 64 * hh;
+#ifdef SPANQ_SPIN_SOFTMAX
+        mbar_wait_spin(&S.s_full[x][buf], (js >> 1) & 1);
+#else
         mbar_wait(&S.s_full[x][buf], (js >> 1) & 1);
+#endif
         if (tr) trace(P, 2 + x, tc, 30);  // 30: S ready
         tc_fence_after();
         // masks only on partial sub-tiles
@@ -782,7 +956,7 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
         }
         if (tr) trace(P, 2 + x, tc, 31);  // 31: P written
         tc_fence_before();
-        mbar_arrive(&S.p_full[x][buf]);
+        arrive_lead_warp<PR>(&S.p_full[x][buf]);
         first = false;
       }
     }
@@ -807,7 +981,7 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int 
     f.n_heads = u.n_heads;
     f.jlast = js - 1;
     f.elast = ecur;
-    epilogue<D>(P, S, ocol, x, f, tc, tr);
+    epilogue<D, PR>(P, S, ocol, x, f, tc, tr);
   }
   tc_fence_before();
 }
@@ -910,8 +1084,8 @@ __device__ __forceinline__ void rotate_q_tile(uint8_t* qs_base, const float2* ro
   }
 }
 
-template <int D, bool EPI>
-__device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_end) {
+template <int D, bool EPI, bool PR>
+__device__ void run_qprep(const TcParams& P, TcSmem<D, PR>& S, int it_begin, int it_end) {
   const AttnArgs& a = P.a;
   const bool J = P.join != 0;
   const int r = threadIdx.x & 127;
@@ -922,12 +1096,12 @@ __device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_
   uint32_t tc = 0;
   uint32_t load_phase = 0;  // bit 2x + s: parity of the next q_load[x][s] completion
   const bool tr = lane == 0;
-  ItemSrc<D, EPI> src(P, S, it_begin, it_end, false);
+  ItemSrc<D, EPI, PR> src(P, S, it_begin, it_end, false, true);
   const bool early_b = (P.qprep_mode & 1) != 0, prefetch = (P.qprep_mode & 2) != 0;
   // thread 0: TMA of head x's pre-RoPE tile into its slot of epoch ep
   auto load = [&](int x, const Unit& u) {
     uint64_t* bar = &S.q_load[x][q_slot(J, ep)];
-    uint8_t* dst = q_tile<D>(S, J, x, ep);
+    uint8_t* dst = q_tile<D, PR>(S, J, x, ep);
     mbar_arrive_expect_tx(bar, kQBytes);
 #pragma unroll
     for (int c = 0; c < D / 64; ++c)
@@ -935,7 +1109,7 @@ __device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_
   };
   int code = src.next();
   while (code >= 0) {
-    const Unit u = decode(P, code);
+    const Unit u = decode<PR>(P, code);
     const WorkItem& w = u.w;
     const int my_row = wq * 32 + lane;  // this lane's row position, shuffled to the warp per row
     const int my_pos = my_row < w.n_rows ? a.pos[static_cast<int64_t>(w.row0) + my_row] : 0;
@@ -977,20 +1151,20 @@ __device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_
           mbar_wait(&S.q_load[x][sl], (load_phase >> bit) & 1);
           load_phase ^= 1u << bit;
           if (tr) trace(P, 4, tc, 44 + x);  // 44/45: Q tile A/B loaded
-          rotate_q_tile<D>(q_tile<D>(S, J, x, ep), a.rope, my_pos, my_row < w.n_rows, rot, a.max_pos);
+          rotate_q_tile<D>(q_tile<D, PR>(S, J, x, ep), a.rope, my_pos, my_row < w.n_rows, rot, a.max_pos);
           fence_proxy_async_smem();
         } else {
           mbar_wait(&S.q_empty[x][sl], epar);
         }
         if (tr) trace(P, 4, tc, 42 + x);  // 42/43: Q tile A/B written
-        mbar_arrive(&S.q_full[x][sl]);
+        arrive_lead_warp<PR>(&S.q_full[x][sl]);
       }
       ++ep;
     }
     // the next item's code is known long before its Q slots free: warm L2 with its q tiles
     code = src.next();
     if (prefetch && code >= 0 && r == 0 && work) {
-      const Unit n = decode(P, code);
+      const Unit n = decode<PR>(P, code);
       for (int x = 0; x < n.n_heads; ++x)
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) tma_prefetch_3d(&P.tmq, c * 64, n.head_a + x, n.w.row0);
@@ -1004,8 +1178,8 @@ __device__ void run_qprep(const TcParams& P, TcSmem<D>& S, int it_begin, int it_
 // (prefill_epilogue, staged in that item's own slot). Order: Q(0); then per item k: Q(k+1), the
 // epilogue of k. Q(k+1) waits for slot (k+1) & 1, released by the epilogue of k - 1 (done in the
 // previous iteration) and item k - 1's last S MMA; the epilogue of k waits for item k's last PV.
-template <int D, bool EPI>
-__device__ void run_qprep_epi(const TcParams& P, TcSmem<D>& S, uint32_t tmem, int it_begin, int it_end) {
+template <int D, bool EPI, bool PR>
+__device__ void run_qprep_epi(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, int it_begin, int it_end) {
   const AttnArgs& a = P.a;
   const int lane = threadIdx.x & 31;
   const int wq = (threadIdx.x / 32) & 3;
@@ -1013,7 +1187,7 @@ __device__ void run_qprep_epi(const TcParams& P, TcSmem<D>& S, uint32_t tmem, in
   uint32_t tc = 0;
   uint32_t load_phase = 0;  // bit 2x + s: parity of the next q_load[x][s] completion
   const bool tr = lane == 0;
-  ItemSrc<D, EPI> src(P, S, it_begin, it_end, false);
+  ItemSrc<D, EPI, PR> src(P, S, it_begin, it_end, false, true);
   const int my_row = wq * 32 + lane;
   // prepare the (single-epoch) Q tiles of item e in slot e & 1
   auto prep = [&](const Unit& u, uint32_t e) {
@@ -1028,7 +1202,7 @@ __device__ void run_qprep_epi(const TcParams& P, TcSmem<D>& S, uint32_t tmem, in
         if (tr) trace(P, 4, tc, 40 + x);  // 40/41: slot free for head A/B
         if (lane == 0) {
           uint64_t* bar = &S.q_load[x][sl];
-          uint8_t* dst = q_tile<D>(S, true, x, e);
+          uint8_t* dst = q_tile<D, PR>(S, true, x, e);
           mbar_arrive_expect_tx(bar, kQBytes);
 #pragma unroll
           for (int c = 0; c < D / 64; ++c) {
@@ -1048,15 +1222,15 @@ __device__ void run_qprep_epi(const TcParams& P, TcSmem<D>& S, uint32_t tmem, in
       mbar_wait(&S.q_load[x][sl], (load_phase >> bit) & 1);
       load_phase ^= 1u << bit;
       if (tr) trace(P, 4, tc, 44 + x);  // 44/45: Q tile A/B loaded
-      rotate_q_tile<D>(q_tile<D>(S, true, x, e), a.rope, my_pos, my_row < w.n_rows, 0, a.max_pos);
+      rotate_q_tile<D>(q_tile<D, PR>(S, true, x, e), a.rope, my_pos, my_row < w.n_rows, 0, a.max_pos);
       fence_proxy_async_smem();
       if (tr) trace(P, 4, tc, 42 + x);  // 42/43: Q tile A/B written
-      mbar_arrive(&S.q_full[x][sl]);
+      arrive_lead_warp<PR>(&S.q_full[x][sl]);
     }
   };
   int code = src.next();
   if (code < 0) return;
-  Unit cur = decode(P, code);
+  Unit cur = decode<PR>(P, code);
   uint32_t jtot = static_cast<uint32_t>(cur.w.n_sub);
   uint32_t cur_jlast = jtot - 1;
   prep(cur, 0);
@@ -1066,32 +1240,40 @@ __device__ void run_qprep_epi(const TcParams& P, TcSmem<D>& S, uint32_t tmem, in
     Unit nxt{};
     uint32_t nxt_jlast = 0;
     if (more) {
-      nxt = decode(P, code);
+      nxt = decode<PR>(P, code);
       jtot += static_cast<uint32_t>(nxt.w.n_sub);
       nxt_jlast = jtot - 1;
       prep(nxt, k + 1);
     }
-    prefill_epilogue<D>(P, S, tmem, cur, cur_jlast, k, tc);
+    prefill_epilogue<D, PR>(P, S, tmem, cur, cur_jlast, k, tc);
     if (!more) break;
     cur = nxt;
     cur_jlast = nxt_jlast;
   }
 }
 
-template <int D, int PM, bool EPI>
+// PR: a CTA pair (cluster of 2 on one TPC, cta_group::2 MMAs issued by the leader); each CTA
+// initialises every barrier, the leader's copies of q_full / p_full / o_free / sched_empty count
+// both CTAs' arrivals
+template <int D, int PM, bool EPI, bool PR>
 __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_constant__ TcParams P) {
   extern __shared__ uint8_t smem_raw[];
-  TcSmem<D>& S = smem_ref<D>(smem_raw);
+  TcSmem<D, PR>& S = smem_ref<D, PR>(smem_raw);
   const int warp = threadIdx.x / 32;
+  const uint32_t rank = PR ? cluster_rank() : 0;
+  constexpr uint32_t kBoth = PR ? 2 : 1;  // CTAs arriving on a leader barrier
+  // arrivals of a 128-thread role on a leader barrier: one per thread, or in a pair one per warp
+  // of each CTA (arrive_lead_warp)
+  constexpr uint32_t kRole = PR ? 4 * 2 : 128;
   if (threadIdx.x == 0) {
     for (int kv = 0; kv < 2; ++kv)
-      for (int i = 0; i < TcSmem<D>::kKSlots; ++i) {
+      for (int i = 0; i < TcSmem<D, PR>::kKSlots; ++i) {
         mbar_init(&S.kv_full[kv][i], 1);
         mbar_init(&S.kv_empty[kv][i], P.paired ? 2 : 1);  // released by each head's issuer
       }
-    for (int i = 0; i < TcSmem<D>::kQSlots; ++i)
+    for (int i = 0; i < TcSmem<D, PR>::kQSlots; ++i)
       for (int sl = 0; sl < 2; ++sl) {
-        mbar_init(&S.q_full[i][sl], 128);
+        mbar_init(&S.q_full[i][sl], kRole);
         // 2-deep ring: + the 128 threads whose epilogue stages in the slot (join: softmax WG of
         // head i, prefill: the Q-prep warps)
         mbar_init(&S.q_empty[i][sl], (EPI || P.join) ? 1 + 128 : 1);
@@ -1100,28 +1282,36 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
     for (int i = 0; i < 2; ++i) {
       for (int b = 0; b < 2; ++b) {
         mbar_init(&S.s_full[i][b], 1);
-        mbar_init(&S.p_full[i][b], 128);
+        mbar_init(&S.p_full[i][b], kRole);
       }
       mbar_init(&S.o_done[i][0], 1);
       mbar_init(&S.sched_full[2 * i], 1);
       mbar_init(&S.sched_full[2 * i + 1], 1);
-      mbar_init(&S.sched_empty[2 * i], kSchedConsumers);
-      mbar_init(&S.sched_empty[2 * i + 1], kSchedConsumers);
+      mbar_init(&S.sched_empty[2 * i], PR ? kSchedConsumersPair : kSchedConsumers);
+      mbar_init(&S.sched_empty[2 * i + 1], PR ? kSchedConsumersPair : kSchedConsumers);
       mbar_init(&S.o_done[i][1], 1);
-      mbar_init(&S.o_free[i], 128);  // every epilogue (Q-prep) thread
+      mbar_init(&S.o_free[i], kRole);  // every epilogue (Q-prep) thread (a pair: warp)
       mbar_init(&S.fin_full[i][0], 128);
       mbar_init(&S.fin_full[i][1], 128);
     }
     fence_barrier_init();
   }
   if (warp == 0 && (threadIdx.x & 31) == 0) {
-    tma_prefetch_desc(&P.tmk);
+    tma_prefetch_desc(PR ? &P.tmk2 : &P.tmk);
     tma_prefetch_desc(&P.tmv);
     tma_prefetch_desc(&P.tmq);
   }
-  if (warp == 2) tmem_alloc<kTmemCols>(&S.tmem_base);
+  if (warp == 2) {
+    if constexpr (PR)
+      tmem_alloc2<kTmemCols>(&S.tmem_base);
+    else
+      tmem_alloc<kTmemCols>(&S.tmem_base);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PR)
+    cluster_sync_all();  // both CTAs' barriers are initialised before any remote arrive
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
   const bool dyn = P.a.sched != nullptr;
@@ -1137,28 +1327,31 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
   if (warp < 4) {
     reg_dealloc<56>();
     if (warp == 0 || warp == 3) {
-      if (elect_one()) run_producer<D, EPI>(P, S, it_begin, it_end, warp == 0 ? 0 : 1);
-    } else {
-      if (elect_one()) run_mma<D, EPI>(P, S, tmem, it_begin, it_end, warp - 1);
+      if (elect_one()) run_producer<D, EPI, PR>(P, S, it_begin, it_end, warp == 0 ? 0 : 1);
+    } else if (rank == 0) {  // a pair: the leader issues the MMAs of both CTAs
+      if (elect_one()) run_mma<D, EPI, PR>(P, S, tmem, it_begin, it_end, warp - 1);
     }
   } else if (warp < 12) {
     reg_alloc<160>();
-    run_softmax<D, PM, EPI>(P, S, tmem, it_begin, it_end, warp < 8 ? 0 : 1);
+    run_softmax<D, PM, EPI, PR>(P, S, tmem, it_begin, it_end, warp < 8 ? 0 : 1);
   } else {
     reg_dealloc<120>();
     if constexpr (EPI)
-      run_qprep_epi<D, EPI>(P, S, tmem, it_begin, it_end);
+      run_qprep_epi<D, EPI, PR>(P, S, tmem, it_begin, it_end);
     else
-      run_qprep<D, EPI>(P, S, it_begin, it_end);
+      run_qprep<D, EPI, PR>(P, S, it_begin, it_end);
   }
   if (warp >= 4 && (threadIdx.x & 31) == 0) bulk_wait<0>();  // epilogue stores done
   tc_fence_before();
-  __syncthreads();
-  if (P.a.sched != nullptr && threadIdx.x == 0) {
-    // the last CTA to finish (all claims of all CTAs are done) resets the counters for the next
-    // launch of this work list
+  if constexpr (PR)
+    cluster_sync_all();  // neither CTA leaves while the other may still touch its smem / TMEM
+  else
+    __syncthreads();
+  if (P.a.sched != nullptr && threadIdx.x == 0 && rank == 0) {
+    // the last CTA (pair) to finish (all claims of all CTAs are done) resets the counters for the
+    // next launch of this work list
     __threadfence();
-    if (atomicAdd(P.a.sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+    if (atomicAdd(P.a.sched + 1, 1) == static_cast<int>(gridDim.x / kBoth) - 1) {
       P.a.sched[0] = 0;
       P.a.sched[1] = 0;
       __threadfence();
@@ -1173,27 +1366,31 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
 #endif
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<kTmemCols>(tmem);
+    if constexpr (PR)
+      tmem_dealloc2<kTmemCols>(tmem);
+    else
+      tmem_dealloc<kTmemCols>(tmem);
   }
 }
 
-template <int D, int PM, bool EPI>
+template <int D, int PM, bool EPI, bool PR = false>
 cudaError_t launch_dp(const AttnArgs& a, cudaStream_t st) {
   // the large-smem attribute is per device: one bit per device ordinal that has it set
   static std::atomic<uint64_t> attr_set{0};
-  const int smem = static_cast<int>(sizeof(TcSmem<D>));
-  static_assert(sizeof(TcSmem<D>) <= 232448, "shared memory budget (227 KB per CTA)");
+  const int smem = static_cast<int>(sizeof(TcSmem<D, PR>));
+  static_assert(sizeof(TcSmem<D, PR>) <= 232448, "shared memory budget (227 KB per CTA)");
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   const uint64_t bit = 1ull << (dev & 63);
   if (!(attr_set.load() & bit)) {
-    e = cudaFuncSetAttribute(span_attn_tc_kernel<D, PM, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    e = cudaFuncSetAttribute(span_attn_tc_kernel<D, PM, EPI, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set.fetch_or(bit);
   }
   TcParams p;
   p.tmk = *a.tmap_k;
+  if (PR) p.tmk2 = *a.tmap_k2;
   p.tmv = *a.tmap_v;
   p.tmq = *a.tmap_q;
   if (a.tmap_o) p.tmo = *a.tmap_o;
@@ -1216,12 +1413,24 @@ cudaError_t launch_dp(const AttnArgs& a, cudaStream_t st) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = static_cast<size_t>(smem);
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (a.pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (PR) {  // CTA pairs: clusters of 2 (one TPC each)
+    if (a.grid % 2 != 0) return cudaErrorInvalidValue;
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = a.pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, span_attn_tc_kernel<D, PM, EPI>, p);
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, span_attn_tc_kernel<D, PM, EPI, PR>, p);
 }
 
 template <int D>
@@ -1231,6 +1440,14 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
   // 0.311 -> 0.296 ms); fp32 O at d = 128 keeps the softmax-WG epilogue (its fp32 drain cycles
   // through 2 x 4 KB per warp of the Q slot, and measured 0.255 vs 0.247 ms)
   const bool epi = a.paired && !a.join && (!a.out_fp32 || D == 64);
+  if (a.cluster == 2) {
+    // CTA-pair kernel (d = 128 prefill with bf16 O, GQA groups of 4k): work codes are 4-head units
+    if constexpr (D == 128) {
+      if (!epi || a.tmap_k2 == nullptr || (a.hq / a.hkv) % 4 != 0) return cudaErrorInvalidValue;
+      return a.poly_mask == 0 ? launch_dp<D, 0, true, true>(a, st) : launch_dp<D, 3, true, true>(a, st);
+    }
+    return cudaErrorInvalidValue;
+  }
   // exp2: 0 = MUFU ex2 (fp32), else MUFU ex2.f16x2 (two exponentials per op)
   if (a.poly_mask == 0) return epi ? launch_dp<D, 0, true>(a, st) : launch_dp<D, 0, false>(a, st);
   return epi ? launch_dp<D, 3, true>(a, st) : launch_dp<D, 3, false>(a, st);

@@ -74,7 +74,7 @@ const std::vector<int32_t> kZeros2 = {0, 0};  // claim counters of a dynamic wor
 
 struct DevWork {  // offsets of one attention work list inside a plan buffer
   size_t tiles, tile_blocks, items, cta_off, cta_items, combine, sched;
-  int32_t n_items = 0, grid = 0, n_combine = 0, n_parts = 0, n_codes = 0;
+  int32_t n_items = 0, grid = 0, n_combine = 0, n_parts = 0, n_codes = 0, cluster = 1;
   bool dynamic = false;
   double flops = 0;
 };
@@ -88,6 +88,8 @@ struct spq_ctx {
   int num_sms = 0;
   float2* rope = nullptr;  // device [max_position][d/2] (cos, sin) fp32: K1 (K pages) + fp32 path
   CUtensorMap tmk, tmv;
+  CUtensorMap tmk2;  // K pool with boxes of min(bs, 32) rows (CTA-pair kernel, d = 128)
+  bool have_tmk2 = false;
   bool have_tmap = false;
   std::vector<cudaEvent_t> pending;  // stream-ordered releases
   int64_t launches = 0;
@@ -103,6 +105,7 @@ struct spq_ctx {
   int exp2_mode = 0;               // SPQ_OPT_EXP2
   float rescale_threshold = 8.0f;  // SPQ_OPT_RESCALE_THRESHOLD (log2 units)
   bool pdl = true;                 // SPQ_OPT_PDL
+  bool pair = false;               // SPQ_OPT_PAIR (measured slower: DESIGN.md §6)
   // profiling builds only (spq_set_trace)
   long long* trace = nullptr;
   int dbg_mode = 0;
@@ -184,10 +187,27 @@ spq::WorkOpts work_opts(const spq_ctx* c, bool allow_split) {
   o.units = paired(c) ? o.hq / 2 : o.hq;
   return o;
 }
+// The prefill launches run on CTA pairs (cta_group::2, span_attn_tc.cu PR) when the shape allows
+// it: bf16, d = 128, GQA groups of 4k heads, bf16 O (the Q-prep-warp epilogue), an even SM count.
+// Decided when a plan's work list is built (the launch follows the list's cluster size).
+bool pair_prefill(const spq_ctx* c) {
+  const spq_config& g = c->cfg;
+  const int sms = c->num_sms > 0 ? c->num_sms : 148;
+  return c->pair && g.dtype == SPQ_BF16 && g.head_dim == 128 && (g.num_q_heads / g.num_kv_heads) % 4 == 0 &&
+         g.out_dtype != SPQ_FP32 && sms % 2 == 0 && (!is_gpu(c) || c->have_tmk2);
+}
+spq::WorkOpts prefill_opts(const spq_ctx* c) {
+  spq::WorkOpts o = work_opts(c, false);
+  if (pair_prefill(c)) {
+    o.units = o.hq / 4;
+    o.cluster = 2;
+  }
+  return o;
+}
 
 int elt_size(const spq_ctx* c) { return c->cfg.dtype == SPQ_FP32 ? 4 : 2; }
 
-spq_status make_tmap(spq_ctx* c, void* pool, CUtensorMap* out) {
+spq_status make_tmap(spq_ctx* c, void* pool, CUtensorMap* out, int max_box_rows = 64) {
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
   CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
@@ -198,7 +218,7 @@ spq_status make_tmap(spq_ctx* c, void* pool, CUtensorMap* out) {
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.head_dim), rows};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.head_dim) * 2};
   // one box = 64 columns x min(bs, 64) rows: the attention kernel streams 64-key sub-tiles
-  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(std::min(g.block_size, 64))};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(std::min(g.block_size, max_box_rows))};
   cuuint32_t es[2] = {1, 1};
   CUresult r = reinterpret_cast<EncodeTiledFn>(fn)(
       out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, pool, dims, strides, box, es,
@@ -300,6 +320,8 @@ void fill_attn(spq_ctx* c, const spq_plan* p, const DevWork& w, spq::AttnArgs* a
   a->cta_off = at<int32_t>(p, w.cta_off);
   a->cta_items = at<int32_t>(p, w.cta_items);
   a->sched = w.dynamic ? at<int32_t>(p, w.sched) : nullptr;
+  a->cluster = w.cluster;
+  a->tmap_k2 = c->have_tmk2 ? &c->tmk2 : nullptr;
   a->n_codes = w.n_codes;
   a->grid = w.grid;
   a->k_pool = c->cfg.k_pool;
@@ -388,6 +410,7 @@ spq_status upload_work(spq_ctx* c, const spq::AttnWorkHost& h, cudaStream_t st, 
   tw->w.combine = pk.add(h.combine);
   tw->w.n_items = static_cast<int32_t>(h.items.size());
   tw->w.grid = h.grid;
+  tw->w.cluster = h.cluster;
   tw->w.n_combine = static_cast<int32_t>(h.combine.size());
   tw->w.n_parts = h.n_parts;
   std::vector<uint8_t> host(pk.size);
@@ -465,6 +488,11 @@ spq_status spq_create(const spq_config* cfg, spq_ctx** out) {
       s = make_tmap(c.get(), g.v_pool, &c->tmv);
       if (s != SPQ_OK) return s;
       c->have_tmap = true;
+      if (g.head_dim == 128) {  // CTA-pair prefill: each CTA loads 32 keys of a K sub-tile
+        s = make_tmap(c.get(), g.k_pool, &c->tmk2, 32);
+        if (s != SPQ_OK) return s;
+        c->have_tmk2 = true;
+      }
     }
     for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
     CUDA_TRY(cudaEventCreateWithFlags(&c->staging_ev, cudaEventDisableTiming));
@@ -608,7 +636,7 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
   // host-only contexts plan for a B200 (148 SMs) so their work lists match a GPU ctx's
   spq::WorkOpts o = work_opts(c, c->cfg.dtype == SPQ_BF16);
   lap("view arrays");
-  spq::build_prefill_work(H, o, 0, static_cast<int>(H.jobs.size()), &p->pw_host);
+  spq::build_prefill_work(H, prefill_opts(c), 0, static_cast<int>(H.jobs.size()), &p->pw_host);
   lap("prefill work");
   spq::build_join_work(H, o, 0, H.n_queries, &p->jw_host);
   // W > 1: the join again as two phases around the exchange (held segments, then the received
@@ -731,6 +759,7 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
       w->combine = pk.add(h.combine);
       w->n_items = static_cast<int32_t>(h.items.size());
       w->grid = h.grid;
+      w->cluster = h.cluster;
       w->n_combine = static_cast<int32_t>(h.combine.size());
       w->n_parts = h.n_parts;
       w->flops = h.flops;
@@ -873,8 +902,7 @@ spq_status spq_prefill_jobs(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, i
     fill_attn(c, p, p->pw, &args);
   } else {
     spq::AttnWorkHost h;
-    spq::WorkOpts o = work_opts(c, false);
-    spq::build_prefill_work(p->host, o, a, b, &h);
+    spq::build_prefill_work(p->host, prefill_opts(c), a, b, &h);
     s = upload_work(c, h, st, &tw);
     if (s != SPQ_OK) return s;
     spq_plan tmp_view;  // only dbuf is read by fill_attn through `at`
@@ -1707,6 +1735,9 @@ spq_status spq_set_option(spq_ctx* c, int32_t key, double value) {
       return SPQ_OK;
     case SPQ_OPT_HASH_SCALAR:
       spq::blake2b_force_scalar(value != 0);
+      return SPQ_OK;
+    case SPQ_OPT_PAIR:
+      c->pair = value != 0;
       return SPQ_OK;
     default:
       return fail(SPQ_EINVAL, "unknown option " + std::to_string(key));

@@ -22,7 +22,7 @@ _lib = None
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, ESTATE = range(6)
 BF16, FP32 = 0, 1
 # spq_option keys (include/spanq.h)
-OPT_EXP2, OPT_RESCALE_THRESHOLD, OPT_PDL, OPT_HASH_SCALAR = 1, 2, 3, 4
+OPT_EXP2, OPT_RESCALE_THRESHOLD, OPT_PDL, OPT_HASH_SCALAR, OPT_PAIR = 1, 2, 3, 4, 5
 
 
 class SpanqError(RuntimeError):
@@ -480,7 +480,7 @@ class Context:
         return order
 
     def set_option(self, key: int, value: float):
-        """spq_set_option (OPT_EXP2, OPT_RESCALE_THRESHOLD, OPT_PDL, OPT_HASH_SCALAR)."""
+        """spq_set_option (OPT_EXP2, OPT_RESCALE_THRESHOLD, OPT_PDL, OPT_HASH_SCALAR, OPT_PAIR)."""
         _check(lib().spq_set_option(self.handle, int(key), float(value)))
 
     def set_trace(self, buf, mode: int = 0):

@@ -171,6 +171,16 @@ def test_bf16_exp2_modes(cuda_dev, exp2):
     run_and_check(w, cuda_dev, options={spanq.OPT_EXP2: exp2})
 
 
+@pytest.mark.parametrize("bs,hq", [(16, 32), (32, 16), (64, 32), (128, 32), (64, 64)])
+def test_bf16_cta_pair_prefill(cuda_dev, bs, hq):
+    # SPQ_OPT_PAIR = 1: the prefill on CTA pairs (cta_group::2, M = 256: the 4 q heads of a GQA
+    # group over two SMs, K / V sub-tiles split between them); ragged segments, several block
+    # sizes (K halves of min(bs, 32) rows), GQA 4 and 8, bf16 O (the path it serves)
+    sh = inputs.Shape(hq=hq, hkv=8, d=128, block_size=bs, vocab=2048)
+    w = inputs.make_rag(120 + bs, sh, 150, 4, [300, 129, 64, 1000], 140)
+    run_and_check(w, cuda_dev, out_dtype="bf16", abs_tol=BF16_MAX_ABS, options={spanq.OPT_PAIR: 1})
+
+
 @pytest.mark.parametrize("out_dtype", ["fp32", "bf16"])
 def test_bf16_multi_query_batch(cuda_dev, out_dtype):
     sh = inputs.Shape(hq=8, hkv=2, d=128, block_size=16, vocab=256)
@@ -250,8 +260,8 @@ def test_full_size_c2_sampled_rows(cuda_dev):
     ctx.close()
 
 
-@pytest.mark.parametrize("out_dtype", ["fp32", "bf16"])
-def test_full_size_c2_all_rows(cuda_dev, out_dtype):
+@pytest.mark.parametrize("out_dtype,pair", [("fp32", 0), ("bf16", 0), ("bf16", 1)])
+def test_full_size_c2_all_rows(cuda_dev, out_dtype, pair):
     """configs[1] at full size in the bench's launch configuration (512-block pool, the bench's
     output dtypes), EVERY output element: all 17,152 prefill rows and all 256 join rows, all 32
     heads, against the fp64 oracle (the whole C2 in a few seconds on the host)."""
@@ -260,6 +270,7 @@ def test_full_size_c2_all_rows(cuda_dev, out_dtype):
     w = inputs.c2()
     s = w.shape
     ctx = spanq.Context(s, 512, device=0, max_position=1 << 15, out_dtype=out_dtype)
+    ctx.set_option(spanq.OPT_PAIR, pair)  # 1: the CTA-pair prefill kernel
     tabs = [runner.device_tables(s, 0, w.seed, cuda_dev)]
     res = runner.run_pass(ctx, w.queries, tabs, cuda_dev)
     torch.cuda.synchronize()
