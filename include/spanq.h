@@ -368,8 +368,11 @@ spq_status spq_cidra_schedule(const spq_ctx *ctx, const int32_t *src, const int3
 
 /* ------------------------------------------------------------------ options */
 typedef enum {
-  SPQ_OPT_EXP2 = 1,              /* softmax exp2 on MUFU: 0 = ex2 fp32 (default), 1 = ex2.f16x2
-                                    (two exponentials per op; inputs rounded to f16)           */
+  SPQ_OPT_EXP2 = 1,              /* softmax exp2: 0 = MUFU ex2 fp32, 1 = MUFU ex2.f16x2 (two
+                                    exponentials per op; inputs rounded to f16), 2 / 3 = a
+                                    quarter / half of them by an FMA-pipe polynomial (rel. error
+                                    1e-4, below the bf16 rounding of P), 4 = auto (default:
+                                    prefill 0, joins 2 — measured fastest for each)            */
   SPQ_OPT_RESCALE_THRESHOLD = 2, /* O is rescaled when a row max grows by more than this (log2
                                     units, default 8; 0 = on every growth). Exact either way  */
   SPQ_OPT_PDL = 3,               /* 1 (default): attention/combine launched as programmatic

@@ -306,6 +306,22 @@ __device__ __forceinline__ float exp2_poly(float x) {
   return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
 }
 
+// two exp2 on the FMA pipe in packed fp32x2 (FADD2 / FFMA2): the same rounding trick and
+// polynomial as exp2_poly, ~5 instructions per value; the exponent is added with one IMAD per
+// value — (t_bits - 0x4B400000) << 23 == t_bits << 23 mod 2^32, the magic's low 9 bits being 0
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -120.f);
+  x.y = fmaxf(x.y, -120.f);
+  const float2 t = fadd2(x, make_float2(12582912.f, 12582912.f));
+  const float2 n = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = ffma2(n, make_float2(-1.f, -1.f), x);
+  float2 p = ffma2(make_float2(0.05500831f, 0.05500831f), f, make_float2(0.24220964f, 0.24220964f));
+  p = ffma2(p, f, make_float2(0.69328305f, 0.69328305f));
+  p = ffma2(p, f, make_float2(1.0f, 1.0f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 // two exp2 with one MUFU op: fp32 inputs rounded to f16 (the large-p keys have x near 0 where
 // f16 is fine-grained: <= 0.07% error for p >= 1/16, below the bf16 rounding of P itself),
 // packed ex2.approx.f16x2, widened back to fp32 for the row sum.
@@ -626,9 +642,16 @@ __device__ __forceinline__ float softmax_sub(uint32_t scol, float sl2, float thr
     if constexpr (PM == 3) {
       ex2_pair_f16(xx.x, xx.y, p0, p1);
     } else {
-      constexpr bool kPoly[4] = {0 < PM, 1 < PM, 2 < PM, 3 < PM};
-      p0 = kPoly[i & 3] ? exp2_poly(xx.x) : ex2_approx(xx.x);
-      p1 = kPoly[i & 3] ? exp2_poly(xx.y) : ex2_approx(xx.y);
+      // PM 1 / 2: a quarter / half of the pairs on the FMA pipe (MUFU: 16 ex2 per SM per clock)
+      constexpr bool kPoly[4] = {0 < PM, 2 < PM, 1 < PM, 3 < PM};
+      if (kPoly[i & 3]) {
+        const float2 pp = exp2_poly2(xx);
+        p0 = pp.x;
+        p1 = pp.y;
+      } else {
+        p0 = ex2_approx(xx.x);
+        p1 = ex2_approx(xx.y);
+      }
     }
     if constexpr (kMasked) {
       p0 = (2 * i <= lim) ? p0 : 0.f;
@@ -1442,12 +1465,16 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
   const bool epi = a.paired && !a.join && (!a.out_fp32 || D == 64);
   if (a.cluster == 2) {
     // CTA-pair kernel (d = 128 prefill with bf16 O, GQA groups of 4k): work codes are 4-head units
+    // (exp2: MUFU fp32 or f16x2 only)
     if constexpr (D == 128) {
       if (!epi || a.tmap_k2 == nullptr || (a.hq / a.hkv) % 4 != 0) return cudaErrorInvalidValue;
-      return a.poly_mask == 0 ? launch_dp<D, 0, true, true>(a, st) : launch_dp<D, 3, true, true>(a, st);
+      return a.poly_mask != 3 ? launch_dp<D, 0, true, true>(a, st) : launch_dp<D, 3, true, true>(a, st);
     }
     return cudaErrorInvalidValue;
   }
+  // a quarter / half of the exponentials on the FMA pipe
+  if (a.poly_mask == 1) return epi ? launch_dp<D, 1, true>(a, st) : launch_dp<D, 1, false>(a, st);
+  if (a.poly_mask == 2) return epi ? launch_dp<D, 2, true>(a, st) : launch_dp<D, 2, false>(a, st);
   // exp2: 0 = MUFU ex2 (fp32), else MUFU ex2.f16x2 (two exponentials per op)
   if (a.poly_mask == 0) return epi ? launch_dp<D, 0, true>(a, st) : launch_dp<D, 0, false>(a, st);
   return epi ? launch_dp<D, 3, true>(a, st) : launch_dp<D, 3, false>(a, st);

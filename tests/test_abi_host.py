@@ -63,10 +63,11 @@ def test_released_plan_handle_reports_estate():
 
 def test_options_validate():
     ctx = spanq.Context(inputs.Shape(hq=2, hkv=1, d=64, block_size=16), 64, device=-1)
-    for key, value in [(spanq.OPT_EXP2, 0), (spanq.OPT_EXP2, 1), (spanq.OPT_RESCALE_THRESHOLD, 0),
-                       (spanq.OPT_RESCALE_THRESHOLD, 8), (spanq.OPT_PDL, 0), (spanq.OPT_PDL, 1)]:
+    for key, value in [(spanq.OPT_EXP2, 0), (spanq.OPT_EXP2, 1), (spanq.OPT_EXP2, 2), (spanq.OPT_EXP2, 3),
+                       (spanq.OPT_EXP2, 4), (spanq.OPT_RESCALE_THRESHOLD, 0), (spanq.OPT_RESCALE_THRESHOLD, 8),
+                       (spanq.OPT_PDL, 0), (spanq.OPT_PDL, 1), (spanq.OPT_PAIR, 0), (spanq.OPT_PAIR, 1)]:
         ctx.set_option(key, value)
-    for key, value in [(spanq.OPT_EXP2, 2), (spanq.OPT_RESCALE_THRESHOLD, -1), (99, 0)]:
+    for key, value in [(spanq.OPT_EXP2, 5), (spanq.OPT_EXP2, -1), (spanq.OPT_RESCALE_THRESHOLD, -1), (99, 0)]:
         with pytest.raises(spanq.SpanqError) as e:
             ctx.set_option(key, value)
         assert e.value.status == spanq.EINVAL

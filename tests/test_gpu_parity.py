@@ -164,9 +164,10 @@ def test_bf16_rescale_every_tile(cuda_dev, out_dtype):
     run_and_check(w, cuda_dev, out_dtype=out_dtype, options={spanq.OPT_RESCALE_THRESHOLD: 0})
 
 
-@pytest.mark.parametrize("exp2", [0, 1])
+@pytest.mark.parametrize("exp2", [0, 1, 2, 3, 4])
 def test_bf16_exp2_modes(cuda_dev, exp2):
-    # SPQ_OPT_EXP2: MUFU ex2 in fp32 (0, default) or ex2.f16x2, two exponentials per op (1)
+    # SPQ_OPT_EXP2: MUFU ex2 in fp32 (0, default), ex2.f16x2 (1), a quarter / half of the
+    # exponentials by the FMA-pipe polynomial (2 / 3)
     w = inputs.make_rag(108, inputs.Shape(**inputs.SHAPE_8B, block_size=64), 64, 2, [256, 200], 140)
     run_and_check(w, cuda_dev, options={spanq.OPT_EXP2: exp2})
 
