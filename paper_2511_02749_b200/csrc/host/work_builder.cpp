@@ -366,6 +366,9 @@ void decode_items(const std::vector<std::pair<int32_t, int32_t>>& row_tiles, int
         it.tile_begin = tb + c * chunk_tiles;
         it.tile_end = std::min(te, tb + (c + 1) * chunk_tiles);
         it.part = n > 1 ? pb + c : -1;
+        it.n_chunks = n;                                                   // chunks of this (row, kv head)
+        it.part0 = n > 1 ? pb : -1;                                     // its first partial slot
+        it.pair = static_cast<int32_t>(r) * hkv + h;                   // (row, kv head) index
         w->items.push_back(it);
       }
       if (n > 1) {

@@ -12,7 +12,7 @@ namespace spq {
 
 struct DecodeItemHost {
   int32_t row, kvh, tile_begin, tile_end, part;  // mirrors kernels/launch.h DecodeItem
-  int32_t pad0, pad1, pad2;
+  int32_t n_chunks, part0, pair;                 // (row, kv head): chunks, first partial, index
 };
 
 struct AttnWorkHost {

@@ -23,6 +23,7 @@
 #include <cstdint>
 
 #include "launch.h"
+#include "sm100.cuh"
 
 namespace spq {
 namespace {
@@ -265,6 +266,309 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const DecodeArgs a) {
   }
 }
 
+// ---------------------------------------------------------------- bf16 pools: warp-split decode
+// The bf16 path is HBM-bound by K and V (2·d·2 bytes per key and kv head) with little arithmetic
+// per byte, so the CTA's chunk is split over its 4 warps instead of walking it in CTA-wide steps
+// with barriers: warp w takes the chunk's 16-key groups w, w+4, ... and runs its own pipeline —
+// cp.async double-buffered K / V group in its smem region (K rows XOR-swizzled by 16-byte unit),
+// its own counter-rotated q (fp32), its own online softmax — with no CTA barrier until the four
+// (m, l, O) partials are merged at the end. Per group: lane = (key, half of d) for the scores
+// (packed FFMA2 over bf16 pairs widened to fp32, halves summed by one shuffle), shuffle max / sum
+// per head over the 16 keys, lane = 4 (d = 128) or 2 (d = 64) columns of every head for P·V.
+constexpr int kGrp = 16;   // keys per warp step
+constexpr int kWarps = 4;
+
+template <int D, int G>
+struct DecSmem {
+  static constexpr int kUnits = D / 8;                        // 16-byte units per bf16 row
+  static constexpr int kStage = 2 * kGrp * D;                 // bf16 elements: K then V of a group
+  __nv_bfloat16 kv[kWarps][2][kStage];                        // per warp, double-buffered
+  float q[kWarps][G * D];                                     // per warp: rotated q (fp32)
+  float p[kWarps][G * kGrp];                                  // per warp: P of the current group
+  float ml[kWarps][2 * G];                                    // merge: m, l per warp and head
+};
+
+template <typename TO, int D, int G>
+__global__ void __launch_bounds__(kThreads) decode_bf16_kernel(const DecodeArgs a) {
+  using T = __nv_bfloat16;
+  using Sm = DecSmem<D, G>;
+  constexpr int U = Sm::kUnits;
+  constexpr int CPL = D / 32;  // P·V columns per lane
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  Sm& S = *reinterpret_cast<Sm*>(smem_raw);
+  const DecodeItem it = a.items[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int pos = a.pos_base[it.row] + a.step;
+  const int h0 = it.kvh * G;
+  const T* qg = static_cast<const T*>(a.q) + (static_cast<int64_t>(it.row) * a.hq + h0) * D;
+  const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));
+  const int64_t layer_rows = static_cast<int64_t>(a.layer) * a.nblk * a.hkv * a.bs;
+  float* qs = S.q[w];
+  float* ps = S.p[w];
+  // this warp's groups: the chunk's groups in (tile, group) order, every kWarps-th one
+  struct Grp {
+    int t, g, nk;  // tile, group in the tile, valid keys
+  };
+  auto n_vis_of = [&](const KvTile& tl) {
+    return tl.causal ? min(tl.n_valid, pos - tl.key_pos0 + 1) : tl.n_valid;
+  };
+  int it_t = it.tile_begin, it_g = 0, gidx = 0;  // iterator over all groups of the chunk
+  auto next_mine = [&](Grp& out) -> bool {
+    while (it_t < it.tile_end) {
+      const int nv = n_vis_of(a.tiles[it_t]);
+      const int ng = nv > 0 ? (nv + kGrp - 1) / kGrp : 0;
+      if (it_g >= ng) {
+        ++it_t;
+        it_g = 0;
+        continue;
+      }
+      const int g = it_g++;
+      if ((gidx++ % kWarps) != w) continue;
+      out = Grp{it_t, g, min(kGrp, nv - g * kGrp)};
+      return true;
+    }
+    return false;
+  };
+  auto issue = [&](const Grp& gr, int buf) {  // cp.async of the group's K and V rows
+    const KvTile tl = a.tiles[gr.t];
+    __nv_bfloat16* Kb = S.kv[w][buf];
+    __nv_bfloat16* Vb = Kb + kGrp * D;
+    for (int i = lane; i < gr.nk * U; i += 32) {
+      const int key = i / U, u = i % U;
+      const int kk = gr.g * kGrp + key;
+      const int32_t blk = a.tile_blocks[tl.blk_off + kk / a.bs];
+      const int64_t row = layer_rows + (static_cast<int64_t>(blk) * a.hkv + it.kvh) * a.bs + kk % a.bs;
+      cp_async16(Kb + key * D + ((u ^ (key & (U - 1))) * 8), static_cast<const T*>(a.k_pool) + row * D + u * 8);
+      cp_async16(Vb + key * D + u * 8, static_cast<const T*>(a.v_pool) + row * D + u * 8);
+    }
+    cp_async_commit();
+  };
+  float m[G], l[G];
+  float2 acc[G][CPL / 2];
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    m[h] = -INFINITY;
+    l[h] = 0.f;
+#pragma unroll
+    for (int e = 0; e < CPL / 2; ++e) acc[h][e] = make_float2(0.f, 0.f);
+  }
+  const int key = lane & (kGrp - 1), half = lane >> 4;
+  int cur_rot = INT32_MIN;
+  Grp cur, nxt;
+  bool have = next_mine(cur);
+  if (have) issue(cur, 0);
+  for (int buf = 0; have; buf ^= 1) {
+    const bool more = next_mine(nxt);
+    if (more) {
+      issue(nxt, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    const int rot = a.tiles[cur.t].rot_delta;
+    if (rot != cur_rot) {  // a new segment: q rotated to pos - Δ (rotate-half pairs), fp32
+      cur_rot = rot;
+      const int rp = min(max(pos - rot, 0), a.max_pos - 1);
+      for (int i = lane; i < G * (D / 2); i += 32) {
+        const int h = i / (D / 2), c = i % (D / 2);
+        const float x = __bfloat162float(qg[h * D + c]), y = __bfloat162float(qg[h * D + c + D / 2]);
+        const float2 cs = a.rope[static_cast<int64_t>(rp) * (D / 2) + c];
+        qs[h * D + c] = x * cs.x - y * cs.y;
+        qs[h * D + c + D / 2] = y * cs.x + x * cs.y;
+      }
+    }
+    __syncwarp();  // every lane's cp.async of this group and the rotated q are visible
+    const __nv_bfloat16* Kb = S.kv[w][buf];
+    const __nv_bfloat16* Vb = Kb + kGrp * D;
+    // scores: lane = (key, half of d); packed fp32x2 products, halves summed by a shuffle
+    float sc[G];
+    {
+      float2 s2[G];
+#pragma unroll
+      for (int h = 0; h < G; ++h) s2[h] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int uu = 0; uu < U / 2; ++uu) {
+        const int u = half * (U / 2) + uu;
+        const uint4 kv = *reinterpret_cast<const uint4*>(Kb + key * D + ((u ^ (key & (U - 1))) * 8));
+        const uint32_t wv[4] = {kv.x, kv.y, kv.z, kv.w};
+        float2 kf[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) kf[e] = make_float2(__uint_as_float(wv[e] << 16), __uint_as_float(wv[e] & 0xFFFF0000u));
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+          const float4 qa = *reinterpret_cast<const float4*>(qs + h * D + u * 8);
+          const float4 qb = *reinterpret_cast<const float4*>(qs + h * D + u * 8 + 4);
+          s2[h] = ffma2(kf[0], make_float2(qa.x, qa.y), s2[h]);
+          s2[h] = ffma2(kf[1], make_float2(qa.z, qa.w), s2[h]);
+          s2[h] = ffma2(kf[2], make_float2(qb.x, qb.y), s2[h]);
+          s2[h] = ffma2(kf[3], make_float2(qb.z, qb.w), s2[h]);
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        float v = s2[h].x + s2[h].y;
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        sc[h] = key < cur.nk ? v * scale_log2 : -INFINITY;
+      }
+    }
+    // online softmax per head over the group's 16 keys (both half-warps hold the same values)
+    float alpha[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      float mx = sc[h];
+#pragma unroll
+      for (int o = kGrp / 2; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const float m_new = fmaxf(m[h], mx);
+      const float pv = key < cur.nk ? exp2f(sc[h] - m_new) : 0.f;
+      float sum = pv;
+#pragma unroll
+      for (int o = kGrp / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      alpha[h] = m[h] == -INFINITY ? 0.f : exp2f(m[h] - m_new);
+      l[h] = l[h] * alpha[h] + sum;
+      m[h] = m_new;
+      if (half == 0) ps[h * kGrp + key] = pv;
+    }
+    __syncwarp();
+    // O = O * alpha + P V: lane = CPL consecutive columns of every head
+#pragma unroll
+    for (int h = 0; h < G; ++h)
+#pragma unroll
+      for (int e = 0; e < CPL / 2; ++e) acc[h][e] = fmul2(acc[h][e], make_float2(alpha[h], alpha[h]));
+    for (int k = 0; k < cur.nk; ++k) {
+      float2 vf[CPL / 2];
+      if constexpr (CPL == 4) {
+        const uint2 vv = *reinterpret_cast<const uint2*>(Vb + k * D + lane * 4);
+        vf[0] = make_float2(__uint_as_float(vv.x << 16), __uint_as_float(vv.x & 0xFFFF0000u));
+        vf[1] = make_float2(__uint_as_float(vv.y << 16), __uint_as_float(vv.y & 0xFFFF0000u));
+      } else {
+        const uint32_t vv = *reinterpret_cast<const uint32_t*>(Vb + k * D + lane * 2);
+        vf[0] = make_float2(__uint_as_float(vv << 16), __uint_as_float(vv & 0xFFFF0000u));
+      }
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        const float pk = ps[h * kGrp + k];
+#pragma unroll
+        for (int e = 0; e < CPL / 2; ++e) acc[h][e] = ffma2(vf[e], make_float2(pk, pk), acc[h][e]);
+      }
+    }
+    __syncwarp();  // the buffer and P are reused by the next group
+    cur = nxt;
+    have = more;
+  }
+  // merge the four warps' partials (buffers reused: every warp is past its last cp.async)
+  __syncthreads();
+  float* om = reinterpret_cast<float*>(&S.kv[0][0][0]);  // [kWarps][G][D]
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+#pragma unroll
+    for (int e = 0; e < CPL / 2; ++e)
+      *reinterpret_cast<float2*>(om + (w * G + h) * D + lane * CPL + 2 * e) = acc[h][e];
+    if (lane == 0) {
+      S.ml[w][2 * h] = m[h];
+      S.ml[w][2 * h + 1] = l[h];
+    }
+  }
+  __syncthreads();
+  for (int f = tid; f < G * D; f += kThreads) {
+    const int h = f / D, c = f % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int ww = 0; ww < kWarps; ++ww) M = fmaxf(M, S.ml[ww][2 * h]);
+    float L = 0.f, O = 0.f;
+#pragma unroll
+    for (int ww = 0; ww < kWarps; ++ww) {
+      const float mw = S.ml[ww][2 * h];
+      const float sc2 = mw == -INFINITY ? 0.f : exp2f(mw - M);
+      L += S.ml[ww][2 * h + 1] * sc2;
+      O += om[(ww * G + h) * D + c] * sc2;
+    }
+    const float v = L > 0.f ? O / L : 0.f;
+    if (it.part >= 0)
+      a.opart[(static_cast<int64_t>(it.part) * G + h) * D + c] = v;
+    else
+      store_out(static_cast<TO*>(a.o) + (static_cast<int64_t>(it.row) * a.hq + h0 + h) * D + c, v);
+    if (c == 0) {
+      const float lse = L > 0.f ? (M + log2f(L)) * 0.69314718055994531f : -INFINITY;
+      if (it.part >= 0)
+        a.lsepart[static_cast<int64_t>(it.part) * G + h] = lse;
+      else if (a.lse != nullptr)
+        a.lse[static_cast<int64_t>(it.row) * a.hq + h0 + h] = lse;
+    }
+  }
+  if (it.part < 0) return;
+  // split (row, kv head): the last of its chunks to finish merges every chunk's partial, in chunk
+  // order (the same fixed-order LSE merge as K4, so the result does not depend on which CTA is
+  // last), instead of a separate combine launch
+  __shared__ int last;
+  __threadfence();  // this chunk's partial is visible before its arrival is counted
+  __syncthreads();
+  if (tid == 0) {
+    last = atomicAdd(a.done + it.pair, 1) == it.n_chunks - 1;
+    if (last) a.done[it.pair] = 0;  // for the next step (no other chunk of this launch is left)
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // LSE weights of every chunk (per head) in shared memory, then one float4 of O per thread and
+  // chunk, loads unrolled (the merge is latency-bound: n_chunks dependent reads otherwise)
+  const int n = it.n_chunks;
+  float* wts = reinterpret_cast<float*>(&S.kv[0][0][0]);  // [n][G] weights, then [G] M and L
+  float* ML = wts + n * G;
+  for (int i = tid; i < n * G; i += kThreads) wts[i] = __ldcg(a.lsepart + static_cast<int64_t>(it.part0) * G + i);
+  __syncthreads();
+  if (tid < G) {
+    float M = -INFINITY;
+    for (int k = 0; k < n; ++k) M = fmaxf(M, wts[k * G + tid]);
+    ML[2 * tid] = M;
+  }
+  __syncthreads();
+  for (int i = tid; i < n * G; i += kThreads) {
+    const float lk = wts[i], M = ML[2 * (i % G)];
+    wts[i] = lk == -INFINITY ? 0.f : __expf(lk - M);
+  }
+  __syncthreads();
+  if (tid < G) {
+    float L = 0.f;
+    for (int k = 0; k < n; ++k) L += wts[k * G + tid];
+    ML[2 * tid + 1] = L;
+  }
+  __syncthreads();
+  for (int f4 = tid; f4 < G * D / 4; f4 += kThreads) {
+    const int h = (f4 * 4) / D, c = (f4 * 4) % D;
+    const float4* src = reinterpret_cast<const float4*>(a.opart + (static_cast<int64_t>(it.part0) * G + h) * D + c);
+    const int64_t stride = static_cast<int64_t>(G) * D / 4;  // next chunk, same (head, columns)
+    float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+    for (int k = 0; k < n; ++k) {
+      const float4 v4 = __ldcg(src + k * stride);
+      const float wk = wts[k * G + h];
+      acc4.x = fmaf(wk, v4.x, acc4.x);
+      acc4.y = fmaf(wk, v4.y, acc4.y);
+      acc4.z = fmaf(wk, v4.z, acc4.z);
+      acc4.w = fmaf(wk, v4.w, acc4.w);
+    }
+    const float inv = 1.f / ML[2 * h + 1];
+    TO* dst = static_cast<TO*>(a.o) + (static_cast<int64_t>(it.row) * a.hq + h0 + h) * D + c;
+    store_out(dst, acc4.x * inv);
+    store_out(dst + 1, acc4.y * inv);
+    store_out(dst + 2, acc4.z * inv);
+    store_out(dst + 3, acc4.w * inv);
+    if (c == 0 && a.lse != nullptr) a.lse[static_cast<int64_t>(it.row) * a.hq + h0 + h] = ML[2 * h] + logf(ML[2 * h + 1]);
+  }
+}
+
+template <typename TO, int D, int G>
+cudaError_t launch_bf16_g(const DecodeArgs& a, cudaStream_t st) {
+  constexpr size_t smem = sizeof(DecSmem<D, G>);
+  static_assert(sizeof(DecSmem<D, G>) <= 232448, "decode smem");
+  static_assert(sizeof(DecSmem<D, G>) >= sizeof(float) * kWarps * G * D, "merge area");
+  cudaError_t e = cudaFuncSetAttribute(decode_bf16_kernel<TO, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  decode_bf16_kernel<TO, D, G><<<a.n_items, kThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 template <typename T, typename TO, int D, int G>
 cudaError_t launch_g(const DecodeArgs& a, cudaStream_t st) {
   constexpr int KP = D + 16 / static_cast<int>(sizeof(T));
@@ -279,6 +583,15 @@ cudaError_t launch_g(const DecodeArgs& a, cudaStream_t st) {
 
 template <typename T, typename TO, int D>
 cudaError_t launch_d(const DecodeArgs& a, cudaStream_t st) {
+  if constexpr (sizeof(T) == 2) {  // bf16 pools: the warp-split kernel
+    switch (a.hq / a.hkv) {
+      case 1: return launch_bf16_g<TO, D, 1>(a, st);
+      case 2: return launch_bf16_g<TO, D, 2>(a, st);
+      case 4: return launch_bf16_g<TO, D, 4>(a, st);
+      case 8: return launch_bf16_g<TO, D, 8>(a, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (a.hq / a.hkv) {
     case 1: return launch_g<T, TO, D, 1>(a, st);
     case 2: return launch_g<T, TO, D, 2>(a, st);

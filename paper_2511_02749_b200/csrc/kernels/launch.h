@@ -89,7 +89,7 @@ struct CombineArgs {
 // K9 decode (decode.cu): one work item = (home query row, kv head, chunk of KV tiles)
 struct DecodeItem {
   int32_t row, kvh, tile_begin, tile_end, part;  // part -1: write o / lse directly
-  int32_t pad0, pad1, pad2;
+  int32_t n_chunks, part0, pair;                 // (row, kv head): chunks, first partial, index
 };
 struct DecodeArgs {
   const DecodeItem* items;
@@ -103,6 +103,8 @@ struct DecodeArgs {
   float* lse;               // [rows][hq] or null
   float* opart;             // [parts][g][d]
   float* lsepart;           // [parts][g]
+  int32_t* done;            // bf16 path: [rows * hkv] chunks finished per (row, kv head), zero
+                            // between launches (the last chunk merges the partials and resets it)
   const void* k_pool;
   const void* v_pool;
   const float2* rope;

@@ -154,7 +154,8 @@ struct spq_plan {
     std::vector<int32_t> rows;                      // home query of each decode row
     std::vector<std::vector<int32_t>> blocks;       // per row: cross blocks + generation blocks
     uint8_t* dbuf = nullptr;
-    size_t off_tiles = 0, off_tb = 0, off_items = 0, off_comb = 0, off_posb = 0, off_kpos = 0, off_kslot = 0;
+    size_t off_tiles = 0, off_tb = 0, off_items = 0, off_comb = 0, off_posb = 0, off_kpos = 0, off_kslot = 0,
+           off_done = 0;
     float* opart = nullptr;
     float* lsepart = nullptr;
     int32_t n_items = 0, n_comb = 0;
@@ -1275,11 +1276,20 @@ spq_status spq_decode_reserve(spq_ctx* c, spq_plan* p, int32_t max_new) {
     }
     row_tiles.push_back(spq::decode_row_tiles(H, sg.query, bl, sg.tok_len + max_new, bs, &w));
   }
-  // chunks of <= T tiles per (row, kv head): ~4 CTAs per SM over the whole batch
-  int64_t tiles = 0;
-  for (const auto& rt : row_tiles) tiles += rt.second - rt.first;
-  const int64_t target = 4LL * (c->num_sms > 0 ? c->num_sms : 148);
-  const int chunk = static_cast<int>(std::max<int64_t>(1, (tiles * c->cfg.num_kv_heads + target - 1) / target));
+  // chunks of <= T tiles per (row, kv head), sized so that the whole batch is ONE wave of
+  // resident CTAs (a second, partial wave of a memory-bound kernel costs a whole CTA time): the
+  // bf16 kernel holds 4 warps x 2 stages x 16 keys of K and V plus per-warp q, P, merge state
+  int64_t max_tiles = 1;
+  for (const auto& rt : row_tiles) max_tiles = std::max<int64_t>(max_tiles, rt.second - rt.first);
+  const int64_t gq = c->cfg.num_q_heads / c->cfg.num_kv_heads, dd = c->cfg.head_dim;
+  const int64_t smem = c->cfg.dtype == SPQ_BF16
+                           ? 4 * 2 * 2 * 16 * dd * 2 + 4 * gq * dd * 4 + 4 * gq * 16 * 4 + 4 * 2 * gq * 4
+                           : 2 * (64 * (dd + 4) + 64 * dd) * 4 + 4 * (gq * dd + gq * 64 + gq * 3);
+  const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(232448 / smem, 16));
+  const int64_t slots = per_sm * (c->num_sms > 0 ? c->num_sms : 148);
+  const int64_t pairs = B * c->cfg.num_kv_heads;  // (row, kv head) pairs
+  const int64_t per_pair = std::max<int64_t>(1, slots / pairs);
+  const int chunk = static_cast<int>(std::max<int64_t>(1, (max_tiles + per_pair - 1) / per_pair));
   spq::decode_items(row_tiles, c->cfg.num_kv_heads, c->cfg.num_q_heads / c->cfg.num_kv_heads, chunk, &w);
   D.max_new = max_new;
   D.n_items = static_cast<int32_t>(w.items.size());
@@ -1293,6 +1303,8 @@ spq_status spq_decode_reserve(spq_ctx* c, spq_plan* p, int32_t max_new) {
   D.off_posb = pk.add(pos_base);
   D.off_kpos = pk.add(kpos);
   D.off_kslot = pk.add(kslot);
+  const std::vector<int32_t> done0(static_cast<size_t>(B) * c->cfg.num_kv_heads, 0);  // (alive until pk.write)
+  D.off_done = pk.add(done0);
   const int g = c->cfg.num_q_heads / c->cfg.num_kv_heads;
   const size_t off_op = align_up(pk.size, 256);
   const size_t off_lp = align_up(off_op + static_cast<size_t>(w.n_parts) * g * c->cfg.head_dim * sizeof(float), 256);
@@ -1353,6 +1365,7 @@ spq_status spq_decode_step(spq_ctx* c, spq_plan* p, int32_t layer, int32_t t, co
   a.lse = lse;
   a.opart = D.opart;
   a.lsepart = D.lsepart;
+  a.done = c->cfg.dtype == SPQ_BF16 ? reinterpret_cast<int32_t*>(D.dbuf + D.off_done) : nullptr;
   a.k_pool = c->cfg.k_pool;
   a.v_pool = c->cfg.v_pool;
   a.rope = c->rope;
@@ -1368,7 +1381,9 @@ spq_status spq_decode_step(spq_ctx* c, spq_plan* p, int32_t layer, int32_t t, co
   e = spq::launch_decode(a, st);
   if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("decode launch: ") + cudaGetErrorString(e));
   c->launches++;
-  if (D.n_comb > 0) {
+  // the bf16 kernel merges a (row, kv head)'s chunks itself (its last chunk to finish); the fp32
+  // path runs K4
+  if (D.n_comb > 0 && a.done == nullptr) {
     spq::CombineArgs ca{};
     ca.desc = reinterpret_cast<const spq::CombineDesc*>(D.dbuf + D.off_comb);
     ca.n_desc = D.n_comb;
