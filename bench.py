@@ -335,8 +335,8 @@ def main():
         c2x.oj = torch.empty(oj.shape, dtype=xdt, device=dev)
         c2x.set_timing(True)
         other_ms = []
-        timed(args.warmup, layers=2, c=c2x)
-        timed(max(3, args.steps // 4), layers=2, attn=other_ms, c=c2x)
+        timed(args.warmup, layers=min(2, L), c=c2x)
+        timed(max(3, args.steps // 4), layers=min(2, L), attn=other_ms, c=c2x)
         c2x.close()
         del c2x
     total_ms = max_over_ranks(float(sum(step_ms)))

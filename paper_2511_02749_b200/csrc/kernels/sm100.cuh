@@ -68,10 +68,47 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t pari
       : "memory");
   return ok != 0;
 }
-// Wait until the phase with the given parity has completed.
+// non-blocking test of a phase (never suspends the thread)
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Wait until the phase with the given parity has completed. SPANQ_WAITMODE (A/B builds): 0 =
+// try_wait with the suspend-time hint, 1 = try_wait without a hint, 2 = test_wait spin
+#ifndef SPANQ_WAITMODE
+#define SPANQ_WAITMODE 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if SPANQ_WAITMODE == 1
+  while (!mbar_try_wait(bar, parity)) {
+  }
+#elif SPANQ_WAITMODE == 2
+  while (!mbar_test_wait(bar, parity)) {
+  }
+#else
   while (!mbar_try_wait_sleep(bar, parity)) {
   }
+#endif
+}
+
+// Register fences: an empty volatile asm that "rewrites" 16 registers. Volatile asm statements keep
+// their order, so arithmetic on these values can be neither hoisted above a preceding barrier nor
+// sunk below a following one (the compiler moves pure register math freely across a barrier asm).
+__device__ __forceinline__ void reg_fence16(uint32_t* r) {
+  asm volatile(""
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]));
+}
+__device__ __forceinline__ void reg_fence_f2(float2& a, float2& b) {
+  asm volatile("" : "+f"(a.x), "+f"(a.y), "+f"(b.x), "+f"(b.y));
 }
 
 // Named CTA barriers (IDs 1..15; 0 is __syncthreads): sync waits for `n` arrivals, arrive does not.

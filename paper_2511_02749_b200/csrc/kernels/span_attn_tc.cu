@@ -51,7 +51,28 @@ namespace {
 
 constexpr int kThreads = 512;
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kColS = 0, kColO = 256;  // S_x at kColS + 128x, O_x at kColO + 128x
+// TMEM columns of head x. Default: one S buffer per head [256x, +64), two P buffers (bf16, 32
+// columns each) [256x + 64, +64), O [256x + 128, +128). The softmax releases S(j) as soon as its
+// LDTM has landed, so S(j+1) is computed while softmax(j) runs and the chain per head is
+// S(j) -> softmax load -> S(j+1), no longer S(j) -> softmax -> PV(j) -> S(j+2).
+// SPANQ_S2 (A/B build): two S buffers per head with P written over its S buffer, O at 256 + 128x.
+#ifdef SPANQ_S2
+constexpr bool kSP = false;
+#else
+constexpr bool kSP = true;
+#endif
+#ifndef SPANQ_PP
+#define SPANQ_PP 0
+#endif
+constexpr bool kPingPong = SPANQ_PP != 0;  // A/B build: -DSPANQ_PP=1 (measured slower: a WG alone
+                                           // needs ~780 cycles per sub-tile, both together ~1150-1300)
+__host__ __device__ constexpr uint32_t col_s(int x, int buf) {
+  return kSP ? 256u * x : 128u * x + 64u * buf;
+}
+__host__ __device__ constexpr uint32_t col_p(int x, int buf) {
+  return kSP ? 256u * x + 64u + 32u * buf : 128u * x + 64u * buf;
+}
+__host__ __device__ constexpr uint32_t col_o(int x) { return kSP ? 256u * x + 128u : 256u + 128u * x; }
 
 template <int D, bool PR = false>
 struct TcSmem {
@@ -82,6 +103,7 @@ struct TcSmem {
   uint64_t q_full[2][2], q_empty[2][2], q_load[2][2];  // [head][Q ring slot]
   __device__ uint8_t* q2(int x) { return reinterpret_cast<uint8_t*>(&stage[0][0][0]) + x * kChunks * kChunkBytes; }
   uint64_t s_full[2][2], p_full[2][2], o_done[2][2];  // [head][S buffer / PV parity j & 1]
+  uint64_t s_free[2][2];  // [head][j & 1]: softmax(j) has loaded S(j) (kSP: S(j+1) may overwrite it)
   // prefill: the epilogue runs on the Q-prep warps (12-15). The softmax WG of head x hands over
   // 1/l of every row through fin_inv[x][item & 1] (fin_full: 128 arrivals), the epilogue warps
   // drain O_x from TMEM into the staging area and arrive o_free[x] (128 threads), which the issuer
@@ -92,6 +114,9 @@ struct TcSmem {
   uint64_t sched_full[kSched], sched_empty[kSched];
   int32_t sched_code[kSched];
   uint32_t tmem_base;
+  // ping-pong: a word that is always 0 (read after the barrier: the exponentials depend on it) and a
+  // sink the row sums are stored to before the hand-over (the stores cannot sink below it)
+  float pp_zero, pp_sink;
 };
 
 struct TcParams {
@@ -207,12 +232,28 @@ __device__ __forceinline__ void arrive_lead_warp(uint64_t* bar) {
     mbar_arrive(bar);
   }
 }
+// Waits of the single-thread roles (TMA producers, MMA issuers). SPANQ_ISSWAIT (A/B builds): 0 =
+// try_wait with the suspend-time hint, 1 = test_wait poll, 2 = try_wait without a hint
+#ifndef SPANQ_ISSWAIT
+#define SPANQ_ISSWAIT 0
+#endif
+__device__ __forceinline__ void mbar_wait_1t(uint64_t* bar, uint32_t parity) {
+#if SPANQ_ISSWAIT == 1
+  while (!mbar_test_wait(bar, parity)) {
+  }
+#elif SPANQ_ISSWAIT == 2
+  while (!mbar_try_wait(bar, parity)) {
+  }
+#else
+  mbar_wait(bar, parity);
+#endif
+}
 template <bool PR>
 __device__ __forceinline__ void wait_lead(uint64_t* bar, uint32_t parity) {
   if constexpr (PR)
     mbar_wait_cl(bar, parity);
   else
-    mbar_wait(bar, parity);
+    mbar_wait_1t(bar, parity);
 }
 // spin (no suspend-time hint) — A/B of the wake-up latency on the step's critical path
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
@@ -371,8 +412,9 @@ __device__ void run_producer(const TcParams& P, TcSmem<D, PR>& S, int it_begin, 
 #pragma unroll 1
       for (int h = 0; h < nsub; ++h, ++n) {
         const int slot = n % kSlots;
-        mbar_wait(&S.kv_empty[kv][slot], ((n / kSlots) & 1) ^ 1);
-        trace(P, 0, tc, 10 + kv);  // 10: K load issued, 11: V load issued
+        trace(P, 0, tc, 12 + kv + (static_cast<int>(n) << 8));  // 12: K slot wanted, 13: V slot wanted
+        mbar_wait_1t(&S.kv_empty[kv][slot], ((n / kSlots) & 1) ^ 1);
+        trace(P, 0, tc, 10 + kv + (static_cast<int>(n) << 8));  // 10: K load issued, 11: V load issued
         if constexpr (PR) {
           // this CTA's half: K keys [64h + 32 rank, +32) (all d columns), V all 64 keys of its
           // d columns [64 rank, +64); completion counted on the leader's barrier, which expects
@@ -476,6 +518,10 @@ __device__ void run_mma(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, int 
     };
     auto issue_s = [&]() {
       const int t = cs.t;
+      if (kSP && js > 0) {  // the single S buffer: softmax(js - 1) has loaded it
+        wait_lead<PR>(&S.s_free[x][(js - 1) & 1], ((js - 1) >> 1) & 1);
+        tc_fence_after();
+      }
       if (cs.h == 0 && (t == tb || a.tiles[t].rot_delta != a.tiles[t - 1].rot_delta)) {
         if (t != tb) release_q();  // the previous epoch's Q tile: free once its S MMAs are done
         wait_lead<PR>(&S.q_full[x][q_slot(J, ep)], q_par(J, ep));
@@ -483,7 +529,7 @@ __device__ void run_mma(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, int 
         qcur = ep++;
       }
       wait_kv(0, js);
-      trace(P, 1, tc, 22);  // 22: K ready
+      trace(P, 1, tc, 22 + (static_cast<int>(js) << 8));  // 22: K ready
       const uint32_t qbase = smem_u32(q_tile<D, PR>(S, J, x, qcur));
       const uint32_t kb = smem_u32(&S.k[js % kKS][0][0]);
       const int buf = js & 1;
@@ -492,9 +538,9 @@ __device__ void run_mma(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, int 
         const uint64_t ad = desc_sw128(qbase + (kk / 4) * Sm::kChunkBytes + (kk % 4) * 32, 16, 1024);
         const uint64_t bd = desc_sw128(kb + (kk / 4) * Sm::kKChunkBytes + (kk % 4) * 32, 16, 1024);
         if constexpr (PR)
-          mma2_ss(tmem + kColS + 128 * x + 64 * buf, ad, bd, idS, kk > 0 ? 1u : 0u);
+          mma2_ss(tmem + col_s(x, buf), ad, bd, idS, kk > 0 ? 1u : 0u);
         else
-          mma_ss(tmem + kColS + 128 * x + 64 * buf, ad, bd, idS, kk > 0 ? 1u : 0u);
+          mma_ss(tmem + col_s(x, buf), ad, bd, idS, kk > 0 ? 1u : 0u);
       }
       commit_x<PR>(&S.s_full[x][buf]);
       commit_x<PR>(&S.kv_empty[0][js % kKS]);  // K_js (one of the heads' two arrivals)
@@ -504,7 +550,7 @@ __device__ void run_mma(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, int 
     };
     auto issue_pv = [&](uint32_t j, bool first) {
       wait_kv(1, j);
-      trace(P, 1, tc, 24);  // 24: V ready
+      trace(P, 1, tc, 24 + (static_cast<int>(j) << 8));  // 24: V ready
       // V sub-tile, MN-major: 64-column d chunks kSubBytes apart (LBO), 16 keys = 2048 B per K step
       const uint32_t vb = smem_u32(&S.v[j % kVS][0][0]);
       const int buf = j & 1;
@@ -512,11 +558,9 @@ __device__ void run_mma(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, int 
       for (int kk = 0; kk < 4; ++kk) {
         const uint64_t vd = desc_sw128(vb + kk * 2048, Sm::kSubBytes, 1024);
         if constexpr (PR)
-          mma2_ts(tmem + kColO + 128 * x, tmem + kColS + 128 * x + 64 * buf + kk * 8, vd, idO,
-                  (!first || kk > 0) ? 1u : 0u);
+          mma2_ts(tmem + col_o(x), tmem + col_p(x, buf) + kk * 8, vd, idO, (!first || kk > 0) ? 1u : 0u);
         else
-          mma_ts(tmem + kColO + 128 * x, tmem + kColS + 128 * x + 64 * buf + kk * 8, vd, idO,
-                 (!first || kk > 0) ? 1u : 0u);
+          mma_ts(tmem + col_o(x), tmem + col_p(x, buf) + kk * 8, vd, idO, (!first || kk > 0) ? 1u : 0u);
       }
       commit_x<PR>(&S.o_done[x][j & 1]);
       commit_x<PR>(&S.kv_empty[1][j % kVS]);  // V_j
@@ -525,16 +569,20 @@ __device__ void run_mma(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, int 
       // prefill items are one epoch (rot_delta 0 on every tile) of w.n_sub sub-tiles: the issuer
       // walks them by count, with no work-list reads on its critical path (each tile read is an
       // L1-miss-prone global load: ~40-600 cycles per step otherwise)
-      const int ns = u.w.n_sub;
-      int si = 0;  // S sub-tiles issued for this item
+      int ns = u.w.n_sub;  // sub-tiles of the item whose S MMAs are being issued
+      int si = 0;          // S sub-tiles issued for that item
       auto issue_s_cnt = [&]() {
+        if (kSP && js > 0) {  // the single S buffer: softmax(js - 1) has loaded it
+          wait_lead<PR>(&S.s_free[x][(js - 1) & 1], ((js - 1) >> 1) & 1);
+          tc_fence_after();
+        }
         if (si == 0) {
           wait_lead<PR>(&S.q_full[x][q_slot(J, ep)], q_par(J, ep));
           trace(P, 1, tc, 21);  // 21: Q ready for new epoch
           qcur = ep++;
         }
         wait_kv(0, js);
-        trace(P, 1, tc, 22);  // 22: K ready
+        trace(P, 1, tc, 22 + (static_cast<int>(js) << 8));  // 22: K ready
         const uint32_t qbase = smem_u32(q_tile<D, PR>(S, J, x, qcur));
         const uint32_t kb = smem_u32(&S.k[js % kKS][0][0]);
         const int buf = js & 1;
@@ -543,15 +591,57 @@ __device__ void run_mma(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, int 
           const uint64_t ad = desc_sw128(qbase + (kk / 4) * Sm::kChunkBytes + (kk % 4) * 32, 16, 1024);
           const uint64_t bd = desc_sw128(kb + (kk / 4) * Sm::kKChunkBytes + (kk % 4) * 32, 16, 1024);
           if constexpr (PR)
-            mma2_ss(tmem + kColS + 128 * x + 64 * buf, ad, bd, idS, kk > 0 ? 1u : 0u);
+            mma2_ss(tmem + col_s(x, buf), ad, bd, idS, kk > 0 ? 1u : 0u);
           else
-            mma_ss(tmem + kColS + 128 * x + 64 * buf, ad, bd, idS, kk > 0 ? 1u : 0u);
+            mma_ss(tmem + col_s(x, buf), ad, bd, idS, kk > 0 ? 1u : 0u);
         }
         commit_x<PR>(&S.s_full[x][buf]);
         commit_x<PR>(&S.kv_empty[0][js % kKS]);
         ++js;
         if (++si == ns) release_q();
       };
+      if constexpr (kSP) {
+        // one flat pipeline over the CTA's items: S(0) of the next item is issued as soon as the
+        // softmax has loaded the current item's last S (its Q was prepared a whole item ahead), so
+        // an item boundary costs no pipeline refill
+        int pv_left = ns, pv_next = -1;
+        bool pv_first = true, s_done = false;
+        issue_s_cnt();
+        for (;;) {
+          const uint32_t j = jg;
+          if (si == ns && pv_next < 0 && !s_done) {  // the S side moves on to the next item
+            const int c = src.next();
+            if (c < 0) {
+              s_done = true;
+            } else {
+              ns = decode<PR>(P, c).w.n_sub;
+              si = 0;
+              pv_next = ns;
+            }
+          }
+          if (si < ns) issue_s_cnt();  // S(j+1) as soon as softmax(j) has loaded S(j)
+          wait_lead<PR>(&S.p_full[x][j & 1], (j >> 1) & 1);
+          trace(P, 1, tc, 20);  // 20: P ready
+          if (pv_first && n_items > 0) {
+            // the previous item's O has been drained by the epilogue warps (the latest possible
+            // completion: this thread waited for n_items - 2 before the previous item's first PV)
+            wait_lead<PR>(&S.o_free[x], (n_items - 1) & 1);
+            tc_fence_after();
+            trace(P, 1, tc, 26);  // 26: O free for the next item
+          }
+          issue_pv(j, pv_first);
+          ++jg;
+          pv_first = false;
+          if (--pv_left == 0) {
+            ++n_items;
+            if (pv_next < 0) break;
+            pv_left = pv_next;
+            pv_next = -1;
+            pv_first = true;
+          }
+        }
+        break;  // every code of the launch has been consumed
+      }
       for (int i = 0; i < 2 && si < ns; ++i) issue_s_cnt();
       for (int pi = 0; pi < ns; ++pi) {
         const uint32_t j = jg;
@@ -569,17 +659,18 @@ __device__ void run_mma(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, int 
           trace(P, 1, tc, 26);  // 26: O free for the next item
         }
         issue_pv(j, pi == 0);
-        if (si < ns) issue_s_cnt();
+        if (si < ns) issue_s_cnt();  // S(j+2) into the buffer PV(j) reads
         ++jg;
       }
       ++n_items;
       continue;
     }
     // prologue: S for the first two sub-tiles
-    for (int i = 0; i < 2 && cs.t < te; ++i) issue_s();
+    for (int i = 0; i < (kSP ? 1 : 2) && cs.t < te; ++i) issue_s();
     bool first = true;
     while (cp.t < te) {
       const uint32_t j = jg;
+      if (kSP && cs.t < te) issue_s();  // S(j+1) as soon as softmax(j) has loaded S(j)
       wait_lead<PR>(&S.p_full[x][j & 1], (j >> 1) & 1);
       trace(P, 1, tc, 20);  // 20: P ready
       if (EPI && first && n_items > 0) {
@@ -591,7 +682,7 @@ __device__ void run_mma(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, int 
         trace(P, 1, tc, 26);  // 26: O free for the next item
       }
       issue_pv(j, first);
-      if (cs.t < te) issue_s();
+      if (!kSP && cs.t < te) issue_s();  // S(j+2) into the buffer PV(j) reads
       advance(cp);
       ++jg;
       first = false;
@@ -606,12 +697,35 @@ __device__ void run_mma(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, int 
 // only moves when the new max exceeds it by more than `thr` (log2 units: P <= 2^thr), and then
 // *alpha = 2^(m_old - m_new) is the factor for O and l. Returns the row sum of P (fp32, before
 // bf16 rounding; 8 independent accumulators).
-template <int PM, bool kMasked>
-__device__ __forceinline__ float softmax_sub(uint32_t scol, float sl2, float thr, int lim, float& m, float& alpha,
+__device__ __forceinline__ float ld_shared_volatile(const float* p) {
+  float v;
+  asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_shared_volatile(float* p, float v) {
+  asm volatile("st.volatile.shared.f32 [%0], %1;" ::"r"(smem_u32(p)), "f"(v) : "memory");
+}
+
+template <int PM, bool kMasked, bool PR>
+__device__ __forceinline__ float softmax_sub(uint32_t scol, uint32_t pcol, uint64_t* sfree, int pp_wait, int pp_give,
+                                             float* pp_words, float sl2, float thr, int lim, float& m, float& alpha,
                                              bool& resc) {
   uint32_t v[64];
   tmem_ld64(scol, v);
   tmem_wait_ld();
+  if constexpr (kSP) {  // S(j) is in registers: the issuer may compute S(j+1) into the buffer
+    tc_fence_before();
+    arrive_lead_warp<PR>(sfree);
+  }
+  // ping-pong: the two heads' softmax WGs take turns (named barriers 1 / 2), so each runs alone on
+  // the SMSPs' MUFU / issue slots and the two heads' MMAs reach the tensor core staggered
+  // (ptxas moves register-only math across a barrier freely: the exponentials are tied to it by
+  // a dependency on a shared-memory word read after it, the hand-over by a store of the row sum)
+  float pp_z = 0.f;
+  if (pp_wait) {
+    named_sync(pp_wait, 256);
+    pp_z = ld_shared_volatile(pp_words);
+  }
   if constexpr (kMasked) {
 #pragma unroll
     for (int i = 0; i < 64; ++i) v[i] = i <= lim ? v[i] : 0xff800000u;  // -inf
@@ -628,7 +742,7 @@ __device__ __forceinline__ float softmax_sub(uint32_t scol, float sl2, float thr
   const float m_use = resc ? m_new : m;
   alpha = resc ? ex2_approx(m - m_new) : 1.f;
   m = m_use;
-  const float msub = (m_use == -INFINITY) ? 0.f : m_use;
+  const float msub = ((m_use == -INFINITY) ? 0.f : m_use) + pp_z;
   // x = s * scale - m and the row sums in packed fp32x2 (FFMA2 / FADD2: half the instructions)
   float2 sum4[4];
 #pragma unroll
@@ -660,11 +774,16 @@ __device__ __forceinline__ float softmax_sub(uint32_t scol, float sl2, float thr
     sum4[i & 3] = fadd2(sum4[i & 3], make_float2(p0, p1));
     pk[i] = pack_bf16x2(p0, p1);
   }
-  tmem_st32(scol, pk);
-  tmem_wait_st();
   const float2 s01 = fadd2(sum4[0], sum4[1]), s23 = fadd2(sum4[2], sum4[3]);
   const float2 st = fadd2(s01, s23);
-  return st.x + st.y;
+  const float rsum = st.x + st.y;
+  if (pp_give) {
+    st_shared_volatile(pp_words + 1, rsum);
+    named_arrive(pp_give, 256);
+  }
+  tmem_st32(pcol, pk);
+  tmem_wait_st();
+  return rsum;
 }
 
 // ------------------------------------------------------------------ softmax + epilogue (one WG per head)
@@ -815,7 +934,7 @@ __device__ void prefill_epilogue(const TcParams& P, TcSmem<D, PR>& S, uint32_t t
     mbar_wait(&S.o_done[x][jlast & 1], (jlast >> 1) & 1);
     tc_fence_after();
     if (tr) trace(P, 4, tc, 61 + 4 * x);  // 61/65: O ready
-    const uint32_t ocol = tmem + lane_base + kColO + 128 * x;
+    const uint32_t ocol = tmem + lane_base + col_o(x);
     const int h = u.head_a + x;
     uint32_t vv[2][32];
     tmem_ld32(ocol, vv[0]);
@@ -907,12 +1026,16 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, 
   const int r = threadIdx.x & 127;  // row within the tile == TMEM lane
   const uint32_t lane_base = static_cast<uint32_t>((r / 32) * 32) << 16;
   const float sl2 = P.scale_log2;
-  const uint32_t ocol = tmem + lane_base + kColO + 128 * x;
+  const uint32_t ocol = tmem + lane_base + col_o(x);
   uint32_t js = 0;  // sub-tiles processed (global; == the MMA warps' PV index)
   uint32_t eps = 0, ecur = 0;  // Q epochs seen / current (join: Q slots are also epilogue staging)
   uint32_t ni = 0;             // prefill: items finished by this WG (fin_inv buffer ni & 1)
   uint32_t tc = 0;
   const bool tr = (threadIdx.x & 31) == 0;
+  // ping-pong of the two WGs (paired launches: both see the same sub-tile sequence). Barrier 1:
+  // A -> B ("A has finished its exponentials of sub-tile j"), barrier 2: B -> A (j -> j + 1)
+  const bool pp = kPingPong && P.paired && dbg_mode(P) == 0;
+  const int pp_give = pp ? 1 + x : 0;
   ItemSrc<D, EPI, PR> src(P, S, it_begin, it_end, false, true);
   for (int code; (code = src.next()) >= 0;) {
     const Unit u = decode<PR>(P, code);
@@ -933,7 +1056,8 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, 
       }
       for (int hh = 0; hh < nsub; ++hh, ++js) {
         const int buf = js & 1;
-        const uint32_t scol = tmem + lane_base + kColS + 128 * x + 64 * buf;
+        const uint32_t scol = tmem + lane_base + col_s(x, buf);
+        const uint32_t pcol = tmem + lane_base + col_p(x, buf);
         // key index i of this sub-tile is visible iff i <= lim
         const int lim = min(tl.n_valid - 1, tl.causal ? p - tl.key_pos0 : kTileKeys - 1) - 64 * hh;
 #ifdef SPANQ_SPIN_SOFTMAX
@@ -941,7 +1065,7 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, 
 #else
         mbar_wait(&S.s_full[x][buf], (js >> 1) & 1);
 #endif
-        if (tr) trace(P, 2 + x, tc, 30);  // 30: S ready
+        if (tr) trace(P, 2 + x, tc, 30 + (static_cast<int>(js) << 8));  // 30: S ready
         tc_fence_after();
         // masks only on partial sub-tiles
         const bool full = __all_sync(0xffffffffu, lim >= 63);
@@ -953,9 +1077,16 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, 
           resc = false;
           sum = 1.f;
           m = 0.f;
+          if (kSP) {
+            tc_fence_before();
+            arrive_lead_warp<PR>(&S.s_free[x][buf]);
+          }
         } else {
-          sum = full ? softmax_sub<PM, false>(scol, sl2, P.rescale_threshold, lim, m, alpha, resc)
-                     : softmax_sub<PM, true>(scol, sl2, P.rescale_threshold, lim, m, alpha, resc);
+          const int pp_wait = !pp ? 0 : (x == 1 ? 1 : (js > 0 ? 2 : 0));
+          sum = full ? softmax_sub<PM, false, PR>(scol, pcol, &S.s_free[x][buf], pp_wait, pp_give, &S.pp_zero, sl2,
+                                                  P.rescale_threshold, lim, m, alpha, resc)
+                     : softmax_sub<PM, true, PR>(scol, pcol, &S.s_free[x][buf], pp_wait, pp_give, &S.pp_zero, sl2,
+                                                 P.rescale_threshold, lim, m, alpha, resc);
         }
         l = l * alpha + sum;
         // O is only touched when a row's running max moved (rare with the threshold): then PV of
@@ -977,7 +1108,7 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, 
           }
           tmem_wait_st();
         }
-        if (tr) trace(P, 2 + x, tc, 31);  // 31: P written
+        if (tr) trace(P, 2 + x, tc, 31 + (static_cast<int>(js) << 8));  // 31: P written
         tc_fence_before();
         arrive_lead_warp<PR>(&S.p_full[x][buf]);
         first = false;
@@ -1006,6 +1137,7 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, 
     f.elast = ecur;
     epilogue<D, PR>(P, S, ocol, x, f, tc, tr);
   }
+  if (pp && x == 0 && js > 0) named_sync(2, 256);  // B's last hand-over
   tc_fence_before();
 }
 
@@ -1065,7 +1197,7 @@ __device__ __forceinline__ void load_cs8(const float2* rope, int64_t idx, float2
 
 template <int D>
 __device__ __forceinline__ void rotate_q_tile(uint8_t* qs_base, const float2* rope, int my_pos, int my_valid, int rot,
-                                              int max_pos) {
+                                              int max_pos, const TcParams* tp = nullptr, uint32_t* tc = nullptr) {
   constexpr int kLanesPerRow = D / 16;       // 8 pairs per lane
   constexpr int R = 32 / kLanesPerRow;       // rows per step
   const int lane = threadIdx.x & 31;
@@ -1079,14 +1211,18 @@ __device__ __forceinline__ void rotate_q_tile(uint8_t* qs_base, const float2* ro
   const bool consecutive = __all_sync(0xffffffffu, !my_valid || my_pos == p_first + lane) && p_first - rot >= 0 &&
                            p_first - rot + 31 < max_pos;
   float2 cc[4], ss[4];
+  if (tp != nullptr && lane == 0) trace(*tp, 4, *tc, consecutive ? 46 : 47);  // 46/47: rotation (fast/slow path)
   if (consecutive) {
     float2 cd[4], sd[4];
     load_cs8(rope, static_cast<int64_t>(p_first - rot + g) * (D / 2) + pair0, cc, ss);
     load_cs8(rope, static_cast<int64_t>(R) * (D / 2) + pair0, cd, sd);  // position R: (cos R th, sin R th)
     float2 sdn[4];
+    if (tp != nullptr && lane == 0) trace(*tp, 4, *tc, 48 + (__float_as_int(cc[0].x) == 0x7fffffff));  // 48: table read
 #pragma unroll
     for (int e = 0; e < 4; ++e) sdn[e] = fmul2(sd[e], make_float2(-1.f, -1.f));
-#pragma unroll
+    // rolled: the unrolled 8-step body is ~8 KB of SASS, and a cold instruction cache made the
+    // first rotation of a launch ~10K cycles (CTA-0 trace of a C2 join)
+#pragma unroll 1
     for (int st = 0; st < 32 / R; ++st) {
       rotate_step<D>(qs_base, wq * 32 + st * R + g, u, cc, ss);
 #pragma unroll
@@ -1174,7 +1310,7 @@ __device__ void run_qprep(const TcParams& P, TcSmem<D, PR>& S, int it_begin, int
           mbar_wait(&S.q_load[x][sl], (load_phase >> bit) & 1);
           load_phase ^= 1u << bit;
           if (tr) trace(P, 4, tc, 44 + x);  // 44/45: Q tile A/B loaded
-          rotate_q_tile<D>(q_tile<D, PR>(S, J, x, ep), a.rope, my_pos, my_row < w.n_rows, rot, a.max_pos);
+          rotate_q_tile<D>(q_tile<D, PR>(S, J, x, ep), a.rope, my_pos, my_row < w.n_rows, rot, a.max_pos, &P, &tc);
           fence_proxy_async_smem();
         } else {
           mbar_wait(&S.q_empty[x][sl], epar);
@@ -1306,6 +1442,7 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
       for (int b = 0; b < 2; ++b) {
         mbar_init(&S.s_full[i][b], 1);
         mbar_init(&S.p_full[i][b], kRole);
+        mbar_init(&S.s_free[i][b], kRole);
       }
       mbar_init(&S.o_done[i][0], 1);
       mbar_init(&S.sched_full[2 * i], 1);
@@ -1317,6 +1454,7 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
       mbar_init(&S.fin_full[i][0], 128);
       mbar_init(&S.fin_full[i][1], 128);
     }
+    S.pp_zero = 0.f;
     fence_barrier_init();
   }
   if (warp == 0 && (threadIdx.x & 31) == 0) {

@@ -75,7 +75,25 @@ __global__ void __launch_bounds__(512, 1) rate(int mode, int iters, long long* o
   tc_fence_after();
   const uint32_t tm = s.tmem;
   long long t0 = clock64();
-  if (warp >= 4 && warp < 12 && (mode & 1)) {
+  if (mode >= 16 && warp >= 4 && warp < ((mode & 1) ? 12 : 8)) {
+    // raw ex2 throughput: 16 independent chains per thread, 64 ex2 per iteration
+    float r[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) r[i] = -0.001f * (t + i);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) r[i] = -ex2_approx(r[i]);
+    }
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc += r[i];
+    sink[blockIdx.x * 512 + t] = acc;
+    long long t1 = clock64();
+    if ((t & 127) == 0) out[blockIdx.x * 4 + (warp < 8 ? 0 : 1)] = t1 - t0;
+  }
+  if (mode < 16 && warp >= 4 && warp < ((mode & 4) ? 8 : 12) && (mode & 1)) {
     const int x = warp < 8 ? 0 : 1;
     const uint32_t lane_base = static_cast<uint32_t>(((t & 127) / 32) * 32) << 16;
     float m = -INFINITY, l = 0.f;
@@ -121,14 +139,14 @@ int main() {
   const int smem = sizeof(Sm) + 1024;
   cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 2000;
-  for (int mode = 1; mode <= 3; ++mode) {
+  for (int mode : {1, 2, 3, 5, 7, 16, 17}) {
     cudaMemset(d, 0, 148 * 4 * 8);
     rate<<<148, 512, smem>>>(mode, iters, d, sink);
     cudaDeviceSynchronize();
     long long h[148 * 4];
     cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
     printf("mode %d (%s): softmax A %.1f B %.1f cycles/sub-tile, MMA %.1f cycles/period\n", mode,
-           mode == 1 ? "softmax only" : mode == 2 ? "MMA only" : "both", h[0] / double(iters), h[1] / double(iters),
+           mode == 1 ? "softmax only" : mode == 2 ? "MMA only" : mode == 3 ? "both" : mode == 5 ? "softmax A only" : mode == 7 ? "softmax A + MMA" : mode == 16 ? "ex2 x64, warps 4-7" : "ex2 x64, warps 4-11", h[0] / double(iters), h[1] / double(iters),
            h[2] / double(iters));
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
