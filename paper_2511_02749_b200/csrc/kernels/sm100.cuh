@@ -447,6 +447,10 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t smem_addr, uint32_t lbo_
   d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
   return d;
 }
+// The descriptor of an operand `bytes` further into shared memory: the start-address field is
+// the low 14 bits (address >> 4) and shared memory stays below 256 KB, so a plain add never
+// carries out of the field (one integer add instead of rebuilding the descriptor)
+__device__ __forceinline__ uint64_t desc_add(uint64_t d, uint32_t bytes) { return d + (bytes >> 4); }
 // kind::f16 instruction descriptor: bf16 x bf16 -> fp32.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N, bool a_mn_major,
                                                       bool b_mn_major) {

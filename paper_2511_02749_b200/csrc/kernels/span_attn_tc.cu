@@ -248,6 +248,27 @@ __device__ __forceinline__ void mbar_wait_1t(uint64_t* bar, uint32_t parity) {
   mbar_wait(bar, parity);
 #endif
 }
+// The softmax hand-overs on the MMA issuer's critical path (S loaded, P written): one arrival per
+// warp (after __syncwarp) instead of 128 per-thread arrivals (SPANQ_WARPARRIVE=1, A/B build: no measurable gain, and
+// compute-sanitizer racecheck does not credit the __syncwarp ordering)
+#ifndef SPANQ_WARPARRIVE
+#define SPANQ_WARPARRIVE 0
+#endif
+template <bool PR>
+__device__ __forceinline__ void arrive_hand(uint64_t* bar) {
+  if constexpr (PR || SPANQ_WARPARRIVE) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      if constexpr (PR)
+        mbar_arrive_cl(cluster_addr(bar, 0));
+      else
+        mbar_arrive(bar);
+    }
+  } else {
+    mbar_arrive(bar);
+  }
+}
+__host__ __device__ constexpr uint32_t kHandCount(bool pr) { return (pr ? 8u : (SPANQ_WARPARRIVE ? 4u : 128u)); }
 template <bool PR>
 __device__ __forceinline__ void wait_lead(uint64_t* bar, uint32_t parity) {
   if constexpr (PR)
@@ -533,10 +554,11 @@ __device__ void run_mma(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, int 
       const uint32_t qbase = smem_u32(q_tile<D, PR>(S, J, x, qcur));
       const uint32_t kb = smem_u32(&S.k[js % kKS][0][0]);
       const int buf = js & 1;
+      const uint64_t ad0 = desc_sw128(qbase, 16, 1024), bd0 = desc_sw128(kb, 16, 1024);
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
-        const uint64_t ad = desc_sw128(qbase + (kk / 4) * Sm::kChunkBytes + (kk % 4) * 32, 16, 1024);
-        const uint64_t bd = desc_sw128(kb + (kk / 4) * Sm::kKChunkBytes + (kk % 4) * 32, 16, 1024);
+        const uint64_t ad = desc_add(ad0, (kk / 4) * Sm::kChunkBytes + (kk % 4) * 32);
+        const uint64_t bd = desc_add(bd0, (kk / 4) * Sm::kKChunkBytes + (kk % 4) * 32);
         if constexpr (PR)
           mma2_ss(tmem + col_s(x, buf), ad, bd, idS, kk > 0 ? 1u : 0u);
         else
@@ -554,9 +576,10 @@ __device__ void run_mma(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, int 
       // V sub-tile, MN-major: 64-column d chunks kSubBytes apart (LBO), 16 keys = 2048 B per K step
       const uint32_t vb = smem_u32(&S.v[j % kVS][0][0]);
       const int buf = j & 1;
+      const uint64_t vd0 = desc_sw128(vb, Sm::kSubBytes, 1024);
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
-        const uint64_t vd = desc_sw128(vb + kk * 2048, Sm::kSubBytes, 1024);
+        const uint64_t vd = desc_add(vd0, kk * 2048);
         if constexpr (PR)
           mma2_ts(tmem + col_o(x), tmem + col_p(x, buf) + kk * 8, vd, idO, (!first || kk > 0) ? 1u : 0u);
         else
@@ -586,10 +609,11 @@ __device__ void run_mma(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, int 
         const uint32_t qbase = smem_u32(q_tile<D, PR>(S, J, x, qcur));
         const uint32_t kb = smem_u32(&S.k[js % kKS][0][0]);
         const int buf = js & 1;
+        const uint64_t ad0 = desc_sw128(qbase, 16, 1024), bd0 = desc_sw128(kb, 16, 1024);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint64_t ad = desc_sw128(qbase + (kk / 4) * Sm::kChunkBytes + (kk % 4) * 32, 16, 1024);
-          const uint64_t bd = desc_sw128(kb + (kk / 4) * Sm::kKChunkBytes + (kk % 4) * 32, 16, 1024);
+          const uint64_t ad = desc_add(ad0, (kk / 4) * Sm::kChunkBytes + (kk % 4) * 32);
+          const uint64_t bd = desc_add(bd0, (kk / 4) * Sm::kKChunkBytes + (kk % 4) * 32);
           if constexpr (PR)
             mma2_ss(tmem + col_s(x, buf), ad, bd, idS, kk > 0 ? 1u : 0u);
           else
@@ -715,7 +739,7 @@ __device__ __forceinline__ float softmax_sub(uint32_t scol, uint32_t pcol, uint6
   tmem_wait_ld();
   if constexpr (kSP) {  // S(j) is in registers: the issuer may compute S(j+1) into the buffer
     tc_fence_before();
-    arrive_lead_warp<PR>(sfree);
+    arrive_hand<PR>(sfree);
   }
   // ping-pong: the two heads' softmax WGs take turns (named barriers 1 / 2), so each runs alone on
   // the SMSPs' MUFU / issue slots and the two heads' MMAs reach the tensor core staggered
@@ -1079,7 +1103,7 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, 
           m = 0.f;
           if (kSP) {
             tc_fence_before();
-            arrive_lead_warp<PR>(&S.s_free[x][buf]);
+            arrive_hand<PR>(&S.s_free[x][buf]);
           }
         } else {
           const int pp_wait = !pp ? 0 : (x == 1 ? 1 : (js > 0 ? 2 : 0));
@@ -1110,7 +1134,7 @@ __device__ void run_softmax(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, 
         }
         if (tr) trace(P, 2 + x, tc, 31 + (static_cast<int>(js) << 8));  // 31: P written
         tc_fence_before();
-        arrive_lead_warp<PR>(&S.p_full[x][buf]);
+        arrive_hand<PR>(&S.p_full[x][buf]);
         first = false;
       }
     }
@@ -1441,8 +1465,8 @@ __global__ void __launch_bounds__(kThreads, 1) span_attn_tc_kernel(const __grid_
     for (int i = 0; i < 2; ++i) {
       for (int b = 0; b < 2; ++b) {
         mbar_init(&S.s_full[i][b], 1);
-        mbar_init(&S.p_full[i][b], kRole);
-        mbar_init(&S.s_free[i][b], kRole);
+        mbar_init(&S.p_full[i][b], kHandCount(PR));
+        mbar_init(&S.s_free[i][b], kHandCount(PR));
       }
       mbar_init(&S.o_done[i][0], 1);
       mbar_init(&S.sched_full[2 * i], 1);

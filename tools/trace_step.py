@@ -1,7 +1,7 @@
 """Profiling only: CTA-0 event timeline of the span_attn_tc kernel for one C2 prefill launch.
 Needs the profiling build (python -m paper_2511_02749_b200.build --profiling); uses it unless
 SPANQ_LIB points elsewhere.
-Usage: python tools/trace_step.py [dbg_mode] [prefill|join] [fp32|bf16] > gpurun_out/trace.txt"""
+Usage: python tools/trace_step.py [dbg_mode] [prefill|join] [fp32|bf16] [C2|C4] > gpurun_out/trace.txt"""
 import os
 import sys
 
@@ -16,7 +16,8 @@ from paper_2511_02749_b200 import inputs, runner, spanq
 mode = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 out_dtype = sys.argv[3] if len(sys.argv) > 3 else "fp32"
 dev = torch.device("cuda:0")
-w = inputs.c2()
+cfg = sys.argv[4] if len(sys.argv) > 4 else "C2"
+w = inputs.c2() if cfg == "C2" else inputs.CONFIGS[cfg]()
 ctx = spanq.Context(w.shape, 1024, device=0, max_position=1 << 15, out_dtype=out_dtype)
 ctx.set_trace(None, mode)
 tabs = [runner.device_tables(w.shape, 0, w.seed, dev)]
@@ -31,14 +32,14 @@ plan = ctx.plan(w.queries)
 view = plan.view()
 ptok = runner.prefill_tokens(view, w.queries)
 q, k, v = runner.gather(tabs[0], ptok, dev)
-o = torch.empty((len(ptok), 32, 128), dtype=torch.float32 if out_dtype == "fp32" else torch.bfloat16, device=dev)
+o = torch.empty((len(ptok), w.shape.hq, w.shape.d), dtype=torch.float32 if out_dtype == "fp32" else torch.bfloat16, device=dev)
 if which == "prefill":
     ctx.set_trace(buf, mode)
 plan.prefill(0, q, k, v, o)
 if which == "join":
     jtok = runner.join_tokens(view, w.queries)
     qj, kj, vj = runner.gather(tabs[0], jtok, dev)
-    oj = torch.empty((len(jtok), 32, 128), dtype=torch.float32 if out_dtype == "fp32" else torch.bfloat16, device=dev)
+    oj = torch.empty((len(jtok), w.shape.hq, w.shape.d), dtype=torch.float32 if out_dtype == "fp32" else torch.bfloat16, device=dev)
     ctx.set_trace(buf, mode)
     plan.join(0, qj, kj, vj, oj)
 torch.cuda.synchronize()
