@@ -564,6 +564,7 @@ __device__ void run_mma(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, int 
         else
           mma_ss(tmem + col_s(x, buf), ad, bd, idS, kk > 0 ? 1u : 0u);
       }
+      trace(P, 1, tc, 25 + (static_cast<int>(js) << 8));  // 25: S MMAs accepted
       commit_x<PR>(&S.s_full[x][buf]);
       commit_x<PR>(&S.kv_empty[0][js % kKS]);  // K_js (one of the heads' two arrivals)
       advance(cs);
@@ -585,6 +586,7 @@ __device__ void run_mma(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, int 
         else
           mma_ts(tmem + col_o(x), tmem + col_p(x, buf) + kk * 8, vd, idO, (!first || kk > 0) ? 1u : 0u);
       }
+      trace(P, 1, tc, 27 + (static_cast<int>(j) << 8));  // 27: PV MMAs accepted
       commit_x<PR>(&S.o_done[x][j & 1]);
       commit_x<PR>(&S.kv_empty[1][j % kVS]);  // V_j
     };
@@ -619,7 +621,8 @@ __device__ void run_mma(const TcParams& P, TcSmem<D, PR>& S, uint32_t tmem, int 
           else
             mma_ss(tmem + col_s(x, buf), ad, bd, idS, kk > 0 ? 1u : 0u);
         }
-        commit_x<PR>(&S.s_full[x][buf]);
+        trace(P, 1, tc, 25 + (static_cast<int>(js) << 8));  // 25: S MMAs accepted
+      commit_x<PR>(&S.s_full[x][buf]);
         commit_x<PR>(&S.kv_empty[0][js % kKS]);
         ++js;
         if (++si == ns) release_q();

@@ -57,7 +57,7 @@ order = np.argsort(en)
 print("# slowest CTAs:", [(int(i), round(float(en[i]), 1)) for i in order[-6:]])
 print("# fastest CTAs:", [(int(i), round(float(en[i]), 1)) for i in order[:6]])
 print("# end_us_by_cta:", " ".join(f"{float(e):.0f}" for e in en))
-names = {10: "K issue", 11: "V issue", 12: "K want", 13: "V want", 20: "P_A rdy", 21: "Q rdy", 22: "K rdy", 23: "P_B rdy", 24: "V rdy", 25: "S issued", 38: "item setup",
+names = {10: "K issue", 11: "V issue", 12: "K want", 13: "V want", 20: "P_A rdy", 21: "Q rdy", 22: "K rdy", 23: "P_B rdy", 24: "V rdy", 25: "S issued", 27: "PV issued", 38: "item setup",
          30: "S rdy", 31: "P done", 32: "O rdy", 33: "epi done", 36: "stg free", 37: "stg stored", 40: "slotA free", 41: "slotB free", 42: "QA done",
          43: "QB done", 46: "rot fast", 47: "rot slow", 48: "rot table", 44: "QA loaded", 45: "QB loaded", 34: "max done", 35: "exp start", 50: "stg0", 51: "stg1", 52: "stg2", 53: "stg3",
          26: "O free", 60: "finA", 61: "O_A rdy", 62: "O_A drained", 64: "finB", 65: "O_B rdy", 66: "O_B drained"}
