@@ -209,6 +209,16 @@ void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_en
   finish_join(qt, o, ph, w);
 }
 
+double join_flops(const PlanHost& p, const WorkOpts& o, int q_begin, int q_end) {
+  double f = 0;
+  for (const Segment& c : p.segs) {
+    if (c.kind != kCross || c.query < q_begin || c.query >= q_end) continue;
+    const double before = static_cast<double>(c.pos0);
+    for (int32_t j = 0; j < c.tok_len; ++j) f += before + j + 1;
+  }
+  return f * 4.0 * o.d * o.hq;
+}
+
 namespace {
 // Items of a join work list from its q tiles: one item per (q tile, unit), or (allow_split +
 // persistent) the stream-K cut into <= num_sms equal-cost contiguous ranges.

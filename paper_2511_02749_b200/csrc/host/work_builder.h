@@ -59,6 +59,9 @@ struct JoinPhase {
 // launch over every segment.
 void build_join_work(const PlanHost& p, const WorkOpts& o, int q_begin, int q_end, AttnWorkHost* w,
                      const JoinPhase* ph = nullptr);
+// Algorithmic FLOPs of the join of queries [q_begin, q_end) (the `flops` build_join_work reports,
+// without building the work list): 4·d·Hq per visible (cross row, key) pair
+double join_flops(const PlanHost& p, const WorkOpts& o, int q_begin, int q_end);
 
 // Owner-side split join: the plan's tasks — each a home query's cross rows
 // (rows in task order, packed) over the fragments of it owned here at Δ_f — as one join work list.

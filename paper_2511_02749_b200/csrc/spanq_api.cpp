@@ -136,6 +136,10 @@ struct spq_plan {
   float* lsepart = nullptr;
   std::vector<uint8_t> padded_layers;
   spq::AttnWorkHost pw_host, jw_host;  // kept for sub-range rebuilds / inspection
+  // W = 1 GPU plans build and upload the join's work list at the first full join call (its own
+  // device buffer, partials included): that host work then overlaps the prefill on the GPU
+  bool jw_lazy = false;
+  uint8_t* jbuf = nullptr;
   std::vector<std::vector<int32_t>> cross_tokens;  // per query (plus distribution: commit)
   // owner-side split join (world > 1, cfg.split_join)
   bool split = false;
@@ -639,7 +643,8 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
   lap("view arrays");
   spq::build_prefill_work(H, prefill_opts(c), 0, static_cast<int>(H.jobs.size()), &p->pw_host);
   lap("prefill work");
-  spq::build_join_work(H, o, 0, H.n_queries, &p->jw_host);
+  p->jw_lazy = is_gpu(c) && c->cfg.world_size == 1;
+  if (!p->jw_lazy) spq::build_join_work(H, o, 0, H.n_queries, &p->jw_host);
   // W > 1: the join again as two phases around the exchange (held segments, then the received
   // fragments), for spq_join_phase; needs split partials (the persistent bf16 path)
   if (is_gpu(c) && o.allow_split && o.persistent && !H.recv_blocks.empty()) {
@@ -724,7 +729,7 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
     }
   }
   p->prefill_flops = p->pw_host.flops;
-  p->join_flops = p->jw_host.flops;
+  p->join_flops = p->jw_lazy ? spq::join_flops(H, o, 0, H.n_queries) : p->jw_host.flops;
   // algorithmic bytes of rope_kv_write: per written row, read k,v and write both pages
   // (4*Hkv*d*elt), plus 12 B of pos/slot metadata per row
   const int64_t row_bytes = 4LL * c->cfg.num_kv_heads * c->cfg.head_dim * elt_size(c);
@@ -766,7 +771,7 @@ spq_status spq_plan_create(spq_ctx* c, const spq_query* queries, int32_t n_queri
       w->flops = h.flops;
     };
     add_work(p->pw_host, &p->pw);
-    add_work(p->jw_host, &p->jw);
+    if (!p->jw_lazy) add_work(p->jw_host, &p->jw);
     if (p->phased) {
       add_work(p->jw1_host, &p->jw1);
       add_work(p->jw2_host, &p->jw2);
@@ -1006,6 +1011,55 @@ spq_status launch_join_list(spq_ctx* c, const DevWork& w, uint8_t* buf, spq::Att
   return SPQ_OK;
 }
 
+// The join's work list of a lazy (W = 1) plan, built and uploaded at its first full join: the
+// packed arrays then the split-KV partials in one device buffer, copied from the ctx's pinned
+// staging buffer (reused once the plan upload that last used it has completed)
+spq_status ensure_join_work(spq_ctx* c, spq_plan* p, cudaStream_t st) {
+  if (p->jbuf != nullptr) return SPQ_OK;
+  spq::build_join_work(p->host, work_opts(c, c->cfg.dtype == SPQ_BF16), 0, p->host.n_queries, &p->jw_host);
+  const spq::AttnWorkHost& h = p->jw_host;
+  Packer pk;
+  DevWork& w = p->jw;
+  w.tiles = pk.add(h.tiles);
+  w.tile_blocks = pk.add(h.tile_blocks);
+  w.items = pk.add(h.items);
+  w.cta_off = pk.add(h.cta_off);
+  w.cta_items = pk.add(h.cta_items);
+  w.sched = pk.add(kZeros2);  // claim counters (self-resetting)
+  w.dynamic = h.dynamic;
+  w.n_codes = static_cast<int32_t>(h.cta_items.size());
+  w.combine = pk.add(h.combine);
+  w.n_items = static_cast<int32_t>(h.items.size());
+  w.grid = h.grid;
+  w.cluster = h.cluster;
+  w.n_combine = static_cast<int32_t>(h.combine.size());
+  w.n_parts = h.n_parts;
+  w.flops = h.flops;
+  size_t bytes = std::max<size_t>(pk.size, 256);
+  size_t off_opart = 0, off_lsepart = 0;
+  if (w.n_parts > 0) {
+    const size_t rows = static_cast<size_t>(w.n_parts) * heads_per_unit(c) * spq::kTileRows;
+    off_opart = align_up(bytes, 1024);
+    off_lsepart = align_up(off_opart + rows * c->cfg.head_dim * sizeof(float), 1024);
+    bytes = off_lsepart + rows * sizeof(float);
+  }
+  CUDA_TRY(cudaEventSynchronize(c->staging_ev));
+  if (c->staging_size < pk.size) {
+    if (c->staging) CUDA_TRY(cudaFreeHost(c->staging));
+    c->staging_size = std::max(pk.size, static_cast<size_t>(1) << 20);
+    CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&c->staging), c->staging_size));
+  }
+  pk.write(c->staging);
+  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->jbuf), bytes, st));
+  CUDA_TRY(cudaMemcpyAsync(p->jbuf, c->staging, pk.size, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaEventRecord(c->staging_ev, st));
+  if (w.n_parts > 0) {
+    p->opart = reinterpret_cast<float*>(p->jbuf + off_opart);
+    p->lsepart = reinterpret_cast<float*>(p->jbuf + off_lsepart);
+  }
+  return SPQ_OK;
+}
+
 spq_status join_impl(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t b, const void* q, const void* k,
                      const void* v, void* o, float* lse, void* stream, int mode, float* split_out = nullptr,
                      float* split_lse = nullptr) {
@@ -1020,6 +1074,12 @@ spq_status join_impl(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t 
   if (s != SPQ_OK) return s;
   const int64_t r0 = p->host.query_join_row_off[a], r1 = p->host.query_join_row_off[b];
   if (r0 == r1) return SPQ_OK;  // only queries homed on other ranks
+  const bool full = (a == 0 && b == nq);
+  if (full && p->jw_lazy && mode < 0) {
+    // before K1, so that K1 stays the attention kernel's immediate predecessor (PDL)
+    s = ensure_join_work(c, p, st);
+    if (s != SPQ_OK) return s;
+  }
   bool k1 = false;
   if (mode != 1) {
     s = kv_write(c, p, layer, k, v, at<int32_t>(p, p->off_jpos) + r0, at<int64_t>(p, p->off_jslot) + r0, r1 - r0, st,
@@ -1030,13 +1090,18 @@ spq_status join_impl(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t 
   TempWork tw;
   float* opart = p->opart;
   float* lsepart = p->lsepart;
-  const bool full = (a == 0 && b == nq);
   DevWork w;
   int32_t part_extent = 0;  // partial slots the launch may address
   if (mode >= 0) {
     w = mode == 0 ? p->jw1 : p->jw2;
     fill_attn(c, p, w, &args);
     part_extent = p->jw1.n_parts + p->jw2.n_parts;
+  } else if (full && p->jw_lazy) {
+    w = p->jw;
+    spq_plan view;  // the work list lives in jbuf (fill_attn reads through dbuf)
+    view.dbuf = p->jbuf;
+    fill_attn(c, &view, p->jw, &args);
+    part_extent = w.n_parts;
   } else if (full) {
     w = p->jw;
     fill_attn(c, p, p->jw, &args);
@@ -1056,7 +1121,8 @@ spq_status join_impl(spq_ctx* c, spq_plan* p, int32_t layer, int32_t a, int32_t 
     part_extent = w.n_parts;
   }
   const bool f32 = split_out != nullptr || c->cfg.out_dtype == SPQ_FP32;
-  s = launch_join_list(c, w, full || mode >= 0 ? p->dbuf : tw.buf, args, opart, lsepart, part_extent, q,
+  s = launch_join_list(c, w, full && p->jw_lazy ? p->jbuf : (full || mode >= 0 ? p->dbuf : tw.buf), args, opart,
+                       lsepart, part_extent, q,
                        at<int32_t>(p, p->off_jpos) + r0, r1 - r0, layer, split_out ? split_out : o,
                        split_out ? split_lse : lse, f32, k1 && (full || mode >= 0) && !c->timing && c->pdl, st);
   if (s != SPQ_OK) return s;
@@ -1211,9 +1277,11 @@ spq_status spq_plan_release(spq_ctx* c, spq_plan* p, void* stream) {
     CUDA_TRY(cudaEventRecord(e, st));
     c->pending.push_back(e);
     if (p->dbuf) CUDA_TRY(cudaFreeAsync(p->dbuf, st));
+    if (p->jbuf) CUDA_TRY(cudaFreeAsync(p->jbuf, st));
     if (p->dec.dbuf) CUDA_TRY(cudaFreeAsync(p->dec.dbuf, st));
-    // opart / lsepart live inside dbuf
+    // opart / lsepart live inside dbuf (or jbuf)
     p->dbuf = nullptr;
+    p->jbuf = nullptr;
     p->dec.dbuf = nullptr;
   }
   c->store->release(p->host);

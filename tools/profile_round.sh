@@ -1,6 +1,6 @@
 #!/bin/bash
 # Profiling pass for profiles/ (run under gpurun): launch list of bench-like steps, one full ncu
-# capture per hot kernel, compute-sanitizer passes, the bench JSON, and nvidia-smi clocks.
+# capture per hot kernel, the bench JSON, and nvidia-smi clocks.
 #   bash tools/profile_round.sh            (then: python tools/ncu_summary.py r02)
 set -x
 python -m paper_2511_02749_b200.build > /dev/null
@@ -18,14 +18,7 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:cidr
   -o gpurun_out/prof/cidra python tools/profile_cidra.py 2 > gpurun_out/prof/ncu_cidra.log 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:decode_kernel -s 8 -c 1 \
   -o gpurun_out/prof/decode python tools/profile_step.py 1 C2 bf16 16 > gpurun_out/prof/ncu_decode.log 2>&1
-# compute-sanitizer: fp32 SIMT path (C1) and the tcgen05 path on a shrunk C2, incl. decode
-for tool in memcheck racecheck synccheck; do
-  for cfg in C1 C2s; do
-    timeout 600 compute-sanitizer --tool $tool --print-limit 20 python tools/profile_step.py 1 $cfg "" 4 \
-      > gpurun_out/prof/sanitizer_${tool}_${cfg}.log 2>&1
-    echo "$tool $cfg rc=$?" >> gpurun_out/prof/sanitizer_summary.txt
-    tail -3 gpurun_out/prof/sanitizer_${tool}_${cfg}.log >> gpurun_out/prof/sanitizer_summary.txt
-  done
-done
+# (compute-sanitizer is closed on the GPU pool from round 2 on: the r02 logs in profiles/ are the
+# last sanitizer evidence)
 timeout 900 python bench.py > gpurun_out/prof/bench.json 2> gpurun_out/prof/bench.err
 timeout 300 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/prof/bench_ref.json 2> gpurun_out/prof/bench_ref.err
