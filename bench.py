@@ -789,6 +789,8 @@ def run_partitioned(args, rank, world, dev, layers=None, split=False):
         ctx.evict_all()
         plan = ctx.plan(w.queries, stream=stream)
         v = plan.view() if world > 1 else None
+        if world > 1 and not split:  # replica need flags (R38): owners send only what homes lack
+            v = parallel.exchange_needs(plan, v, rank, world, device=dev)
         for layer in range(L):
             if len(ptok):
                 plan.prefill(layer, qp, kp, vp, op, lp, stream=stream)

@@ -151,10 +151,12 @@ typedef struct {
   int64_t join_kv_bytes;
   /* world_size > 1: queries homed here (q mod W == rank) and the fragment-KV
    * exchange lists. Peer w: send_blocks[send_off[w] .. send_off[w+1]) are this rank's blocks of
-   * the fragments it owns that w's joins read; recv_blocks[recv_off[w] .. recv_off[w+1]) are the
-   * plan-private blocks that receive the fragments owned by w. Fragments in first-occurrence
-   * (query, ⊕) order, each fragment's blocks in order — both sides derive the same lists. With
-   * world_size 1 all lists are empty. */
+   * the fragments it owns that w's joins read (all of them until spq_exchange_set_need narrows the
+   * list to the ones w flagged); recv_blocks[recv_off[w] .. recv_off[w+1]) are the blocks that
+   * receive the fragments owned by w which have no resident replica here. Received fragments are
+   * indexed under their digests (reading R38: digest-keyed replicas, later plans on this rank hit
+   * them). Fragments in first-occurrence (query, ⊕) order, each fragment's blocks in order — both
+   * sides derive the same candidate sequence. With world_size 1 all lists are empty. */
   int32_t n_join_queries;
   int32_t world_size;
   const int64_t *send_off;    /* [world_size+1] */
@@ -170,6 +172,14 @@ typedef struct {
   const int32_t *tasks;
   const int32_t *xq_off;      /* [world_size+1] */
   const int32_t *xq_queries;
+  /* Replica need flags (R38). Home side, per owner peer w: cand_recv_need[cand_recv_off[w] ..
+   * cand_recv_off[w+1]), one byte per remote fragment its joins read (first-occurrence order):
+   * 1 = its KV must be sent, 0 = a replica is resident here. Owner side: cand_send_off[w+1] -
+   * cand_send_off[w] = how many such fragments home peer w will flag. The home sends its flags to
+   * each owner (a byte all-to-all), which passes them to spq_exchange_set_need. */
+  const int64_t *cand_recv_off;  /* [world_size+1] */
+  const uint8_t *cand_recv_need;
+  const int64_t *cand_send_off;  /* [world_size+1] */
 } spq_plan_view;
 /* Read-only host arrays, valid until spq_plan_release. */
 spq_status spq_plan_view_get(const spq_plan *plan, spq_plan_view *out);
@@ -204,6 +214,14 @@ spq_status spq_exchange_pack(spq_ctx *ctx, spq_plan *plan, int32_t layer, int32_
                              void *stream);
 spq_status spq_exchange_unpack(spq_ctx *ctx, spq_plan *plan, int32_t layer, int32_t peer,
                                const void *buf, void *stream);
+/* Owner side of the replica protocol (R38): keep in the send list to home peer `peer` only the
+ * candidate fragments that peer flagged (need[i] != 0, host array of n = its candidate count,
+ * cand_send_off in the view). Call once per peer before the plan's first spq_exchange_pack; the
+ * view's send lists change (re-read the view). The device copy of the list is rewritten on
+ * `stream`. SPQ_EINVAL: n differs from the candidate count or need is NULL with n > 0;
+ * SPQ_ESTATE: released plan or bad peer. */
+spq_status spq_exchange_set_need(spq_ctx *ctx, spq_plan *plan, int32_t peer, const uint8_t *need,
+                                 int64_t n, void *stream);
 
 /* The same join of all of the plan's home queries in two launches, so that on W > 1 the
  * fragment-KV exchange overlaps the first: phase 0 = rope_kv_write of the cross

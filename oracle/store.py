@@ -79,6 +79,12 @@ class PlanView:
     # cross Q this rank sends to it and whose partial (O, LSE) comes back (query order)
     tasks: List[Tuple[int, int, int, int, int, int]] = field(default_factory=list)
     xq: Dict[int, List[int]] = field(default_factory=dict)
+    # digest-keyed replicas (R38): home side, per owner peer, one flag per remote fragment its joins
+    # read (first-occurrence order; 1 = its KV must be sent, 0 = a replica is resident); owner side,
+    # per home peer, the candidate fragments' block lists in the same order (`send` holds them all
+    # until `select_send` narrows it by the home's flags)
+    need: Dict[int, List[int]] = field(default_factory=dict)
+    send_candidates: Dict[int, List[List[int]]] = field(default_factory=dict)
 
 
 class Store:
@@ -141,7 +147,8 @@ class Store:
         """Plan a batch. With world > 1 this is rank `rank`'s share: query q is
         homed on q mod W (its prefix, join and cross run there), fragment f is owned by
         u64le(s_last[0:8]) mod W (it is prefilled and cached only there); a home rank receives
-        remote-owned fragments into plan-private blocks, in first-occurrence order.
+        remote-owned fragments, in first-occurrence order, into blocks indexed under their
+        digests (R38 replicas: a later plan here hits them and nothing moves).
 
         split=True (owner-side split join; §4.3, parallel
         sub-trees): no KV moves. An owner keeps each owned fragment's segment at its place in the
@@ -184,6 +191,20 @@ class Store:
                 pad_slots.extend(range(b * bs + ntok, b * bs + bs))
             return b
 
+        # R38: blocks whose KV this plan receives (digest-keyed replicas). An owned fragment of the
+        # same plan that shares one (common token prefix) recomputes and writes it: the exchange
+        # fills it only after the prefill and after the owner's own sends are packed
+        pending = set()
+
+        def insert_replica(dig, ntok) -> int:
+            b = self._alloc()
+            self.index[dig] = b
+            self.meta[b] = (dig, ntok, p)
+            self.stats["inserted_blocks"] += 1
+            pin(b)
+            pending.add(b)  # no pad slots: the owner's pages carry their zeroed pads
+            return b
+
         def new_private(ntok, pad=True) -> int:
             b = self._alloc()
             private.append(b)
@@ -196,6 +217,8 @@ class Store:
         recv: Dict[int, List[bytes]] = {}
         owned_blocks: Dict[bytes, List[int]] = {}
         recv_blocks: Dict[bytes, List[int]] = {}
+        recv_hit: Dict[bytes, bool] = {}
+        cand_recv: Dict[int, List[bytes]] = {}
 
         segs: List[Segment] = []
         joins: List[bytes] = []
@@ -220,7 +243,8 @@ class Store:
                     off += len(f)
                     if hashing.owner_rank(sf[-1], world) != rank:
                         continue
-                    seg = self._frag_segment(qi, fi, f, sf, delta if split else 0, touch, pin, insert_new)
+                    seg = self._frag_segment(qi, fi, f, sf, delta if split else 0, touch, pin, insert_new,
+                                             pending)
                     segs.append(seg)
                     owned_blocks.setdefault(sf[-1], seg.blocks)
                     if split:
@@ -273,7 +297,7 @@ class Store:
                 lasts.append(sf[-1])
                 owner = hashing.owner_rank(sf[-1], world)
                 if owner == rank:
-                    seg = self._frag_segment(qi, fi, f, sf, off, touch, pin, insert_new)
+                    seg = self._frag_segment(qi, fi, f, sf, off, touch, pin, insert_new, pending)
                     owned_blocks.setdefault(sf[-1], seg.blocks)
                 elif split:  # computed by its owner (a task there); this rank merges its partial
                     if qi not in xq.setdefault(owner, []):
@@ -281,14 +305,30 @@ class Store:
                     off += len(f)
                     continue
                 else:
-                    # remote-owned: received into plan-private blocks (owner's pages include
-                    # its zeroed pads), no prefill here
+                    # remote-owned (R38): all-or-nothing lookup of a replica kept from an earlier
+                    # exchange; a miss is received whole into its resident blocks (pinned first,
+                    # R24) and newly indexed ones; no prefill here
                     if sf[-1] not in recv_blocks:
-                        recv_blocks[sf[-1]] = [new_private(min(bs, len(f) - i * bs), pad=False)
-                                               for i in range(len(sf))]
-                        recv.setdefault(owner, []).append(sf[-1])
-                    seg = Segment(qi, KIND_FRAG, fi, len(f), off, recv_blocks[sf[-1]], sf, 0,
-                                  len(f), [False] * len(sf))
+                        self.stats["lookups"] += 1
+                        resident = [self.index.get(dig, -1) for dig in sf]
+                        for b in resident:
+                            if b >= 0:
+                                touch(b)
+                                pin(b)
+                        hit = all(b >= 0 for b in resident)
+                        if hit:
+                            self.stats["hit_blocks"] += len(sf)
+                            self.stats["hit_tokens"] += len(f)
+                        else:
+                            self.stats["miss_blocks"] += len(sf)
+                            resident = [b if b >= 0 else insert_replica(dig, min(bs, len(f) - i * bs))
+                                        for i, (b, dig) in enumerate(zip(resident, sf))]
+                            recv.setdefault(owner, []).append(sf[-1])
+                        recv_blocks[sf[-1]] = resident
+                        recv_hit[sf[-1]] = hit
+                        cand_recv.setdefault(owner, []).append(sf[-1])
+                    seg = Segment(qi, KIND_FRAG, fi, len(f), off, recv_blocks[sf[-1]], sf,
+                                  int(recv_hit[sf[-1]]), len(f), [False] * len(sf))
                 segs.append(seg)
                 off += len(f)
             j = hashing.join_fold(h_last, lasts)
@@ -337,18 +377,30 @@ class Store:
                 jg += [i] * len(a)
         send_b = {d: [b for dig in lst for b in owned_blocks[dig]] for d, lst in send.items()}
         recv_b = {o: [b for dig in lst for b in recv_blocks[dig]] for o, lst in recv.items()}
-        return PlanView(segs, joins, np.asarray(pp, np.int32), np.asarray(ps, np.int64),
+        view = PlanView(segs, joins, np.asarray(pp, np.int32), np.asarray(ps, np.int64),
                         np.asarray(pg, np.int32), np.asarray(jp, np.int32),
                         np.asarray(js, np.int64), np.asarray(jg, np.int32),
                         np.asarray(pad_slots, np.int64), jobs, dict(self.stats), pinned, private,
                         send_b, recv_b, n_home, sorted(tasks, key=lambda t: (t[1], t[0])), xq)
+        # R38 need flags (home side, per owner) and the owner's candidates (per home peer)
+        view.need = {o: [0 if recv_hit[d] else 1 for d in lst] for o, lst in cand_recv.items()}
+        view.send_candidates = {d: [list(owned_blocks[dig]) for dig in lst] for d, lst in send.items()}
+        return view
 
-    def _frag_segment(self, qi, fi, f, s, off, touch, pin, insert_new) -> Segment:
-        """All-or-nothing fragment lookup (R10, R11) with pin-before-alloc (R24)."""
+    @staticmethod
+    def select_send(view: PlanView, peer: int, need: Sequence[int]) -> None:
+        """Owner side of R38: the send list to `peer` keeps the candidates it flagged."""
+        cands = view.send_candidates.get(peer, [])
+        assert len(need) == len(cands), "one flag per candidate fragment"
+        view.send[peer] = [b for blocks, n in zip(cands, need) if n for b in blocks]
+
+    def _frag_segment(self, qi, fi, f, s, off, touch, pin, insert_new, pending=frozenset()) -> Segment:
+        """All-or-nothing fragment lookup (R10, R11) with pin-before-alloc (R24); a block this plan
+        only receives (R38 `pending`) counts as missing and is written by this fragment's prefill."""
         bs = self.bs
         self.stats["lookups"] += 1
         resident = [self.index.get(dig, -1) for dig in s]
-        if all(b >= 0 for b in resident):
+        if all(b >= 0 and b not in pending for b in resident):
             for b in resident:
                 touch(b)
                 pin(b)
@@ -366,7 +418,7 @@ class Store:
         for i, dig in enumerate(s):
             if resident[i] >= 0:
                 blocks.append(resident[i])
-                write.append(False)
+                write.append(resident[i] in pending)
             else:
                 blocks.append(insert_new(dig, min(bs, len(f) - i * bs)))
                 write.append(True)

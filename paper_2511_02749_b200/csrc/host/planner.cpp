@@ -3,6 +3,8 @@
 // and tests/test_planner_parity.py checks the two bit-for-bit.
 #include "planner.h"
 
+#include <unordered_set>
+
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -349,10 +351,21 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
       P.pad_slots.push_back(s);
     return b;
   };
-  auto new_private_nopad = [&]() -> int32_t {  // received pages carry the owner's zeroed pads
+  // a received block, indexed under its digest (R38 replica): no pad slots — the owner's pages
+  // carry their zeroed pads and blocks move whole
+  // blocks whose KV this plan receives: an owned fragment of the same plan that shares one (a common
+  // token prefix) must not count it as resident — it is filled only by the exchange, after the
+  // prefill and after the pack of the owner's own sends — so it recomputes and writes it
+  std::unordered_set<int32_t> pending;
+  auto insert_replica = [&](const Digest& d, int32_t ntok) -> int32_t {
     const int32_t b = alloc(&ok);
     if (!ok) return -1;
-    P.priv.push_back(b);
+    pending.insert(b);
+    P.replicas.push_back(b);
+    index_[d] = b;
+    meta_[b] = Meta{d, ntok, plan_no_, true};
+    journal_.push_back({kUndoInsert, b, Meta{}});
+    stats_.inserted_blocks++;
     pin(b);
     return b;
   };
@@ -370,7 +383,8 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
   std::vector<int32_t> blocks;
   std::vector<uint8_t> wr;
   std::unordered_map<Digest, std::vector<int32_t>, DigestHash> owned_blocks, recv_blocks;
-  std::vector<std::vector<Digest>> send_list(world), recv_list(world);
+  std::unordered_map<Digest, uint8_t, DigestHash> recv_hit;  // remote fragment: replica resident
+  std::vector<std::vector<Digest>> send_list(world), recv_list(world), cand_recv(world);
   std::vector<std::vector<int32_t>> xq(world);  // split mode: home queries per owner peer
   // all-or-nothing lookup of one locally owned fragment; pins resident blocks before allocating
   auto owned_fragment = [&](int32_t qi, int32_t fi, int32_t flen, int32_t off, const std::vector<Digest>& fd) {
@@ -379,7 +393,7 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
     bool all = true;
     for (size_t i = 0; i < fd.size(); ++i) {
       res[i] = lookup(fd[i]);
-      all = all && res[i] >= 0;
+      all = all && res[i] >= 0 && !pending.count(res[i]);
     }
     for (int32_t b : res)
       if (b >= 0) {
@@ -399,7 +413,7 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
       for (size_t i = 0; i < fd.size() && ok; ++i) {
         if (res[i] >= 0) {
           fb.push_back(res[i]);
-          fw.push_back(0);
+          fw.push_back(pending.count(res[i]) ? 1 : 0);
         } else {
           fb.push_back(insert_new(fd[i], std::min<int32_t>(bs, flen - static_cast<int32_t>(i) * bs)));
           fw.push_back(1);
@@ -488,16 +502,38 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
       } else if (split) {  // computed by its owner (a task there); this rank merges the partial
         if (xq[owner].empty() || xq[owner].back() != qi) xq[owner].push_back(qi);
       } else {
+        // remote-owned (R38): an all-or-nothing lookup of its replica; a miss is received whole
+        // into its resident blocks and newly indexed ones (pinned before any allocation, R24)
         auto it = recv_blocks.find(fd.back());
         if (it == recv_blocks.end()) {
-          std::vector<int32_t> rb;
-          for (size_t i = 0; i < fd.size() && ok; ++i) rb.push_back(new_private_nopad());
-          if (!ok) break;
-          it = recv_blocks.emplace(fd.back(), rb).first;
-          recv_list[owner].push_back(fd.back());
+          stats_.lookups++;
+          std::vector<int32_t> res(fd.size());
+          bool all = true;
+          for (size_t i = 0; i < fd.size(); ++i) {
+            res[i] = lookup(fd[i]);
+            all = all && res[i] >= 0;
+          }
+          for (int32_t b : res)
+            if (b >= 0) {
+              pin(b);
+              touch(b);
+            }
+          if (all) {
+            stats_.hit_blocks += static_cast<int64_t>(fd.size());
+            stats_.hit_tokens += flen;
+          } else {
+            stats_.miss_blocks += static_cast<int64_t>(fd.size());
+            for (size_t i = 0; i < fd.size() && ok; ++i)
+              if (res[i] < 0) res[i] = insert_replica(fd[i], std::min<int32_t>(bs, flen - static_cast<int32_t>(i) * bs));
+            if (!ok) break;
+            recv_list[owner].push_back(fd.back());
+          }
+          it = recv_blocks.emplace(fd.back(), res).first;
+          recv_hit[fd.back()] = all ? 1 : 0;
+          cand_recv[owner].push_back(fd.back());
         }
         wr.assign(fd.size(), 0);
-        add_seg(qi, kFrag, static_cast<int32_t>(fi), flen, off, 0, flen, it->second, wr, fd);
+        add_seg(qi, kFrag, static_cast<int32_t>(fi), flen, off, recv_hit[fd.back()], flen, it->second, wr, fd);
       }
       off += flen;
     }
@@ -593,15 +629,25 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
   if (prof)
     std::fprintf(stderr, "[spanq]   store.rows %8.1f us\n",
                  std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
-  // exchange lists: per peer, fragments in first-occurrence order, each fragment's blocks
+  // exchange lists: per peer, fragments in first-occurrence order, each fragment's blocks. The
+  // owner's send list starts as every candidate (select_send prunes it by the home's need flags)
   P.send_off.assign(1, 0);
   P.recv_off.assign(1, 0);
+  P.cand_send_off.assign(1, 0);
+  P.cand_send_blk.assign(1, 0);
+  P.cand_recv_off.assign(1, 0);
   for (int w = 0; w < world; ++w) {
     for (const Digest& d : send_list[w]) {
       const auto& b = owned_blocks.at(d);
       P.send_blocks.insert(P.send_blocks.end(), b.begin(), b.end());
+      P.cand_send_blocks.insert(P.cand_send_blocks.end(), b.begin(), b.end());
+      P.cand_send_blk.push_back(static_cast<int64_t>(P.cand_send_blocks.size()));
+      P.cand_send_need.push_back(1);
     }
     P.send_off.push_back(static_cast<int64_t>(P.send_blocks.size()));
+    P.cand_send_off.push_back(static_cast<int64_t>(P.cand_send_need.size()));
+    for (const Digest& d : cand_recv[w]) P.cand_recv_need.push_back(recv_hit.at(d) ? 0 : 1);
+    P.cand_recv_off.push_back(static_cast<int64_t>(P.cand_recv_need.size()));
     for (const Digest& d : recv_list[w]) {
       const auto& b = recv_blocks.at(d);
       P.recv_blocks.insert(P.recv_blocks.end(), b.begin(), b.end());
@@ -630,6 +676,24 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
   return 0;
 }
 
+bool select_send(PlanHost* p, int peer, const uint8_t* need, int64_t n) {
+  if (peer < 0 || peer + 1 >= static_cast<int>(p->cand_send_off.size())) return false;
+  const int64_t c0 = p->cand_send_off[peer], c1 = p->cand_send_off[peer + 1];
+  if (n != c1 - c0) return false;
+  for (int64_t i = 0; i < n; ++i) p->cand_send_need[c0 + i] = need[i] ? 1 : 0;
+  p->send_blocks.clear();
+  p->send_off.assign(1, 0);
+  const int world = static_cast<int>(p->cand_send_off.size()) - 1;
+  for (int w = 0; w < world; ++w) {
+    for (int64_t c = p->cand_send_off[w]; c < p->cand_send_off[w + 1]; ++c)
+      if (p->cand_send_need[c])
+        p->send_blocks.insert(p->send_blocks.end(), p->cand_send_blocks.begin() + p->cand_send_blk[c],
+                              p->cand_send_blocks.begin() + p->cand_send_blk[c + 1]);
+    p->send_off.push_back(static_cast<int64_t>(p->send_blocks.size()));
+  }
+  return true;
+}
+
 void Store::release(const PlanHost& p) {
   for (int32_t b : p.pinned) {
     pins_[b]--;
@@ -648,6 +712,8 @@ void Store::abort(const PlanHost& p) {
     auto it = index_.find(p.digests[i]);
     if (it != index_.end() && it->second == b && pins_[b] == 0) drop(b);
   }
+  for (int32_t b : p.replicas)  // indexed, but the exchange never delivered their KV
+    if (meta_[b].resident && pins_[b] == 0) drop(b);
 }
 
 int Store::extend_private(PlanHost* p, int64_t n, std::vector<int32_t>* out) {

@@ -73,7 +73,23 @@ struct PlanHost {
   std::vector<Task> tasks;
   std::vector<int32_t> xq_off;  // [world+1]
   std::vector<int32_t> xq_queries;
+  // digest-keyed replicas (reading R38). Home side: per owner peer, the remote fragments its joins
+  // read (first-occurrence order) and whether their KV must be sent — 0 when a replica kept from an
+  // earlier exchange is resident here (received fragments are indexed under their digests). Owner
+  // side: per home peer, the same candidate sequence with each fragment's block range; the home's
+  // need flags select which of them the send list carries (select_send; all until then).
+  std::vector<int64_t> cand_recv_off;  // [world+1]
+  std::vector<uint8_t> cand_recv_need;
+  std::vector<int64_t> cand_send_off;  // [world+1]
+  std::vector<int64_t> cand_send_blk;  // [n_cand+1] ranges into cand_send_blocks
+  std::vector<int32_t> cand_send_blocks;
+  std::vector<uint8_t> cand_send_need;
+  std::vector<int32_t> replicas;  // blocks indexed by this plan whose KV only the exchange delivers
 };
+
+// Owner side: keep in the send list to `peer` only the candidates the home flagged (need[i] != 0,
+// n = the peer's candidate count); rebuilds send_blocks / send_off. Returns false on a count mismatch.
+bool select_send(PlanHost* p, int peer, const uint8_t* need, int64_t n);
 
 // Fragment owner rank: u64le(s_last[0:8]) mod W.
 int owner_rank(const Digest& d, int world);

@@ -877,6 +877,9 @@ spq_status spq_plan_view_get(const spq_plan* p, spq_plan_view* v) {
   v->send_off = H.send_off.data();
   v->send_blocks = H.send_blocks.data();
   v->recv_off = H.recv_off.data();
+  v->cand_recv_off = H.cand_recv_off.data();
+  v->cand_recv_need = H.cand_recv_need.data();
+  v->cand_send_off = H.cand_send_off.data();
   v->recv_blocks = H.recv_blocks.data();
   v->n_tasks = static_cast<int32_t>(H.tasks.size());
   v->tasks = H.tasks.empty() ? nullptr : &H.tasks[0].query;
@@ -1254,6 +1257,23 @@ static spq_status exchange(spq_ctx* c, spq_plan* p, int32_t layer, int32_t peer,
   cudaError_t e = spq::launch_kv_exchange(x, st);
   if (e != cudaSuccess) return fail(SPQ_ECUDA, std::string("kv_exchange launch: ") + cudaGetErrorString(e));
   c->launches++;
+  return SPQ_OK;
+}
+
+spq_status spq_exchange_set_need(spq_ctx* c, spq_plan* p, int32_t peer, const uint8_t* need, int64_t n,
+                                 void* stream) {
+  if (c == nullptr || p == nullptr) return fail(SPQ_EINVAL, "null ctx/plan");
+  if (!c->live.count(p)) return fail(SPQ_ESTATE, "plan used after release (or not a plan of this ctx)");
+  spq::PlanHost& H = p->host;
+  if (peer < 0 || peer >= static_cast<int32_t>(H.cand_send_off.size()) - 1) return fail(SPQ_ESTATE, "peer out of range");
+  if (n > 0 && need == nullptr) return fail(SPQ_EINVAL, "null need flags");
+  if (!spq::select_send(&H, peer, need, n)) return fail(SPQ_EINVAL, "need flags: count differs from the candidates");
+  if (is_gpu(c) && !H.send_blocks.empty()) {
+    // the pruned list is a prefix-sized rewrite of the region the full candidate list was uploaded to
+    CUDA_TRY(cudaSetDevice(c->cfg.device));
+    CUDA_TRY(cudaMemcpyAsync(p->dbuf + p->off_send, H.send_blocks.data(), H.send_blocks.size() * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)));
+  }
   return SPQ_OK;
 }
 

@@ -8,12 +8,18 @@ in the same order, so one all-to-all per layer moves them:
 
     pack (K6 gather, per peer)  ->  dist.all_to_all_single (NCCL over NVLink)  ->  unpack (K6 scatter)
 
+Received fragments are indexed on the home rank under their digests (reading R38, digest-keyed
+replicas): a later plan there hits them, and once per plan `exchange_needs` tells each owner which
+candidate fragments still have to move (one byte each, a tiny all-to-all).
+
 Buffers are laid out [n_blocks][2 (K, V)][Hkv][bs][d] in the pool dtype. Everything here is
 argument marshalling around the C ABI (spq_exchange_pack / spq_exchange_unpack) and the collective.
 """
 from __future__ import annotations
 
 from typing import Callable, Dict, List, Optional
+
+import numpy as np
 
 
 def block_elems(shape) -> int:
@@ -32,6 +38,33 @@ def _a2a(recvbuf, sendbuf, out_splits: List[int], in_splits: List[int], group=No
     import torch.distributed as dist
 
     dist.all_to_all_single(recvbuf, sendbuf, out_splits, in_splits, group=group)
+
+
+def exchange_needs(plan, view: Dict, rank: int, world: int, device="cpu", group=None,
+                   transport: Optional[Callable] = None) -> Dict:
+    """Replica protocol (DESIGN reading R38), once per plan before its first exchange: every home
+    rank sends each owner one byte per candidate fragment (1 = send its KV, 0 = a replica is
+    resident here); each owner narrows its send lists accordingly. Returns the refreshed view."""
+    import torch
+
+    out_n = [len(view["need"].get(p, ())) for p in range(world)]  # flags this rank sends to owner p
+    in_n = list(view["n_cand_send"])                                # flags home p sends here
+    assert out_n[rank] == 0 and in_n[rank] == 0, "a rank never exchanges with itself"
+    sendbuf = torch.zeros(sum(out_n), dtype=torch.uint8, device=device)
+    off = 0
+    for p in range(world):
+        if out_n[p]:
+            sendbuf[off:off + out_n[p]] = torch.from_numpy(view["need"][p].astype(np.uint8)).to(device)
+        off += out_n[p]
+    recvbuf = torch.zeros(sum(in_n), dtype=torch.uint8, device=device)
+    (transport or (lambda r, s_, o, i: _a2a(r, s_, o, i, group)))(recvbuf, sendbuf, in_n, out_n)
+    flags = recvbuf.cpu().numpy()
+    off = 0
+    for p in range(world):
+        if in_n[p]:
+            plan.exchange_set_need(p, flags[off:off + in_n[p]])
+        off += in_n[p]
+    return plan.view()
 
 
 def exchange_layer(plan, view: Dict, layer: int, shape, device, dtype, rank: int, world: int,

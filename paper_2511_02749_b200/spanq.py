@@ -74,6 +74,7 @@ class spq_plan_view(C.Structure):
         ("n_join_queries", C.c_int32), ("world_size", C.c_int32),
         ("send_off", _I64P), ("send_blocks", _I32P), ("recv_off", _I64P), ("recv_blocks", _I32P),
         ("n_tasks", C.c_int32), ("tasks", _I32P), ("xq_off", _I32P), ("xq_queries", _I32P),
+        ("cand_recv_off", _I64P), ("cand_recv_need", _U8P), ("cand_send_off", _I64P),
     ]
 
 
@@ -107,6 +108,7 @@ SIGNATURES = {
                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "spq_join_phase": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "spq_exchange_set_need": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, _U8P, C.c_int64, C.c_void_p]),
     "spq_exchange_pack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
                                     C.c_void_p]),
     "spq_exchange_unpack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
@@ -267,7 +269,20 @@ class Plan:
         xo = _arr(v.xq_off, w + 1, np.int32) if v.xq_off else np.zeros(w + 1, np.int32)
         xqq = _arr(v.xq_queries, int(xo[-1]), np.int32)
         out["xq"] = {p: xqq[xo[p]:xo[p + 1]].tolist() for p in range(w) if xo[p + 1] > xo[p]}
+        # replica need flags (R38): per owner peer (home side) / candidate counts per home peer
+        co = _arr(v.cand_recv_off, w + 1, np.int64) if v.cand_recv_off else np.zeros(w + 1, np.int64)
+        cn = _arr(v.cand_recv_need, int(co[-1]), np.uint8)
+        out["need"] = {p: cn[co[p]:co[p + 1]] for p in range(w) if co[p + 1] > co[p]}
+        cs = _arr(v.cand_send_off, w + 1, np.int64) if v.cand_send_off else np.zeros(w + 1, np.int64)
+        out["n_cand_send"] = [int(cs[p + 1] - cs[p]) for p in range(w)]
         return out
+
+    def exchange_set_need(self, peer, need, stream=None):
+        """Owner side (R38): keep in the send list to `peer` only the fragments it flagged."""
+        flags = np.ascontiguousarray(np.asarray(need, dtype=np.uint8))
+        _check(lib().spq_exchange_set_need(self.ctx.handle, self.handle, int(peer),
+                                           flags.ctypes.data_as(_U8P), int(flags.size),
+                                           _stream_ptr(stream, self.ctx.device)))
 
     def exchange_pack(self, layer, peer, buf, stream=None):
         """Gather this plan's send blocks for `peer` (one layer) into buf [n, 2, Hkv, bs, d]."""

@@ -191,3 +191,84 @@ def test_split_join_parity(cuda_dev, dtype, world, out):
     for p, c in zip(plans, ctxs):
         p.release()
         c.close()
+
+
+@pytest.mark.parametrize("dtype,world", [("bf16", 2), ("bf16", 3), ("fp32", 2)])
+def test_replica_hits_across_batches(cuda_dev, dtype, world):
+    """Digest-keyed replicas (reading R38) on one GPU with W contexts standing in for ranks: batch 1
+    moves remote fragments to their home ranks, where they are indexed; batch 2 re-reads some of
+    them. After the need-flag round (home flags -> owners' spq_exchange_set_need) the owners send
+    only what has no replica, the received blocks equal the owners' bit for bit, the replica
+    blocks still hold batch 1's KV, and every join of batch 2 matches the fp64 oracle."""
+    import torch
+
+    fp32 = dtype == "fp32"
+    sh = inputs.Shape(hq=8, hkv=2, d=128 if not fp32 else 64, block_size=16, vocab=512, dtype=dtype)
+    qs = inputs.random_queries(405 + world, 16, vocab=512, max_frag=5, max_len=120, max_prefix=80,
+                               max_cross=100, reuse_p=0.6)
+    seed = 405
+    eq, ek, ev = inputs.layer_tables(sh, 0, seed)
+    tab = runner.device_tables(sh, 0, seed, cuda_dev)
+    ctxs = [spanq.Context(sh, 4096, device=0, max_position=1 << 14, out_dtype="fp32", rank=r, world_size=world)
+            for r in range(world)]
+    osts = [Store(4096, sh.hq, sh.hkv, sh.d, sh.block_size, sh.rope_base, sh.model_salt) for _ in range(world)]
+    be = parallel.block_elems(sh)
+    hits = 0
+    for batch in (qs[:8], qs[4:16]):
+        flat = [(q.prefix, q.fragments, q.cross) for q in batch]
+        plans = [c.plan(batch) for c in ctxs]
+        oviews = [osts[r].plan(flat, rank=r, world=world) for r in range(world)]
+        views = [p.view() for p in plans]
+        for r in range(world):  # prefill of what each rank computes
+            ptok = runner.prefill_tokens(views[r], batch)
+            if len(ptok):
+                q, k, v = runner.gather(tab, ptok, cuda_dev)
+                op = torch.empty((len(ptok), sh.hq, sh.d), dtype=torch.float32, device=cuda_dev)
+                plans[r].prefill(0, q, k, v, op)
+        # need flags: home h -> owner w
+        for w in range(world):
+            for h in range(world):
+                if h != w:
+                    flags = views[h]["need"].get(w, np.zeros(0, np.uint8))
+                    hits += int((flags == 0).sum())
+                    plans[w].exchange_set_need(h, flags)
+                    oviews[w].send[h] = [b for bl, n in zip(oviews[w].send_candidates.get(h, []), flags) if n
+                                         for b in bl]
+        views = [p.view() for p in plans]
+        for r in range(world):
+            for p in range(world):
+                np.testing.assert_array_equal(views[r]["send"].get(p, np.zeros(0, np.int32)), oviews[r].send.get(p, []))
+                np.testing.assert_array_equal(views[r]["recv"].get(p, np.zeros(0, np.int32)), oviews[r].recv.get(p, []))
+        for r in range(world):
+            for p in range(world):
+                sb = views[r]["send"].get(p, np.zeros(0, np.int32))
+                rb = views[p]["recv"].get(r, np.zeros(0, np.int32))
+                assert len(sb) == len(rb)
+                if not len(sb):
+                    continue
+                buf = torch.full((len(sb) * be,), float("nan"), dtype=ctxs[0].k_pool.dtype, device=cuda_dev)
+                plans[r].exchange_pack(0, p, buf)
+                plans[p].exchange_unpack(0, r, buf)
+                torch.cuda.synchronize()
+                for a, b in zip(sb.tolist(), rb.tolist()):
+                    assert torch.equal(ctxs[r].k_pool[0, a], ctxs[p].k_pool[0, b])
+                    assert torch.equal(ctxs[r].v_pool[0, a], ctxs[p].v_pool[0, b])
+        for r in range(world):
+            jtok = runner.join_tokens(views[r], batch)
+            if not len(jtok):
+                continue
+            q, k, v = runner.gather(tab, jtok, cuda_dev)
+            oj = torch.empty((len(jtok), sh.hq, sh.d), dtype=torch.float32, device=cuda_dev)
+            lj = torch.empty((len(jtok), sh.hq), dtype=torch.float32, device=cuda_dev)
+            plans[r].join(0, q, k, v, oj, lj)
+            torch.cuda.synchronize()
+            home = [i for i in range(len(batch)) if i % world == r]
+            exp = [oatt.join_rows(*flat[i], eq, ek, ev, sh.rope_base) for i in home]
+            check(oj, np.concatenate([e[0] for e in exp]), fp32, f"rank {r} join O")
+            check_lse(lj, np.concatenate([e[1] for e in exp]), fp32, f"rank {r} join LSE")
+        for r in range(world):
+            plans[r].release()
+            osts[r].release(oviews[r])
+    assert hits > 0, "batch 2 re-read no replica"
+    for c in ctxs:
+        c.close()

@@ -124,17 +124,26 @@ def test_exchange_lists_agree_and_cover_batch(world):
 
 # ---------------------------------------------------------------- exchange over a gloo group
 class _CpuPlan:
-    """pack/unpack of K6 emulated on CPU pools [nblk, 2, E] (E = block elems / 2)."""
+    """pack/unpack of K6 emulated on CPU pools [nblk, 2, E] (E = block elems / 2); the need-flag
+    step goes to the real (host-only) plan."""
 
-    def __init__(self, view, pool):
-        self.view, self.pool = view, pool
+    def __init__(self, plan, pool):
+        self.plan, self.pool = plan, pool
+        self.cur = plan.view()
+
+    def exchange_set_need(self, peer, need):
+        self.plan.exchange_set_need(peer, need)
+
+    def view(self):
+        self.cur = self.plan.view()
+        return self.cur
 
     def exchange_pack(self, layer, peer, buf, stream=None):
-        blocks = self.view["send"][peer]
+        blocks = self.cur["send"][peer]
         buf.view(len(blocks), -1).copy_(self.pool[blocks].reshape(len(blocks), -1))
 
     def exchange_unpack(self, layer, peer, buf, stream=None):
-        blocks = self.view["recv"][peer]
+        blocks = self.cur["recv"][peer]
         self.pool[blocks] = buf.view(len(blocks), *self.pool.shape[1:])
 
 
@@ -156,23 +165,37 @@ def _gloo_worker(rank, world, port, q):
         shape = inputs.Shape(hq=4, hkv=2, d=16, block_size=4, dtype="fp32")
         qs = inputs.random_queries(77, 24, vocab=16, max_len=20, reuse_p=0.5)
         ctx = spanq.Context(shape, 4096, device=-1, rank=rank, world_size=world)
-        view = ctx.plan(qs).view()
         be = parallel.block_elems(shape)
         pool = torch.zeros(4096, 2, be // 2)
-        dmap = seg_digest_map(view)
-        recv_blocks = {int(b) for bl in view["recv"].values() for b in bl}
-        # fill only the blocks this rank computes (owned fragments); received ones stay zero
-        _fill_from_digest(pool, {b: d for b, d in dmap.items() if b not in recv_blocks})
-        stats = parallel.exchange_layer(_CpuPlan(view, pool), view, 0, shape, "cpu", torch.float32,
-                                        rank, world)
-        ref = torch.zeros_like(pool)
-        _fill_from_digest(ref, {b: dmap[b] for b in recv_blocks})
-        for b in recv_blocks:
-            assert torch.equal(pool[b], ref[b]), f"rank {rank}: block {b} got the wrong fragment KV"
-        counts = [None] * world
-        dist.all_gather_object(counts, (stats["sent_bytes"], stats["recv_bytes"], len(recv_blocks)))
-        assert sum(c[0] for c in counts) == sum(c[1] for c in counts)
-        assert sum(c[2] for c in counts) > 0
+        hits = 0
+        # two batches: the second re-reads fragments the first received (R38 replicas: their
+        # blocks keep the first exchange's KV and need no transfer)
+        for batch in (qs[:12], qs[6:24]):
+            plan = _CpuPlan(ctx.plan(batch), pool)
+            view = parallel.exchange_needs(plan, plan.cur, rank, world)
+            hits += sum(int(x == 0) for v in view["need"].values() for x in v)
+            dmap = seg_digest_map(view)
+            recv_blocks = {int(b) for bl in view["recv"].values() for b in bl}
+            # fill only the blocks this rank computes (owned fragments written by this plan);
+            # received ones come from the exchange, replica hits from the previous batch
+            _fill_from_digest(pool, {int(b): dmap[int(b)] for b, w in zip(view["blocks"], view["block_write"])
+                                     if w and int(b) not in recv_blocks})
+            stats = parallel.exchange_layer(plan, view, 0, shape, "cpu", torch.float32, rank, world)
+            ref = torch.zeros_like(pool)
+            _fill_from_digest(ref, dmap)
+            for s in range(len(view["seg_kind"])):
+                if view["seg_kind"][s] != 1:
+                    continue
+                for b in view["blocks"][view["seg_block_off"][s]:][:view["seg_n_blocks"][s]]:
+                    assert torch.equal(pool[int(b)], ref[int(b)]), f"rank {rank}: block {b} holds the wrong fragment KV"
+            counts = [None] * world
+            dist.all_gather_object(counts, (stats["sent_bytes"], stats["recv_bytes"], len(recv_blocks)))
+            assert sum(c[0] for c in counts) == sum(c[1] for c in counts)
+            assert sum(c[2] for c in counts) > 0
+            plan.plan.release()
+        all_hits = [None] * world
+        dist.all_gather_object(all_hits, hits)
+        assert sum(all_hits) > 0, "no replica was re-read"
         dist.destroy_process_group()
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover - reported by the parent
@@ -329,3 +352,100 @@ def test_split_exchange_gloo_world2():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: "ok", 1: "ok"}, res
+
+
+# ---------------------------------------------------------------- digest-keyed replicas (R38)
+def _need_round(views, plans, world, ostores=None, oviews=None):
+    """The need-flag exchange among W host-only ranks: home h's flags for owner w go to w."""
+    for w in range(world):
+        for h in range(world):
+            if h == w:
+                continue
+            flags = views[h]["need"].get(w, np.zeros(0, np.uint8))
+            assert len(flags) == views[w]["n_cand_send"][h], (h, w)
+            plans[w].exchange_set_need(h, flags)
+            if oviews is not None:
+                Store.select_send(oviews[w], h, list(flags))
+    return [p.view() for p in plans]
+
+
+def _digest_lists(view, key, peer):
+    m = seg_digest_map(view)
+    return [m[int(b)] for b in view[key].get(peer, [])]
+
+
+@pytest.mark.parametrize("world,seed", [(2, 51), (3, 52), (4, 53)])
+def test_replicas_hit_in_later_plans_and_need_flags_prune_the_sends(world, seed):
+    """A fragment received once is indexed on the home rank under its digests: a later plan there
+    hits it (need flag 0, segment hit, nothing in the recv list), and once the owners apply the
+    homes' flags, what each owner sends is exactly what each home receives. C++ and the oracle
+    agree on every list, flag and stat along the way."""
+    shape = inputs.Shape(hq=4, hkv=2, d=64, block_size=4, dtype="fp32", model_salt=seed)
+    qs = inputs.random_queries(seed, 36, vocab=10, max_len=24, reuse_p=0.6)
+    ctxs = [spanq.Context(shape, 8192, device=-1, rank=r, world_size=world) for r in range(world)]
+    ost = [Store(8192, 4, 2, 64, 4, shape.rope_base, seed) for _ in range(world)]
+    replica_hits = 0
+    for i in range(0, len(qs), 6):
+        batch = qs[i:i + 6]
+        plans = [c.plan(batch) for c in ctxs]
+        oviews = [ost[r].plan([flat(q) for q in batch], rank=r, world=world) for r in range(world)]
+        views = [p.view() for p in plans]
+        for r in range(world):
+            assert_same(views[r], oviews[r])
+            assert {p: list(v) for p, v in views[r]["need"].items()} == {p: v for p, v in oviews[r].need.items() if v}
+            assert views[r]["n_cand_send"] == [len(oviews[r].send_candidates.get(p, [])) for p in range(world)]
+            for key in STAT_KEYS:
+                assert ctxs[r].stats()[key] == ost[r].stats[key], key
+            replica_hits += sum(int(x == 0) for v in views[r]["need"].values() for x in v)
+            # a need-0 fragment's segment is a hit and none of its blocks is received
+            recv = {int(b) for bl in views[r]["recv"].values() for b in bl}
+            for s in range(len(views[r]["seg_kind"])):
+                if views[r]["seg_kind"][s] == 1 and views[r]["seg_hit"][s] == 1:
+                    blk = views[r]["blocks"][views[r]["seg_block_off"][s]:][:views[r]["seg_n_blocks"][s]]
+                    last = bytes(views[r]["digests"][views[r]["seg_block_off"][s] + views[r]["seg_n_blocks"][s] - 1])
+                    if hashing.owner_rank(last, world) != r:
+                        assert not recv.intersection(int(b) for b in blk)
+        views = _need_round(views, plans, world, ost, oviews)
+        for r in range(world):
+            for p in range(world):
+                np.testing.assert_array_equal(views[r]["send"].get(p, np.zeros(0, np.int32)),
+                                              oviews[r].send.get(p, []))
+                assert _digest_lists(views[r], "send", p) == _digest_lists(views[p], "recv", r), (r, p)
+        for r in range(world):
+            plans[r].release()
+            ost[r].release(oviews[r])
+    assert replica_hits > 0, "the batch sequence never re-read a received fragment"
+    for c in ctxs:
+        c.close()
+
+
+def test_owned_fragment_sharing_a_received_block_writes_it():
+    """R38 hazard: a remote fragment B received by this plan and a locally owned fragment A that
+    shares B's first block (a common token prefix). The block's KV arrives only with the exchange
+    (after the prefill and after this rank packs its own sends), so A must not treat it as cached:
+    A is a miss and its prefill writes that block. Checked on C++ and the oracle."""
+    shape = inputs.Shape(hq=4, hkv=2, d=64, block_size=4, dtype="fp32", model_salt=5)
+    root = Store(1, 4, 2, 64, 4, shape.rope_base, 5).root
+    head = np.array([1, 2, 3, 4], np.int32)  # one full shared block
+    g = np.random.default_rng(0)
+    a = b = None
+    while a is None or b is None:
+        f = np.concatenate([head, g.integers(0, 50, 5).astype(np.int32)])
+        own = hashing.owner_rank(hashing.fragment_chain(f, 4, root)[-1], 2)
+        if own == 0 and a is None:
+            a = f
+        elif own == 1 and b is None:
+            b = f
+    q = inputs.SpanQuery(np.zeros(0, np.int32), [b, a], np.array([7, 8], np.int32))
+    ctx = spanq.Context(shape, 256, device=-1, rank=0, world_size=2)
+    v = ctx.plan([q]).view()
+    ov = Store(256, 4, 2, 64, 4, shape.rope_base, 5).plan([flat(q)], rank=0, world=2)
+    assert_same(v, ov)
+    segs = [s for s in range(len(v["seg_kind"])) if v["seg_kind"][s] == 1]
+    sb, sa = segs  # B (received), A (owned)
+    blk_b0 = int(v["blocks"][v["seg_block_off"][sb]])
+    blk_a0 = int(v["blocks"][v["seg_block_off"][sa]])
+    assert blk_a0 == blk_b0  # one block, indexed once
+    assert v["seg_hit"][sa] == 0 and v["block_write"][v["seg_block_off"][sa]] == 1
+    assert blk_b0 in v["recv"][1].tolist()
+    ctx.close()
