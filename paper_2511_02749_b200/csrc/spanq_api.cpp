@@ -101,6 +101,12 @@ struct spq_ctx {
   uint8_t* staging = nullptr;
   size_t staging_size = 0;
   cudaEvent_t staging_ev = nullptr;
+  // a second one for the lazily built join work lists (W = 1 plans, ensure_join_work): with one
+  // buffer a join's upload would wait for its own plan's upload and the next plan for that join's,
+  // so the host could no longer run a whole query ahead of the GPU
+  uint8_t* jstaging = nullptr;
+  size_t jstaging_size = 0;
+  cudaEvent_t jstaging_ev = nullptr;
   // options (spq_set_option)
   int exp2_mode = -1;              // SPQ_OPT_EXP2 (kernel poly_mask; -1 = auto: prefill 0, joins 1)
   float rescale_threshold = 8.0f;  // SPQ_OPT_RESCALE_THRESHOLD (log2 units)
@@ -501,6 +507,7 @@ spq_status spq_create(const spq_config* cfg, spq_ctx** out) {
     }
     for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
     CUDA_TRY(cudaEventCreateWithFlags(&c->staging_ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->jstaging_ev, cudaEventDisableTiming));
   }
   *out = c.release();
   return SPQ_OK;
@@ -516,6 +523,8 @@ void spq_destroy(spq_ctx* c) {
       if (e) cudaEventDestroy(e);
     if (c->staging_ev) cudaEventDestroy(c->staging_ev);
     if (c->staging) cudaFreeHost(c->staging);
+    if (c->jstaging_ev) cudaEventDestroy(c->jstaging_ev);
+    if (c->jstaging) cudaFreeHost(c->jstaging);
     if (c->rope) cudaFree(c->rope);
   }
   for (spq_plan* p : c->live) {  // plans never released: their device arrays go with the ctx
@@ -1015,8 +1024,8 @@ spq_status launch_join_list(spq_ctx* c, const DevWork& w, uint8_t* buf, spq::Att
 }
 
 // The join's work list of a lazy (W = 1) plan, built and uploaded at its first full join: the
-// packed arrays then the split-KV partials in one device buffer, copied from the ctx's pinned
-// staging buffer (reused once the plan upload that last used it has completed)
+// packed arrays then the split-KV partials in one device buffer, copied from the ctx's second
+// pinned staging buffer (reused once the previous join-work upload has completed)
 spq_status ensure_join_work(spq_ctx* c, spq_plan* p, cudaStream_t st) {
   if (p->jbuf != nullptr) return SPQ_OK;
   spq::build_join_work(p->host, work_opts(c, c->cfg.dtype == SPQ_BF16), 0, p->host.n_queries, &p->jw_host);
@@ -1046,16 +1055,16 @@ spq_status ensure_join_work(spq_ctx* c, spq_plan* p, cudaStream_t st) {
     off_lsepart = align_up(off_opart + rows * c->cfg.head_dim * sizeof(float), 1024);
     bytes = off_lsepart + rows * sizeof(float);
   }
-  CUDA_TRY(cudaEventSynchronize(c->staging_ev));
-  if (c->staging_size < pk.size) {
-    if (c->staging) CUDA_TRY(cudaFreeHost(c->staging));
-    c->staging_size = std::max(pk.size, static_cast<size_t>(1) << 20);
-    CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&c->staging), c->staging_size));
+  CUDA_TRY(cudaEventSynchronize(c->jstaging_ev));  // the previous join-work upload has read it
+  if (c->jstaging_size < pk.size) {
+    if (c->jstaging) CUDA_TRY(cudaFreeHost(c->jstaging));
+    c->jstaging_size = std::max(pk.size, static_cast<size_t>(1) << 20);
+    CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&c->jstaging), c->jstaging_size));
   }
-  pk.write(c->staging);
+  pk.write(c->jstaging);
   CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->jbuf), bytes, st));
-  CUDA_TRY(cudaMemcpyAsync(p->jbuf, c->staging, pk.size, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaEventRecord(c->staging_ev, st));
+  CUDA_TRY(cudaMemcpyAsync(p->jbuf, c->jstaging, pk.size, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaEventRecord(c->jstaging_ev, st));
   if (w.n_parts > 0) {
     p->opart = reinterpret_cast<float*>(p->jbuf + off_opart);
     p->lsepart = reinterpret_cast<float*>(p->jbuf + off_lsepart);
