@@ -376,6 +376,7 @@ def main():
             judge = measure_judge(dev, stream, flush, args)
 
     peak_burst, peak_sust, hbm, peak_src = peaks()
+    peak_sust = peak_sust or peak_burst
     # ---- CIDRA: in-place repositioning of the C2 query's blocks, all layers
     with torch.cuda.stream(stream):
         reposition = measure_reposition(ctx, s, stream, flush, len(view["blocks"]), hbm)
@@ -395,14 +396,20 @@ def main():
         "plan_host_ms": statistics.median(plan_host_ms),
         "step_ms_p50": statistics.median(step_ms), "step_ms_p99": float(np.percentile(step_ms, 99)),
         "flops_per_step": flops, "flops_per_layer": flops_layer,
+        # the kernel is timed inside the 40-layer step, which runs at the 1000 W power cap
+        # (tools/clock_under_load.py: SM clock ~1770 MHz median): per the measurement contract the
+        # sustained peak is its denominator; the burst fraction is reported beside it
         "roofline": {"kernel": "span_attn_tc (fragment+prefix prefill, K2)", "bound": "tensor",
-                     "achieved": achieved, "peak": peak_burst, "unit": "TFLOP/s",
-                     "frac": achieved / peak_burst, "traffic": ncu_traffic("span_attn_tc prefill"),
-                     "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)" if peak_src == "measured" else "fallback",
+                     "achieved": achieved, "peak": peak_sust, "unit": "TFLOP/s",
+                     "frac": achieved / peak_sust, "traffic": ncu_traffic("span_attn_tc prefill"),
+                     "peak_source": (f"{peak_src} bf16 sustained (MEASURED_PEAKS.json; kernel timed inside the "
+                                     f"40-layer step)") if peak_src == "measured" else "fallback",
+                     "peak_burst": peak_burst, "frac_burst": achieved / peak_burst,
                      "kernel_ms": pre_ms, "algorithmic_flops": view["prefill_flops"]},
         "join_kernel": {"kernel": "span_attn_tc (join, K3)", "ms": join_ms,
                         "achieved": view["join_flops"] / (join_ms / 1e3) / 1e12 if join_ms > 0 else None,
-                        "frac": (view["join_flops"] / (join_ms / 1e3) / 1e12) / peak_burst if join_ms > 0 else None},
+                        "frac": (view["join_flops"] / (join_ms / 1e3) / 1e12) / peak_sust if join_ms > 0 else None,
+                        "frac_burst": (view["join_flops"] / (join_ms / 1e3) / 1e12) / peak_burst if join_ms > 0 else None},
         f"out_{other}": {"note": f"the same C2 kernels writing {other} O (separate 2-layer steps)",
                          "prefill_kernel_ms": opre,
                          "prefill_frac": view["prefill_flops"] / (opre / 1e3) / 1e12 / peak_burst,
@@ -956,7 +963,8 @@ def measure_c5(dev, stream, args):
         run(4, False)  # warm-up (4 queries)
         ttft, flops = run(len(w.queries), True)
     st = ctx.stats()
-    peak_burst, _, _, _ = peaks()
+    peak_burst, peak_sust, _, _ = peaks()
+    peak_sust = peak_sust or peak_burst
     makespan = ttft[-1]
     n_inc = sum(len(q.fragments) for q in w.queries)
     counts = {}
@@ -972,7 +980,8 @@ def measure_c5(dev, stream, args):
                         "from a shared pool of 512, one GPU, L = 1, queries served in arrival order",
             "queries": len(w.queries), "unique_fragments": len(counts), "overlap_realized": overlap,
             "makespan_ms": makespan, "flops": flops, "tflops": flops / (makespan / 1e3) / 1e12,
-            "frac_of_peak": flops / (makespan / 1e3) / 1e12 / peak_burst,
+            "frac_of_peak": flops / (makespan / 1e3) / 1e12 / peak_sust,  # a 0.6 s run: sustained
+            "frac_of_burst_peak": flops / (makespan / 1e3) / 1e12 / peak_burst,
             "ttft_ms_p50": float(np.percentile(ttft, 50)), "ttft_ms_p99": float(np.percentile(ttft, 99)),
             "service_ms_p50": float(np.percentile(np.diff([0.0] + ttft), 50)),
             "service_ms_p99": float(np.percentile(np.diff([0.0] + ttft), 99)),
