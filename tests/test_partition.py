@@ -449,3 +449,30 @@ def test_owned_fragment_sharing_a_received_block_writes_it():
     assert v["seg_hit"][sa] == 0 and v["block_write"][v["seg_block_off"][sa]] == 1
     assert blk_b0 in v["recv"][1].tolist()
     ctx.close()
+
+
+def test_exchange_set_need_rejects_bad_input():
+    """spq_exchange_set_need (R38): the flag count must equal the peer's candidate count, the
+    peer must exist, and a released plan is refused."""
+    shape = inputs.Shape(hq=4, hkv=2, d=64, block_size=4, dtype="fp32")
+    qs = inputs.random_queries(61, 12, vocab=10, max_len=20, reuse_p=0.5)
+    ctx = spanq.Context(shape, 4096, device=-1, rank=1, world_size=2)
+    plan = ctx.plan(qs)
+    v = plan.view()
+    n = v["n_cand_send"][0]
+    assert n > 0
+    with pytest.raises(spanq.SpanqError) as e:
+        plan.exchange_set_need(0, np.ones(n + 1, np.uint8))
+    assert e.value.status == spanq.EINVAL
+    with pytest.raises(spanq.SpanqError) as e:
+        plan.exchange_set_need(2, np.ones(n, np.uint8))
+    assert e.value.status == spanq.ESTATE
+    plan.exchange_set_need(0, np.zeros(n, np.uint8))  # nothing to send to rank 0
+    assert 0 not in plan.view()["send"]
+    plan.exchange_set_need(0, np.ones(n, np.uint8))  # flags can be re-applied: all again
+    np.testing.assert_array_equal(plan.view()["send"][0], v["send"][0])
+    plan.release()
+    with pytest.raises(spanq.SpanqError) as e:
+        plan.exchange_set_need(0, np.ones(n, np.uint8))
+    assert e.value.status == spanq.ESTATE
+    ctx.close()
