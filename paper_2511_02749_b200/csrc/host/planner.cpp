@@ -169,6 +169,7 @@ Store::Store(int64_t num_blocks, int block_size, const Digest& root)
   pins_.assign(num_blocks, 0);
   pinned_mark_.assign(num_blocks, 0);
   free_.init(num_blocks);
+  index_.init(num_blocks);
 }
 
 int64_t Store::pinned_count() const {
@@ -178,8 +179,7 @@ int64_t Store::pinned_count() const {
 }
 
 int32_t Store::lookup(const Digest& d) const {
-  auto it = index_.find(d);
-  return it == index_.end() ? -1 : it->second;
+  return index_.find(d);
 }
 
 void Store::set_evictable(int32_t b, bool on) {
@@ -231,7 +231,7 @@ void Store::rollback() {
         break;
       case kUndoEvict:
         meta_[b] = it->meta;
-        index_[meta_[b].dig] = b;
+        index_.set(meta_[b].dig, b);
         if (pins_[b] == 0) set_evictable(b, true);
         break;
       case kUndoInsert:
@@ -333,7 +333,7 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
   auto insert_new = [&](const Digest& d, int32_t ntok) -> int32_t {
     const int32_t b = alloc(&ok);
     if (!ok) return -1;
-    index_[d] = b;
+    index_.set(d, b);
     meta_[b] = Meta{d, ntok, plan_no_, true};
     journal_.push_back({kUndoInsert, b, Meta{}});
     stats_.inserted_blocks++;
@@ -362,7 +362,7 @@ int Store::plan(const std::vector<FlatQuery>& qs, PlanHost* out, ThreadPool* poo
     if (!ok) return -1;
     pending.insert(b);
     P.replicas.push_back(b);
-    index_[d] = b;
+    index_.set(d, b);
     meta_[b] = Meta{d, ntok, plan_no_, true};
     journal_.push_back({kUndoInsert, b, Meta{}});
     stats_.inserted_blocks++;
@@ -709,8 +709,7 @@ void Store::abort(const PlanHost& p) {
   for (size_t i = 0; i < p.blocks.size(); ++i) {
     const int32_t b = p.blocks[i];
     if (!p.block_write[i] || priv[b] || !meta_[b].resident) continue;
-    auto it = index_.find(p.digests[i]);
-    if (it != index_.end() && it->second == b && pins_[b] == 0) drop(b);
+    if (index_.find(p.digests[i]) == b && pins_[b] == 0) drop(b);
   }
   for (int32_t b : p.replicas)  // indexed, but the exchange never delivered their KV
     if (meta_[b].resident && pins_[b] == 0) drop(b);
@@ -745,13 +744,12 @@ int64_t Store::commit(PlanHost* p, const int32_t* blocks, const Digest* dig, con
   int64_t done = 0;
   for (int64_t i = 0; i < n; ++i) {
     const int32_t b = blocks[i];
-    auto it = index_.find(dig[i]);
-    if (it != index_.end()) continue;  // resident already (here or in an equal-content block)
+    if (index_.find(dig[i]) >= 0) continue;  // resident already (here or in an equal-content block)
     if (meta_[b].resident) {           // re-key (e.g. a full cross block under its X digest)
       if (pins_[b] == 0) set_evictable(b, false);
       index_.erase(meta_[b].dig);
     }
-    index_[dig[i]] = b;
+    index_.set(dig[i], b);
     meta_[b] = Meta{dig[i], ntok[i], plan_no_, true};
     auto pv = std::find(p->priv.begin(), p->priv.end(), b);
     if (pv != p->priv.end()) p->priv.erase(pv);
@@ -775,8 +773,8 @@ void Store::drop(int32_t b) {
 
 void Store::evict_all() {
   std::vector<int32_t> victims;
-  for (const auto& kv : index_)
-    if (pins_[kv.second] == 0) victims.push_back(kv.second);
+  for (int32_t b = 0; b < static_cast<int32_t>(nblocks_); ++b)
+    if (meta_[b].resident && pins_[b] == 0) victims.push_back(b);
   for (int32_t b : victims) {
     set_evictable(b, false);
     index_.erase(meta_[b].dig);
@@ -798,7 +796,7 @@ int Store::insert(const Digest* d, const int32_t* ntok, int64_t n, int32_t* ids)
     }
     const int32_t b = alloc(&ok);
     if (!ok) break;
-    index_[d[i]] = b;
+    index_.set(d[i], b);
     meta_[b] = Meta{d[i], ntok[i], plan_no_, true};
     journal_.push_back({kUndoInsert, b, Meta{}});
     set_evictable(b, true);

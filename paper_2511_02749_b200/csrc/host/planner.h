@@ -134,6 +134,64 @@ class FreeSet {
   int64_t count_ = 0, hint_ = 0;
 };
 
+// Digest -> block id, open addressing with linear probing and backward-shift deletion (no
+// tombstones) over a power-of-two table of >= 2x the pool's blocks: no allocation per insert
+// (std::unordered_map allocated a node for every block a plan inserted)
+class DigestIndex {
+ public:
+  void init(int64_t max_entries) {
+    size_t cap = 16;
+    while (cap < static_cast<size_t>(2 * max_entries)) cap <<= 1;
+    keys_.assign(cap, Digest{});
+    vals_.assign(cap, -1);
+    mask_ = cap - 1;
+    n_ = 0;
+  }
+  int32_t find(const Digest& d) const {
+    for (size_t i = slot(d);; i = (i + 1) & mask_) {
+      if (vals_[i] < 0) return -1;
+      if (keys_[i] == d) return vals_[i];
+    }
+  }
+  void set(const Digest& d, int32_t v) {  // insert or overwrite
+    size_t i = slot(d);
+    for (; vals_[i] >= 0; i = (i + 1) & mask_)
+      if (keys_[i] == d) {
+        vals_[i] = v;
+        return;
+      }
+    keys_[i] = d;
+    vals_[i] = v;
+    ++n_;
+  }
+  void erase(const Digest& d) {
+    size_t i = slot(d);
+    for (;; i = (i + 1) & mask_) {
+      if (vals_[i] < 0) return;
+      if (keys_[i] == d) break;
+    }
+    // backward shift: pull later entries of the probe run into the hole when their home slot
+    // does not lie (cyclically) after the hole
+    for (size_t j = (i + 1) & mask_; vals_[j] >= 0; j = (j + 1) & mask_) {
+      const size_t k = slot(keys_[j]);
+      if (((j - k) & mask_) >= ((j - i) & mask_)) {
+        keys_[i] = keys_[j];
+        vals_[i] = vals_[j];
+        i = j;
+      }
+    }
+    vals_[i] = -1;
+    --n_;
+  }
+  size_t size() const { return n_; }
+
+ private:
+  size_t slot(const Digest& d) const { return DigestHash()(d) & mask_; }
+  std::vector<Digest> keys_;
+  std::vector<int32_t> vals_;
+  size_t mask_ = 0, n_ = 0;
+};
+
 class Store {
  public:
   Store(int64_t num_blocks, int block_size, const Digest& root);
@@ -196,7 +254,7 @@ class Store {
   int64_t nblocks_;
   int bs_;
   Digest root_;
-  std::unordered_map<Digest, int32_t, DigestHash> index_;
+  DigestIndex index_;
   std::vector<Meta> meta_;
   std::vector<int32_t> pins_;
   FreeSet free_;
