@@ -193,13 +193,16 @@ def test_split_join_parity(cuda_dev, dtype, world, out):
         c.close()
 
 
-@pytest.mark.parametrize("dtype,world", [("bf16", 2), ("bf16", 3), ("fp32", 2)])
-def test_replica_hits_across_batches(cuda_dev, dtype, world):
+@pytest.mark.parametrize("dtype,world,phased", [("bf16", 2, False), ("bf16", 3, False), ("fp32", 2, False),
+                                                ("bf16", 2, True), ("bf16", 3, True)])
+def test_replica_hits_across_batches(cuda_dev, dtype, world, phased):
     """Digest-keyed replicas (reading R38) on one GPU with W contexts standing in for ranks: batch 1
     moves remote fragments to their home ranks, where they are indexed; batch 2 re-reads some of
     them. After the need-flag round (home flags -> owners' spq_exchange_set_need) the owners send
     only what has no replica, the received blocks equal the owners' bit for bit, the replica
-    blocks still hold batch 1's KV, and every join of batch 2 matches the fp64 oracle."""
+    blocks still hold batch 1's KV, and every join of batch 2 matches the fp64 oracle. phased: the
+    join runs in two phases around the exchange, phase 0 with the blocks being received poisoned
+    (NaN) — replica hits belong to phase 0 and must not read a poisoned block."""
     import torch
 
     fp32 = dtype == "fp32"
@@ -239,6 +242,26 @@ def test_replica_hits_across_batches(cuda_dev, dtype, world):
             for p in range(world):
                 np.testing.assert_array_equal(views[r]["send"].get(p, np.zeros(0, np.int32)), oviews[r].send.get(p, []))
                 np.testing.assert_array_equal(views[r]["recv"].get(p, np.zeros(0, np.int32)), oviews[r].recv.get(p, []))
+        joins = {}
+        for r in range(world):
+            jtok = runner.join_tokens(views[r], batch)
+            if not len(jtok):
+                continue
+            q, k, v = runner.gather(tab, jtok, cuda_dev)
+            oj = torch.empty((len(jtok), sh.hq, sh.d), dtype=torch.float32, device=cuda_dev)
+            lj = torch.empty((len(jtok), sh.hq), dtype=torch.float32, device=cuda_dev)
+            joins[r] = (q, k, v, oj, lj)
+            if phased:
+                rid = [views[r]["recv"].get(p, np.zeros(0, np.int32)) for p in range(world)]
+                rid = torch.from_numpy(np.concatenate(rid).astype(np.int64)).to(cuda_dev)
+                saved = (ctxs[r].k_pool[0, rid].clone(), ctxs[r].v_pool[0, rid].clone()) if len(rid) else None
+                if len(rid):
+                    ctxs[r].k_pool[0, rid] = float("nan")
+                    ctxs[r].v_pool[0, rid] = float("nan")
+                plans[r].join_phase(0, 0, q, k, v, oj, lj)
+                torch.cuda.synchronize()
+                if saved is not None:  # blocks shared with an owned fragment keep their own KV
+                    ctxs[r].k_pool[0, rid], ctxs[r].v_pool[0, rid] = saved
         for r in range(world):
             for p in range(world):
                 sb = views[r]["send"].get(p, np.zeros(0, np.int32))
@@ -254,13 +277,13 @@ def test_replica_hits_across_batches(cuda_dev, dtype, world):
                     assert torch.equal(ctxs[r].k_pool[0, a], ctxs[p].k_pool[0, b])
                     assert torch.equal(ctxs[r].v_pool[0, a], ctxs[p].v_pool[0, b])
         for r in range(world):
-            jtok = runner.join_tokens(views[r], batch)
-            if not len(jtok):
+            if r not in joins:
                 continue
-            q, k, v = runner.gather(tab, jtok, cuda_dev)
-            oj = torch.empty((len(jtok), sh.hq, sh.d), dtype=torch.float32, device=cuda_dev)
-            lj = torch.empty((len(jtok), sh.hq), dtype=torch.float32, device=cuda_dev)
-            plans[r].join(0, q, k, v, oj, lj)
+            q, k, v, oj, lj = joins[r]
+            if phased:
+                plans[r].join_phase(0, 1, q, k, v, oj, lj)
+            else:
+                plans[r].join(0, q, k, v, oj, lj)
             torch.cuda.synchronize()
             home = [i for i in range(len(batch)) if i % world == r]
             exp = [oatt.join_rows(*flat[i], eq, ek, ev, sh.rope_base) for i in home]
