@@ -501,3 +501,26 @@ def test_many_tiny_epochs_stress(cuda_dev, hq, hkv, d, out_dtype):
         qs = inputs.random_queries(300 + rep, 12, vocab=128, max_frag=6, max_len=20, max_prefix=24,
                                    max_cross=40, reuse_p=0.3)
         run_and_check(inputs.Workload("tiny", sh, qs, 300 + rep), cuda_dev, nblk=2048, out_dtype=out_dtype)
+
+
+@pytest.mark.parametrize("seed", list(range(32)))
+def test_random_workloads_fuzz(cuda_dev, seed):
+    """Seeded random shapes and batches against the fp64 oracle: GQA group 1-8 (paired and unpaired
+    launches), d 64 / 128, block size 16-128, bf16 (fp32 or bf16 O) or fp32, multi-query batches with
+    repeated and permuted fragments, nested ⊕, empty prefixes, ragged lengths, and a warm-up batch on
+    the same store so part of the second batch hits the cache. Slot maps bit-exact, outputs and LSE
+    within the stated tolerances, K/V pages within their rounding bound."""
+    g = np.random.default_rng(9000 + seed)
+    hkv = int(g.choice([1, 2, 4]))
+    group = int(g.choice([1, 2, 4, 8]))
+    dtype = "fp32" if seed % 4 == 3 else "bf16"
+    d = int(g.choice([64, 128])) if dtype == "bf16" else 64
+    bs = int(g.choice([16, 32, 64, 128]))
+    sh = inputs.Shape(hq=hkv * group, hkv=hkv, d=d, block_size=bs, vocab=512, dtype=dtype, model_salt=seed)
+    qs = inputs.random_queries(9100 + seed, int(g.integers(2, 6)), vocab=512, max_frag=5,
+                               max_len=int(g.integers(20, 260)), max_prefix=int(g.integers(0, 200)),
+                               max_cross=int(g.integers(1, 200)), reuse_p=0.4)
+    warm, batch = qs[: len(qs) // 2], qs[len(qs) // 2:]
+    w = inputs.Workload(f"fuzz{seed}", sh, batch, 9200 + seed, warmup_queries=warm)
+    out = "fp32" if dtype == "fp32" or seed % 2 == 0 else "bf16"
+    run_and_check(w, cuda_dev, nblk=8192, out_dtype=out)
