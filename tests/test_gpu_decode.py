@@ -132,3 +132,23 @@ def test_plus_distribution_commit_equals_recompute(cuda_dev):
         assert torch.equal(ka, kb) and torch.equal(va, vb)
     ctx.close()
     fresh.close()
+
+
+@pytest.mark.parametrize("seed", list(range(12)))
+def test_decode_random_fuzz(cuda_dev, seed):
+    """Seeded random shapes (GQA group 1-8, d 64 / 128, block size 16-128, bf16 / fp32) and
+    multi-query batches; a few decode steps per query, each row against the oracle's decode_row."""
+    g = np.random.default_rng(7000 + seed)
+    hkv = int(g.choice([1, 2, 4]))
+    group = int(g.choice([1, 2, 4, 8]))
+    dtype = "fp32" if seed % 4 == 3 else "bf16"
+    d = int(g.choice([64, 128])) if dtype == "bf16" else 64
+    bs = int(g.choice([16, 32, 64, 128]))
+    sh = inputs.Shape(hq=hkv * group, hkv=hkv, d=d, block_size=bs, vocab=512, dtype=dtype, model_salt=seed)
+    qs = inputs.random_queries(7100 + seed, int(g.integers(1, 4)), vocab=512, max_frag=4,
+                               max_len=int(g.integers(20, 200)), max_prefix=int(g.integers(0, 120)),
+                               max_cross=int(g.integers(1, 150)), reuse_p=0.4)
+    out = "fp32" if dtype == "fp32" or seed % 2 == 0 else "bf16"
+    ctx, *_ = run_decode(inputs.Workload(f"dfuzz{seed}", sh, qs, 7200 + seed), cuda_dev, int(g.integers(1, 6)),
+                         out_dtype=out, nblk=4096)
+    ctx.close()
