@@ -71,7 +71,7 @@ def launches(path: str):
 
 def short(name: str) -> str:
     for k in ("span_attn_tc", "span_attn_f32", "rope_kv_write", "combine_kernel", "kv_exchange", "cidra_kernel",
-              "decode_kernel", "gather_rows", "merge_split"):
+              "decode_bf16_kernel", "decode_kernel", "gather_rows", "merge_split"):
         if k in name:
             return k
     return name.split("(")[0][-60:]

@@ -16,7 +16,7 @@ timeout 300 ncu --set full --clock-control none -k regex:combine -s 1 -c 1 \
   -o gpurun_out/prof/combine python tools/profile_step.py 2 > gpurun_out/prof/ncu_comb.log 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:cidra -s 1 -c 1 \
   -o gpurun_out/prof/cidra python tools/profile_cidra.py 2 > gpurun_out/prof/ncu_cidra.log 2>&1
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:decode_kernel -s 8 -c 1 \
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:decode -s 8 -c 1 \
   -o gpurun_out/prof/decode python tools/profile_step.py 1 C2 bf16 16 > gpurun_out/prof/ncu_decode.log 2>&1
 # (compute-sanitizer is closed on the GPU pool from round 2 on: the r02 logs in profiles/ are the
 # last sanitizer evidence)
