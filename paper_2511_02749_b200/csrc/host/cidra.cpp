@@ -2,7 +2,6 @@
 #include "cidra.h"
 
 #include <algorithm>
-#include <unordered_map>
 
 namespace spq {
 
@@ -10,38 +9,38 @@ bool cidra_schedule(const int32_t* src, const int32_t* dst, const int32_t* delta
                     CidraSchedule* out, std::string* err) {
   *out = CidraSchedule();
   out->comp_off.push_back(0);
-  // node ids: every block a move touches
-  std::unordered_map<int32_t, int32_t> id;
-  std::vector<int32_t> block;
-  auto node = [&](int32_t b) {
-    auto it = id.find(b);
-    if (it != id.end()) return it->second;
-    const int32_t k = static_cast<int32_t>(block.size());
-    id.emplace(b, k);
-    block.push_back(b);
-    return k;
-  };
-  std::vector<int32_t> in_move;              // node -> the move writing it, or -1
-  std::vector<std::vector<int32_t>> out_mv;  // node -> moves reading it
-  for (int64_t i = 0; i < n; ++i) {
+  for (int64_t i = 0; i < n; ++i)
     if (src[i] < 0 || src[i] >= num_blocks || dst[i] < 0 || dst[i] >= num_blocks) {
       *err = "block id out of range";
       return false;
     }
-    const int32_t s = node(src[i]), d = node(dst[i]);
-    if (static_cast<size_t>(std::max(s, d)) >= in_move.size()) {
-      in_move.resize(block.size(), -1);
-      out_mv.resize(block.size());
-    }
-    if (in_move[d] >= 0) {
+  // node ids: every block a move touches, compacted by sorting (no per-node allocation)
+  std::vector<int32_t> block(src, src + n);
+  block.insert(block.end(), dst, dst + n);
+  std::sort(block.begin(), block.end());
+  block.erase(std::unique(block.begin(), block.end()), block.end());
+  auto node = [&](int32_t b) {
+    return static_cast<int32_t>(std::lower_bound(block.begin(), block.end(), b) - block.begin());
+  };
+  const int32_t nn = static_cast<int32_t>(block.size());
+  std::vector<int32_t> s_id(n), d_id(n);
+  std::vector<int32_t> in_move(nn, -1);  // node -> the move writing it, or -1
+  std::vector<int32_t> out_off(nn + 1, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    s_id[i] = node(src[i]);
+    d_id[i] = node(dst[i]);
+    if (in_move[d_id[i]] >= 0) {
       *err = "block " + std::to_string(dst[i]) + " is the destination of two moves";
       return false;
     }
-    in_move[d] = static_cast<int32_t>(i);
-    out_mv[s].push_back(static_cast<int32_t>(i));
+    in_move[d_id[i]] = static_cast<int32_t>(i);
+    out_off[s_id[i] + 1]++;
   }
-  for (const auto& m : out_mv) out->duplicates += std::max<int64_t>(0, static_cast<int64_t>(m.size()) - 1);
-  const int32_t nn = static_cast<int32_t>(block.size());
+  // node -> moves reading it (CSR, in move order)
+  for (int32_t v = 0; v < nn; ++v) out_off[v + 1] += out_off[v];
+  std::vector<int32_t> out_mv(n), fill(out_off.begin(), out_off.end() - 1);
+  for (int64_t i = 0; i < n; ++i) out_mv[fill[s_id[i]]++] = static_cast<int32_t>(i);
+  for (int32_t v = 0; v < nn; ++v) out->duplicates += std::max<int32_t>(0, out_off[v + 1] - out_off[v] - 1);
   std::vector<int32_t> done(nn, 0), stamp(nn, -1);
   std::vector<int32_t> level;  // BFS frontier of nodes
   std::vector<int32_t> tree;   // BFS-ordered moves of the current component
@@ -51,14 +50,14 @@ bool cidra_schedule(const int32_t* src, const int32_t* dst, const int32_t* delta
     int32_t v = start;
     while (in_move[v] >= 0 && stamp[v] != start) {
       stamp[v] = start;
-      v = id[src[in_move[v]]];
+      v = s_id[in_move[v]];
     }
     std::vector<int32_t> cyc;  // W[0..k): W[j+1] = source of W[j]
     if (in_move[v] >= 0) {
       int32_t u = v;
       do {
         cyc.push_back(u);
-        u = id[src[in_move[u]]];
+        u = s_id[in_move[u]];
       } while (u != v);
     }
     // BFS over the moves leaving the core (root, or the cycle nodes), skipping cycle edges
@@ -73,8 +72,9 @@ bool cidra_schedule(const int32_t* src, const int32_t* dst, const int32_t* delta
     while (!level.empty()) {
       std::vector<int32_t> next;
       for (int32_t u : level)
-        for (int32_t m : out_mv[u]) {
-          const int32_t w = id[dst[m]];
+        for (int32_t e = out_off[u]; e < out_off[u + 1]; ++e) {
+          const int32_t m = out_mv[e];
+          const int32_t w = d_id[m];
           if (done[w]) continue;  // a cycle edge (its destination is a core node)
           done[w] = 1;
           tree.push_back(m);

@@ -1641,10 +1641,12 @@ spq_status cidra_run(spq_ctx* c, const spq::CidraSchedule& sch, int32_t layer_be
   if (s != SPQ_OK) return s;
   // one stream-ordered device buffer: ops then component offsets (pageable H2D: staged before return)
   const size_t ob = sch.ops.size() * sizeof(spq::CidraOp), cb = sch.comp_off.size() * sizeof(int32_t);
+  std::vector<uint8_t> host(ob + cb);  // one copy instead of two
+  std::memcpy(host.data(), sch.ops.data(), ob);
+  std::memcpy(host.data() + ob, sch.comp_off.data(), cb);
   void* buf = nullptr;
   CUDA_TRY(cudaMallocAsync(&buf, ob + cb, st));
-  CUDA_TRY(cudaMemcpyAsync(buf, sch.ops.data(), ob, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(buf) + ob, sch.comp_off.data(), cb, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(buf, host.data(), ob + cb, cudaMemcpyHostToDevice, st));
   spq::CidraArgs a{};
   a.ops = static_cast<const int4*>(buf);
   a.comp_off = reinterpret_cast<const int32_t*>(static_cast<uint8_t*>(buf) + ob);
