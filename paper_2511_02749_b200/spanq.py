@@ -210,8 +210,41 @@ class _QueryBuf:
                            self.tokens.ctypes.data_as(_I32P), len(self.tokens))
 
 
+class _FlatQueryBuf(_QueryBuf):
+    """The common ⋈[prefix?, ⊕[f…]?, cross] tree encoded straight into the ABI layout (the same
+    nodes as inputs.query_to_tree builds for a non-nested query, without its intermediate arrays)."""
+
+    def __init__(self, q):  # noqa: super().__init__ not called: the arrays are built here
+        parts = ([q.prefix] if len(q.prefix) else []) + list(q.fragments) + [q.cross]
+        lens = np.fromiter((len(p) for p in parts), dtype=np.int64, count=len(parts))
+        offs = np.zeros(len(parts), np.int64)
+        np.cumsum(lens[:-1], out=offs[1:])
+        nf = len(q.fragments)
+        n_top = (1 if len(q.prefix) else 0) + (1 if nf else 0) + 1
+        nodes = np.zeros((1 + len(parts) + (1 if nf else 0), 3), np.int64)
+        nodes[0, 0] = _inputs.OP_CROSS | (n_top << 32)
+        r, k = 1, 0
+        if len(q.prefix):
+            nodes[r] = (_inputs.OP_TOKENS, offs[0], lens[0])
+            r, k = r + 1, 1
+        if nf:
+            nodes[r, 0] = _inputs.OP_PLUS | (nf << 32)
+            r += 1
+            nodes[r:r + nf, 0] = _inputs.OP_TOKENS
+            nodes[r:r + nf, 1] = offs[k:k + nf]
+            nodes[r:r + nf, 2] = lens[k:k + nf]
+            r, k = r + nf, k + nf
+        nodes[r] = (_inputs.OP_TOKENS, offs[k], lens[k])
+        self.nodes = nodes
+        self.tokens = np.ascontiguousarray(np.concatenate(parts), dtype=np.int32)
+        self.q = spq_query(self.nodes.ctypes.data_as(C.POINTER(spq_node)), len(nodes),
+                           self.tokens.ctypes.data_as(_I32P), len(self.tokens))
+
+
 def to_query(q) -> _QueryBuf:
     if isinstance(q, _inputs.SpanQuery):
+        if not q.nest or len(q.fragments) < 3:
+            return _FlatQueryBuf(q)
         return _QueryBuf(*_inputs.query_to_tree(q))
     nodes, toks = q
     return _QueryBuf(nodes, toks)

@@ -318,3 +318,20 @@ def test_decode_reserve_and_commit_errors():
     with pytest.raises(spanq.SpanqError) as e:  # more than reserved
         ctx.plan([inputs.SpanQuery(np.zeros(0, np.int32), [], q.cross)]).commit_span(0, [1] * 9)
     assert e.value.status == spanq.ESTATE
+
+
+def test_flat_query_encoding_equals_the_generic_tree():
+    """spanq._FlatQueryBuf (the binding's fast path for ⋈[prefix?, ⊕[…]?, cross]) encodes exactly
+    the nodes and tokens inputs.query_to_tree + _QueryBuf produce."""
+    n_checked = 0
+    for seed in range(40):
+        for q in inputs.random_queries(seed, 6, vocab=50, max_len=20):
+            if q.nest and len(q.fragments) >= 3:
+                continue
+            a = spanq._FlatQueryBuf(q)
+            b = spanq._QueryBuf(*inputs.query_to_tree(q))
+            assert a.q.num_nodes == b.q.num_nodes
+            np.testing.assert_array_equal(a.nodes, b.nodes[: len(a.nodes)])
+            np.testing.assert_array_equal(a.tokens, b.tokens)
+            n_checked += 1
+    assert n_checked > 100
