@@ -267,44 +267,77 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const DecodeArgs a) {
 }
 
 // ---------------------------------------------------------------- bf16 pools: warp-split decode
-// The bf16 path is HBM-bound by K and V (2·d·2 bytes per key and kv head) with little arithmetic
-// per byte, so the CTA's chunk is split over its 4 warps instead of walking it in CTA-wide steps
-// with barriers: warp w takes the chunk's 16-key groups w, w+4, ... and runs its own pipeline —
-// cp.async double-buffered K / V group in its smem region (K rows XOR-swizzled by 16-byte unit),
-// its own counter-rotated q (fp32), its own online softmax — with no CTA barrier until the four
-// (m, l, O) partials are merged at the end. Per group: lane = (key, half of d) for the scores
-// (packed FFMA2 over bf16 pairs widened to fp32, halves summed by one shuffle), shuffle max / sum
-// per head over the 16 keys, lane = 4 (d = 128) or 2 (d = 64) columns of every head for P·V.
+// The bf16 path is HBM-bound by K and V (2·d·2 bytes per key and kv head), so what limits it is
+// how many bytes each SM keeps in flight, and that is set by how long a warp spends on each group
+// of keys between its loads. The CTA's chunk is split over its 4 warps: warp w takes the chunk's
+// 16-key groups w, w+4, ... and runs its own pipeline — cp.async double-buffered K / V group in
+// its smem region (rows XOR-swizzled by 16-byte unit), its own online softmax — with no CTA
+// barrier until the four (m, l, O) partials are merged at the end. Per group the two products are
+// warp-level tensor-core MMAs (mma.sync m16n8k16, bf16 in, fp32 accumulate) with the q heads as
+// the N = 8 side: S^T[16 keys x 8 heads] = K · Q^T (K by ldmatrix, the counter-rotated Q^T held
+// in registers per segment, rounded to bf16 like the join's tcgen05 operand), then
+// O^T[d x 8 heads] += V^T · P^T (V^T by ldmatrix.trans, P^T bf16 through 256 bytes of smem).
+// That is ~150 instructions per group where per-lane FMA dot products took ~1200, so a warp gets
+// back to its next load ~8x sooner. Heads >= G are zero padding of the N side.
 constexpr int kGrp = 16;   // keys per warp step
 constexpr int kWarps = 4;
+constexpr int kPadHeads = 8;  // MMA N
 
 template <int D, int G>
 struct DecSmem {
   static constexpr int kUnits = D / 8;                        // 16-byte units per bf16 row
   static constexpr int kStage = 2 * kGrp * D;                 // bf16 elements: K then V of a group
   __nv_bfloat16 kv[kWarps][2][kStage];                        // per warp, double-buffered
-  float q[kWarps][G * D];                                     // per warp: rotated q (fp32)
-  float p[kWarps][G * kGrp];                                  // per warp: P of the current group
+  __nv_bfloat16 pt[kWarps][kPadHeads * kGrp];                 // per warp: P^T [head][key] (bf16)
   float ml[kWarps][2 * G];                                    // merge: m, l per warp and head
 };
+
+__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
+}
+// D[16x8] += A[16x16] · B[16x8]: bf16 operands, fp32 accumulators (thread fragments as in PTX ISA
+// "mma.m16n8k16": g = lane / 4, t = lane % 4; A rows g / g+8, cols 2t+{0,1} / +8; B rows
+// (k) 2t+{0,1} / +8, col g; C rows g / g+8, cols 2t+{0,1})
+__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+               "{%0, %1, %2, %3};"
+               : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
 
 template <typename TO, int D, int G>
 __global__ void __launch_bounds__(kThreads) decode_bf16_kernel(const DecodeArgs a) {
   using T = __nv_bfloat16;
   using Sm = DecSmem<D, G>;
   constexpr int U = Sm::kUnits;
-  constexpr int CPL = D / 32;  // P·V columns per lane
+  constexpr int KS = D / 16;  // k-steps of the score MMA = m-tiles of the P·V MMA
   extern __shared__ __align__(16) uint8_t smem_raw[];
   Sm& S = *reinterpret_cast<Sm*>(smem_raw);
   const DecodeItem it = a.items[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;  // MMA fragment coordinates
   const int pos = a.pos_base[it.row] + a.step;
   const int h0 = it.kvh * G;
   const T* qg = static_cast<const T*>(a.q) + (static_cast<int64_t>(it.row) * a.hq + h0) * D;
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));
   const int64_t layer_rows = static_cast<int64_t>(a.layer) * a.nblk * a.hkv * a.bs;
-  float* qs = S.q[w];
-  float* ps = S.p[w];
+  __nv_bfloat16* pt = S.pt[w];
   // this warp's groups: the chunk's groups in (tile, group) order, every kWarps-th one
   struct Grp {
     int t, g, nk;  // tile, group in the tile, valid keys
@@ -322,37 +355,44 @@ __global__ void __launch_bounds__(kThreads) decode_bf16_kernel(const DecodeArgs 
         it_g = 0;
         continue;
       }
-      const int g = it_g++;
+      const int gg = it_g++;
       if ((gidx++ % kWarps) != w) continue;
-      out = Grp{it_t, g, min(kGrp, nv - g * kGrp)};
+      out = Grp{it_t, gg, min(kGrp, nv - gg * kGrp)};
       return true;
     }
     return false;
   };
   auto issue = [&](const Grp& gr, int buf) {  // cp.async of the group's K and V rows
-    const KvTile tl = a.tiles[gr.t];
+    // bf16 pools have bs >= 16 (a power of two), so a 16-key group lies in one block and its
+    // K (and V) rows of this kv head are one contiguous run: one block-table read per group,
+    // then lane i copies 16-byte unit i of the run. Rows past the valid keys are zero-filled
+    // (P is 0 there, and 0 · V must not meet stale bits that decode as NaN).
+    const int kk0 = gr.g * kGrp;
+    const int32_t blk = a.tile_blocks[a.tiles[gr.t].blk_off + kk0 / a.bs];
+    const int64_t row0 = layer_rows + (static_cast<int64_t>(blk) * a.hkv + it.kvh) * a.bs + (kk0 & (a.bs - 1));
+    const T* ks = static_cast<const T*>(a.k_pool) + row0 * D;
+    const T* vs = static_cast<const T*>(a.v_pool) + row0 * D;
     __nv_bfloat16* Kb = S.kv[w][buf];
     __nv_bfloat16* Vb = Kb + kGrp * D;
-    for (int i = lane; i < gr.nk * U; i += 32) {
+    const int n = gr.nk * U;
+#pragma unroll
+    for (int j = 0; j < kGrp * U / 32; ++j) {
+      const int i = lane + 32 * j;
       const int key = i / U, u = i % U;
-      const int kk = gr.g * kGrp + key;
-      const int32_t blk = a.tile_blocks[tl.blk_off + kk / a.bs];
-      const int64_t row = layer_rows + (static_cast<int64_t>(blk) * a.hkv + it.kvh) * a.bs + kk % a.bs;
-      cp_async16(Kb + key * D + ((u ^ (key & (U - 1))) * 8), static_cast<const T*>(a.k_pool) + row * D + u * 8);
-      cp_async16(Vb + key * D + u * 8, static_cast<const T*>(a.v_pool) + row * D + u * 8);
+      const int so = (key * U + (u ^ (key & (U - 1)))) * 8;
+      const bool ok = i < n;
+      cp_async16_zfill(Kb + so, ks + (ok ? i * 8 : 0), ok);
+      cp_async16_zfill(Vb + so, vs + (ok ? i * 8 : 0), ok);
     }
     cp_async_commit();
   };
-  float m[G], l[G];
-  float2 acc[G][CPL / 2];
+  float m2[2] = {-INFINITY, -INFINITY}, l2[2] = {0.f, 0.f};  // heads 2t, 2t+1
+  float oc[KS][4];  // O^T: d = mt*16 + g (+8), heads 2t, 2t+1
 #pragma unroll
-  for (int h = 0; h < G; ++h) {
-    m[h] = -INFINITY;
-    l[h] = 0.f;
+  for (int mt = 0; mt < KS; ++mt)
 #pragma unroll
-    for (int e = 0; e < CPL / 2; ++e) acc[h][e] = make_float2(0.f, 0.f);
-  }
-  const int key = lane & (kGrp - 1), half = lane >> 4;
+    for (int e = 0; e < 4; ++e) oc[mt][e] = 0.f;
+  uint32_t qf[KS][2];  // Q^T B fragments: head g, d = ks*16 + 2t + {0,1} (and + 8)
   int cur_rot = INT32_MIN;
   Grp cur, nxt;
   bool have = next_mine(cur);
@@ -366,92 +406,84 @@ __global__ void __launch_bounds__(kThreads) decode_bf16_kernel(const DecodeArgs 
       cp_async_wait<0>();
     }
     const int rot = a.tiles[cur.t].rot_delta;
-    if (rot != cur_rot) {  // a new segment: q rotated to pos - Δ (rotate-half pairs), fp32
+    if (rot != cur_rot) {  // a new segment: q rotated to pos - Δ (rotate-half pairs), fp32 -> bf16
       cur_rot = rot;
       const int rp = min(max(pos - rot, 0), a.max_pos - 1);
-      for (int i = lane; i < G * (D / 2); i += 32) {
-        const int h = i / (D / 2), c = i % (D / 2);
-        const float x = __bfloat162float(qg[h * D + c]), y = __bfloat162float(qg[h * D + c + D / 2]);
-        const float2 cs = a.rope[static_cast<int64_t>(rp) * (D / 2) + c];
-        qs[h * D + c] = x * cs.x - y * cs.y;
-        qs[h * D + c + D / 2] = y * cs.x + x * cs.y;
-      }
+      const float2* cs = a.rope + static_cast<int64_t>(rp) * (D / 2);
+#pragma unroll
+      for (int ks = 0; ks < KS / 2; ++ks)
+#pragma unroll
+        for (int hi = 0; hi < 2; ++hi) {
+          const int c = ks * 16 + hi * 8 + 2 * t;  // c, c + 1 < D / 2; partners c + D / 2 in k-step ks + KS / 2
+          if (g < G) {
+            const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(qg + g * D + c));
+            const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(qg + g * D + c + D / 2));
+            const float2 c0 = cs[c], c1 = cs[c + 1];
+            qf[ks][hi] = pack_bf16x2(x.x * c0.x - y.x * c0.y, x.y * c1.x - y.y * c1.y);
+            qf[ks + KS / 2][hi] = pack_bf16x2(y.x * c0.x + x.x * c0.y, y.y * c1.x + x.y * c1.y);
+          } else {
+            qf[ks][hi] = 0u;
+            qf[ks + KS / 2][hi] = 0u;
+          }
+        }
     }
-    __syncwarp();  // every lane's cp.async of this group and the rotated q are visible
+    __syncwarp();  // every lane's cp.async of this group is visible
     const __nv_bfloat16* Kb = S.kv[w][buf];
     const __nv_bfloat16* Vb = Kb + kGrp * D;
-    // scores: lane = (key, half of d); packed fp32x2 products, halves summed by a shuffle
-    float sc[G];
+    const int mi = lane >> 3, r8 = lane & 7;  // ldmatrix: this lane's matrix and row
+    // S^T = K · Q^T: sc = S[key g][heads 2t, 2t+1], S[key g+8][heads 2t, 2t+1]
+    float sc[4] = {0.f, 0.f, 0.f, 0.f};
     {
-      float2 s2[G];
+      const int key = r8 + (mi & 1) * 8;
 #pragma unroll
-      for (int h = 0; h < G; ++h) s2[h] = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int uu = 0; uu < U / 2; ++uu) {
-        const int u = half * (U / 2) + uu;
-        const uint4 kv = *reinterpret_cast<const uint4*>(Kb + key * D + ((u ^ (key & (U - 1))) * 8));
-        const uint32_t wv[4] = {kv.x, kv.y, kv.z, kv.w};
-        float2 kf[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) kf[e] = make_float2(__uint_as_float(wv[e] << 16), __uint_as_float(wv[e] & 0xFFFF0000u));
-#pragma unroll
-        for (int h = 0; h < G; ++h) {
-          const float4 qa = *reinterpret_cast<const float4*>(qs + h * D + u * 8);
-          const float4 qb = *reinterpret_cast<const float4*>(qs + h * D + u * 8 + 4);
-          s2[h] = ffma2(kf[0], make_float2(qa.x, qa.y), s2[h]);
-          s2[h] = ffma2(kf[1], make_float2(qa.z, qa.w), s2[h]);
-          s2[h] = ffma2(kf[2], make_float2(qb.x, qb.y), s2[h]);
-          s2[h] = ffma2(kf[3], make_float2(qb.z, qb.w), s2[h]);
-        }
-      }
-#pragma unroll
-      for (int h = 0; h < G; ++h) {
-        float v = s2[h].x + s2[h].y;
-        v += __shfl_xor_sync(0xffffffffu, v, 16);
-        sc[h] = key < cur.nk ? v * scale_log2 : -INFINITY;
+      for (int ks = 0; ks < KS; ++ks) {
+        uint32_t af[4];
+        ldsm_x4(af, Kb + (key * U + ((ks * 2 + (mi >> 1)) ^ (key & (U - 1)))) * 8);
+        mma_bf16(sc, af, qf[ks][0], qf[ks][1]);
       }
     }
-    // online softmax per head over the group's 16 keys (both half-warps hold the same values)
-    float alpha[G];
+    // online softmax per head over the group's 16 keys: a head's 16 scores sit in the 8 lanes
+    // of equal t (2 rows each)
+    float alpha[2];
 #pragma unroll
-    for (int h = 0; h < G; ++h) {
-      float mx = sc[h];
+    for (int j = 0; j < 2; ++j) {
+      const float s0 = g < cur.nk ? sc[j] * scale_log2 : -INFINITY;
+      const float s1 = g + 8 < cur.nk ? sc[j + 2] * scale_log2 : -INFINITY;
+      float mx = fmaxf(s0, s1);
 #pragma unroll
-      for (int o = kGrp / 2; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      const float m_new = fmaxf(m[h], mx);
-      const float pv = key < cur.nk ? exp2f(sc[h] - m_new) : 0.f;
-      float sum = pv;
+      for (int o = 4; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const float m_new = fmaxf(m2[j], mx);
+      const float p0 = exp2f(s0 - m_new), p1 = exp2f(s1 - m_new);
+      float sum = p0 + p1;
 #pragma unroll
-      for (int o = kGrp / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      alpha[h] = m[h] == -INFINITY ? 0.f : exp2f(m[h] - m_new);
-      l[h] = l[h] * alpha[h] + sum;
-      m[h] = m_new;
-      if (half == 0) ps[h * kGrp + key] = pv;
+      for (int o = 4; o < 32; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      alpha[j] = m2[j] == -INFINITY ? 0.f : exp2f(m2[j] - m_new);
+      l2[j] = l2[j] * alpha[j] + sum;
+      m2[j] = m_new;
+      pt[(2 * t + j) * kGrp + g] = __float2bfloat16_rn(p0);
+      pt[(2 * t + j) * kGrp + g + 8] = __float2bfloat16_rn(p1);
     }
-    __syncwarp();
-    // O = O * alpha + P V: lane = CPL consecutive columns of every head
 #pragma unroll
-    for (int h = 0; h < G; ++h)
+    for (int mt = 0; mt < KS; ++mt) {
+      oc[mt][0] *= alpha[0];
+      oc[mt][1] *= alpha[1];
+      oc[mt][2] *= alpha[0];
+      oc[mt][3] *= alpha[1];
+    }
+    __syncwarp();  // P^T visible
+    const uint32_t pb0 = *reinterpret_cast<const uint32_t*>(pt + g * kGrp + 2 * t);
+    const uint32_t pb1 = *reinterpret_cast<const uint32_t*>(pt + g * kGrp + 2 * t + 8);
+    // O^T += V^T · P^T
+    {
+      const int key = r8 + (mi >> 1) * 8;
 #pragma unroll
-      for (int e = 0; e < CPL / 2; ++e) acc[h][e] = fmul2(acc[h][e], make_float2(alpha[h], alpha[h]));
-    for (int k = 0; k < cur.nk; ++k) {
-      float2 vf[CPL / 2];
-      if constexpr (CPL == 4) {
-        const uint2 vv = *reinterpret_cast<const uint2*>(Vb + k * D + lane * 4);
-        vf[0] = make_float2(__uint_as_float(vv.x << 16), __uint_as_float(vv.x & 0xFFFF0000u));
-        vf[1] = make_float2(__uint_as_float(vv.y << 16), __uint_as_float(vv.y & 0xFFFF0000u));
-      } else {
-        const uint32_t vv = *reinterpret_cast<const uint32_t*>(Vb + k * D + lane * 2);
-        vf[0] = make_float2(__uint_as_float(vv << 16), __uint_as_float(vv & 0xFFFF0000u));
-      }
-#pragma unroll
-      for (int h = 0; h < G; ++h) {
-        const float pk = ps[h * kGrp + k];
-#pragma unroll
-        for (int e = 0; e < CPL / 2; ++e) acc[h][e] = ffma2(vf[e], make_float2(pk, pk), acc[h][e]);
+      for (int mt = 0; mt < KS; ++mt) {
+        uint32_t af[4];
+        ldsm_x4_t(af, Vb + (key * U + ((mt * 2 + (mi & 1)) ^ (key & (U - 1)))) * 8);
+        mma_bf16(oc[mt], af, pb0, pb1);
       }
     }
-    __syncwarp();  // the buffer and P are reused by the next group
+    __syncwarp();  // the buffer and P^T are reused by the next group
     cur = nxt;
     have = more;
   }
@@ -459,13 +491,18 @@ __global__ void __launch_bounds__(kThreads) decode_bf16_kernel(const DecodeArgs 
   __syncthreads();
   float* om = reinterpret_cast<float*>(&S.kv[0][0][0]);  // [kWarps][G][D]
 #pragma unroll
-  for (int h = 0; h < G; ++h) {
+  for (int j = 0; j < 2; ++j) {
+    const int h = 2 * t + j;
+    if (h < G) {
 #pragma unroll
-    for (int e = 0; e < CPL / 2; ++e)
-      *reinterpret_cast<float2*>(om + (w * G + h) * D + lane * CPL + 2 * e) = acc[h][e];
-    if (lane == 0) {
-      S.ml[w][2 * h] = m[h];
-      S.ml[w][2 * h + 1] = l[h];
+      for (int mt = 0; mt < KS; ++mt) {
+        om[(w * G + h) * D + mt * 16 + g] = oc[mt][j];
+        om[(w * G + h) * D + mt * 16 + g + 8] = oc[mt][j + 2];
+      }
+      if (g == 0) {
+        S.ml[w][2 * h] = m2[j];
+        S.ml[w][2 * h + 1] = l2[j];
+      }
     }
   }
   __syncthreads();
