@@ -287,7 +287,7 @@ template <int D, int G>
 struct DecSmem {
   static constexpr int kUnits = D / 8;                        // 16-byte units per bf16 row
   static constexpr int kStage = 2 * kGrp * D;                 // bf16 elements: K then V of a group
-  __nv_bfloat16 kv[kWarps][2][kStage];                        // per warp, double-buffered
+  __nv_bfloat16 kv[kWarps][kDecStages][kStage];               // per warp: ring of groups
   __nv_bfloat16 pt[kWarps][kPadHeads * kGrp];                 // per warp: P^T [head][key] (bf16)
   float ml[kWarps][2 * G];                                    // merge: m, l per warp and head
 };
@@ -394,17 +394,24 @@ __global__ void __launch_bounds__(kThreads) decode_bf16_kernel(const DecodeArgs 
     for (int e = 0; e < 4; ++e) oc[mt][e] = 0.f;
   uint32_t qf[KS][2];  // Q^T B fragments: head g, d = ks*16 + 2t + {0,1} (and + 8)
   int cur_rot = INT32_MIN;
-  Grp cur, nxt;
-  bool have = next_mine(cur);
-  if (have) issue(cur, 0);
-  for (int buf = 0; have; buf ^= 1) {
-    const bool more = next_mine(nxt);
-    if (more) {
-      issue(nxt, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+  // kDecStages-deep ring: groups pend[0..NS-2] are in flight, pend[0] in buffer `buf`; every
+  // iteration commits one cp.async group (possibly empty) so wait_group<NS-1> means "pend[0] landed"
+  constexpr int NS = kDecStages;
+  Grp pend[NS - 1];
+  bool hv[NS - 1];
+#pragma unroll
+  for (int s = 0; s < NS - 1; ++s) {
+    hv[s] = (s == 0 || hv[s - 1]) && next_mine(pend[s]);
+    if (hv[s]) issue(pend[s], s);
+    else cp_async_commit();
+  }
+  for (int buf = 0; hv[0]; buf = buf + 1 == NS ? 0 : buf + 1) {
+    Grp nxt;
+    const bool more = hv[NS - 2] && next_mine(nxt);
+    if (more) issue(nxt, buf + NS - 1 >= NS ? buf - 1 : buf + NS - 1);  // the slot freed last iteration
+    else cp_async_commit();
+    cp_async_wait<NS - 1>();
+    const Grp cur = pend[0];
     const int rot = a.tiles[cur.t].rot_delta;
     if (rot != cur_rot) {  // a new segment: q rotated to pos - Δ (rotate-half pairs), fp32 -> bf16
       cur_rot = rot;
@@ -484,8 +491,13 @@ __global__ void __launch_bounds__(kThreads) decode_bf16_kernel(const DecodeArgs 
       }
     }
     __syncwarp();  // the buffer and P^T are reused by the next group
-    cur = nxt;
-    have = more;
+#pragma unroll
+    for (int s = 0; s < NS - 2; ++s) {
+      pend[s] = pend[s + 1];
+      hv[s] = hv[s + 1];
+    }
+    pend[NS - 2] = nxt;
+    hv[NS - 2] = more;
   }
   // merge the four warps' partials (buffers reused: every warp is past its last cp.async)
   __syncthreads();

@@ -7,6 +7,13 @@
 
 #include "work.h"
 
+// K9 bf16 decode: per-warp ring depth (16-key K / V groups in flight + 1 being consumed); the host
+// sizes decode chunks for one wave of resident CTAs from the same constant
+#ifndef SPQ_DEC_STAGES
+#define SPQ_DEC_STAGES 2
+#endif
+constexpr int kDecStages = SPQ_DEC_STAGES;
+
 namespace spq {
 
 struct KvWriteArgs {

@@ -1375,12 +1375,12 @@ spq_status spq_decode_reserve(spq_ctx* c, spq_plan* p, int32_t max_new) {
   }
   // chunks of <= T tiles per (row, kv head), sized so that the whole batch is ONE wave of
   // resident CTAs (a second, partial wave of a memory-bound kernel costs a whole CTA time): the
-  // bf16 kernel holds 4 warps x 2 stages x 16 keys of K and V plus per-warp P^T and merge state
+  // bf16 kernel holds 4 warps x kDecStages stages x 16 keys of K and V plus per-warp P^T and merge state
   int64_t max_tiles = 1;
   for (const auto& rt : row_tiles) max_tiles = std::max<int64_t>(max_tiles, rt.second - rt.first);
   const int64_t gq = c->cfg.num_q_heads / c->cfg.num_kv_heads, dd = c->cfg.head_dim;
   const int64_t smem = c->cfg.dtype == SPQ_BF16
-                           ? 4 * 2 * 2 * 16 * dd * 2 + 4 * 8 * 16 * 2 + 4 * 2 * gq * 4
+                           ? 4 * kDecStages * 2 * 16 * dd * 2 + 4 * 8 * 16 * 2 + 4 * 2 * gq * 4
                            : 2 * (64 * (dd + 4) + 64 * dd) * 4 + 4 * (gq * dd + gq * 64 + gq * 3);
   const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(232448 / smem, 16));
   const int64_t slots = per_sm * (c->num_sms > 0 ? c->num_sms : 148);
