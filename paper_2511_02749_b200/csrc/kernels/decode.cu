@@ -565,21 +565,25 @@ __global__ void __launch_bounds__(kThreads) decode_bf16_kernel(const DecodeArgs 
   float* ML = wts + n * G;
   for (int i = tid; i < n * G; i += kThreads) wts[i] = __ldcg(a.lsepart + static_cast<int64_t>(it.part0) * G + i);
   __syncthreads();
-  if (tid < G) {
+  // M and L per head: warp w reduces heads w, w + 4, ... over the n chunks (lane-strided + shuffles)
+  for (int h = w; h < G; h += kWarps) {
     float M = -INFINITY;
-    for (int k = 0; k < n; ++k) M = fmaxf(M, wts[k * G + tid]);
-    ML[2 * tid] = M;
-  }
-  __syncthreads();
-  for (int i = tid; i < n * G; i += kThreads) {
-    const float lk = wts[i], M = ML[2 * (i % G)];
-    wts[i] = lk == -INFINITY ? 0.f : __expf(lk - M);
-  }
-  __syncthreads();
-  if (tid < G) {
+    for (int k = lane; k < n; k += 32) M = fmaxf(M, wts[k * G + h]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
     float L = 0.f;
-    for (int k = 0; k < n; ++k) L += wts[k * G + tid];
-    ML[2 * tid + 1] = L;
+    for (int k = lane; k < n; k += 32) {
+      const float lk = wts[k * G + h];
+      const float wk = lk == -INFINITY ? 0.f : __expf(lk - M);
+      wts[k * G + h] = wk;
+      L += wk;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    if (lane == 0) {
+      ML[2 * h] = M;
+      ML[2 * h + 1] = L;
+    }
   }
   __syncthreads();
   for (int f4 = tid; f4 < G * D / 4; f4 += kThreads) {
@@ -587,14 +591,21 @@ __global__ void __launch_bounds__(kThreads) decode_bf16_kernel(const DecodeArgs 
     const float4* src = reinterpret_cast<const float4*>(a.opart + (static_cast<int64_t>(it.part0) * G + h) * D + c);
     const int64_t stride = static_cast<int64_t>(G) * D / 4;  // next chunk, same (head, columns)
     float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 8
-    for (int k = 0; k < n; ++k) {
-      const float4 v4 = __ldcg(src + k * stride);
-      const float wk = wts[k * G + h];
-      acc4.x = fmaf(wk, v4.x, acc4.x);
-      acc4.y = fmaf(wk, v4.y, acc4.y);
-      acc4.z = fmaf(wk, v4.z, acc4.z);
-      acc4.w = fmaf(wk, v4.w, acc4.w);
+    // batches of kMB predicated loads, all in flight before their FMAs: ceil(n / kMB) L2 round
+    // trips (a runtime-n unrolled loop leaves a serial remainder of up to kMB - 1 dependent loads)
+    constexpr int kMB = 16;
+    for (int k0 = 0; k0 < n; k0 += kMB) {
+      float4 v4[kMB];
+#pragma unroll
+      for (int j = 0; j < kMB; ++j) v4[j] = k0 + j < n ? __ldcg(src + (k0 + j) * stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < kMB; ++j) {
+        const float wk = k0 + j < n ? wts[(k0 + j) * G + h] : 0.f;
+        acc4.x = fmaf(wk, v4[j].x, acc4.x);
+        acc4.y = fmaf(wk, v4[j].y, acc4.y);
+        acc4.z = fmaf(wk, v4[j].z, acc4.z);
+        acc4.w = fmaf(wk, v4[j].w, acc4.w);
+      }
     }
     const float inv = 1.f / ML[2 * h + 1];
     TO* dst = static_cast<TO*>(a.o) + (static_cast<int64_t>(it.row) * a.hq + h0 + h) * D + c;

@@ -1385,7 +1385,10 @@ spq_status spq_decode_reserve(spq_ctx* c, spq_plan* p, int32_t max_new) {
   const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(232448 / smem, 16));
   const int64_t slots = per_sm * (c->num_sms > 0 ? c->num_sms : 148);
   const int64_t pairs = B * c->cfg.num_kv_heads;  // (row, kv head) pairs
-  const int64_t per_pair = std::max<int64_t>(1, slots / pairs);
+#ifndef SPQ_DEC_CHUNK_DIV
+#define SPQ_DEC_CHUNK_DIV 1
+#endif
+  const int64_t per_pair = std::max<int64_t>(1, slots / pairs / SPQ_DEC_CHUNK_DIV);
   const int chunk = static_cast<int>(std::max<int64_t>(1, (max_tiles + per_pair - 1) / per_pair));
   spq::decode_items(row_tiles, c->cfg.num_kv_heads, c->cfg.num_q_heads / c->cfg.num_kv_heads, chunk, &w);
   D.max_new = max_new;
