@@ -340,25 +340,35 @@ __global__ void __launch_bounds__(kThreads) decode_bf16_kernel(const DecodeArgs 
   __nv_bfloat16* pt = S.pt[w];
   // this warp's groups: the chunk's groups in (tile, group) order, every kWarps-th one
   struct Grp {
-    int t, g, nk;  // tile, group in the tile, valid keys
+    int g, nk, blk_off, rot;  // group in its tile, valid keys, the tile's block-table offset and Δ
   };
   auto n_vis_of = [&](const KvTile& tl) {
     return tl.causal ? min(tl.n_valid, pos - tl.key_pos0 + 1) : tl.n_valid;
   };
-  int it_t = it.tile_begin, it_g = 0, gidx = 0;  // iterator over all groups of the chunk
+  // iterator over this warp's groups: chunk-order group indices w, w + 4, ...; the current tile's
+  // fields are read once per tile (not once per group scanned: a per-group reload of the tile
+  // record was a dependent load on every step of the walk)
+  int it_t = it.tile_begin, it_base = 0, my_gi = w;
+  KvTile cur_tile{};
+  int it_nv = 0;
+  if (it_t < it.tile_end) {
+    cur_tile = a.tiles[it_t];
+    it_nv = n_vis_of(cur_tile);
+  }
   auto next_mine = [&](Grp& out) -> bool {
     while (it_t < it.tile_end) {
-      const int nv = n_vis_of(a.tiles[it_t]);
-      const int ng = nv > 0 ? (nv + kGrp - 1) / kGrp : 0;
-      if (it_g >= ng) {
-        ++it_t;
-        it_g = 0;
-        continue;
+      const int ng = it_nv > 0 ? (it_nv + kGrp - 1) / kGrp : 0;
+      const int local = my_gi - it_base;
+      if (local < ng) {
+        out = Grp{local, min(kGrp, it_nv - local * kGrp), cur_tile.blk_off, cur_tile.rot_delta};
+        my_gi += kWarps;
+        return true;
       }
-      const int gg = it_g++;
-      if ((gidx++ % kWarps) != w) continue;
-      out = Grp{it_t, gg, min(kGrp, nv - gg * kGrp)};
-      return true;
+      it_base += ng;
+      if (++it_t < it.tile_end) {
+        cur_tile = a.tiles[it_t];
+        it_nv = n_vis_of(cur_tile);
+      }
     }
     return false;
   };
@@ -368,7 +378,7 @@ __global__ void __launch_bounds__(kThreads) decode_bf16_kernel(const DecodeArgs 
     // then lane i copies 16-byte unit i of the run. Rows past the valid keys are zero-filled
     // (P is 0 there, and 0 · V must not meet stale bits that decode as NaN).
     const int kk0 = gr.g * kGrp;
-    const int32_t blk = a.tile_blocks[a.tiles[gr.t].blk_off + kk0 / a.bs];
+    const int32_t blk = a.tile_blocks[gr.blk_off + kk0 / a.bs];
     const int64_t row0 = layer_rows + (static_cast<int64_t>(blk) * a.hkv + it.kvh) * a.bs + (kk0 & (a.bs - 1));
     const T* ks = static_cast<const T*>(a.k_pool) + row0 * D;
     const T* vs = static_cast<const T*>(a.v_pool) + row0 * D;
@@ -412,7 +422,7 @@ __global__ void __launch_bounds__(kThreads) decode_bf16_kernel(const DecodeArgs 
     else cp_async_commit();
     cp_async_wait<NS - 1>();
     const Grp cur = pend[0];
-    const int rot = a.tiles[cur.t].rot_delta;
+    const int rot = cur.rot;
     if (rot != cur_rot) {  // a new segment: q rotated to pos - Δ (rotate-half pairs), fp32 -> bf16
       cur_rot = rot;
       const int rp = min(max(pos - rot, 0), a.max_pos - 1);
