@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(kThreads) decode_bf16_kernel(const DecodeArgs 
   using Sm = DecSmem<D, G>;
   constexpr int U = Sm::kUnits;
   constexpr int KS = D / 16;  // k-steps of the score MMA = m-tiles of the P·V MMA
+  static_assert(G <= kPadHeads && D % 32 == 0, "q heads per kv head fill at most the MMA N side; d in 16-column k-steps, halves in whole k-steps");
   extern __shared__ __align__(16) uint8_t smem_raw[];
   Sm& S = *reinterpret_cast<Sm*>(smem_raw);
   const DecodeItem it = a.items[blockIdx.x];
