@@ -532,7 +532,7 @@ def measure_decode(dev, stream, args, n_gen: int = 64):
                      "launches_per_step": (ctx.launch_count() - n0) / n_gen}
         plan.release(stream=stream)
         ctx.close()
-    out["note"] = ("per step: K1 of the new tokens + K9 split-KV decode + combine, one layer; bytes = K and V "
+    out["note"] = ("per step: K1 of the new tokens + K9 split-KV decode (chunk merge in-kernel), one layer; bytes = K and V "
                    "of every visible key (HBM-bound)")
     return out
 
